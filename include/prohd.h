@@ -1,0 +1,160 @@
+/*
+ * prohd.h — C ABI of the B200-native ProHD hot path (arxiv 2511.18207).
+ *
+ * The library (libprohd.so, sm_100a only) exposes the paper's problem
+ * statement: given two point clouds A (nA x D) and B (nB x D), compute
+ *   - the exact directed Hausdorff distance h(A,B) = max_{a in A} min_{b in B} ||a-b||_2
+ *     (Eq. (1))                              -> directed_hd
+ *   - the undirected H(A,B) = max{h(A,B), h(B,A)}      -> hausdorff
+ *   - the ProHD estimate H^ of Alg. 3 "ProjHausdorff":
+ *     centroid axis (Alg. 1) + top-k principal directions of A u B
+ *     (Alg. 2), top/bottom-m extremes per direction (P:205-214,
+ *     P:242-251), union, exact HD on the subsets
+ *                                                                      -> prohd_estimate
+ * Notation (BASELINE.json): k = number of principal directions (the paper's
+ * m = floor(sqrt D)), m = points kept per (set, direction, tail) (the paper's
+ * k_X = max{1, floor(alpha n_X)}).
+ *
+ * Conventions shared by every call
+ *   - Point clouds are fp32, row-major, contiguous, leading dimension D
+ *     (row i starts at X + i*D). They may be DEVICE pointers (CUDA memory on the
+ *     context's device) or HOST pointers; host inputs are copied into the
+ *     workspace inside the call (cudaMemcpyAsync on the context stream), so the
+ *     workspace must have been sized with PROHD_WS_HOST_INPUTS.
+ *   - Ownership: the caller owns every input/output buffer and the workspace;
+ *     the library never frees caller memory and allocates no device memory of
+ *     its own beyond its context (TMA descriptors live in kernel parameters).
+ *   - All calls enqueue on the context's CUDA stream and are BLOCKING: they
+ *     synchronize that stream before filling the host result struct.
+ *   - Distances are Euclidean, returned in fp64: `dist` is the fp64 direct
+ *     re-evaluation sum_k (a_k - b_k)^2 of the witness pair, square-rooted.
+ *   - Ties: nearest neighbour = lowest
+ *     column index among equal fp64 distances; directed maximum = lowest row
+ *     among equal row minima; undirected witness = the A->B side on equality.
+ *   - Errors: every call returns a prohd_status; no exception crosses the ABI.
+ *     prohd_last_error(ctx) returns a NUL-terminated message for the last
+ *     failing call on that context (valid until the next call).
+ *   - Thread-safety: a context may be used by one host thread at a time.
+ */
+#ifndef PROHD_H_
+#define PROHD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PROHD_OK = 0,
+  PROHD_E_INVALID = 2,   /* null pointer, n < 1, D < 1, k < 0 or k > D, m < 1, bad shard */
+  PROHD_E_DATA = 3,      /* non-finite input (detected from the row norms / moments)     */
+  PROHD_E_INTERNAL = 4,  /* an internal invariant failed                                 */
+  PROHD_E_CUDA = 5,      /* a CUDA runtime/driver call failed (message has the name)     */
+  PROHD_E_WORKSPACE = 6, /* workspace missing or smaller than prohd_workspace_bytes()    */
+  PROHD_E_NOTIMPL = 7,   /* feature not built (e.g. not an sm_100 device)                */
+  PROHD_E_DEVICE = 8     /* the context's device is not a compute-capability 10.0 GPU    */
+} prohd_status;
+
+/* flags for prohd_workspace_bytes */
+#define PROHD_WS_HOST_INPUTS 1u /* inputs may be host pointers: reserve staging space */
+
+typedef struct prohd_ctx prohd_ctx; /* opaque: device, stream, workspace, last error */
+
+/* Create a context on `device` that enqueues on `cuda_stream` (a cudaStream_t;
+ * NULL = the legacy default stream). Returns PROHD_E_DEVICE if the device is
+ * not sm_100. *out is set to NULL on failure. */
+int prohd_create(int device, void* cuda_stream, prohd_ctx** out);
+int prohd_destroy(prohd_ctx* ctx);
+int prohd_set_stream(prohd_ctx* ctx, void* cuda_stream);
+const char* prohd_last_error(const prohd_ctx* ctx);
+/* Library version string, e.g. "prohd-b200 0.1 sm_100a". Never NULL. */
+const char* prohd_version(void);
+
+/* Bytes of device workspace any call below needs for these sizes (max over
+ * directed_hd, hausdorff and prohd_estimate). Pure host arithmetic. */
+size_t prohd_workspace_bytes(int64_t nA, int64_t nB, int32_t D, int32_t k, int64_t m,
+                             uint32_t flags);
+/* Attach a caller-owned device buffer (>= 256-byte aligned) as workspace. */
+int prohd_set_workspace(prohd_ctx* ctx, void* dptr, size_t bytes);
+
+/* ---------------------------------------------------------------- results */
+typedef struct {
+  double dist;   /* h = sqrt(dist2)                                          */
+  double dist2;  /* fp64 direct-form squared distance of the witness pair    */
+  int64_t a;     /* witness row in the FIRST argument (the argmax row)       */
+  int64_t b;     /* witness row in the SECOND argument (a's nearest point)   */
+  double dist2_tc; /* the kernel's 3xTF32 row minimum of row a (diagnostic)  */
+} prohd_directed;
+
+typedef struct {
+  double value;      /* max(ab.dist, ba.dist)                                */
+  prohd_directed ab; /* h(A,B): a in A, b in B                               */
+  prohd_directed ba; /* h(B,A): a in B, b in A                               */
+} prohd_hd;
+
+typedef struct {
+  double value;      /* H^ = max(h(A_sel,B_sel), h(B_sel,A_sel)), Alg. 3 l.6-7 */
+  prohd_directed ab; /* witnesses are ORIGINAL indices into A and B          */
+  prohd_directed ba;
+  int64_t size_a;    /* |I^A| (Alg. 3 return value)                   */
+  int64_t size_b;    /* |I^B|                                                */
+  int32_t n_dirs;    /* directions used: 1 + number of PCs kept (<= k+1)     */
+  int32_t _pad;
+} prohd_est;
+
+/* ---------------------------------------------------------------- exact HD */
+/* h(A,B) (Eq. 1). Cost nA*nB*D; the fused distance kernel never writes the
+ * nA x nB distance matrix. Errors: PROHD_E_INVALID for null/empty/D<1,
+ * PROHD_E_DATA for non-finite input, PROHD_E_WORKSPACE, PROHD_E_CUDA. */
+int directed_hd(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB,
+                int32_t D, prohd_directed* out);
+
+/* H(A,B) = max(h(A,B), h(B,A)). */
+int hausdorff(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB,
+              int32_t D, prohd_hd* out);
+
+/* Test hook: per-row minima of A against B, d2_i = min_j ||a_i - b_j||^2 as the
+ * kernel computes them (3xTF32 tensor-core products, fp32 accumulation), written
+ * to rowmin_dev (DEVICE, nA floats). */
+int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB,
+                       int32_t D, float* rowmin_dev);
+
+/* ---------------------------------------------------------------- ProHD   */
+/* Alg. 3 with k principal directions plus the centroid axis and m points per
+ * (set, direction, tail). 0 <= k <= D, m >= 1; if 2m >= n_X all of X is kept.
+ * Optional outputs (NULL to skip), HOST pointers:
+ *   dirs_out  D x (k+1) fp64, column-major by direction (dirs_out[l*D + d]);
+ *             column 0 is the centroid axis; columns >= n_dirs are zero.
+ *   idxA_out  capacity min(nA, 2m(k+1)): sorted unique I^A (size_a entries)
+ *   idxB_out  capacity min(nB, 2m(k+1)): sorted unique I^B (size_b entries) */
+int prohd_estimate(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB,
+                   int32_t D, int32_t k, int64_t m, prohd_est* out,
+                   double* dirs_out, int64_t* idxA_out, int64_t* idxB_out);
+
+/* Test hook: steps 2-4 with caller-supplied directions
+ * `dirs` (HOST, fp64, D x n_dirs, same layout as dirs_out; n_dirs >= 1). */
+int prohd_estimate_with_dirs(prohd_ctx* ctx, const float* A, int64_t nA, const float* B,
+                             int64_t nB, int32_t D, int32_t n_dirs, int64_t m,
+                             const double* dirs, prohd_est* out, int64_t* idxA_out,
+                             int64_t* idxB_out);
+
+/* ---------------------------------------------------------------- sharding */
+/* Row-sharded exact HD: this rank holds rows
+ * [row_offset, row_offset + nA_local) of the full A and all of B. Writes the
+ * rank's packed key  (float_bits(d2_tc) << 32) | (0xFFFFFFFF - global_row)
+ * (max over ranks = global argmax, lowest row on ties) to *key_out (HOST).
+ * The caller all-reduces the key (MAX), then calls directed_hd_witness on the
+ * rank that owns the winning row. */
+int directed_hd_local(prohd_ctx* ctx, const float* A_local, int64_t nA_local, int64_t row_offset,
+                      const float* B, int64_t nB, int32_t D, uint64_t* key_out);
+/* fp64 nearest neighbour of one point a (HOST or DEVICE, D floats) in B:
+ * fills out->b, out->dist2, out->dist (out->a is left to the caller). */
+int directed_hd_witness(prohd_ctx* ctx, const float* a, const float* B, int64_t nB, int32_t D,
+                        prohd_directed* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROHD_H_ */

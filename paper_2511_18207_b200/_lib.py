@@ -1,0 +1,79 @@
+"""ctypes declarations for libprohd.so (include/prohd.h). Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libprohd.so")
+
+PROHD_OK = 0
+PROHD_E_INVALID = 2
+PROHD_E_DATA = 3
+PROHD_E_INTERNAL = 4
+PROHD_E_CUDA = 5
+PROHD_E_WORKSPACE = 6
+PROHD_E_NOTIMPL = 7
+PROHD_E_DEVICE = 8
+PROHD_WS_HOST_INPUTS = 1
+
+STATUS_NAMES = {0: "PROHD_OK", 2: "PROHD_E_INVALID", 3: "PROHD_E_DATA", 4: "PROHD_E_INTERNAL",
+                5: "PROHD_E_CUDA", 6: "PROHD_E_WORKSPACE", 7: "PROHD_E_NOTIMPL", 8: "PROHD_E_DEVICE"}
+
+# every symbol include/prohd.h declares (checked by tests/test_abi.py)
+EXPORTED = [
+    "prohd_create", "prohd_destroy", "prohd_set_stream", "prohd_last_error", "prohd_version",
+    "prohd_workspace_bytes", "prohd_set_workspace", "directed_hd", "hausdorff", "directed_hd_rowmin",
+    "prohd_estimate", "prohd_estimate_with_dirs", "directed_hd_local", "directed_hd_witness",
+]
+
+
+class Directed(C.Structure):
+    _fields_ = [("dist", C.c_double), ("dist2", C.c_double), ("a", C.c_int64), ("b", C.c_int64),
+                ("dist2_tc", C.c_double)]
+
+
+class HD(C.Structure):
+    _fields_ = [("value", C.c_double), ("ab", Directed), ("ba", Directed)]
+
+
+class Est(C.Structure):
+    _fields_ = [("value", C.c_double), ("ab", Directed), ("ba", Directed), ("size_a", C.c_int64),
+                ("size_b", C.c_int64), ("n_dirs", C.c_int32), ("_pad", C.c_int32)]
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libprohd.so; raises (never falls back) if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not found: build it with `python -m paper_2511_18207_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i64, i32, f = C.c_void_p, C.c_int64, C.c_int32, C.c_int
+    lib.prohd_create.argtypes = [f, vp, C.POINTER(vp)]
+    lib.prohd_destroy.argtypes = [vp]
+    lib.prohd_set_stream.argtypes = [vp, vp]
+    lib.prohd_last_error.argtypes = [vp]
+    lib.prohd_last_error.restype = C.c_char_p
+    lib.prohd_version.restype = C.c_char_p
+    lib.prohd_workspace_bytes.argtypes = [i64, i64, i32, i32, i64, C.c_uint32]
+    lib.prohd_workspace_bytes.restype = C.c_size_t
+    lib.prohd_set_workspace.argtypes = [vp, vp, C.c_size_t]
+    lib.directed_hd.argtypes = [vp, vp, i64, vp, i64, i32, C.POINTER(Directed)]
+    lib.hausdorff.argtypes = [vp, vp, i64, vp, i64, i32, C.POINTER(HD)]
+    lib.directed_hd_rowmin.argtypes = [vp, vp, i64, vp, i64, i32, vp]
+    lib.prohd_estimate.argtypes = [vp, vp, i64, vp, i64, i32, i32, i64, C.POINTER(Est), vp, vp, vp]
+    lib.prohd_estimate_with_dirs.argtypes = [vp, vp, i64, vp, i64, i32, i32, i64, vp, C.POINTER(Est), vp, vp]
+    lib.directed_hd_local.argtypes = [vp, vp, i64, i64, vp, i64, i32, C.POINTER(C.c_uint64)]
+    lib.directed_hd_witness.argtypes = [vp, vp, vp, i64, i32, C.POINTER(Directed)]
+    for name in EXPORTED:
+        fn = getattr(lib, name)
+        if name not in ("prohd_last_error", "prohd_version", "prohd_workspace_bytes"):
+            fn.restype = C.c_int
+    _lib = lib
+    return lib

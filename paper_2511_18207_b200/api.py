@@ -1,0 +1,200 @@
+"""Python binding of the C ABI (include/prohd.h): same names, argument marshalling only.
+
+Every step of the path runs in libprohd.so's sm_100a kernels. PyTorch supplies
+device memory (inputs, the workspace) and the CUDA stream. There is no CPU
+fallback: without the library or a B200 these calls raise.
+
+Inputs are 2-D float32 tensors (n x D, contiguous). CUDA tensors are passed as
+device pointers; CPU tensors are passed as host pointers and the library copies
+them to the device inside the call (the end-to-end path).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+class ProHDError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{L.STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _directed(d: L.Directed) -> dict:
+    return {"dist": d.dist, "dist2": d.dist2, "a": int(d.a), "b": int(d.b), "dist2_tc": d.dist2_tc}
+
+
+def _as_points(X, name: str) -> torch.Tensor:
+    if isinstance(X, np.ndarray):
+        X = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32))
+    if not isinstance(X, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor or numpy array")
+    if X.dtype != torch.float32 or X.dim() != 2:
+        raise TypeError(f"{name} must be a 2-D float32 tensor (got {X.dtype}, dim {X.dim()})")
+    return X.contiguous()
+
+
+class Context:
+    """A prohd_ctx bound to one CUDA device, with a torch-allocated workspace."""
+
+    def __init__(self, device: int | None = None):
+        self.lib = L.load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        h = C.c_void_p()
+        rc = self.lib.prohd_create(self.device, None, C.byref(h))
+        if rc != L.PROHD_OK:
+            raise ProHDError(rc, f"prohd_create(device={self.device}) failed")
+        self.h = h
+        self._ws = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.prohd_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    # ---------------------------------------------------------------- plumbing
+    def _check(self, rc: int):
+        if rc != L.PROHD_OK:
+            raise ProHDError(rc, self.lib.prohd_last_error(self.h).decode())
+
+    def reserve(self, nA: int, nB: int, D: int, k: int = 0, m: int = 1, host_inputs: bool = False) -> int:
+        flags = L.PROHD_WS_HOST_INPUTS if host_inputs else 0
+        need = int(self.lib.prohd_workspace_bytes(nA, nB, D, k, m, flags))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = None
+            torch.cuda.synchronize(self.device)
+            self._ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.device}")
+        self._check(self.lib.prohd_set_workspace(self.h, self._ws.data_ptr(), self._ws.numel()))
+        return need
+
+    def _prepare(self, A, B, k=0, m=1):
+        A = _as_points(A, "A")
+        B = _as_points(B, "B")
+        if A.shape[1] != B.shape[1]:
+            raise ValueError("A and B must have the same dimension D")
+        host = not (A.is_cuda and B.is_cuda)
+        self.reserve(A.shape[0], B.shape[0], A.shape[1], k, m, host_inputs=host)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._check(self.lib.prohd_set_stream(self.h, C.c_void_p(stream)))
+        return A, B
+
+    # ---------------------------------------------------------------- ABI calls
+    def directed_hd(self, A, B) -> dict:
+        A, B = self._prepare(A, B)
+        out = L.Directed()
+        self._check(self.lib.directed_hd(self.h, A.data_ptr(), A.shape[0], B.data_ptr(), B.shape[0],
+                                         A.shape[1], C.byref(out)))
+        return _directed(out)
+
+    def hausdorff(self, A, B) -> dict:
+        A, B = self._prepare(A, B)
+        out = L.HD()
+        self._check(self.lib.hausdorff(self.h, A.data_ptr(), A.shape[0], B.data_ptr(), B.shape[0],
+                                       A.shape[1], C.byref(out)))
+        return {"value": out.value, "ab": _directed(out.ab), "ba": _directed(out.ba)}
+
+    def directed_hd_rowmin(self, A, B) -> torch.Tensor:
+        A, B = self._prepare(A, B)
+        rowmin = torch.empty(A.shape[0], dtype=torch.float32, device=f"cuda:{self.device}")
+        self._check(self.lib.directed_hd_rowmin(self.h, A.data_ptr(), A.shape[0], B.data_ptr(), B.shape[0],
+                                                A.shape[1], rowmin.data_ptr()))
+        return rowmin
+
+    def _est_out(self, out: L.Est) -> dict:
+        return {"value": out.value, "ab": _directed(out.ab), "ba": _directed(out.ba),
+                "size_a": int(out.size_a), "size_b": int(out.size_b), "n_dirs": int(out.n_dirs)}
+
+    def prohd_estimate(self, A, B, k: int, m: int, return_dirs: bool = False,
+                       return_indices: bool = False) -> dict:
+        A, B = self._prepare(A, B, k, m)
+        nA, nB, D = A.shape[0], B.shape[0], A.shape[1]
+        out = L.Est()
+        dirs = np.zeros((k + 1, D), dtype=np.float64) if return_dirs else None
+        capA = min(nA, 2 * m * (k + 1))
+        capB = min(nB, 2 * m * (k + 1))
+        ia = np.empty(capA, dtype=np.int64) if return_indices else None
+        ib = np.empty(capB, dtype=np.int64) if return_indices else None
+        ptr = (lambda a: a.ctypes.data if a is not None else None)
+        self._check(self.lib.prohd_estimate(self.h, A.data_ptr(), nA, B.data_ptr(), nB, D, k, m, C.byref(out),
+                                            ptr(dirs), ptr(ia), ptr(ib)))
+        res = self._est_out(out)
+        if return_dirs:
+            res["U"] = dirs[: res["n_dirs"]].T.copy()  # D x n_dirs
+        if return_indices:
+            res["IA"] = ia[: res["size_a"]].copy()
+            res["IB"] = ib[: res["size_b"]].copy()
+        return res
+
+    def prohd_estimate_with_dirs(self, A, B, U: np.ndarray, m: int, return_indices: bool = True) -> dict:
+        U = np.asarray(U, dtype=np.float64)
+        n_dirs = U.shape[1]
+        A, B = self._prepare(A, B, n_dirs - 1, m)
+        nA, nB, D = A.shape[0], B.shape[0], A.shape[1]
+        dirs = np.ascontiguousarray(U.T)  # [n_dirs][D]
+        out = L.Est()
+        capA = min(nA, 2 * m * n_dirs)
+        capB = min(nB, 2 * m * n_dirs)
+        ia = np.empty(capA, dtype=np.int64)
+        ib = np.empty(capB, dtype=np.int64)
+        self._check(self.lib.prohd_estimate_with_dirs(self.h, A.data_ptr(), nA, B.data_ptr(), nB, D, n_dirs, m,
+                                                      dirs.ctypes.data, C.byref(out), ia.ctypes.data,
+                                                      ib.ctypes.data))
+        res = self._est_out(out)
+        res["IA"] = ia[: res["size_a"]].copy()
+        res["IB"] = ib[: res["size_b"]].copy()
+        return res
+
+    def directed_hd_local(self, A_local, row_offset: int, B) -> int:
+        A, B = self._prepare(A_local, B)
+        key = C.c_uint64()
+        self._check(self.lib.directed_hd_local(self.h, A.data_ptr(), A.shape[0], int(row_offset), B.data_ptr(),
+                                               B.shape[0], A.shape[1], C.byref(key)))
+        return int(key.value)
+
+    def directed_hd_witness(self, a, B) -> dict:
+        a = _as_points(a.reshape(1, -1) if a.dim() == 1 else a, "a")
+        a, B = self._prepare(a, B)
+        out = L.Directed()
+        self._check(self.lib.directed_hd_witness(self.h, a.data_ptr(), B.data_ptr(), B.shape[0], B.shape[1],
+                                                 C.byref(out)))
+        return _directed(out)
+
+
+_default: dict[int, Context] = {}
+
+
+def context(device: int | None = None) -> Context:
+    dev = torch.cuda.current_device() if device is None else int(device)
+    if dev not in _default:
+        _default[dev] = Context(dev)
+    return _default[dev]
+
+
+def directed_hd(A, B) -> dict:
+    """h(A,B) = max_a min_b ||a-b|| with witness (Eq. (1))."""
+    return context().directed_hd(A, B)
+
+
+def hausdorff(A, B) -> dict:
+    """H(A,B) = max(h(A,B), h(B,A)) (Eq. (1))."""
+    return context().hausdorff(A, B)
+
+
+def prohd_estimate(A, B, k: int, m: int, **kw) -> dict:
+    """ProHD Alg. 3 estimate with k principal directions and m points per tail."""
+    return context().prohd_estimate(A, B, k, m, **kw)
+
+
+def unpack_key(key: int) -> tuple[float, int]:
+    """(d2 as float32, global row) from a packed row-max key."""
+    d2 = np.array([key >> 32], dtype=np.uint32).view(np.float32)[0]
+    row = 0xFFFFFFFF - (key & 0xFFFFFFFF)
+    return float(d2), int(row)

@@ -1,0 +1,243 @@
+// api_common.cuh — host-side helpers shared by the C-ABI translation units:
+// context struct, error reporting, workspace carving, input staging, operand
+// preparation and the distance-kernel driver.
+#pragma once
+#include "../../include/prohd.h"
+#include "internal.cuh"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+struct prohd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint8_t* ws = nullptr;
+  size_t ws_bytes = 0;
+  int num_sms = 148;
+  std::string err;
+};
+
+namespace prohd {
+
+// ------------------------------------------------------------------ TMA descriptors
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+inline bool make_tmap_2d(CUtensorMap* map, const float* base, int64_t rows, int Dp, int box_rows, char* err,
+                  size_t errlen) {
+  PFN_encodeTiled enc = get_encode();
+  if (enc == nullptr) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(Dp), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(Dp) * 4};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled failed (%d) rows=%lld Dp=%d box=%d", static_cast<int>(r),
+             static_cast<long long>(rows), Dp, box_rows);
+    return false;
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------ workspace carving
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  size_t cap;
+  bool dry;  // size-only pass
+  template <typename T>
+  T* take(int64_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = dry ? nullptr : reinterpret_cast<T*>(base + off);
+    off += static_cast<size_t>(count) * sizeof(T);
+    return p;
+  }
+};
+
+// Operands of one point set for the distance kernel.
+struct SetOps {
+  const float* x = nullptr;  // device copy of the fp32 input (D stride)
+  float* hi = nullptr;
+  float* lo = nullptr;
+  float* norms = nullptr;  // padded to kBN with +inf
+  int64_t n = 0;
+};
+
+struct ExactWs {
+  float* stageA = nullptr;
+  float* stageB = nullptr;
+  SetOps A, B;
+  float* rowmin = nullptr;
+  unsigned long long* keys = nullptr;  // [2]
+  double* nn_d = nullptr;              // [2]
+  long long* nn_j = nullptr;           // [2]
+  double* blk_d = nullptr;
+  long long* blk_j = nullptr;
+  int* bad = nullptr;
+};
+
+inline void carve_set(Carver& c, SetOps& s, int64_t n, int D) {
+  const int Dp = pad_dim(D);
+  s.n = n;
+  s.hi = c.take<float>(n * Dp);
+  s.lo = c.take<float>(n * Dp);
+  s.norms = c.take<float>(round_up(n, kBN));
+}
+
+inline size_t carve_exact(Carver& c, ExactWs& w, int64_t nA, int64_t nB, int D, bool host_inputs) {
+  if (host_inputs) {
+    w.stageA = c.take<float>(nA * D);
+    w.stageB = c.take<float>(nB * D);
+  }
+  carve_set(c, w.A, nA, D);
+  carve_set(c, w.B, nB, D);
+  w.rowmin = c.take<float>(nA > nB ? nA : nB);
+  w.keys = c.take<unsigned long long>(2);
+  w.nn_d = c.take<double>(2);
+  w.nn_j = c.take<long long>(2);
+  w.blk_d = c.take<double>(kNNBlocks);
+  w.blk_j = c.take<long long>(kNNBlocks);
+  w.bad = c.take<int>(1);
+  return c.off;
+}
+
+}  // namespace prohd
+
+using namespace prohd;
+
+// ------------------------------------------------------------------ helpers
+inline int fail(prohd_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) return fail(ctx, PROHD_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+inline bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+inline int enter(prohd_ctx* ctx) {
+  if (ctx == nullptr) return PROHD_E_INVALID;
+  ctx->err.clear();
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return fail(ctx, PROHD_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  return PROHD_OK;
+}
+
+inline int check_sets(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D) {
+  if (A == nullptr || B == nullptr) return fail(ctx, PROHD_E_INVALID, "null input pointer");
+  if (nA < 1 || nB < 1) return fail(ctx, PROHD_E_INVALID, "empty point cloud (nA=%lld nB=%lld)", (long long)nA,
+                                    (long long)nB);
+  if (D < 1) return fail(ctx, PROHD_E_INVALID, "D must be >= 1 (got %d)", D);
+  if (nA > 0x7FFFFF00LL || nB > 0x7FFFFF00LL) return fail(ctx, PROHD_E_INVALID, "n too large for 32-bit row keys");
+  return PROHD_OK;
+}
+
+// Make device copies of A/B available (staging host inputs through the workspace).
+inline int stage_inputs(prohd_ctx* ctx, const float*& A, int64_t nA, const float*& B, int64_t nB, int32_t D,
+                        float* stA, float* stB, bool& host_inputs) {
+  const bool dA = is_device_ptr(A), dB = is_device_ptr(B);
+  host_inputs = !(dA && dB);
+  if (!dA) {
+    if (stA == nullptr) return fail(ctx, PROHD_E_WORKSPACE, "host inputs need a PROHD_WS_HOST_INPUTS workspace");
+    CK(cudaMemcpyAsync(stA, A, sizeof(float) * nA * D, cudaMemcpyHostToDevice, ctx->stream));
+    A = stA;
+  }
+  if (!dB) {
+    if (stB == nullptr) return fail(ctx, PROHD_E_WORKSPACE, "host inputs need a PROHD_WS_HOST_INPUTS workspace");
+    CK(cudaMemcpyAsync(stB, B, sizeof(float) * nB * D, cudaMemcpyHostToDevice, ctx->stream));
+    B = stB;
+  }
+  return PROHD_OK;
+}
+
+inline int prep_set(prohd_ctx* ctx, const float* X, int64_t n, int D, SetOps& s, int* bad) {
+  s.x = X;
+  CK(launch_prep(X, n, D, pad_dim(D), round_up(n, kBN), s.hi, s.lo, s.norms, bad, ctx->stream));
+  return PROHD_OK;
+}
+
+// rows of `R` against columns of `C` -> rowmin (device)
+inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, float* rowmin) {
+  CUtensorMap maps[4];
+  char err[256];
+  const int Dp = pad_dim(D);
+  if (!make_tmap_2d(&maps[0], R.hi, R.n, Dp, kBM, err, sizeof err) ||
+      !make_tmap_2d(&maps[1], R.lo, R.n, Dp, kBM, err, sizeof err) ||
+      !make_tmap_2d(&maps[2], C.hi, C.n, Dp, kBN, err, sizeof err) ||
+      !make_tmap_2d(&maps[3], C.lo, C.n, Dp, kBN, err, sizeof err))
+    return fail(ctx, PROHD_E_CUDA, "%s", err);
+  DistArgs a;
+  a.maps = maps;
+  a.nA = R.n;
+  a.nB = C.n;
+  a.D = D;
+  a.na = R.norms;
+  a.nb = C.norms;
+  a.rowmin = rowmin;
+  a.num_sms = ctx->num_sms;
+  CK(launch_dist_rowmin(a, ctx->stream));
+  return PROHD_OK;
+}
+
+// h(R, C) on prepared operands; result lands in w.keys[slot], w.nn_d[slot], w.nn_j[slot].
+inline int directed_on_ops(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, ExactWs& w, int slot) {
+  int rc = run_dist(ctx, R, C, D, w.rowmin);
+  if (rc) return rc;
+  CK(launch_rowmax_key(w.rowmin, R.n, 0, &w.keys[slot], ctx->stream));
+  CK(launch_nn64_from_key(R.x, 0, R.n, &w.keys[slot], C.x, C.n, D, w.blk_d, w.blk_j, kNNBlocks, &w.nn_d[slot],
+                          &w.nn_j[slot], ctx->stream));
+  return PROHD_OK;
+}
+
+inline void fill_directed(prohd_directed* o, unsigned long long key, double d2, long long j) {
+  o->a = static_cast<int64_t>(0xFFFFFFFFu - static_cast<uint32_t>(key & 0xFFFFFFFFull));
+  o->b = j;
+  o->dist2 = d2;
+  o->dist = std::sqrt(d2);
+  uint32_t fb = static_cast<uint32_t>(key >> 32);
+  float f;
+  std::memcpy(&f, &fb, 4);
+  o->dist2_tc = f;
+}
+

@@ -1,0 +1,55 @@
+// internal.cuh — launchers shared between the kernel files and the C-ABI layer.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace prohd {
+
+constexpr int kBM = 128;  // rows of the row operand per CTA tile (UMMA M)
+constexpr int kBN = 256;  // columns (points of the column operand) per tile (UMMA N)
+constexpr int kBK = 32;   // fp32 K elements per pipeline chunk (one 128-B swizzle row)
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int pad_dim(int D) { return static_cast<int>(round_up(D, 4)); }  // 16-B TMA row stride
+
+// K0: split fp32 points into TF32 hi/lo operands + fp32 norms (fp64 accumulated).
+//   hi = x with the low 13 mantissa bits cleared (exact TF32), lo = x - hi.
+//   hi/lo rows have stride Dp (zero padded); norms[i] = ||x_i||^2 for i < n and
+//   +inf for n <= i < n_pad. Sets *bad = 1 if any norm is not finite.
+cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, float* hi, float* lo,
+                        float* norms, int* bad, cudaStream_t st);
+// Same, for a gathered subset: rows X[idx[i]] for i < n (subset operands).
+cudaError_t launch_prep_gather(const float* X, const int64_t* idx, int64_t n, int D, int Dp, int64_t n_pad,
+                               float* hi, float* lo, float* norms, int* bad, cudaStream_t st);
+
+struct DistArgs {
+  const CUtensorMap* maps;  // [A_hi, A_lo, B_hi, B_lo]
+  int64_t nA, nB;
+  int D;
+  const float* na;  // row-operand norms
+  const float* nb;  // column-operand norms, padded to a multiple of kBN with +inf
+  float* rowmin;    // out: min_j d2(i, j), clamped >= 0
+  int num_sms;
+};
+// K6: fused 3xTF32 tcgen05 distance + row-min kernel.
+cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st);
+
+// K7a: packed max key over rows: (bits(d2) << 32) | (0xFFFFFFFF - (row + row_offset)).
+cudaError_t launch_rowmax_key(const float* rowmin, int64_t n, int64_t row_offset, unsigned long long* key,
+                              cudaStream_t st);
+// K7b: fp64 nearest neighbour of point `a` (D floats, device) in B (device, stride D):
+//   writes {d2 (double), j (int64)} to out2 (device, 16 bytes). `scratch` holds
+//   2 * nblocks entries. Lowest j on exact ties.
+cudaError_t launch_nn64(const float* a, const float* B, int64_t nB, int D, double* blk_d, long long* blk_j,
+                        int nblocks, double* out_d, long long* out_j, cudaStream_t st);
+// helper: a = X + row * D where row is decoded from the key on the device
+cudaError_t launch_nn64_from_key(const float* X, int64_t x_offset, int64_t nX, const unsigned long long* key,
+                                 const float* B, int64_t nB, int D, double* blk_d, long long* blk_j, int nblocks,
+                                 double* out_d, long long* out_j, cudaStream_t st);
+constexpr int kNNBlocks = 592;  // 4 x 148 SMs
+
+// TMA descriptor for a row-major fp32 matrix [rows x Dp], box {kBK, box_rows}, SWIZZLE_128B.
+bool make_tmap_2d(CUtensorMap* map, const float* base, int64_t rows, int Dp, int box_rows, char* err, size_t errlen);
+
+}  // namespace prohd

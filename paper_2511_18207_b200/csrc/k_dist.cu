@@ -1,0 +1,253 @@
+// k_dist.cu — K6: fused 3xTF32 tcgen05 distance + row-minimum kernel.
+//
+// Computes, for every row a_i of the row operand A and all columns b_j of B,
+//     v_ij = ||b_j||^2 - 2 a_i . b_j        (a_i . b_j on tcgen05, 3xTF32)
+//     rowmin_i = max(0, ||a_i||^2 + min_j v_ij)
+// which is min_j ||a_i - b_j||^2 (Eq. (1), inner min). The
+// n_A x n_B distance matrix never leaves TMEM/registers.
+//
+// 3xTF32 (SURVEY.md §8(a) "shared fused distance kernel"): with x = hi + lo,
+//   a.b ~= hi_a.hi_b + hi_a.lo_b + lo_a.hi_b
+// (lo.lo ~ 2^-22 |a||b| dropped); all three products accumulate into one fp32
+// TMEM accumulator.
+//
+// Structure (persistent, 1 CTA per SM, warp-specialised, 192 threads):
+//   warp 0      TMA producer: per K-chunk (32 fp32 = one 128-B swizzle row) it
+//               loads A_hi/A_lo [128 x 32] and B_hi/B_lo [256 x 32] into a
+//               2-stage ring (96 KB per stage) with SWIZZLE_128B.
+//   warp 1      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//               and single-thread MMA issuer: tcgen05.mma.cta_group::1.kind::tf32
+//               M=128, N=256, K=8, 3 MMAs per K-step, commit -> smem slot free,
+//               commit -> accumulator full.
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 (one TMEM lane = one row per
+//               thread), v = fma(-2, acc, ||b||^2), running min in a register
+//               across all B tiles of the unit; the accumulator is double
+//               buffered so the epilogue of tile t overlaps the MMAs of t+1.
+// Work unit = (128-row block of A, contiguous range of B tiles). With one range
+// the row minimum is stored; with several (small n_A) it is combined with an
+// integer atomicMin on the float bits (valid since d2 >= 0).
+#include "internal.cuh"
+#include "sm100.cuh"
+
+#include <cstdio>
+
+namespace prohd {
+namespace {
+
+constexpr int kStages = 2;
+constexpr int kThreads = 192;
+constexpr uint32_t kATile = kBM * kBK * 4;                  // 16 KB
+constexpr uint32_t kBTile = kBN * kBK * 4;                  // 32 KB
+constexpr uint32_t kStageBytes = 2 * kATile + 2 * kBTile;   // 96 KB
+constexpr uint32_t kTmemCols = 512;
+constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + 1024 + 256;
+
+struct Sched {
+  int64_t nA, nB;
+  int nrb, nt, nsplit, tps, nk, ks_last;
+  int atomic_out;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    dist_rowmin_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
+                       const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
+                       const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin) {
+  using namespace sm100;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tAh);
+    tma_prefetch(&tAl);
+    tma_prefetch(&tBh);
+    tma_prefetch(&tBl);
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int units = s.nrb * s.nsplit;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int rb = u / s.nsplit, sp = u % s.nsplit;
+        const int t0 = sp * s.tps;
+        const int t1 = min(s.nt, t0 + s.tps);
+        for (int t = t0; t < t1; ++t) {
+          for (int c = 0; c < s.nk; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            uint8_t* st = smem + stage * kStageBytes;
+            mbar_arrive_expect_tx(&full[stage], kStageBytes);
+            tma_load_2d(st, &tAh, c * kBK, rb * kBM, &full[stage]);
+            tma_load_2d(st + kATile, &tAl, c * kBK, rb * kBM, &full[stage]);
+            tma_load_2d(st + 2 * kATile, &tBh, c * kBK, t * kBN, &full[stage]);
+            tma_load_2d(st + 2 * kATile + kBTile, &tBl, c * kBK, t * kBN, &full[stage]);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int sp = u % s.nsplit;
+        const int t0 = sp * s.tps;
+        const int t1 = min(s.nt, t0 + s.tps);
+        for (int t = t0; t < t1; ++t) {
+          mbar_wait(&tempty[acc], aphase ^ 1u);
+          tc_fence_after();
+          const uint32_t d = tmem_base + static_cast<uint32_t>(acc * kBN);
+          for (int c = 0; c < s.nk; ++c) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t ah = smem_u32(smem + stage * kStageBytes);
+            const uint32_t al = ah + kATile;
+            const uint32_t bh = ah + 2 * kATile;
+            const uint32_t bl = bh + kBTile;
+            const int ks = (c == s.nk - 1) ? s.ks_last : (kBK / 8);
+            for (int kk = 0; kk < ks; ++kk) {
+              const uint32_t off = static_cast<uint32_t>(kk * 32);  // 8 tf32 = 32 B along K
+              const uint64_t dah = smem_desc_k_sw128(ah + off);
+              const uint64_t dal = smem_desc_k_sw128(al + off);
+              const uint64_t dbh = smem_desc_k_sw128(bh + off);
+              const uint64_t dbl = smem_desc_k_sw128(bl + off);
+              mma_tf32(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);
+              mma_tf32(d, dah, dbl, idesc, 1u);
+              mma_tf32(d, dal, dbh, idesc, 1u);
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          mma_commit(&tfull[acc]);
+          acc ^= 1;
+          if (acc == 0) aphase ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_local = q * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int rb = u / s.nsplit, sp = u % s.nsplit;
+      const int t0 = sp * s.tps;
+      const int t1 = min(s.nt, t0 + s.tps);
+      float rmin = __int_as_float(0x7f800000);
+      for (int t = t0; t < t1; ++t) {
+        mbar_wait(&tfull[acc], aphase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(acc * kBN);
+        const float4* nbp = reinterpret_cast<const float4*>(nb + static_cast<int64_t>(t) * kBN);
+#pragma unroll 1
+        for (int cc = 0; cc < kBN / 32; ++cc) {
+          float v[32];
+          tmem_ld32(taddr + cc * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 n4 = __ldg(nbp + cc * 8 + i);
+            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 0], n4.x));
+            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 1], n4.y));
+            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 2], n4.z));
+            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 3], n4.w));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1u;
+      }
+      const int64_t row = static_cast<int64_t>(rb) * kBM + row_local;
+      if (row < s.nA) {
+        const float d2 = fmaxf(rmin + __ldg(na + row), 0.0f);
+        if (s.atomic_out)
+          atomicMin(reinterpret_cast<int*>(rowmin + row), __float_as_int(d2));
+        else
+          rowmin[row] = d2;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
+  Sched s{};
+  s.nA = a.nA;
+  s.nB = a.nB;
+  s.nrb = static_cast<int>((a.nA + kBM - 1) / kBM);
+  s.nt = static_cast<int>((a.nB + kBN - 1) / kBN);
+  s.nk = (a.D + kBK - 1) / kBK;
+  s.ks_last = ((a.D - (s.nk - 1) * kBK) + 7) / 8;
+  // enough units to fill the machine twice when A is small (subset HD)
+  int want = 2 * a.num_sms;
+  int nsplit = (want + s.nrb - 1) / s.nrb;
+  if (nsplit < 1) nsplit = 1;
+  if (nsplit > s.nt) nsplit = s.nt;
+  s.tps = (s.nt + nsplit - 1) / nsplit;
+  s.nsplit = (s.nt + s.tps - 1) / s.tps;
+  s.atomic_out = s.nsplit > 1 ? 1 : 0;
+  if (s.atomic_out) {
+    cudaError_t e = cudaMemsetAsync(a.rowmin, 0x7F, sizeof(float) * a.nA, st);  // 3.39e38 (finite, > any d2)
+    if (e != cudaSuccess) return e;
+  }
+  {
+    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemBytes));
+    if (e != cudaSuccess) return e;
+  }
+  const int units = s.nrb * s.nsplit;
+  const int grid = units < a.num_sms ? units : a.num_sms;
+  dist_rowmin_kernel<<<grid, kThreads, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na,
+                                                           a.nb, a.rowmin);
+  return cudaGetLastError();
+}
+
+}  // namespace prohd

@@ -1,0 +1,213 @@
+// prohd_api.cu — the C ABI declared in include/prohd.h.
+//
+// Orchestration only: argument validation, workspace carving, host->device
+// staging of host inputs, TMA descriptor creation and the kernel launch
+// sequence. Every arithmetic step of the path runs in the kernels (k_*.cu).
+#include "../../include/prohd.h"
+#include "api_common.cuh"
+#include "prohd_steps.cuh"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+// ================================================================== ABI
+extern "C" {
+
+const char* prohd_version(void) { return "prohd-b200 0.1 sm_100a"; }
+
+int prohd_create(int device, void* cuda_stream, prohd_ctx** out) {
+  if (out == nullptr) return PROHD_E_INVALID;
+  *out = nullptr;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return PROHD_E_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return PROHD_E_DEVICE;
+  prohd_ctx* c = new prohd_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  c->num_sms = prop.multiProcessorCount;
+  *out = c;
+  return PROHD_OK;
+}
+
+int prohd_destroy(prohd_ctx* ctx) {
+  delete ctx;
+  return PROHD_OK;
+}
+
+int prohd_set_stream(prohd_ctx* ctx, void* cuda_stream) {
+  if (ctx == nullptr) return PROHD_E_INVALID;
+  ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+  return PROHD_OK;
+}
+
+const char* prohd_last_error(const prohd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+size_t prohd_workspace_bytes(int64_t nA, int64_t nB, int32_t D, int32_t k, int64_t m, uint32_t flags) {
+  if (nA < 1 || nB < 1 || D < 1) return 0;
+  Carver c{nullptr, 0, 0, true};
+  ExactWs w;
+  size_t exact = carve_exact(c, w, nA, nB, D, (flags & PROHD_WS_HOST_INPUTS) != 0);
+  size_t est = estimate_workspace_bytes(nA, nB, D, k < 0 ? 0 : k, m < 1 ? 1 : m,
+                                        (flags & PROHD_WS_HOST_INPUTS) != 0);
+  return (exact > est ? exact : est) + 256;
+}
+
+int prohd_set_workspace(prohd_ctx* ctx, void* dptr, size_t bytes) {
+  if (ctx == nullptr) return PROHD_E_INVALID;
+  if (dptr != nullptr && (reinterpret_cast<uintptr_t>(dptr) & 255) != 0)
+    return fail(ctx, PROHD_E_INVALID, "workspace must be 256-byte aligned");
+  ctx->ws = static_cast<uint8_t*>(dptr);
+  ctx->ws_bytes = dptr ? bytes : 0;
+  return PROHD_OK;
+}
+
+static int exact_common(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                        ExactWs& w) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if ((rc = check_sets(ctx, A, nA, B, nB, D))) return rc;
+  const bool host_in = !(is_device_ptr(A) && is_device_ptr(B));
+  Carver dry{nullptr, 0, 0, true};
+  ExactWs tmp;
+  size_t need = carve_exact(dry, tmp, nA, nB, D, host_in);
+  if (ctx->ws == nullptr || ctx->ws_bytes < need)
+    return fail(ctx, PROHD_E_WORKSPACE, "workspace too small: need %zu bytes, have %zu", need, ctx->ws_bytes);
+  Carver c{ctx->ws, 0, ctx->ws_bytes, false};
+  carve_exact(c, w, nA, nB, D, host_in);
+  bool hi;
+  if ((rc = stage_inputs(ctx, A, nA, B, nB, D, w.stageA, w.stageB, hi))) return rc;
+  CK(cudaMemsetAsync(w.bad, 0, sizeof(int), ctx->stream));
+  if ((rc = prep_set(ctx, A, nA, D, w.A, w.bad))) return rc;
+  if ((rc = prep_set(ctx, B, nB, D, w.B, w.bad))) return rc;
+  return PROHD_OK;
+}
+
+struct ExactHost {
+  unsigned long long keys[2];
+  double nn_d[2];
+  long long nn_j[2];
+  int bad;
+};
+
+static int fetch(prohd_ctx* ctx, const ExactWs& w, ExactHost& h) {
+  CK(cudaMemcpyAsync(h.keys, w.keys, sizeof h.keys, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(h.nn_d, w.nn_d, sizeof h.nn_d, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(h.nn_j, w.nn_j, sizeof h.nn_j, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&h.bad, w.bad, sizeof h.bad, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (h.bad) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate (or squared norm overflow)");
+  return PROHD_OK;
+}
+
+int directed_hd(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                prohd_directed* out) {
+  if (out == nullptr) return fail(ctx, PROHD_E_INVALID, "null output");
+  ExactWs w;
+  int rc = exact_common(ctx, A, nA, B, nB, D, w);
+  if (rc) return rc;
+  if ((rc = directed_on_ops(ctx, w.A, w.B, D, w, 0))) return rc;
+  ExactHost h;
+  if ((rc = fetch(ctx, w, h))) return rc;
+  fill_directed(out, h.keys[0], h.nn_d[0], h.nn_j[0]);
+  return PROHD_OK;
+}
+
+int hausdorff(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D, prohd_hd* out) {
+  if (out == nullptr) return fail(ctx, PROHD_E_INVALID, "null output");
+  ExactWs w;
+  int rc = exact_common(ctx, A, nA, B, nB, D, w);
+  if (rc) return rc;
+  if ((rc = directed_on_ops(ctx, w.A, w.B, D, w, 0))) return rc;
+  if ((rc = directed_on_ops(ctx, w.B, w.A, D, w, 1))) return rc;
+  ExactHost h;
+  if ((rc = fetch(ctx, w, h))) return rc;
+  fill_directed(&out->ab, h.keys[0], h.nn_d[0], h.nn_j[0]);
+  fill_directed(&out->ba, h.keys[1], h.nn_d[1], h.nn_j[1]);
+  out->value = out->ab.dist2 >= out->ba.dist2 ? out->ab.dist : out->ba.dist;
+  return PROHD_OK;
+}
+
+int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                       float* rowmin_dev) {
+  if (rowmin_dev == nullptr || !is_device_ptr(rowmin_dev))
+    return fail(ctx, PROHD_E_INVALID, "rowmin_dev must be a device pointer");
+  ExactWs w;
+  int rc = exact_common(ctx, A, nA, B, nB, D, w);
+  if (rc) return rc;
+  if ((rc = run_dist(ctx, w.A, w.B, D, rowmin_dev))) return rc;
+  ExactHost h{};
+  CK(cudaMemcpyAsync(&h.bad, w.bad, sizeof h.bad, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (h.bad) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate");
+  return PROHD_OK;
+}
+
+int directed_hd_local(prohd_ctx* ctx, const float* A_local, int64_t nA_local, int64_t row_offset,
+                      const float* B, int64_t nB, int32_t D, uint64_t* key_out) {
+  if (key_out == nullptr) return fail(ctx, PROHD_E_INVALID, "null key_out");
+  if (row_offset < 0) return fail(ctx, PROHD_E_INVALID, "negative row_offset");
+  if (row_offset + nA_local > 0x7FFFFF00LL) return fail(ctx, PROHD_E_INVALID, "global row too large");
+  ExactWs w;
+  int rc = exact_common(ctx, A_local, nA_local, B, nB, D, w);
+  if (rc) return rc;
+  if ((rc = run_dist(ctx, w.A, w.B, D, w.rowmin))) return rc;
+  CK(launch_rowmax_key(w.rowmin, nA_local, row_offset, &w.keys[0], ctx->stream));
+  ExactHost h{};
+  CK(cudaMemcpyAsync(h.keys, w.keys, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&h.bad, w.bad, sizeof h.bad, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (h.bad) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate");
+  *key_out = h.keys[0];
+  return PROHD_OK;
+}
+
+int directed_hd_witness(prohd_ctx* ctx, const float* a, const float* B, int64_t nB, int32_t D,
+                        prohd_directed* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (a == nullptr || out == nullptr) return fail(ctx, PROHD_E_INVALID, "null pointer");
+  if ((rc = check_sets(ctx, a, 1, B, nB, D))) return rc;
+  Carver dry{nullptr, 0, 0, true};
+  ExactWs tmp;
+  const bool host_in = !(is_device_ptr(a) && is_device_ptr(B));
+  size_t need = carve_exact(dry, tmp, 1, nB, D, host_in);
+  if (ctx->ws == nullptr || ctx->ws_bytes < need)
+    return fail(ctx, PROHD_E_WORKSPACE, "workspace too small: need %zu bytes, have %zu", need, ctx->ws_bytes);
+  Carver c{ctx->ws, 0, ctx->ws_bytes, false};
+  ExactWs w;
+  carve_exact(c, w, 1, nB, D, host_in);
+  bool hi;
+  if ((rc = stage_inputs(ctx, a, 1, B, nB, D, w.stageA, w.stageB, hi))) return rc;
+  CK(launch_nn64(a, B, nB, D, w.blk_d, w.blk_j, kNNBlocks, &w.nn_d[0], &w.nn_j[0], ctx->stream));
+  double d;
+  long long j;
+  CK(cudaMemcpyAsync(&d, w.nn_d, sizeof d, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&j, w.nn_j, sizeof j, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  out->b = j;
+  out->dist2 = d;
+  out->dist = std::sqrt(d);
+  out->dist2_tc = NAN;
+  return PROHD_OK;
+}
+
+int prohd_estimate(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D, int32_t k,
+                   int64_t m, prohd_est* out, double* dirs_out, int64_t* idxA_out, int64_t* idxB_out) {
+  return prohd_run(ctx, A, nA, B, nB, D, k, m, nullptr, 0, out, dirs_out, idxA_out, idxB_out);
+}
+
+int prohd_estimate_with_dirs(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                             int32_t n_dirs, int64_t m, const double* dirs, prohd_est* out, int64_t* idxA_out,
+                             int64_t* idxB_out) {
+  if (dirs == nullptr || n_dirs < 1) return fail(ctx, PROHD_E_INVALID, "dirs must be non-null with n_dirs >= 1");
+  return prohd_run(ctx, A, nA, B, nB, D, n_dirs - 1, m, dirs, n_dirs, out, nullptr, idxA_out, idxB_out);
+}
+
+}  // extern "C"

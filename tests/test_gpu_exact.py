@@ -1,0 +1,159 @@
+"""GPU parity for the exact Hausdorff path (K0 + K6 + K7) through the C ABI.
+
+Bar (BASELINE.json north_star):
+  |d2_gpu - d2_ref| <= 1e-5 * (||a||^2 + ||b||^2)
+for every checked row minimum (pair = the row and its oracle nearest neighbour)
+and for the HD value; the reported witness must be a valid one (its fp64
+distance within tolerance of the oracle's value), and the fp64-recomputed
+witness column must be the oracle's exact nearest neighbour of that row.
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2511_18207_b200 import Context
+    return Context(0)
+
+
+def _check_rowmins(A, B, rowmin_gpu, rows=None):
+    ref, arg = oracle.row_minima(A, B, rows=rows)
+    Ar = A if rows is None else A[rows]
+    na = (Ar.astype(np.float64) ** 2).sum(1)
+    nb = (B.astype(np.float64) ** 2).sum(1)[arg]
+    g = rowmin_gpu if rows is None else rowmin_gpu[rows]
+    err = np.abs(g.astype(np.float64) - ref) / (na + nb + 1e-300)
+    assert err.max() <= TOL, f"max rel err {err.max():.3e} at row {int(err.argmax())}"
+    return err.max()
+
+
+def _check_directed(A, B, got, ref):
+    """got = GPU directed result, ref = oracle directed result."""
+    nd = lambda x: float((np.asarray(x, np.float64) ** 2).sum())
+    a_star, b_star = ref["a"], ref["b"]
+    tol = TOL * (nd(A[a_star]) + nd(B[b_star]))
+    assert abs(got["dist2"] - ref["dist2"]) <= tol
+    # the GPU's witness row: its exact fp64 row-min equals the reported value,
+    # and its column is the oracle's nearest neighbour of that row
+    rmin, arg = oracle.row_minima(A, B, rows=np.array([got["a"]]))
+    assert got["b"] == int(arg[0])
+    assert abs(got["dist2"] - rmin[0]) <= 1e-12 * max(1.0, rmin[0])
+    assert abs(got["dist"] - np.sqrt(got["dist2"])) <= 1e-12 * max(1.0, got["dist"])
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (4, 4, 2), (5, 7, 3), (130, 257, 8), (300, 513, 16),
+                                   (129, 255, 20), (1000, 3000, 64), (700, 900, 128), (513, 1100, 256),
+                                   (257, 300, 40)])
+def test_rowmin_random(ctx, shape):
+    nA, nB, D = shape
+    rng = np.random.default_rng(nA * 7 + nB * 13 + D)
+    A = rng.standard_normal((nA, D)).astype(np.float32)
+    B = (rng.standard_normal((nB, D)) * 1.5 + 0.25).astype(np.float32)
+    rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    _check_rowmins(A, B, rm)
+
+
+def test_w3_bit_exact(ctx, golden):
+    """W3 values are exact in fp32; the tie rules must reproduce the oracle exactly."""
+    g = golden["W3"]
+    A = np.array(g["A"], np.float32)
+    B = A + np.array(g["B_offset"], np.float32)
+    h = ctx.hausdorff(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    assert h["value"] == g["H"]
+    assert [h["ab"]["a"], h["ab"]["b"]] == g["h_ab_witness"]
+    assert [h["ba"]["a"], h["ba"]["b"]] == g["h_ba_witness"]
+
+
+def test_w0_w1(ctx, golden):
+    for key in ("W0", "W1"):
+        g = golden[key]
+        A = torch.tensor(g["A"], dtype=torch.float32).cuda()
+        B = torch.tensor(g["B"], dtype=torch.float32).cuda()
+        assert ctx.hausdorff(A, B)["value"] == g["H"]
+    g = golden["W1"]
+    r = ctx.directed_hd(torch.tensor(g["A"], dtype=torch.float32).cuda(),
+                        torch.tensor(g["B"], dtype=torch.float32).cuda())
+    assert [r["a"], r["b"]] == g["h_ab_witness"] and r["dist"] == g["h_ab"]
+
+
+def test_cfg1_full(ctx):
+    A, B = datagen.generate(1)
+    h = ctx.hausdorff(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    ref = oracle.hausdorff(A, B)
+    _check_directed(A, B, h["ab"], ref["ab"])
+    _check_directed(B, A, h["ba"], ref["ba"])
+    # cfg1's witnesses are robust (top-two row-min gap >> tolerance): identical
+    assert (h["ab"]["a"], h["ab"]["b"]) == (ref["ab"]["a"], ref["ab"]["b"])
+    assert (h["ba"]["a"], h["ba"]["b"]) == (ref["ba"]["a"], ref["ba"]["b"])
+    rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    _check_rowmins(A, B, rm)
+
+
+def test_host_inputs_match_device_inputs(ctx):
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((777, 32)).astype(np.float32)
+    B = rng.standard_normal((555, 32)).astype(np.float32)
+    hd = ctx.hausdorff(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    hh = ctx.hausdorff(torch.from_numpy(A), torch.from_numpy(B))  # host pointers -> staged copy
+    assert hd == hh
+
+
+def test_identity_zero_and_symmetry(ctx):
+    rng = np.random.default_rng(6)
+    A = rng.standard_normal((1500, 64)).astype(np.float32)
+    At = torch.from_numpy(A).cuda()
+    h = ctx.hausdorff(At, At.clone())
+    assert h["value"] == 0.0  # fp64 witness re-evaluation of identical points is exactly 0
+    B = rng.standard_normal((900, 64)).astype(np.float32)
+    Bt = torch.from_numpy(B).cuda()
+    assert ctx.hausdorff(At, Bt)["value"] == ctx.hausdorff(Bt, At)["value"]
+
+
+def test_determinism(ctx):
+    A, B = datagen.generate(2, n=20000)
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    r1 = ctx.hausdorff(At, Bt)
+    r2 = ctx.hausdorff(At, Bt)
+    assert r1 == r2
+
+
+def test_errors(ctx):
+    from paper_2511_18207_b200 import ProHDError
+    A = torch.zeros((4, 3), device="cuda")
+    B = torch.zeros((5, 3), device="cuda")
+    with pytest.raises(ProHDError) as e:
+        ctx.directed_hd(A[:0], B)
+    assert e.value.code == 2
+    Bn = B.clone()
+    Bn[2, 1] = float("nan")
+    with pytest.raises(ProHDError) as e:
+        ctx.directed_hd(A, Bn)
+    assert e.value.code == 3
+    Bi = B.clone()
+    Bi[0, 0] = float("inf")
+    with pytest.raises(ProHDError) as e:
+        ctx.hausdorff(A, Bi)
+    assert e.value.code == 3
+
+
+@pytest.mark.parametrize("cfg", [2])
+def test_cfg_full_rows(ctx, cfg):
+    """cfg2 at full size: every row minimum checked."""
+    A, B = datagen.generate(cfg)
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    rm = ctx.directed_hd_rowmin(At, Bt).cpu().numpy()
+    _check_rowmins(A, B, rm)
+    r = ctx.directed_hd(At, Bt)
+    ref_rows = oracle.row_minima(A, B, rows=np.array([r["a"]]))
+    assert abs(r["dist2"] - ref_rows[0][0]) <= 1e-12 * ref_rows[0][0]
+    # no row's true minimum exceeds the reported value by more than the tolerance
+    assert rm.max() <= r["dist2_tc"] + 1e-6
