@@ -66,10 +66,11 @@ def jacobi_eigh(C: np.ndarray, tol: float = 1e-15, max_sweeps: int = 60) -> tupl
             app = A[p, p]
             aqq = A[q, q]
             act = apq != 0.0
-            t = np.zeros_like(apq)
-            tau = np.where(act, (aqq - app) / np.where(act, 2.0 * apq, 1.0), 0.0)
-            sgn = np.where(tau >= 0.0, 1.0, -1.0)
-            t = np.where(act, sgn / (np.abs(tau) + np.sqrt(1.0 + tau * tau)), 0.0)
+            with np.errstate(over="ignore", divide="ignore"):
+                tau = np.where(act, (aqq - app) / np.where(act, 2.0 * apq, 1.0), 0.0)
+                sgn = np.where(tau >= 0.0, 1.0, -1.0)
+                # sqrt(1 + tau^2) as hypot(1, tau): no overflow for |tau| > 1e154 (t -> 0 limit)
+                t = np.where(act, sgn / (np.abs(tau) + np.hypot(1.0, tau)), 0.0)
             c = 1.0 / np.sqrt(1.0 + t * t)
             s = t * c
             # A <- A J (columns p, q)

@@ -1,0 +1,272 @@
+// k_moments.cu — K1: centroid sums and the covariance of A u B (ProHD step 1a).
+//
+// PAPER.md Alg. 1 line 1 (centroids) and Alg. 2 lines 1-2 (P:231-232,
+// "Stack points Z~ = [X;Y]" / "Compute the top m principal components"): the
+// principal components are eigenvectors of
+//     C = (1/N) sum_{p in A u B} (p - mu)(p - mu)^T,   N = nA + nB.
+// One pass over the data with a shift s (fp64 mean of the first <= 4096 rows of
+// A and of B) so no large-mean cancellation occurs:
+//     S_X = sum_{x in X} (x - s),  G = sum_{p in A u B} (p - s)(p - s)^T
+//     mu_X = S_X / n_X + s,  C = G / N - (mu - s)(mu - s)^T.
+// Arithmetic: fp64 (products of exact fp64 differences, fp64 accumulation). The
+// direction parity bar (near-degenerate spectra down to
+// relative gaps 1.1e-4) needs C far more accurate than fp32 tensor-core
+// accumulation gives, so this step runs on the fp64 pipes.
+//
+// Decomposition: the upper triangle of G in 64x64 feature blocks (pair bi <= bj);
+// grid = (pair, point range). 256 threads = 4 groups x 64; each thread owns an
+// 8x8 register block; each group streams its share of every 64-point chunk from
+// shared memory. Per-CTA partials are written to their own slot and reduced in a
+// fixed order (deterministic, run-to-run bit-identical).
+#include "internal.cuh"
+#include "prohd_kernels.cuh"
+
+namespace prohd {
+namespace {
+
+constexpr int kFB = 64;       // feature block
+constexpr int kChunk = 64;    // points per shared-memory chunk
+constexpr int kThreads = 256;
+
+__global__ void __launch_bounds__(256) shift_kernel(const float* __restrict__ A, int64_t nA,
+                                                    const float* __restrict__ B, int64_t nB, int D,
+                                                    double* __restrict__ s) {
+  // one thread per feature: fp64 mean of the first <= 4096 rows of A and of B
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < D; f += gridDim.x * blockDim.x) {
+    const int64_t ca = nA < 4096 ? nA : 4096;
+    const int64_t cb = nB < 4096 ? nB : 4096;
+    double acc = 0.0;
+    for (int64_t i = 0; i < ca; ++i) acc += static_cast<double>(A[i * D + f]);
+    for (int64_t i = 0; i < cb; ++i) acc += static_cast<double>(B[i * D + f]);
+    s[f] = acc / static_cast<double>(ca + cb);
+  }
+}
+
+struct MomArgs {
+  const float* X;
+  int64_t n;
+  int D;
+  const double* s;
+  int nb;          // feature blocks
+  int slot0;       // first partial slot of this set
+  int nranges;     // point ranges for this set
+  int nslots;      // total slots (A + B)
+  double* Gpart;   // [pair][slot][64][64]
+  double* Spart;   // [slot][nb*64]
+};
+
+__device__ __forceinline__ void pair_of(int p, int nb, int& bi, int& bj) {
+  // enumerate (bi <= bj) row-major
+  int r = 0;
+  while (p >= nb - r) {
+    p -= nb - r;
+    ++r;
+  }
+  bi = r;
+  bj = r + p;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) moments_kernel(MomArgs a) {
+  extern __shared__ double cs[];  // [kChunk][128]: features of block bi (0..63) then bj (64..127)
+  const int pair = blockIdx.x;
+  const int range = blockIdx.y;
+  int bi, bj;
+  pair_of(pair, a.nb, bi, bj);
+  const int tid = threadIdx.x;
+  const int g = tid >> 6, t = tid & 63, ti = t >> 3, tj = t & 7;
+  const int64_t per = (a.n + a.nranges - 1) / a.nranges;
+  const int64_t p0 = static_cast<int64_t>(range) * per;
+  const int64_t p1 = p0 + per < a.n ? p0 + per : a.n;
+
+  // loader mapping: thread -> (feature column lf in 0..127, row parity)
+  const int lf = tid & 127;
+  const int lrow = tid >> 7;  // 0..1
+  const int feat = lf < 64 ? bi * kFB + lf : bj * kFB + (lf - 64);
+  const bool fvalid = feat < a.D;
+  const double sf = fvalid ? a.s[feat] : 0.0;
+  double ssum = 0.0;  // column sum of (x - s) for diagonal pairs
+
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+
+  for (int64_t c0 = p0; c0 < p1; c0 += kChunk) {
+    __syncthreads();
+    for (int r = lrow; r < kChunk; r += 2) {
+      const int64_t p = c0 + r;
+      double v = 0.0;
+      if (p < p1 && fvalid) v = static_cast<double>(__ldg(a.X + p * a.D + feat)) - sf;
+      cs[r * 128 + lf] = v;
+      ssum += v;
+    }
+    __syncthreads();
+    const int rend = static_cast<int>(p1 - c0 < kChunk ? p1 - c0 : kChunk);
+    for (int r = g; r < rend; r += 4) {
+      const double* row = cs + r * 128;
+      double x[8], y[8];
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const double2 u = *reinterpret_cast<const double2*>(row + ti * 8 + i);
+        x[i] = u.x;
+        x[i + 1] = u.y;
+        const double2 w = *reinterpret_cast<const double2*>(row + 64 + tj * 8 + i);
+        y[i] = w.x;
+        y[i + 1] = w.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
+    }
+  }
+  // reduce the 4 groups' register blocks through shared memory (fixed order)
+  __syncthreads();
+  double* red = cs;  // 64 x 64 doubles = 32 KB (smem is 64 KB)
+  for (int gg = 1; gg < 4; ++gg) {
+    if (g == gg) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) red[(ti * 8 + i) * 64 + tj * 8 + j] = acc[i][j];
+    }
+    __syncthreads();
+    if (g == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] += red[(ti * 8 + i) * 64 + tj * 8 + j];
+    }
+    __syncthreads();
+  }
+  const int slot = a.slot0 + range;
+  if (g == 0) {
+    double* out = a.Gpart + (static_cast<int64_t>(pair) * a.nslots + slot) * (kFB * kFB);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) out[(ti * 8 + i) * 64 + tj * 8 + j] = acc[i][j];
+  }
+  // column sums: only diagonal pairs, features of block bi (lf < 64); two row parities
+  __syncthreads();
+  if (bi == bj) {
+    double* tmp = cs;
+    tmp[tid] = ssum;
+    __syncthreads();
+    if (tid < 64) {
+      const double v = tmp[tid] + tmp[tid + 128];
+      a.Spart[static_cast<int64_t>(slot) * (a.nb * kFB) + bi * kFB + tid] = v;
+    }
+  }
+}
+
+// G (full symmetric D x D) and S_A, S_B from the partials, fixed summation order.
+__global__ void __launch_bounds__(256) moments_reduce_kernel(const double* __restrict__ Gpart,
+                                                             const double* __restrict__ Spart, int nb, int D,
+                                                             int slotsA, int nslots, double* __restrict__ G,
+                                                             double* __restrict__ SA, double* __restrict__ SB) {
+  const int npairs = nb * (nb + 1) / 2;
+  const int64_t total = static_cast<int64_t>(npairs) * kFB * kFB;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int pair = static_cast<int>(e / (kFB * kFB));
+    const int w = static_cast<int>(e % (kFB * kFB));
+    int bi, bj;
+    pair_of(pair, nb, bi, bj);
+    const int i = bi * kFB + w / kFB, j = bj * kFB + w % kFB;
+    if (i >= D || j >= D) continue;
+    double acc = 0.0;
+    const double* src = Gpart + static_cast<int64_t>(pair) * nslots * (kFB * kFB) + w;
+    for (int s = 0; s < nslots; ++s) acc += src[static_cast<int64_t>(s) * (kFB * kFB)];
+    G[static_cast<int64_t>(i) * D + j] = acc;
+    G[static_cast<int64_t>(j) * D + i] = acc;
+  }
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < D; f += gridDim.x * blockDim.x) {
+    double sa = 0.0, sb = 0.0;
+    for (int s = 0; s < slotsA; ++s) sa += Spart[static_cast<int64_t>(s) * (nb * kFB) + f];
+    for (int s = slotsA; s < nslots; ++s) sb += Spart[static_cast<int64_t>(s) * (nb * kFB) + f];
+    SA[f] = sa;
+    SB[f] = sb;
+  }
+}
+
+// mu and u0 (Alg. 1 line 2) and C (in place over G). One block.
+__global__ void __launch_bounds__(256) moments_finalize_kernel(double* __restrict__ G, const double* __restrict__ SA,
+                                                               const double* __restrict__ SB,
+                                                               const double* __restrict__ s, int64_t nA, int64_t nB,
+                                                               int D, double* __restrict__ mu_out,
+                                                               double* __restrict__ u0, double* __restrict__ dnorm) {
+  __shared__ double red[256];
+  const double N = static_cast<double>(nA + nB);
+  double part = 0.0;
+  for (int f = threadIdx.x; f < D; f += blockDim.x) {
+    const double d = SB[f] / static_cast<double>(nB) - SA[f] / static_cast<double>(nA);  // mu_B - mu_A
+    u0[f] = d;
+    part += d * d;
+    mu_out[f] = (SA[f] + SB[f]) / N + s[f];
+  }
+  red[threadIdx.x] = part;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  const double nrm = sqrt(red[0]);
+  __syncthreads();
+  for (int f = threadIdx.x; f < D; f += blockDim.x) {
+    if (nrm < 1e-9)
+      u0[f] = f == 0 ? 1.0 : 0.0;  // "If ||u|| < 1e-9, set u = e1"
+    else
+      u0[f] = u0[f] / nrm;
+  }
+  if (threadIdx.x == 0) *dnorm = nrm;
+  for (int64_t e = threadIdx.x; e < static_cast<int64_t>(D) * D; e += blockDim.x) {
+    const int i = static_cast<int>(e / D), j = static_cast<int>(e % D);
+    const double mi = (SA[i] + SB[i]) / N, mj = (SA[j] + SB[j]) / N;  // mu - s
+    G[e] = G[e] / N - mi * mj;
+  }
+}
+
+}  // namespace
+
+MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
+  MomentsPlan p;
+  p.nb = (D + kFB - 1) / kFB;
+  p.npairs = p.nb * (p.nb + 1) / 2;
+  const int target = 3 * num_sms;  // CTAs
+  int per_pair = (target + p.npairs - 1) / p.npairs;
+  if (per_pair < 2) per_pair = 2;
+  const double fa = static_cast<double>(nA) / static_cast<double>(nA + nB);
+  p.rangesA = static_cast<int>(per_pair * fa + 0.5);
+  if (p.rangesA < 1) p.rangesA = 1;
+  p.rangesB = per_pair - p.rangesA;
+  if (p.rangesB < 1) p.rangesB = 1;
+  // never more ranges than chunks
+  const int64_t ca = (nA + kChunk - 1) / kChunk, cb = (nB + kChunk - 1) / kChunk;
+  if (p.rangesA > ca) p.rangesA = static_cast<int>(ca);
+  if (p.rangesB > cb) p.rangesB = static_cast<int>(cb);
+  p.nslots = p.rangesA + p.rangesB;
+  p.gpart_doubles = static_cast<int64_t>(p.npairs) * p.nslots * kFB * kFB;
+  p.spart_doubles = static_cast<int64_t>(p.nslots) * p.nb * kFB;
+  return p;
+}
+
+cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB, int D,
+                           const MomentsBufs& b, cudaStream_t st) {
+  shift_kernel<<<(D + 255) / 256, 256, 0, st>>>(A, nA, B, nB, D, b.s);
+  const size_t smem = sizeof(double) * kChunk * 128;
+  cudaError_t e = cudaFuncSetAttribute(moments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  MomArgs a{A, nA, D, b.s, p.nb, 0, p.rangesA, p.nslots, b.Gpart, b.Spart};
+  moments_kernel<<<dim3(p.npairs, p.rangesA), kThreads, smem, st>>>(a);
+  MomArgs bb{B, nB, D, b.s, p.nb, p.rangesA, p.rangesB, p.nslots, b.Gpart, b.Spart};
+  moments_kernel<<<dim3(p.npairs, p.rangesB), kThreads, smem, st>>>(bb);
+  moments_reduce_kernel<<<148 * 2, 256, 0, st>>>(b.Gpart, b.Spart, p.nb, D, p.rangesA, p.nslots, b.C, b.SA,
+                                                 b.SB);
+  moments_finalize_kernel<<<1, 256, 0, st>>>(b.C, b.SA, b.SB, b.s, nA, nB, D, b.mu, b.u0, b.dnorm);
+  return cudaGetLastError();
+}
+
+}  // namespace prohd

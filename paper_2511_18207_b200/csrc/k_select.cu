@@ -1,0 +1,361 @@
+// k_select.cu — K3 projection, K4 top/bottom-m selection, K5 union + gather.
+//
+// PAPER.md Alg. 1 lines 3-9 and Alg. 2 lines 4-11: for
+// each set X and direction u_l, project every point (pi = x^T u), keep
+// the m smallest and m largest projections, and take the union of all kept
+// indices ("keep the unique indices").
+//
+// Selection semantics are the oracle's: the order is
+// that of the fp64 projections of the fp32 points onto the fp64 directions, with
+// ties broken by lower index: bottom = (pi asc, idx asc), top = (pi desc, idx asc).
+//
+// GPU scheme:
+//   K3  pi32 = x . u32 in fp32 (one warp per point; HBM-bound) and max ||x||^2.
+//   K4  radix select (11/11/10-bit digits, 3 histogram rounds over
+//       order-preserving uint32 keys; the bottom tail uses the complemented key)
+//       gives T, the m-th best fp32 projection per (direction, tail).
+//       Every point with pi32 within the guard band 2*eps of T (or better) is a
+//       candidate, eps = (D + 8) 2^-24 max||x|| bounding |pi32 - pi64|, so the
+//       true fp64 top-m is always inside the band. Candidates are re-ranked by
+//       their fp64 projection (fp64 dot with the fp64 direction) and the total
+//       order above; rank < m is kept, at position `rank` of the list.
+//   K5  kept indices are OR-ed into an n-bit bitmap; one CTA compacts it into
+//       the sorted unique union; the rows are gathered for the subset HD.
+#include "internal.cuh"
+#include "prohd_kernels.cuh"
+
+#include <cfloat>
+
+namespace prohd {
+namespace {
+
+__device__ __forceinline__ unsigned order_key(float f) {
+  unsigned u = __float_as_uint(f == 0.0f ? 0.0f : f);  // canonicalise -0 -> +0
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_to_float(unsigned k) {
+  const unsigned u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(u);
+}
+
+// ------------------------------------------------------------------ K3
+constexpr int kProjGroup = 8;
+
+__global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ X, int64_t n, int D,
+                                                      const float* __restrict__ U32, int L,
+                                                      float* __restrict__ P32, unsigned* maxnorm2) {
+  extern __shared__ float su[];  // [L][D]
+  for (int i = threadIdx.x; i < L * D; i += blockDim.x) su[i] = U32[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  float wmax = 0.0f;
+  for (int64_t r = warp; r < n; r += nwarps) {
+    const float* x = X + r * D;
+    float nrm = 0.0f;
+    for (int g0 = 0; g0 < L; g0 += kProjGroup) {
+      float acc[kProjGroup];
+#pragma unroll
+      for (int j = 0; j < kProjGroup; ++j) acc[j] = 0.0f;
+      for (int c = lane; c < D; c += 32) {
+        const float v = __ldg(x + c);
+        if (g0 == 0) nrm = fmaf(v, v, nrm);
+#pragma unroll
+        for (int j = 0; j < kProjGroup; ++j)
+          if (g0 + j < L) acc[j] = fmaf(v, su[(g0 + j) * D + c], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kProjGroup; ++j) {
+        float s = acc[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == j && g0 + j < L) P32[static_cast<int64_t>(g0 + j) * n + r] = s;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    // non-finite input must poison the max (fmaxf would drop a NaN)
+    wmax = (isfinite(nrm) && isfinite(wmax)) ? fmaxf(wmax, nrm) : __int_as_float(0x7fffffff);
+  }
+  if (lane == 0) atomicMax(maxnorm2, __float_as_uint(wmax));  // non-negative floats order as uints
+}
+
+// ------------------------------------------------------------------ K4 radix select
+__device__ __forceinline__ void round_params(int round, int& shift, unsigned& binmask) {
+  if (round == 0) {
+    shift = 21;
+    binmask = 0x7FFu;
+  } else if (round == 1) {
+    shift = 10;
+    binmask = 0x7FFu;
+  } else {
+    shift = 0;
+    binmask = 0x3FFu;
+  }
+}
+
+__global__ void __launch_bounds__(256) radix_hist_kernel(const float* __restrict__ P32, int64_t n, int L,
+                                                         const int* n_dirs, int round,
+                                                         const unsigned* __restrict__ state, unsigned* hist) {
+  __shared__ unsigned sh[2][kRadixBins];
+  const int l = blockIdx.y;
+  if (l >= *n_dirs) return;
+  for (int i = threadIdx.x; i < 2 * kRadixBins; i += blockDim.x) (&sh[0][0])[i] = 0u;
+  __syncthreads();
+  int shift;
+  unsigned binmask;
+  round_params(round, shift, binmask);
+  const unsigned pre0 = state[(l * 2 + 0) * 4 + 0], msk0 = state[(l * 2 + 0) * 4 + 1];
+  const unsigned pre1 = state[(l * 2 + 1) * 4 + 0], msk1 = state[(l * 2 + 1) * 4 + 1];
+  const float* p = P32 + static_cast<int64_t>(l) * n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const unsigned kt = order_key(__ldg(p + i));
+    const unsigned kb = ~kt;
+    if ((kt & msk0) == pre0) atomicAdd(&sh[0][(kt >> shift) & binmask], 1u);
+    if ((kb & msk1) == pre1) atomicAdd(&sh[1][(kb >> shift) & binmask], 1u);
+  }
+  __syncthreads();
+  unsigned* g = hist + (static_cast<int64_t>(round) * L + l) * 2 * kRadixBins;
+  for (int i = threadIdx.x; i < 2 * kRadixBins; i += blockDim.x) {
+    const unsigned v = (&sh[0][0])[i];
+    if (v) atomicAdd(g + i, v);
+  }
+}
+
+// one thread per (direction, tail): walk the bins from the top
+__global__ void radix_scan_kernel(const unsigned* __restrict__ hist, int L, const int* n_dirs, int round,
+                                  unsigned* state) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= 2 * L) return;
+  const int l = id >> 1, t = id & 1;
+  if (l >= *n_dirs) return;
+  int shift;
+  unsigned binmask;
+  round_params(round, shift, binmask);
+  const unsigned* h = hist + ((static_cast<int64_t>(round) * L + l) * 2 + t) * kRadixBins;
+  unsigned* s = state + (l * 2 + t) * 4;
+  unsigned rem = s[2];
+  unsigned cum = 0;
+  int b = static_cast<int>(binmask);
+  for (; b > 0; --b) {
+    if (cum + h[b] >= rem) break;
+    cum += h[b];
+  }
+  s[0] |= static_cast<unsigned>(b) << shift;
+  s[1] |= binmask << shift;
+  s[2] = rem - cum;
+}
+
+__global__ void __launch_bounds__(256) collect_kernel(const float* __restrict__ P32, int64_t n, int D, int L,
+                                                      const int* n_dirs, const unsigned* __restrict__ state,
+                                                      const unsigned* maxnorm2, int* cand, unsigned* ccount,
+                                                      int64_t cap, int* overflow) {
+  const int l = blockIdx.y;
+  if (l >= *n_dirs) return;
+  const double eps = (D + 8) * 0x1p-24 * sqrt(static_cast<double>(__uint_as_float(*maxnorm2))) * 1.0625;
+  const double Ttop = static_cast<double>(key_to_float(state[(l * 2 + 0) * 4 + 0]));
+  const double Tbot = static_cast<double>(key_to_float(~state[(l * 2 + 1) * 4 + 0]));
+  const double lo_top = Ttop - 2.0 * eps;  // top candidates: pi >= lo_top
+  const double hi_bot = Tbot + 2.0 * eps;  // bottom candidates: pi <= hi_bot
+  const float* p = P32 + static_cast<int64_t>(l) * n;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n;
+       base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const double v = i < n ? static_cast<double>(__ldg(p + i)) : 0.0;
+    const bool ct = i < n && v >= lo_top;
+    const bool cb = i < n && v <= hi_bot;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const bool c = t == 0 ? ct : cb;
+      const unsigned bal = __ballot_sync(0xffffffffu, c);
+      if (bal == 0u) continue;
+      unsigned pos0 = 0;
+      if (lane == 0) pos0 = atomicAdd(&ccount[l * 2 + t], __popc(bal));
+      pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+      if (c) {
+        const unsigned pos = pos0 + __popc(bal & ((1u << lane) - 1u));
+        if (pos < cap)
+          cand[(static_cast<int64_t>(l) * 2 + t) * cap + pos] = static_cast<int>(i);
+        else
+          *overflow = 1;
+      }
+    }
+  }
+}
+
+// fp64 projection of every candidate: one warp per candidate
+__global__ void __launch_bounds__(256) cand_p64_kernel(const float* __restrict__ X, int D,
+                                                       const double* __restrict__ U64, int L, const int* n_dirs,
+                                                       const int* __restrict__ cand, const unsigned* ccount,
+                                                       int64_t cap, double* cval) {
+  const int lt = blockIdx.y;  // l*2 + t
+  const int l = lt >> 1;
+  if (l >= *n_dirs) return;
+  const unsigned cnt = min(static_cast<int64_t>(ccount[lt]), cap);
+  const int lane = threadIdx.x & 31;
+  const double* u = U64 + static_cast<int64_t>(l) * D;
+  for (int64_t c = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; c < cnt;
+       c += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int i = cand[static_cast<int64_t>(lt) * cap + c];
+    const float* x = X + static_cast<int64_t>(i) * D;
+    double s = 0.0;
+    for (int d = lane; d < D; d += 32) s = fma(static_cast<double>(__ldg(x + d)), u[d], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) cval[static_cast<int64_t>(lt) * cap + c] = s;
+  }
+}
+
+// rank of each candidate in its (direction, tail) total order; keep rank < m
+__global__ void __launch_bounds__(256) rank_kernel(int L, const int* n_dirs, const int* __restrict__ cand,
+                                                   const double* __restrict__ cval, const unsigned* ccount,
+                                                   int64_t cap, int64_t m, int* lists, unsigned* bitmap) {
+  const int lt = blockIdx.y;
+  const int l = lt >> 1, t = lt & 1;
+  if (l >= *n_dirs) return;
+  const int64_t cnt = min(static_cast<int64_t>(ccount[lt]), cap);
+  const int* ci = cand + static_cast<int64_t>(lt) * cap;
+  const double* cv = cval + static_cast<int64_t>(lt) * cap;
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < cnt;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = cv[c];
+    const int i = ci[c];
+    int64_t rank = 0;
+    for (int64_t o = 0; o < cnt; ++o) {
+      const double w = cv[o];
+      const int j = ci[o];
+      const bool better = (t == 0) ? (w > v || (w == v && j < i)) : (w < v || (w == v && j < i));
+      rank += better ? 1 : 0;
+    }
+    if (rank < m) {
+      lists[static_cast<int64_t>(lt) * m + rank] = i;
+      atomicOr(&bitmap[i >> 5], 1u << (i & 31));
+    }
+  }
+}
+
+// single-CTA compaction of the bitmap into the sorted unique union
+__global__ void __launch_bounds__(1024) compact_kernel(const unsigned* __restrict__ bitmap, int64_t nwords,
+                                                       long long* uidx, unsigned* ucount) {
+  __shared__ unsigned part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (nwords + 1023) / 1024;
+  const int64_t w0 = tid * per, w1 = min(nwords, w0 + per);
+  unsigned c = 0;
+  for (int64_t w = w0; w < w1; ++w) c += __popc(bitmap[w]);
+  part[tid] = c;
+  __syncthreads();
+  // inclusive scan (Hillis-Steele)
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned v = tid >= o ? part[tid - o] : 0u;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  unsigned pos = part[tid] - c;
+  for (int64_t w = w0; w < w1; ++w) {
+    unsigned bits = bitmap[w];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      uidx[pos++] = w * 32 + b;
+      bits &= bits - 1;
+    }
+  }
+  if (tid == 1023) *ucount = part[1023];
+}
+
+__global__ void iota_kernel(long long* idx, unsigned* count, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    idx[i] = i;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = static_cast<unsigned>(n);
+}
+
+__global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ X, int D,
+                                                     const long long* __restrict__ idx, const unsigned* count,
+                                                     float* __restrict__ Y) {
+  const unsigned n = *count;
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const float* src = X + idx[r] * D;
+    float* dst = Y + r * D;
+    for (int c = lane; c < D; c += 32) dst[c] = __ldg(src + c);
+  }
+}
+
+__global__ void dirs_to_f32_kernel(const double* U64, float* U32, int total) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
+    U32[i] = static_cast<float>(U64[i]);
+}
+
+__global__ void init_state_kernel(unsigned* state, int L, int64_t m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 2 * L) {
+    state[i * 4 + 0] = 0u;
+    state[i * 4 + 1] = 0u;
+    state[i * 4 + 2] = static_cast<unsigned>(m);
+    state[i * 4 + 3] = 0u;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_dirs_to_f32(const double* U64, float* U32, int rows, int D, cudaStream_t st) {
+  dirs_to_f32_kernel<<<(rows * D + 255) / 256, 256, 0, st>>>(U64, U32, rows * D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
+                          const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(b.maxnorm2, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.hist, 0, sizeof(unsigned) * 3 * L * 2 * kRadixBins, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.ccount, 0, sizeof(unsigned) * 2 * L, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.bitmap, 0, sizeof(unsigned) * ((n + 31) / 32), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.overflow, 0, sizeof(int), st)) != cudaSuccess) return e;
+  init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, m);
+  // K3
+  const size_t psmem = sizeof(float) * L * D;
+  if ((e = cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(psmem))) != cudaSuccess)
+    return e;
+  int64_t pblocks = (n + 7) / 8;
+  if (pblocks > 148 * 8) pblocks = 148 * 8;
+  project_kernel<<<static_cast<int>(pblocks), 256, psmem, st>>>(X, n, D, U32, L, b.P32, b.maxnorm2);
+  // K4: three radix rounds
+  int64_t hb = (n + 255) / 256;
+  if (hb > 148 * 2) hb = 148 * 2;
+  for (int r = 0; r < 3; ++r) {
+    radix_hist_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, L, n_dirs, r, b.state, b.hist);
+    radix_scan_kernel<<<(2 * L + 63) / 64, 64, 0, st>>>(b.hist, L, n_dirs, r, b.state);
+  }
+  collect_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, D, L, n_dirs, b.state, b.maxnorm2,
+                                                                     b.cand, b.ccount, b.cap, b.overflow);
+  cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
+  rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap);
+  // K5
+  compact_kernel<<<1, 1024, 0, st>>>(b.bitmap, (n + 31) / 32, b.uidx, b.ucount);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_iota(long long* idx, unsigned* count, int64_t n, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  iota_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(idx, count, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const float* X, int D, const long long* idx, const unsigned* count, int64_t cap,
+                          float* Y, cudaStream_t st) {
+  int64_t blocks = (cap + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  gather_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(X, D, idx, count, Y);
+  return cudaGetLastError();
+}
+
+}  // namespace prohd

@@ -1,14 +1,228 @@
-// prohd_estimate.cu — ProHD Alg. 3 orchestration (filled in by the K1-K5 kernels).
+// prohd_estimate.cu — orchestration of ProHD Alg. 3 on the device.
+//
+//   step 1a  K1 moments: centroids + covariance of A u B            (Alg.1 l.1, Alg.2 l.1-2)
+//   step 1b  u0 = normalised centroid difference (e1 rule) + K2 eigen (Alg.1 l.2, Alg.2 l.2)
+//   step 2   K3 projections onto U = [u0 u1..uk]                     (Alg.1 l.3-4, Alg.2 l.5-7)
+//   step 3   K4 top/bottom-m per direction, K5 union + gather        (Alg.1 l.5-9, Alg.2 l.8-11, Alg.3 l.4-5)
+//   step 4   K0+K6+K7 exact HD on the subsets, both directions       (Alg.3 l.6-7)
+// One host synchronisation (after step 3) reads the subset sizes to size the
+// distance-kernel launches; everything else is stream-ordered.
 #include "api_common.cuh"
+#include "prohd_kernels.cuh"
 #include "prohd_steps.cuh"
 
+#include <vector>
+
 namespace prohd {
-size_t estimate_workspace_bytes(int64_t, int64_t, int, int, int64_t, bool) { return 0; }
+
+struct EstWs {
+  float* stageA = nullptr;
+  float* stageB = nullptr;
+  MomentsBufs mom{};
+  double* V = nullptr;
+  double* Xe = nullptr;
+  double* U64 = nullptr;
+  float* U32 = nullptr;
+  double* lam = nullptr;
+  int* n_dirs = nullptr;
+  SelectBufs sel[2]{};
+  float* Xs[2] = {nullptr, nullptr};
+  SetOps ops[2];
+  float* rowmin = nullptr;
+  unsigned long long* keys = nullptr;
+  double* nn_d = nullptr;
+  long long* nn_j = nullptr;
+  double* blk_d = nullptr;
+  long long* blk_j = nullptr;
+  int* bad = nullptr;
+  int64_t capU[2] = {0, 0};
+};
+
+static void carve_select(Carver& c, SelectBufs& b, int64_t n, int L, int64_t m) {
+  b.cap = n < m + 65536 ? n : m + 65536;
+  b.P32 = c.take<float>(static_cast<int64_t>(L) * n);
+  b.maxnorm2 = c.take<unsigned>(1);
+  b.hist = c.take<unsigned>(static_cast<int64_t>(3) * L * 2 * kRadixBins);
+  b.state = c.take<unsigned>(static_cast<int64_t>(L) * 2 * 4);
+  b.cand = c.take<int>(static_cast<int64_t>(L) * 2 * b.cap);
+  b.cval = c.take<double>(static_cast<int64_t>(L) * 2 * b.cap);
+  b.ccount = c.take<unsigned>(static_cast<int64_t>(L) * 2);
+  b.lists = c.take<int>(static_cast<int64_t>(L) * 2 * m);
+  b.bitmap = c.take<unsigned>((n + 31) / 32);
+  const int64_t capU = n < 2 * m * L ? n : 2 * m * L;
+  b.uidx = c.take<long long>(capU > n ? n : (2 * m >= n ? n : capU));
+  b.ucount = c.take<unsigned>(1);
+  b.overflow = c.take<int>(1);
+}
+
+static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int k, int64_t m, bool host_inputs,
+                        int num_sms) {
+  const int L = k + 1;
+  if (host_inputs) {
+    w.stageA = c.take<float>(nA * D);
+    w.stageB = c.take<float>(nB * D);
+  }
+  const MomentsPlan mp = plan_moments(nA, nB, D, num_sms);
+  w.mom.s = c.take<double>(D);
+  w.mom.Gpart = c.take<double>(mp.gpart_doubles);
+  w.mom.Spart = c.take<double>(mp.spart_doubles);
+  w.mom.C = c.take<double>(static_cast<int64_t>(D) * D);
+  w.mom.SA = c.take<double>(D);
+  w.mom.SB = c.take<double>(D);
+  w.mom.mu = c.take<double>(D);
+  w.mom.dnorm = c.take<double>(1);
+  w.V = c.take<double>(static_cast<int64_t>(D) * D);
+  w.Xe = c.take<double>(static_cast<int64_t>(k > 0 ? k : 1) * D);
+  w.U64 = c.take<double>(static_cast<int64_t>(L) * D);
+  w.mom.u0 = w.U64;  // row 0 of U is the centroid axis
+  w.U32 = c.take<float>(static_cast<int64_t>(L) * D);
+  w.lam = c.take<double>(k > 0 ? k : 1);
+  w.n_dirs = c.take<int>(1);
+  const int64_t n[2] = {nA, nB};
+  for (int s = 0; s < 2; ++s) {
+    carve_select(c, w.sel[s], n[s], L, m);
+    w.capU[s] = (2 * m >= n[s]) ? n[s] : (n[s] < 2 * m * L ? n[s] : 2 * m * L);
+    w.Xs[s] = c.take<float>(w.capU[s] * D);
+    carve_set(c, w.ops[s], w.capU[s], D);
+  }
+  w.rowmin = c.take<float>(w.capU[0] > w.capU[1] ? w.capU[0] : w.capU[1]);
+  w.keys = c.take<unsigned long long>(2);
+  w.nn_d = c.take<double>(2);
+  w.nn_j = c.take<long long>(2);
+  w.blk_d = c.take<double>(kNNBlocks);
+  w.blk_j = c.take<long long>(kNNBlocks);
+  w.bad = c.take<int>(1);
+  return c.off;
+}
+
+size_t estimate_workspace_bytes(int64_t nA, int64_t nB, int D, int k, int64_t m, bool host_inputs) {
+  Carver c{nullptr, 0, 0, true};
+  EstWs w;
+  return carve_est(c, w, nA, nB, D, k, m, host_inputs, 148);
+}
+
 }  // namespace prohd
 
-int prohd_run(prohd_ctx* ctx, const float*, int64_t, const float*, int64_t, int32_t, int32_t, int64_t,
-              const double*, int32_t, prohd_est*, double*, int64_t*, int64_t*) {
+int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D, int32_t k,
+              int64_t m, const double* dirs_in, int32_t n_dirs_in, prohd_est* out, double* dirs_out,
+              int64_t* idxA_out, int64_t* idxB_out) {
   int rc = enter(ctx);
   if (rc) return rc;
-  return fail(ctx, PROHD_E_NOTIMPL, "prohd_estimate not built yet");
+  if (out == nullptr) return fail(ctx, PROHD_E_INVALID, "null output");
+  if ((rc = check_sets(ctx, A, nA, B, nB, D))) return rc;
+  if (k < 0 || k > D) return fail(ctx, PROHD_E_INVALID, "k must satisfy 0 <= k <= D (k=%d, D=%d)", k, D);
+  if (m < 1) return fail(ctx, PROHD_E_INVALID, "m must be >= 1 (m=%lld)", static_cast<long long>(m));
+  if (dirs_in == nullptr && k > 0 && D > 256)
+    return fail(ctx, PROHD_E_NOTIMPL, "the device eigen-solver supports D <= 256 (D=%d)", D);
+  if (m > 0x7FFFFFFFLL) return fail(ctx, PROHD_E_INVALID, "m too large");
+  const int L = k + 1;
+  const bool host_in = !(is_device_ptr(A) && is_device_ptr(B));
+  Carver dry{nullptr, 0, 0, true};
+  EstWs tmp;
+  const size_t need = carve_est(dry, tmp, nA, nB, D, k, m, host_in, ctx->num_sms);
+  if (ctx->ws == nullptr || ctx->ws_bytes < need)
+    return fail(ctx, PROHD_E_WORKSPACE, "workspace too small: need %zu bytes, have %zu", need, ctx->ws_bytes);
+  Carver c{ctx->ws, 0, ctx->ws_bytes, false};
+  EstWs w;
+  carve_est(c, w, nA, nB, D, k, m, host_in, ctx->num_sms);
+  cudaStream_t st = ctx->stream;
+  bool hi;
+  if ((rc = stage_inputs(ctx, A, nA, B, nB, D, w.stageA, w.stageB, hi))) return rc;
+  CK(cudaMemsetAsync(w.bad, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(w.U64, 0, sizeof(double) * L * D, st));
+
+  // ------------------------------------------------------------ step 1: directions
+  if (dirs_in == nullptr) {
+    const MomentsPlan mp = plan_moments(nA, nB, D, ctx->num_sms);
+    CK(launch_moments(mp, A, nA, B, nB, D, w.mom, st));
+    if (k > 0) {
+      CK(launch_eigen_topk(w.mom.C, D, k, w.V, w.Xe, w.U64, w.U32, w.lam, w.n_dirs, st));
+    } else {
+      const int one = 1;
+      CK(cudaMemcpyAsync(w.n_dirs, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    CK(launch_dirs_to_f32(w.U64, w.U32, L, D, st));
+  } else {
+    CK(cudaMemcpyAsync(w.U64, dirs_in, sizeof(double) * n_dirs_in * D, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.n_dirs, &n_dirs_in, sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(launch_dirs_to_f32(w.U64, w.U32, L, D, st));
+  }
+
+  // ------------------------------------------------------------ steps 2-3: projection, selection, union
+  const float* X[2] = {A, B};
+  const int64_t n[2] = {nA, nB};
+  for (int s = 0; s < 2; ++s) {
+    // projections run for every point (also when 2m >= n) so non-finite input is always detected
+    SelectBufs& b = w.sel[s];
+    if (2 * m >= n[s]) {
+      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, st));  // finiteness pass
+      CK(launch_iota(b.uidx, b.ucount, n[s], st));
+    } else {
+      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m, b, st));
+    }
+  }
+  unsigned ucount[2];
+  int ndirs = 0, ovf[2] = {0, 0};
+  unsigned maxn[2];
+  CK(cudaMemcpyAsync(&ucount[0], w.sel[0].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&ucount[1], w.sel[1].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&ovf[0], w.sel[0].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&ovf[1], w.sel[1].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&maxn[0], w.sel[0].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&maxn[1], w.sel[1].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&ndirs, w.n_dirs, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int s = 0; s < 2; ++s) {
+    float f;
+    std::memcpy(&f, &maxn[s], 4);
+    if (!std::isfinite(f)) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate (or squared norm overflow)");
+  }
+  if (ovf[0] || ovf[1])
+    return fail(ctx, PROHD_E_INTERNAL, "selection guard band overflow (more than m + 65536 candidates)");
+  if (ucount[0] < 1 || ucount[1] < 1 || ucount[0] > w.capU[0] || ucount[1] > w.capU[1])
+    return fail(ctx, PROHD_E_INTERNAL, "bad union sizes %u %u", ucount[0], ucount[1]);
+
+  // ------------------------------------------------------------ step 4: exact HD on the subsets
+  for (int s = 0; s < 2; ++s) {
+    CK(launch_gather(X[s], D, w.sel[s].uidx, w.sel[s].ucount, ucount[s], w.Xs[s], st));
+    w.ops[s].n = ucount[s];
+    if ((rc = prep_set(ctx, w.Xs[s], ucount[s], D, w.ops[s], w.bad))) return rc;
+  }
+  ExactWs ew;
+  ew.rowmin = w.rowmin;
+  ew.keys = w.keys;
+  ew.nn_d = w.nn_d;
+  ew.nn_j = w.nn_j;
+  ew.blk_d = w.blk_d;
+  ew.blk_j = w.blk_j;
+  if ((rc = directed_on_ops(ctx, w.ops[0], w.ops[1], D, ew, 0))) return rc;
+  if ((rc = directed_on_ops(ctx, w.ops[1], w.ops[0], D, ew, 1))) return rc;
+  unsigned long long keys[2];
+  double nn_d[2];
+  long long nn_j[2];
+  CK(cudaMemcpyAsync(keys, w.keys, sizeof keys, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(nn_d, w.nn_d, sizeof nn_d, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(nn_j, w.nn_j, sizeof nn_j, cudaMemcpyDeviceToHost, st));
+  std::vector<long long> ua(ucount[0]), ub(ucount[1]);
+  CK(cudaMemcpyAsync(ua.data(), w.sel[0].uidx, sizeof(long long) * ucount[0], cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ub.data(), w.sel[1].uidx, sizeof(long long) * ucount[1], cudaMemcpyDeviceToHost, st));
+  if (dirs_out != nullptr)
+    CK(cudaMemcpyAsync(dirs_out, w.U64, sizeof(double) * L * D, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+
+  fill_directed(&out->ab, keys[0], nn_d[0], nn_j[0]);
+  fill_directed(&out->ba, keys[1], nn_d[1], nn_j[1]);
+  // map subset rows to original indices (a in the first argument, b in the second)
+  out->ab.a = ua[out->ab.a];
+  out->ab.b = ub[out->ab.b];
+  out->ba.a = ub[out->ba.a];
+  out->ba.b = ua[out->ba.b];
+  out->value = out->ab.dist2 >= out->ba.dist2 ? out->ab.dist : out->ba.dist;
+  out->size_a = ucount[0];
+  out->size_b = ucount[1];
+  out->n_dirs = ndirs;
+  out->_pad = 0;
+  if (idxA_out) std::memcpy(idxA_out, ua.data(), sizeof(long long) * ucount[0]);
+  if (idxB_out) std::memcpy(idxB_out, ub.data(), sizeof(long long) * ucount[1]);
+  return PROHD_OK;
 }

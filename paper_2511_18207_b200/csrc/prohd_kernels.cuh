@@ -1,0 +1,62 @@
+// prohd_kernels.cuh — launchers of the ProHD-specific kernels (K1 moments, K2
+// eigen, K3 projection, K4 selection, K5 union/gather).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace prohd {
+
+// ---------------------------------------------------------------- K1
+struct MomentsPlan {
+  int nb = 0, npairs = 0, rangesA = 0, rangesB = 0, nslots = 0;
+  int64_t gpart_doubles = 0, spart_doubles = 0;
+};
+struct MomentsBufs {
+  double* s;      // [D] shift
+  double* Gpart;  // partial Grams
+  double* Spart;  // partial column sums
+  double* C;      // [D][D] -> covariance
+  double* SA;     // [D]
+  double* SB;     // [D]
+  double* mu;     // [D] mean of A u B
+  double* u0;     // [D] centroid axis (row 0 of U64)
+  double* dnorm;  // ||mu_B - mu_A||
+};
+MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms);
+cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB, int D,
+                           const MomentsBufs& b, cudaStream_t st);
+
+// ---------------------------------------------------------------- K2
+// Top-k eigenvectors of C (destroyed). Writes rows 1..k of out64/out32 ([k+1][D]),
+// lam[0..k), and *n_dirs = 1 + number kept. V: D*D doubles, X: k*D doubles scratch.
+cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, double* out64, float* out32,
+                              double* lam, int* n_dirs, cudaStream_t st);
+// U32 = (float)U64 for rows [0, rows)
+cudaError_t launch_dirs_to_f32(const double* U64, float* U32, int rows, int D, cudaStream_t st);
+
+// ---------------------------------------------------------------- K3/K4/K5 (one point set)
+constexpr int kRadixBins = 2048;
+struct SelectBufs {
+  float* P32;             // [L][n] fp32 projections, direction-major
+  unsigned* maxnorm2;     // float bits of max ||x||^2 (atomicMax)
+  unsigned* hist;         // [3 rounds][L][2][kRadixBins]
+  unsigned* state;        // [L][2][4]: prefix, mask, remaining, unused
+  int* cand;              // [L][2][cap]
+  double* cval;           // [L][2][cap]
+  unsigned* ccount;       // [L][2]
+  int* lists;             // [L][2][m]
+  unsigned* bitmap;       // [ceil(n/32)]
+  long long* uidx;        // sorted unique union (capacity min(n, 2mL))
+  unsigned* ucount;       // union size
+  int* overflow;          // guard-band overflow flag
+  int64_t cap;            // candidates per list
+};
+cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
+                          const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st);
+// Gather rows X[idx[i]] -> Y (row-major, stride D) for i < count (count on the device).
+cudaError_t launch_gather(const float* X, int D, const long long* idx, const unsigned* count, int64_t cap,
+                          float* Y, cudaStream_t st);
+cudaError_t launch_iota(long long* idx, unsigned* count, int64_t n, cudaStream_t st);
+
+}  // namespace prohd

@@ -1,0 +1,208 @@
+"""GPU parity for ProHD (Alg. 3) through the C ABI, layered as SURVEY.md §8(c4):
+
+  L2 directions   u0 within 1e-9; each PC an eigenvector of the oracle's C
+                  (residual <= 1e-9 ||C||) and, where the oracle's spectral gap
+                  allows, within the Davis-Kahan angle of the oracle's PC.
+  L3 selection    the oracle run with the GPU's directions injected: per-set
+                  unions bit-exact, except swaps across the m-th boundary between
+                  points whose fp64 projections differ by <= 1e-6 max(||p||,||q||)
+                  (north_star "bit-exact except at projection ties within 1e-6").
+  L4 subset HD    same subsets -> |H^_gpu - H^_ref| <= 1e-4 H^_ref and the d2
+                  tolerance 1e-5 (||a||^2 + ||b||^2) on the witness pair.
+  L5 end to end   the oracle with its own C and Jacobi directions.
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+from oracle import prohd as OP
+
+pytestmark = pytest.mark.gpu
+
+TIE = 1e-6
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2511_18207_b200 import Context
+    return Context(0)
+
+
+def _excused_union_diff(X, U, m, got, ref):
+    """Set differences allowed only as boundary swaps at projection ties (<= TIE relative)."""
+    got, ref = set(got.tolist()), set(ref.tolist())
+    extra, missing = got - ref, ref - got
+    if not extra and not missing:
+        return 0
+    P = X.astype(np.float64) @ U
+    nrm = np.linalg.norm(X.astype(np.float64), axis=1)
+    # every extra/missing point must sit within TIE of the m-th boundary value on some direction/tail
+    for i in extra | missing:
+        ok = False
+        for l in range(U.shape[1]):
+            srt = np.sort(P[:, l])
+            for bval in (srt[m - 1], srt[-m]):
+                if abs(P[i, l] - bval) <= TIE * max(nrm[i], 1e-30) * 2:
+                    ok = True
+        assert ok, f"index {i} differs without a projection tie"
+    return len(extra) + len(missing)
+
+
+def _run(ctx, A, B, k, m):
+    return ctx.prohd_estimate(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), k, m,
+                              return_dirs=True, return_indices=True)
+
+
+def _check_layers(ctx, A, B, k, m, exact_sets=True):
+    g = _run(ctx, A, B, k, m)
+    U = g["U"]
+    ref = OP.estimate(A, B, k, m)
+    # L2: directions
+    assert np.linalg.norm(U[:, 0] - ref["u0"]) <= 1e-9
+    C = ref["C"]
+    cn = np.linalg.norm(C, 2)
+    assert g["n_dirs"] == ref["n_dirs"]
+    lam = np.sort(np.linalg.eigvalsh(C))[::-1]
+    for l in range(1, U.shape[1]):
+        v = U[:, l]
+        assert abs(np.linalg.norm(v) - 1) <= 1e-12
+        r = C @ v - (v @ C @ v) * v
+        assert np.linalg.norm(r) <= 1e-9 * cn, f"PC{l} residual {np.linalg.norm(r) / cn:.2e}"
+        gap = min(abs(lam[l - 1] - lam[j]) for j in range(len(lam)) if j != l - 1)
+        if gap > 1e-6 * lam[0]:
+            s = np.linalg.norm(v - (v @ ref["U"][:, l]) * ref["U"][:, l])
+            assert s <= 1e-9 * cn / gap + 1e-12, f"PC{l} angle {s:.2e}, gap {gap / lam[0]:.2e}"
+    # L3: oracle with the GPU's directions injected
+    inj = OP.estimate(A, B, k, m, U=U)
+    nd = _excused_union_diff(A, U, m, g["IA"], inj["IA"]) + _excused_union_diff(B, U, m, g["IB"], inj["IB"])
+    if exact_sets:
+        assert nd == 0
+    # L4: subset HD on identical subsets
+    if nd == 0:
+        assert abs(g["value"] - inj["value"]) <= 1e-4 * inj["value"] + 1e-12
+        for side in ("ab", "ba"):
+            a_set, b_set = (A, B) if side == "ab" else (B, A)
+            tol = 1e-5 * (float((a_set[inj[side]["a"]].astype(np.float64) ** 2).sum())
+                          + float((b_set[inj[side]["b"]].astype(np.float64) ** 2).sum()))
+            assert abs(g[side]["dist2"] - inj[side]["dist2"]) <= tol
+    # L5: end to end against the oracle's own directions
+    assert g["size_a"] == len(g["IA"]) and g["size_b"] == len(g["IB"])
+    return g, ref, inj
+
+
+def test_w3_bit_exact(ctx, golden):
+    gw = golden["W3"]
+    A = np.array(gw["A"], np.float32)
+    B = A + np.array(gw["B_offset"], np.float32)
+    for key, k in (("k1_m1", 1), ("k2_m1", 2)):
+        g = _run(ctx, A, B, k, 1)
+        assert g["IA"].tolist() == gw[key]["IA"] and g["IB"].tolist() == gw[key]["IB"]
+        assert g["value"] == gw[key]["H_hat"]
+        assert [g["ab"]["a"], g["ab"]["b"]] == gw[key]["ab_witness"]
+    g = _run(ctx, A, B, 2, 1)
+    assert np.allclose(g["U"][:, 0], gw["u0"], atol=0)
+    assert np.allclose(np.abs(g["U"][:, 1]), np.abs(np.array(gw["pc1"])), atol=1e-14)
+
+
+def test_w5_injected(ctx, golden):
+    gw = golden["W5"]
+    A = np.array(gw["A"], np.float32)
+    B = np.array(gw["B"], np.float32)
+    r = ctx.prohd_estimate_with_dirs(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(),
+                                     np.array(gw["U"]), gw["m"])
+    assert r["IA"].tolist() == gw["IA"] and r["IB"].tolist() == gw["IB"]
+    assert abs(r["value"] - gw["H_hat_ss"]) <= 1e-6
+
+
+def test_cfg1_layers(ctx, golden):
+    A, B = datagen.generate(1)
+    g, ref, inj = _check_layers(ctx, A, B, 4, 20)
+    gw = golden["CFG1_SEED0"]
+    assert (g["size_a"], g["size_b"]) == (gw["size_a"], gw["size_b"])
+    assert np.array_equal(g["IA"], ref["IA"]) and np.array_equal(g["IB"], ref["IB"])
+    assert abs(g["value"] - ref["value"]) <= 1e-4 * ref["value"]
+    assert [g["ab"]["a"], g["ab"]["b"]] == gw["hhat_ab_witness"]
+    assert [g["ba"]["a"], g["ba"]["b"]] == gw["hhat_ba_witness"]
+
+
+@pytest.mark.parametrize("cfg,n", [(2, 20000), (3, 65536), (4, 65536), (5, 65536)])
+def test_reduced_scale_layers(ctx, cfg, n):
+    c = datagen.CONFIGS[cfg]
+    A, B = datagen.generate(cfg, n=n)
+    m = c.m(n)
+    g, ref, inj = _check_layers(ctx, A, B, c.k, m)
+    if np.array_equal(g["IA"], ref["IA"]) and np.array_equal(g["IB"], ref["IB"]):
+        assert abs(g["value"] - ref["value"]) <= 1e-4 * ref["value"]
+
+
+def test_full_selection_equals_exact(ctx):
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((50, 8)).astype(np.float32)
+    B = (rng.standard_normal((40, 8)) + 0.5).astype(np.float32)
+    g = _run(ctx, A, B, 3, 25)  # 2m >= n for both sets
+    assert g["size_a"] == 50 and g["size_b"] == 40
+    h = ctx.hausdorff(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    assert g["value"] == h["value"]
+
+
+def test_identical_sets(ctx):
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((3000, 16)).astype(np.float32)
+    g = _run(ctx, A, A.copy(), 4, 10)
+    assert g["value"] == 0.0
+    assert g["U"][:, 0].tolist() == [1.0] + [0.0] * 15  # equal centroids -> e1
+
+
+def test_k0_centroid_only(ctx):
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((5000, 12)).astype(np.float32)
+    B = (rng.standard_normal((4000, 12)) + 1.0).astype(np.float32)
+    g = _run(ctx, A, B, 0, 30)
+    ref = OP.estimate(A, B, 0, 30)
+    assert g["n_dirs"] == 1
+    assert np.array_equal(g["IA"], ref["IA"]) and np.array_equal(g["IB"], ref["IB"])
+    assert abs(g["value"] - ref["value"]) <= 1e-4 * ref["value"]
+
+
+def test_ragged_and_ties(ctx):
+    """Duplicate points (exact projection ties) and n not a multiple of any tile."""
+    rng = np.random.default_rng(6)
+    A = rng.standard_normal((1001, 20)).astype(np.float32)
+    A[500:600] = A[0]
+    B = rng.standard_normal((777, 20)).astype(np.float32)
+    B[100:300] = B[5]
+    _check_layers(ctx, A, B, 3, 7)
+
+
+def test_host_inputs(ctx):
+    A, B = datagen.generate(2, n=20000)
+    c = datagen.CONFIGS[2]
+    gd = ctx.prohd_estimate(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), c.k, c.m(20000))
+    gh = ctx.prohd_estimate(torch.from_numpy(A), torch.from_numpy(B), c.k, c.m(20000))
+    assert gd == gh
+
+
+def test_determinism(ctx):
+    A, B = datagen.generate(5, n=65536)
+    r = [_run(ctx, A, B, 16, 32) for _ in range(2)]
+    assert r[0]["value"] == r[1]["value"] and np.array_equal(r[0]["U"], r[1]["U"])
+    assert np.array_equal(r[0]["IA"], r[1]["IA"]) and np.array_equal(r[0]["IB"], r[1]["IB"])
+
+
+def test_errors(ctx):
+    from paper_2511_18207_b200 import ProHDError
+    A = torch.randn(100, 4, device="cuda")
+    B = torch.randn(90, 4, device="cuda")
+    with pytest.raises(ProHDError) as e:
+        ctx.prohd_estimate(A, B, 5, 3)  # k > D
+    assert e.value.code == 2
+    with pytest.raises(ProHDError) as e:
+        ctx.prohd_estimate(A, B, 2, 0)  # m < 1
+    assert e.value.code == 2
+    An = A.clone()
+    An[7, 2] = float("nan")
+    with pytest.raises(ProHDError) as e:
+        ctx.prohd_estimate(An, B, 2, 3)
+    assert e.value.code == 3
