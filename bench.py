@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the ProHD hot path (arxiv 2511.18207) on B200 — one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+
+One STEP = one pass of the whole hot path over the config's synthetic pair
+(SURVEY.md §8(a) rows a1-a6):
+    prohd_estimate(A, B, k, m)   # Alg. 3: moments, eigen, projection, selection, subset HD
+    directed_hd(A, B)            # exact h(A,B) = max_a min_b ||a-b|| (Eq. 1)
+`value` = exact-HD point pairs processed per second over the timed steps
+(nA*nB per step / device time of the step, whole job), `prohd_ms` = the
+ProHD part of the step. Inputs are device-resident and larger than L2
+(2 GB per set at cfg5), so no L2 flush is needed between steps.
+
+N > 1 (torchrun, one rank per GPU): rows of A are sharded for the exact kernel
+(B replicated, one NCCL MAX all-reduce of the packed key);
+ProHD runs replicated on every rank in this round (not yet sharded).
+
+`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded row sample
+of the same workload (the reference arm for this paper-only tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+METRIC = "exact-HD Gpair/s and ProHD ms at n=2M,D=256 on 1/2/4/8 B200 (% of roofline)"
+NOMINAL_TF32_OVER_BF16 = 1.1 / 2.25  # B200_PROFILING.md nominal dense ratio
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+def peaks() -> dict:
+    p = {"source": "fallback (B200_PROFILING.md)", "hbm_gbs": 6650.0, "bf16_tflops": 1590.0,
+         "bf16_tflops_sustained": 1400.0}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            m = json.load(f)
+        p = {"source": "MEASURED_PEAKS.json", "hbm_gbs": m["hbm_gbs"], "bf16_tflops": m["bf16_tflops"],
+             "bf16_tflops_sustained": m.get("bf16_tflops_sustained", m["bf16_tflops"])}
+    return p
+
+
+def k6_traffic_per_pair(D: int):
+    """dram bytes per point pair of K6 from the committed ncu capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "k6_traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as f:
+        t = json.load(f)
+    e = t.get(str(D))
+    if not e:
+        return None, None
+    return e["dram_bytes"] / e["pairs"], e["source"]
+
+
+def cpu_baseline(A, B, budget_s: float = 15.0) -> dict:
+    """The fp64 oracle's exact-HD row minima on a bounded row sample, host cores."""
+    import oracle
+    rows_all = datagen.sample_rows(A.shape[0], 4096, seed=7)
+    t0 = time.perf_counter()
+    oracle.row_minima(A, B, rows=rows_all[:8])
+    dt = time.perf_counter() - t0
+    nrows = int(max(8, min(4096, budget_s / max(dt / 8, 1e-6))))
+    rows = rows_all[:nrows]
+    t0 = time.perf_counter()
+    oracle.row_minima(A, B, rows=rows)
+    dt = time.perf_counter() - t0
+    pairs = nrows * B.shape[0]
+    threads = os.environ.get("OMP_NUM_THREADS") or os.environ.get("OPENBLAS_NUM_THREADS") or str(os.cpu_count())
+    return {"value": pairs / dt / 1e9, "unit": "Gpair/s", "cores": int(threads), "kind": "oracle",
+            "sample": f"exact-HD row minima (fp64, oracle/hausdorff.py) of {nrows} seeded rows of A against "
+                      f"all {B.shape[0]} rows of B: {pairs:.3e} pairs in {dt:.1f} s",
+            "seconds": dt}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    c = datagen.CONFIGS[args.config]
+    A = datagen.generate_set(args.config, "A")
+    B = datagen.generate_set(args.config, "B")
+    import oracle
+    rows_all = datagen.sample_rows(A.shape[0], 4096, seed=11)
+    t0 = time.perf_counter()
+    oracle.row_minima(A, B, rows=rows_all[:4])
+    per_row = (time.perf_counter() - t0) / 4
+    nrows = int(max(4, min(1024, 6.0 / max(per_row, 1e-6))))  # ~6 s of CPU work per step
+    times = []
+    for s in range(args.warmup + args.steps):
+        rows = rows_all[(s * nrows) % 4096:][:nrows]
+        t0 = time.perf_counter()
+        oracle.row_minima(A, B, rows=rows)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    pairs = nrows * B.shape[0]
+    ms = 1e3 * sum(times) / len(times)
+    value = pairs / (ms / 1e3) / 1e9
+    threads = os.environ.get("OMP_NUM_THREADS") or os.environ.get("OPENBLAS_NUM_THREADS") or str(os.cpu_count())
+    sample = f"exact-HD row minima of {nrows} seeded rows of A vs all {B.shape[0]} rows of B per step (fp64 oracle)"
+    out = {"metric": METRIC, "value": value, "unit": "Gpair/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen cfg%d, seed 0)" % args.config,
+           "impl": "reference",
+           "config": {"workload": f"cfg{c.cfg} {c.name} n={c.n} D={c.D} k={c.k} m={c.m()}", "nA": c.n, "nB": c.n,
+                      "D": c.D, "sample_rows_per_step": nrows},
+           "cpu_baseline": {"value": value, "unit": "Gpair/s", "cores": int(threads), "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "Gpair/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank: int, world: int):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2511_18207_b200 import Context
+    from paper_2511_18207_b200.dist import cuda_fns, row_range, sharded_directed_hd
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c = datagen.CONFIGS[args.config]
+    n, D, k, m = c.n, c.D, c.k, c.m()
+    t0 = time.perf_counter()
+    Ah = datagen.generate_set(args.config, "A")
+    Bh = datagen.generate_set(args.config, "B")
+    log(f"[rank {rank}] generated cfg{args.config} in {time.perf_counter() - t0:.1f}s")
+    A = torch.from_numpy(Ah).to(dev)
+    B = torch.from_numpy(Bh).to(dev)
+    lo, hi = row_range(n, rank, world)
+    A_local = A[lo:hi].contiguous()
+    ctx = Context(local_rank)
+    ctx.enable_timing(True)
+    stream = torch.cuda.current_stream(dev)
+    local_fn, witness_fn = cuda_fns(ctx)
+
+    def exact_step():
+        if world == 1:
+            r = ctx.directed_hd(A, B)
+        else:
+            r = sharded_directed_hd(A_local, lo, B, local_fn, witness_fn, device=dev)
+        return r, ctx.last_timings() if world == 1 else ctx.last_timings()
+
+    def step():
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        est = ctx.prohd_estimate(A, B, k, m)
+        t_est = ctx.last_timings()
+        ev[1].record(stream)
+        if world == 1:
+            ex = ctx.directed_hd(A, B)
+            t_ex = ctx.last_timings()
+        else:
+            t_ex = None
+            ex = sharded_directed_hd(A_local, lo, B, local_fn, witness_fn, device=dev)
+            t_ex = dict(ctx._last_local) if hasattr(ctx, "_last_local") else ctx.last_timings()
+        ev[2].record(stream)
+        return est, ex, t_est, t_ex, ev
+
+    # local timings of the sharded exact step are those of directed_hd_local (last ABI call before the witness)
+    if world > 1:
+        orig_local = local_fn
+
+        def local_fn(A_l, off, Bm):  # noqa: F811
+            key = orig_local(A_l, off, Bm)
+            ctx._last_local = ctx.last_timings()
+            return key
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    g0 = torch.cuda.Event(enable_timing=True)
+    g1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    g0.record(stream)
+    recs = [step() for _ in range(args.steps)]
+    g1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    clk = clocks.stop()
+    total_ms = g0.elapsed_time(g1)
+    prohd_ms = [r[4][0].elapsed_time(r[4][1]) for r in recs]
+    exact_ms = [r[4][1].elapsed_time(r[4][2]) for r in recs]
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    pairs_step = float(n) * float(n)
+    value = pairs_step / (ms_step / 1e3) / 1e9
+    est, ex = recs[-1][0], recs[-1][1]
+    # dominant kernel: K6 of the exact step, per launch, timed with events on its stream (inside the library)
+    t_ex = recs[-1][3]
+    dist_ms = [r[3]["dist_ms"] / max(1, r[3]["dist_launches"]) for r in recs]
+    k6_ms = sum(dist_ms) / len(dist_ms)
+    pairs_launch = float(hi - lo) * float(n)
+    k6_tflops = 6.0 * D * pairs_launch / (k6_ms / 1e3) / 1e12
+    pk = peaks()
+    tf32_peak = pk["bf16_tflops_sustained"] * NOMINAL_TF32_OVER_BF16
+    tpp, tsrc = k6_traffic_per_pair(D)
+    launches = sum(r[2]["kernel_launches"] + (r[3]["kernel_launches"] if r[3] else 0) for r in recs)
+    if world > 1:
+        launches = None  # witness kernels on the owner rank only; reported per rank below
+    # ------------------------------------------------------------ end to end (host buffers through the ABI)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        Ap = torch.from_numpy(Ah).pin_memory()
+        Bp = torch.from_numpy(Bh).pin_memory()
+        ctx.prohd_estimate(Ap, Bp, k, m)  # reserve the staging workspace outside the timed region
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        d2h = 0
+        for _ in range(args.steps):
+            ee = ctx.prohd_estimate(Ap, Bp, k, m)
+            ctx.directed_hd(Ap, Bp)
+            d2h += 8 * (ee["size_a"] + ee["size_b"]) + 256
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / args.steps
+        e2e = {"value": pairs_step / (e_ms / 1e3) / 1e9, "unit": "Gpair/s",
+               "h2d_bytes_per_step": int(2 * (Ah.nbytes + Bh.nbytes)),
+               "d2h_bytes_per_step": int(d2h / args.steps), "ms_per_step": e_ms}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(Ah, Bh, budget_s=args.cpu_budget)
+    if rank != 0:
+        return
+    est_t = recs[-1][2]
+    out = {
+        "metric": METRIC, "value": value, "unit": "Gpair/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg{args.config}, seed 0)",
+        "config": {"workload": f"cfg{c.cfg} {c.name}: nA=nB={n}, D={D}, k={k}, m={m} (prohd_estimate + "
+                               f"directed_hd per step)",
+                   "nA": n, "nB": n, "D": D, "k": k, "m": m, "parallelism": f"rows-of-A x{world}",
+                   "l2": "inputs larger than L2 (2 x %.1f GB), no flush" % (Ah.nbytes / 1e9)},
+        "prohd_ms": statistics.mean(prohd_ms), "exact_ms": statistics.mean(exact_ms),
+        "prohd": {"value": est["value"], "size_a": est["size_a"], "size_b": est["size_b"],
+                  "n_dirs": est["n_dirs"], "phases_ms": {kk: est_t[kk] for kk in
+                                                         ("moments_ms", "eigen_ms", "select_ms", "subset_ms",
+                                                          "total_ms")}},
+        "exact": {"dist": ex["dist"], "a": ex["a"], "b": ex["b"], "Gpair_s_kernel": pairs_launch / k6_ms / 1e6},
+        "roofline": {"bound": "tensor", "kernel": "K6 dist_rowmin_kernel (tcgen05 kind::tf32, 3xTF32)",
+                     "achieved": k6_tflops, "peak": tf32_peak, "unit": "TFLOP/s", "frac": k6_tflops / tf32_peak,
+                     "traffic": (tpp * pairs_launch) if tpp else None,
+                     "note": ("achieved = 6*D executed tensor flops per pair (3 TF32 MMAs of 2*D) x pairs per "
+                              "launch / mean launch time from CUDA events on the launch stream; peak = "
+                              f"{pk['source']} bf16 sustained {pk['bf16_tflops_sustained']} x nominal tf32/bf16 "
+                              f"{NOMINAL_TF32_OVER_BF16:.4f}; traffic from {tsrc or 'n/a'}"),
+                     "launch_ms": k6_ms},
+        "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as tdist
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group(backend=backend)
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

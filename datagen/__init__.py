@@ -16,18 +16,19 @@ Rules
   even); the cast arrays are what both sides read.
 * cfg1 is literal: ``rng = default_rng(seed)``, A drawn then B (BASELINE.json cfg1,
   seed 0; SURVEY.md §8(c3) pins the sha256 of these bytes).
-* cfg2-cfg5: shared parameters come from ``default_rng([cfg, seed, 2])``; the
-  rows of A from ``default_rng([cfg, seed, 0])`` and of B from
-  ``default_rng([cfg, seed, 1])``, drawn in row chunks of ``CHUNK`` rows, each
-  chunk drawing its variables in the order listed per recipe. Chunking keeps the
-  host memory bounded and lets A and B be generated independently.
+* cfg2-cfg5: shared parameters come from ``default_rng([cfg, seed, 2])``; row
+  chunk c (``CHUNK`` rows) of A is drawn from ``default_rng([cfg, seed, 0, c])``
+  and of B from ``default_rng([cfg, seed, 1, c])``, each chunk drawing its
+  variables in the order listed per recipe. Independent chunk streams keep host
+  memory bounded and let chunks (and A and B) be generated in parallel.
 * ``rows=(lo, hi)`` generates only that row range of a set bit-identically to the
-  full draw (used for row-sharded multi-GPU runs and for oracle samples), as long
-  as ``lo`` is a multiple of ``CHUNK``.
+  full draw (used for row-sharded multi-GPU runs and for oracle samples).
 """
 from __future__ import annotations
 
 import hashlib
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -174,26 +175,28 @@ def generate_set(cfg: int, which: str, seed: int = 0, n: int | None = None,
         b = rng.standard_normal((n, D))
         b[:, 0] += 0.5
         return np.ascontiguousarray(b[lo:hi].astype(np.float32))
-    if lo % CHUNK != 0:
-        raise ValueError("row range must start on a CHUNK boundary")
     p = _params(cfg, seed, D)
     outliers = None
     if cfg == 2 and w == 1:
         orng = np.random.default_rng([cfg, seed, 3])
         outliers = np.sort(orng.choice(n, size=n // 1000, replace=False))
-    rng = np.random.default_rng([cfg, seed, w])
     out = np.empty((hi - lo, D), dtype=np.float32)
-    g = 0
-    while g < hi:
+
+    def work(c: int) -> None:
+        g = c * CHUNK
         r = min(CHUNK, n - g)
-        if g + r <= lo:
-            # skip: advance this chunk's stream deterministically by drawing it
-            _chunk(cfg, w, rng, r, D, p, g, outliers)
-        else:
-            x = _chunk(cfg, w, rng, r, D, p, g, outliers)
-            s0, s1 = max(lo, g), min(hi, g + r)
-            out[s0 - lo:s1 - lo] = x[s0 - g:s1 - g].astype(np.float32)
-        g += r
+        rng = np.random.default_rng([cfg, seed, w, c])
+        x = _chunk(cfg, w, rng, r, D, p, g, outliers)
+        s0, s1 = max(lo, g), min(hi, g + r)
+        out[s0 - lo:s1 - lo] = x[s0 - g:s1 - g].astype(np.float32)
+
+    chunks = list(range(lo // CHUNK, (hi + CHUNK - 1) // CHUNK)) if hi > lo else []
+    if len(chunks) <= 1:
+        for c in chunks:
+            work(c)
+    else:
+        with ThreadPoolExecutor(max_workers=min(len(chunks), os.cpu_count() or 1)) as ex:
+            list(ex.map(work, chunks))
     return out
 
 

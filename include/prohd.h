@@ -154,6 +154,27 @@ int directed_hd_local(prohd_ctx* ctx, const float* A_local, int64_t nA_local, in
 int directed_hd_witness(prohd_ctx* ctx, const float* a, const float* B, int64_t nB, int32_t D,
                         prohd_directed* out);
 
+/* ---------------------------------------------------------------- tracing */
+/* Per-phase device times of the LAST call on this context, measured with CUDA
+ * events recorded on the context stream around each phase (enable first;
+ * disabled by default; costs two event records per phase). A phase that did
+ * not run reads 0. */
+typedef struct {
+  double total_ms;          /* first to last enqueued operation of the call          */
+  double h2d_ms;            /* staging copies of host inputs                        */
+  double prep_ms;           /* K0 TF32 hi/lo split + norms (full sets)              */
+  double dist_ms;           /* K6 fused distance kernel, summed over its launches   */
+  double reduce_ms;         /* K7 row-max key + fp64 witness search                 */
+  double moments_ms;        /* K1 centroid sums + covariance                        */
+  double eigen_ms;          /* K2 top-k eigenvectors                                */
+  double select_ms;         /* K3 projection + K4 selection + K5 union (both sets)  */
+  double subset_ms;         /* step 4: gather + K0 + K6 + K7 on the subsets         */
+  int32_t dist_launches;    /* number of K6 launches in dist_ms                     */
+  int32_t kernel_launches;  /* all kernels this call launched                       */
+} prohd_timings;
+int prohd_enable_timing(prohd_ctx* ctx, int on);
+int prohd_last_timings(const prohd_ctx* ctx, prohd_timings* out);
+
 #ifdef __cplusplus
 }
 #endif

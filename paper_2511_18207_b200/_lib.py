@@ -25,6 +25,7 @@ EXPORTED = [
     "prohd_create", "prohd_destroy", "prohd_set_stream", "prohd_last_error", "prohd_version",
     "prohd_workspace_bytes", "prohd_set_workspace", "directed_hd", "hausdorff", "directed_hd_rowmin",
     "prohd_estimate", "prohd_estimate_with_dirs", "directed_hd_local", "directed_hd_witness",
+    "prohd_enable_timing", "prohd_last_timings",
 ]
 
 
@@ -40,6 +41,13 @@ class HD(C.Structure):
 class Est(C.Structure):
     _fields_ = [("value", C.c_double), ("ab", Directed), ("ba", Directed), ("size_a", C.c_int64),
                 ("size_b", C.c_int64), ("n_dirs", C.c_int32), ("_pad", C.c_int32)]
+
+
+class Timings(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("h2d_ms", C.c_double), ("prep_ms", C.c_double),
+                ("dist_ms", C.c_double), ("reduce_ms", C.c_double), ("moments_ms", C.c_double),
+                ("eigen_ms", C.c_double), ("select_ms", C.c_double), ("subset_ms", C.c_double),
+                ("dist_launches", C.c_int32), ("kernel_launches", C.c_int32)]
 
 
 _lib = None
@@ -71,6 +79,8 @@ def load() -> C.CDLL:
     lib.prohd_estimate_with_dirs.argtypes = [vp, vp, i64, vp, i64, i32, i32, i64, vp, C.POINTER(Est), vp, vp]
     lib.directed_hd_local.argtypes = [vp, vp, i64, i64, vp, i64, i32, C.POINTER(C.c_uint64)]
     lib.directed_hd_witness.argtypes = [vp, vp, vp, i64, i32, C.POINTER(Directed)]
+    lib.prohd_enable_timing.argtypes = [vp, f]
+    lib.prohd_last_timings.argtypes = [vp, C.POINTER(Timings)]
     for name in EXPORTED:
         fn = getattr(lib, name)
         if name not in ("prohd_last_error", "prohd_version", "prohd_workspace_bytes"):

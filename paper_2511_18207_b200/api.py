@@ -86,6 +86,16 @@ class Context:
         self._check(self.lib.prohd_set_stream(self.h, C.c_void_p(stream)))
         return A, B
 
+    def enable_timing(self, on: bool = True):
+        """Record per-phase CUDA events inside every following call (prohd_enable_timing)."""
+        self._check(self.lib.prohd_enable_timing(self.h, 1 if on else 0))
+
+    def last_timings(self) -> dict:
+        """Per-phase device milliseconds and kernel-launch counts of the last call."""
+        t = L.Timings()
+        self._check(self.lib.prohd_last_timings(self.h, C.byref(t)))
+        return {name: getattr(t, name) for name, _ in L.Timings._fields_}
+
     # ---------------------------------------------------------------- ABI calls
     def directed_hd(self, A, B) -> dict:
         A, B = self._prepare(A, B)

@@ -13,6 +13,11 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
+
+namespace prohd {
+enum Phase { PH_TOTAL, PH_H2D, PH_PREP, PH_DIST, PH_REDUCE, PH_MOMENTS, PH_EIGEN, PH_SELECT, PH_SUBSET, PH_COUNT };
+}
 
 struct prohd_ctx {
   int device = 0;
@@ -21,6 +26,17 @@ struct prohd_ctx {
   size_t ws_bytes = 0;
   int num_sms = 148;
   std::string err;
+  // tracing (prohd_enable_timing): CUDA events recorded on `stream` around phases
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  int nev = 0;
+  struct Mark {
+    int phase, e0, e1;
+  };
+  std::vector<Mark> marks;
+  int t_total = -1;
+  long long launches0 = 0;
+  prohd_timings last{};
 };
 
 namespace prohd {
@@ -130,6 +146,51 @@ inline size_t carve_exact(Carver& c, ExactWs& w, int64_t nA, int64_t nB, int D, 
 
 using namespace prohd;
 
+// ------------------------------------------------------------------ tracing
+inline int tmark(prohd_ctx* ctx) {
+  if (!ctx->timing) return -1;
+  if (ctx->nev >= static_cast<int>(ctx->ev.size())) return -1;
+  cudaEventRecord(ctx->ev[ctx->nev], ctx->stream);
+  return ctx->nev++;
+}
+inline void tspan(prohd_ctx* ctx, int phase, int e0) {
+  if (e0 < 0) return;
+  const int e1 = tmark(ctx);
+  if (e1 >= 0) ctx->marks.push_back({phase, e0, e1});
+}
+// call at the start of an ABI call (after enter)
+inline void call_begin(prohd_ctx* ctx) {
+  ctx->nev = 0;
+  ctx->marks.clear();
+  ctx->last = prohd_timings{};
+  ctx->launches0 = launch_counter().load();
+  ctx->t_total = tmark(ctx);
+}
+// call right before the final stream synchronisation
+inline void call_end(prohd_ctx* ctx) { tspan(ctx, PH_TOTAL, ctx->t_total); }
+// call after the final synchronisation
+inline void call_collect(prohd_ctx* ctx) {
+  prohd_timings& t = ctx->last;
+  t.kernel_launches = static_cast<int32_t>(launch_counter().load() - ctx->launches0);
+  if (!ctx->timing) return;
+  double acc[PH_COUNT] = {0};
+  for (const auto& mk : ctx->marks) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, ctx->ev[mk.e0], ctx->ev[mk.e1]) == cudaSuccess) acc[mk.phase] += ms;
+    if (mk.phase == PH_DIST) t.dist_launches++;
+  }
+  t.total_ms = acc[PH_TOTAL];
+  t.h2d_ms = acc[PH_H2D];
+  t.prep_ms = acc[PH_PREP];
+  t.dist_ms = acc[PH_DIST];
+  t.reduce_ms = acc[PH_REDUCE];
+  t.moments_ms = acc[PH_MOMENTS];
+  t.eigen_ms = acc[PH_EIGEN];
+  t.select_ms = acc[PH_SELECT];
+  t.subset_ms = acc[PH_SUBSET];
+}
+
+
 // ------------------------------------------------------------------ helpers
 inline int fail(prohd_ctx* ctx, int code, const char* fmt, ...) {
   char buf[512];
@@ -178,6 +239,7 @@ inline int stage_inputs(prohd_ctx* ctx, const float*& A, int64_t nA, const float
                         float* stA, float* stB, bool& host_inputs) {
   const bool dA = is_device_ptr(A), dB = is_device_ptr(B);
   host_inputs = !(dA && dB);
+  const int t0 = tmark(ctx);
   if (!dA) {
     if (stA == nullptr) return fail(ctx, PROHD_E_WORKSPACE, "host inputs need a PROHD_WS_HOST_INPUTS workspace");
     CK(cudaMemcpyAsync(stA, A, sizeof(float) * nA * D, cudaMemcpyHostToDevice, ctx->stream));
@@ -188,12 +250,15 @@ inline int stage_inputs(prohd_ctx* ctx, const float*& A, int64_t nA, const float
     CK(cudaMemcpyAsync(stB, B, sizeof(float) * nB * D, cudaMemcpyHostToDevice, ctx->stream));
     B = stB;
   }
+  if (host_inputs) tspan(ctx, PH_H2D, t0);
   return PROHD_OK;
 }
 
 inline int prep_set(prohd_ctx* ctx, const float* X, int64_t n, int D, SetOps& s, int* bad) {
   s.x = X;
+  const int t0 = tmark(ctx);
   CK(launch_prep(X, n, D, pad_dim(D), round_up(n, kBN), s.hi, s.lo, s.norms, bad, ctx->stream));
+  tspan(ctx, PH_PREP, t0);
   return PROHD_OK;
 }
 
@@ -216,7 +281,9 @@ inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, flo
   a.nb = C.norms;
   a.rowmin = rowmin;
   a.num_sms = ctx->num_sms;
+  const int t0 = tmark(ctx);
   CK(launch_dist_rowmin(a, ctx->stream));
+  tspan(ctx, PH_DIST, t0);
   return PROHD_OK;
 }
 
@@ -224,9 +291,11 @@ inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, flo
 inline int directed_on_ops(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, ExactWs& w, int slot) {
   int rc = run_dist(ctx, R, C, D, w.rowmin);
   if (rc) return rc;
+  const int t0 = tmark(ctx);
   CK(launch_rowmax_key(w.rowmin, R.n, 0, &w.keys[slot], ctx->stream));
   CK(launch_nn64_from_key(R.x, 0, R.n, &w.keys[slot], C.x, C.n, D, w.blk_d, w.blk_j, kNNBlocks, &w.nn_d[slot],
                           &w.nn_j[slot], ctx->stream));
+  tspan(ctx, PH_REDUCE, t0);
   return PROHD_OK;
 }
 

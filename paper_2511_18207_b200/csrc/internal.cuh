@@ -2,9 +2,17 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 namespace prohd {
+
+// Process-wide count of kernel launches issued by this library (for tracing).
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> c{0};
+  return c;
+}
+inline void count_launch(int n = 1) { launch_counter().fetch_add(n, std::memory_order_relaxed); }
 
 constexpr int kBM = 128;  // rows of the row operand per CTA tile (UMMA M)
 constexpr int kBN = 256;  // columns (points of the column operand) per tile (UMMA N)

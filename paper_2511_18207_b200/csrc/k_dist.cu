@@ -245,6 +245,7 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   }
   const int units = s.nrb * s.nsplit;
   const int grid = units < a.num_sms ? units : a.num_sms;
+  count_launch();
   dist_rowmin_kernel<<<grid, kThreads, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na,
                                                            a.nb, a.rowmin);
   return cudaGetLastError();

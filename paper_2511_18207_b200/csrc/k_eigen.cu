@@ -342,6 +342,7 @@ cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, dou
   cudaError_t e = cudaFuncSetAttribute(eigen_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
+  count_launch();
   eigen_topk_kernel<<<1, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -254,17 +254,22 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
 
 cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB, int D,
                            const MomentsBufs& b, cudaStream_t st) {
+  count_launch();
   shift_kernel<<<(D + 255) / 256, 256, 0, st>>>(A, nA, B, nB, D, b.s);
   const size_t smem = sizeof(double) * kChunk * 128;
   cudaError_t e = cudaFuncSetAttribute(moments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   MomArgs a{A, nA, D, b.s, p.nb, 0, p.rangesA, p.nslots, b.Gpart, b.Spart};
+  count_launch();
   moments_kernel<<<dim3(p.npairs, p.rangesA), kThreads, smem, st>>>(a);
   MomArgs bb{B, nB, D, b.s, p.nb, p.rangesA, p.rangesB, p.nslots, b.Gpart, b.Spart};
+  count_launch();
   moments_kernel<<<dim3(p.npairs, p.rangesB), kThreads, smem, st>>>(bb);
+  count_launch();
   moments_reduce_kernel<<<148 * 2, 256, 0, st>>>(b.Gpart, b.Spart, p.nb, D, p.rangesA, p.nslots, b.C, b.SA,
                                                  b.SB);
+  count_launch();
   moments_finalize_kernel<<<1, 256, 0, st>>>(b.C, b.SA, b.SB, b.s, nA, nB, D, b.mu, b.u0, b.dnorm);
   return cudaGetLastError();
 }

@@ -65,12 +65,14 @@ static int grid_for_rows(int64_t rows) {
 
 cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, float* hi, float* lo,
                         float* norms, int* bad, cudaStream_t st) {
+  count_launch();
   prep_kernel<false><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, hi, lo, norms, bad);
   return cudaGetLastError();
 }
 
 cudaError_t launch_prep_gather(const float* X, const int64_t* idx, int64_t n, int D, int Dp, int64_t n_pad,
                                float* hi, float* lo, float* norms, int* bad, cudaStream_t st) {
+  count_launch();
   prep_kernel<true><<<grid_for_rows(n_pad), 256, 0, st>>>(X, idx, n, D, Dp, n_pad, hi, lo, norms, bad);
   return cudaGetLastError();
 }
@@ -113,6 +115,7 @@ cudaError_t launch_rowmax_key(const float* rowmin, int64_t n, int64_t row_offset
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 4) blocks = 148 * 4;
   if (blocks < 1) blocks = 1;
+  count_launch();
   rowmax_key_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(rowmin, n, row_offset, key);
   return cudaGetLastError();
 }
@@ -199,7 +202,9 @@ __global__ void __launch_bounds__(256) nn64_final_kernel(const double* blk_d, co
 
 cudaError_t launch_nn64(const float* a, const float* B, int64_t nB, int D, double* blk_d, long long* blk_j,
                         int nblocks, double* out_d, long long* out_j, cudaStream_t st) {
+  count_launch();
   nn64_kernel<<<nblocks, 256, 0, st>>>(nullptr, 0, 0, nullptr, a, B, nB, D, blk_d, blk_j);
+  count_launch();
   nn64_final_kernel<<<1, 256, 0, st>>>(blk_d, blk_j, nblocks, out_d, out_j);
   return cudaGetLastError();
 }
@@ -207,7 +212,9 @@ cudaError_t launch_nn64(const float* a, const float* B, int64_t nB, int D, doubl
 cudaError_t launch_nn64_from_key(const float* X, int64_t x_offset, int64_t nX, const unsigned long long* key,
                                  const float* B, int64_t nB, int D, double* blk_d, long long* blk_j, int nblocks,
                                  double* out_d, long long* out_j, cudaStream_t st) {
+  count_launch();
   nn64_kernel<<<nblocks, 256, 0, st>>>(X, x_offset, nX, key, nullptr, B, nB, D, blk_d, blk_j);
+  count_launch();
   nn64_final_kernel<<<1, 256, 0, st>>>(blk_d, blk_j, nblocks, out_d, out_j);
   return cudaGetLastError();
 }

@@ -305,6 +305,7 @@ __global__ void init_state_kernel(unsigned* state, int L, int64_t m) {
 }  // namespace
 
 cudaError_t launch_dirs_to_f32(const double* U64, float* U32, int rows, int D, cudaStream_t st) {
+  count_launch();
   dirs_to_f32_kernel<<<(rows * D + 255) / 256, 256, 0, st>>>(U64, U32, rows * D);
   return cudaGetLastError();
 }
@@ -317,6 +318,7 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   if ((e = cudaMemsetAsync(b.ccount, 0, sizeof(unsigned) * 2 * L, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(b.bitmap, 0, sizeof(unsigned) * ((n + 31) / 32), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(b.overflow, 0, sizeof(int), st)) != cudaSuccess) return e;
+  count_launch();
   init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, m);
   // K3
   const size_t psmem = sizeof(float) * L * D;
@@ -325,19 +327,26 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
     return e;
   int64_t pblocks = (n + 7) / 8;
   if (pblocks > 148 * 8) pblocks = 148 * 8;
+  count_launch();
   project_kernel<<<static_cast<int>(pblocks), 256, psmem, st>>>(X, n, D, U32, L, b.P32, b.maxnorm2);
   // K4: three radix rounds
   int64_t hb = (n + 255) / 256;
   if (hb > 148 * 2) hb = 148 * 2;
   for (int r = 0; r < 3; ++r) {
+    count_launch();
     radix_hist_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, L, n_dirs, r, b.state, b.hist);
+    count_launch();
     radix_scan_kernel<<<(2 * L + 63) / 64, 64, 0, st>>>(b.hist, L, n_dirs, r, b.state);
   }
+  count_launch();
   collect_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, D, L, n_dirs, b.state, b.maxnorm2,
                                                                      b.cand, b.ccount, b.cap, b.overflow);
+  count_launch();
   cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
+  count_launch();
   rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap);
   // K5
+  count_launch();
   compact_kernel<<<1, 1024, 0, st>>>(b.bitmap, (n + 31) / 32, b.uidx, b.ucount);
   return cudaGetLastError();
 }
@@ -345,6 +354,7 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
 cudaError_t launch_iota(long long* idx, unsigned* count, int64_t n, cudaStream_t st) {
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
+  count_launch();
   iota_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(idx, count, n);
   return cudaGetLastError();
 }
@@ -354,6 +364,7 @@ cudaError_t launch_gather(const float* X, int D, const long long* idx, const uns
   int64_t blocks = (cap + 7) / 8;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
+  count_launch();
   gather_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(X, D, idx, count, Y);
   return cudaGetLastError();
 }

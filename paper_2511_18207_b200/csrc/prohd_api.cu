@@ -37,7 +37,30 @@ int prohd_create(int device, void* cuda_stream, prohd_ctx** out) {
 }
 
 int prohd_destroy(prohd_ctx* ctx) {
+  if (ctx == nullptr) return PROHD_OK;
+  for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   delete ctx;
+  return PROHD_OK;
+}
+
+int prohd_enable_timing(prohd_ctx* ctx, int on) {
+  if (ctx == nullptr) return PROHD_E_INVALID;
+  if (on && ctx->ev.empty()) {
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return fail(ctx, PROHD_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    ctx->ev.resize(128);
+    for (auto& ev : ctx->ev) {
+      e = cudaEventCreate(&ev);
+      if (e != cudaSuccess) return fail(ctx, PROHD_E_CUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
+    }
+  }
+  ctx->timing = on != 0;
+  return PROHD_OK;
+}
+
+int prohd_last_timings(const prohd_ctx* ctx, prohd_timings* out) {
+  if (ctx == nullptr || out == nullptr) return PROHD_E_INVALID;
+  *out = ctx->last;
   return PROHD_OK;
 }
 
@@ -73,6 +96,7 @@ static int exact_common(prohd_ctx* ctx, const float* A, int64_t nA, const float*
   int rc = enter(ctx);
   if (rc) return rc;
   if ((rc = check_sets(ctx, A, nA, B, nB, D))) return rc;
+  call_begin(ctx);
   const bool host_in = !(is_device_ptr(A) && is_device_ptr(B));
   Carver dry{nullptr, 0, 0, true};
   ExactWs tmp;
@@ -101,7 +125,9 @@ static int fetch(prohd_ctx* ctx, const ExactWs& w, ExactHost& h) {
   CK(cudaMemcpyAsync(h.nn_d, w.nn_d, sizeof h.nn_d, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(h.nn_j, w.nn_j, sizeof h.nn_j, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(&h.bad, w.bad, sizeof h.bad, cudaMemcpyDeviceToHost, ctx->stream));
+  call_end(ctx);
   CK(cudaStreamSynchronize(ctx->stream));
+  call_collect(ctx);
   if (h.bad) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate (or squared norm overflow)");
   return PROHD_OK;
 }
@@ -144,7 +170,9 @@ int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* 
   if ((rc = run_dist(ctx, w.A, w.B, D, rowmin_dev))) return rc;
   ExactHost h{};
   CK(cudaMemcpyAsync(&h.bad, w.bad, sizeof h.bad, cudaMemcpyDeviceToHost, ctx->stream));
+  call_end(ctx);
   CK(cudaStreamSynchronize(ctx->stream));
+  call_collect(ctx);
   if (h.bad) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate");
   return PROHD_OK;
 }
@@ -162,7 +190,9 @@ int directed_hd_local(prohd_ctx* ctx, const float* A_local, int64_t nA_local, in
   ExactHost h{};
   CK(cudaMemcpyAsync(h.keys, w.keys, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(&h.bad, w.bad, sizeof h.bad, cudaMemcpyDeviceToHost, ctx->stream));
+  call_end(ctx);
   CK(cudaStreamSynchronize(ctx->stream));
+  call_collect(ctx);
   if (h.bad) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate");
   *key_out = h.keys[0];
   return PROHD_OK;

@@ -116,6 +116,7 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
     return fail(ctx, PROHD_E_NOTIMPL, "the device eigen-solver supports D <= 256 (D=%d)", D);
   if (m > 0x7FFFFFFFLL) return fail(ctx, PROHD_E_INVALID, "m too large");
   const int L = k + 1;
+  call_begin(ctx);
   const bool host_in = !(is_device_ptr(A) && is_device_ptr(B));
   Carver dry{nullptr, 0, 0, true};
   EstWs tmp;
@@ -134,9 +135,13 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   // ------------------------------------------------------------ step 1: directions
   if (dirs_in == nullptr) {
     const MomentsPlan mp = plan_moments(nA, nB, D, ctx->num_sms);
+    int t0 = tmark(ctx);
     CK(launch_moments(mp, A, nA, B, nB, D, w.mom, st));
+    tspan(ctx, PH_MOMENTS, t0);
     if (k > 0) {
+      t0 = tmark(ctx);
       CK(launch_eigen_topk(w.mom.C, D, k, w.V, w.Xe, w.U64, w.U32, w.lam, w.n_dirs, st));
+      tspan(ctx, PH_EIGEN, t0);
     } else {
       const int one = 1;
       CK(cudaMemcpyAsync(w.n_dirs, &one, sizeof(int), cudaMemcpyHostToDevice, st));
@@ -151,6 +156,7 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   // ------------------------------------------------------------ steps 2-3: projection, selection, union
   const float* X[2] = {A, B};
   const int64_t n[2] = {nA, nB};
+  const int t_sel = tmark(ctx);
   for (int s = 0; s < 2; ++s) {
     // projections run for every point (also when 2m >= n) so non-finite input is always detected
     SelectBufs& b = w.sel[s];
@@ -161,6 +167,7 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
       CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m, b, st));
     }
   }
+  tspan(ctx, PH_SELECT, t_sel);
   unsigned ucount[2];
   int ndirs = 0, ovf[2] = {0, 0};
   unsigned maxn[2];
@@ -183,6 +190,7 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
     return fail(ctx, PROHD_E_INTERNAL, "bad union sizes %u %u", ucount[0], ucount[1]);
 
   // ------------------------------------------------------------ step 4: exact HD on the subsets
+  const int t_sub = tmark(ctx);
   for (int s = 0; s < 2; ++s) {
     CK(launch_gather(X[s], D, w.sel[s].uidx, w.sel[s].ucount, ucount[s], w.Xs[s], st));
     w.ops[s].n = ucount[s];
@@ -197,6 +205,7 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   ew.blk_j = w.blk_j;
   if ((rc = directed_on_ops(ctx, w.ops[0], w.ops[1], D, ew, 0))) return rc;
   if ((rc = directed_on_ops(ctx, w.ops[1], w.ops[0], D, ew, 1))) return rc;
+  tspan(ctx, PH_SUBSET, t_sub);
   unsigned long long keys[2];
   double nn_d[2];
   long long nn_j[2];
@@ -208,7 +217,9 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   CK(cudaMemcpyAsync(ub.data(), w.sel[1].uidx, sizeof(long long) * ucount[1], cudaMemcpyDeviceToHost, st));
   if (dirs_out != nullptr)
     CK(cudaMemcpyAsync(dirs_out, w.U64, sizeof(double) * L * D, cudaMemcpyDeviceToHost, st));
+  call_end(ctx);
   CK(cudaStreamSynchronize(st));
+  call_collect(ctx);
 
   fill_directed(&out->ab, keys[0], nn_d[0], nn_j[0]);
   fill_directed(&out->ba, keys[1], nn_d[1], nn_j[1]);
