@@ -269,8 +269,8 @@ inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, flo
   const int Dp = pad_dim(D);
   if (!make_tmap_2d(&maps[0], R.hi, R.n, Dp, kBM, err, sizeof err) ||
       !make_tmap_2d(&maps[1], R.lo, R.n, Dp, kBM, err, sizeof err) ||
-      !make_tmap_2d(&maps[2], C.hi, C.n, Dp, kBN, err, sizeof err) ||
-      !make_tmap_2d(&maps[3], C.lo, C.n, Dp, kBN, err, sizeof err))
+      !make_tmap_2d(&maps[2], C.hi, C.n, Dp, dist_b_box_rows(D), err, sizeof err) ||
+      !make_tmap_2d(&maps[3], C.lo, C.n, Dp, dist_b_box_rows(D), err, sizeof err))
     return fail(ctx, PROHD_E_CUDA, "%s", err);
   DistArgs a;
   a.maps = maps;

@@ -30,6 +30,7 @@
 #include "sm100.cuh"
 
 #include <cstdio>
+#include <cstdlib>
 
 namespace prohd {
 namespace {
@@ -216,18 +217,229 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================================
+// 2-SM variant (cta_group::2): a CTA pair computes a 256-row block of A against
+// 256-column tiles of B with one M=256, N=256 MMA per K-step. Each CTA stages its
+// own 128 rows of A and its 128-column half of the B tile (64 KB per stage with
+// hi+lo, 3 stages), so per SM the operand traffic per pair drops from 24 B to
+// 16 B and the tensor core reads half as much of each SM's shared memory.
+// Barriers: full[] lives in the leader (rank 0) and counts both CTAs' TMA bytes
+// (2-SM TMA); empty[] and tfull[] exist in both CTAs and are signalled by the
+// leader's multicast tcgen05.commit; tempty[] lives in the leader and counts the
+// 8 epilogue warps of the pair.
+// ============================================================================
+constexpr int kStages2 = 3;
+constexpr uint32_t kHalf = 128 * kBK * 4;     // 16 KB: 128 rows x 32 fp32
+constexpr uint32_t kStage2Bytes = 4 * kHalf;  // A_hi, A_lo, B_hi, B_lo halves
+constexpr size_t kSmem2 = static_cast<size_t>(kStages2) * kStage2Bytes + 1024 + 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    dist_rowmin_2sm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
+                           const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
+                           const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin) {
+  using namespace sm100;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStage2Bytes);
+  uint64_t* empty = full + kStages2;
+  uint64_t* tfull = empty + kStages2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = static_cast<int>(cluster_id_x());
+  const int ncl = static_cast<int>(nclusters_x());
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages2; ++i) {
+      mbar_init(&full[i], 2);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tAh);
+    tma_prefetch(&tAl);
+    tma_prefetch(&tBh);
+    tma_prefetch(&tBl);
+  }
+  if (warp == 1) tmem_alloc_2sm<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int units = s.nrb * s.nsplit;  // nrb counts 256-row blocks here
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int pb = u / s.nsplit, sp = u % s.nsplit;
+        const int t0 = sp * s.tps;
+        const int t1 = min(s.nt, t0 + s.tps);
+        const int arow = pb * 256 + static_cast<int>(rank) * 128;
+        for (int t = t0; t < t1; ++t) {
+          const int brow = t * kBN + static_cast<int>(rank) * 128;
+          for (int c = 0; c < s.nk; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            const uint32_t fl = mapa(smem_u32(&full[stage]), 0);
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], 2 * kStage2Bytes);
+            else
+              mbar_arrive_cluster(fl);
+            uint8_t* st = smem + stage * kStage2Bytes;
+            tma_load_2d_2sm(st, &tAh, c * kBK, arow, fl);
+            tma_load_2d_2sm(st + kHalf, &tAl, c * kBK, arow, fl);
+            tma_load_2d_2sm(st + 2 * kHalf, &tBh, c * kBK, brow, fl);
+            tma_load_2d_2sm(st + 3 * kHalf, &tBl, c * kBK, brow, fl);
+            if (++stage == kStages2) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_tf32(256, kBN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int sp = u % s.nsplit;
+        const int t0 = sp * s.tps;
+        const int t1 = min(s.nt, t0 + s.tps);
+        for (int t = t0; t < t1; ++t) {
+          mbar_wait(&tempty[acc], aphase ^ 1u);
+          tc_fence_after();
+          const uint32_t d = tmem_base + static_cast<uint32_t>(acc * kBN);
+          for (int c = 0; c < s.nk; ++c) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t ah = smem_u32(smem + stage * kStage2Bytes);
+            const uint32_t al = ah + kHalf;
+            const uint32_t bh = ah + 2 * kHalf;
+            const uint32_t bl = ah + 3 * kHalf;
+            const int ks = (c == s.nk - 1) ? s.ks_last : (kBK / 8);
+            for (int kk = 0; kk < ks; ++kk) {
+              const uint32_t off = static_cast<uint32_t>(kk * 32);
+              const uint64_t dah = smem_desc_k_sw128(ah + off);
+              const uint64_t dal = smem_desc_k_sw128(al + off);
+              const uint64_t dbh = smem_desc_k_sw128(bh + off);
+              const uint64_t dbl = smem_desc_k_sw128(bl + off);
+              mma_tf32_2sm(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);
+              mma_tf32_2sm(d, dah, dbl, idesc, 1u);
+              mma_tf32_2sm(d, dal, dbh, idesc, 1u);
+            }
+            mma_commit_2sm_mc(&empty[stage], 0x3);
+            if (++stage == kStages2) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          mma_commit_2sm_mc(&tfull[acc], 0x3);
+          acc ^= 1;
+          if (acc == 0) aphase ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const int row_local = q * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t te[2] = {mapa(smem_u32(&tempty[0]), 0), mapa(smem_u32(&tempty[1]), 0)};
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int u = cid; u < units; u += ncl) {
+      const int pb = u / s.nsplit, sp = u % s.nsplit;
+      const int t0 = sp * s.tps;
+      const int t1 = min(s.nt, t0 + s.tps);
+      float rmin = __int_as_float(0x7f800000);
+      for (int t = t0; t < t1; ++t) {
+        mbar_wait(&tfull[acc], aphase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(acc * kBN);
+        const float4* nbp = reinterpret_cast<const float4*>(nb + static_cast<int64_t>(t) * kBN);
+#pragma unroll 1
+        for (int cc = 0; cc < kBN / 32; ++cc) {
+          float v[32];
+          tmem_ld32(taddr + cc * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 n4 = __ldg(nbp + cc * 8 + i);
+            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 0], n4.x));
+            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 1], n4.y));
+            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 2], n4.z));
+            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 3], n4.w));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(te[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1u;
+      }
+      const int64_t row = static_cast<int64_t>(pb) * 256 + static_cast<int64_t>(rank) * 128 + row_local;
+      if (row < s.nA) {
+        const float d2 = fmaxf(rmin + __ldg(na + row), 0.0f);
+        if (s.atomic_out)
+          atomicMin(reinterpret_cast<int*>(rowmin + row), __float_as_int(d2));
+        else
+          rowmin[row] = d2;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm<kTmemCols>(tmem_base);
+  }
+}
+
 }  // namespace
 
+// Variant by D (measured r01, tools/time_exact.py): the 2-SM pair wins where the kernel is
+// operand-bandwidth bound (D=256: 507 vs 464 Gpair/s); at D <= 128 the row-min epilogue
+// dominates and coupling two CTAs' epilogues costs more than the operand saving
+// (D=128: 882 vs 926, D=64: 1010 vs 1125). PROHD_K6_VARIANT=1sm|2sm overrides (A/B testing).
+static int dist_variant(int D) {
+  const char* e = getenv("PROHD_K6_VARIANT");
+  if (e != nullptr && e[0] == '1') return 1;
+  if (e != nullptr && e[0] == '2') return 2;
+  return D >= 192 ? 2 : 1;
+}
+
+int dist_b_box_rows(int D) { return dist_variant(D) == 2 ? 128 : kBN; }
+
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
+  const bool pair = dist_variant(a.D) == 2 && a.num_sms >= 2;
+  const int rows_per_unit = pair ? 256 : kBM;
+  const int ctas_per_unit = pair ? 2 : 1;
   Sched s{};
   s.nA = a.nA;
   s.nB = a.nB;
-  s.nrb = static_cast<int>((a.nA + kBM - 1) / kBM);
+  s.nrb = static_cast<int>((a.nA + rows_per_unit - 1) / rows_per_unit);
   s.nt = static_cast<int>((a.nB + kBN - 1) / kBN);
   s.nk = (a.D + kBK - 1) / kBK;
   s.ks_last = ((a.D - (s.nk - 1) * kBK) + 7) / 8;
+  const int slots = a.num_sms / ctas_per_unit;  // concurrent units
   // enough units to fill the machine twice when A is small (subset HD)
-  int want = 2 * a.num_sms;
+  const int want = 2 * slots;
   int nsplit = (want + s.nrb - 1) / s.nrb;
   if (nsplit < 1) nsplit = 1;
   if (nsplit > s.nt) nsplit = s.nt;
@@ -238,16 +450,25 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(a.rowmin, 0x7F, sizeof(float) * a.nA, st);  // 3.39e38 (finite, > any d2)
     if (e != cudaSuccess) return e;
   }
+  const int units = s.nrb * s.nsplit;
+  const int nunits = units < slots ? units : slots;
+  if (pair) {
+    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmem2));
+    if (e != cudaSuccess) return e;
+    count_launch();
+    dist_rowmin_2sm_kernel<<<2 * nunits, kThreads, kSmem2, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
+                                                                   a.na, a.nb, a.rowmin);
+    return cudaGetLastError();
+  }
   {
     cudaError_t e = cudaFuncSetAttribute(dist_rowmin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kSmemBytes));
     if (e != cudaSuccess) return e;
   }
-  const int units = s.nrb * s.nsplit;
-  const int grid = units < a.num_sms ? units : a.num_sms;
   count_launch();
-  dist_rowmin_kernel<<<grid, kThreads, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na,
-                                                           a.nb, a.rowmin);
+  dist_rowmin_kernel<<<nunits, kThreads, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na,
+                                                            a.nb, a.rowmin);
   return cudaGetLastError();
 }
 
