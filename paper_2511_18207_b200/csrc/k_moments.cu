@@ -66,14 +66,25 @@ __device__ __forceinline__ void pair_of(int p, int nb, int& bi, int& bj) {
   bj = r + p;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) moments_kernel(MomArgs a) {
-  extern __shared__ double cs[];  // [kChunk][128]: features of block bi (0..63) then bj (64..127)
+// fp64 tensor-core MMA (legacy warp-level DMMA): D[8x8] += A[8x4] * B[4x8], fp64 in and out.
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+constexpr int kLds = 136;  // fp64 row stride of the chunk tile (128 features + 8 pad: 2-way banks)
+
+// One CTA: one 64x64 block (bi, bj) of G over one point range. 8 warps; warp w owns
+// rows [16*(w/2), +16) x cols [32*(w%2), +32) = 2 x 4 DMMA tiles. The next 64-point
+// chunk is prefetched into registers while the current one is multiplied.
+__global__ void __launch_bounds__(kThreads, 2) moments_kernel(MomArgs a) {
+  extern __shared__ double cs[];  // [kChunk][kLds]: features of block bi (0..63) then bj (64..127)
   const int pair = blockIdx.x;
   const int range = blockIdx.y;
   int bi, bj;
   pair_of(pair, a.nb, bi, bj);
-  const int tid = threadIdx.x;
-  const int g = tid >> 6, t = tid & 63, ti = t >> 3, tj = t & 7;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t per = (a.n + a.nranges - 1) / a.nranges;
   const int64_t p0 = static_cast<int64_t>(range) * per;
   const int64_t p1 = p0 + per < a.n ? p0 + per : a.n;
@@ -84,70 +95,61 @@ __global__ void __launch_bounds__(kThreads, 1) moments_kernel(MomArgs a) {
   const int feat = lf < 64 ? bi * kFB + lf : bj * kFB + (lf - 64);
   const bool fvalid = feat < a.D;
   const double sf = fvalid ? a.s[feat] : 0.0;
-  double ssum = 0.0;  // column sum of (x - s) for diagonal pairs
+  double ssum = 0.0;  // column sum of (x - s) (used by diagonal pairs)
 
-  double acc[8][8];
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[2][4][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  float pre[kChunk / 2];
+  auto load = [&](int64_t c0) {
+#pragma unroll
+    for (int r = 0; r < kChunk / 2; ++r) {
+      const int64_t p = c0 + 2 * r + lrow;
+      pre[r] = (p < p1 && fvalid) ? __ldg(a.X + p * a.D + feat) : 0.0f;
+    }
+  };
+  if (p0 < p1) load(p0);
   for (int64_t c0 = p0; c0 < p1; c0 += kChunk) {
     __syncthreads();
-    for (int r = lrow; r < kChunk; r += 2) {
-      const int64_t p = c0 + r;
-      double v = 0.0;
-      if (p < p1 && fvalid) v = static_cast<double>(__ldg(a.X + p * a.D + feat)) - sf;
-      cs[r * 128 + lf] = v;
+#pragma unroll
+    for (int r = 0; r < kChunk / 2; ++r) {
+      const int64_t p = c0 + 2 * r + lrow;
+      const double v = (p < p1 && fvalid) ? static_cast<double>(pre[r]) - sf : 0.0;
+      cs[(2 * r + lrow) * kLds + lf] = v;
       ssum += v;
     }
     __syncthreads();
-    const int rend = static_cast<int>(p1 - c0 < kChunk ? p1 - c0 : kChunk);
-    for (int r = g; r < rend; r += 4) {
-      const double* row = cs + r * 128;
-      double x[8], y[8];
+    if (c0 + kChunk < p1) load(c0 + kChunk);  // in flight during the MMAs below
+#pragma unroll 4
+    for (int k0 = 0; k0 < kChunk; k0 += 4) {
+      const double* row = cs + (k0 + fk) * kLds;
+      double af[2], bf[4];
 #pragma unroll
-      for (int i = 0; i < 8; i += 2) {
-        const double2 u = *reinterpret_cast<const double2*>(row + ti * 8 + i);
-        x[i] = u.x;
-        x[i + 1] = u.y;
-        const double2 w = *reinterpret_cast<const double2*>(row + 64 + tj * 8 + i);
-        y[i] = w.x;
-        y[i + 1] = w.y;
-      }
+      for (int i = 0; i < 2; ++i) af[i] = row[wm + i * 8 + fr];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 4; ++j) bf[j] = row[64 + wn + j * 8 + fr];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
     }
-  }
-  // reduce the 4 groups' register blocks through shared memory (fixed order)
-  __syncthreads();
-  double* red = cs;  // 64 x 64 doubles = 32 KB (smem is 64 KB)
-  for (int gg = 1; gg < 4; ++gg) {
-    if (g == gg) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) red[(ti * 8 + i) * 64 + tj * 8 + j] = acc[i][j];
-    }
-    __syncthreads();
-    if (g == 0) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] += red[(ti * 8 + i) * 64 + tj * 8 + j];
-    }
-    __syncthreads();
   }
   const int slot = a.slot0 + range;
-  if (g == 0) {
-    double* out = a.Gpart + (static_cast<int64_t>(pair) * a.nslots + slot) * (kFB * kFB);
+  double* out = a.Gpart + (static_cast<int64_t>(pair) * a.nslots + slot) * (kFB * kFB);
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) out[(ti * 8 + i) * 64 + tj * 8 + j] = acc[i][j];
-  }
+    for (int j = 0; j < 4; ++j) {
+      const int r = wm + i * 8 + fr;
+      const int c = wn + j * 8 + 2 * fk;
+      out[r * 64 + c] = acc[i][j][0];
+      out[r * 64 + c + 1] = acc[i][j][1];
+    }
   // column sums: only diagonal pairs, features of block bi (lf < 64); two row parities
   __syncthreads();
   if (bi == bj) {
@@ -234,7 +236,7 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
   MomentsPlan p;
   p.nb = (D + kFB - 1) / kFB;
   p.npairs = p.nb * (p.nb + 1) / 2;
-  const int target = 3 * num_sms;  // CTAs
+  const int target = 4 * num_sms;  // CTAs (2 resident per SM)
   int per_pair = (target + p.npairs - 1) / p.npairs;
   if (per_pair < 2) per_pair = 2;
   const double fa = static_cast<double>(nA) / static_cast<double>(nA + nB);
@@ -256,7 +258,7 @@ cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, con
                            const MomentsBufs& b, cudaStream_t st) {
   count_launch();
   shift_kernel<<<(D + 255) / 256, 256, 0, st>>>(A, nA, B, nB, D, b.s);
-  const size_t smem = sizeof(double) * kChunk * 128;
+  const size_t smem = sizeof(double) * kChunk * kLds;
   cudaError_t e = cudaFuncSetAttribute(moments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
