@@ -12,18 +12,31 @@
 //   4. back-transformation y = Q x, normalisation, sign rule (largest-|coord|
 //      entry positive, lowest index on ties), rank drop
 //      (lambda <= D 2^-52 lambda_1).
-// One CTA of 1024 threads; the matrix lives in shared memory when it fits
-// (D <= 160) and in global memory (L2-resident) otherwise. Latency-bound.
+//
+// Layout: ONE thread-block cluster of 8 CTAs. The matrix is kept on chip: row r
+// lives in CTA r % 8 (cyclic, so every CTA keeps work as the trailing block
+// shrinks), <= 32 rows x 256 fp64 = 64 KB of shared memory per CTA. Each
+// Householder step needs three cluster barriers: (1) column norm partials,
+// (2) the Householder vector v, (3) p = 2 A v and v^T p; the vectors are
+// exchanged by direct stores into every CTA's shared memory (DSMEM).
+// Latency-bound: ~3 x (D-2) cluster barriers.
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
 
+#include <cooperative_groups.h>
+
 #include <cfloat>
+
+namespace cg = cooperative_groups;
 
 namespace prohd {
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kWarps = kThreads / 32;
+constexpr int kCl = 8;       // CTAs per cluster
+constexpr int kT = 256;      // threads per CTA
+constexpr int kWarps = kT / 32;
+constexpr int kMaxD = 256;
+constexpr int kRows = kMaxD / kCl;  // rows per CTA (max)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -31,7 +44,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// block-wide sum; `red` has >= kWarps doubles; result broadcast to all threads
 __device__ double block_sum(double v, double* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -39,8 +51,7 @@ __device__ double block_sum(double v, double* red) {
   if (l == 0) red[w] = v;
   __syncthreads();
   double t = (l < kWarps) ? red[l] : 0.0;
-  t = warp_sum(t);
-  return t;
+  return warp_sum(t);
 }
 
 // number of eigenvalues of T (d, e2 = e^2) strictly less than x (Sturm count)
@@ -58,136 +69,215 @@ __device__ int sturm_count(const double* d, const double* e2, int n, double x, d
 }
 
 struct EigArgs {
-  double* C;  // D x D (destroyed); used as the working matrix when it does not fit in smem
+  const double* C;  // D x D symmetric (read)
   int D;
-  int k;           // requested PCs
-  double* V;       // Householder vectors [D][D] (row j = v_j), workspace
-  double* X;       // [k][D] eigenvectors of T, then of C (workspace)
-  double* out64;   // U64 rows 1..k: [k+1][D] (row 0 = u0, untouched)
-  float* out32;    // U32 rows
-  double* lam;     // [k] eigenvalues (desc)
-  int* n_dirs;     // 1 + kept
-  int use_smem;
+  int k;          // requested PCs
+  double* V;      // Householder vectors [D][D] (row j = v_j), workspace (global)
+  double* X;      // [k][D] eigenvectors of T, then of C (workspace)
+  double* out64;  // U64 rows 1..k: [k+1][D] (row 0 = u0, untouched)
+  float* out32;   // U32 rows
+  double* lam;    // [k] eigenvalues (desc)
+  int* n_dirs;    // 1 + kept
 };
 
-__global__ void __launch_bounds__(kThreads, 1) eigen_topk_kernel(EigArgs a) {
-  extern __shared__ double sm[];
+// inverse iteration for eigenvalue `lam` of T (one warp; lane 0 runs the serial solve)
+__device__ void inverse_iteration(const double* d, const double* e, int D, double lam, double tnorm, double pivmin,
+                                  double* x, double* u0, double* u1, double* u2, const double* X, const int* prev,
+                                  int nprev, int w, int lane) {
+  for (int i = lane; i < D; i += 32) {
+    unsigned h = static_cast<unsigned>(i) * 2654435761u ^ (static_cast<unsigned>(w) * 40503u + 17u);
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    x[i] = 0.5 + (h & 0xffff) / 65536.0;
+  }
+  __syncwarp();
+  const double eps_p = DBL_EPSILON * tnorm + pivmin;
+  for (int iter = 0; iter < 3; ++iter) {
+    if (lane == 0) {
+      // (T - lam I) y = x, Gaussian elimination with partial pivoting (tridiagonal, fill u2)
+      double dd = d[0] - lam, ee = (D > 1) ? e[0] : 0.0;
+      for (int i = 0; i < D - 1; ++i) {
+        const double sub = e[i];
+        const double dn = d[i + 1] - lam;
+        const double en = (i + 2 < D) ? e[i + 1] : 0.0;
+        if (fabs(dd) >= fabs(sub)) {
+          if (dd == 0.0) dd = eps_p;
+          const double mlt = sub / dd;
+          u0[i] = dd;
+          u1[i] = ee;
+          u2[i] = 0.0;
+          x[i + 1] -= mlt * x[i];
+          dd = dn - mlt * ee;
+          ee = en;
+        } else {
+          const double mlt = dd / sub;
+          u0[i] = sub;
+          u1[i] = dn;
+          u2[i] = en;
+          const double t = x[i];
+          x[i] = x[i + 1];
+          x[i + 1] = t - mlt * x[i + 1];
+          dd = ee - mlt * dn;
+          ee = -mlt * en;
+        }
+      }
+      if (dd == 0.0) dd = eps_p;
+      u0[D - 1] = dd;
+      x[D - 1] /= u0[D - 1];
+      if (D >= 2) x[D - 2] = (x[D - 2] - u1[D - 2] * x[D - 1]) / u0[D - 2];
+      for (int i = D - 3; i >= 0; --i) x[i] = (x[i] - u1[i] * x[i + 1] - u2[i] * x[i + 2]) / u0[i];
+    }
+    __syncwarp();
+    // modified Gram-Schmidt against the earlier vectors of the same cluster, then normalise
+    for (int q = 0; q < nprev; ++q) {
+      const double* y = X + static_cast<int64_t>(prev[q]) * D;
+      double s = 0.0;
+      for (int i = lane; i < D; i += 32) s += y[i] * x[i];
+      s = warp_sum(s);
+      for (int i = lane; i < D; i += 32) x[i] -= s * y[i];
+      __syncwarp();
+    }
+    double s = 0.0;
+    for (int i = lane; i < D; i += 32) s += x[i] * x[i];
+    s = warp_sum(s);
+    const double inv = 1.0 / sqrt(s);
+    for (int i = lane; i < D; i += 32) x[i] *= inv;
+    __syncwarp();
+  }
+}
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_cluster_kernel(EigArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = static_cast<int>(cl.block_rank());
+  extern __shared__ double dyn[];
+  double* M = dyn;                   // [kRows][D] own rows (row r -> M[(r/8)*D])
+  double* lu = dyn + kRows * kMaxD;  // [kWarps][3][kMaxD] LU scratch
   __shared__ double red[kWarps];
-  __shared__ double d[256], e[256], e2[256], lamv[256];
-  __shared__ double vbuf[256], pbuf[256];
-  __shared__ double u0[256], u1[256], u2[256];  // LU factors of (T - lambda I), inverse iteration
-  __shared__ double s_alpha, s_scale;
+  __shared__ double vfull[kMaxD], pfull[kMaxD], wfull[kMaxD];
+  __shared__ double part[kCl], part2[kCl];
+  __shared__ double d[kMaxD], e[kMaxD], e2[kMaxD], lamv[kMaxD];
+  __shared__ double s_x0;
+  __shared__ int s_prev[kWarps][16];
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double* M = a.use_smem ? sm : a.C;
-  if (a.use_smem) {
-    for (int i = tid; i < D * D; i += kThreads) M[i] = a.C[i];
-    __syncthreads();
+  const int nloc = (D - rank + kCl - 1) / kCl;  // rows r = rank + 8*i, i < nloc
+  for (int t = tid; t < nloc * D; t += kT) {
+    const int i = t / D, c = t % D;
+    M[i * D + c] = a.C[static_cast<int64_t>(rank + kCl * i) * D + c];
   }
+  cl.sync();
 
   // ---------------------------------------------------------------- 1. tridiagonalise
   for (int j = 0; j + 2 < D; ++j) {
-    const int L = D - j - 1;  // length of the column below the diagonal
-    double part = 0.0;
-    for (int i = tid; i < L; i += kThreads) {
-      const double x = M[(j + 1 + i) * D + j];
-      vbuf[i] = x;
-      part += x * x;
+    // phase 1: publish d[j], x0 = M[j+1][j], and this CTA's sum of squares of column j below j
+    if (tid == 0 && (j % kCl) == rank) {
+      const double v = M[(j / kCl) * D + j];
+      for (int q = 0; q < kCl; ++q) *cl.map_shared_rank(&d[j], q) = v;
     }
-    const double nrm2 = block_sum(part, red);
-    if (tid == 0) {
-      const double nrm = sqrt(nrm2);
-      const double x0 = vbuf[0];
-      const double alpha = (x0 > 0.0) ? -nrm : nrm;  // avoid cancellation in v0 = x0 - alpha
-      s_alpha = alpha;
-      const double v0 = x0 - alpha;
-      // ||v||^2 = ||x||^2 - x0^2 + v0^2
-      const double vn2 = nrm2 - x0 * x0 + v0 * v0;
-      s_scale = (vn2 > 0.0 && nrm > 0.0) ? 1.0 / sqrt(vn2) : 0.0;
-      vbuf[0] = v0;
+    if (tid == 0 && ((j + 1) % kCl) == rank) {
+      const double v = M[((j + 1) / kCl) * D + j];
+      for (int q = 0; q < kCl; ++q) *cl.map_shared_rank(&s_x0, q) = v;
     }
-    __syncthreads();
-    const double sc = s_scale;
-    for (int i = tid; i < L; i += kThreads) vbuf[i] *= sc;
-    for (int i = tid; i < D; i += kThreads) a.V[static_cast<int64_t>(j) * D + i] = (i > j) ? vbuf[i - j - 1] : 0.0;
-    __syncthreads();
-    if (tid == 0) {
-      d[j] = M[j * D + j];
-      e[j] = (sc != 0.0) ? s_alpha : 0.0;
+    double ps = 0.0;
+    for (int i = tid; i < nloc; i += kT) {
+      const int r = rank + kCl * i;
+      if (r > j) {
+        const double x = M[i * D + j];
+        ps += x * x;
+      }
     }
-    if (sc == 0.0) {  // column already zero below the subdiagonal: H = I
-      __syncthreads();
-      continue;
+    ps = block_sum(ps, red);
+    if (tid < kCl) *cl.map_shared_rank(&part[rank], tid) = ps;
+    cl.sync();
+    // phase 2: every CTA forms alpha and the scale redundantly; publish own entries of v
+    double nrm2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kCl; ++q) nrm2 += part[q];
+    const double nrm = sqrt(nrm2);
+    const double x0 = s_x0;
+    const double alpha = (x0 > 0.0) ? -nrm : nrm;
+    const double v0 = x0 - alpha;
+    const double vn2 = nrm2 - x0 * x0 + v0 * v0;
+    const double sc = (vn2 > 0.0 && nrm > 0.0) ? 1.0 / sqrt(vn2) : 0.0;
+    if (tid == 0) e[j] = (sc != 0.0) ? alpha : 0.0;
+    for (int t = tid; t < nloc * kCl; t += kT) {
+      const int i = t / kCl, q = t % kCl;
+      const int r = rank + kCl * i;
+      double v = 0.0;
+      if (r > j) v = ((r == j + 1) ? v0 : M[i * D + j]) * sc;
+      if (r > j) *cl.map_shared_rank(&vfull[r], q) = v;
+      if (q == 0) a.V[static_cast<int64_t>(j) * D + r] = v;
     }
-    // p = 2 A' v  (A' = trailing L x L block), warp per row
-    for (int r = warp; r < L; r += kWarps) {
-      const double* row = M + (j + 1 + r) * D + (j + 1);
-      double s = 0.0;
-      for (int c = lane; c < L; c += 32) s += row[c] * vbuf[c];
-      s = warp_sum(s);
-      if (lane == 0) pbuf[r] = 2.0 * s;
-    }
-    __syncthreads();
+    cl.sync();
+    if (sc == 0.0) continue;  // column already zero below the subdiagonal: H = I (uniform decision)
+    // phase 3: p_r = 2 sum_c M[r][c] v_c (own rows r > j), and v^T p partial
     double vp = 0.0;
-    for (int i = tid; i < L; i += kThreads) vp += vbuf[i] * pbuf[i];
-    const double K = block_sum(vp, red);
-    for (int i = tid; i < L; i += kThreads) pbuf[i] = pbuf[i] - K * vbuf[i];  // w = p - (v^T p) v
+    for (int i = warp; i < nloc; i += kWarps) {
+      const int r = rank + kCl * i;
+      if (r <= j) continue;
+      const double* row = M + i * D;
+      double s = 0.0;
+      for (int c = j + 1 + lane; c < D; c += 32) s += row[c] * vfull[c];
+      s = 2.0 * warp_sum(s);
+      if (lane < kCl) *cl.map_shared_rank(&pfull[r], lane) = s;
+      vp += (lane == 0) ? s * vfull[r] : 0.0;
+    }
+    vp = block_sum(vp, red);
+    if (tid < kCl) *cl.map_shared_rank(&part2[rank], tid) = vp;
+    cl.sync();
+    // phase 4: w = p - (v^T p) v, then A' -= v w^T + w v^T on own rows
+    double K = 0.0;
+#pragma unroll
+    for (int q = 0; q < kCl; ++q) K += part2[q];
+    for (int c = j + 1 + tid; c < D; c += kT) wfull[c] = pfull[c] - K * vfull[c];
     __syncthreads();
-    // A' -= v w^T + w v^T
-    for (int64_t t = tid; t < static_cast<int64_t>(L) * L; t += kThreads) {
-      const int r = static_cast<int>(t / L), c = static_cast<int>(t % L);
-      double* pm = M + (j + 1 + r) * D + (j + 1 + c);
-      *pm = *pm - vbuf[r] * pbuf[c] - pbuf[r] * vbuf[c];
+    for (int t = tid; t < nloc * (D - j - 1); t += kT) {
+      const int i = t / (D - j - 1), c = j + 1 + t % (D - j - 1);
+      const int r = rank + kCl * i;
+      if (r <= j) continue;
+      M[i * D + c] -= vfull[r] * wfull[c] + wfull[r] * vfull[c];
     }
     __syncthreads();
   }
-  if (tid == 0) {
-    if (D >= 2) {
-      d[D - 2] = M[(D - 2) * D + (D - 2)];
-      e[D - 2] = M[(D - 1) * D + (D - 2)];
-    }
-    d[D - 1] = M[(D - 1) * D + (D - 1)];
+  // last 2x2 block
+  if (tid == 0 && D >= 2 && ((D - 2) % kCl) == rank) {
+    const double v = M[((D - 2) / kCl) * D + (D - 2)];
+    for (int q = 0; q < kCl; ++q) *cl.map_shared_rank(&d[D - 2], q) = v;
   }
-  __syncthreads();
-  for (int i = tid; i < D - 1; i += kThreads) e2[i] = e[i] * e[i];
+  if (tid == 0 && ((D - 1) % kCl) == rank) {
+    const int i = (D - 1) / kCl;
+    const double dv = M[i * D + (D - 1)];
+    const double ev = D >= 2 ? M[i * D + (D - 2)] : 0.0;
+    for (int q = 0; q < kCl; ++q) {
+      *cl.map_shared_rank(&d[D - 1], q) = dv;
+      if (D >= 2) *cl.map_shared_rank(&e[D - 2], q) = ev;
+    }
+  }
+  cl.sync();
+  for (int i = tid; i < D - 1; i += kT) e2[i] = e[i] * e[i];
   __syncthreads();
 
-  // ---------------------------------------------------------------- 2. eigenvalues
-  // Gershgorin bounds
-  double gl = 0.0, gu = 0.0, tnorm = 0.0;
-  if (tid == 0) {
-    gl = DBL_MAX;
-    gu = -DBL_MAX;
-    for (int i = 0; i < D; ++i) {
-      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < D ? fabs(e[i]) : 0.0);
-      gl = fmin(gl, d[i] - r);
-      gu = fmax(gu, d[i] + r);
-    }
-    tnorm = fmax(fabs(gl), fabs(gu));
-    red[0] = gl;
-    red[1] = gu;
-    red[2] = tnorm;
+  // ---------------------------------------------------------------- 2. eigenvalues (every CTA, redundantly)
+  double gl = DBL_MAX, gu = -DBL_MAX;
+  for (int i = 0; i < D; ++i) {
+    const double rr = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < D ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - rr);
+    gu = fmax(gu, d[i] + rr);
   }
-  __syncthreads();
-  gl = red[0];
-  gu = red[1];
-  tnorm = red[2];
-  __syncthreads();
+  const double tnorm = fmax(fabs(gl), fabs(gu));
   const double pivmin = fmax(DBL_MIN, 1e-300 * tnorm) + DBL_MIN;
   const int kk = a.k < D ? a.k : D;
-  // eigenvalue index (ascending) D-1-w for w = 0..kk-1 -> one warp each
   for (int w = warp; w < kk; w += kWarps) {
-    const int target = D - 1 - w;  // want lambda with exactly `target` eigenvalues below
+    const int target = D - 1 - w;  // the eigenvalue with exactly `target` eigenvalues below it
     double lo = gl - 1e-12 * tnorm - pivmin, hi = gu + 1e-12 * tnorm + pivmin;
     for (int it = 0; it < 64; ++it) {
       const double width = hi - lo;
       if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
       const double x = lo + width * (lane + 1) / 33.0;
       const int cnt = sturm_count(d, e2, D, x, pivmin);
-      // predicate: count(x) <= target  (x is at or below the wanted eigenvalue)
       const unsigned below = __ballot_sync(0xffffffffu, cnt <= target);
-      // probes are increasing in x; find the last probe with cnt <= target
-      const int nb = __popc(below);  // probes 0..nb-1 satisfy (monotone)
+      const int nb = __popc(below);  // monotone: probes 0..nb-1 are at or below the eigenvalue
       const double nlo = (nb == 0) ? lo : lo + width * nb / 33.0;
       const double nhi = (nb == 32) ? hi : lo + width * (nb + 1) / 33.0;
       lo = nlo;
@@ -197,100 +287,48 @@ __global__ void __launch_bounds__(kThreads, 1) eigen_topk_kernel(EigArgs a) {
   }
   __syncthreads();
 
-  // ---------------------------------------------------------------- 3. inverse iteration (warp 0, serial in lane 0)
-  // clusters: consecutive eigenvalues within 1e-3 * ||T|| are re-orthogonalised
+  // ---------------------------------------------------------------- 3. inverse iteration
+  // clusters of consecutive eigenvalues closer than 1e-3 ||T|| are handled by one warp in order
   const double clus = 1e-3 * tnorm;
-  if (warp == 0) {
-    for (int w = 0; w < kk; ++w) {
-      double* xw = a.X + static_cast<int64_t>(w) * D;
-      const double lam = lamv[w];
-      // initial vector: deterministic pseudo-random
-      for (int i = lane; i < D; i += 32) {
-        unsigned h = (unsigned)(i * 2654435761u) ^ (unsigned)(w * 40503u + 17u);
-        h ^= h >> 13;
-        h *= 0x5bd1e995u;
-        h ^= h >> 15;
-        a.X[static_cast<int64_t>(w) * D + i] = 0.5 + (h & 0xffff) / 65536.0;
-      }
-      __syncwarp();
-      for (int iter = 0; iter < 4; ++iter) {
-        if (lane == 0) {
-          // solve (T - lam I) y = x by Gaussian elimination with partial pivoting (tridiagonal)
-          // store factors in pbuf/vbuf-like local arrays (use e2 as scratch? no: use local)
-          double* x = a.X + static_cast<int64_t>(w) * D;
-          const double eps_p = DBL_EPSILON * tnorm + pivmin;
-          // factor
-          double dd = d[0] - lam, ee = (D > 1) ? e[0] : 0.0;
-          for (int i = 0; i < D - 1; ++i) {
-            const double sub = e[i];
-            const double dn = d[i + 1] - lam;
-            const double en = (i + 2 < D) ? e[i + 1] : 0.0;
-            if (fabs(dd) >= fabs(sub)) {
-              if (dd == 0.0) dd = eps_p;
-              const double mlt = sub / dd;
-              u0[i] = dd;
-              u1[i] = ee;
-              u2[i] = 0.0;
-              x[i + 1] -= mlt * x[i];
-              dd = dn - mlt * ee;
-              ee = en;
-            } else {
-              const double mlt = dd / sub;
-              u0[i] = sub;
-              u1[i] = dn;
-              u2[i] = en;
-              const double t = x[i];
-              x[i] = x[i + 1];
-              x[i + 1] = t - mlt * x[i + 1];
-              dd = ee - mlt * dn;
-              ee = -mlt * en;
-            }
-          }
-          if (dd == 0.0) dd = eps_p;
-          u0[D - 1] = dd;
-          // back substitution
-          x[D - 1] /= u0[D - 1];
-          if (D >= 2) x[D - 2] = (x[D - 2] - u1[D - 2] * x[D - 1]) / u0[D - 2];
-          for (int i = D - 3; i >= 0; --i) x[i] = (x[i] - u1[i] * x[i + 1] - u2[i] * x[i + 2]) / u0[i];
-        }
-        __syncwarp();
-        // re-orthogonalise against previous vectors of the same cluster (MGS), then normalise
-        for (int p = 0; p < w; ++p) {
-          if (fabs(lamv[p] - lam) > clus) continue;
-          double s = 0.0;
-          for (int i = lane; i < D; i += 32) s += a.X[static_cast<int64_t>(p) * D + i] * xw[i];
-          s = warp_sum(s);
-          for (int i = lane; i < D; i += 32) xw[i] -= s * a.X[static_cast<int64_t>(p) * D + i];
+  {
+    int c = 0;  // cluster index
+    int start = 0;
+    while (start < kk) {
+      int end = start + 1;
+      while (end < kk && fabs(lamv[end - 1] - lamv[end]) <= clus) ++end;
+      const int slot = c % (kCl * kWarps);
+      if (slot / kWarps == rank && slot % kWarps == warp) {
+        double* u0 = lu + warp * 3 * kMaxD;
+        int nprev = 0;
+        for (int w = start; w < end; ++w) {
+          inverse_iteration(d, e, D, lamv[w], tnorm, pivmin, a.X + static_cast<int64_t>(w) * D, u0, u0 + kMaxD,
+                            u0 + 2 * kMaxD, a.X, s_prev[warp], nprev, w, lane);
+          if (lane == 0 && nprev < 16) s_prev[warp][nprev] = w;
           __syncwarp();
+          if (nprev < 16) ++nprev;
         }
-        double s = 0.0;
-        for (int i = lane; i < D; i += 32) s += xw[i] * xw[i];
-        s = warp_sum(s);
-        const double inv = 1.0 / sqrt(s);
-        for (int i = lane; i < D; i += 32) xw[i] *= inv;
-        __syncwarp();
       }
+      ++c;
+      start = end;
     }
   }
-  __syncthreads();
+  cl.sync();  // eigenvectors of T (global memory) visible to the whole cluster
 
   // ---------------------------------------------------------------- 4. back-transform, sign, output
-  const double lam1 = kk > 0 ? lamv[0] : 0.0;
-  for (int w = warp; w < kk; w += kWarps) {
+  for (int w = rank * kWarps + warp; w < kk; w += kCl * kWarps) {
     double* y = a.X + static_cast<int64_t>(w) * D;
     for (int j = D - 3; j >= 0; --j) {
       const double* v = a.V + static_cast<int64_t>(j) * D;
       double s = 0.0;
-      for (int i = lane; i < D; i += 32) s += v[i] * y[i];
+      for (int i = j + 1 + lane; i < D; i += 32) s += v[i] * y[i];
       s = warp_sum(s);
-      for (int i = lane; i < D; i += 32) y[i] -= 2.0 * s * v[i];
+      for (int i = j + 1 + lane; i < D; i += 32) y[i] -= 2.0 * s * v[i];
       __syncwarp();
     }
     double s = 0.0;
     for (int i = lane; i < D; i += 32) s += y[i] * y[i];
     s = warp_sum(s);
     const double inv = 1.0 / sqrt(s);
-    // largest |coordinate|, lowest index on ties
     double best = -1.0;
     int bidx = D;
     for (int i = lane; i < D; i += 32) {
@@ -317,7 +355,8 @@ __global__ void __launch_bounds__(kThreads, 1) eigen_topk_kernel(EigArgs a) {
     }
     if (lane == 0) a.lam[w] = lamv[w];
   }
-  if (tid == 0) {
+  if (rank == 0 && tid == 0) {
+    const double lam1 = kk > 0 ? lamv[0] : 0.0;
     int kept = 0;
     if (lam1 > 0.0) {
       for (int w = 0; w < kk; ++w) {
@@ -333,17 +372,14 @@ __global__ void __launch_bounds__(kThreads, 1) eigen_topk_kernel(EigArgs a) {
 
 cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, double* out64, float* out32,
                               double* lam, int* n_dirs, cudaStream_t st) {
-  EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs, 0};
-  size_t smem = 0;
-  if (static_cast<size_t>(D) * D * sizeof(double) <= 160 * 1024) {
-    a.use_smem = 1;
-    smem = static_cast<size_t>(D) * D * sizeof(double);
-  }
-  cudaError_t e = cudaFuncSetAttribute(eigen_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (D > kMaxD) return cudaErrorInvalidValue;
+  EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs};
+  const size_t smem = sizeof(double) * (static_cast<size_t>(kRows) * kMaxD + static_cast<size_t>(kWarps) * 3 * kMaxD);
+  cudaError_t e = cudaFuncSetAttribute(eigen_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   count_launch();
-  eigen_topk_kernel<<<1, kThreads, smem, st>>>(a);
+  eigen_cluster_kernel<<<kCl, kT, smem, st>>>(a);
   return cudaGetLastError();
 }
 
