@@ -73,13 +73,17 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-constexpr int kLds = 136;  // fp64 row stride of the chunk tile (128 features + 8 pad: 2-way banks)
+constexpr int kLds = 136;   // fp64 row stride of the chunk tile (128 features + 8 pad)
+constexpr int kMT = 128;    // threads per CTA (4 warps)
+constexpr int kMC = 32;     // points per chunk
 
-// One CTA: one 64x64 block (bi, bj) of G over one point range. 8 warps; warp w owns
-// rows [16*(w/2), +16) x cols [32*(w%2), +32) = 2 x 4 DMMA tiles. The next 64-point
-// chunk is prefetched into registers while the current one is multiplied.
-__global__ void __launch_bounds__(kThreads, 2) moments_kernel(MomArgs a) {
-  extern __shared__ double cs[];  // [kChunk][kLds]: features of block bi (0..63) then bj (64..127)
+// One CTA: one 64x64 block (bi, bj) of G over one point range. 4 warps, warp w
+// owns the 32x32 tile (w/2, w%2) = 4 x 4 DMMA tiles (16 MMAs per 8 fragment
+// loads). In diagonal blocks the strictly-lower warp tile (1,0) is skipped (its
+// mirror (0,1) is computed). The next 32-point chunk is prefetched into
+// registers while the current one is multiplied.
+__global__ void __launch_bounds__(kMT, 3) moments_kernel(MomArgs a) {
+  extern __shared__ double cs[];  // [kMC][kLds]: features of block bi (0..63) then bj (64..127)
   const int pair = blockIdx.x;
   const int range = blockIdx.y;
   int bi, bj;
@@ -89,78 +93,73 @@ __global__ void __launch_bounds__(kThreads, 2) moments_kernel(MomArgs a) {
   const int64_t p0 = static_cast<int64_t>(range) * per;
   const int64_t p1 = p0 + per < a.n ? p0 + per : a.n;
 
-  // loader mapping: thread -> (feature column lf in 0..127, row parity)
-  const int lf = tid & 127;
-  const int lrow = tid >> 7;  // 0..1
+  // loader mapping: thread -> feature column lf (0..127)
+  const int lf = tid;
   const int feat = lf < 64 ? bi * kFB + lf : bj * kFB + (lf - 64);
   const bool fvalid = feat < a.D;
   const double sf = fvalid ? a.s[feat] : 0.0;
   double ssum = 0.0;  // column sum of (x - s) (used by diagonal pairs)
 
-  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const bool active = !(bi == bj && wm > wn);
   const int fr = lane >> 2, fk = lane & 3;
-  double acc[2][4][2];
+  double acc[4][4][2];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  float pre[kChunk / 2];
+  float pre[kMC];
   auto load = [&](int64_t c0) {
 #pragma unroll
-    for (int r = 0; r < kChunk / 2; ++r) {
-      const int64_t p = c0 + 2 * r + lrow;
+    for (int r = 0; r < kMC; ++r) {
+      const int64_t p = c0 + r;
       pre[r] = (p < p1 && fvalid) ? __ldg(a.X + p * a.D + feat) : 0.0f;
     }
   };
   if (p0 < p1) load(p0);
-  for (int64_t c0 = p0; c0 < p1; c0 += kChunk) {
+  for (int64_t c0 = p0; c0 < p1; c0 += kMC) {
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kChunk / 2; ++r) {
-      const int64_t p = c0 + 2 * r + lrow;
+    for (int r = 0; r < kMC; ++r) {
+      const int64_t p = c0 + r;
       const double v = (p < p1 && fvalid) ? static_cast<double>(pre[r]) - sf : 0.0;
-      cs[(2 * r + lrow) * kLds + lf] = v;
+      cs[r * kLds + lf] = v;
       ssum += v;
     }
     __syncthreads();
-    if (c0 + kChunk < p1) load(c0 + kChunk);  // in flight during the MMAs below
-#pragma unroll 4
-    for (int k0 = 0; k0 < kChunk; k0 += 4) {
-      const double* row = cs + (k0 + fk) * kLds;
-      double af[2], bf[4];
+    if (c0 + kMC < p1) load(c0 + kMC);  // in flight during the MMAs below
+    if (active) {
+#pragma unroll 2
+      for (int k0 = 0; k0 < kMC; k0 += 4) {
+        const double* row = cs + (k0 + fk) * kLds;
+        double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) af[i] = row[wm + i * 8 + fr];
+        for (int i = 0; i < 4; ++i) af[i] = row[wm + i * 8 + fr];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = row[64 + wn + j * 8 + fr];
+        for (int j = 0; j < 4; ++j) bf[j] = row[64 + wn + j * 8 + fr];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+      }
     }
   }
   const int slot = a.slot0 + range;
   double* out = a.Gpart + (static_cast<int64_t>(pair) * a.nslots + slot) * (kFB * kFB);
+  if (active) {
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = wm + i * 8 + fr;
-      const int c = wn + j * 8 + 2 * fk;
-      out[r * 64 + c] = acc[i][j][0];
-      out[r * 64 + c + 1] = acc[i][j][1];
-    }
-  // column sums: only diagonal pairs, features of block bi (lf < 64); two row parities
-  __syncthreads();
-  if (bi == bj) {
-    double* tmp = cs;
-    tmp[tid] = ssum;
-    __syncthreads();
-    if (tid < 64) {
-      const double v = tmp[tid] + tmp[tid + 128];
-      a.Spart[static_cast<int64_t>(slot) * (a.nb * kFB) + bi * kFB + tid] = v;
-    }
+      for (int j = 0; j < 4; ++j) {
+        const int r = wm + i * 8 + fr;
+        const int c = wn + j * 8 + 2 * fk;
+        out[r * 64 + c] = acc[i][j][0];
+        out[r * 64 + c + 1] = acc[i][j][1];
+      }
   }
+  // column sums: only diagonal pairs, features of block bi (lf < 64)
+  if (bi == bj && lf < 64) a.Spart[static_cast<int64_t>(slot) * (a.nb * kFB) + bi * kFB + lf] = ssum;
 }
 
 // G (full symmetric D x D) and S_A, S_B from the partials, fixed summation order.
@@ -176,6 +175,7 @@ __global__ void __launch_bounds__(256) moments_reduce_kernel(const double* __res
     const int w = static_cast<int>(e % (kFB * kFB));
     int bi, bj;
     pair_of(pair, nb, bi, bj);
+    if (bi == bj && (w / kFB) > (w % kFB)) continue;  // diagonal blocks: upper triangle is authoritative
     const int i = bi * kFB + w / kFB, j = bj * kFB + w % kFB;
     if (i >= D || j >= D) continue;
     double acc = 0.0;
@@ -236,7 +236,7 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
   MomentsPlan p;
   p.nb = (D + kFB - 1) / kFB;
   p.npairs = p.nb * (p.nb + 1) / 2;
-  const int target = 4 * num_sms;  // CTAs (2 resident per SM)
+  const int target = 6 * num_sms;  // CTAs (3 resident per SM)
   int per_pair = (target + p.npairs - 1) / p.npairs;
   if (per_pair < 2) per_pair = 2;
   const double fa = static_cast<double>(nA) / static_cast<double>(nA + nB);
@@ -258,16 +258,16 @@ cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, con
                            const MomentsBufs& b, cudaStream_t st) {
   count_launch();
   shift_kernel<<<(D + 255) / 256, 256, 0, st>>>(A, nA, B, nB, D, b.s);
-  const size_t smem = sizeof(double) * kChunk * kLds;
+  const size_t smem = sizeof(double) * kMC * kLds;
   cudaError_t e = cudaFuncSetAttribute(moments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   MomArgs a{A, nA, D, b.s, p.nb, 0, p.rangesA, p.nslots, b.Gpart, b.Spart};
   count_launch();
-  moments_kernel<<<dim3(p.npairs, p.rangesA), kThreads, smem, st>>>(a);
+  moments_kernel<<<dim3(p.npairs, p.rangesA), kMT, smem, st>>>(a);
   MomArgs bb{B, nB, D, b.s, p.nb, p.rangesA, p.rangesB, p.nslots, b.Gpart, b.Spart};
   count_launch();
-  moments_kernel<<<dim3(p.npairs, p.rangesB), kThreads, smem, st>>>(bb);
+  moments_kernel<<<dim3(p.npairs, p.rangesB), kMT, smem, st>>>(bb);
   count_launch();
   moments_reduce_kernel<<<148 * 2, 256, 0, st>>>(b.Gpart, b.Spart, p.nb, D, p.rangesA, p.nslots, b.C, b.SA,
                                                  b.SB);

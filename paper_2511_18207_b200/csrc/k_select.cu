@@ -81,6 +81,107 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
   if (lane == 0) atomicMax(maxnorm2, __float_as_uint(wmax));  // non-negative floats order as uints
 }
 
+// K3 fast path (D % 4 == 0, L <= 32): one thread per point, the CTA's 256 points
+// staged through shared memory in 64-feature chunks with cp.async double
+// buffering; the direction rows are read as 16-byte broadcasts. FFMA-bound at
+// ~17 x D FMAs per point, close to the HBM time of reading the points once.
+constexpr int kPP = 256;  // points per CTA tile (= threads)
+constexpr int kFC = 32;   // features per chunk
+constexpr int kXS = 36;   // smem row stride (floats): 16-B aligned, 8 rows cover all banks
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int n = valid ? 16 : 0;  // src-size 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int LMAX, bool kExact>
+__global__ void __launch_bounds__(kPP, 2) project_tile_kernel(const float* __restrict__ X, int64_t n, int D,
+                                                              const float* __restrict__ U32, int L,
+                                                              float* __restrict__ P32, unsigned* maxnorm2) {
+  extern __shared__ float smp[];
+  float* su = smp;                      // [L][D]
+  float* xs = smp + ((L * D + 3) & ~3);  // [2][kPP][kXS]
+  for (int i = threadIdx.x; i < L * D; i += blockDim.x) su[i] = U32[i];
+  const int tid = threadIdx.x;
+  const int nch = (D + kFC - 1) / kFC;
+  float wmax = 0.0f;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * kPP; base < n;
+       base += static_cast<int64_t>(gridDim.x) * kPP) {
+    // issue chunk 0
+    auto issue = [&](int c, int buf) {
+      float* dst = xs + buf * kPP * kXS;
+      const int f0 = c * kFC;
+      // kPP rows x (kFC/4) 16-byte pieces, coalesced along the row
+      for (int q = tid; q < kPP * (kFC / 4); q += kPP) {
+        const int r = q / (kFC / 4), v = q % (kFC / 4);
+        const int64_t p = base + r;
+        const int f = f0 + 4 * v;
+        const bool ok = p < n && f < D;
+        cp_async16(dst + r * kXS + 4 * v, ok ? X + p * D + f : X, ok);
+      }
+      cp_async_commit();
+    };
+    float acc[LMAX];
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) acc[l] = 0.0f;
+    float nrm = 0.0f;
+    __syncthreads();  // previous tile's readers are done with both buffers
+    issue(0, 0);
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) {
+        issue(c + 1, (c + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const float* xr = xs + (c & 1) * kPP * kXS + tid * kXS;
+      const int f0 = c * kFC;
+      const int fe = min(kFC, D - f0);
+      for (int f = 0; f < fe; f += 4) {
+        const float4 x4 = *reinterpret_cast<const float4*>(xr + f);
+        nrm = fmaf(x4.x, x4.x, nrm);
+        nrm = fmaf(x4.y, x4.y, nrm);
+        nrm = fmaf(x4.z, x4.z, nrm);
+        nrm = fmaf(x4.w, x4.w, nrm);
+#pragma unroll
+        for (int l = 0; l < LMAX; ++l) {
+          if (kExact || l < L) {
+            const float4 u4 = *reinterpret_cast<const float4*>(su + l * D + f0 + f);
+            float a = acc[l];
+            a = fmaf(x4.x, u4.x, a);
+            a = fmaf(x4.y, u4.y, a);
+            a = fmaf(x4.z, u4.z, a);
+            a = fmaf(x4.w, u4.w, a);
+            acc[l] = a;
+          }
+        }
+      }
+      __syncthreads();  // buffer (c & 1) may be refilled by the next issue
+    }
+    const int64_t p = base + tid;
+    if (p < n) {
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (kExact || l < L) P32[static_cast<int64_t>(l) * n + p] = acc[l];
+      wmax = (isfinite(nrm) && isfinite(wmax)) ? fmaxf(wmax, nrm) : __int_as_float(0x7fffffff);
+    }
+  }
+  // block max of wmax -> one atomic
+  __shared__ unsigned bm;
+  if (tid == 0) bm = 0u;
+  __syncthreads();
+  atomicMax(&bm, __float_as_uint(wmax));
+  __syncthreads();
+  if (tid == 0) atomicMax(maxnorm2, bm);
+}
+
 // ------------------------------------------------------------------ K4 radix select
 __device__ __forceinline__ void round_params(int round, int& shift, unsigned& binmask) {
   if (round == 0) {
@@ -321,14 +422,44 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   count_launch();
   init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, m);
   // K3
-  const size_t psmem = sizeof(float) * L * D;
-  if ((e = cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(psmem))) != cudaSuccess)
-    return e;
-  int64_t pblocks = (n + 7) / 8;
-  if (pblocks > 148 * 8) pblocks = 148 * 8;
-  count_launch();
-  project_kernel<<<static_cast<int>(pblocks), 256, psmem, st>>>(X, n, D, U32, L, b.P32, b.maxnorm2);
+  const size_t tsmem = sizeof(float) * (((L * D + 3) & ~3) + 2 * kPP * kXS);
+  if (D % 4 == 0 && L <= 32 && tsmem <= 200 * 1024) {
+    int64_t tiles = (n + kPP - 1) / kPP;
+    if (tiles > 2 * 148) tiles = 2 * 148;
+    auto launch = [&](auto kern) -> cudaError_t {
+      cudaError_t ee = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(tsmem));
+      if (ee != cudaSuccess) return ee;
+      count_launch();
+      kern<<<static_cast<int>(tiles), kPP, tsmem, st>>>(X, n, D, U32, L, b.P32, b.maxnorm2);
+      return cudaGetLastError();
+    };
+    switch (L) {  // exact direction counts of the BASELINE configs (k+1 = 5, 9, 17) unroll fully
+      case 1: e = launch(project_tile_kernel<1, true>); break;
+      case 5: e = launch(project_tile_kernel<5, true>); break;
+      case 9: e = launch(project_tile_kernel<9, true>); break;
+      case 17: e = launch(project_tile_kernel<17, true>); break;
+      default:
+        if (L <= 8)
+          e = launch(project_tile_kernel<8, false>);
+        else if (L <= 16)
+          e = launch(project_tile_kernel<16, false>);
+        else if (L <= 24)
+          e = launch(project_tile_kernel<24, false>);
+        else
+          e = launch(project_tile_kernel<32, false>);
+    }
+    if (e != cudaSuccess) return e;
+  } else {
+    const size_t psmem = sizeof(float) * L * D;
+    if ((e = cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(psmem))) != cudaSuccess)
+      return e;
+    int64_t pblocks = (n + 7) / 8;
+    if (pblocks > 148 * 8) pblocks = 148 * 8;
+    count_launch();
+    project_kernel<<<static_cast<int>(pblocks), 256, psmem, st>>>(X, n, D, U32, L, b.P32, b.maxnorm2);
+  }
   // K4: three radix rounds
   int64_t hb = (n + 255) / 256;
   if (hb > 148 * 2) hb = 148 * 2;
