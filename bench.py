@@ -14,7 +14,8 @@ ProHD part of the step. Inputs are device-resident and larger than L2
 
 N > 1 (torchrun, one rank per GPU): rows of A are sharded for the exact kernel
 (B replicated, one NCCL MAX all-reduce of the packed key, SURVEY.md §8(e));
-ProHD runs replicated on every rank in this round (not yet sharded).
+ProHD shards the rows of A and B (SUM all-reduce of the moments, all-gather of
+candidate lists and selected rows, MAX all-reduce of the subset-HD keys).
 
 `--impl reference` times the fp64 CPU oracle (oracle/) on a bounded row sample
 of the same workload (the reference arm for this paper-only tier).
@@ -127,10 +128,8 @@ def cpu_baseline(A, B, budget_s: float = 15.0) -> dict:
     """The fp64 oracle's exact-HD row minima on a bounded row sample, host cores."""
     import oracle
     rows_all = datagen.sample_rows(A.shape[0], 4096, seed=7)
-    t0 = time.perf_counter()
-    oracle.row_minima(A, B, rows=rows_all[:8])
-    dt = time.perf_counter() - t0
-    nrows = int(max(8, min(4096, budget_s / max(dt / 8, 1e-6))))
+    per_row = _oracle_seconds_per_row(A, B, rows_all)
+    nrows = int(max(8, min(4096, budget_s / per_row)))
     rows = rows_all[:nrows]
     t0 = time.perf_counter()
     oracle.row_minima(A, B, rows=rows)
@@ -143,6 +142,14 @@ def cpu_baseline(A, B, budget_s: float = 15.0) -> dict:
             "seconds": dt}
 
 
+def _oracle_seconds_per_row(A, B, rows_all) -> float:
+    """Oracle seconds per A-row measured on a 256-row probe (one full row block)."""
+    import oracle
+    t0 = time.perf_counter()
+    oracle.row_minima(A, B, rows=rows_all[:256])
+    return max((time.perf_counter() - t0) / 256, 1e-6)
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args, rank: int, world: int):
     if rank != 0:
@@ -152,10 +159,8 @@ def run_reference(args, rank: int, world: int):
     B = datagen.generate_set(args.config, "B")
     import oracle
     rows_all = datagen.sample_rows(A.shape[0], 4096, seed=11)
-    t0 = time.perf_counter()
-    oracle.row_minima(A, B, rows=rows_all[:4])
-    per_row = (time.perf_counter() - t0) / 4
-    nrows = int(max(4, min(1024, 6.0 / max(per_row, 1e-6))))  # ~6 s of CPU work per step
+    per_row = _oracle_seconds_per_row(A, B, rows_all)
+    nrows = int(max(4, min(1024, 6.0 / per_row)))  # ~6 s of CPU work per step
     times = []
     for s in range(args.warmup + args.steps):
         rows = rows_all[(s * nrows) % 4096:][:nrows]
@@ -187,7 +192,7 @@ def run_ours(args, rank: int, world: int):
     import torch.distributed as tdist
 
     from paper_2511_18207_b200 import Context
-    from paper_2511_18207_b200.dist import cuda_fns, row_range, sharded_directed_hd
+    from paper_2511_18207_b200.dist import CudaPhases, row_range, sharded_directed_hd, sharded_prohd_estimate
 
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
@@ -205,39 +210,34 @@ def run_ours(args, rank: int, world: int):
     ctx = Context(local_rank)
     ctx.enable_timing(True)
     stream = torch.cuda.current_stream(dev)
-    local_fn, witness_fn = cuda_fns(ctx)
+    phases = CudaPhases(ctx)
+    lb, hb = row_range(n, rank, world)  # B rows of this rank for the sharded ProHD
+    B_local = B[lb:hb].contiguous()
+    last_local = {}
 
-    def exact_step():
-        if world == 1:
-            r = ctx.directed_hd(A, B)
-        else:
-            r = sharded_directed_hd(A_local, lo, B, local_fn, witness_fn, device=dev)
-        return r, ctx.last_timings() if world == 1 else ctx.last_timings()
+    def local_fn(A_l, off, Bm):  # K6 on this rank's rows; keep its in-library timings
+        key = ctx.directed_hd_local(A_l, off, Bm)
+        last_local.update(ctx.last_timings())
+        return key
 
     def step():
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
-        est = ctx.prohd_estimate(A, B, k, m)
-        t_est = ctx.last_timings()
+        if world == 1:
+            est = ctx.prohd_estimate(A, B, k, m)
+            t_est = ctx.last_timings()
+        else:
+            est = sharded_prohd_estimate(A_local, lo, n, B_local, lb, n, k, m, phases, device=dev)
+            t_est = None
         ev[1].record(stream)
         if world == 1:
             ex = ctx.directed_hd(A, B)
             t_ex = ctx.last_timings()
         else:
-            t_ex = None
-            ex = sharded_directed_hd(A_local, lo, B, local_fn, witness_fn, device=dev)
-            t_ex = dict(ctx._last_local) if hasattr(ctx, "_last_local") else ctx.last_timings()
+            ex = sharded_directed_hd(A_local, lo, B, local_fn, phases.witness_fn, device=dev)
+            t_ex = dict(last_local)
         ev[2].record(stream)
         return est, ex, t_est, t_ex, ev
-
-    # local timings of the sharded exact step are those of directed_hd_local (last ABI call before the witness)
-    if world > 1:
-        orig_local = local_fn
-
-        def local_fn(A_l, off, Bm):  # noqa: F811
-            key = orig_local(A_l, off, Bm)
-            ctx._last_local = ctx.last_timings()
-            return key
 
     for _ in range(args.warmup):
         step()
@@ -278,9 +278,9 @@ def run_ours(args, rank: int, world: int):
     pk = peaks()
     tf32_peak = pk["bf16_tflops_sustained"] * NOMINAL_TF32_OVER_BF16
     tpp, tsrc = k6_traffic_per_pair(D)
-    launches = sum(r[2]["kernel_launches"] + (r[3]["kernel_launches"] if r[3] else 0) for r in recs)
+    launches = sum((r[2]["kernel_launches"] if r[2] else 0) + (r[3]["kernel_launches"] if r[3] else 0) for r in recs)
     if world > 1:
-        launches = None  # witness kernels on the owner rank only; reported per rank below
+        launches = None  # sharded step: phase calls on every rank plus witness kernels on the owner rank
     # ------------------------------------------------------------ end to end (host buffers through the ABI)
     e2e = None
     if world == 1 and not args.no_e2e:
@@ -307,7 +307,7 @@ def run_ours(args, rank: int, world: int):
         cpu = cpu_baseline(Ah, Bh, budget_s=args.cpu_budget)
     if rank != 0:
         return
-    est_t = recs[-1][2]
+    est_t = recs[-1][2] or {kk: None for kk in ("moments_ms", "eigen_ms", "select_ms", "subset_ms", "total_ms")}
     out = {
         "metric": METRIC, "value": value, "unit": "Gpair/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",

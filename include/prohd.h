@@ -154,6 +154,49 @@ int directed_hd_local(prohd_ctx* ctx, const float* A_local, int64_t nA_local, in
 int directed_hd_witness(prohd_ctx* ctx, const float* a, const float* B, int64_t nB, int32_t D,
                         prohd_directed* out);
 
+/* ------------------------------------------------- sharded ProHD (phase calls)
+ * Alg. 3 with the rows of A and of B split across ranks. The caller
+ * (paper_2511_18207_b200/dist.py) runs the collectives between the calls:
+ *   s = prohd_shift(rank 0's first rows)            -> broadcast s
+ *   prohd_local_moments(own rows, s)                -> all_reduce(SUM)      (C1)
+ *   prohd_directions(reduced moments)               (replicated, deterministic)
+ *   prohd_local_candidates(own rows, global offset) -> all_gather           (C2)
+ *   prohd_merge_union(all lists)                    (replicated)
+ *   prohd_gather_owned(own rows of the union)       -> all_gather           (C3)
+ *   directed_hd_local on a row shard of each subset -> all_reduce(MAX)      (C4)
+ * The merged lists equal the single-GPU lists (same fp64 values, same order).
+ * Workspace: prohd_shard_workspace_bytes(max local rows, max total rows, D, k, m, flags). */
+size_t prohd_shard_workspace_bytes(int64_t n_local_max, int64_t n_total_max, int32_t D, int32_t k,
+                                   int64_t m, uint32_t flags);
+/* Shift s (HOST out, D fp64): fp64 mean of the first min(n, 4096) rows of A and of B. */
+int prohd_shift(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                double* shift_out);
+/* This rank's moments about s (HOST, D fp64): moments_out (DEVICE, 2D + D*D fp64) =
+ * [S_A | S_B | G], S_X = sum (x - s), G = sum over own A and B rows of (p - s)(p - s)^T
+ * (full, row-major). n_local may be 0. */
+int prohd_local_moments(prohd_ctx* ctx, const float* A_local, int64_t nA_local, const float* B_local,
+                        int64_t nB_local, int32_t D, const double* shift, double* moments_out);
+/* Directions from the all-reduced moments (DEVICE) of nA + nB points: dirs_out (DEVICE,
+ * (k+1) x D fp64, row l = direction l, row 0 = centroid axis), *n_dirs_out (HOST). */
+int prohd_directions(prohd_ctx* ctx, const double* moments, int64_t nA, int64_t nB, int32_t D, int32_t k,
+                     const double* shift, double* dirs_out, int32_t* n_dirs_out);
+/* Local top/bottom-m per direction of rows X_local (global rows row_offset + i): lists
+ * (DEVICE, [n_dirs][2 (top, bottom)][m]) of fp64 projection values and GLOBAL indices, in
+ * list order; empty slots have index -1. */
+int prohd_local_candidates(prohd_ctx* ctx, const float* X_local, int64_t n_local, int64_t row_offset,
+                           int32_t D, const double* dirs, int32_t n_dirs, int64_t m,
+                           double* cand_val_out, int64_t* cand_idx_out);
+/* Merge G ranks' lists (DEVICE, [G][n_dirs][2][m]) into the sorted unique union of global
+ * indices (DEVICE out, capacity min(n_total, 2 m n_dirs)); *count_out (HOST). */
+int prohd_merge_union(prohd_ctx* ctx, const double* cand_val, const int64_t* cand_idx, int32_t G,
+                      int32_t n_dirs, int64_t m, int64_t n_total, int64_t* union_out,
+                      int64_t* count_out);
+/* Rows of X_local (DEVICE) whose global index is in the sorted union (DEVICE), in union
+ * order -> rows_out (DEVICE); *first_out = their position in the union, *count_out. */
+int prohd_gather_owned(prohd_ctx* ctx, const float* X_local, int64_t n_local, int64_t row_offset,
+                       int32_t D, const int64_t* union_idx, int64_t union_count, float* rows_out,
+                       int64_t* first_out, int64_t* count_out);
+
 /* ---------------------------------------------------------------- tracing */
 /* Per-phase device times of the LAST call on this context, measured with CUDA
  * events recorded on the context stream around each phase (enable first;

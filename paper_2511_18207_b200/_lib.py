@@ -26,6 +26,8 @@ EXPORTED = [
     "prohd_workspace_bytes", "prohd_set_workspace", "directed_hd", "hausdorff", "directed_hd_rowmin",
     "prohd_estimate", "prohd_estimate_with_dirs", "directed_hd_local", "directed_hd_witness",
     "prohd_enable_timing", "prohd_last_timings",
+    "prohd_shard_workspace_bytes", "prohd_shift", "prohd_local_moments", "prohd_directions",
+    "prohd_local_candidates", "prohd_merge_union", "prohd_gather_owned",
 ]
 
 
@@ -80,10 +82,20 @@ def load() -> C.CDLL:
     lib.directed_hd_local.argtypes = [vp, vp, i64, i64, vp, i64, i32, C.POINTER(C.c_uint64)]
     lib.directed_hd_witness.argtypes = [vp, vp, vp, i64, i32, C.POINTER(Directed)]
     lib.prohd_enable_timing.argtypes = [vp, f]
+    lib.prohd_shard_workspace_bytes.argtypes = [i64, i64, i32, i32, i64, C.c_uint32]
+    lib.prohd_shard_workspace_bytes.restype = C.c_size_t
+    lib.prohd_shift.argtypes = [vp, vp, i64, vp, i64, i32, vp]
+    lib.prohd_local_moments.argtypes = [vp, vp, i64, vp, i64, i32, vp, vp]
+    lib.prohd_directions.argtypes = [vp, vp, i64, i64, i32, i32, vp, vp, C.POINTER(C.c_int32)]
+    lib.prohd_local_candidates.argtypes = [vp, vp, i64, i64, i32, vp, i32, i64, vp, vp]
+    lib.prohd_merge_union.argtypes = [vp, vp, vp, i32, i32, i64, i64, vp, C.POINTER(C.c_int64)]
+    lib.prohd_gather_owned.argtypes = [vp, vp, i64, i64, i32, vp, i64, vp, C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int64)]
     lib.prohd_last_timings.argtypes = [vp, C.POINTER(Timings)]
     for name in EXPORTED:
         fn = getattr(lib, name)
-        if name not in ("prohd_last_error", "prohd_version", "prohd_workspace_bytes"):
+        if name not in ("prohd_last_error", "prohd_version", "prohd_workspace_bytes",
+                        "prohd_shard_workspace_bytes"):
             fn.restype = C.c_int
     _lib = lib
     return lib

@@ -68,6 +68,9 @@ class Context:
     def reserve(self, nA: int, nB: int, D: int, k: int = 0, m: int = 1, host_inputs: bool = False) -> int:
         flags = L.PROHD_WS_HOST_INPUTS if host_inputs else 0
         need = int(self.lib.prohd_workspace_bytes(nA, nB, D, k, m, flags))
+        return self._ensure_ws(need)
+
+    def _ensure_ws(self, need: int) -> int:
         if self._ws is None or self._ws.numel() < need:
             self._ws = None
             torch.cuda.synchronize(self.device)
@@ -176,6 +179,76 @@ class Context:
         self._check(self.lib.directed_hd_witness(self.h, a.data_ptr(), B.data_ptr(), B.shape[0], B.shape[1],
                                                  C.byref(out)))
         return _directed(out)
+
+
+    # ---------------------------------------------------------------- sharded ProHD phases
+    def _shard_ws(self, n_local: int, n_total: int, D: int, k: int, m: int):
+        need = int(self.lib.prohd_shard_workspace_bytes(n_local, n_total, D, k, m, 0))
+        self._ensure_ws(need)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._check(self.lib.prohd_set_stream(self.h, C.c_void_p(stream)))
+
+    def shift(self, A_first, B_first) -> np.ndarray:
+        A, B = _as_points(A_first, "A"), _as_points(B_first, "B")
+        D = A.shape[1]
+        self._shard_ws(max(A.shape[0], B.shape[0]), 1, D, 0, 1)
+        s = np.zeros(D, dtype=np.float64)
+        self._check(self.lib.prohd_shift(self.h, A.data_ptr(), A.shape[0], B.data_ptr(), B.shape[0], D,
+                                         s.ctypes.data))
+        return s
+
+    def local_moments(self, A_local, B_local, shift: np.ndarray) -> torch.Tensor:
+        A, B = _as_points(A_local, "A"), _as_points(B_local, "B")
+        D = A.shape[1]
+        self._shard_ws(max(A.shape[0], B.shape[0]), 1, D, 0, 1)
+        s = np.ascontiguousarray(shift, dtype=np.float64)
+        out = torch.empty(2 * D + D * D, dtype=torch.float64, device=f"cuda:{self.device}")
+        self._check(self.lib.prohd_local_moments(self.h, A.data_ptr() if A.numel() else None, A.shape[0],
+                                                 B.data_ptr() if B.numel() else None, B.shape[0], D,
+                                                 s.ctypes.data, out.data_ptr()))
+        return out
+
+    def directions(self, moments: torch.Tensor, nA: int, nB: int, D: int, k: int, shift: np.ndarray):
+        self._shard_ws(0, 1, D, k, 1)
+        s = np.ascontiguousarray(shift, dtype=np.float64)
+        dirs = torch.zeros(k + 1, D, dtype=torch.float64, device=f"cuda:{self.device}")
+        nd = C.c_int32()
+        self._check(self.lib.prohd_directions(self.h, moments.data_ptr(), nA, nB, D, k, s.ctypes.data,
+                                              dirs.data_ptr(), C.byref(nd)))
+        return dirs[: nd.value].contiguous(), int(nd.value)
+
+    def local_candidates(self, X_local, row_offset: int, dirs: torch.Tensor, m: int):
+        X = _as_points(X_local, "X")
+        n_dirs, D = dirs.shape
+        self._shard_ws(X.shape[0], 1, D, n_dirs - 1, m)
+        val = torch.empty(n_dirs, 2, m, dtype=torch.float64, device=f"cuda:{self.device}")
+        idx = torch.empty(n_dirs, 2, m, dtype=torch.int64, device=f"cuda:{self.device}")
+        self._check(self.lib.prohd_local_candidates(self.h, X.data_ptr() if X.numel() else None, X.shape[0],
+                                                    int(row_offset), D, dirs.data_ptr(), n_dirs, m,
+                                                    val.data_ptr(), idx.data_ptr()))
+        return val, idx
+
+    def merge_union(self, vals: torch.Tensor, idxs: torch.Tensor, m: int, n_total: int) -> torch.Tensor:
+        G, n_dirs = vals.shape[0], vals.shape[1]
+        self._shard_ws(0, n_total, 1, n_dirs - 1, 1)
+        cap = min(n_total, 2 * m * n_dirs)
+        out = torch.empty(max(cap, 1), dtype=torch.int64, device=f"cuda:{self.device}")
+        cnt = C.c_int64()
+        self._check(self.lib.prohd_merge_union(self.h, vals.contiguous().data_ptr(), idxs.contiguous().data_ptr(),
+                                               G, n_dirs, m, n_total, out.data_ptr(), C.byref(cnt)))
+        return out[: cnt.value]
+
+    def gather_owned(self, X_local, row_offset: int, union: torch.Tensor):
+        X = _as_points(X_local, "X")
+        D = X.shape[1]
+        rows = torch.empty(max(union.numel(), 1), D, dtype=torch.float32, device=f"cuda:{self.device}")
+        first, cnt = C.c_int64(), C.c_int64()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._check(self.lib.prohd_set_stream(self.h, C.c_void_p(stream)))
+        self._check(self.lib.prohd_gather_owned(self.h, X.data_ptr() if X.numel() else None, X.shape[0],
+                                                int(row_offset), D, union.data_ptr(), union.numel(),
+                                                rows.data_ptr(), C.byref(first), C.byref(cnt)))
+        return rows[: cnt.value], int(first.value), int(cnt.value)
 
 
 _default: dict[int, Context] = {}

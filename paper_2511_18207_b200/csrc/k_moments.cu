@@ -239,11 +239,13 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
   const int target = 6 * num_sms;  // CTAs (3 resident per SM)
   int per_pair = (target + p.npairs - 1) / p.npairs;
   if (per_pair < 2) per_pair = 2;
-  const double fa = static_cast<double>(nA) / static_cast<double>(nA + nB);
+  const double fa = (nA + nB) > 0 ? static_cast<double>(nA) / static_cast<double>(nA + nB) : 0.5;
   p.rangesA = static_cast<int>(per_pair * fa + 0.5);
   if (p.rangesA < 1) p.rangesA = 1;
   p.rangesB = per_pair - p.rangesA;
   if (p.rangesB < 1) p.rangesB = 1;
+  if (nA <= 0) p.rangesA = 0;
+  if (nB <= 0) p.rangesB = 0;
   // never more ranges than chunks
   const int64_t ca = (nA + kChunk - 1) / kChunk, cb = (nB + kChunk - 1) / kChunk;
   if (p.rangesA > ca) p.rangesA = static_cast<int>(ca);
@@ -254,26 +256,46 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
   return p;
 }
 
-cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB, int D,
-                           const MomentsBufs& b, cudaStream_t st) {
+cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB, int D, double* s,
+                         cudaStream_t st) {
   count_launch();
-  shift_kernel<<<(D + 255) / 256, 256, 0, st>>>(A, nA, B, nB, D, b.s);
+  shift_kernel<<<(D + 255) / 256, 256, 0, st>>>(A, nA, B, nB, D, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moments_partial(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB,
+                                   int D, const MomentsBufs& b, cudaStream_t st) {
   const size_t smem = sizeof(double) * kMC * kLds;
   cudaError_t e = cudaFuncSetAttribute(moments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  MomArgs a{A, nA, D, b.s, p.nb, 0, p.rangesA, p.nslots, b.Gpart, b.Spart};
+  if (nA > 0 && p.rangesA > 0) {
+    MomArgs a{A, nA, D, b.s, p.nb, 0, p.rangesA, p.nslots, b.Gpart, b.Spart};
+    count_launch();
+    moments_kernel<<<dim3(p.npairs, p.rangesA), kMT, smem, st>>>(a);
+  }
+  if (nB > 0 && p.rangesB > 0) {
+    MomArgs bb{B, nB, D, b.s, p.nb, p.rangesA, p.rangesB, p.nslots, b.Gpart, b.Spart};
+    count_launch();
+    moments_kernel<<<dim3(p.npairs, p.rangesB), kMT, smem, st>>>(bb);
+  }
   count_launch();
-  moments_kernel<<<dim3(p.npairs, p.rangesA), kMT, smem, st>>>(a);
-  MomArgs bb{B, nB, D, b.s, p.nb, p.rangesA, p.rangesB, p.nslots, b.Gpart, b.Spart};
-  count_launch();
-  moments_kernel<<<dim3(p.npairs, p.rangesB), kMT, smem, st>>>(bb);
-  count_launch();
-  moments_reduce_kernel<<<148 * 2, 256, 0, st>>>(b.Gpart, b.Spart, p.nb, D, p.rangesA, p.nslots, b.C, b.SA,
-                                                 b.SB);
+  moments_reduce_kernel<<<148 * 2, 256, 0, st>>>(b.Gpart, b.Spart, p.nb, D, p.rangesA, p.nslots, b.C, b.SA, b.SB);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moments_finalize(int64_t nA, int64_t nB, int D, const MomentsBufs& b, cudaStream_t st) {
   count_launch();
   moments_finalize_kernel<<<1, 256, 0, st>>>(b.C, b.SA, b.SB, b.s, nA, nB, D, b.mu, b.u0, b.dnorm);
   return cudaGetLastError();
+}
+
+cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB, int D,
+                           const MomentsBufs& b, cudaStream_t st) {
+  cudaError_t e = launch_shift(A, nA, B, nB, D, b.s, st);
+  if (e != cudaSuccess) return e;
+  if ((e = launch_moments_partial(p, A, nA, B, nB, D, b, st)) != cudaSuccess) return e;
+  return launch_moments_finalize(nA, nB, D, b, st);
 }
 
 }  // namespace prohd

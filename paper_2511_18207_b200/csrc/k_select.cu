@@ -252,14 +252,15 @@ __global__ void radix_scan_kernel(const unsigned* __restrict__ hist, int L, cons
 __global__ void __launch_bounds__(256) collect_kernel(const float* __restrict__ P32, int64_t n, int D, int L,
                                                       const int* n_dirs, const unsigned* __restrict__ state,
                                                       const unsigned* maxnorm2, int* cand, unsigned* ccount,
-                                                      int64_t cap, int* overflow) {
+                                                      int64_t cap, int* overflow, int all) {
   const int l = blockIdx.y;
   if (l >= *n_dirs) return;
   const double eps = (D + 8) * 0x1p-24 * sqrt(static_cast<double>(__uint_as_float(*maxnorm2))) * 1.0625;
   const double Ttop = static_cast<double>(key_to_float(state[(l * 2 + 0) * 4 + 0]));
   const double Tbot = static_cast<double>(key_to_float(~state[(l * 2 + 1) * 4 + 0]));
-  const double lo_top = Ttop - 2.0 * eps;  // top candidates: pi >= lo_top
-  const double hi_bot = Tbot + 2.0 * eps;  // bottom candidates: pi <= hi_bot
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const double lo_top = all ? -inf : Ttop - 2.0 * eps;  // top candidates: pi >= lo_top
+  const double hi_bot = all ? inf : Tbot + 2.0 * eps;   // bottom candidates: pi <= hi_bot
   const float* p = P32 + static_cast<int64_t>(l) * n;
   const int lane = threadIdx.x & 31;
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n;
@@ -313,7 +314,8 @@ __global__ void __launch_bounds__(256) cand_p64_kernel(const float* __restrict__
 // rank of each candidate in its (direction, tail) total order; keep rank < m
 __global__ void __launch_bounds__(256) rank_kernel(int L, const int* n_dirs, const int* __restrict__ cand,
                                                    const double* __restrict__ cval, const unsigned* ccount,
-                                                   int64_t cap, int64_t m, int* lists, unsigned* bitmap) {
+                                                   int64_t cap, int64_t m, int* lists, unsigned* bitmap,
+                                                   double* cv_out, long long* ci_out, int64_t row_offset) {
   const int lt = blockIdx.y;
   const int l = lt >> 1, t = lt & 1;
   if (l >= *n_dirs) return;
@@ -332,8 +334,12 @@ __global__ void __launch_bounds__(256) rank_kernel(int L, const int* n_dirs, con
       rank += better ? 1 : 0;
     }
     if (rank < m) {
-      lists[static_cast<int64_t>(lt) * m + rank] = i;
-      atomicOr(&bitmap[i >> 5], 1u << (i & 31));
+      if (lists != nullptr) lists[static_cast<int64_t>(lt) * m + rank] = i;
+      if (bitmap != nullptr) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
+      if (cv_out != nullptr) {
+        cv_out[static_cast<int64_t>(lt) * m + rank] = v;
+        ci_out[static_cast<int64_t>(lt) * m + rank] = row_offset + i;
+      }
     }
   }
 }
@@ -388,6 +394,48 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ X
   }
 }
 
+// merge: rank every entry of list (l, t) among the G*m entries of all ranks; keep rank < m
+__global__ void __launch_bounds__(256) merge_rank_kernel(const double* __restrict__ cval,
+                                                         const long long* __restrict__ cidx, int G, int L,
+                                                         const int* n_dirs, int64_t m, unsigned* bitmap) {
+  const int lt = blockIdx.y;
+  const int l = lt >> 1, t = lt & 1;
+  if (l >= *n_dirs) return;
+  const int64_t tot = static_cast<int64_t>(G) * m;
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < tot;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t gc = c / m, jc = c % m;
+    const int64_t off = (gc * L * 2 + lt) * m;
+    const long long i = cidx[off + jc];
+    if (i < 0) continue;
+    const double v = cval[off + jc];
+    int64_t rank = 0;
+    for (int64_t o = 0; o < tot && rank < m; ++o) {
+      const int64_t go = o / m, jo = o % m;
+      const int64_t oo = (go * L * 2 + lt) * m + jo;
+      const long long j = cidx[oo];
+      if (j < 0) continue;
+      const double w = cval[oo];
+      const bool better = (t == 0) ? (w > v || (w == v && j < i)) : (w < v || (w == v && j < i));
+      rank += better ? 1 : 0;
+    }
+    if (rank < m) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
+  }
+}
+
+__global__ void __launch_bounds__(256) gather_offset_kernel(const float* __restrict__ X, int D,
+                                                            const long long* __restrict__ idx, int64_t lo,
+                                                            int64_t cnt, int64_t row_offset,
+                                                            float* __restrict__ Y) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < cnt;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const float* src = X + (idx[lo + r] - row_offset) * D;
+    float* dst = Y + r * D;
+    for (int c = lane; c < D; c += 32) dst[c] = __ldg(src + c);
+  }
+}
+
 __global__ void dirs_to_f32_kernel(const double* U64, float* U32, int total) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
     U32[i] = static_cast<float>(U64[i]);
@@ -411,17 +459,9 @@ cudaError_t launch_dirs_to_f32(const double* U64, float* U32, int rows, int D, c
   return cudaGetLastError();
 }
 
-cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
-                          const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st) {
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(b.maxnorm2, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(b.hist, 0, sizeof(unsigned) * 3 * L * 2 * kRadixBins, st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(b.ccount, 0, sizeof(unsigned) * 2 * L, st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(b.bitmap, 0, sizeof(unsigned) * ((n + 31) / 32), st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(b.overflow, 0, sizeof(int), st)) != cudaSuccess) return e;
-  count_launch();
-  init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, m);
-  // K3
+static cudaError_t launch_project(const float* X, int64_t n, int D, const float* U32, int L, float* P32,
+                                  unsigned* maxnorm2, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
   const size_t tsmem = sizeof(float) * (((L * D + 3) & ~3) + 2 * kPP * kXS);
   if (D % 4 == 0 && L <= 32 && tsmem <= 200 * 1024) {
     int64_t tiles = (n + kPP - 1) / kPP;
@@ -431,7 +471,7 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
                                             static_cast<int>(tsmem));
       if (ee != cudaSuccess) return ee;
       count_launch();
-      kern<<<static_cast<int>(tiles), kPP, tsmem, st>>>(X, n, D, U32, L, b.P32, b.maxnorm2);
+      kern<<<static_cast<int>(tiles), kPP, tsmem, st>>>(X, n, D, U32, L, P32, maxnorm2);
       return cudaGetLastError();
     };
     switch (L) {  // exact direction counts of the BASELINE configs (k+1 = 5, 9, 17) unroll fully
@@ -458,8 +498,23 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
     int64_t pblocks = (n + 7) / 8;
     if (pblocks > 148 * 8) pblocks = 148 * 8;
     count_launch();
-    project_kernel<<<static_cast<int>(pblocks), 256, psmem, st>>>(X, n, D, U32, L, b.P32, b.maxnorm2);
+    project_kernel<<<static_cast<int>(pblocks), 256, psmem, st>>>(X, n, D, U32, L, P32, maxnorm2);
   }
+  return e;
+}
+
+cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
+                          const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(b.maxnorm2, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.hist, 0, sizeof(unsigned) * 3 * L * 2 * kRadixBins, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.ccount, 0, sizeof(unsigned) * 2 * L, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.bitmap, 0, sizeof(unsigned) * ((n + 31) / 32), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.overflow, 0, sizeof(int), st)) != cudaSuccess) return e;
+  count_launch();
+  init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, m);
+  // K3
+  if ((e = launch_project(X, n, D, U32, L, b.P32, b.maxnorm2, st)) != cudaSuccess) return e;
   // K4: three radix rounds
   int64_t hb = (n + 255) / 256;
   if (hb > 148 * 2) hb = 148 * 2;
@@ -471,14 +526,73 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   }
   count_launch();
   collect_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, D, L, n_dirs, b.state, b.maxnorm2,
-                                                                     b.cand, b.ccount, b.cap, b.overflow);
+                                                                     b.cand, b.ccount, b.cap, b.overflow, 0);
   count_launch();
   cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
   count_launch();
-  rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap);
+  rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap,
+                                              nullptr, nullptr, 0);
   // K5
   count_launch();
   compact_kernel<<<1, 1024, 0, st>>>(b.bitmap, (n + 31) / 32, b.uidx, b.ucount);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offset, int D, const double* U64,
+                                    const float* U32, int L, const int* n_dirs, int64_t m, const SelectBufs& b,
+                                    double* cval_out, long long* cidx_out, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(cidx_out, 0xFF, sizeof(long long) * L * 2 * m, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(cval_out, 0, sizeof(double) * L * 2 * m, st)) != cudaSuccess) return e;
+  if (n <= 0) return cudaSuccess;
+  if ((e = cudaMemsetAsync(b.maxnorm2, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.hist, 0, sizeof(unsigned) * 3 * L * 2 * kRadixBins, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.ccount, 0, sizeof(unsigned) * 2 * L, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.overflow, 0, sizeof(int), st)) != cudaSuccess) return e;
+  const bool all = m >= n;
+  count_launch();
+  init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, all ? 1 : m);
+  if ((e = launch_project(X, n, D, U32, L, b.P32, b.maxnorm2, st)) != cudaSuccess) return e;
+  int64_t hb = (n + 255) / 256;
+  if (hb > 148 * 2) hb = 148 * 2;
+  if (!all) {
+    for (int r = 0; r < 3; ++r) {
+      count_launch();
+      radix_hist_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, L, n_dirs, r, b.state, b.hist);
+      count_launch();
+      radix_scan_kernel<<<(2 * L + 63) / 64, 64, 0, st>>>(b.hist, L, n_dirs, r, b.state);
+    }
+  }
+  count_launch();
+  collect_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, D, L, n_dirs, b.state, b.maxnorm2,
+                                                                     b.cand, b.ccount, b.cap, b.overflow, all ? 1 : 0);
+  count_launch();
+  cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
+  count_launch();
+  rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, nullptr, nullptr,
+                                              cval_out, cidx_out, row_offset);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_union(const double* cval, const long long* cidx, int G, int L, int64_t m, int64_t n_total,
+                               unsigned* bitmap, long long* uidx, unsigned* ucount, const int* n_dirs,
+                               cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(bitmap, 0, sizeof(unsigned) * ((n_total + 31) / 32), st);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  merge_rank_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(cval, cidx, G, L, n_dirs, m, bitmap);
+  count_launch();
+  compact_kernel<<<1, 1024, 0, st>>>(bitmap, (n_total + 31) / 32, uidx, ucount);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_offset(const float* X, int D, const long long* idx, int64_t lo, int64_t cnt,
+                                 int64_t row_offset, float* rows_out, cudaStream_t st) {
+  if (cnt <= 0) return cudaSuccess;
+  int64_t blocks = (cnt + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  count_launch();
+  gather_offset_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(X, D, idx, lo, cnt, row_offset, rows_out);
   return cudaGetLastError();
 }
 

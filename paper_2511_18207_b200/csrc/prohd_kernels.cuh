@@ -26,6 +26,12 @@ struct MomentsBufs {
 MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms);
 cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB, int D,
                            const MomentsBufs& b, cudaStream_t st);
+// pieces of launch_moments (sharded path): shift s from the first <= 4096 rows of A and B;
+// partial sums about b.s (-> b.SA, b.SB, b.C = G); finalize (mu, u0, C from the sums).
+cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB, int D, double* s, cudaStream_t st);
+cudaError_t launch_moments_partial(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB,
+                                   int D, const MomentsBufs& b, cudaStream_t st);
+cudaError_t launch_moments_finalize(int64_t nA, int64_t nB, int D, const MomentsBufs& b, cudaStream_t st);
 
 // ---------------------------------------------------------------- K2
 // Top-k eigenvectors of C (destroyed). Writes rows 1..k of out64/out32 ([k+1][D]),
@@ -54,6 +60,20 @@ struct SelectBufs {
 };
 cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
                           const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st);
+// Sharded selection: local top/bottom-m lists with their fp64 projection values and GLOBAL
+// indices (row_offset + local row) -> cval_out/cidx_out [L][2][m] (index -1 = empty slot).
+// If m >= n every local point is a candidate of every list.
+cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offset, int D, const double* U64,
+                                    const float* U32, int L, const int* n_dirs, int64_t m, const SelectBufs& b,
+                                    double* cval_out, long long* cidx_out, cudaStream_t st);
+// Merge G ranks' lists [G][L][2][m] into the global top/bottom-m per list (same total
+// order) and the sorted unique union of their global indices (bitmap over n_total rows).
+cudaError_t launch_merge_union(const double* cval, const long long* cidx, int G, int L, int64_t m, int64_t n_total,
+                               unsigned* bitmap, long long* uidx, unsigned* ucount, const int* n_dirs,
+                               cudaStream_t st);
+// rows_out[i] = X_local[idx[lo + i] - row_offset] for i < cnt
+cudaError_t launch_gather_offset(const float* X, int D, const long long* idx, int64_t lo, int64_t cnt,
+                                 int64_t row_offset, float* rows_out, cudaStream_t st);
 // Gather rows X[idx[i]] -> Y (row-major, stride D) for i < count (count on the device).
 cudaError_t launch_gather(const float* X, int D, const long long* idx, const unsigned* count, int64_t cap,
                           float* Y, cudaStream_t st);

@@ -46,7 +46,7 @@ def sharded_directed_hd(A_local, row_offset: int, B, local_fn, witness_fn, devic
     local_fn(A_local, row_offset, B) -> packed key of this shard (int)
     witness_fn(a_row, B) -> {"b": int, "dist2": float} (fp64 nearest neighbour)
     """
-    key = int(local_fn(A_local, row_offset, B))
+    key = int(local_fn(A_local, row_offset, B)) if A_local.shape[0] > 0 else 0  # empty shard: no candidate
     t = torch.tensor([key], dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     gkey = int(t.item())
@@ -62,6 +62,96 @@ def sharded_directed_hd(A_local, row_offset: int, B, local_fn, witness_fn, devic
     b = int(w[0].item()) - 1
     d2 = float(w[1].item())
     return {"dist": float(np.sqrt(d2)), "dist2": d2, "a": row, "b": b, "dist2_tc": d2_tc, "key": gkey}
+
+
+def _all_gather_rows(rows: torch.Tensor, D: int, device, group=None) -> torch.Tensor:
+    """Concatenate every rank's rows (variable counts) in rank order (C3)."""
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([rows.shape[0]], dtype=torch.int64, device=device)
+    cnts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt, group=group)
+    cnts = [int(c.item()) for c in cnts]
+    mx = max(max(cnts), 1)
+    pad = torch.zeros(mx, D, dtype=rows.dtype, device=device)
+    pad[: rows.shape[0]] = rows
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([b[:c] for b, c in zip(bufs, cnts)], dim=0).contiguous()
+
+
+def sharded_prohd_estimate(A_local, offA: int, nA: int, B_local, offB: int, nB: int, k: int, m: int,
+                           phases, device=None, group=None) -> dict:
+    """Alg. 3 with the rows of A and B sharded across the group.
+
+    Rank r holds rows [offA, offA + len(A_local)) of A and [offB, ...) of B (contiguous
+    blocks in rank order; rank 0 starts at row 0). `phases` provides the per-rank compute
+    (CUDA: `CudaPhases(ctx)`): shift, local_moments, directions, local_candidates,
+    merge_union, gather_owned, local_fn, witness_fn. Collectives: broadcast of the shift,
+    C1 SUM all-reduce of the moments, C2 all-gather of the candidate lists, C3 all-gather
+    of the selected rows, C4 MAX all-reduce of the subset-HD keys.
+    """
+    rank = dist.get_rank(group)
+    D = A_local.shape[1]
+    # shift from the first <= 4096 rows (owned by rank 0), broadcast
+    s = torch.zeros(D, dtype=torch.float64, device=device)
+    if rank == 0:
+        s.copy_(torch.as_tensor(phases.shift(A_local[:4096], B_local[:4096])))
+    dist.broadcast(s, src=0, group=group)
+    s_np = s.cpu().numpy()
+    # C1: moments
+    mom = phases.local_moments(A_local, B_local, s_np)
+    dist.all_reduce(mom, op=dist.ReduceOp.SUM, group=group)
+    dirs, n_dirs = phases.directions(mom, nA, nB, D, k, s_np)
+    # C2 + merge + C3 per set
+    world = dist.get_world_size(group)
+    unions, subsets = [], []
+    for X_local, off, n in ((A_local, offA, nA), (B_local, offB, nB)):
+        val, idx = phases.local_candidates(X_local, off, dirs, m)
+        vals = [torch.empty_like(val) for _ in range(world)]
+        idxs = [torch.empty_like(idx) for _ in range(world)]
+        dist.all_gather(vals, val, group=group)
+        dist.all_gather(idxs, idx, group=group)
+        union = phases.merge_union(torch.stack(vals), torch.stack(idxs), m, n)
+        rows, _, _ = phases.gather_owned(X_local, off, union)
+        subsets.append(_all_gather_rows(rows, D, device, group))
+        unions.append(union)
+    # C4: exact HD on the subsets, rows of each subset sharded over the ranks
+    res = {}
+    for side, (R, Cm, uR, uC) in {"ab": (subsets[0], subsets[1], unions[0], unions[1]),
+                                  "ba": (subsets[1], subsets[0], unions[1], unions[0])}.items():
+        lo, hi = row_range(R.shape[0], rank, world)
+        r = sharded_directed_hd(R[lo:hi], lo, Cm, phases.local_fn, phases.witness_fn, device=device, group=group)
+        res[side] = {**r, "a": int(uR[r["a"]].item()), "b": int(uC[r["b"]].item())}
+    ab, ba = res["ab"], res["ba"]
+    value = ab["dist"] if ab["dist2"] >= ba["dist2"] else ba["dist"]
+    return {"value": value, "ab": ab, "ba": ba, "size_a": int(unions[0].numel()),
+            "size_b": int(unions[1].numel()), "n_dirs": n_dirs, "IA": unions[0], "IB": unions[1], "U": dirs}
+
+
+class CudaPhases:
+    """The product phase implementations: every step runs in libprohd.so kernels."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.local_fn, self.witness_fn = cuda_fns(ctx)
+
+    def shift(self, A_first, B_first):
+        return self.ctx.shift(A_first, B_first)
+
+    def local_moments(self, A_local, B_local, s):
+        return self.ctx.local_moments(A_local, B_local, s)
+
+    def directions(self, moments, nA, nB, D, k, s):
+        return self.ctx.directions(moments, nA, nB, D, k, s)
+
+    def local_candidates(self, X_local, off, dirs, m):
+        return self.ctx.local_candidates(X_local, off, dirs, m)
+
+    def merge_union(self, vals, idxs, m, n):
+        return self.ctx.merge_union(vals, idxs, m, n)
+
+    def gather_owned(self, X_local, off, union):
+        return self.ctx.gather_owned(X_local, off, union)
 
 
 def cuda_fns(ctx):

@@ -1,0 +1,89 @@
+"""The sharded-ProHD phase calls on one GPU: G row shards simulated in sequence (the sums,
+concatenations and maxima stand in for the NCCL collectives), compared with the one-shot
+prohd_estimate and with the oracle. Also: exact HD via directed_hd_local on row shards is
+bit-identical to the unsharded call (GPU-count invariance of the packed key)."""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+from oracle import prohd as OP
+from paper_2511_18207_b200.dist import CudaPhases, row_range, unpack_key
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2511_18207_b200 import Context
+    return Context(0)
+
+
+def _sim_sharded(ctx, A, B, k, m, G):
+    ph = CudaPhases(ctx)
+    nA, nB, D = A.shape[0], B.shape[0], A.shape[1]
+    la = [row_range(nA, g, G) for g in range(G)]
+    lb = [row_range(nB, g, G) for g in range(G)]
+    s = ph.shift(A[:4096], B[:4096])
+    mom = None
+    for g in range(G):
+        part = ph.local_moments(A[la[g][0]:la[g][1]], B[lb[g][0]:lb[g][1]], s)
+        mom = part if mom is None else mom + part
+    dirs, nd = ph.directions(mom, nA, nB, D, k, s)
+    unions, subsets = [], []
+    for X, rng in ((A, la), (B, lb)):
+        lists = [ph.local_candidates(X[lo:hi], lo, dirs, m) for lo, hi in rng]
+        union = ph.merge_union(torch.stack([v for v, _ in lists]), torch.stack([i for _, i in lists]), m,
+                               X.shape[0])
+        rows = torch.cat([ph.gather_owned(X[lo:hi], lo, union)[0] for lo, hi in rng])
+        unions.append(union)
+        subsets.append(rows)
+    out = {}
+    for side, (R, Cm, uR, uC) in {"ab": (subsets[0], subsets[1], unions[0], unions[1]),
+                                  "ba": (subsets[1], subsets[0], unions[1], unions[0])}.items():
+        keys = []
+        for g in range(G):
+            lo, hi = row_range(R.shape[0], g, G)
+            if hi > lo:
+                keys.append(ctx.directed_hd_local(R[lo:hi], lo, Cm))
+        key = max(keys)
+        _, row = unpack_key(key)
+        w = ctx.directed_hd_witness(R[row], Cm)
+        out[side] = {"a": int(uR[row]), "b": int(uC[w["b"]]), "dist2": w["dist2"]}
+    value = float(np.sqrt(max(out["ab"]["dist2"], out["ba"]["dist2"])))
+    return {"value": value, "IA": unions[0].cpu().numpy(), "IB": unions[1].cpu().numpy(), "U": dirs.cpu().numpy(),
+            "n_dirs": nd, **out}
+
+
+@pytest.mark.parametrize("cfg,n,G", [(1, None, 2), (2, 20000, 3), (5, 65536, 2), (4, 65536, 4)])
+def test_sharded_phases_equal_single(ctx, cfg, n, G):
+    c = datagen.CONFIGS[cfg]
+    A, B = datagen.generate(cfg, n=n)
+    m = c.m(A.shape[0])
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    one = ctx.prohd_estimate(At, Bt, c.k, m, return_dirs=True, return_indices=True)
+    sh = _sim_sharded(ctx, At, Bt, c.k, m, G)
+    assert sh["n_dirs"] == one["n_dirs"]
+    assert np.allclose(sh["U"].T, one["U"], rtol=0, atol=1e-12)
+    assert np.array_equal(sh["IA"], one["IA"]) and np.array_equal(sh["IB"], one["IB"])
+    assert sh["value"] == one["value"]
+    assert (sh["ab"]["a"], sh["ab"]["b"]) == (one["ab"]["a"], one["ab"]["b"])
+    assert (sh["ba"]["a"], sh["ba"]["b"]) == (one["ba"]["a"], one["ba"]["b"])
+    ref = OP.estimate(A, B, c.k, m)
+    assert np.array_equal(sh["IA"], ref["IA"]) and np.array_equal(sh["IB"], ref["IB"])
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_exact_key_invariant_to_shard_count(ctx, G):
+    A, B = datagen.generate(2, n=30000)
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    one = ctx.directed_hd(At, Bt)
+    keys = []
+    for g in range(G):
+        lo, hi = row_range(A.shape[0], g, G)
+        keys.append(ctx.directed_hd_local(At[lo:hi], lo, Bt))
+    key = max(keys)
+    d2, row = unpack_key(key)
+    assert row == one["a"] and np.float32(d2) == np.float32(one["dist2_tc"])
+    w = ctx.directed_hd_witness(At[row], Bt)
+    assert w["b"] == one["b"] and w["dist2"] == one["dist2"]
