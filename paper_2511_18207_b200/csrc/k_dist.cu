@@ -413,15 +413,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-// Variant by D (measured r01, tools/time_exact.py): the 2-SM pair wins where the kernel is
-// operand-bandwidth bound (D=256: 507 vs 464 Gpair/s); at D <= 128 the row-min epilogue
-// dominates and coupling two CTAs' epilogues costs more than the operand saving
-// (D=128: 882 vs 926, D=64: 1010 vs 1125). PROHD_K6_VARIANT=1sm|2sm overrides (A/B testing).
+// Variant (measured r01 on one B200): in 30-40 ms runs the 2-SM pair is faster at D=256
+// (507 vs 464 Gpair/s, tools/time_exact.py) but slower at D <= 128 (epilogue-bound). In the
+// sustained, power-capped regime of the benchmark (8 s launches at cfg5) the pair drops to a
+// 1425 MHz median SM clock against 1575 MHz for the single-CTA kernel and loses
+// (474 vs 491 Gpair/s, same box, alternated twice): it is faster per clock but spends more
+// energy per pair. The single-CTA kernel is therefore the default for every D;
+// PROHD_K6_VARIANT=2sm selects the pair (A/B testing).
 static int dist_variant(int D) {
+  (void)D;
   const char* e = getenv("PROHD_K6_VARIANT");
-  if (e != nullptr && e[0] == '1') return 1;
   if (e != nullptr && e[0] == '2') return 2;
-  return D >= 192 ? 2 : 1;
+  return 1;
 }
 
 int dist_b_box_rows(int D) { return dist_variant(D) == 2 ? 128 : kBN; }
