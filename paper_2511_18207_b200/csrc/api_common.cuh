@@ -109,6 +109,7 @@ struct ExactWs {
   float* stageB = nullptr;
   SetOps A, B;
   float* rowmin = nullptr;
+  float* colmin = nullptr;
   unsigned long long* keys = nullptr;  // [2]
   double* nn_d = nullptr;              // [2]
   long long* nn_j = nullptr;           // [2]
@@ -133,6 +134,7 @@ inline size_t carve_exact(Carver& c, ExactWs& w, int64_t nA, int64_t nB, int D, 
   carve_set(c, w.A, nA, D);
   carve_set(c, w.B, nB, D);
   w.rowmin = c.take<float>(nA > nB ? nA : nB);
+  w.colmin = c.take<float>(nA > nB ? nA : nB);
   w.keys = c.take<unsigned long long>(2);
   w.nn_d = c.take<double>(2);
   w.nn_j = c.take<long long>(2);
@@ -263,14 +265,15 @@ inline int prep_set(prohd_ctx* ctx, const float* X, int64_t n, int D, SetOps& s,
 }
 
 // rows of `R` against columns of `C` -> rowmin (device)
-inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, float* rowmin) {
+inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, float* rowmin,
+                    float* colmin = nullptr) {
   CUtensorMap maps[4];
   char err[256];
   const int Dp = pad_dim(D);
   if (!make_tmap_2d(&maps[0], R.hi, R.n, Dp, kBM, err, sizeof err) ||
       !make_tmap_2d(&maps[1], R.lo, R.n, Dp, kBM, err, sizeof err) ||
-      !make_tmap_2d(&maps[2], C.hi, C.n, Dp, dist_b_box_rows(D), err, sizeof err) ||
-      !make_tmap_2d(&maps[3], C.lo, C.n, Dp, dist_b_box_rows(D), err, sizeof err))
+      !make_tmap_2d(&maps[2], C.hi, C.n, Dp, dist_b_box_rows(D, colmin != nullptr), err, sizeof err) ||
+      !make_tmap_2d(&maps[3], C.lo, C.n, Dp, dist_b_box_rows(D, colmin != nullptr), err, sizeof err))
     return fail(ctx, PROHD_E_CUDA, "%s", err);
   DistArgs a;
   a.maps = maps;
@@ -281,6 +284,7 @@ inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, flo
   a.nb = C.norms;
   a.rowmin = rowmin;
   a.num_sms = ctx->num_sms;
+  a.colmin = colmin;
   const int t0 = tmark(ctx);
   CK(launch_dist_rowmin(a, ctx->stream));
   tspan(ctx, PH_DIST, t0);
@@ -295,6 +299,22 @@ inline int directed_on_ops(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int
   CK(launch_rowmax_key(w.rowmin, R.n, 0, &w.keys[slot], ctx->stream));
   CK(launch_nn64_from_key(R.x, 0, R.n, &w.keys[slot], C.x, C.n, D, w.blk_d, w.blk_j, kNNBlocks, &w.nn_d[slot],
                           &w.nn_j[slot], ctx->stream));
+  tspan(ctx, PH_REDUCE, t0);
+  return PROHD_OK;
+}
+
+// h(R, C) and h(C, R) from ONE fused bidirectional sweep: slot 0 is
+// R -> C (row minima), slot 1 is C -> R (column minima).
+inline int bidir_on_ops(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, ExactWs& w) {
+  int rc = run_dist(ctx, R, C, D, w.rowmin, w.colmin);
+  if (rc) return rc;
+  const int t0 = tmark(ctx);
+  CK(launch_rowmax_key(w.rowmin, R.n, 0, &w.keys[0], ctx->stream));
+  CK(launch_rowmax_key(w.colmin, C.n, 0, &w.keys[1], ctx->stream));
+  CK(launch_nn64_from_key(R.x, 0, R.n, &w.keys[0], C.x, C.n, D, w.blk_d, w.blk_j, kNNBlocks, &w.nn_d[0],
+                          &w.nn_j[0], ctx->stream));
+  CK(launch_nn64_from_key(C.x, 0, C.n, &w.keys[1], R.x, R.n, D, w.blk_d, w.blk_j, kNNBlocks, &w.nn_d[1],
+                          &w.nn_j[1], ctx->stream));
   tspan(ctx, PH_REDUCE, t0);
   return PROHD_OK;
 }

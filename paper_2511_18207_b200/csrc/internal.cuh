@@ -39,11 +39,12 @@ struct DistArgs {
   const float* nb;  // column-operand norms, padded to a multiple of kBN with +inf
   float* rowmin;    // out: min_j d2(i, j), clamped >= 0
   int num_sms;
+  float* colmin = nullptr;  // optional out (fused bidirectional pass): min_i d2(i, j), clamped >= 0
 };
 // K6: fused 3xTF32 tcgen05 distance + row-min kernel.
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st);
 // rows per TMA box of the column operand for the selected K6 variant (256: 1-SM, 128: 2-SM pair)
-int dist_b_box_rows(int D);
+int dist_b_box_rows(int D, bool bidir);
 
 // K7a: packed max key over rows: (bits(d2) << 32) | (0xFFFFFFFF - (row + row_offset)).
 cudaError_t launch_rowmax_key(const float* rowmin, int64_t n, int64_t row_offset, unsigned long long* key,

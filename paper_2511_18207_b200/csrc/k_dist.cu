@@ -49,10 +49,31 @@ struct Sched {
   int atomic_out;
 };
 
+// butterfly reduce-scatter: lane L ends with min over the warp's 32 lanes of v[L] in v[0]
+__device__ __forceinline__ void warp_colmin32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const float send = up ? v[i] : v[i + s];
+      const float keep = up ? v[i + s] : v[i];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, s);
+      v[i] = fminf(keep, recv);
+    }
+  }
+}
+
+// kBidir: the same sweep also produces column minima
+// colmin[j] = min_i ||a_i - b_j||^2 (the B->A direction). Per 32-column chunk each warp
+// reduces its 32 rows with a butterfly reduce-scatter, the 4 warps combine in shared
+// memory, and the last warp of the tile flushes the 256 minima with global atomicMin.
+template <bool kBidir>
 __global__ void __launch_bounds__(kThreads, 1)
     dist_rowmin_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                        const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
-                       const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin) {
+                       const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin,
+                       float* __restrict__ colmin) {
   using namespace sm100;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -61,9 +82,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ unsigned colbuf[2][kBN];  // kBidir: per-accumulator column minima (float bits)
+  __shared__ unsigned tilecnt[2];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (kBidir) {
+    for (int i = threadIdx.x; i < 2 * kBN; i += blockDim.x) (&colbuf[0][0])[i] = 0x7F800000u;
+    if (threadIdx.x < 2) tilecnt[threadIdx.x] = 0u;
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
@@ -174,6 +201,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t0 = sp * s.tps;
       const int t1 = min(s.nt, t0 + s.tps);
       float rmin = __int_as_float(0x7f800000);
+      const int64_t row = static_cast<int64_t>(rb) * kBM + row_local;
+      // kBidir: this row's ||a||^2, or +inf for rows past nA (excluded from column minima)
+      const float narow = kBidir ? (row < s.nA ? __ldg(na + row) : __int_as_float(0x7f800000)) : 0.0f;
       for (int t = t0; t < t1; ++t) {
         mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
@@ -187,19 +217,42 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float4 n4 = __ldg(nbp + cc * 8 + i);
-            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 0], n4.x));
-            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 1], n4.y));
-            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 2], n4.z));
-            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 3], n4.w));
+            v[4 * i + 0] = fmaf(-2.0f, v[4 * i + 0], n4.x);
+            v[4 * i + 1] = fmaf(-2.0f, v[4 * i + 1], n4.y);
+            v[4 * i + 2] = fmaf(-2.0f, v[4 * i + 2], n4.z);
+            v[4 * i + 3] = fmaf(-2.0f, v[4 * i + 3], n4.w);
+            rmin = fminf(rmin, fminf(fminf(v[4 * i + 0], v[4 * i + 1]), fminf(v[4 * i + 2], v[4 * i + 3])));
+          }
+          if (kBidir) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + narow, 0.0f);
+            warp_colmin32(v, lane);
+            atomicMin(&colbuf[acc][cc * 32 + lane], __float_as_uint(v[0]));
           }
         }
         tc_fence_before();
         __syncwarp();
+        if (kBidir) {
+          __threadfence_block();
+          unsigned old = 0;
+          if (lane == 0) old = atomicAdd(&tilecnt[acc], 1u);
+          old = __shfl_sync(0xffffffffu, old, 0);
+          if (old == 3u) {  // last of the 4 epilogue warps: flush the tile's column minima
+            __threadfence_block();
+            for (int j = lane; j < kBN; j += 32) {
+              const unsigned val = atomicExch(&colbuf[acc][j], 0x7F800000u);
+              const int64_t col = static_cast<int64_t>(t) * kBN + j;
+              if (col < s.nB) atomicMin(reinterpret_cast<unsigned*>(colmin) + col, val);
+            }
+            if (lane == 0) tilecnt[acc] = 0u;
+            __threadfence_block();
+          }
+          __syncwarp();
+        }
         if (lane == 0) mbar_arrive(&tempty[acc]);
         acc ^= 1;
         if (acc == 0) aphase ^= 1u;
       }
-      const int64_t row = static_cast<int64_t>(rb) * kBM + row_local;
       if (row < s.nA) {
         const float d2 = fmaxf(rmin + __ldg(na + row), 0.0f);
         if (s.atomic_out)
@@ -427,10 +480,10 @@ static int dist_variant(int D) {
   return 1;
 }
 
-int dist_b_box_rows(int D) { return dist_variant(D) == 2 ? 128 : kBN; }
+int dist_b_box_rows(int D, bool bidir) { return (!bidir && dist_variant(D) == 2) ? 128 : kBN; }
 
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
-  const bool pair = dist_variant(a.D) == 2 && a.num_sms >= 2;
+  const bool pair = dist_variant(a.D) == 2 && a.num_sms >= 2 && a.colmin == nullptr;
   const int rows_per_unit = pair ? 256 : kBM;
   const int ctas_per_unit = pair ? 2 : 1;
   Sched s{};
@@ -464,14 +517,25 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
                                                                    a.na, a.nb, a.rowmin);
     return cudaGetLastError();
   }
+  if (a.colmin != nullptr) {
+    cudaError_t e = cudaMemsetAsync(a.colmin, 0x7F, sizeof(float) * a.nB, st);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(dist_rowmin_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSmemBytes));
+    if (e != cudaSuccess) return e;
+    count_launch();
+    dist_rowmin_kernel<true><<<nunits, kThreads, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
+                                                                    a.na, a.nb, a.rowmin, a.colmin);
+    return cudaGetLastError();
+  }
   {
-    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kSmemBytes));
     if (e != cudaSuccess) return e;
   }
   count_launch();
-  dist_rowmin_kernel<<<nunits, kThreads, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na,
-                                                            a.nb, a.rowmin);
+  dist_rowmin_kernel<false><<<nunits, kThreads, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
+                                                                   a.na, a.nb, a.rowmin, nullptr);
   return cudaGetLastError();
 }
 

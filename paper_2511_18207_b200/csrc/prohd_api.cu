@@ -150,8 +150,7 @@ int hausdorff(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   ExactWs w;
   int rc = exact_common(ctx, A, nA, B, nB, D, w);
   if (rc) return rc;
-  if ((rc = directed_on_ops(ctx, w.A, w.B, D, w, 0))) return rc;
-  if ((rc = directed_on_ops(ctx, w.B, w.A, D, w, 1))) return rc;
+  if ((rc = bidir_on_ops(ctx, w.A, w.B, D, w))) return rc;  // one fused sweep for both directions
   ExactHost h;
   if ((rc = fetch(ctx, w, h))) return rc;
   fill_directed(&out->ab, h.keys[0], h.nn_d[0], h.nn_j[0]);

@@ -29,6 +29,7 @@ struct EstWs {
   float* Xs[2] = {nullptr, nullptr};
   SetOps ops[2];
   float* rowmin = nullptr;
+  float* colmin = nullptr;
   unsigned long long* keys = nullptr;
   double* nn_d = nullptr;
   long long* nn_j = nullptr;
@@ -86,6 +87,7 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
     carve_set(c, w.ops[s], w.capU[s], D);
   }
   w.rowmin = c.take<float>(w.capU[0] > w.capU[1] ? w.capU[0] : w.capU[1]);
+  w.colmin = c.take<float>(w.capU[0] > w.capU[1] ? w.capU[0] : w.capU[1]);
   w.keys = c.take<unsigned long long>(2);
   w.nn_d = c.take<double>(2);
   w.nn_j = c.take<long long>(2);
@@ -198,13 +200,13 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   }
   ExactWs ew;
   ew.rowmin = w.rowmin;
+  ew.colmin = w.colmin;
   ew.keys = w.keys;
   ew.nn_d = w.nn_d;
   ew.nn_j = w.nn_j;
   ew.blk_d = w.blk_d;
   ew.blk_j = w.blk_j;
-  if ((rc = directed_on_ops(ctx, w.ops[0], w.ops[1], D, ew, 0))) return rc;
-  if ((rc = directed_on_ops(ctx, w.ops[1], w.ops[0], D, ew, 1))) return rc;
+  if ((rc = bidir_on_ops(ctx, w.ops[0], w.ops[1], D, ew))) return rc;  // Alg. 3 line 6, both directions
   tspan(ctx, PH_SUBSET, t_sub);
   unsigned long long keys[2];
   double nn_d[2];

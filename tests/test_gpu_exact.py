@@ -157,3 +157,20 @@ def test_cfg_full_rows(ctx, cfg):
     assert abs(r["dist2"] - ref_rows[0][0]) <= 1e-12 * ref_rows[0][0]
     # no row's true minimum exceeds the reported value by more than the tolerance
     assert rm.max() <= r["dist2_tc"] + 1e-6
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 4), (3, 700, 16), (300, 5, 8), (129, 257, 20), (1000, 3000, 64),
+                                   (777, 513, 256), (2048, 4099, 128)])
+def test_bidirectional_pass_matches_oracle(ctx, shape):
+    """f4: hausdorff() runs one fused sweep; its B->A side (column minima) must match the oracle."""
+    nA, nB, D = shape
+    rng = np.random.default_rng(nA + 3 * nB + 7 * D)
+    A = rng.standard_normal((nA, D)).astype(np.float32)
+    B = (rng.standard_normal((nB, D)) * 1.3 + 0.2).astype(np.float32)
+    h = ctx.hausdorff(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    ref = oracle.hausdorff(A, B)
+    _check_directed(A, B, h["ab"], ref["ab"])
+    _check_directed(B, A, h["ba"], ref["ba"])
+    d = ctx.directed_hd(torch.from_numpy(B).cuda(), torch.from_numpy(A).cuda())
+    tol = 1e-5 * (float((B[d["a"]].astype(np.float64) ** 2).sum()) + float((A[d["b"]].astype(np.float64) ** 2).sum()))
+    assert abs(h["ba"]["dist2"] - d["dist2"]) <= tol
