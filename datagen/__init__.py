@@ -210,3 +210,35 @@ def sample_rows(n: int, count: int, seed: int = 12345) -> np.ndarray:
     rng = np.random.default_rng([99, seed])
     count = min(count, n)
     return np.sort(rng.choice(n, size=count, replace=False))
+
+
+# ----------------------------------------------------------------------------
+# Paper workloads and baseline draws
+# ----------------------------------------------------------------------------
+
+def random_clouds(nA: int, nB: int, D: int, seed: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """PAPER.md:457 "randomly generated point clouds which are distributed uniformly in the
+    unit cube [0,1]^D with an offset of 0.1": A ~ U[0,1]^D, B ~ U[0,1]^D + 0.1 (the offset
+    applied to B, SPEC.md:391-399 reading), float64 draws cast to float32."""
+    rng = np.random.default_rng([7, seed, D])
+    A = rng.uniform(0.0, 1.0, size=(nA, D))
+    B = rng.uniform(0.0, 1.0, size=(nB, D)) + 0.1
+    return A.astype(np.float32), B.astype(np.float32)
+
+
+def uniform_sample(n: int, size: int, seed: int) -> np.ndarray:
+    """Random Sampling baseline draw: `size` indices of [0, n) uniformly
+    without replacement (sorted)."""
+    rng = np.random.default_rng([11, seed, n])
+    return np.sort(rng.choice(n, size=min(size, n), replace=False)).astype(np.int64)
+
+
+def systematic_sample(n: int, alpha: float, seed: int) -> np.ndarray:
+    """Systematic Random Sampling draw: a seeded random permutation of [0, n),
+    then every floor(1/alpha)-th element starting at position 0."""
+    stride = int(np.floor(1.0 / alpha))
+    if stride < 1:
+        raise ValueError("alpha must be <= 1")
+    rng = np.random.default_rng([13, seed, n])
+    perm = rng.permutation(n)
+    return perm[::stride].astype(np.int64)

@@ -59,6 +59,7 @@ typedef enum {
 
 /* flags for prohd_workspace_bytes */
 #define PROHD_WS_HOST_INPUTS 1u /* inputs may be host pointers: reserve staging space */
+#define PROHD_WS_CERTIFIED 2u   /* include prohd_estimate_certified (full-set operands)  */
 
 typedef struct prohd_ctx prohd_ctx; /* opaque: device, stream, workspace, last error */
 
@@ -132,6 +133,36 @@ int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* 
 int prohd_estimate(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB,
                    int32_t D, int32_t k, int64_t m, prohd_est* out,
                    double* dirs_out, int64_t* idxA_out, int64_t* idxB_out);
+
+/* Certified subset-full estimate: same selection as
+ * prohd_estimate, then
+ *   H^_sf = max( max_{a in A_sel} min_{b in B} ||a-b||, max_{b in B_sel} min_{a in A} ||b-a|| )
+ * which never exceeds H(A,B) (each term is an exact directed distance of a subset of
+ * the rows), restoring the paper's "never overestimates" claim that
+ * Alg. 3's subset-subset estimate does not satisfy. Witness b indices refer to the full
+ * sets. Cost |A_sel| nB + |B_sel| nA pairs. Workspace: PROHD_WS_CERTIFIED. */
+int prohd_estimate_certified(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB,
+                             int32_t D, int32_t k, int64_t m, prohd_est* out,
+                             double* dirs_out, int64_t* idxA_out, int64_t* idxB_out);
+
+/* Paper-literal parameterisation: Alg. 3 line 1
+ * k = m_pc = max(1, floor(sqrt D)) principal directions, alpha' = alpha / m_pc; per-tail counts
+ * max{1, floor(alpha n_X)} on the centroid axis (Alg. 1) and max{1, floor(alpha' n_X)}
+ * on each PC (Alg. 2), per set. 0 < alpha < 1. Outputs as prohd_estimate (idx
+ * capacities min(n_X, 2 (c0 + m_pc c1))). Workspace: prohd_workspace_bytes(nA, nB, D, m_pc,
+ * max per-tail count, flags). */
+int prohd_estimate_alpha(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB,
+                         int32_t D, double alpha, prohd_est* out, double* dirs_out,
+                         int64_t* idxA_out, int64_t* idxB_out);
+
+/* H(A[idxA], B[idxB]) with witnesses as indices into A and B: the exact HD of two index
+ * subsets (HOST or DEVICE int64 lists, 0 <= idx < n, duplicates allowed), one fused
+ * bidirectional sweep. The paper's sampling baselines (Random Sampling, Systematic
+ * Random Sampling) are this call on seeded index draws (datagen). Workspace:
+ * prohd_workspace_bytes(max(nA,nB), max(nA,nB), D, 0, 1, flags) suffices. */
+int hausdorff_subsets(prohd_ctx* ctx, const float* A, int64_t nA, const int64_t* idxA, int64_t kA,
+                      const float* B, int64_t nB, const int64_t* idxB, int64_t kB, int32_t D,
+                      prohd_hd* out);
 
 /* Test hook: steps 2-4 with caller-supplied directions
  * `dirs` (HOST, fp64, D x n_dirs, same layout as dirs_out; n_dirs >= 1). */

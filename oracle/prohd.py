@@ -251,6 +251,41 @@ def paper_parameters(D: int, alpha: float, nX: int) -> tuple[int, int, int]:
     return m_pc, c0, c1
 
 
+def select_counts(X: np.ndarray, U: np.ndarray, counts: list[int]) -> dict:
+    """O6+O7 with a per-direction tail count counts[l] (Alg. 1 uses k_X on the centroid axis,
+    Alg. 2 uses floor(alpha' n_X) on the PCs). All of X if 2 counts[l] >= n for any l."""
+    n = X.shape[0]
+    P = project(X, U)
+    lists = [extremes(P[:, l], counts[l]) for l in range(U.shape[1])]
+    if any(2 * c >= n for c in counts):
+        union = np.arange(n, dtype=np.int64)
+    else:
+        union = np.unique(np.concatenate([np.concatenate(t) for t in lists])).astype(np.int64)
+    return {"lists": lists, "union": union, "proj": P}
+
+
+def estimate_paper(A: np.ndarray, B: np.ndarray, alpha: float) -> dict:
+    """Alg. 3 with the paper's own parameters (O11): m_pc = floor(sqrt D) PCs, alpha on the
+    centroid axis (Alg. 1 with alpha), alpha' = alpha/m_pc on each PC (Alg. 2 with alpha')."""
+    D = A.shape[1]
+    m_pc = min(D, paper_parameters(D, alpha, 1)[0])
+    info = directions(A, B, m_pc)
+    U = info["U"]
+    sel = []
+    for X in (A, B):
+        _, c0, c1 = paper_parameters(D, alpha, X.shape[0])
+        sel.append(select_counts(X, U, [c0] + [c1] * (U.shape[1] - 1)))
+    hd = subset_hd(A, B, sel[0]["union"], sel[1]["union"])
+    return {"value": hd["value"], "ab": hd["ab"], "ba": hd["ba"], "IA": sel[0]["union"], "IB": sel[1]["union"],
+            "size_a": int(sel[0]["union"].size), "size_b": int(sel[1]["union"].size), "U": U,
+            "n_dirs": int(U.shape[1]), "k": m_pc}
+
+
+def sampling_hd(A: np.ndarray, B: np.ndarray, IA: np.ndarray, IB: np.ndarray) -> dict:
+    """The paper's sampling baselines given their index draws: exact HD of the samples."""
+    return subset_hd(A, B, np.asarray(IA), np.asarray(IB))
+
+
 def sharded_select(X: np.ndarray, U: np.ndarray, m: int, G: int) -> dict:
     """O12: split rows into G contiguous blocks, local top/bottom-m per block, then
     merge the G*m candidates by the same total order. Must equal `select`."""

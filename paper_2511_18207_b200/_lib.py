@@ -16,6 +16,7 @@ PROHD_E_WORKSPACE = 6
 PROHD_E_NOTIMPL = 7
 PROHD_E_DEVICE = 8
 PROHD_WS_HOST_INPUTS = 1
+PROHD_WS_CERTIFIED = 2
 
 STATUS_NAMES = {0: "PROHD_OK", 2: "PROHD_E_INVALID", 3: "PROHD_E_DATA", 4: "PROHD_E_INTERNAL",
                 5: "PROHD_E_CUDA", 6: "PROHD_E_WORKSPACE", 7: "PROHD_E_NOTIMPL", 8: "PROHD_E_DEVICE"}
@@ -24,7 +25,8 @@ STATUS_NAMES = {0: "PROHD_OK", 2: "PROHD_E_INVALID", 3: "PROHD_E_DATA", 4: "PROH
 EXPORTED = [
     "prohd_create", "prohd_destroy", "prohd_set_stream", "prohd_last_error", "prohd_version",
     "prohd_workspace_bytes", "prohd_set_workspace", "directed_hd", "hausdorff", "directed_hd_rowmin",
-    "prohd_estimate", "prohd_estimate_with_dirs", "directed_hd_local", "directed_hd_witness",
+    "prohd_estimate", "prohd_estimate_certified", "prohd_estimate_alpha", "hausdorff_subsets",
+    "prohd_estimate_with_dirs", "directed_hd_local", "directed_hd_witness",
     "prohd_enable_timing", "prohd_last_timings",
     "prohd_shard_workspace_bytes", "prohd_shift", "prohd_local_moments", "prohd_directions",
     "prohd_local_candidates", "prohd_merge_union", "prohd_gather_owned",
@@ -78,6 +80,9 @@ def load() -> C.CDLL:
     lib.hausdorff.argtypes = [vp, vp, i64, vp, i64, i32, C.POINTER(HD)]
     lib.directed_hd_rowmin.argtypes = [vp, vp, i64, vp, i64, i32, vp]
     lib.prohd_estimate.argtypes = [vp, vp, i64, vp, i64, i32, i32, i64, C.POINTER(Est), vp, vp, vp]
+    lib.prohd_estimate_certified.argtypes = [vp, vp, i64, vp, i64, i32, i32, i64, C.POINTER(Est), vp, vp, vp]
+    lib.prohd_estimate_alpha.argtypes = [vp, vp, i64, vp, i64, i32, C.c_double, C.POINTER(Est), vp, vp, vp]
+    lib.hausdorff_subsets.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64, i32, C.POINTER(HD)]
     lib.prohd_estimate_with_dirs.argtypes = [vp, vp, i64, vp, i64, i32, i32, i64, vp, C.POINTER(Est), vp, vp]
     lib.directed_hd_local.argtypes = [vp, vp, i64, i64, vp, i64, i32, C.POINTER(C.c_uint64)]
     lib.directed_hd_witness.argtypes = [vp, vp, vp, i64, i32, C.POINTER(Directed)]

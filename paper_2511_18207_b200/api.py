@@ -65,8 +65,9 @@ class Context:
         if rc != L.PROHD_OK:
             raise ProHDError(rc, self.lib.prohd_last_error(self.h).decode())
 
-    def reserve(self, nA: int, nB: int, D: int, k: int = 0, m: int = 1, host_inputs: bool = False) -> int:
-        flags = L.PROHD_WS_HOST_INPUTS if host_inputs else 0
+    def reserve(self, nA: int, nB: int, D: int, k: int = 0, m: int = 1, host_inputs: bool = False,
+                certified: bool = False) -> int:
+        flags = (L.PROHD_WS_HOST_INPUTS if host_inputs else 0) | (L.PROHD_WS_CERTIFIED if certified else 0)
         need = int(self.lib.prohd_workspace_bytes(nA, nB, D, k, m, flags))
         return self._ensure_ws(need)
 
@@ -78,13 +79,13 @@ class Context:
         self._check(self.lib.prohd_set_workspace(self.h, self._ws.data_ptr(), self._ws.numel()))
         return need
 
-    def _prepare(self, A, B, k=0, m=1):
+    def _prepare(self, A, B, k=0, m=1, certified=False):
         A = _as_points(A, "A")
         B = _as_points(B, "B")
         if A.shape[1] != B.shape[1]:
             raise ValueError("A and B must have the same dimension D")
         host = not (A.is_cuda and B.is_cuda)
-        self.reserve(A.shape[0], B.shape[0], A.shape[1], k, m, host_inputs=host)
+        self.reserve(A.shape[0], B.shape[0], A.shape[1], k, m, host_inputs=host, certified=certified)
         stream = torch.cuda.current_stream(self.device).cuda_stream
         self._check(self.lib.prohd_set_stream(self.h, C.c_void_p(stream)))
         return A, B
@@ -126,8 +127,9 @@ class Context:
                 "size_a": int(out.size_a), "size_b": int(out.size_b), "n_dirs": int(out.n_dirs)}
 
     def prohd_estimate(self, A, B, k: int, m: int, return_dirs: bool = False,
-                       return_indices: bool = False) -> dict:
-        A, B = self._prepare(A, B, k, m)
+                       return_indices: bool = False, certified: bool = False) -> dict:
+        """Alg. 3; certified=True gives the subset-full estimate (prohd_estimate_certified)."""
+        A, B = self._prepare(A, B, k, m, certified=certified)
         nA, nB, D = A.shape[0], B.shape[0], A.shape[1]
         out = L.Est()
         dirs = np.zeros((k + 1, D), dtype=np.float64) if return_dirs else None
@@ -136,8 +138,9 @@ class Context:
         ia = np.empty(capA, dtype=np.int64) if return_indices else None
         ib = np.empty(capB, dtype=np.int64) if return_indices else None
         ptr = (lambda a: a.ctypes.data if a is not None else None)
-        self._check(self.lib.prohd_estimate(self.h, A.data_ptr(), nA, B.data_ptr(), nB, D, k, m, C.byref(out),
-                                            ptr(dirs), ptr(ia), ptr(ib)))
+        fn = self.lib.prohd_estimate_certified if certified else self.lib.prohd_estimate
+        self._check(fn(self.h, A.data_ptr(), nA, B.data_ptr(), nB, D, k, m, C.byref(out), ptr(dirs), ptr(ia),
+                       ptr(ib)))
         res = self._est_out(out)
         if return_dirs:
             res["U"] = dirs[: res["n_dirs"]].T.copy()  # D x n_dirs
@@ -145,6 +148,46 @@ class Context:
             res["IA"] = ia[: res["size_a"]].copy()
             res["IB"] = ib[: res["size_b"]].copy()
         return res
+
+    def prohd_estimate_alpha(self, A, B, alpha: float, return_dirs: bool = False,
+                             return_indices: bool = False) -> dict:
+        """Paper-literal Alg. 3: k = floor(sqrt D) PCs, alpha on the centroid axis, alpha/k on the PCs."""
+        A0, B0 = _as_points(A, "A"), _as_points(B, "B")
+        nA, nB, D = A0.shape[0], B0.shape[0], A0.shape[1]
+        k = min(D, max(1, int(np.floor(np.sqrt(D)))))
+        c = [max(1, int(np.floor(alpha * x))) for x in (nA, nB)] + \
+            [max(1, int(np.floor((alpha / k) * x))) for x in (nA, nB)]
+        mmax = max(c)
+        A, B = self._prepare(A0, B0, k, mmax)
+        out = L.Est()
+        dirs = np.zeros((k + 1, D), dtype=np.float64) if return_dirs else None
+        capA = min(nA, 2 * mmax * (k + 1))
+        capB = min(nB, 2 * mmax * (k + 1))
+        ia = np.empty(capA, dtype=np.int64) if return_indices else None
+        ib = np.empty(capB, dtype=np.int64) if return_indices else None
+        ptr = (lambda a: a.ctypes.data if a is not None else None)
+        self._check(self.lib.prohd_estimate_alpha(self.h, A.data_ptr(), nA, B.data_ptr(), nB, D, float(alpha),
+                                                  C.byref(out), ptr(dirs), ptr(ia), ptr(ib)))
+        res = self._est_out(out)
+        if return_dirs:
+            res["U"] = dirs[: res["n_dirs"]].T.copy()
+        if return_indices:
+            res["IA"] = ia[: res["size_a"]].copy()
+            res["IB"] = ib[: res["size_b"]].copy()
+        return res
+
+    def hausdorff_subsets(self, A, idxA, B, idxB) -> dict:
+        """H(A[idxA], B[idxB]) with witnesses as indices into A and B."""
+        A, B = self._prepare(A, B)
+        ia = np.ascontiguousarray(np.asarray(idxA, dtype=np.int64))
+        ib = np.ascontiguousarray(np.asarray(idxB, dtype=np.int64))
+        self.reserve(max(A.shape[0], B.shape[0]), max(A.shape[0], B.shape[0]), A.shape[1],
+                     host_inputs=not (A.is_cuda and B.is_cuda))
+        out = L.HD()
+        self._check(self.lib.hausdorff_subsets(self.h, A.data_ptr(), A.shape[0], ia.ctypes.data, ia.size,
+                                               B.data_ptr(), B.shape[0], ib.ctypes.data, ib.size, A.shape[1],
+                                               C.byref(out)))
+        return {"value": out.value, "ab": _directed(out.ab), "ba": _directed(out.ba)}
 
     def prohd_estimate_with_dirs(self, A, B, U: np.ndarray, m: int, return_indices: bool = True) -> dict:
         U = np.asarray(U, dtype=np.float64)

@@ -504,13 +504,16 @@ static cudaError_t launch_project(const float* X, int64_t n, int D, const float*
 }
 
 cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
-                          const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st) {
+                          const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st, bool first,
+                          bool last) {
   cudaError_t e;
-  if ((e = cudaMemsetAsync(b.maxnorm2, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  if (first) {
+    if ((e = cudaMemsetAsync(b.maxnorm2, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(b.bitmap, 0, sizeof(unsigned) * ((n + 31) / 32), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(b.overflow, 0, sizeof(int), st)) != cudaSuccess) return e;
+  }
   if ((e = cudaMemsetAsync(b.hist, 0, sizeof(unsigned) * 3 * L * 2 * kRadixBins, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(b.ccount, 0, sizeof(unsigned) * 2 * L, st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(b.bitmap, 0, sizeof(unsigned) * ((n + 31) / 32), st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(b.overflow, 0, sizeof(int), st)) != cudaSuccess) return e;
   count_launch();
   init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, m);
   // K3
@@ -533,8 +536,18 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap,
                                               nullptr, nullptr, 0);
   // K5
+  if (last) {
+    count_launch();
+    compact_kernel<<<1, 1024, 0, st>>>(b.bitmap, (n + 31) / 32, b.uidx, b.ucount);
+  }
+  return cudaGetLastError();
+}
+
+__global__ void minus_one_kernel(const int* a, int* b) { *b = *a > 0 ? *a - 1 : 0; }
+
+cudaError_t launch_minus_one(const int* a, int* b, cudaStream_t st) {
   count_launch();
-  compact_kernel<<<1, 1024, 0, st>>>(b.bitmap, (n + 31) / 32, b.uidx, b.ucount);
+  minus_one_kernel<<<1, 1, 0, st>>>(a, b);
   return cudaGetLastError();
 }
 

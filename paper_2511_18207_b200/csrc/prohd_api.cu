@@ -5,7 +5,11 @@
 // sequence. Every arithmetic step of the path runs in the kernels (k_*.cu).
 #include "../../include/prohd.h"
 #include "api_common.cuh"
+#include "prohd_kernels.cuh"
 #include "prohd_steps.cuh"
+
+#include <algorithm>
+#include <vector>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -78,7 +82,7 @@ size_t prohd_workspace_bytes(int64_t nA, int64_t nB, int32_t D, int32_t k, int64
   ExactWs w;
   size_t exact = carve_exact(c, w, nA, nB, D, (flags & PROHD_WS_HOST_INPUTS) != 0);
   size_t est = estimate_workspace_bytes(nA, nB, D, k < 0 ? 0 : k, m < 1 ? 1 : m,
-                                        (flags & PROHD_WS_HOST_INPUTS) != 0);
+                                        (flags & PROHD_WS_HOST_INPUTS) != 0, (flags & PROHD_WS_CERTIFIED) != 0);
   return (exact > est ? exact : est) + 256;
 }
 
@@ -230,6 +234,94 @@ int directed_hd_witness(prohd_ctx* ctx, const float* a, const float* B, int64_t 
 int prohd_estimate(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D, int32_t k,
                    int64_t m, prohd_est* out, double* dirs_out, int64_t* idxA_out, int64_t* idxB_out) {
   return prohd_run(ctx, A, nA, B, nB, D, k, m, nullptr, 0, out, dirs_out, idxA_out, idxB_out);
+}
+
+int prohd_estimate_certified(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                             int32_t k, int64_t m, prohd_est* out, double* dirs_out, int64_t* idxA_out,
+                             int64_t* idxB_out) {
+  return prohd_run(ctx, A, nA, B, nB, D, k, m, nullptr, 0, out, dirs_out, idxA_out, idxB_out, 1);
+}
+
+int prohd_estimate_alpha(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                         double alpha, prohd_est* out, double* dirs_out, int64_t* idxA_out, int64_t* idxB_out) {
+  if (!(alpha > 0.0 && alpha < 1.0)) return fail(ctx, PROHD_E_INVALID, "alpha must be in (0, 1)");
+  if (D < 1 || nA < 1 || nB < 1) return fail(ctx, PROHD_E_INVALID, "bad sizes");
+  int k = static_cast<int>(std::floor(std::sqrt(static_cast<double>(D))));  // Alg. 3 l.1: m = floor(sqrt D)
+  if (k < 1) k = 1;
+  if (k > D) k = D;
+  const double ap = alpha / k;  // alpha' = alpha / m
+  int64_t cnt[4];
+  const int64_t n[2] = {nA, nB};
+  for (int s = 0; s < 2; ++s) {  // k_X = max{1, floor(alpha n_X)}
+    cnt[2 * s] = std::max<int64_t>(1, static_cast<int64_t>(std::floor(alpha * n[s])));
+    cnt[2 * s + 1] = std::max<int64_t>(1, static_cast<int64_t>(std::floor(ap * n[s])));
+  }
+  const int64_t m = std::max(std::max(cnt[0], cnt[1]), std::max(cnt[2], cnt[3]));
+  return prohd_run(ctx, A, nA, B, nB, D, k, m, nullptr, 0, out, dirs_out, idxA_out, idxB_out, 0, cnt);
+}
+
+int hausdorff_subsets(prohd_ctx* ctx, const float* A, int64_t nA, const int64_t* idxA, int64_t kA, const float* B,
+                      int64_t nB, const int64_t* idxB, int64_t kB, int32_t D, prohd_hd* out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (out == nullptr || idxA == nullptr || idxB == nullptr) return fail(ctx, PROHD_E_INVALID, "null pointer");
+  if ((rc = check_sets(ctx, A, nA, B, nB, D))) return rc;
+  if (kA < 1 || kB < 1 || kA > nA || kB > nB) return fail(ctx, PROHD_E_INVALID, "bad subset sizes");
+  // host copies of the index lists: validated, and used to map witnesses back
+  std::vector<int64_t> ia(kA), ib(kB);
+  CK(cudaMemcpy(ia.data(), idxA, sizeof(int64_t) * kA, cudaMemcpyDefault));
+  CK(cudaMemcpy(ib.data(), idxB, sizeof(int64_t) * kB, cudaMemcpyDefault));
+  for (int64_t v : ia)
+    if (v < 0 || v >= nA) return fail(ctx, PROHD_E_INVALID, "idxA entry out of range");
+  for (int64_t v : ib)
+    if (v < 0 || v >= nB) return fail(ctx, PROHD_E_INVALID, "idxB entry out of range");
+  call_begin(ctx);
+  const bool host_in = !(is_device_ptr(A) && is_device_ptr(B));
+  // workspace: staged inputs (if host) + gathered subsets + their operands + exact-HD scratch
+  Carver dry{nullptr, 0, 0, true};
+  float* stA = nullptr;
+  float* stB = nullptr;
+  auto carve = [&](Carver& c, ExactWs& w, float*& xa, float*& xb, long long*& dia, long long*& dib) {
+    if (host_in) {
+      stA = c.take<float>(nA * D);
+      stB = c.take<float>(nB * D);
+    }
+    xa = c.take<float>(kA * D);
+    xb = c.take<float>(kB * D);
+    dia = c.take<long long>(kA);
+    dib = c.take<long long>(kB);
+    return carve_exact(c, w, kA, kB, D, false);
+  };
+  ExactWs tmp;
+  float *xa, *xb;
+  long long *dia, *dib;
+  const size_t need = carve(dry, tmp, xa, xb, dia, dib);
+  if (ctx->ws == nullptr || ctx->ws_bytes < need)
+    return fail(ctx, PROHD_E_WORKSPACE, "workspace too small: need %zu bytes, have %zu", need, ctx->ws_bytes);
+  Carver c{ctx->ws, 0, ctx->ws_bytes, false};
+  ExactWs w;
+  carve(c, w, xa, xb, dia, dib);
+  cudaStream_t st = ctx->stream;
+  bool hi;
+  if ((rc = stage_inputs(ctx, A, nA, B, nB, D, stA, stB, hi))) return rc;
+  CK(cudaMemcpyAsync(dia, ia.data(), sizeof(int64_t) * kA, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dib, ib.data(), sizeof(int64_t) * kB, cudaMemcpyHostToDevice, st));
+  CK(launch_gather_offset(A, D, dia, 0, kA, 0, xa, st));
+  CK(launch_gather_offset(B, D, dib, 0, kB, 0, xb, st));
+  CK(cudaMemsetAsync(w.bad, 0, sizeof(int), st));
+  if ((rc = prep_set(ctx, xa, kA, D, w.A, w.bad))) return rc;
+  if ((rc = prep_set(ctx, xb, kB, D, w.B, w.bad))) return rc;
+  if ((rc = bidir_on_ops(ctx, w.A, w.B, D, w))) return rc;
+  ExactHost h;
+  if ((rc = fetch(ctx, w, h))) return rc;
+  fill_directed(&out->ab, h.keys[0], h.nn_d[0], h.nn_j[0]);
+  fill_directed(&out->ba, h.keys[1], h.nn_d[1], h.nn_j[1]);
+  out->ab.a = ia[out->ab.a];
+  out->ab.b = ib[out->ab.b];
+  out->ba.a = ib[out->ba.a];
+  out->ba.b = ia[out->ba.b];
+  out->value = out->ab.dist2 >= out->ba.dist2 ? out->ab.dist : out->ba.dist;
+  return PROHD_OK;
 }
 
 int prohd_estimate_with_dirs(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,

@@ -25,9 +25,11 @@ struct EstWs {
   float* U32 = nullptr;
   double* lam = nullptr;
   int* n_dirs = nullptr;
+  int* n_dirs1 = nullptr;  // n_dirs - 1 (principal directions only)
   SelectBufs sel[2]{};
   float* Xs[2] = {nullptr, nullptr};
   SetOps ops[2];
+  SetOps full[2];  // certified mode: operands of the full sets (columns of the subset-full HD)
   float* rowmin = nullptr;
   float* colmin = nullptr;
   unsigned long long* keys = nullptr;
@@ -57,7 +59,7 @@ static void carve_select(Carver& c, SelectBufs& b, int64_t n, int L, int64_t m) 
 }
 
 static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int k, int64_t m, bool host_inputs,
-                        int num_sms) {
+                        int num_sms, bool certified = false) {
   const int L = k + 1;
   if (host_inputs) {
     w.stageA = c.take<float>(nA * D);
@@ -79,12 +81,17 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
   w.U32 = c.take<float>(static_cast<int64_t>(L) * D);
   w.lam = c.take<double>(k > 0 ? k : 1);
   w.n_dirs = c.take<int>(1);
+  w.n_dirs1 = c.take<int>(1);
   const int64_t n[2] = {nA, nB};
   for (int s = 0; s < 2; ++s) {
     carve_select(c, w.sel[s], n[s], L, m);
     w.capU[s] = (2 * m >= n[s]) ? n[s] : (n[s] < 2 * m * L ? n[s] : 2 * m * L);
     w.Xs[s] = c.take<float>(w.capU[s] * D);
     carve_set(c, w.ops[s], w.capU[s], D);
+  }
+  if (certified) {
+    carve_set(c, w.full[0], nA, D);
+    carve_set(c, w.full[1], nB, D);
   }
   w.rowmin = c.take<float>(w.capU[0] > w.capU[1] ? w.capU[0] : w.capU[1]);
   w.colmin = c.take<float>(w.capU[0] > w.capU[1] ? w.capU[0] : w.capU[1]);
@@ -97,17 +104,18 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
   return c.off;
 }
 
-size_t estimate_workspace_bytes(int64_t nA, int64_t nB, int D, int k, int64_t m, bool host_inputs) {
+size_t estimate_workspace_bytes(int64_t nA, int64_t nB, int D, int k, int64_t m, bool host_inputs,
+                                bool certified) {
   Carver c{nullptr, 0, 0, true};
   EstWs w;
-  return carve_est(c, w, nA, nB, D, k, m, host_inputs, 148);
+  return carve_est(c, w, nA, nB, D, k, m, host_inputs, 148, certified);
 }
 
 }  // namespace prohd
 
 int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D, int32_t k,
               int64_t m, const double* dirs_in, int32_t n_dirs_in, prohd_est* out, double* dirs_out,
-              int64_t* idxA_out, int64_t* idxB_out) {
+              int64_t* idxA_out, int64_t* idxB_out, int mode, const int64_t* counts) {
   int rc = enter(ctx);
   if (rc) return rc;
   if (out == nullptr) return fail(ctx, PROHD_E_INVALID, "null output");
@@ -122,12 +130,13 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   const bool host_in = !(is_device_ptr(A) && is_device_ptr(B));
   Carver dry{nullptr, 0, 0, true};
   EstWs tmp;
-  const size_t need = carve_est(dry, tmp, nA, nB, D, k, m, host_in, ctx->num_sms);
+  const bool certified = mode == 1;
+  const size_t need = carve_est(dry, tmp, nA, nB, D, k, m, host_in, ctx->num_sms, certified);
   if (ctx->ws == nullptr || ctx->ws_bytes < need)
     return fail(ctx, PROHD_E_WORKSPACE, "workspace too small: need %zu bytes, have %zu", need, ctx->ws_bytes);
   Carver c{ctx->ws, 0, ctx->ws_bytes, false};
   EstWs w;
-  carve_est(c, w, nA, nB, D, k, m, host_in, ctx->num_sms);
+  carve_est(c, w, nA, nB, D, k, m, host_in, ctx->num_sms, certified);
   cudaStream_t st = ctx->stream;
   bool hi;
   if ((rc = stage_inputs(ctx, A, nA, B, nB, D, w.stageA, w.stageB, hi))) return rc;
@@ -162,11 +171,18 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   for (int s = 0; s < 2; ++s) {
     // projections run for every point (also when 2m >= n) so non-finite input is always detected
     SelectBufs& b = w.sel[s];
-    if (2 * m >= n[s]) {
+    const int64_t m0 = counts ? counts[2 * s] : m;      // centroid axis
+    const int64_t m1 = counts ? counts[2 * s + 1] : m;  // principal directions
+    const bool all = 2 * m0 >= n[s] || (L > 1 && 2 * m1 >= n[s]);
+    if (all) {
       CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, st));  // finiteness pass
       CK(launch_iota(b.uidx, b.ucount, n[s], st));
-    } else {
-      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m, b, st));
+    } else if (m0 == m1 || L == 1) {
+      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, st));
+    } else {  // two direction groups with different per-tail counts, one shared union bitmap
+      CK(launch_select(X[s], n[s], D, w.U64, w.U32, 1, w.n_dirs, m0, b, st, true, false));
+      CK(launch_minus_one(w.n_dirs, w.n_dirs1, st));
+      CK(launch_select(X[s], n[s], D, w.U64 + D, w.U32 + D, L - 1, w.n_dirs1, m1, b, st, false, true));
     }
   }
   tspan(ctx, PH_SELECT, t_sel);
@@ -206,7 +222,15 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   ew.nn_j = w.nn_j;
   ew.blk_d = w.blk_d;
   ew.blk_j = w.blk_j;
-  if ((rc = bidir_on_ops(ctx, w.ops[0], w.ops[1], D, ew))) return rc;  // Alg. 3 line 6, both directions
+  if (!certified) {
+    if ((rc = bidir_on_ops(ctx, w.ops[0], w.ops[1], D, ew))) return rc;  // Alg. 3 line 6, both directions
+  } else {
+    // certified mode (SPEC.md:279 subset-full): rows of each subset against the FULL other set
+    if ((rc = prep_set(ctx, A, nA, D, w.full[0], w.bad))) return rc;
+    if ((rc = prep_set(ctx, B, nB, D, w.full[1], w.bad))) return rc;
+    if ((rc = directed_on_ops(ctx, w.ops[0], w.full[1], D, ew, 0))) return rc;
+    if ((rc = directed_on_ops(ctx, w.ops[1], w.full[0], D, ew, 1))) return rc;
+  }
   tspan(ctx, PH_SUBSET, t_sub);
   unsigned long long keys[2];
   double nn_d[2];
@@ -227,9 +251,11 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   fill_directed(&out->ba, keys[1], nn_d[1], nn_j[1]);
   // map subset rows to original indices (a in the first argument, b in the second)
   out->ab.a = ua[out->ab.a];
-  out->ab.b = ub[out->ab.b];
   out->ba.a = ub[out->ba.a];
-  out->ba.b = ua[out->ba.b];
+  if (!certified) {  // certified mode: the columns already are the full sets
+    out->ab.b = ub[out->ab.b];
+    out->ba.b = ua[out->ba.b];
+  }
   out->value = out->ab.dist2 >= out->ba.dist2 ? out->ab.dist : out->ba.dist;
   out->size_a = ucount[0];
   out->size_b = ucount[1];

@@ -58,8 +58,12 @@ struct SelectBufs {
   int* overflow;          // guard-band overflow flag
   int64_t cap;            // candidates per list
 };
+// first: reset the union bitmap/flags; last: compact the bitmap into the sorted union. Two calls
+// (first=true,last=false then first=false,last=true) select with different m per direction group.
 cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
-                          const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st);
+                          const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st, bool first = true,
+                          bool last = true);
+cudaError_t launch_minus_one(const int* a, int* b, cudaStream_t st);  // *b = max(*a - 1, 0)
 // Sharded selection: local top/bottom-m lists with their fp64 projection values and GLOBAL
 // indices (row_offset + local row) -> cval_out/cidx_out [L][2][m] (index -1 = empty slot).
 // If m >= n every local point is a candidate of every list.

@@ -250,3 +250,42 @@ def test_cfg1_seed0(golden):
     assert abs(e["ab"]["dist"] - g["hhat_ab"]) < 1e-9 and [e["ab"]["a"], e["ab"]["b"]] == g["hhat_ab_witness"]
     assert abs(e["ba"]["dist"] - g["hhat_ba"]) < 1e-9 and [e["ba"]["a"], e["ba"]["b"]] == g["hhat_ba_witness"]
     assert np.allclose(e["lam"], g["top_eigenvalues"], atol=1e-4)
+
+
+# ------------------------------------------------------------------ paper-literal parameters (O11)
+
+def test_estimate_paper_reduces_to_fixed_m():
+    """With n small enough that floor(alpha n) and floor(alpha/m_pc n) clamp to the same count,
+    the paper-literal estimate is Alg. 3 with that fixed m (O6 with one count)."""
+    rng = np.random.default_rng(21)
+    A = rng.standard_normal((90, 9)).astype(np.float32)
+    B = (rng.standard_normal((80, 9)) + 0.4).astype(np.float32)
+    e = prohd.estimate_paper(A, B, 0.01)  # m_pc = 3, counts max(1, 0) = 1 everywhere
+    r = prohd.estimate(A, B, 3, 1)
+    assert e["k"] == 3 and np.array_equal(e["IA"], r["IA"]) and np.array_equal(e["IB"], r["IB"])
+    assert e["value"] == r["value"]
+
+
+def test_select_counts_per_direction():
+    rng = np.random.default_rng(22)
+    X = rng.standard_normal((400, 5))
+    U = np.linalg.qr(rng.standard_normal((5, 3)))[0]
+    s = prohd.select_counts(X, U, [10, 3, 3])
+    P = X @ U
+    for l, c in enumerate([10, 3, 3]):
+        b, t = s["lists"][l]
+        assert len(b) == c and len(t) == c
+        assert P[b, l].max() <= np.delete(P[:, l], b).min()
+        assert P[t, l].min() >= np.delete(P[:, l], t).max()
+    assert s["union"].size <= 2 * (10 + 3 + 3)
+
+
+def test_sampling_draws():
+    import datagen
+    u = datagen.uniform_sample(1000, 30, seed=1)
+    assert u.size == 30 and np.unique(u).size == 30 and u.min() >= 0 and u.max() < 1000
+    sy = datagen.systematic_sample(10, 0.34, seed=1)  # SPEC.md:346: stride 2 -> 5 points
+    assert sy.size == 5 and np.unique(sy).size == 5
+    assert datagen.systematic_sample(1001, 0.01, 3).size == 11  # ceil(n / floor(1/alpha))
+    A, B = datagen.random_clouds(50, 40, 4, seed=0)
+    assert A.min() >= 0 and A.max() <= 1 and B.min() >= 0.1 and B.max() <= 1.1
