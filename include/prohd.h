@@ -164,6 +164,20 @@ int hausdorff_subsets(prohd_ctx* ctx, const float* A, int64_t nA, const int64_t*
                       const float* B, int64_t nB, const int64_t* idxB, int64_t kB, int32_t D,
                       prohd_hd* out);
 
+/* Bound report for directions `dirs` (HOST, n_dirs x D fp64, row l =
+ * u_l, 1 <= n_dirs <= 32), e.g. dirs_out of prohd_estimate:
+ *   per_dir_out (HOST, n_dirs x 4): delta(u_l) through the origin (Eq. 2),
+ *     delta(u_l) centred at the mean of A u B, h_u(A,B), h_u(B,A)
+ *     (1-D Hausdorff distances of the projections);
+ *   summary_out (HOST, 3): H_U = max_l H_u, min delta over both frames and all
+ *     directions, and H_U + 2 min delta (the upper end of Eq. 4).
+ * delta is evaluated from fp32 dot products and inflated by a bound of their rounding error, so
+ * it never falls below the exact value (the interval stays valid); H_u uses the fp32
+ * projections (|error| <= 2 (D+8) 2^-24 max ||p||). One extra pass over A and B plus a radix
+ * sort of the n x n_dirs projections of each set. */
+int prohd_bounds(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                 const double* dirs, int32_t n_dirs, double* per_dir_out, double* summary_out);
+
 /* Test hook: steps 2-4 with caller-supplied directions
  * `dirs` (HOST, fp64, D x n_dirs, same layout as dirs_out; n_dirs >= 1). */
 int prohd_estimate_with_dirs(prohd_ctx* ctx, const float* A, int64_t nA, const float* B,

@@ -189,6 +189,24 @@ class Context:
                                                C.byref(out)))
         return {"value": out.value, "ab": _directed(out.ab), "ba": _directed(out.ba)}
 
+    def bounds(self, A, B, U: np.ndarray) -> dict:
+        """f2 bound report for directions U (D x n_dirs): per-direction delta (origin, centred),
+        h_u(A,B), h_u(B,A); H_U, min delta and H_U + 2 min delta (Eq. 4)."""
+        U = np.asarray(U, dtype=np.float64)
+        n_dirs = U.shape[1]
+        A, B = self._prepare(A, B)
+        nmax = max(A.shape[0], B.shape[0])
+        D = A.shape[1]
+        extra = 8 * (4 * n_dirs * nmax + 256 * n_dirs * (nmax // 1024 + 1) + 2 * 296 * D) + (1 << 20)
+        self._ensure_ws(self._ws.numel() + extra if self._ws is not None else extra)
+        dirs = np.ascontiguousarray(U.T)
+        per = np.zeros((n_dirs, 4), dtype=np.float64)
+        summ = np.zeros(3, dtype=np.float64)
+        self._check(self.lib.prohd_bounds(self.h, A.data_ptr(), A.shape[0], B.data_ptr(), B.shape[0], D,
+                                          dirs.ctypes.data, n_dirs, per.ctypes.data, summ.ctypes.data))
+        return {"delta_origin": per[:, 0].copy(), "delta_centered": per[:, 1].copy(), "hu_ab": per[:, 2].copy(),
+                "hu_ba": per[:, 3].copy(), "H_U": summ[0], "min_delta": summ[1], "upper": summ[2]}
+
     def prohd_estimate_with_dirs(self, A, B, U: np.ndarray, m: int, return_indices: bool = True) -> dict:
         U = np.asarray(U, dtype=np.float64)
         n_dirs = U.shape[1]

@@ -83,4 +83,21 @@ cudaError_t launch_gather(const float* X, int D, const long long* idx, const uns
                           float* Y, cudaStream_t st);
 cudaError_t launch_iota(long long* idx, unsigned* count, int64_t n, cudaStream_t st);
 
+// ---------------------------------------------------------------- f2 bounds
+struct BoundsPlan {
+  int nblk = 0;
+  int64_t keys_words = 0, count_words = 0;
+};
+struct BoundsBufs {
+  unsigned *keysA, *keysB, *sortA, *sortB, *tmp, *counts;  // [L][n] order-preserving keys, radix scratch
+  unsigned long long* delta2;  // [L][2] fp64 bits: max delta^2 (origin, centred), error-inflated
+  unsigned long long* hu;      // [2][L] fp64 bits: h_u(A,B) then h_u(B,A)
+};
+constexpr int kMeanParts = 296;
+BoundsPlan plan_bounds(int64_t nA, int64_t nB, int L);
+cudaError_t launch_union_mean(const float* A, int64_t nA, const float* B, int64_t nB, int D, double* part,
+                              double* mu, cudaStream_t st);
+cudaError_t launch_bounds(const float* A, int64_t nA, const float* B, int64_t nB, int D, const float* U32, int L,
+                          const double* mu, const BoundsBufs& b, cudaStream_t st);
+
 }  // namespace prohd

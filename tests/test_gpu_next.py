@@ -95,3 +95,35 @@ def test_sampling_baselines(ctx, scheme):
     # host index lists and host points give the same answer
     h = ctx.hausdorff_subsets(torch.from_numpy(A), ia, torch.from_numpy(B), ib)
     assert h == g
+
+
+# ---------------------------------------------------------------- f2: bound report
+
+@pytest.mark.parametrize("cfg,n", [(1, None), (2, 20000), (3, 65536), (5, 65536)])
+def test_bound_report(ctx, cfg, n):
+    c = datagen.CONFIGS[cfg]
+    A, B = datagen.generate(cfg, n=n)
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    e = ctx.prohd_estimate(At, Bt, c.k, c.m(A.shape[0]), return_dirs=True)
+    U = e["U"]
+    r = ctx.bounds(At, Bt, U)
+    D = A.shape[1]
+    mu = (A.astype(np.float64).sum(0) + B.astype(np.float64).sum(0)) / (A.shape[0] + B.shape[0])
+    xmax = max(np.linalg.norm(A.astype(np.float64), axis=1).max(), np.linalg.norm(B.astype(np.float64), axis=1).max())
+    g = (4 * D + 16) * 2.0 ** -24
+    eps = (D + 8) * 2.0 ** -24 * xmax * 1.07
+    for l in range(U.shape[1]):
+        u = U[:, l]
+        d0 = OP.delta(A, B, u)
+        d1 = OP.delta(A, B, u, center=mu)
+        # never below the exact value, and within the rounding-error inflation above it
+        assert d0 <= r["delta_origin"][l] <= np.sqrt(d0 ** 2 + 2 * g * xmax ** 2) + 1e-12
+        assert d1 <= r["delta_centered"][l] <= np.sqrt(d1 ** 2 + 2 * g * (xmax + np.linalg.norm(mu)) ** 2) + 1e-12
+        hab, hba = OP.hd_1d(A.astype(np.float64) @ u, B.astype(np.float64) @ u)
+        assert abs(r["hu_ab"][l] - hab) <= 2 * eps and abs(r["hu_ba"][l] - hba) <= 2 * eps
+    HU = OP.multi_direction_hd(A, B, U)
+    assert abs(r["H_U"] - HU) <= 2 * eps
+    # Eq. (4): H_U <= H <= H_U + 2 min delta holds for the exact H (computed on the GPU)
+    H = ctx.hausdorff(At, Bt)["value"]
+    assert r["H_U"] <= H * (1 + 1e-6) + 2 * eps
+    assert H <= r["upper"] + 1e-6 * H
