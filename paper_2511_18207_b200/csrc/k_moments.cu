@@ -21,38 +21,60 @@
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
 
+#include <cstdlib>
+
 namespace prohd {
 namespace {
 
 constexpr int kFB = 64;       // feature block
-constexpr int kChunk = 64;    // points per shared-memory chunk
-constexpr int kThreads = 256;
 
-__global__ void __launch_bounds__(256) shift_kernel(const float* __restrict__ A, int64_t nA,
-                                                    const float* __restrict__ B, int64_t nB, int D,
-                                                    double* __restrict__ s) {
-  // one thread per feature: fp64 mean of the first <= 4096 rows of A and of B
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < D; f += gridDim.x * blockDim.x) {
-    const int64_t ca = nA < 4096 ? nA : 4096;
-    const int64_t cb = nB < 4096 ? nB : 4096;
-    double acc = 0.0;
-    for (int64_t i = 0; i < ca; ++i) acc += static_cast<double>(A[i * D + f]);
-    for (int64_t i = 0; i < cb; ++i) acc += static_cast<double>(B[i * D + f]);
-    s[f] = acc / static_cast<double>(ca + cb);
+// s = fp64 mean of the first <= 4096 rows of A and of B. One CTA per 32 features:
+// lane = feature (coalesced 128-B rows), warp w sums rows w, w + 32, ... with 4
+// independent accumulators, then a fixed-order tree over the 32 warps (deterministic).
+__global__ void __launch_bounds__(1024) shift_kernel(const float* __restrict__ A, int64_t nA,
+                                                     const float* __restrict__ B, int64_t nB, int D,
+                                                     double* __restrict__ s) {
+  __shared__ double part[32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + lane;
+  const int64_t ca = nA < 4096 ? nA : 4096;
+  const int64_t cb = nB < 4096 ? nB : 4096;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (f < D) {
+    int64_t i = w;
+    for (; i + 96 < ca; i += 128) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += static_cast<double>(__ldg(A + (i + 32 * u) * D + f));
+    }
+    for (; i < ca; i += 32) acc[0] += static_cast<double>(__ldg(A + i * D + f));
+    i = w;
+    for (; i + 96 < cb; i += 128) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += static_cast<double>(__ldg(B + (i + 32 * u) * D + f));
+    }
+    for (; i < cb; i += 32) acc[0] += static_cast<double>(__ldg(B + i * D + f));
   }
+  part[w][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) {
+    if (w < o) part[w][lane] += part[w + o][lane];
+    __syncthreads();
+  }
+  if (w == 0 && f < D) s[f] = part[0][lane] / static_cast<double>(ca + cb);
 }
 
 struct MomArgs {
-  const float* X;
-  int64_t n;
+  const float* A;
+  const float* B;
+  int64_t nA, nB;  // the CTAs of a pair split the concatenated index space [0, nA + nB)
   int D;
   const double* s;
   int nb;          // feature blocks
-  int slot0;       // first partial slot of this set
-  int nranges;     // point ranges for this set
-  int nslots;      // total slots (A + B)
-  double* Gpart;   // [pair][slot][64][64]
-  double* Spart;   // [slot][nb*64]
+  int c_diag;      // CTAs per diagonal pair (bi == bj)
+  int c_off;       // CTAs per off-diagonal pair
+  int nslots;      // max(c_diag, c_off): partial-slot stride of a pair
+  double* Gpart;   // [pair][nslots][64][64]
+  double* Spart;   // [bi][c_diag][2 sets][64]
 };
 
 __device__ __forceinline__ void pair_of(int p, int nb, int& bi, int& bj) {
@@ -73,32 +95,69 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-constexpr int kLds = 136;   // fp64 row stride of the chunk tile (128 features + 8 pad)
+// Row stride (doubles) of the chunk tile: 128 features + 4 pad. A fragment load reads
+// rows k0 + (lane & 3) at columns base + (lane >> 2); a 64-bit load is served per
+// half-warp, whose 16 addresses (fk * kLds + fr, fk, fr < 4) fall in distinct bank pairs
+// iff kLds = 4 (mod 16).
+constexpr int kLds = 132;
 constexpr int kMT = 128;    // threads per CTA (4 warps)
 constexpr int kMC = 32;     // points per chunk
+// resident CTAs per SM (register-limited: 160 regs at 3, 128 at 4). PROHD_K1_CTAS=3|4 (dev A/B).
+static int mom_ctas_per_sm() {
+  const char* e = getenv("PROHD_K1_CTAS");
+  return (e != nullptr && e[0] == '3') ? 3 : 4;
+}
 
-// One CTA: one 64x64 block (bi, bj) of G over one point range. 4 warps, warp w
-// owns the 32x32 tile (w/2, w%2) = 4 x 4 DMMA tiles (16 MMAs per 8 fragment
-// loads). In diagonal blocks the strictly-lower warp tile (1,0) is skipped (its
-// mirror (0,1) is computed). The next 32-point chunk is prefetched into
-// registers while the current one is multiplied.
-__global__ void __launch_bounds__(kMT, 3) moments_kernel(MomArgs a) {
+// CTA -> (bi, bj, pair index, slot). Pairs (bi <= bj) are enumerated row-major; row r
+// holds the diagonal pair (c_diag CTAs) then nb-1-r off-diagonal pairs (c_off CTAs each).
+__device__ __forceinline__ void cta_work(int cta, int nb, int c_diag, int c_off, int& bi, int& bj, int& pair,
+                                         int& slot) {
+  int r = 0, pbase = 0;
+  for (;;) {
+    const int row_ctas = c_diag + (nb - 1 - r) * c_off;
+    if (cta < row_ctas || r == nb - 1) break;
+    cta -= row_ctas;
+    pbase += nb - r;
+    ++r;
+  }
+  bi = r;
+  if (cta < c_diag) {
+    bj = r;
+    slot = cta;
+  } else {
+    cta -= c_diag;
+    bj = r + 1 + cta / c_off;
+    slot = cta % c_off;
+  }
+  pair = pbase + (bj - r);
+}
+
+// One CTA: one 64x64 block (bi, bj) of G over one range of the concatenated points of
+// A u B (G is a sum over the union; the column sums S_A, S_B are kept apart). 4 warps,
+// warp w owns the 32x32 tile (w/2, w%2) = 4 x 4 DMMA tiles (16 MMAs per 8 fragment
+// loads). In diagonal blocks the strictly-lower warp tile (1,0) is skipped (its mirror
+// (0,1) is computed). The grid is one wave (kMomCtasPerSm per SM) with CTA counts per
+// pair proportional to the pair's warp tiles (3 diagonal, 4 off-diagonal), so every CTA
+// carries about the same work. The next 32-point chunk is prefetched into registers
+// while the current one is multiplied.
+template <int kCtas>
+__global__ void __launch_bounds__(kMT, kCtas) moments_kernel(MomArgs a) {
   extern __shared__ double cs[];  // [kMC][kLds]: features of block bi (0..63) then bj (64..127)
-  const int pair = blockIdx.x;
-  const int range = blockIdx.y;
-  int bi, bj;
-  pair_of(pair, a.nb, bi, bj);
+  int bi, bj, pair, slot;
+  cta_work(blockIdx.x, a.nb, a.c_diag, a.c_off, bi, bj, pair, slot);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t per = (a.n + a.nranges - 1) / a.nranges;
-  const int64_t p0 = static_cast<int64_t>(range) * per;
-  const int64_t p1 = p0 + per < a.n ? p0 + per : a.n;
+  const int64_t N = a.nA + a.nB;
+  const int cp = bi == bj ? a.c_diag : a.c_off;
+  const int64_t per = (N + cp - 1) / cp;
+  const int64_t p0 = static_cast<int64_t>(slot) * per;
+  const int64_t p1 = p0 + per < N ? p0 + per : N;
 
   // loader mapping: thread -> feature column lf (0..127)
   const int lf = tid;
   const int feat = lf < 64 ? bi * kFB + lf : bj * kFB + (lf - 64);
   const bool fvalid = feat < a.D;
   const double sf = fvalid ? a.s[feat] : 0.0;
-  double ssum = 0.0;  // column sum of (x - s) (used by diagonal pairs)
+  double ssA = 0.0, ssB = 0.0;  // column sums of (x - s) over A and over B (used by diagonal pairs)
 
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const bool active = !(bi == bj && wm > wn);
@@ -114,7 +173,8 @@ __global__ void __launch_bounds__(kMT, 3) moments_kernel(MomArgs a) {
 #pragma unroll
     for (int r = 0; r < kMC; ++r) {
       const int64_t p = c0 + r;
-      pre[r] = (p < p1 && fvalid) ? __ldg(a.X + p * a.D + feat) : 0.0f;
+      const float* src = p < a.nA ? a.A + p * a.D : a.B + (p - a.nA) * a.D;
+      pre[r] = (p < p1 && fvalid) ? __ldg(src + feat) : 0.0f;
     }
   };
   if (p0 < p1) load(p0);
@@ -125,7 +185,10 @@ __global__ void __launch_bounds__(kMT, 3) moments_kernel(MomArgs a) {
       const int64_t p = c0 + r;
       const double v = (p < p1 && fvalid) ? static_cast<double>(pre[r]) - sf : 0.0;
       cs[r * kLds + lf] = v;
-      ssum += v;
+      if (p < a.nA)
+        ssA += v;
+      else
+        ssB += v;
     }
     __syncthreads();
     if (c0 + kMC < p1) load(c0 + kMC);  // in flight during the MMAs below
@@ -145,7 +208,6 @@ __global__ void __launch_bounds__(kMT, 3) moments_kernel(MomArgs a) {
       }
     }
   }
-  const int slot = a.slot0 + range;
   double* out = a.Gpart + (static_cast<int64_t>(pair) * a.nslots + slot) * (kFB * kFB);
   if (active) {
 #pragma unroll
@@ -154,19 +216,23 @@ __global__ void __launch_bounds__(kMT, 3) moments_kernel(MomArgs a) {
       for (int j = 0; j < 4; ++j) {
         const int r = wm + i * 8 + fr;
         const int c = wn + j * 8 + 2 * fk;
-        out[r * 64 + c] = acc[i][j][0];
-        out[r * 64 + c + 1] = acc[i][j][1];
+        *reinterpret_cast<double2*>(out + r * 64 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
       }
   }
   // column sums: only diagonal pairs, features of block bi (lf < 64)
-  if (bi == bj && lf < 64) a.Spart[static_cast<int64_t>(slot) * (a.nb * kFB) + bi * kFB + lf] = ssum;
+  if (bi == bj && lf < 64) {
+    double* sp = a.Spart + (static_cast<int64_t>(bi) * a.c_diag + slot) * (2 * kFB);
+    sp[lf] = ssA;
+    sp[kFB + lf] = ssB;
+  }
 }
 
 // G (full symmetric D x D) and S_A, S_B from the partials, fixed summation order.
 __global__ void __launch_bounds__(256) moments_reduce_kernel(const double* __restrict__ Gpart,
                                                              const double* __restrict__ Spart, int nb, int D,
-                                                             int slotsA, int nslots, double* __restrict__ G,
-                                                             double* __restrict__ SA, double* __restrict__ SB) {
+                                                             int c_diag, int c_off, int nslots,
+                                                             double* __restrict__ G, double* __restrict__ SA,
+                                                             double* __restrict__ SB) {
   const int npairs = nb * (nb + 1) / 2;
   const int64_t total = static_cast<int64_t>(npairs) * kFB * kFB;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
@@ -178,16 +244,20 @@ __global__ void __launch_bounds__(256) moments_reduce_kernel(const double* __res
     if (bi == bj && (w / kFB) > (w % kFB)) continue;  // diagonal blocks: upper triangle is authoritative
     const int i = bi * kFB + w / kFB, j = bj * kFB + w % kFB;
     if (i >= D || j >= D) continue;
+    const int cp = bi == bj ? c_diag : c_off;
     double acc = 0.0;
     const double* src = Gpart + static_cast<int64_t>(pair) * nslots * (kFB * kFB) + w;
-    for (int s = 0; s < nslots; ++s) acc += src[static_cast<int64_t>(s) * (kFB * kFB)];
+    for (int s = 0; s < cp; ++s) acc += src[static_cast<int64_t>(s) * (kFB * kFB)];
     G[static_cast<int64_t>(i) * D + j] = acc;
     G[static_cast<int64_t>(j) * D + i] = acc;
   }
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < D; f += gridDim.x * blockDim.x) {
+    const double* sp = Spart + static_cast<int64_t>(f / kFB) * c_diag * (2 * kFB) + (f % kFB);
     double sa = 0.0, sb = 0.0;
-    for (int s = 0; s < slotsA; ++s) sa += Spart[static_cast<int64_t>(s) * (nb * kFB) + f];
-    for (int s = slotsA; s < nslots; ++s) sb += Spart[static_cast<int64_t>(s) * (nb * kFB) + f];
+    for (int s = 0; s < c_diag; ++s) {
+      sa += sp[static_cast<int64_t>(s) * (2 * kFB)];
+      sb += sp[static_cast<int64_t>(s) * (2 * kFB) + kFB];
+    }
     SA[f] = sa;
     SB[f] = sb;
   }
@@ -236,51 +306,55 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
   MomentsPlan p;
   p.nb = (D + kFB - 1) / kFB;
   p.npairs = p.nb * (p.nb + 1) / 2;
-  const int target = 6 * num_sms;  // CTAs (3 resident per SM)
-  int per_pair = (target + p.npairs - 1) / p.npairs;
-  if (per_pair < 2) per_pair = 2;
-  const double fa = (nA + nB) > 0 ? static_cast<double>(nA) / static_cast<double>(nA + nB) : 0.5;
-  p.rangesA = static_cast<int>(per_pair * fa + 0.5);
-  if (p.rangesA < 1) p.rangesA = 1;
-  p.rangesB = per_pair - p.rangesA;
-  if (p.rangesB < 1) p.rangesB = 1;
-  if (nA <= 0) p.rangesA = 0;
-  if (nB <= 0) p.rangesB = 0;
-  // never more ranges than chunks
-  const int64_t ca = (nA + kChunk - 1) / kChunk, cb = (nB + kChunk - 1) / kChunk;
-  if (p.rangesA > ca) p.rangesA = static_cast<int>(ca);
-  if (p.rangesB > cb) p.rangesB = static_cast<int>(cb);
-  p.nslots = p.rangesA + p.rangesB;
+  const int ndiag = p.nb, noff = p.npairs - p.nb;
+  // one wave of CTAs, split over the pairs in proportion to their warp tiles (3 / 4)
+  int T = mom_ctas_per_sm() * (num_sms > 0 ? num_sms : 148);
+  const int64_t N = nA + nB;
+  const int64_t chunks = (N + kMC - 1) / kMC;
+  int cd = 1, co = noff > 0 ? 1 : 0;
+  if (T < ndiag + noff) T = ndiag + noff;
+  // greedy: add a CTA where it lowers the larger per-CTA work (3/cd vs 4/co) most, within T
+  while (true) {
+    const int used = ndiag * cd + noff * co;
+    const bool can_d = used + ndiag <= T && cd < chunks;
+    const bool can_o = noff > 0 && used + noff <= T && co < chunks;
+    if (!can_d && !can_o) break;
+    const double wd = 3.0 / cd, wo = noff > 0 ? 4.0 / co : 0.0;
+    if (can_o && (wo >= wd || !can_d))
+      ++co;
+    else if (can_d)
+      ++cd;
+    else
+      break;
+  }
+  p.c_diag = cd;
+  p.c_off = co > 0 ? co : 1;
+  p.nctas = ndiag * cd + noff * co;
+  p.nslots = cd > p.c_off ? cd : p.c_off;
   p.gpart_doubles = static_cast<int64_t>(p.npairs) * p.nslots * kFB * kFB;
-  p.spart_doubles = static_cast<int64_t>(p.nslots) * p.nb * kFB;
+  p.spart_doubles = static_cast<int64_t>(p.nb) * p.c_diag * 2 * kFB;
   return p;
 }
 
 cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB, int D, double* s,
                          cudaStream_t st) {
   count_launch();
-  shift_kernel<<<(D + 255) / 256, 256, 0, st>>>(A, nA, B, nB, D, s);
+  shift_kernel<<<(D + 31) / 32, 1024, 0, st>>>(A, nA, B, nB, D, s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_moments_partial(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB,
                                    int D, const MomentsBufs& b, cudaStream_t st) {
   const size_t smem = sizeof(double) * kMC * kLds;
-  cudaError_t e = cudaFuncSetAttribute(moments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  auto kern = mom_ctas_per_sm() == 3 ? moments_kernel<3> : moments_kernel<4>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  if (nA > 0 && p.rangesA > 0) {
-    MomArgs a{A, nA, D, b.s, p.nb, 0, p.rangesA, p.nslots, b.Gpart, b.Spart};
-    count_launch();
-    moments_kernel<<<dim3(p.npairs, p.rangesA), kMT, smem, st>>>(a);
-  }
-  if (nB > 0 && p.rangesB > 0) {
-    MomArgs bb{B, nB, D, b.s, p.nb, p.rangesA, p.rangesB, p.nslots, b.Gpart, b.Spart};
-    count_launch();
-    moments_kernel<<<dim3(p.npairs, p.rangesB), kMT, smem, st>>>(bb);
-  }
+  MomArgs a{A, B, nA, nB, D, b.s, p.nb, p.c_diag, p.c_off, p.nslots, b.Gpart, b.Spart};
   count_launch();
-  moments_reduce_kernel<<<148 * 2, 256, 0, st>>>(b.Gpart, b.Spart, p.nb, D, p.rangesA, p.nslots, b.C, b.SA, b.SB);
+  kern<<<p.nctas, kMT, smem, st>>>(a);
+  count_launch();
+  moments_reduce_kernel<<<148 * 2, 256, 0, st>>>(b.Gpart, b.Spart, p.nb, D, p.c_diag, p.c_off, p.nslots, b.C,
+                                                 b.SA, b.SB);
   return cudaGetLastError();
 }
 

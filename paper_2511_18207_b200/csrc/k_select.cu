@@ -225,28 +225,72 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const float* __restrict
   }
 }
 
-// one thread per (direction, tail): walk the bins from the top
-__global__ void radix_scan_kernel(const unsigned* __restrict__ hist, int L, const int* n_dirs, int round,
-                                  unsigned* state) {
-  const int id = blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= 2 * L) return;
+// One CTA per (direction, tail): find the bin b (scanning from the top) where the
+// running count reaches the remaining rank `rem`, i.e. the first b >= 1 in descending
+// order with cum(> b) + h[b] >= rem (else b = 0), as a block-wide suffix scan: thread i
+// owns descending positions [i * per, (i + 1) * per), bin = binmask - position.
+constexpr int kScanT = 256;
+__global__ void __launch_bounds__(kScanT) radix_scan_kernel(const unsigned* __restrict__ hist, int L,
+                                                           const int* n_dirs, int round, unsigned* state) {
+  const int id = blockIdx.x;
   const int l = id >> 1, t = id & 1;
   if (l >= *n_dirs) return;
   int shift;
   unsigned binmask;
   round_params(round, shift, binmask);
+  const int nbins = static_cast<int>(binmask) + 1;
+  const int per = nbins / kScanT;  // 8 or 4
   const unsigned* h = hist + ((static_cast<int64_t>(round) * L + l) * 2 + t) * kRadixBins;
   unsigned* s = state + (l * 2 + t) * 4;
-  unsigned rem = s[2];
-  unsigned cum = 0;
-  int b = static_cast<int>(binmask);
-  for (; b > 0; --b) {
-    if (cum + h[b] >= rem) break;
-    cum += h[b];
+  const unsigned rem = s[2];
+  __shared__ unsigned wsum[kScanT / 32];
+  __shared__ int first;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  unsigned v[8];
+  unsigned tot = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    v[j] = j < per ? h[binmask - (tid * per + j)] : 0u;
+    tot += v[j];
   }
-  s[0] |= static_cast<unsigned>(b) << shift;
-  s[1] |= binmask << shift;
-  s[2] = rem - cum;
+  // exclusive scan of the thread totals in descending-bin order
+  unsigned inc = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (tid == 0) first = 0x7FFFFFFF;
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  unsigned excl = inc - tot;
+  for (int i = 0; i < w; ++i) excl += wsum[i];
+  unsigned cum = excl;
+  int hit = 0x7FFFFFFF;
+  unsigned cum_hit = 0, cum_ge1 = 0;
+  for (int j = 0; j < per; ++j) {
+    const int d = tid * per + j;
+    const int bin = static_cast<int>(binmask) - d;
+    if (bin >= 1 && hit == 0x7FFFFFFF && cum + v[j] >= rem) {
+      hit = d;
+      cum_hit = cum;
+    }
+    cum += v[j];
+    if (bin == 1) cum_ge1 = cum;  // sum of all bins >= 1
+  }
+  if (hit != 0x7FFFFFFF) atomicMin(&first, hit);
+  __syncthreads();
+  const int f = first;
+  if (f != 0x7FFFFFFF) {
+    if (hit == f) {
+      s[0] |= static_cast<unsigned>(static_cast<int>(binmask) - f) << shift;
+      s[1] |= binmask << shift;
+      s[2] = rem - cum_hit;
+    }
+  } else if (tid == (nbins - 2) / per) {  // owner of bin 1: fall back to bin 0
+    s[1] |= binmask << shift;
+    s[2] = rem - cum_ge1;
+  }
 }
 
 __global__ void __launch_bounds__(256) collect_kernel(const float* __restrict__ P32, int64_t n, int D, int L,
@@ -525,7 +569,7 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
     count_launch();
     radix_hist_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, L, n_dirs, r, b.state, b.hist);
     count_launch();
-    radix_scan_kernel<<<(2 * L + 63) / 64, 64, 0, st>>>(b.hist, L, n_dirs, r, b.state);
+    radix_scan_kernel<<<2 * L, kScanT, 0, st>>>(b.hist, L, n_dirs, r, b.state);
   }
   count_launch();
   collect_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, D, L, n_dirs, b.state, b.maxnorm2,
@@ -573,7 +617,7 @@ cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offse
       count_launch();
       radix_hist_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, L, n_dirs, r, b.state, b.hist);
       count_launch();
-      radix_scan_kernel<<<(2 * L + 63) / 64, 64, 0, st>>>(b.hist, L, n_dirs, r, b.state);
+      radix_scan_kernel<<<2 * L, kScanT, 0, st>>>(b.hist, L, n_dirs, r, b.state);
     }
   }
   count_launch();

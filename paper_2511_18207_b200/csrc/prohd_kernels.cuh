@@ -9,7 +9,7 @@ namespace prohd {
 
 // ---------------------------------------------------------------- K1
 struct MomentsPlan {
-  int nb = 0, npairs = 0, rangesA = 0, rangesB = 0, nslots = 0;
+  int nb = 0, npairs = 0, c_diag = 0, c_off = 0, nctas = 0, nslots = 0;
   int64_t gpart_doubles = 0, spart_doubles = 0;
 };
 struct MomentsBufs {
