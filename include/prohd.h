@@ -191,9 +191,21 @@ int prohd_estimate_with_dirs(prohd_ctx* ctx, const float* A, int64_t nA, const f
  * rank's packed key  (float_bits(d2_tc) << 32) | (0xFFFFFFFF - global_row)
  * (max over ranks = global argmax, lowest row on ties) to *key_out (HOST).
  * The caller all-reduces the key (MAX), then calls directed_hd_witness on the
- * rank that owns the winning row. */
+ * rank that owns the winning row. `centre` (HOST or DEVICE, D fp64, or NULL): the
+ * common translation applied before the tensor-core distances (K0); NULL = the
+ * default of directed_hd, prohd_centre(NULL, 0, B, nB), so any shard count reproduces
+ * directed_hd's key bit for bit. The sharded subset HD passes prohd_centre(A_sel, B_sel),
+ * the centre prohd_estimate uses. */
 int directed_hd_local(prohd_ctx* ctx, const float* A_local, int64_t nA_local, int64_t row_offset,
-                      const float* B, int64_t nB, int32_t D, uint64_t* key_out);
+                      const float* B, int64_t nB, int32_t D, const double* centre, uint64_t* key_out);
+/* Common centre of a pair (HOST out, D fp64): the fp64 mean of the first min(nX, 4096)
+ * rows of X and the first min(nY, 4096) rows of Y (DEVICE inputs; either count may be 0),
+ * per-set sums added last so centre(X, Y) == centre(Y, X) bit for bit. The distance
+ * operands are prepared about this point (directed_hd: centre(-, B); hausdorff and the
+ * subset HD of prohd_estimate: centre(A, B) of the pair they compare). Workspace: 2D
+ * doubles. */
+int prohd_centre(prohd_ctx* ctx, const float* X, int64_t nX, const float* Y, int64_t nY, int32_t D,
+                 double* centre_out);
 /* fp64 nearest neighbour of one point a (HOST or DEVICE, D floats) in B:
  * fills out->b, out->dist2, out->dist (out->a is left to the caller). */
 int directed_hd_witness(prohd_ctx* ctx, const float* a, const float* B, int64_t nB, int32_t D,
@@ -213,7 +225,11 @@ int directed_hd_witness(prohd_ctx* ctx, const float* a, const float* B, int64_t 
  * Workspace: prohd_shard_workspace_bytes(max local rows, max total rows, D, k, m, flags). */
 size_t prohd_shard_workspace_bytes(int64_t n_local_max, int64_t n_total_max, int32_t D, int32_t k,
                                    int64_t m, uint32_t flags);
-/* Shift s (HOST out, D fp64): fp64 mean of the first min(n, 4096) rows of A and of B. */
+/* Shift s (HOST out, D fp64): the fp64 mean m of the first min(n, 4096) rows of A and of
+ * B if that offset is large against the rows' spread (sum m_f^2 > 1024 sum var_f), else all
+ * zeros (the moments are then taken about the origin: fp32 products are exact in fp64,
+ * and the bounded offset bounds the cancellation in C = G/N - mu mu^T). Any s is valid
+ * for prohd_local_moments / prohd_directions as long as every rank uses the same one. */
 int prohd_shift(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
                 double* shift_out);
 /* This rank's moments about s (HOST, D fp64): moments_out (DEVICE, 2D + D*D fp64) =

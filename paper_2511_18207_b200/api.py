@@ -226,12 +226,28 @@ class Context:
         res["IB"] = ib[: res["size_b"]].copy()
         return res
 
-    def directed_hd_local(self, A_local, row_offset: int, B) -> int:
+    def directed_hd_local(self, A_local, row_offset: int, B, centre=None) -> int:
+        """Packed key of this row shard; `centre` (fp64, D) defaults to centre(-, B)."""
         A, B = self._prepare(A_local, B)
         key = C.c_uint64()
+        cptr = None
+        if centre is not None:
+            c = centre if isinstance(centre, torch.Tensor) else torch.as_tensor(np.asarray(centre, np.float64))
+            c = c.to(dtype=torch.float64).contiguous()
+            cptr = c.data_ptr()
         self._check(self.lib.directed_hd_local(self.h, A.data_ptr(), A.shape[0], int(row_offset), B.data_ptr(),
-                                               B.shape[0], A.shape[1], C.byref(key)))
+                                               B.shape[0], A.shape[1], cptr, C.byref(key)))
         return int(key.value)
+
+    def centre(self, X, Y) -> np.ndarray:
+        """prohd_centre: fp64 mean of the first <= 4096 rows of X and of Y (device tensors)."""
+        X, Y = _as_points(X, "X"), _as_points(Y, "Y")
+        D = X.shape[1]
+        self._shard_ws(max(X.shape[0], Y.shape[0]), 1, D, 0, 1)
+        out = np.zeros(D, dtype=np.float64)
+        self._check(self.lib.prohd_centre(self.h, X.data_ptr(), X.shape[0], Y.data_ptr(), Y.shape[0], D,
+                                          out.ctypes.data))
+        return out
 
     def directed_hd_witness(self, a, B) -> dict:
         a = _as_points(a.reshape(1, -1) if a.dim() == 1 else a, "a")

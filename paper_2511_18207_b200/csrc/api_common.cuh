@@ -116,6 +116,7 @@ struct ExactWs {
   double* blk_d = nullptr;
   long long* blk_j = nullptr;
   int* bad = nullptr;
+  double* centre = nullptr;  // [2D]: the pair's common centre (K0), then scratch
 };
 
 inline void carve_set(Carver& c, SetOps& s, int64_t n, int D) {
@@ -141,6 +142,7 @@ inline size_t carve_exact(Carver& c, ExactWs& w, int64_t nA, int64_t nB, int D, 
   w.blk_d = c.take<double>(kNNBlocks);
   w.blk_j = c.take<long long>(kNNBlocks);
   w.bad = c.take<int>(1);
+  w.centre = c.take<double>(2 * static_cast<int64_t>(D));
   return c.off;
 }
 
@@ -256,10 +258,11 @@ inline int stage_inputs(prohd_ctx* ctx, const float*& A, int64_t nA, const float
   return PROHD_OK;
 }
 
-inline int prep_set(prohd_ctx* ctx, const float* X, int64_t n, int D, SetOps& s, int* bad) {
+inline int prep_set(prohd_ctx* ctx, const float* X, int64_t n, int D, SetOps& s, int* bad,
+                    const double* centre) {
   s.x = X;
   const int t0 = tmark(ctx);
-  CK(launch_prep(X, n, D, pad_dim(D), round_up(n, kBN), s.hi, s.lo, s.norms, bad, ctx->stream));
+  CK(launch_prep(X, n, D, pad_dim(D), round_up(n, kBN), centre, s.hi, s.lo, s.norms, bad, ctx->stream));
   tspan(ctx, PH_PREP, t0);
   return PROHD_OK;
 }

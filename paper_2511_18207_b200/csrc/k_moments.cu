@@ -28,39 +28,76 @@ namespace {
 
 constexpr int kFB = 64;       // feature block
 
-// s = fp64 mean of the first <= 4096 rows of A and of B. One CTA per 32 features:
-// lane = feature (coalesced 128-B rows), warp w sums rows w, w + 32, ... with 4
-// independent accumulators, then a fixed-order tree over the 32 warps (deterministic).
+// Shift s (fp64, D values; s + D: D doubles of scratch). m = fp64 mean of the first
+// <= 4096 rows of A and of B, v = their per-feature variance. One CTA per 32 features:
+// lane = feature (coalesced 128-B rows), warp w sums rows w, w + 32, ... then a
+// fixed-order tree over the 32 warps (deterministic). shift_decide_kernel then keeps
+// s = m only if the mean offset is large against the spread (sum m^2 > 1024 sum v): the
+// Gram pass subtracts s in fp64, which costs fp64-pipe time; with s = 0 it multiplies
+// the raw fp32 values, whose products are exact in fp64, and the centring happens in
+// moments_finalize (C = G/N - mu mu^T), whose cancellation grows with the ratio. Measured
+// at full size (tools/dir_accuracy.py): cfg4 (ratio 31.7, top-16 gaps down to 1.1e-4)
+// gives PC sin-angles of 2.7e-12 unshifted vs 1.2e-13 shifted, against a selection
+// margin of 5e-8; linear in the ratio, the 1024 bound keeps them below ~1e-10.
 __global__ void __launch_bounds__(1024) shift_kernel(const float* __restrict__ A, int64_t nA,
                                                      const float* __restrict__ B, int64_t nB, int D,
                                                      double* __restrict__ s) {
-  __shared__ double part[32][33];
+  __shared__ double part[4][32][33];  // sum and sum of squares, of A and of B
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int f = blockIdx.x * 32 + lane;
   const int64_t ca = nA < 4096 ? nA : 4096;
   const int64_t cb = nB < 4096 ? nB : 4096;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (f < D) {
-    int64_t i = w;
-    for (; i + 96 < ca; i += 128) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += static_cast<double>(__ldg(A + (i + 32 * u) * D + f));
+    for (int64_t i = w; i < ca; i += 32) {
+      const double x = static_cast<double>(__ldg(A + i * D + f));
+      acc[0] += x;
+      acc[1] += x * x;
     }
-    for (; i < ca; i += 32) acc[0] += static_cast<double>(__ldg(A + i * D + f));
-    i = w;
-    for (; i + 96 < cb; i += 128) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += static_cast<double>(__ldg(B + (i + 32 * u) * D + f));
+    for (int64_t i = w; i < cb; i += 32) {
+      const double x = static_cast<double>(__ldg(B + i * D + f));
+      acc[2] += x;
+      acc[3] += x * x;
     }
-    for (; i < cb; i += 32) acc[0] += static_cast<double>(__ldg(B + i * D + f));
   }
-  part[w][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) part[q][w][lane] = acc[q];
   __syncthreads();
   for (int o = 16; o > 0; o >>= 1) {
-    if (w < o) part[w][lane] += part[w + o][lane];
+    if (w < o)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) part[q][w][lane] += part[q][w + o][lane];
     __syncthreads();
   }
-  if (w == 0 && f < D) s[f] = part[0][lane] / static_cast<double>(ca + cb);
+  if (w == 0 && f < D) {
+    // per-set sums added last: the same bits for (A, B) and (B, A)
+    const double cnt = static_cast<double>(ca + cb);
+    const double m = (part[0][0][lane] + part[2][0][lane]) / cnt;
+    s[f] = m;
+    s[D + f] = fmax((part[1][0][lane] + part[3][0][lane]) / cnt - m * m, 0.0);
+  }
+}
+
+__global__ void __launch_bounds__(256) shift_decide_kernel(double* __restrict__ s, int D, int force) {
+  __shared__ double r1[256], r2[256];
+  double a = 0.0, b = 0.0;
+  for (int f = threadIdx.x; f < D; f += 256) {
+    a += s[f] * s[f];
+    b += s[D + f];
+  }
+  r1[threadIdx.x] = a;
+  r2[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      r1[threadIdx.x] += r1[threadIdx.x + o];
+      r2[threadIdx.x] += r2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  const bool keep = force >= 0 ? force != 0 : r1[0] > 1024.0 * r2[0];
+  if (!keep)
+    for (int f = threadIdx.x; f < D; f += 256) s[f] = 0.0;
 }
 
 struct MomArgs {
@@ -333,18 +370,36 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
   p.nslots = cd > p.c_off ? cd : p.c_off;
   p.gpart_doubles = static_cast<int64_t>(p.npairs) * p.nslots * kFB * kFB;
   p.spart_doubles = static_cast<int64_t>(p.nb) * p.c_diag * 2 * kFB;
+  const char* leg = getenv("PROHD_K1_LEGACY");
+  p.gram = !(leg != nullptr && leg[0] == '1') && plan_gram(nA, nB, D, num_sms, p.gp);
+  if (p.gram) {
+    if (p.gp.gpart_doubles > p.gpart_doubles) p.gpart_doubles = p.gp.gpart_doubles;
+    if (p.gp.spart_doubles > p.spart_doubles) p.spart_doubles = p.gp.spart_doubles;
+  }
   return p;
+}
+
+cudaError_t launch_centre(const float* X, int64_t nX, const float* Y, int64_t nY, int D, double* c,
+                          cudaStream_t st) {
+  count_launch();
+  shift_kernel<<<(D + 31) / 32, 1024, 0, st>>>(X, nX, Y, nY, D, c);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB, int D, double* s,
                          cudaStream_t st) {
   count_launch();
   shift_kernel<<<(D + 31) / 32, 1024, 0, st>>>(A, nA, B, nB, D, s);
+  count_launch();
+  const char* fe = getenv("PROHD_SHIFT");  // dev A/B only: 0 = never shift, 1 = always
+  const int force = (fe != nullptr && (fe[0] == '0' || fe[0] == '1')) ? fe[0] - '0' : -1;
+  shift_decide_kernel<<<1, 256, 0, st>>>(s, D, force);
   return cudaGetLastError();
 }
 
 cudaError_t launch_moments_partial(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB,
                                    int D, const MomentsBufs& b, cudaStream_t st) {
+  if (p.gram) return launch_gram(p.gp, A, nA, B, nB, D, b.s, b.Gpart, b.Spart, b.C, b.SA, b.SB, st);
   const size_t smem = sizeof(double) * kMC * kLds;
   auto kern = mom_ctas_per_sm() == 3 ? moments_kernel<3> : moments_kernel<4>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -1,9 +1,10 @@
 // k_prep.cu — K0 operand preparation, K7 row-max key and fp64 witness search.
 //
-// K0: per point, hi = trunc_tf32(x) (low 13 mantissa bits
-// cleared, so the tensor core reads hi exactly whatever its fp32->tf32
-// conversion mode), lo = x - hi (exact in fp32), and ||x||^2 accumulated in
-// fp64 then rounded to fp32. One warp per row; HBM-bound.
+// K0 (SURVEY.md §2f, §8(a) "Centering"): per point, y = x - c (fp64, c the pair's
+// common centre), hi = trunc_tf32(fp32(y)) (low 13 mantissa bits cleared, so the
+// tensor core reads hi exactly whatever its fp32->tf32 conversion mode),
+// lo = fp32(y - hi), and ||y||^2 accumulated in fp64 then rounded to fp32 (without
+// a centre: y = x and lo = x - hi exactly). One warp per row; HBM-bound.
 //
 // K7: the directed maximum over row minima packed as
 //   key = (float_bits(d2) << 32) | (0xFFFFFFFF - row)
@@ -22,9 +23,10 @@ __device__ __forceinline__ float tf32_trunc(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-template <bool kGather>
+template <bool kGather, bool kCentre>
 __global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, const int64_t* __restrict__ idx,
-                                                   int64_t n, int D, int Dp, int64_t n_pad, float* __restrict__ hi,
+                                                   int64_t n, int D, int Dp, int64_t n_pad,
+                                                   const double* __restrict__ centre, float* __restrict__ hi,
                                                    float* __restrict__ lo, float* __restrict__ norms, int* bad) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -41,10 +43,18 @@ __global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, 
     double s = 0.0;
     for (int c = lane; c < Dp; c += 32) {
       const float v = c < D ? __ldg(x + c) : 0.0f;
-      const float vh = tf32_trunc(v);
-      h[c] = vh;
-      l[c] = v - vh;
-      s = fma(static_cast<double>(v), static_cast<double>(v), s);
+      if (kCentre) {
+        const double y = c < D ? static_cast<double>(v) - __ldg(centre + c) : 0.0;
+        const float vh = tf32_trunc(static_cast<float>(y));
+        h[c] = vh;
+        l[c] = static_cast<float>(y - static_cast<double>(vh));
+        s = fma(y, y, s);
+      } else {
+        const float vh = tf32_trunc(v);
+        h[c] = vh;
+        l[c] = v - vh;
+        s = fma(static_cast<double>(v), static_cast<double>(v), s);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -63,17 +73,28 @@ static int grid_for_rows(int64_t rows) {
   return static_cast<int>(blocks);
 }
 
-cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, float* hi, float* lo,
-                        float* norms, int* bad, cudaStream_t st) {
+cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, const double* centre, float* hi,
+                        float* lo, float* norms, int* bad, cudaStream_t st) {
   count_launch();
-  prep_kernel<false><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, hi, lo, norms, bad);
+  if (centre)
+    prep_kernel<false, true><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, centre, hi, lo,
+                                                                    norms, bad);
+  else
+    prep_kernel<false, false><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, nullptr, hi, lo,
+                                                                     norms, bad);
   return cudaGetLastError();
 }
 
 cudaError_t launch_prep_gather(const float* X, const int64_t* idx, int64_t n, int D, int Dp, int64_t n_pad,
-                               float* hi, float* lo, float* norms, int* bad, cudaStream_t st) {
+                               const double* centre, float* hi, float* lo, float* norms, int* bad,
+                               cudaStream_t st) {
   count_launch();
-  prep_kernel<true><<<grid_for_rows(n_pad), 256, 0, st>>>(X, idx, n, D, Dp, n_pad, hi, lo, norms, bad);
+  if (centre)
+    prep_kernel<true, true><<<grid_for_rows(n_pad), 256, 0, st>>>(X, idx, n, D, Dp, n_pad, centre, hi, lo, norms,
+                                                                   bad);
+  else
+    prep_kernel<true, false><<<grid_for_rows(n_pad), 256, 0, st>>>(X, idx, n, D, Dp, n_pad, nullptr, hi, lo, norms,
+                                                                    bad);
   return cudaGetLastError();
 }
 

@@ -95,8 +95,13 @@ int prohd_set_workspace(prohd_ctx* ctx, void* dptr, size_t bytes) {
   return PROHD_OK;
 }
 
+// Common centre of the pair for K0 (translation invariance, no cancellation far from the
+// origin): kCentreCols = centre(-, B) (the column set alone, so row shards of A on any
+// number of GPUs prepare identical operands), kCentrePair = centre(A, B) (symmetric).
+enum { kCentreCols = 0, kCentrePair = 1 };
+
 static int exact_common(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
-                        ExactWs& w) {
+                        ExactWs& w, int centre_mode, const double* centre_in = nullptr) {
   int rc = enter(ctx);
   if (rc) return rc;
   if ((rc = check_sets(ctx, A, nA, B, nB, D))) return rc;
@@ -112,8 +117,14 @@ static int exact_common(prohd_ctx* ctx, const float* A, int64_t nA, const float*
   bool hi;
   if ((rc = stage_inputs(ctx, A, nA, B, nB, D, w.stageA, w.stageB, hi))) return rc;
   CK(cudaMemsetAsync(w.bad, 0, sizeof(int), ctx->stream));
-  if ((rc = prep_set(ctx, A, nA, D, w.A, w.bad))) return rc;
-  if ((rc = prep_set(ctx, B, nB, D, w.B, w.bad))) return rc;
+  if (centre_in != nullptr)
+    CK(cudaMemcpyAsync(w.centre, centre_in, sizeof(double) * D, cudaMemcpyDefault, ctx->stream));
+  else if (centre_mode == kCentrePair)
+    CK(launch_centre(A, nA, B, nB, D, w.centre, ctx->stream));
+  else
+    CK(launch_centre(nullptr, 0, B, nB, D, w.centre, ctx->stream));
+  if ((rc = prep_set(ctx, A, nA, D, w.A, w.bad, w.centre))) return rc;
+  if ((rc = prep_set(ctx, B, nB, D, w.B, w.bad, w.centre))) return rc;
   return PROHD_OK;
 }
 
@@ -140,7 +151,7 @@ int directed_hd(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int6
                 prohd_directed* out) {
   if (out == nullptr) return fail(ctx, PROHD_E_INVALID, "null output");
   ExactWs w;
-  int rc = exact_common(ctx, A, nA, B, nB, D, w);
+  int rc = exact_common(ctx, A, nA, B, nB, D, w, kCentreCols);
   if (rc) return rc;
   if ((rc = directed_on_ops(ctx, w.A, w.B, D, w, 0))) return rc;
   ExactHost h;
@@ -152,7 +163,7 @@ int directed_hd(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int6
 int hausdorff(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D, prohd_hd* out) {
   if (out == nullptr) return fail(ctx, PROHD_E_INVALID, "null output");
   ExactWs w;
-  int rc = exact_common(ctx, A, nA, B, nB, D, w);
+  int rc = exact_common(ctx, A, nA, B, nB, D, w, kCentrePair);
   if (rc) return rc;
   if ((rc = bidir_on_ops(ctx, w.A, w.B, D, w))) return rc;  // one fused sweep for both directions
   ExactHost h;
@@ -168,7 +179,7 @@ int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* 
   if (rowmin_dev == nullptr || !is_device_ptr(rowmin_dev))
     return fail(ctx, PROHD_E_INVALID, "rowmin_dev must be a device pointer");
   ExactWs w;
-  int rc = exact_common(ctx, A, nA, B, nB, D, w);
+  int rc = exact_common(ctx, A, nA, B, nB, D, w, kCentreCols);
   if (rc) return rc;
   if ((rc = run_dist(ctx, w.A, w.B, D, rowmin_dev))) return rc;
   ExactHost h{};
@@ -181,12 +192,12 @@ int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* 
 }
 
 int directed_hd_local(prohd_ctx* ctx, const float* A_local, int64_t nA_local, int64_t row_offset,
-                      const float* B, int64_t nB, int32_t D, uint64_t* key_out) {
+                      const float* B, int64_t nB, int32_t D, const double* centre, uint64_t* key_out) {
   if (key_out == nullptr) return fail(ctx, PROHD_E_INVALID, "null key_out");
   if (row_offset < 0) return fail(ctx, PROHD_E_INVALID, "negative row_offset");
   if (row_offset + nA_local > 0x7FFFFF00LL) return fail(ctx, PROHD_E_INVALID, "global row too large");
   ExactWs w;
-  int rc = exact_common(ctx, A_local, nA_local, B, nB, D, w);
+  int rc = exact_common(ctx, A_local, nA_local, B, nB, D, w, kCentreCols, centre);
   if (rc) return rc;
   if ((rc = run_dist(ctx, w.A, w.B, D, w.rowmin))) return rc;
   CK(launch_rowmax_key(w.rowmin, nA_local, row_offset, &w.keys[0], ctx->stream));
@@ -198,6 +209,31 @@ int directed_hd_local(prohd_ctx* ctx, const float* A_local, int64_t nA_local, in
   call_collect(ctx);
   if (h.bad) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate");
   *key_out = h.keys[0];
+  return PROHD_OK;
+}
+
+int prohd_centre(prohd_ctx* ctx, const float* X, int64_t nX, const float* Y, int64_t nY, int32_t D,
+                 double* centre_out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (centre_out == nullptr) return fail(ctx, PROHD_E_INVALID, "null centre_out");
+  if (D < 1 || nX < 0 || nY < 0 || nX + nY < 1) return fail(ctx, PROHD_E_INVALID, "bad sizes");
+  if ((nX > 0 && X == nullptr) || (nY > 0 && Y == nullptr)) return fail(ctx, PROHD_E_INVALID, "null input");
+  const int64_t cx = nX < 4096 ? nX : 4096, cy = nY < 4096 ? nY : 4096;
+  if ((cx > 0 && !is_device_ptr(X)) || (cy > 0 && !is_device_ptr(Y)))
+    return fail(ctx, PROHD_E_INVALID, "prohd_centre takes device inputs");
+  Carver dry{nullptr, 0, 0, true};
+  dry.take<double>(2 * static_cast<int64_t>(D));
+  if (ctx->ws == nullptr || ctx->ws_bytes < dry.off)
+    return fail(ctx, PROHD_E_WORKSPACE, "workspace too small: need %zu bytes, have %zu", dry.off, ctx->ws_bytes);
+  Carver c{ctx->ws, 0, ctx->ws_bytes, false};
+  double* cbuf = c.take<double>(2 * static_cast<int64_t>(D));
+  call_begin(ctx);
+  CK(launch_centre(X, cx, Y, cy, D, cbuf, ctx->stream));
+  CK(cudaMemcpyAsync(centre_out, cbuf, sizeof(double) * D, cudaMemcpyDefault, ctx->stream));
+  call_end(ctx);
+  CK(cudaStreamSynchronize(ctx->stream));
+  call_collect(ctx);
   return PROHD_OK;
 }
 
@@ -309,8 +345,9 @@ int hausdorff_subsets(prohd_ctx* ctx, const float* A, int64_t nA, const int64_t*
   CK(launch_gather_offset(A, D, dia, 0, kA, 0, xa, st));
   CK(launch_gather_offset(B, D, dib, 0, kB, 0, xb, st));
   CK(cudaMemsetAsync(w.bad, 0, sizeof(int), st));
-  if ((rc = prep_set(ctx, xa, kA, D, w.A, w.bad))) return rc;
-  if ((rc = prep_set(ctx, xb, kB, D, w.B, w.bad))) return rc;
+  CK(launch_centre(xa, kA, xb, kB, D, w.centre, st));
+  if ((rc = prep_set(ctx, xa, kA, D, w.A, w.bad, w.centre))) return rc;
+  if ((rc = prep_set(ctx, xb, kB, D, w.B, w.bad, w.centre))) return rc;
   if ((rc = bidir_on_ops(ctx, w.A, w.B, D, w))) return rc;
   ExactHost h;
   if ((rc = fetch(ctx, w, h))) return rc;

@@ -38,6 +38,7 @@ struct EstWs {
   double* blk_d = nullptr;
   long long* blk_j = nullptr;
   int* bad = nullptr;
+  double* centre = nullptr;  // [2D] common centre of the subset pair (K0)
   int64_t capU[2] = {0, 0};
 };
 
@@ -66,7 +67,7 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
     w.stageB = c.take<float>(nB * D);
   }
   const MomentsPlan mp = plan_moments(nA, nB, D, num_sms);
-  w.mom.s = c.take<double>(D);
+  w.mom.s = c.take<double>(2 * static_cast<int64_t>(D));  // shift + scratch
   w.mom.Gpart = c.take<double>(mp.gpart_doubles);
   w.mom.Spart = c.take<double>(mp.spart_doubles);
   w.mom.C = c.take<double>(static_cast<int64_t>(D) * D);
@@ -101,6 +102,7 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
   w.blk_d = c.take<double>(kNNBlocks);
   w.blk_j = c.take<long long>(kNNBlocks);
   w.bad = c.take<int>(1);
+  w.centre = c.take<double>(2 * static_cast<int64_t>(D));
   return c.off;
 }
 
@@ -209,10 +211,13 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
 
   // ------------------------------------------------------------ step 4: exact HD on the subsets
   const int t_sub = tmark(ctx);
+  for (int s = 0; s < 2; ++s) CK(launch_gather(X[s], D, w.sel[s].uidx, w.sel[s].ucount, ucount[s], w.Xs[s], st));
+  // one common centre for every operand of the subset HD: centre(A_sel, B_sel) (symmetric;
+  // the sharded driver computes the same from the all-gathered subsets)
+  CK(launch_centre(w.Xs[0], ucount[0], w.Xs[1], ucount[1], D, w.centre, st));
   for (int s = 0; s < 2; ++s) {
-    CK(launch_gather(X[s], D, w.sel[s].uidx, w.sel[s].ucount, ucount[s], w.Xs[s], st));
     w.ops[s].n = ucount[s];
-    if ((rc = prep_set(ctx, w.Xs[s], ucount[s], D, w.ops[s], w.bad))) return rc;
+    if ((rc = prep_set(ctx, w.Xs[s], ucount[s], D, w.ops[s], w.bad, w.centre))) return rc;
   }
   ExactWs ew;
   ew.rowmin = w.rowmin;
@@ -226,8 +231,8 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
     if ((rc = bidir_on_ops(ctx, w.ops[0], w.ops[1], D, ew))) return rc;  // Alg. 3 line 6, both directions
   } else {
     // certified mode (SPEC.md:279 subset-full): rows of each subset against the FULL other set
-    if ((rc = prep_set(ctx, A, nA, D, w.full[0], w.bad))) return rc;
-    if ((rc = prep_set(ctx, B, nB, D, w.full[1], w.bad))) return rc;
+    if ((rc = prep_set(ctx, A, nA, D, w.full[0], w.bad, w.centre))) return rc;
+    if ((rc = prep_set(ctx, B, nB, D, w.full[1], w.bad, w.centre))) return rc;
     if ((rc = directed_on_ops(ctx, w.ops[0], w.full[1], D, ew, 0))) return rc;
     if ((rc = directed_on_ops(ctx, w.ops[1], w.full[0], D, ew, 1))) return rc;
   }

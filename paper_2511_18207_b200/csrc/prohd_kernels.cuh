@@ -8,12 +8,35 @@
 namespace prohd {
 
 // ---------------------------------------------------------------- K1
+// Gram pass (k_gram.cu): groups of <= 4 upper-triangle 32x32 tiles over <= 4 feature blocks
+constexpr int kGramMaxFb = 32;       // D <= 1024
+constexpr int kGramMaxGroups = 136;  // 120 off-diagonal + 12 diagonal groups at D = 1024
+struct GramGroup {
+  unsigned char ntiles, nfb;
+  unsigned char fb[4];   // feature blocks (32 features each) staged in slots 0..3
+  unsigned char si[4];   // tile t = (fb[si[t]], fb[sj[t]])
+  unsigned char sj[4];
+  unsigned char own[4];  // slot s accumulates the column sums of fb[s]
+};
+struct GramPlan {
+  int ngroups = 0, rpg = 0, nctas = 0;
+  int64_t per = 0, gpart_doubles = 0, spart_doubles = 0;
+  int owner[2 * kGramMaxFb];
+  GramGroup grp[kGramMaxGroups];
+};
+bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p);
+cudaError_t launch_gram(const GramPlan& p, const float* A, int64_t nA, const float* B, int64_t nB, int D,
+                        const double* s, double* Gpart, double* Spart, double* Gout, double* SA, double* SB,
+                        cudaStream_t st);
+
 struct MomentsPlan {
   int nb = 0, npairs = 0, c_diag = 0, c_off = 0, nctas = 0, nslots = 0;
+  bool gram = false;  // warp-specialised Gram pass (k_gram.cu); else the legacy 64x64-block kernel
+  GramPlan gp;
   int64_t gpart_doubles = 0, spart_doubles = 0;
 };
 struct MomentsBufs {
-  double* s;      // [D] shift
+  double* s;      // [2D]: shift s (0 unless the offset is large), then D doubles of scratch
   double* Gpart;  // partial Grams
   double* Spart;  // partial column sums
   double* C;      // [D][D] -> covariance

@@ -44,7 +44,7 @@ static size_t carve_shard(Carver& c, ShardWs& w, int64_t nA, int64_t nB, int64_t
     w.stageB = c.take<float>(nB * D);
   }
   const MomentsPlan mp = plan_moments(nA, nB, D, num_sms);
-  w.mom.s = c.take<double>(D);
+  w.mom.s = c.take<double>(2 * static_cast<int64_t>(D));  // shift + scratch
   w.mom.Gpart = c.take<double>(mp.gpart_doubles);
   w.mom.Spart = c.take<double>(mp.spart_doubles);
   w.mom.C = c.take<double>(static_cast<int64_t>(D) * D);

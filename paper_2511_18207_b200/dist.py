@@ -115,12 +115,15 @@ def sharded_prohd_estimate(A_local, offA: int, nA: int, B_local, offB: int, nB: 
         rows, _, _ = phases.gather_owned(X_local, off, union)
         subsets.append(_all_gather_rows(rows, D, device, group))
         unions.append(union)
-    # C4: exact HD on the subsets, rows of each subset sharded over the ranks
+    # C4: exact HD on the subsets, rows of each subset sharded over the ranks; every rank
+    # prepares the distance operands about the same centre(A_sel, B_sel) as prohd_estimate
+    centre = phases.centre(subsets[0], subsets[1])
     res = {}
     for side, (R, Cm, uR, uC) in {"ab": (subsets[0], subsets[1], unions[0], unions[1]),
                                   "ba": (subsets[1], subsets[0], unions[1], unions[0])}.items():
         lo, hi = row_range(R.shape[0], rank, world)
-        r = sharded_directed_hd(R[lo:hi], lo, Cm, phases.local_fn, phases.witness_fn, device=device, group=group)
+        local = (lambda A_l, off, Bm: phases.local_fn(A_l, off, Bm, centre))
+        r = sharded_directed_hd(R[lo:hi], lo, Cm, local, phases.witness_fn, device=device, group=group)
         res[side] = {**r, "a": int(uR[r["a"]].item()), "b": int(uC[r["b"]].item())}
     ab, ba = res["ab"], res["ba"]
     value = ab["dist"] if ab["dist2"] >= ba["dist2"] else ba["dist"]
@@ -137,6 +140,9 @@ class CudaPhases:
 
     def shift(self, A_first, B_first):
         return self.ctx.shift(A_first, B_first)
+
+    def centre(self, X, Y):
+        return self.ctx.centre(X, Y)
 
     def local_moments(self, A_local, B_local, s):
         return self.ctx.local_moments(A_local, B_local, s)
@@ -156,8 +162,8 @@ class CudaPhases:
 
 def cuda_fns(ctx):
     """The product local/witness functions: both run in libprohd.so kernels."""
-    def local_fn(A_local, row_offset, B):
-        return ctx.directed_hd_local(A_local, row_offset, B)
+    def local_fn(A_local, row_offset, B, centre=None):
+        return ctx.directed_hd_local(A_local, row_offset, B, centre)
 
     def witness_fn(a_row, B):
         return ctx.directed_hd_witness(a_row, B)

@@ -75,7 +75,10 @@ class OraclePhases:
         sel = u[(u >= off) & (u < off + X_l.shape[0])] - off
         return torch.as_tensor(np.asarray(X_l)[sel]), 0, len(sel)
 
-    def local_fn(self, Al, off, Bm):
+    def centre(self, X, Y):
+        return None  # the oracle's distances are exact: no translation needed
+
+    def local_fn(self, Al, off, Bm, centre=None):
         rmin, _ = oracle.row_minima(np.asarray(Al), np.asarray(Bm))
         rmin32 = rmin.astype(np.float32)
         i = int(np.argmax(rmin32))

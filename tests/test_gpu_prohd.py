@@ -206,3 +206,35 @@ def test_errors(ctx):
     with pytest.raises(ProHDError) as e:
         ctx.prohd_estimate(An, B, 2, 3)
     assert e.value.code == 3
+
+
+def test_large_offset_uses_shift(ctx):
+    """A common offset far above the spread: the shift kernel keeps s, the Gram pass
+    subtracts it in fp64, and every layer still matches the oracle's two-pass C."""
+    A, B = datagen.generate(2, n=20000)
+    A = (A + np.float32(4096.0)).astype(np.float32)
+    B = (B + np.float32(4096.0)).astype(np.float32)
+    s = ctx.shift(torch.from_numpy(A[:4096]).cuda(), torch.from_numpy(B[:4096]).cuda())
+    assert np.all(s != 0.0)
+    c = datagen.CONFIGS[2]
+    _check_layers(ctx, A, B, c.k, c.m(20000))
+
+
+def test_small_offset_drops_shift(ctx):
+    A, B = datagen.generate(2, n=20000)
+    s = ctx.shift(torch.from_numpy(A[:4096]).cuda(), torch.from_numpy(B[:4096]).cuda())
+    assert np.all(s == 0.0)
+
+
+@pytest.mark.parametrize("D", [13, 16])
+def test_special_values(ctx, D):
+    """Signed zeros and subnormals (the Gram pass converts fp32 -> fp64 on the integer
+    pipe and falls back to F2F for subnormals); D = 13 takes the 4-byte loader path."""
+    rng = np.random.default_rng(11 + D)
+    A = rng.standard_normal((3000, D)).astype(np.float32)
+    B = (rng.standard_normal((2500, D)) + 0.25).astype(np.float32)
+    A[::7, 1] = np.float32(-0.0)
+    A[::11, 2] = np.float32(0.0)
+    A[::13, 3] = np.float32(3e-40)   # subnormal
+    B[::5, 0] = np.float32(-2e-39)   # subnormal
+    _check_layers(ctx, A, B, 3, 9)

@@ -39,13 +39,14 @@ def _sim_sharded(ctx, A, B, k, m, G):
         unions.append(union)
         subsets.append(rows)
     out = {}
+    centre = ctx.centre(subsets[0], subsets[1])  # prohd_estimate's subset-HD centre
     for side, (R, Cm, uR, uC) in {"ab": (subsets[0], subsets[1], unions[0], unions[1]),
                                   "ba": (subsets[1], subsets[0], unions[1], unions[0])}.items():
         keys = []
         for g in range(G):
             lo, hi = row_range(R.shape[0], g, G)
             if hi > lo:
-                keys.append(ctx.directed_hd_local(R[lo:hi], lo, Cm))
+                keys.append(ctx.directed_hd_local(R[lo:hi], lo, Cm, centre))
         key = max(keys)
         _, row = unpack_key(key)
         w = ctx.directed_hd_witness(R[row], Cm)
