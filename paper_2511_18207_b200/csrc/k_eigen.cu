@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include <cfloat>
+#include <cstdlib>
 
 namespace cg = cooperative_groups;
 
@@ -37,6 +38,7 @@ constexpr int kT = 256;      // threads per CTA
 constexpr int kWarps = kT / 32;
 constexpr int kMaxD = 256;
 constexpr int kRows = kMaxD / kCl;  // rows per CTA (max)
+constexpr size_t kEigDynMax = 220 * 1024;  // tail kernel's dynamic smem budget (static use ~6.5 KB)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -78,6 +80,9 @@ struct EigArgs {
   float* out32;   // U32 rows
   double* lam;    // [k] eigenvalues (desc)
   int* n_dirs;    // 1 + kept
+  int j0;         // Householder steps done by the cluster; the rest by CTA 0 in shared memory
+  int stop;       // dev timing only (PROHD_EIG_STOP): return after phase `stop` (0 = run all)
+  double* de;     // [2][kMaxD]: diagonal d, then off-diagonal e of T (global hand-off)
 };
 
 // inverse iteration for eigenvalue `lam` of T (one warp; lane 0 runs the serial solve)
@@ -147,18 +152,16 @@ __device__ void inverse_iteration(const double* d, const double* e, int D, doubl
   }
 }
 
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_cluster_kernel(EigArgs a) {
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduce_cluster_kernel(EigArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
   extern __shared__ double dyn[];
-  double* M = dyn;                   // [kRows][D] own rows (row r -> M[(r/8)*D])
-  double* lu = dyn + kRows * kMaxD;  // [kWarps][3][kMaxD] LU scratch
+  double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/8)*D])
   __shared__ double red[kWarps];
   __shared__ double vfull[kMaxD], pfull[kMaxD], wfull[kMaxD];
   __shared__ double part[kCl], part2[kCl];
-  __shared__ double d[kMaxD], e[kMaxD], e2[kMaxD], lamv[kMaxD];
+  __shared__ double d[kMaxD], e[kMaxD];
   __shared__ double s_x0;
-  __shared__ int s_prev[kWarps][16];
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nloc = (D - rank + kCl - 1) / kCl;  // rows r = rank + 8*i, i < nloc
@@ -169,7 +172,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_clust
   cl.sync();
 
   // ---------------------------------------------------------------- 1. tridiagonalise
-  for (int j = 0; j + 2 < D; ++j) {
+  // 1a. steps j < j0 on the cluster (the trailing matrix does not fit one SM yet)
+  for (int j = 0; j + 2 < D && j < a.j0; ++j) {
     // phase 1: publish d[j], x0 = M[j+1][j], and this CTA's sum of squares of column j below j
     if (tid == 0 && (j % kCl) == rank) {
       const double v = M[(j / kCl) * D + j];
@@ -240,24 +244,168 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_clust
     }
     __syncthreads();
   }
-  // last 2x2 block
-  if (tid == 0 && D >= 2 && ((D - 2) % kCl) == rank) {
-    const double v = M[((D - 2) / kCl) * D + (D - 2)];
-    for (int q = 0; q < kCl; ++q) *cl.map_shared_rank(&d[D - 2], q) = v;
+  // hand-off of the trailing lower triangle (rows/cols >= j0) through global scratch P,
+  // packed row by row: L(r, c) at po(r) + c - j0, po(r) = t (t + 1) / 2 with t = r - j0;
+  // and d, e of the cluster steps
+  const int j0 = a.j0;
+  double* P = a.V + static_cast<int64_t>(j0) * D;
+  for (int i = 0; i < nloc; ++i) {
+    const int r = rank + kCl * i;
+    if (r < j0) continue;
+    const int t = r - j0;
+    for (int c = j0 + tid; c <= r; c += kT) P[t * (t + 1) / 2 + (c - j0)] = M[i * D + c];
   }
-  if (tid == 0 && ((D - 1) % kCl) == rank) {
-    const int i = (D - 1) / kCl;
-    const double dv = M[i * D + (D - 1)];
-    const double ev = D >= 2 ? M[i * D + (D - 2)] : 0.0;
-    for (int q = 0; q < kCl; ++q) {
-      *cl.map_shared_rank(&d[D - 1], q) = dv;
-      if (D >= 2) *cl.map_shared_rank(&e[D - 2], q) = ev;
+  if (rank == 0)
+    for (int j = tid; j < j0; j += kT) {
+      a.de[j] = d[j];
+      a.de[kMaxD + j] = e[j];
     }
+}
+
+// Steps j0 .. D-3 of the Householder tridiagonalisation on ONE CTA of 1024 threads with the
+// packed trailing lower triangle in shared memory (every step needs only CTA barriers):
+//   column j -> v (V row j), p = 2 M v (warp per row: lanes along the row for the stored
+//   lower part, down the column for the mirrored upper part, 8 rows per warp reduced by one
+//   butterfly), K = v.p, w = p - K v, L -= v w^T + w v^T (warp per row).
+// j0 = 0: the triangle is read from C directly. Writes d, e (de) and V rows j0 .. D-3.
+constexpr int kTT = 1024;
+constexpr int kTW = kTT / 32;
+
+__device__ __forceinline__ double block_sum_t(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = (l < kTW) ? red[l] : 0.0;
+  return warp_sum(t);
+}
+
+__global__ void __launch_bounds__(kTT, 1) eigen_reduce_tail_kernel(EigArgs a) {
+  extern __shared__ double L[];
+  __shared__ double red[kTW];
+  __shared__ double vfull[kMaxD], pfull[kMaxD], wfull[kMaxD];
+  __shared__ double s_x0;
+  const int D = a.D, j0 = a.j0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto po = [&](int r) { return (r - j0) * (r - j0 + 1) / 2; };
+  const int nt = (D - j0) * (D - j0 + 1) / 2;
+  if (j0 == 0) {
+    for (int r = warp; r < D; r += kTW)
+      for (int c = lane; c <= r; c += 32) L[po(r) + c] = a.C[static_cast<int64_t>(r) * D + c];
+  } else {
+    const double* P = a.V + static_cast<int64_t>(j0) * D;
+    for (int t = tid; t < nt; t += kTT) L[t] = P[t];
   }
-  cl.sync();
+  __syncthreads();
+  double* dg = a.de;
+  double* eg = a.de + kMaxD;
+  for (int j = j0; j + 2 < D; ++j) {
+    const int n1 = D - j - 1;  // rows r = j+1 .. D-1
+    const double x = tid < n1 ? L[po(j + 1 + tid) + (j - j0)] : 0.0;
+    if (tid == 0) {
+      dg[j] = L[po(j) + (j - j0)];
+      s_x0 = x;
+    }
+    const double nrm2 = block_sum_t(x * x, red);
+    const double nrm = sqrt(nrm2);
+    const double x0 = s_x0;
+    const double alpha = (x0 > 0.0) ? -nrm : nrm;
+    const double v0 = x0 - alpha;
+    const double vn2 = nrm2 - x0 * x0 + v0 * v0;
+    const double sc = (vn2 > 0.0 && nrm > 0.0) ? 1.0 / sqrt(vn2) : 0.0;
+    if (tid == 0) eg[j] = (sc != 0.0) ? alpha : 0.0;
+    if (tid < n1) {
+      const double v = ((tid == 0) ? v0 : x) * sc;
+      vfull[j + 1 + tid] = v;
+      a.V[static_cast<int64_t>(j) * D + j + 1 + tid] = v;
+    }
+    __syncthreads();
+    if (sc == 0.0) continue;  // uniform
+    // p = 2 M v: warp w owns rows r_i = j+1+w+32 i (i < 8)
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      acc[i] = 0.0;
+      const int r = j + 1 + warp + kTW * i;
+      if (r < D) {
+        const double* row = L + po(r) - j0;
+        double s = 0.0;
+        for (int c = j + 1 + lane; c <= r; c += 32) s = fma(row[c], vfull[c], s);
+        for (int c = r + 1 + lane; c < D; c += 32) s = fma(L[po(c) + (r - j0)], vfull[c], s);
+        acc[i] = s;
+      }
+    }
+    // butterfly reduce-scatter of the 8 row sums: lane l ends with row i = (l >> 2) & 7
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool up = (lane & 16) != 0;
+      const double send = up ? acc[i] : acc[i + 4];
+      const double keep = up ? acc[i + 4] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const bool up = (lane & 8) != 0;
+      const double send = up ? acc[i] : acc[i + 2];
+      const double keep = up ? acc[i + 2] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+      const bool up = (lane & 4) != 0;
+      const double send = up ? acc[0] : acc[1];
+      const double keep = up ? acc[1] : acc[0];
+      acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+    double vp = 0.0;
+    {
+      const int ri = (lane >> 2) & 7;
+      const int r = j + 1 + warp + kTW * ri;
+      if ((lane & 3) == 0 && r < D) {
+        const double pr = 2.0 * acc[0];
+        pfull[r] = pr;
+        vp = pr * vfull[r];
+      }
+    }
+    const double K = block_sum_t(vp, red);
+    if (tid < n1) wfull[j + 1 + tid] = pfull[j + 1 + tid] - K * vfull[j + 1 + tid];
+    __syncthreads();
+    for (int r = j + 1 + warp; r < D; r += kTW) {
+      double* row = L + po(r) - j0;
+      const double vr = vfull[r], wr = wfull[r];
+      for (int c = j + 1 + lane; c <= r; c += 32) row[c] -= vr * wfull[c] + wr * vfull[c];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const int jl = D >= 2 ? D - 2 : 0;
+    if (D >= 2 && jl >= j0) dg[D - 2] = L[po(D - 2) + (D - 2 - j0)];
+    dg[D - 1] = L[po(D - 1) + (D - 1 - j0)];
+    if (D >= 2) eg[D - 2] = L[po(D - 1) + (D - 2 - j0)];
+  }
+}
+
+// Eigenvalues (bisection), eigenvectors of T (inverse iteration) and the back-transform,
+// on the cluster, from d, e (de) and the Householder vectors (V).
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vectors_cluster_kernel(EigArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = static_cast<int>(cl.block_rank());
+  extern __shared__ double dyn[];
+  double* lu = dyn;  // [kWarps][3][kMaxD] LU scratch
+  __shared__ double d[kMaxD], e[kMaxD], e2[kMaxD], lamv[kMaxD];
+  __shared__ int s_prev[kWarps][16];
+  const int D = a.D;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < D; i += kT) {
+    d[i] = a.de[i];
+    e[i] = i < D - 1 ? a.de[kMaxD + i] : 0.0;
+  }
+  __syncthreads();
+  if (a.stop == 1) return;
   for (int i = tid; i < D - 1; i += kT) e2[i] = e[i] * e[i];
   __syncthreads();
-
   // ---------------------------------------------------------------- 2. eigenvalues (every CTA, redundantly)
   double gl = DBL_MAX, gu = -DBL_MAX;
   for (int i = 0; i < D; ++i) {
@@ -268,7 +416,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_clust
   const double tnorm = fmax(fabs(gl), fabs(gu));
   const double pivmin = fmax(DBL_MIN, 1e-300 * tnorm) + DBL_MIN;
   const int kk = a.k < D ? a.k : D;
-  for (int w = warp; w < kk; w += kWarps) {
+  // one warp per eigenvalue across the whole cluster (warp slot rank * kWarps + warp)
+  for (int w = rank * kWarps + warp; w < kk; w += kCl * kWarps) {
     const int target = D - 1 - w;  // the eigenvalue with exactly `target` eigenvalues below it
     double lo = gl - 1e-12 * tnorm - pivmin, hi = gu + 1e-12 * tnorm + pivmin;
     for (int it = 0; it < 64; ++it) {
@@ -283,13 +432,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_clust
       lo = nlo;
       hi = nhi;
     }
-    if (lane == 0) lamv[w] = 0.5 * (lo + hi);
+    if (lane < kCl) *cl.map_shared_rank(&lamv[w], lane) = 0.5 * (lo + hi);
   }
-  __syncthreads();
+  cl.sync();
+  if (a.stop == 2) return;
 
   // ---------------------------------------------------------------- 3. inverse iteration
-  // clusters of consecutive eigenvalues closer than 1e-3 ||T|| are handled by one warp in order
-  const double clus = 1e-3 * tnorm;
+  // Consecutive eigenvalues closer than 1e-6 ||T|| form a cluster, handled by one warp in
+  // order with re-orthogonalisation (as LAPACK's dstein); every other eigenvector comes from
+  // an independent inverse iteration on its own warp, whose error eps ||T|| / gap stays
+  // below ~1e-10 at that gap (dstein's 1e-3 ||T|| would serialise spectra such as cfg4's,
+  // top-16 relative gaps ~1e-4, onto a single warp).
+  const double clus = 1e-6 * tnorm;
   {
     int c = 0;  // cluster index
     int start = 0;
@@ -313,6 +467,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_clust
     }
   }
   cl.sync();  // eigenvectors of T (global memory) visible to the whole cluster
+  if (a.stop == 3) return;
 
   // ---------------------------------------------------------------- 4. back-transform, sign, output
   for (int w = rank * kWarps + warp; w < kk; w += kCl * kWarps) {
@@ -373,13 +528,34 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_clust
 cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, double* out64, float* out32,
                               double* lam, int* n_dirs, cudaStream_t st) {
   if (D > kMaxD) return cudaErrorInvalidValue;
-  EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs};
-  const size_t smem = sizeof(double) * (static_cast<size_t>(kRows) * kMaxD + static_cast<size_t>(kWarps) * 3 * kMaxD);
-  cudaError_t e = cudaFuncSetAttribute(eigen_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
+  // cluster steps until the packed trailing triangle fits the tail kernel's shared memory
+  int npk = D;
+  while (npk > 2 && sizeof(double) * static_cast<size_t>(npk) * (npk + 1) / 2 > kEigDynMax) --npk;
+  const int j0 = D - npk;
+  const size_t packed = sizeof(double) * static_cast<size_t>(npk) * (npk + 1) / 2;
+  const char* es = getenv("PROHD_EIG_STOP");
+  EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs, j0, es != nullptr ? atoi(es) : 0,
+            V + static_cast<int64_t>(D) * D};
+  cudaError_t e;
+  if (j0 > 0) {
+    const size_t smem = sizeof(double) * static_cast<size_t>(kRows) * kMaxD;
+    if ((e = cudaFuncSetAttribute(eigen_reduce_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem))) != cudaSuccess)
+      return e;
+    count_launch();
+    eigen_reduce_cluster_kernel<<<kCl, kT, smem, st>>>(a);
+  }
+  if ((e = cudaFuncSetAttribute(eigen_reduce_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(packed))) != cudaSuccess)
+    return e;
   count_launch();
-  eigen_cluster_kernel<<<kCl, kT, smem, st>>>(a);
+  eigen_reduce_tail_kernel<<<1, kTT, packed, st>>>(a);
+  const size_t smem3 = sizeof(double) * static_cast<size_t>(kWarps) * 3 * kMaxD;
+  if ((e = cudaFuncSetAttribute(eigen_vectors_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem3))) != cudaSuccess)
+    return e;
+  count_launch();
+  eigen_vectors_cluster_kernel<<<kCl, kT, smem3, st>>>(a);
   return cudaGetLastError();
 }
 

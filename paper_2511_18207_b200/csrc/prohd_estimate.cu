@@ -75,7 +75,7 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
   w.mom.SB = c.take<double>(D);
   w.mom.mu = c.take<double>(D);
   w.mom.dnorm = c.take<double>(1);
-  w.V = c.take<double>(static_cast<int64_t>(D) * D);
+  w.V = c.take<double>(static_cast<int64_t>(D) * D + 2 * 256);  // Householder vectors + d, e of T
   w.Xe = c.take<double>(static_cast<int64_t>(k > 0 ? k : 1) * D);
   w.U64 = c.take<double>(static_cast<int64_t>(L) * D);
   w.mom.u0 = w.U64;  // row 0 of U is the centroid axis
