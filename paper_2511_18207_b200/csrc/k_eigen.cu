@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 
 namespace cg = cooperative_groups;
@@ -38,22 +39,11 @@ constexpr int kT = 256;      // threads per CTA
 constexpr int kWarps = kT / 32;
 constexpr int kMaxD = 256;
 constexpr int kRows = kMaxD / kCl;  // rows per CTA (max)
-constexpr size_t kEigDynMax = 220 * 1024;  // tail kernel's dynamic smem budget (static use ~6.5 KB)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-__device__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  double t = (l < kWarps) ? red[l] : 0.0;
-  return warp_sum(t);
 }
 
 // number of eigenvalues of T (d, e2 = e^2) strictly less than x (Sturm count)
@@ -80,7 +70,6 @@ struct EigArgs {
   float* out32;   // U32 rows
   double* lam;    // [k] eigenvalues (desc)
   int* n_dirs;    // 1 + kept
-  int j0;         // Householder steps done by the cluster; the rest by CTA 0 in shared memory
   int stop;       // dev timing only (PROHD_EIG_STOP): return after phase `stop` (0 = run all)
   double* de;     // [2][kMaxD]: diagonal d, then off-diagonal e of T (global hand-off)
 };
@@ -152,16 +141,24 @@ __device__ void inverse_iteration(const double* d, const double* e, int D, doubl
   }
 }
 
+// Householder tridiagonalisation T = Q^T C Q on one 8-CTA cluster (Golub & Van Loan
+// 8.3.1). Row r of C lives in CTA r % 8 as a full row in shared memory (<= 32 rows x 256
+// fp64). Step j, with two cluster barriers:
+//   A. every CTA scatters its rows' column-j entries (r > j) into every CTA's colbuf
+//      (DSMEM stores); the owner of row j scatters d_j.               -> barrier A
+//   B. each CTA forms the norm, alpha and v = (x - alpha e1)/||.|| redundantly from the
+//      full column, computes p_r = 2 sum_c M[r][c] v_c for its rows (warp per row,
+//      lanes along the contiguous row) and scatters p_r and its v.p partial.  -> barrier B
+//   C. K = v.p, w = p - K v, and M[r][c] -= v_r w_c + w_r v_c on its own rows.
+// Writes d, e (de) and the Householder vectors (V rows 0 .. D-3).
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduce_cluster_kernel(EigArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
   extern __shared__ double dyn[];
   double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/8)*D])
-  __shared__ double red[kWarps];
-  __shared__ double vfull[kMaxD], pfull[kMaxD], wfull[kMaxD];
-  __shared__ double part[kCl], part2[kCl];
-  __shared__ double d[kMaxD], e[kMaxD];
-  __shared__ double s_x0;
+  __shared__ double colbuf2[2][kMaxD], pbuf[kMaxD];  // colbuf double-buffered: step j uses [j & 1]
+  __shared__ double vpart[kCl * kWarps];
+  __shared__ double s_d;
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nloc = (D - rank + kCl - 1) / kCl;  // rows r = rank + 8*i, i < nloc
@@ -169,221 +166,86 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
     const int i = t / D, c = t % D;
     M[i * D + c] = a.C[static_cast<int64_t>(rank + kCl * i) * D + c];
   }
-  cl.sync();
-
-  // ---------------------------------------------------------------- 1. tridiagonalise
-  // 1a. steps j < j0 on the cluster (the trailing matrix does not fit one SM yet)
-  for (int j = 0; j + 2 < D && j < a.j0; ++j) {
-    // phase 1: publish d[j], x0 = M[j+1][j], and this CTA's sum of squares of column j below j
-    if (tid == 0 && (j % kCl) == rank) {
-      const double v = M[(j / kCl) * D + j];
-      for (int q = 0; q < kCl; ++q) *cl.map_shared_rank(&d[j], q) = v;
-    }
-    if (tid == 0 && ((j + 1) % kCl) == rank) {
-      const double v = M[((j + 1) / kCl) * D + j];
-      for (int q = 0; q < kCl; ++q) *cl.map_shared_rank(&s_x0, q) = v;
-    }
-    double ps = 0.0;
-    for (int i = tid; i < nloc; i += kT) {
+  __syncthreads();
+  double* dg = a.de;
+  double* eg = a.de + kMaxD;
+  for (int j = 0; j + 2 < D; ++j) {
+    double* colbuf = colbuf2[j & 1];  // step j+1 may scatter while a slow CTA still reads step j's
+    // A. scatter column j (rows > j) and d_j into every CTA
+    {
+      const int i = tid / kCl, q = tid % kCl;  // own row slot i, target CTA q
       const int r = rank + kCl * i;
-      if (r > j) {
-        const double x = M[i * D + j];
-        ps += x * x;
-      }
+      if (i < nloc && r > j) *cl.map_shared_rank(&colbuf[r], q) = M[i * D + j];
+      if (j % kCl == rank && tid < kCl) *cl.map_shared_rank(&s_d, tid) = M[(j / kCl) * D + j];
     }
-    ps = block_sum(ps, red);
-    if (tid < kCl) *cl.map_shared_rank(&part[rank], tid) = ps;
     cl.sync();
-    // phase 2: every CTA forms alpha and the scale redundantly; publish own entries of v
-    double nrm2 = 0.0;
-#pragma unroll
-    for (int q = 0; q < kCl; ++q) nrm2 += part[q];
+    // B. every warp forms ||x||, alpha and the scale itself (no CTA barrier); v_c is
+    // recomputed on the fly as vc(c) = (c == j+1 ? x0 - alpha : colbuf[c]) * sc
+    double ss = 0.0;
+    for (int c = j + 1 + lane; c < D; c += 32) ss = fma(colbuf[c], colbuf[c], ss);
+    const double nrm2 = warp_sum(ss);
     const double nrm = sqrt(nrm2);
-    const double x0 = s_x0;
+    const double x0 = colbuf[j + 1];
     const double alpha = (x0 > 0.0) ? -nrm : nrm;
     const double v0 = x0 - alpha;
     const double vn2 = nrm2 - x0 * x0 + v0 * v0;
     const double sc = (vn2 > 0.0 && nrm > 0.0) ? 1.0 / sqrt(vn2) : 0.0;
-    if (tid == 0) e[j] = (sc != 0.0) ? alpha : 0.0;
-    for (int t = tid; t < nloc * kCl; t += kT) {
-      const int i = t / kCl, q = t % kCl;
-      const int r = rank + kCl * i;
-      double v = 0.0;
-      if (r > j) v = ((r == j + 1) ? v0 : M[i * D + j]) * sc;
-      if (r > j) *cl.map_shared_rank(&vfull[r], q) = v;
-      if (q == 0) a.V[static_cast<int64_t>(j) * D + r] = v;
+    auto vc = [&](int c) { return (c == j + 1 ? v0 : colbuf[c]) * sc; };
+    if (rank == 0) {
+      if (tid == 0) {
+        dg[j] = s_d;
+        eg[j] = (sc != 0.0) ? alpha : 0.0;
+      }
+      for (int c = j + 1 + tid; c < D; c += kT) a.V[static_cast<int64_t>(j) * D + c] = vc(c);
     }
-    cl.sync();
-    if (sc == 0.0) continue;  // column already zero below the subdiagonal: H = I (uniform decision)
-    // phase 3: p_r = 2 sum_c M[r][c] v_c (own rows r > j), and v^T p partial
+    if (sc == 0.0) {  // column already zero below the subdiagonal: H = I (uniform decision)
+      cl.sync();      // everyone is done reading colbuf before step j+1 scatters into it
+      continue;
+    }
+    // p_r = 2 M[r][j+1:] . v for own rows r > j (warp per row); v.p partial per warp
     double vp = 0.0;
     for (int i = warp; i < nloc; i += kWarps) {
       const int r = rank + kCl * i;
       if (r <= j) continue;
       const double* row = M + i * D;
-      double s = 0.0;
-      for (int c = j + 1 + lane; c < D; c += 32) s += row[c] * vfull[c];
-      s = 2.0 * warp_sum(s);
-      if (lane < kCl) *cl.map_shared_rank(&pfull[r], lane) = s;
-      vp += (lane == 0) ? s * vfull[r] : 0.0;
+      double s0 = 0.0, s1 = 0.0;
+      int c = j + 1 + lane;
+      for (; c + 32 < D; c += 64) {
+        s0 = fma(row[c], vc(c), s0);
+        s1 = fma(row[c + 32], vc(c + 32), s1);
+      }
+      if (c < D) s0 = fma(row[c], vc(c), s0);
+      const double pr = 2.0 * warp_sum(s0 + s1);
+      if (lane < kCl) *cl.map_shared_rank(&pbuf[r], lane) = pr;
+      vp += pr * vc(r);
     }
-    vp = block_sum(vp, red);
-    if (tid < kCl) *cl.map_shared_rank(&part2[rank], tid) = vp;
+    if (lane < kCl) *cl.map_shared_rank(&vpart[rank * kWarps + warp], lane) = vp;
     cl.sync();
-    // phase 4: w = p - (v^T p) v, then A' -= v w^T + w v^T on own rows
+    // C. K = v.p; M[r][c] -= v_r w_c + w_r v_c with w = p - K v, on own rows
     double K = 0.0;
-#pragma unroll
-    for (int q = 0; q < kCl; ++q) K += part2[q];
-    for (int c = j + 1 + tid; c < D; c += kT) wfull[c] = pfull[c] - K * vfull[c];
-    __syncthreads();
-    for (int t = tid; t < nloc * (D - j - 1); t += kT) {
-      const int i = t / (D - j - 1), c = j + 1 + t % (D - j - 1);
+    for (int q = lane; q < kCl * kWarps; q += 32) K += vpart[q];
+    K = warp_sum(K);
+    for (int i = warp; i < nloc; i += kWarps) {
       const int r = rank + kCl * i;
       if (r <= j) continue;
-      M[i * D + c] -= vfull[r] * wfull[c] + wfull[r] * vfull[c];
-    }
-    __syncthreads();
-  }
-  // hand-off of the trailing lower triangle (rows/cols >= j0) through global scratch P,
-  // packed row by row: L(r, c) at po(r) + c - j0, po(r) = t (t + 1) / 2 with t = r - j0;
-  // and d, e of the cluster steps
-  const int j0 = a.j0;
-  double* P = a.V + static_cast<int64_t>(j0) * D;
-  for (int i = 0; i < nloc; ++i) {
-    const int r = rank + kCl * i;
-    if (r < j0) continue;
-    const int t = r - j0;
-    for (int c = j0 + tid; c <= r; c += kT) P[t * (t + 1) / 2 + (c - j0)] = M[i * D + c];
-  }
-  if (rank == 0)
-    for (int j = tid; j < j0; j += kT) {
-      a.de[j] = d[j];
-      a.de[kMaxD + j] = e[j];
-    }
-}
-
-// Steps j0 .. D-3 of the Householder tridiagonalisation on ONE CTA of 1024 threads with the
-// packed trailing lower triangle in shared memory (every step needs only CTA barriers):
-//   column j -> v (V row j), p = 2 M v (warp per row: lanes along the row for the stored
-//   lower part, down the column for the mirrored upper part, 8 rows per warp reduced by one
-//   butterfly), K = v.p, w = p - K v, L -= v w^T + w v^T (warp per row).
-// j0 = 0: the triangle is read from C directly. Writes d, e (de) and V rows j0 .. D-3.
-constexpr int kTT = 1024;
-constexpr int kTW = kTT / 32;
-
-__device__ __forceinline__ double block_sum_t(double v, double* red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  double t = (l < kTW) ? red[l] : 0.0;
-  return warp_sum(t);
-}
-
-__global__ void __launch_bounds__(kTT, 1) eigen_reduce_tail_kernel(EigArgs a) {
-  extern __shared__ double L[];
-  __shared__ double red[kTW];
-  __shared__ double vfull[kMaxD], pfull[kMaxD], wfull[kMaxD];
-  __shared__ double s_x0;
-  const int D = a.D, j0 = a.j0;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  auto po = [&](int r) { return (r - j0) * (r - j0 + 1) / 2; };
-  const int nt = (D - j0) * (D - j0 + 1) / 2;
-  if (j0 == 0) {
-    for (int r = warp; r < D; r += kTW)
-      for (int c = lane; c <= r; c += 32) L[po(r) + c] = a.C[static_cast<int64_t>(r) * D + c];
-  } else {
-    const double* P = a.V + static_cast<int64_t>(j0) * D;
-    for (int t = tid; t < nt; t += kTT) L[t] = P[t];
-  }
-  __syncthreads();
-  double* dg = a.de;
-  double* eg = a.de + kMaxD;
-  for (int j = j0; j + 2 < D; ++j) {
-    const int n1 = D - j - 1;  // rows r = j+1 .. D-1
-    const double x = tid < n1 ? L[po(j + 1 + tid) + (j - j0)] : 0.0;
-    if (tid == 0) {
-      dg[j] = L[po(j) + (j - j0)];
-      s_x0 = x;
-    }
-    const double nrm2 = block_sum_t(x * x, red);
-    const double nrm = sqrt(nrm2);
-    const double x0 = s_x0;
-    const double alpha = (x0 > 0.0) ? -nrm : nrm;
-    const double v0 = x0 - alpha;
-    const double vn2 = nrm2 - x0 * x0 + v0 * v0;
-    const double sc = (vn2 > 0.0 && nrm > 0.0) ? 1.0 / sqrt(vn2) : 0.0;
-    if (tid == 0) eg[j] = (sc != 0.0) ? alpha : 0.0;
-    if (tid < n1) {
-      const double v = ((tid == 0) ? v0 : x) * sc;
-      vfull[j + 1 + tid] = v;
-      a.V[static_cast<int64_t>(j) * D + j + 1 + tid] = v;
-    }
-    __syncthreads();
-    if (sc == 0.0) continue;  // uniform
-    // p = 2 M v: warp w owns rows r_i = j+1+w+32 i (i < 8)
-    double acc[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      acc[i] = 0.0;
-      const int r = j + 1 + warp + kTW * i;
-      if (r < D) {
-        const double* row = L + po(r) - j0;
-        double s = 0.0;
-        for (int c = j + 1 + lane; c <= r; c += 32) s = fma(row[c], vfull[c], s);
-        for (int c = r + 1 + lane; c < D; c += 32) s = fma(L[po(c) + (r - j0)], vfull[c], s);
-        acc[i] = s;
+      double* row = M + i * D;
+      const double vr = vc(r), wr = pbuf[r] - K * vr;
+      for (int c = j + 1 + lane; c < D; c += 32) {
+        const double v = vc(c);
+        row[c] -= vr * (pbuf[c] - K * v) + wr * v;
       }
     }
-    // butterfly reduce-scatter of the 8 row sums: lane l ends with row i = (l >> 2) & 7
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const bool up = (lane & 16) != 0;
-      const double send = up ? acc[i] : acc[i + 4];
-      const double keep = up ? acc[i + 4] : acc[i];
-      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const bool up = (lane & 8) != 0;
-      const double send = up ? acc[i] : acc[i + 2];
-      const double keep = up ? acc[i + 2] : acc[i];
-      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    {
-      const bool up = (lane & 4) != 0;
-      const double send = up ? acc[0] : acc[1];
-      const double keep = up ? acc[1] : acc[0];
-      acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
-    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
-    double vp = 0.0;
-    {
-      const int ri = (lane >> 2) & 7;
-      const int r = j + 1 + warp + kTW * ri;
-      if ((lane & 3) == 0 && r < D) {
-        const double pr = 2.0 * acc[0];
-        pfull[r] = pr;
-        vp = pr * vfull[r];
-      }
-    }
-    const double K = block_sum_t(vp, red);
-    if (tid < n1) wfull[j + 1 + tid] = pfull[j + 1 + tid] - K * vfull[j + 1 + tid];
-    __syncthreads();
-    for (int r = j + 1 + warp; r < D; r += kTW) {
-      double* row = L + po(r) - j0;
-      const double vr = vfull[r], wr = wfull[r];
-      for (int c = j + 1 + lane; c <= r; c += 32) row[c] -= vr * wfull[c] + wr * vfull[c];
-    }
     __syncthreads();
   }
-  if (tid == 0) {
-    const int jl = D >= 2 ? D - 2 : 0;
-    if (D >= 2 && jl >= j0) dg[D - 2] = L[po(D - 2) + (D - 2 - j0)];
-    dg[D - 1] = L[po(D - 1) + (D - 1 - j0)];
-    if (D >= 2) eg[D - 2] = L[po(D - 1) + (D - 2 - j0)];
+  // last 2x2 block
+  if (D >= 2 && ((D - 2) % kCl) == rank && tid == 0) {
+    const int i = (D - 2) / kCl;
+    dg[D - 2] = M[i * D + (D - 2)];
+  }
+  if (((D - 1) % kCl) == rank && tid == 0) {
+    const int i = (D - 1) / kCl;
+    dg[D - 1] = M[i * D + (D - 1)];
+    if (D >= 2) eg[D - 2] = M[i * D + (D - 2)];
   }
 }
 
@@ -472,14 +334,37 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
   // ---------------------------------------------------------------- 4. back-transform, sign, output
   for (int w = rank * kWarps + warp; w < kk; w += kCl * kWarps) {
     double* y = a.X + static_cast<int64_t>(w) * D;
-    for (int j = D - 3; j >= 0; --j) {
-      const double* v = a.V + static_cast<int64_t>(j) * D;
-      double s = 0.0;
-      for (int i = j + 1 + lane; i < D; i += 32) s += v[i] * y[i];
-      s = warp_sum(s);
-      for (int i = j + 1 + lane; i < D; i += 32) y[i] -= 2.0 * s * v[i];
-      __syncwarp();
+    // y <- H_0 H_1 ... H_{D-3} y with y in registers (lane holds y[lane + 32 t]) and the next
+    // reflector's row prefetched into registers while the current one is applied
+    constexpr int kYT = kMaxD / 32;
+    double yr[kYT], vn[kYT];
+#pragma unroll
+    for (int t = 0; t < kYT; ++t) {
+      const int i = lane + 32 * t;
+      yr[t] = i < D ? y[i] : 0.0;
+      vn[t] = (D >= 3 && i < D) ? a.V[static_cast<int64_t>(D - 3) * D + i] : 0.0;
     }
+    for (int j = D - 3; j >= 0; --j) {
+      double vc[kYT];
+#pragma unroll
+      for (int t = 0; t < kYT; ++t) {
+        const int i = lane + 32 * t;
+        vc[t] = i > j ? vn[t] : 0.0;  // V row j holds v_j[i] for i > j only
+        if (j > 0 && i < D) vn[t] = a.V[static_cast<int64_t>(j - 1) * D + i];
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < kYT; ++t) s = fma(vc[t], yr[t], s);
+      s = 2.0 * warp_sum(s);
+#pragma unroll
+      for (int t = 0; t < kYT; ++t) yr[t] = fma(-s, vc[t], yr[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < kYT; ++t) {
+      const int i = lane + 32 * t;
+      if (i < D) y[i] = yr[t];
+    }
+    __syncwarp();
     double s = 0.0;
     for (int i = lane; i < D; i += 32) s += y[i] * y[i];
     s = warp_sum(s);
@@ -528,28 +413,15 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
 cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, double* out64, float* out32,
                               double* lam, int* n_dirs, cudaStream_t st) {
   if (D > kMaxD) return cudaErrorInvalidValue;
-  // cluster steps until the packed trailing triangle fits the tail kernel's shared memory
-  int npk = D;
-  while (npk > 2 && sizeof(double) * static_cast<size_t>(npk) * (npk + 1) / 2 > kEigDynMax) --npk;
-  const int j0 = D - npk;
-  const size_t packed = sizeof(double) * static_cast<size_t>(npk) * (npk + 1) / 2;
   const char* es = getenv("PROHD_EIG_STOP");
-  EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs, j0, es != nullptr ? atoi(es) : 0,
-            V + static_cast<int64_t>(D) * D};
+  EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs, es != nullptr ? atoi(es) : 0, V + static_cast<int64_t>(D) * D};
   cudaError_t e;
-  if (j0 > 0) {
-    const size_t smem = sizeof(double) * static_cast<size_t>(kRows) * kMaxD;
-    if ((e = cudaFuncSetAttribute(eigen_reduce_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem))) != cudaSuccess)
-      return e;
-    count_launch();
-    eigen_reduce_cluster_kernel<<<kCl, kT, smem, st>>>(a);
-  }
-  if ((e = cudaFuncSetAttribute(eigen_reduce_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(packed))) != cudaSuccess)
+  const size_t smem = sizeof(double) * static_cast<size_t>(kRows) * kMaxD;
+  if ((e = cudaFuncSetAttribute(eigen_reduce_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem))) != cudaSuccess)
     return e;
   count_launch();
-  eigen_reduce_tail_kernel<<<1, kTT, packed, st>>>(a);
+  eigen_reduce_cluster_kernel<<<kCl, kT, smem, st>>>(a);
   const size_t smem3 = sizeof(double) * static_cast<size_t>(kWarps) * 3 * kMaxD;
   if ((e = cudaFuncSetAttribute(eigen_vectors_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem3))) != cudaSuccess)

@@ -183,111 +183,6 @@ __global__ void __launch_bounds__(kPP, 2) project_tile_kernel(const float* __res
   if (tid == 0) atomicMax(maxnorm2, bm);
 }
 
-// K3 (FFMA2 form): as project_tile_kernel, but two directions per instruction. The
-// directions are staged transposed and zero-padded to Lp = 2 NP (a multiple of 4):
-// su[f][0..Lp), so one float4 broadcast load feeds two FFMA2 (fma.rn.f32x2, the point's
-// x_f as the scalar operand of both lanes). Every direction still accumulates
-// fma(x_f, u_lf, acc) over f in ascending order, so P32 is bit-identical to the scalar
-// kernel's and the K4 guard band (eps = (D + 8) 2^-24 max||x||) still bounds |pi32 - pi64|.
-__device__ __forceinline__ void ffma2_bcast(unsigned long long& acc, float x, float2 u) {
-  unsigned long long xx, uu;
-  asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(uu) : "f"(u.x), "f"(u.y));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xx), "l"(uu));
-}
-
-constexpr int kFC2 = 16;     // features per pipeline stage
-constexpr int kXS2 = 20;     // smem row stride (floats): 16-B aligned, conflict-free float4 reads
-constexpr int kNS2 = 4;      // stages in the cp.async ring
-
-template <int NP>
-__global__ void __launch_bounds__(kPP, 2) project_pair_kernel(const float* __restrict__ X, int64_t n, int D,
-                                                              const float* __restrict__ U32, int L,
-                                                              float* __restrict__ P32, unsigned* maxnorm2) {
-  constexpr int Lp = 2 * NP;
-  extern __shared__ float smp[];
-  float* su = smp;            // [D][Lp], transposed, zero-padded
-  float* xs = smp + D * Lp;   // [kNS2][kPP][kXS2]
-  for (int i = threadIdx.x; i < D * Lp; i += blockDim.x) {
-    const int f = i / Lp, l = i % Lp;
-    su[i] = l < L ? U32[l * D + f] : 0.0f;
-  }
-  const int tid = threadIdx.x;
-  const int nch = (D + kFC2 - 1) / kFC2;
-  const int64_t ntiles = (n + kPP - 1) / kPP;
-  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t total = my_tiles * nch;  // this CTA's (tile, chunk) sequence
-  // chunk g of the sequence -> stage g % kNS2 (one cp.async group per chunk, empty past the end)
-  auto issue = [&](int64_t g) {
-    if (g < total) {
-      const int64_t base = (blockIdx.x + (g / nch) * gridDim.x) * static_cast<int64_t>(kPP);
-      const int f0 = static_cast<int>(g % nch) * kFC2;
-      float* dst = xs + (g % kNS2) * kPP * kXS2;
-      for (int q = tid; q < kPP * (kFC2 / 4); q += kPP) {
-        const int r = q / (kFC2 / 4), v = q % (kFC2 / 4);
-        const int64_t p = base + r;
-        const int f = f0 + 4 * v;
-        const bool ok = p < n && f < D;
-        cp_async16(dst + r * kXS2 + 4 * v, ok ? X + p * D + f : X, ok);
-      }
-    }
-    cp_async_commit();
-  };
-#pragma unroll
-  for (int g = 0; g < kNS2 - 1; ++g) issue(g);
-  unsigned long long acc[NP];
-#pragma unroll
-  for (int q = 0; q < NP; ++q) acc[q] = 0ull;
-  float nrm = 0.0f, wmax = 0.0f;
-  for (int64_t g = 0; g < total; ++g) {
-    cp_async_wait<kNS2 - 2>();
-    __syncthreads();  // chunk g landed for everyone; stage (g - 1) % kNS2 is free (and su staged)
-    issue(g + kNS2 - 1);
-    const int c = static_cast<int>(g % nch);
-    const float* xr = xs + (g % kNS2) * kPP * kXS2 + tid * kXS2;
-    const int f0 = c * kFC2;
-    const int fe = min(kFC2, D - f0);
-    for (int f = 0; f < fe; f += 4) {
-      const float4 x4 = *reinterpret_cast<const float4*>(xr + f);
-      const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        nrm = fmaf(xv[t], xv[t], nrm);
-        const float4* u4 = reinterpret_cast<const float4*>(su + (f0 + f + t) * Lp);
-#pragma unroll
-        for (int q = 0; q < NP / 2; ++q) {
-          const float4 u = u4[q];
-          ffma2_bcast(acc[2 * q], xv[t], make_float2(u.x, u.y));
-          ffma2_bcast(acc[2 * q + 1], xv[t], make_float2(u.z, u.w));
-        }
-      }
-    }
-    if (c == nch - 1) {  // tile done: store its projections, reset
-      const int64_t p = (blockIdx.x + (g / nch) * gridDim.x) * static_cast<int64_t>(kPP) + tid;
-      if (p < n) {
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-          const float lo = __uint_as_float(static_cast<unsigned>(acc[q] & 0xffffffffull));
-          const float hi = __uint_as_float(static_cast<unsigned>(acc[q] >> 32));
-          if (2 * q < L) P32[static_cast<int64_t>(2 * q) * n + p] = lo;
-          if (2 * q + 1 < L) P32[static_cast<int64_t>(2 * q + 1) * n + p] = hi;
-        }
-        wmax = (isfinite(nrm) && isfinite(wmax)) ? fmaxf(wmax, nrm) : __int_as_float(0x7fffffff);
-      }
-#pragma unroll
-      for (int q = 0; q < NP; ++q) acc[q] = 0ull;
-      nrm = 0.0f;
-    }
-  }
-  cp_async_wait<0>();
-  __shared__ unsigned bm;
-  if (tid == 0) bm = 0u;
-  __syncthreads();
-  atomicMax(&bm, __float_as_uint(wmax));
-  __syncthreads();
-  if (tid == 0) atomicMax(maxnorm2, bm);
-}
-
 // ------------------------------------------------------------------ K4 radix select
 __device__ __forceinline__ void round_params(int round, int& shift, unsigned& binmask) {
   if (round == 0) {
@@ -612,32 +507,6 @@ cudaError_t launch_dirs_to_f32(const double* U64, float* U32, int rows, int D, c
 static cudaError_t launch_project(const float* X, int64_t n, int D, const float* U32, int L, float* P32,
                                   unsigned* maxnorm2, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
-  const int Lp = (L + 3) & ~3;
-  const size_t tsmem = sizeof(float) * (static_cast<size_t>(D) * Lp + kNS2 * kPP * kXS2);
-  const char* leg = getenv("PROHD_K3_SCALAR");  // dev A/B: the scalar-FFMA tile kernel
-  if (D % 4 == 0 && L <= 32 && tsmem <= 200 * 1024 && !(leg != nullptr && leg[0] == '1')) {
-    int64_t tiles = (n + kPP - 1) / kPP;
-    if (tiles > 2 * 148) tiles = 2 * 148;
-    auto launch = [&](auto kern) -> cudaError_t {
-      cudaError_t ee = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(tsmem));
-      if (ee != cudaSuccess) return ee;
-      count_launch();
-      kern<<<static_cast<int>(tiles), kPP, tsmem, st>>>(X, n, D, U32, L, P32, maxnorm2);
-      return cudaGetLastError();
-    };
-    switch (Lp / 2) {
-      case 2: e = launch(project_pair_kernel<2>); break;
-      case 4: e = launch(project_pair_kernel<4>); break;
-      case 6: e = launch(project_pair_kernel<6>); break;
-      case 8: e = launch(project_pair_kernel<8>); break;
-      case 10: e = launch(project_pair_kernel<10>); break;
-      case 12: e = launch(project_pair_kernel<12>); break;
-      case 14: e = launch(project_pair_kernel<14>); break;
-      default: e = launch(project_pair_kernel<16>); break;
-    }
-    return e;
-  }
   const size_t tsmem0 = sizeof(float) * (((L * D + 3) & ~3) + 2 * kPP * kXS);
   if (D % 4 == 0 && L <= 32 && tsmem0 <= 200 * 1024) {
     int64_t tiles = (n + kPP - 1) / kPP;
