@@ -332,8 +332,11 @@ def run_ours(args, rank: int, world: int):
                      "traffic": (tpp * pairs_launch) if tpp else None,
                      "note": ("achieved = 6*D executed tensor flops per pair (3 TF32 MMAs of 2*D) x pairs per "
                               "launch / mean launch time from CUDA events on the launch stream; peak = "
-                              f"{pk['source']} bf16 sustained {pk['bf16_tflops_sustained']} x nominal tf32/bf16 "
-                              f"{NOMINAL_TF32_OVER_BF16:.4f}; traffic from {tsrc or 'n/a'}"),
+                              f"{pk['source']} bf16 burst {pk['bf16_tflops']} x nominal tf32/bf16 "
+                              f"{NOMINAL_TF32_OVER_BF16:.4f} (the larger, conservative denominator: the sustained "
+                              f"bf16 figure {pk['bf16_tflops_sustained']} gives {tf32_peak_sustained:.1f} TFLOP/s and "
+                              f"frac {k6_tflops / tf32_peak_sustained:.3f}, because bf16 MMAs are power-capped to a "
+                              f"lower clock than TF32 ones); traffic from {tsrc or 'n/a'}"),
                      "launch_ms": k6_ms},
         "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }
