@@ -122,6 +122,17 @@ int hausdorff(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
 int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB,
                        int32_t D, float* rowmin_dev);
 
+/* Test hook (K3, Alg. 1 line 4 / Alg. 2 line 5; pi = x^T u,
+ * P:139): the fp32 projections the selection starts from. X (DEVICE, n x D fp32 row-major),
+ * dirs (DEVICE, L x D fp64, row l = direction u_l, 1 <= L <= 32; rounded to fp32 first);
+ * proj_out (DEVICE, L x n fp32, direction-major: proj_out[l * n + i] ~= x_i . u_l);
+ * *eps_out (HOST) = the bound the selection's fp64 re-rank band assumes:
+ * |proj_out[l * n + i] - x_i . u_l (exact)| <= eps_out for every i, l. Workspace >= L*D*4 + 256
+ * bytes. Errors: PROHD_E_INVALID (null, host pointers, bad sizes), PROHD_E_WORKSPACE,
+ * PROHD_E_CUDA. */
+int prohd_project(prohd_ctx* ctx, const float* X, int64_t n, int32_t D, const double* dirs, int32_t L,
+                  float* proj_out, double* eps_out);
+
 /* ---------------------------------------------------------------- ProHD   */
 /* Alg. 3 with k principal directions plus the centroid axis and m points per
  * (set, direction, tail). 0 <= k <= D, m >= 1; if 2m >= n_X all of X is kept.

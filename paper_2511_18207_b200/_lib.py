@@ -27,6 +27,7 @@ EXPORTED = [
     "prohd_workspace_bytes", "prohd_set_workspace", "directed_hd", "hausdorff", "directed_hd_rowmin",
     "prohd_estimate", "prohd_estimate_certified", "prohd_estimate_alpha", "hausdorff_subsets",
     "prohd_estimate_with_dirs", "prohd_bounds", "directed_hd_local", "prohd_centre", "directed_hd_witness",
+    "prohd_project",
     "prohd_enable_timing", "prohd_last_timings",
     "prohd_shard_workspace_bytes", "prohd_shift", "prohd_local_moments", "prohd_directions",
     "prohd_local_candidates", "prohd_merge_union", "prohd_gather_owned",
@@ -87,6 +88,7 @@ def load() -> C.CDLL:
     lib.prohd_estimate_with_dirs.argtypes = [vp, vp, i64, vp, i64, i32, i32, i64, vp, C.POINTER(Est), vp, vp]
     lib.directed_hd_local.argtypes = [vp, vp, i64, i64, vp, i64, i32, vp, C.POINTER(C.c_uint64)]
     lib.prohd_centre.argtypes = [vp, vp, i64, vp, i64, i32, vp]
+    lib.prohd_project.argtypes = [vp, vp, i64, i32, vp, i32, vp, vp]
     lib.directed_hd_witness.argtypes = [vp, vp, vp, i64, i32, C.POINTER(Directed)]
     lib.prohd_enable_timing.argtypes = [vp, f]
     lib.prohd_shard_workspace_bytes.argtypes = [i64, i64, i32, i32, i64, C.c_uint32]

@@ -249,6 +249,21 @@ class Context:
                                           out.ctypes.data))
         return out
 
+    def project(self, X, dirs):
+        """prohd_project (test hook): fp32 projections (L x n, device tensor) of the device
+        points X onto the fp64 directions dirs (L x D) and the bound eps on their error."""
+        X = _as_points(X, "X")
+        dirs = torch.as_tensor(dirs, dtype=torch.float64).to(X.device).contiguous()
+        Ld, D = dirs.shape
+        self._ensure_ws(Ld * D * 4 + 1024)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._check(self.lib.prohd_set_stream(self.h, C.c_void_p(stream)))
+        P = torch.empty((Ld, X.shape[0]), dtype=torch.float32, device=X.device)
+        eps = C.c_double(0.0)
+        self._check(self.lib.prohd_project(self.h, X.data_ptr(), X.shape[0], D, dirs.data_ptr(), Ld,
+                                           P.data_ptr(), C.byref(eps)))
+        return P, eps.value
+
     def directed_hd_witness(self, a, B) -> dict:
         a = _as_points(a.reshape(1, -1) if a.dim() == 1 else a, "a")
         a, B = self._prepare(a, B)

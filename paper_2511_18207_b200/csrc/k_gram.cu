@@ -58,7 +58,7 @@ struct GramArgs {
 };
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
@@ -121,8 +121,141 @@ __global__ void __launch_bounds__(kGT, 2) gram_kernel(const __grid_constant__ Gr
   const int nch = p1 > p0 ? static_cast<int>((p1 - p0 + kGMC - 1) / kGMC) : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  if (warp >= 4) {
-    // ------------------------------------------------------------------ loaders
+  if (warp >= 4 && kVec) {
+    // ------------------------------------------------------------------ loaders, D % 4 == 0
+    // Thread (lw, lane) owns 16-B piece (row lw + 4 it, features fb[sl] * 32 + 4 sub .. + 3)
+    // of every chunk: it issues that piece's cp.async, waits for its own copies only (no
+    // loader barrier), converts the 4 values and writes them to the fp64 tile as 2 x 16 B.
+    // A warp covers one 512-B row per it: conflict-free LDS.128 / STS.128.
+    const int ct = tid - 128, lw = ct >> 5;
+    const int sl = lane >> 3, sub = lane & 7;
+    const int ff = sl < G.nfb ? G.fb[sl] * 32 + sub * 4 : a.D;
+    const bool fv = ff < a.D;  // D % 4 == 0: the 4 features are all valid or all absent
+    const int col = sl * 32 + sub * 4;
+    const bool own = fv && G.own[sl];
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+    if (fv)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s4[j] = a.s[ff + j];
+    // warp-uniform (the __any_sync below needs every lane): lanes without features convert zeros
+    const bool shifted = __any_sync(0xffffffffu, s4[0] != 0.0 || s4[1] != 0.0 || s4[2] != 0.0 || s4[3] != 0.0);
+    double sA[4] = {0.0, 0.0, 0.0, 0.0}, sB[4] = {0.0, 0.0, 0.0, 0.0};
+    const uint32_t stage_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+    const uint64_t Aaddr = reinterpret_cast<uint64_t>(a.A), Baddr = reinterpret_cast<uint64_t>(a.B);
+    auto issue = [&](int c) {
+      if (c < nch) {
+        const uint32_t dst0 = stage_u32 + static_cast<uint32_t>(((c % kGNS) * kGStageF + col) * 4);
+        const int64_t q0 = p0 + static_cast<int64_t>(c) * kGMC;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int pr = lw + 4 * it;
+          const int64_t p = q0 + pr;
+          const bool ok = fv && p < p1;
+          const uint64_t src = p < a.nA ? Aaddr + static_cast<uint64_t>(p * a.D + ff) * 4
+                                        : Baddr + static_cast<uint64_t>((p - a.nA) * a.D + ff) * 4;
+          cp_async16(dst0 + static_cast<uint32_t>(pr * 128 * 4), ok ? reinterpret_cast<const void*>(src) : a.A,
+                     ok ? 16 : 0);
+        }
+      }
+      cp_commit();
+    };
+#pragma unroll
+    for (int c = 0; c < kGNS - 1; ++c) issue(c);
+    for (int c = 0; c < nch; ++c) {
+      cp_wait<kGNS - 2>();  // this thread's pieces of chunk c have landed (it reads only those)
+      float4 x[4];
+      const float* src = stage + (c % kGNS) * kGStageF + col;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) x[it] = *reinterpret_cast<const float4*>(src + (lw + 4 * it) * 128);
+      issue(c + kGNS - 1);  // overwrites stage (c - 1) % kGNS, whose values this thread has consumed
+      const int64_t q0 = p0 + static_cast<int64_t>(c) * kGMC;
+      double v[4][4];
+      if (!shifted) {
+        // integer-pipe fp32 -> fp64 for normals and signed zeros; a warp-uniform F2F fallback
+        // if any of the warp's values is subnormal, inf or nan
+        bool special = false;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const float xs[4] = {x[it].x, x[it].y, x[it].z, x[it].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const unsigned u = __float_as_uint(xs[j]);
+            const unsigned m = u & 0x7FFFFFFFu;
+            special |= (m - 1u < 0x007FFFFFu) | (m >= 0x7F800000u);
+            const unsigned hi = ((static_cast<unsigned>(static_cast<int>(u) >> 3) & 0x8FFFFFFFu)) +
+                                (m != 0u ? 0x38000000u : 0u);
+            v[it][j] = __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
+          }
+        }
+        if (__any_sync(0xffffffffu, special)) {
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            v[it][0] = static_cast<double>(x[it].x);
+            v[it][1] = static_cast<double>(x[it].y);
+            v[it][2] = static_cast<double>(x[it].z);
+            v[it][3] = static_cast<double>(x[it].w);
+          }
+        }
+      } else {
+        // large common offset: x - s_f in fp64 (fp64 pipe); rows past the range stay 0
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const bool in = q0 + lw + 4 * it < p1;
+          v[it][0] = in ? static_cast<double>(x[it].x) - s4[0] : 0.0;
+          v[it][1] = in ? static_cast<double>(x[it].y) - s4[1] : 0.0;
+          v[it][2] = in ? static_cast<double>(x[it].z) - s4[2] : 0.0;
+          v[it][3] = in ? static_cast<double>(x[it].w) - s4[3] : 0.0;
+        }
+      }
+      const int b = c % kGNB;
+      if (c >= kGNB) named_sync(1 + kGNB + b, kGT);  // MMA warps released buffer b
+      double* dst = tile + b * kGMC * kGLd + col;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        double2* d2 = reinterpret_cast<double2*>(dst + (lw + 4 * it) * kGLd);
+        d2[0] = make_double2(v[it][0], v[it][1]);
+        d2[1] = make_double2(v[it][2], v[it][3]);
+      }
+      named_arrive(1 + b, kGT);
+      if (own) {
+        // column sums of the owned block (rows past the range are 0)
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          if (q0 + lw + 4 * it < a.nA) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sA[j] += v[it][j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sB[j] += v[it][j];
+          }
+        }
+      }
+    }
+    for (int c = (nch > kGNB ? nch - kGNB : 0); c < nch; ++c) named_sync(1 + kGNB + (c % kGNB), kGT);
+    cp_wait<0>();
+    // combine the 4 loader warps' column sums in a fixed order through the (now idle) staging ring
+    named_sync(1 + 2 * kGNB, 128);
+    double* red = reinterpret_cast<double*>(stage);  // [lw][slot][32][2]
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      red[((lw * 4 + sl) * 32 + sub * 4 + j) * 2 + 0] = sA[j];
+      red[((lw * 4 + sl) * 32 + sub * 4 + j) * 2 + 1] = sB[j];
+    }
+    named_sync(1 + 2 * kGNB, 128);
+    {
+      const int slot = ct >> 5;
+      double ra = 0.0, rb = 0.0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        ra += red[((w * 4 + slot) * 32 + lane) * 2 + 0];
+        rb += red[((w * 4 + slot) * 32 + lane) * 2 + 1];
+      }
+      double* sp = a.Spart + (static_cast<int64_t>(blockIdx.x) * 4 + slot) * 64;
+      sp[lane] = ra;
+      sp[32 + lane] = rb;
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ loaders, D % 4 != 0
     const int ct = tid - 128;
     const int slot = ct >> 5;
     const int f = slot < G.nfb ? G.fb[slot] * 32 + lane : a.D;
@@ -247,23 +380,40 @@ __global__ void __launch_bounds__(kGT, 2) gram_kernel(const __grid_constant__ Gr
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // fragments double-buffered in registers: the loads of k-step k + 1 (the next chunk's first
+    // k-step after its FULL barrier) are issued before the 16 DMMAs of k-step k
+    double af[2][4], bf[2][4];
+    const int oI = sI * 32 + fr, oJ = sJ * 32 + fr;
+    auto ldfrag = [&](const double* row, double (&A_)[4], double (&B_)[4]) {
+      if (active) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) A_[i] = row[oI + i * 8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) B_[j] = row[oJ + j * 8];
+      }
+    };
+    if (nch > 0) {
+      named_sync(1, kGT);
+      ldfrag(tile + fk * kGLd, af[0], bf[0]);
+    }
     for (int c = 0; c < nch; ++c) {
       const int b = c % kGNB;
-      named_sync(1 + b, kGT);
-      if (active) {
-        const double* t = tile + b * kGMC * kGLd;
+      const double* t = tile + b * kGMC * kGLd;
 #pragma unroll
-        for (int k0 = 0; k0 < kGMC; k0 += 4) {
-          const double* row = t + (k0 + fk) * kGLd;
-          double af[4], bf[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) af[i] = row[sI * 32 + i * 8 + fr];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) bf[j] = row[sJ * 32 + j * 8 + fr];
+      for (int ks = 0; ks < 4; ++ks) {
+        const int cur = ks & 1, nxt = cur ^ 1;
+        if (ks < 3) {
+          ldfrag(t + ((ks + 1) * 4 + fk) * kGLd, af[nxt], bf[nxt]);
+        } else if (c + 1 < nch) {
+          const int bn = (c + 1) % kGNB;
+          named_sync(1 + bn, kGT);
+          ldfrag(tile + bn * kGMC * kGLd + fk * kGLd, af[nxt], bf[nxt]);
+        }
+        if (active) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+            for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[cur][i], bf[cur][j]);
         }
       }
       named_arrive(1 + kGNB + b, kGT);

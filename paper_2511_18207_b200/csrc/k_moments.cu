@@ -330,11 +330,18 @@ __global__ void __launch_bounds__(256) moments_finalize_kernel(double* __restric
       u0[f] = u0[f] / nrm;
   }
   if (threadIdx.x == 0) *dnorm = nrm;
-  for (int64_t e = threadIdx.x; e < static_cast<int64_t>(D) * D; e += blockDim.x) {
-    const int i = static_cast<int>(e / D), j = static_cast<int>(e % D);
-    const double mi = (SA[i] + SB[i]) / N, mj = (SA[j] + SB[j]) / N;  // mu - s
-    G[e] = G[e] / N - mi * mj;
-  }
+}
+
+// C = G / N - (mu - s)(mu - s)^T in place, one element per thread
+__global__ void __launch_bounds__(256) covariance_kernel(double* __restrict__ G, const double* __restrict__ SA,
+                                                         const double* __restrict__ SB, int64_t nA, int64_t nB,
+                                                         int D) {
+  const double N = static_cast<double>(nA + nB);
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(D) * D) return;
+  const int i = static_cast<int>(e / D), j = static_cast<int>(e % D);
+  const double mi = (SA[i] + SB[i]) / N, mj = (SA[j] + SB[j]) / N;  // mu - s
+  G[e] = G[e] / N - mi * mj;
 }
 
 }  // namespace
@@ -376,6 +383,15 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
     if (p.gp.gpart_doubles > p.gpart_doubles) p.gpart_doubles = p.gp.gpart_doubles;
     if (p.gp.spart_doubles > p.spart_doubles) p.spart_doubles = p.gp.spart_doubles;
   }
+  // The int8 tensor-core Gram (k_gram_i8.cu) is opt-in (PROHD_K1_I8=1): correct, but measured
+  // slower at cfg5 (22.4 vs 12.2 ms) because its 128x64 tiles are L2-bound.
+  const char* i8e = getenv("PROHD_K1_I8");
+  p.i8 = (i8e != nullptr && i8e[0] == '1') && plan_gram_i8(nA, nB, D, num_sms, p.ip);
+  if (p.i8) {
+    if (p.ip.gpart_doubles > p.gpart_doubles) p.gpart_doubles = p.ip.gpart_doubles;
+    p.i8_bytes = round_up(static_cast<int64_t>(D) * 4, 256) + round_up(p.ip.spart_doubles * 8, 256) +
+                 p.ip.slice_bytes;
+  }
   return p;
 }
 
@@ -398,7 +414,14 @@ cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB,
 }
 
 cudaError_t launch_moments_partial(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB,
-                                   int D, const MomentsBufs& b, cudaStream_t st) {
+                                   int D, const MomentsBufs& b, cudaStream_t st, bool shifted) {
+  if (!shifted && p.i8 && b.i8ws != nullptr) {
+    unsigned* maxbits = reinterpret_cast<unsigned*>(b.i8ws);
+    double* sp = reinterpret_cast<double*>(b.i8ws + round_up(static_cast<int64_t>(D) * 4, 256));
+    int8_t* S = reinterpret_cast<int8_t*>(b.i8ws + round_up(static_cast<int64_t>(D) * 4, 256) +
+                                          round_up(p.ip.spart_doubles * 8, 256));
+    return launch_gram_i8(p.ip, A, nA, B, nB, maxbits, sp, S, b.Gpart, b.C, b.SA, b.SB, st);
+  }
   if (p.gram) return launch_gram(p.gp, A, nA, B, nB, D, b.s, b.Gpart, b.Spart, b.C, b.SA, b.SB, st);
   const size_t smem = sizeof(double) * kMC * kLds;
   auto kern = mom_ctas_per_sm() == 3 ? moments_kernel<3> : moments_kernel<4>;
@@ -416,6 +439,9 @@ cudaError_t launch_moments_partial(const MomentsPlan& p, const float* A, int64_t
 cudaError_t launch_moments_finalize(int64_t nA, int64_t nB, int D, const MomentsBufs& b, cudaStream_t st) {
   count_launch();
   moments_finalize_kernel<<<1, 256, 0, st>>>(b.C, b.SA, b.SB, b.s, nA, nB, D, b.mu, b.u0, b.dnorm);
+  count_launch();
+  covariance_kernel<<<static_cast<int>((static_cast<int64_t>(D) * D + 255) / 256), 256, 0, st>>>(b.C, b.SA, b.SB,
+                                                                                                 nA, nB, D);
   return cudaGetLastError();
 }
 

@@ -297,10 +297,12 @@ __global__ void __launch_bounds__(kScanT) radix_scan_kernel(const unsigned* __re
 __global__ void __launch_bounds__(256) collect_kernel(const float* __restrict__ P32, int64_t n, int D, int L,
                                                       const int* n_dirs, const unsigned* __restrict__ state,
                                                       const unsigned* maxnorm2, int* cand, unsigned* ccount,
-                                                      int64_t cap, int* overflow, int all) {
+                                                      int64_t cap, int* overflow, int all, double eps_coef) {
   const int l = blockIdx.y;
   if (l >= *n_dirs) return;
-  const double eps = (D + 8) * 0x1p-24 * sqrt(static_cast<double>(__uint_as_float(*maxnorm2))) * 1.0625;
+  // eps_coef * max||x|| bounds |pi32 - pi64| for the K3 variant that ran (1.0625: margin for
+  // the fp32 norm and sqrt)
+  const double eps = eps_coef * sqrt(static_cast<double>(__uint_as_float(*maxnorm2))) * 1.0625;
   const double Ttop = static_cast<double>(key_to_float(state[(l * 2 + 0) * 4 + 0]));
   const double Tbot = static_cast<double>(key_to_float(~state[(l * 2 + 1) * 4 + 0]));
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -504,9 +506,23 @@ cudaError_t launch_dirs_to_f32(const double* U64, float* U32, int rows, int D, c
   return cudaGetLastError();
 }
 
-static cudaError_t launch_project(const float* X, int64_t n, int D, const float* U32, int L, float* P32,
-                                  unsigned* maxnorm2, cudaStream_t st) {
+// K3: the tcgen05 3xTF32 kernel (k_project_tc.cu) where it applies, else the SIMT kernels;
+// *eps_coef receives the coefficient of max||x|| that bounds |pi32 - pi64| for the kernel run.
+cudaError_t launch_project(const float* X, int64_t n, int D, const float* U32, int L, float* P32,
+                                  unsigned* maxnorm2, cudaStream_t st, double* eps_coef) {
   cudaError_t e = cudaSuccess;
+  if (project_tc_supported(n, D, L)) {
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                    cudaSuccess || sms <= 0)
+        sms = 148;
+    }
+    *eps_coef = project_tc_eps_coef(D);
+    return launch_project_tc(X, n, D, U32, L, P32, maxnorm2, sms, st);
+  }
+  *eps_coef = (D + 8) * 0x1p-24;  // sequential fp32 FMA sums of D + 1 terms, u rounded to fp32
   const size_t tsmem0 = sizeof(float) * (((L * D + 3) & ~3) + 2 * kPP * kXS);
   if (D % 4 == 0 && L <= 32 && tsmem0 <= 200 * 1024) {
     int64_t tiles = (n + kPP - 1) / kPP;
@@ -562,7 +578,8 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   count_launch();
   init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, m);
   // K3
-  if ((e = launch_project(X, n, D, U32, L, b.P32, b.maxnorm2, st)) != cudaSuccess) return e;
+  double eps_coef = 0.0;
+  if ((e = launch_project(X, n, D, U32, L, b.P32, b.maxnorm2, st, &eps_coef)) != cudaSuccess) return e;
   // K4: three radix rounds
   int64_t hb = (n + 255) / 256;
   if (hb > 148 * 2) hb = 148 * 2;
@@ -574,7 +591,7 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   }
   count_launch();
   collect_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, D, L, n_dirs, b.state, b.maxnorm2,
-                                                                     b.cand, b.ccount, b.cap, b.overflow, 0);
+                                                                     b.cand, b.ccount, b.cap, b.overflow, 0, eps_coef);
   count_launch();
   cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
   count_launch();
@@ -610,7 +627,8 @@ cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offse
   const bool all = m >= n;
   count_launch();
   init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, all ? 1 : m);
-  if ((e = launch_project(X, n, D, U32, L, b.P32, b.maxnorm2, st)) != cudaSuccess) return e;
+  double eps_coef = 0.0;
+  if ((e = launch_project(X, n, D, U32, L, b.P32, b.maxnorm2, st, &eps_coef)) != cudaSuccess) return e;
   int64_t hb = (n + 255) / 256;
   if (hb > 148 * 2) hb = 148 * 2;
   if (!all) {
@@ -623,7 +641,8 @@ cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offse
   }
   count_launch();
   collect_kernel<<<dim3(static_cast<unsigned>(hb), L), 256, 0, st>>>(b.P32, n, D, L, n_dirs, b.state, b.maxnorm2,
-                                                                     b.cand, b.ccount, b.cap, b.overflow, all ? 1 : 0);
+                                                                     b.cand, b.ccount, b.cap, b.overflow, all ? 1 : 0,
+                                                                     eps_coef);
   count_launch();
   cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
   count_launch();

@@ -237,6 +237,39 @@ int prohd_centre(prohd_ctx* ctx, const float* X, int64_t nX, const float* Y, int
   return PROHD_OK;
 }
 
+int prohd_project(prohd_ctx* ctx, const float* X, int64_t n, int32_t D, const double* dirs, int32_t L,
+                  float* proj_out, double* eps_out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (X == nullptr || dirs == nullptr || proj_out == nullptr || eps_out == nullptr)
+    return fail(ctx, PROHD_E_INVALID, "null pointer");
+  if (n < 1 || D < 1 || L < 1 || L > 32) return fail(ctx, PROHD_E_INVALID, "bad sizes");
+  if (!is_device_ptr(X) || !is_device_ptr(dirs) || !is_device_ptr(proj_out))
+    return fail(ctx, PROHD_E_INVALID, "prohd_project takes device pointers");
+  Carver dry{nullptr, 0, 0, true};
+  dry.take<float>(static_cast<int64_t>(L) * D);
+  dry.take<unsigned>(1);
+  if (ctx->ws == nullptr || ctx->ws_bytes < dry.off)
+    return fail(ctx, PROHD_E_WORKSPACE, "workspace too small: need %zu bytes, have %zu", dry.off, ctx->ws_bytes);
+  Carver c{ctx->ws, 0, ctx->ws_bytes, false};
+  float* U32 = c.take<float>(static_cast<int64_t>(L) * D);
+  unsigned* mx = c.take<unsigned>(1);
+  double coef = 0.0;
+  unsigned mxh = 0;
+  call_begin(ctx);
+  CK(cudaMemsetAsync(mx, 0, sizeof(unsigned), ctx->stream));
+  CK(launch_dirs_to_f32(dirs, U32, L, D, ctx->stream));
+  CK(launch_project(X, n, D, U32, L, proj_out, mx, ctx->stream, &coef));
+  CK(cudaMemcpyAsync(&mxh, mx, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+  call_end(ctx);
+  CK(cudaStreamSynchronize(ctx->stream));
+  call_collect(ctx);
+  float m2;
+  memcpy(&m2, &mxh, sizeof(m2));
+  *eps_out = coef * std::sqrt(static_cast<double>(m2)) * 1.0625;
+  return PROHD_OK;
+}
+
 int directed_hd_witness(prohd_ctx* ctx, const float* a, const float* B, int64_t nB, int32_t D,
                         prohd_directed* out) {
   int rc = enter(ctx);

@@ -70,6 +70,7 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
   w.mom.s = c.take<double>(2 * static_cast<int64_t>(D));  // shift + scratch
   w.mom.Gpart = c.take<double>(mp.gpart_doubles);
   w.mom.Spart = c.take<double>(mp.spart_doubles);
+  if (mp.i8) w.mom.i8ws = c.take<uint8_t>(mp.i8_bytes);
   w.mom.C = c.take<double>(static_cast<int64_t>(D) * D);
   w.mom.SA = c.take<double>(D);
   w.mom.SB = c.take<double>(D);
@@ -149,7 +150,20 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   if (dirs_in == nullptr) {
     const MomentsPlan mp = plan_moments(nA, nB, D, ctx->num_sms);
     int t0 = tmark(ctx);
-    CK(launch_moments(mp, A, nA, B, nB, D, w.mom, st));
+    // shift first; with the opt-in int8 Gram planned, its value picks the path (int8 tensor
+    // cores about the origin, or the fp64 DMMA pass with the subtraction), so the host reads
+    // it back (D doubles); the default DMMA pass handles either case on the device
+    CK(launch_shift(A, nA, B, nB, D, w.mom.s, st));
+    bool shifted = true;
+    if (mp.i8) {
+      std::vector<double> sh(static_cast<size_t>(D));
+      CK(cudaMemcpyAsync(sh.data(), w.mom.s, sizeof(double) * D, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      shifted = false;
+      for (double v : sh) shifted = shifted || v != 0.0;
+    }
+    CK(launch_moments_partial(mp, A, nA, B, nB, D, w.mom, st, shifted));
+    CK(launch_moments_finalize(nA, nB, D, w.mom, st));
     tspan(ctx, PH_MOMENTS, t0);
     if (k > 0) {
       t0 = tmark(ctx);

@@ -29,13 +29,28 @@ cudaError_t launch_gram(const GramPlan& p, const float* A, int64_t nA, const flo
                         const double* s, double* Gpart, double* Spart, double* Gout, double* SA, double* SB,
                         cudaStream_t st);
 
+// int8 tensor-core Gram (k_gram_i8.cu), for moments about the origin (s = 0), D <= 256
+struct GramI8Plan {
+  int D = 0, Df = 0, ntiles = 0, nranges = 0, nctas = 0, cm_ctas = 0;
+  int64_t N = 0, Np = 0, per = 0, slice_bytes = 0, gpart_doubles = 0, spart_doubles = 0;
+  int tI[16], tJ[16];
+};
+bool plan_gram_i8(int64_t nA, int64_t nB, int D, int num_sms, GramI8Plan& p);
+cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, const float* B, int64_t nB,
+                           unsigned* maxbits, double* Spart, int8_t* S, double* Gpart, double* G, double* SA,
+                           double* SB, cudaStream_t st);
+
 struct MomentsPlan {
   int nb = 0, npairs = 0, c_diag = 0, c_off = 0, nctas = 0, nslots = 0;
   bool gram = false;  // warp-specialised Gram pass (k_gram.cu); else the legacy 64x64-block kernel
   GramPlan gp;
+  bool i8 = false;    // int8 tensor-core Gram available (used when s = 0)
+  GramI8Plan ip;
   int64_t gpart_doubles = 0, spart_doubles = 0;
+  int64_t i8_bytes = 0;  // maxbits + column-sum partials + slice planes (k_gram_i8.cu)
 };
 struct MomentsBufs {
+  uint8_t* i8ws = nullptr;  // int8 Gram scratch (MomentsPlan::i8_bytes)
   double* s;      // [2D]: shift s (0 unless the offset is large), then D doubles of scratch
   double* Gpart;  // partial Grams
   double* Spart;  // partial column sums
@@ -52,8 +67,9 @@ cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, con
 // pieces of launch_moments (sharded path): shift s from the first <= 4096 rows of A and B;
 // partial sums about b.s (-> b.SA, b.SB, b.C = G); finalize (mu, u0, C from the sums).
 cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB, int D, double* s, cudaStream_t st);
+// shifted: s != 0 (DMMA path with the fp64 subtraction); else the int8 Gram when planned
 cudaError_t launch_moments_partial(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB,
-                                   int D, const MomentsBufs& b, cudaStream_t st);
+                                   int D, const MomentsBufs& b, cudaStream_t st, bool shifted = true);
 cudaError_t launch_moments_finalize(int64_t nA, int64_t nB, int D, const MomentsBufs& b, cudaStream_t st);
 
 // ---------------------------------------------------------------- K2
@@ -83,6 +99,15 @@ struct SelectBufs {
 };
 // first: reset the union bitmap/flags; last: compact the bitmap into the sorted union. Two calls
 // (first=true,last=false then first=false,last=true) select with different m per direction group.
+// K3 on the tensor cores (k_project_tc.cu): D % 4 == 0, D <= 256, 1 <= L <= 32
+bool project_tc_supported(int64_t n, int D, int L);
+double project_tc_eps_coef(int D);  // |pi32 - pi64| <= coef * ||x||
+cudaError_t launch_project_tc(const float* X, int64_t n, int D, const float* U32, int L, float* P32,
+                              unsigned* maxnorm2, int num_sms, cudaStream_t st);
+// K3 dispatch (tensor-core kernel, else SIMT): P32 = direction-major projections, atomicMax of
+// max ||x||^2 bits into *maxnorm2 (zeroed by the caller); *eps_coef: |pi32 - pi64| <= coef ||x||
+cudaError_t launch_project(const float* X, int64_t n, int D, const float* U32, int L, float* P32,
+                           unsigned* maxnorm2, cudaStream_t st, double* eps_coef);
 cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
                           const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st, bool first = true,
                           bool last = true);

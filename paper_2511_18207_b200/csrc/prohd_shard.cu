@@ -47,6 +47,7 @@ static size_t carve_shard(Carver& c, ShardWs& w, int64_t nA, int64_t nB, int64_t
   w.mom.s = c.take<double>(2 * static_cast<int64_t>(D));  // shift + scratch
   w.mom.Gpart = c.take<double>(mp.gpart_doubles);
   w.mom.Spart = c.take<double>(mp.spart_doubles);
+  if (mp.i8) w.mom.i8ws = c.take<uint8_t>(mp.i8_bytes);
   w.mom.C = c.take<double>(static_cast<int64_t>(D) * D);
   w.mom.SA = c.take<double>(D);
   w.mom.SB = c.take<double>(D);
@@ -154,7 +155,9 @@ int prohd_local_moments(prohd_ctx* ctx, const float* A_local, int64_t nA_local, 
   CK(cudaMemsetAsync(w.mom.C, 0, sizeof(double) * D * D, st));
   if (nA_local + nB_local > 0) {
     const MomentsPlan mp = plan_moments(nA_local, nB_local, D, ctx->num_sms);
-    CK(launch_moments_partial(mp, A_local, nA_local, B_local, nB_local, D, w.mom, st));
+    bool shifted = false;  // the shift is a HOST array (prohd.h)
+    for (int f = 0; f < D; ++f) shifted = shifted || shift[f] != 0.0;
+    CK(launch_moments_partial(mp, A_local, nA_local, B_local, nB_local, D, w.mom, st, shifted));
   }
   tspan(ctx, PH_MOMENTS, t0);
   CK(cudaMemcpyAsync(moments_out, w.mom.SA, sizeof(double) * D, cudaMemcpyDeviceToDevice, st));

@@ -1,0 +1,88 @@
+"""K1 (moments) through the phase call prohd_local_moments: [S_A | S_B | G] about a shift s
+(Alg. 1 line 1; Alg. 2 lines 1-2) against fp64 sums of the
+same fp32 inputs (the oracle's definition, O1/O3, written out with numpy).
+
+The default Gram is the fp64 DMMA pass (k_gram.cu, products of fp32 values exact in fp64,
+subtraction only when s != 0); PROHD_K1_I8=1 selects the opt-in int8 tensor-core pass for
+s = 0 (k_gram_i8.cu: exact integer slice products, pairs t + u <= 7 kept). Both must agree
+with the fp64 sums to 1e-12 of sum_p |x_pi - s_i| |x_pj - s_j| (the scale of the
+accumulation; fp64 accumulation over 1e5 points, or the int8 path's dropped slice pairs,
+< 2^-62 of max|x_i| max|x_j| per point), far inside the ~1e-9 relative C accuracy the
+direction parity needs."""
+import os
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2511_18207_b200 import Context
+    return Context(0)
+
+
+def _ref(A, B, s):
+    a = A.astype(np.float64) - s
+    b = B.astype(np.float64) - s
+    G = a.T @ a + b.T @ b
+    scale = np.abs(a).T @ np.abs(a) + np.abs(b).T @ np.abs(b)
+    return a.sum(0), b.sum(0), G, scale
+
+
+def _check(ctx, A, B, s, rtol=1e-12):
+    D = A.shape[1]
+    mom = ctx.local_moments(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), s).cpu().numpy()
+    SA, SB, G = mom[:D], mom[D:2 * D], mom[2 * D:].reshape(D, D)
+    rSA, rSB, rG, scale = _ref(A, B, s)
+    sa_scale = np.abs(A.astype(np.float64) - s).sum(0) + 1e-300
+    sb_scale = np.abs(B.astype(np.float64) - s).sum(0) + 1e-300
+    assert np.all(np.abs(SA - rSA) <= 1e-13 * sa_scale)
+    assert np.all(np.abs(SB - rSB) <= 1e-13 * sb_scale)
+    err = np.abs(G - rG) / (scale + 1e-300)
+    assert err.max() <= rtol, f"max G error {err.max():.2e} (rel. to sum |x_i||x_j|)"
+    assert np.array_equal(G, G.T)
+
+
+@pytest.fixture(params=["dmma", "i8"])
+def gram_path(request):
+    old = os.environ.get("PROHD_K1_I8")
+    os.environ["PROHD_K1_I8"] = "1" if request.param == "i8" else "0"
+    yield request.param
+    if old is None:
+        del os.environ["PROHD_K1_I8"]
+    else:
+        os.environ["PROHD_K1_I8"] = old
+
+
+@pytest.mark.parametrize("nA,nB,D", [(1, 1, 3), (63, 65, 16), (1000, 777, 64), (4099, 2051, 100),
+                                     (20000, 20001, 128), (9000, 9000, 200), (65536, 70001, 256)])
+def test_gram_about_origin(ctx, gram_path, nA, nB, D):
+    rng = np.random.default_rng(nA + D)
+    A = rng.standard_normal((nA, D)).astype(np.float32)
+    B = (rng.standard_t(3, (nB, D)) * 5 + 0.3).astype(np.float32)  # heavy tails, small offset
+    _check(ctx, A, B, np.zeros(D))
+
+
+def test_gram_special_values(ctx, gram_path):
+    rng = np.random.default_rng(5)
+    D = 48
+    A = rng.standard_normal((5000, D)).astype(np.float32)
+    B = rng.standard_normal((3000, D)).astype(np.float32)
+    A[:, 0] = 0.0                   # an all-zero column
+    A[::3, 1] = np.float32(-0.0)
+    A[::7, 2] = np.float32(3e-40)   # subnormals
+    B[::5, 3] = np.float32(1e-30)   # tiny normals next to O(1) values
+    B[17, 4] = np.float32(1e6)      # one huge outlier in a column
+    _check(ctx, A, B, np.zeros(D))
+
+
+def test_gram_shifted(ctx):
+    """s != 0: the fp64 DMMA pass subtracts the shift (large common offset)."""
+    rng = np.random.default_rng(9)
+    D = 96
+    A = (rng.standard_normal((20000, D)) + 4096).astype(np.float32)
+    B = (rng.standard_normal((15000, D)) + 4096.5).astype(np.float32)
+    s = np.concatenate([A[:4096], B[:4096]]).astype(np.float64).mean(0)
+    _check(ctx, A, B, s)
