@@ -6,41 +6,53 @@
 // centroids (Alg. 1 line 1) and C = G/N - (mu - s)(mu - s)^T.
 //
 // Work decomposition. The upper triangle of G is cut into 32x32 warp tiles (I <= J over
-// 32-feature blocks) and the tiles into GROUPS of <= 4 that together need <= 4 feature
-// blocks (<= 128 features): every off-diagonal 64x64 block is one group of 4 tiles, and
-// the 3 upper tiles of consecutive diagonal 64x64 blocks are packed 4 at a time. At
-// D = 256 that is 36 tiles in 9 full groups, so no warp idles. CTA = (point range r,
-// group g), blockIdx = r * ngroups + g: the ngroups CTAs reading the same rows are
-// adjacent in launch order, run concurrently, and share the rows through L2.
+// 32-feature blocks) and the tiles into GROUPS of <= 12 that together need <= 8 feature
+// blocks (<= 256 features, staged in "slots"): for D <= 256 every group stages all of D and
+// the tiles are split evenly (D = 256: 36 tiles in 3 groups of 12); for larger D each 4x4
+// square of blocks on or above the diagonal gives one or two groups. A group with fewer
+// than 12 tiles runs each tile on kRep = 2 or 4 warps that take alternate k-steps (partial
+// accumulators summed by the reduce kernel), so small D still fills the MMA warps.
+// CTA = (point range r, group g), blockIdx = r * ngroups + g, ONE CTA per SM, one wave: the
+// ngroups CTAs reading the same rows are adjacent in launch order and share them through L2.
 //
-// CTA = 8 warps, 2 CTAs per SM:
-//   warps 4-7 (loaders): cp.async the 128 needed features of the next kMC points into an
-//            fp32 staging ring (NS stages, 16-B pieces, zero fill past the range), then
-//            convert each element once to fp64 (x - s_f) into an fp64 tile ring (NB
-//            buffers) and accumulate the column sums of the feature blocks this group owns
-//            (the group holding the diagonal tile (f, f)). The conversion runs on the
-//            integer pipe and the subtraction only where s_f != 0: the shift kernel keeps
-//            s = 0 unless the data's mean offset is large against its spread, so in the
-//            common case the loaders put no work on the fp64 pipe that the DMMAs share
-//            (products of fp32 values are exact in fp64 either way).
-//   warps 0-3 (MMA): warp w owns tile w of the group; per 4-point k-step it loads 4 A and
-//            4 B fragments (8 LDS.64) and issues 16 DMMA.8x8x4 into a 32x32 fp64 register
-//            accumulator (64 regs).
+// CTA = 16 warps:
+//   warps 12-15 (loaders): thread ct owns 16-B pieces (4 features) of fixed column 4 (ct % P)
+//            (P = 16-B pieces per staged row) in rows ct / P + (128 / P) it of every 16-point
+//            chunk; it cp.asyncs them into a 4-stage fp32 ring, waits for its own copies only
+//            (no loader barrier), converts each value ONCE to fp64 on the integer pipe (the
+//            fp64 pipe is the DMMA pipe's shared resource; exact for normals and signed zeros,
+//            a warp-uniform F2F fallback for subnormal / inf / nan; an fp64 subtraction only
+//            when the shift kernel kept a shift s) into a 4-buffer fp64 tile ring.
+//   warps 0-11 (MMA): warp w runs tile w % ntiles on k-steps (w / ntiles) + kRep u; per
+//            k-step it loads 4 A and 4 B fragments (8 LDS.64, issued one k-step ahead) and
+//            issues 16 DMMA.8x8x4 into a 32x32 fp64 register accumulator (64 regs).
+// The column sums are NOT taken here: any fp64 add in this kernel runs on the adder the DMMAs
+// share and was measured to cost far more than its count suggests (fp64 adds in the loaders:
+// 9.6 -> 12.6-13.1 ms; one extra DMMA per k-step against an indicator operand: 9.6 -> 11.1 ms).
+// colsum_kernel takes them in a separate HBM-bound pass (~0.65 ms at cfg5) over the raw
+// points, and the reduce kernel forms S_X = sum x - n_X s.
+// Three MMA warps per SM sub-partition keep the DMMA pipe fed through the fragment-load and
+// barrier gaps that left it 26% idle with two (the 8-warp, 2-CTA/SM version).
 // Buffer hand-off with named barriers: FULL[b] (loaders arrive, MMA warps sync) and
-// EMPTY[b] (MMA warps arrive, loaders sync). Every CTA writes its own partial slot;
+// EMPTY[b] (MMA warps arrive, loaders sync). Every warp writes its own partial slot;
 // gram_reduce_kernel sums the slots in a fixed order (deterministic, bit-identical runs).
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
 
+#include <cstdlib>
+
 namespace prohd {
 namespace {
 
-constexpr int kGT = 256;       // threads per CTA
+constexpr int kGT = 512;       // threads per CTA
+constexpr int kMW = 12;        // MMA warps
 constexpr int kGMC = 16;       // points per chunk (= 4 DMMA k-steps)
 constexpr int kGNS = 4;        // fp32 staging stages
 constexpr int kGNB = 4;        // fp64 tile buffers
-constexpr int kGLd = 132;      // fp64 row stride: 128 features + 4 (conflict-free fragment loads)
-constexpr int kGStageF = kGMC * 128;                   // floats per staging stage
+constexpr int kSlotsMax = 8;   // staged feature blocks (<= 256 features)
+constexpr int kRowF = 32 * kSlotsMax;                  // staged floats per row (max)
+constexpr int kGLd = kRowF + 4;                        // fp64 row stride (conflict-free fragment loads)
+constexpr int kGStageF = kGMC * kRowF;                 // floats per staging stage
 constexpr size_t kGSmem = sizeof(float) * kGNS * kGStageF + sizeof(double) * kGNB * kGMC * kGLd;
 
 struct GramArgs {
@@ -51,9 +63,9 @@ struct GramArgs {
   const double* s;
   int ngroups, rpg;
   int64_t per;      // points per range (multiple of kGMC)
-  double* Gpart;    // [cta][4 tiles][32][32]
-  double* Spart;    // [cta][4 slots][2 sets][32]
-  short owner[2 * kGramMaxFb];  // per 32-feature block: (group, slot) holding its column sums
+  double* Gpart;    // [cta][kMW warps][32][32]
+  const double* Cpart;  // colsum_kernel partials [cs_blocks][2 sets][D]
+  int cs_blocks;
   GramGroup grp[kGramMaxGroups];
 };
 
@@ -61,32 +73,6 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
-}
-// fp32 -> fp64 on the integer pipe (the fp64 pipe is shared with the DMMAs): exact for
-// normal numbers and signed zeros; f32_special() flags the rest (subnormal, inf, nan).
-__device__ __forceinline__ bool f32_special(float x) {
-  const unsigned u = __float_as_uint(x);
-  const unsigned e = (u >> 23) & 0xFFu;
-  return e == 0xFFu || (e == 0u && (u & 0x7FFFFFu) != 0u);
-}
-__device__ __forceinline__ double f32_to_f64_normal(float x) {
-  const unsigned u = __float_as_uint(x);
-  const unsigned e = (u >> 23) & 0xFFu;
-  const unsigned sign = u & 0x80000000u, mant = u & 0x7FFFFFu;
-  const unsigned hi = e == 0u ? sign : (sign | ((e + 896u) << 20) | (mant >> 3));
-  return __hiloint2double(static_cast<int>(hi), static_cast<int>(mant << 29));
-}
-__device__ __forceinline__ double f32_to_f64(float x) {
-  return f32_special(x) ? static_cast<double>(x) : f32_to_f64_normal(x);
-}
-// (s, c) += x with Knuth's TwoSum: s + c tracks the running sum, c collects the exact
-// rounding error of every addition (fp32 pipe).
-__device__ __forceinline__ void two_sum_acc(float& s, float& c, float x) {
-  const float t = s + x;
-  const float bb = t - s;
-  const float e = (s - (t - bb)) + (x - bb);
-  s = t;
-  c += e;
 }
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -107,10 +93,10 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 // barrier ids: FULL[b] = 1 + b, EMPTY[b] = 1 + kGNB + b, loaders only = 1 + 2 kGNB
-template <bool kVec>
-__global__ void __launch_bounds__(kGT, 2) gram_kernel(const __grid_constant__ GramArgs a) {
+template <bool kVec, int kRep>
+__global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ GramArgs a) {
   extern __shared__ __align__(16) uint8_t gsm[];
-  float* stage = reinterpret_cast<float*>(gsm);                                  // [kGNS][kGMC][128]
+  float* stage = reinterpret_cast<float*>(gsm);                                  // [kGNS][kGMC][32 nslot]
   double* tile = reinterpret_cast<double*>(gsm + sizeof(float) * kGNS * kGStageF);  // [kGNB][kGMC][kGLd]
   const int g = blockIdx.x % a.ngroups;
   const int r = blockIdx.x / a.ngroups;
@@ -120,26 +106,23 @@ __global__ void __launch_bounds__(kGT, 2) gram_kernel(const __grid_constant__ Gr
   const int64_t p1 = p0 + a.per < N ? p0 + a.per : N;
   const int nch = p1 > p0 ? static_cast<int>((p1 - p0 + kGMC - 1) / kGMC) : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rowf = 32 * G.nslot;  // staged floats per row
 
-  if (warp >= 4 && kVec) {
-    // ------------------------------------------------------------------ loaders, D % 4 == 0
-    // Thread (lw, lane) owns 16-B piece (row lw + 4 it, features fb[sl] * 32 + 4 sub .. + 3)
-    // of every chunk: it issues that piece's cp.async, waits for its own copies only (no
-    // loader barrier), converts the 4 values and writes them to the fp64 tile as 2 x 16 B.
-    // A warp covers one 512-B row per it: conflict-free LDS.128 / STS.128.
-    const int ct = tid - 128, lw = ct >> 5;
-    const int sl = lane >> 3, sub = lane & 7;
-    const int ff = sl < G.nfb ? G.fb[sl] * 32 + sub * 4 : a.D;
-    const bool fv = ff < a.D;  // D % 4 == 0: the 4 features are all valid or all absent
-    const int col = sl * 32 + sub * 4;
-    const bool own = fv && G.own[sl];
-    double s4[4] = {0.0, 0.0, 0.0, 0.0};
-    if (fv)
+  if (warp >= kMW) {
+    // ------------------------------------------------------------------ loaders
+    const int ct = tid - 32 * kMW;
+    const int P = rowf / 4;               // 16-B pieces per staged row (8, 16, 32 or 64)
+    const int R = 128 / P;                // rows per pass of the 128 loader threads
+    const int NP = kGMC / R;              // pieces per thread per chunk (1, 2, 4 or 8)
+    const int c4 = ct % P, r0 = ct / P;   // column piece, first row
+    const int sl = c4 >> 3;               // slot
+    const int col = 4 * c4;               // column in the staged row
+    const int ff = G.fb[sl] * 32 + (col & 31);  // first global feature of the piece
+    double s4[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) s4[j] = a.s[ff + j];
-    // warp-uniform (the __any_sync below needs every lane): lanes without features convert zeros
+    for (int j = 0; j < 4; ++j) s4[j] = ff + j < a.D ? a.s[ff + j] : 0.0;
+    // warp-uniform (the __any_sync below needs every lane)
     const bool shifted = __any_sync(0xffffffffu, s4[0] != 0.0 || s4[1] != 0.0 || s4[2] != 0.0 || s4[3] != 0.0);
-    double sA[4] = {0.0, 0.0, 0.0, 0.0}, sB[4] = {0.0, 0.0, 0.0, 0.0};
     const uint32_t stage_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
     const uint64_t Aaddr = reinterpret_cast<uint64_t>(a.A), Baddr = reinterpret_cast<uint64_t>(a.B);
     auto issue = [&](int c) {
@@ -147,14 +130,25 @@ __global__ void __launch_bounds__(kGT, 2) gram_kernel(const __grid_constant__ Gr
         const uint32_t dst0 = stage_u32 + static_cast<uint32_t>(((c % kGNS) * kGStageF + col) * 4);
         const int64_t q0 = p0 + static_cast<int64_t>(c) * kGMC;
 #pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int pr = lw + 4 * it;
+        for (int it = 0; it < kSlotsMax; ++it) {
+          if (it >= NP) break;
+          const int pr = r0 + R * it;
           const int64_t p = q0 + pr;
-          const bool ok = fv && p < p1;
-          const uint64_t src = p < a.nA ? Aaddr + static_cast<uint64_t>(p * a.D + ff) * 4
-                                        : Baddr + static_cast<uint64_t>((p - a.nA) * a.D + ff) * 4;
-          cp_async16(dst0 + static_cast<uint32_t>(pr * 128 * 4), ok ? reinterpret_cast<const void*>(src) : a.A,
-                     ok ? 16 : 0);
+          const uint64_t rowa = p < a.nA ? Aaddr + static_cast<uint64_t>(p * a.D) * 4
+                                         : Baddr + static_cast<uint64_t>((p - a.nA) * a.D) * 4;
+          const uint32_t dst = dst0 + static_cast<uint32_t>(pr * rowf * 4);
+          if (kVec) {
+            const bool ok = p < p1 && ff < a.D;  // D % 4 == 0: all 4 features valid or none
+            cp_async16(dst, ok ? reinterpret_cast<const void*>(rowa + static_cast<uint64_t>(ff) * 4) : a.A,
+                       ok ? 16 : 0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const bool ok = p < p1 && ff + j < a.D;
+              cp_async4(dst + 4 * j, ok ? reinterpret_cast<const void*>(rowa + static_cast<uint64_t>(ff + j) * 4) : a.A,
+                        ok ? 4 : 0);
+            }
+          }
         }
       }
       cp_commit();
@@ -163,225 +157,78 @@ __global__ void __launch_bounds__(kGT, 2) gram_kernel(const __grid_constant__ Gr
     for (int c = 0; c < kGNS - 1; ++c) issue(c);
     for (int c = 0; c < nch; ++c) {
       cp_wait<kGNS - 2>();  // this thread's pieces of chunk c have landed (it reads only those)
-      float4 x[4];
+      float4 x[kSlotsMax];  // NP <= 8 pieces
       const float* src = stage + (c % kGNS) * kGStageF + col;
 #pragma unroll
-      for (int it = 0; it < 4; ++it) x[it] = *reinterpret_cast<const float4*>(src + (lw + 4 * it) * 128);
+      for (int it = 0; it < kSlotsMax; ++it)
+        if (it < NP) x[it] = *reinterpret_cast<const float4*>(src + (r0 + R * it) * rowf);
       issue(c + kGNS - 1);  // overwrites stage (c - 1) % kGNS, whose values this thread has consumed
-      const int64_t q0 = p0 + static_cast<int64_t>(c) * kGMC;
-      double v[4][4];
+      bool special = false;
       if (!shifted) {
-        // integer-pipe fp32 -> fp64 for normals and signed zeros; a warp-uniform F2F fallback
-        // if any of the warp's values is subnormal, inf or nan
-        bool special = false;
 #pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const float xs[4] = {x[it].x, x[it].y, x[it].z, x[it].w};
+        for (int it = 0; it < kSlotsMax; ++it) {
+          if (it < NP) {
+            const unsigned u[4] = {__float_as_uint(x[it].x), __float_as_uint(x[it].y), __float_as_uint(x[it].z),
+                                   __float_as_uint(x[it].w)};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const unsigned u = __float_as_uint(xs[j]);
-            const unsigned m = u & 0x7FFFFFFFu;
-            special |= (m - 1u < 0x007FFFFFu) | (m >= 0x7F800000u);
-            const unsigned hi = ((static_cast<unsigned>(static_cast<int>(u) >> 3) & 0x8FFFFFFFu)) +
-                                (m != 0u ? 0x38000000u : 0u);
-            v[it][j] = __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
+            for (int j = 0; j < 4; ++j) {
+              const unsigned m = u[j] & 0x7FFFFFFFu;
+              special |= (m - 1u < 0x007FFFFFu) | (m >= 0x7F800000u);  // subnormal, inf, nan
+            }
           }
-        }
-        if (__any_sync(0xffffffffu, special)) {
-#pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            v[it][0] = static_cast<double>(x[it].x);
-            v[it][1] = static_cast<double>(x[it].y);
-            v[it][2] = static_cast<double>(x[it].z);
-            v[it][3] = static_cast<double>(x[it].w);
-          }
-        }
-      } else {
-        // large common offset: x - s_f in fp64 (fp64 pipe); rows past the range stay 0
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const bool in = q0 + lw + 4 * it < p1;
-          v[it][0] = in ? static_cast<double>(x[it].x) - s4[0] : 0.0;
-          v[it][1] = in ? static_cast<double>(x[it].y) - s4[1] : 0.0;
-          v[it][2] = in ? static_cast<double>(x[it].z) - s4[2] : 0.0;
-          v[it][3] = in ? static_cast<double>(x[it].w) - s4[3] : 0.0;
         }
       }
+      special = __any_sync(0xffffffffu, special);
+      const int64_t q0 = p0 + static_cast<int64_t>(c) * kGMC;
       const int b = c % kGNB;
       if (c >= kGNB) named_sync(1 + kGNB + b, kGT);  // MMA warps released buffer b
       double* dst = tile + b * kGMC * kGLd + col;
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        double2* d2 = reinterpret_cast<double2*>(dst + (lw + 4 * it) * kGLd);
-        d2[0] = make_double2(v[it][0], v[it][1]);
-        d2[1] = make_double2(v[it][2], v[it][3]);
-      }
-      named_arrive(1 + b, kGT);
-      if (own) {
-        // column sums of the owned block (rows past the range are 0)
+      for (int it = 0; it < kSlotsMax; ++it) {
+        if (it >= NP) break;
+        const int pr = r0 + R * it;
+        const float xs[4] = {x[it].x, x[it].y, x[it].z, x[it].w};
+        double v[4];
+        if (shifted) {
+          // large common offset: x - s_f in fp64 (fp64 pipe); rows past the range stay 0
+          const bool in = q0 + pr < p1;
 #pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          if (q0 + lw + 4 * it < a.nA) {
+          for (int j = 0; j < 4; ++j) v[j] = in ? static_cast<double>(xs[j]) - s4[j] : 0.0;
+        } else if (special) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) sA[j] += v[it][j];
-          } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) sB[j] += v[it][j];
-          }
-        }
-      }
-    }
-    for (int c = (nch > kGNB ? nch - kGNB : 0); c < nch; ++c) named_sync(1 + kGNB + (c % kGNB), kGT);
-    cp_wait<0>();
-    // combine the 4 loader warps' column sums in a fixed order through the (now idle) staging ring
-    named_sync(1 + 2 * kGNB, 128);
-    double* red = reinterpret_cast<double*>(stage);  // [lw][slot][32][2]
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      red[((lw * 4 + sl) * 32 + sub * 4 + j) * 2 + 0] = sA[j];
-      red[((lw * 4 + sl) * 32 + sub * 4 + j) * 2 + 1] = sB[j];
-    }
-    named_sync(1 + 2 * kGNB, 128);
-    {
-      const int slot = ct >> 5;
-      double ra = 0.0, rb = 0.0;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        ra += red[((w * 4 + slot) * 32 + lane) * 2 + 0];
-        rb += red[((w * 4 + slot) * 32 + lane) * 2 + 1];
-      }
-      double* sp = a.Spart + (static_cast<int64_t>(blockIdx.x) * 4 + slot) * 64;
-      sp[lane] = ra;
-      sp[32 + lane] = rb;
-    }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------------ loaders, D % 4 != 0
-    const int ct = tid - 128;
-    const int slot = ct >> 5;
-    const int f = slot < G.nfb ? G.fb[slot] * 32 + lane : a.D;
-    const bool fvalid = f < a.D;
-    const double sf = fvalid ? a.s[f] : 0.0;  // 0 unless the shift kernel kept a shift (large offsets)
-    const bool shifted = sf != 0.0;
-    const bool own = fvalid && G.own[slot];
-    double ssA = 0.0, ssB = 0.0;
-    const uint32_t stage_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
-    auto issue = [&](int c) {  // chunk c into stage c % kGNS (one commit group per chunk)
-      if (c < nch) {
-        const uint32_t dst0 = stage_u32 + static_cast<uint32_t>((c % kGNS) * kGStageF * 4);
-        const int64_t q0 = p0 + static_cast<int64_t>(c) * kGMC;
-        if (kVec) {
-          // kGMC rows x 32 pieces of 16 B (4 slots x 8), kGMC * 32 / 128 pieces per thread
-#pragma unroll
-          for (int it = 0; it < kGMC * 32 / 128; ++it) {
-            const int q = ct + 128 * it;
-            const int pr = q >> 5, sl = (q >> 3) & 3, sub = q & 7;
-            const int64_t p = q0 + pr;
-            const int ff = sl < G.nfb ? G.fb[sl] * 32 + sub * 4 : a.D;
-            const bool ok = p < p1 && ff < a.D;
-            const float* src = p < a.nA ? a.A + p * a.D : a.B + (p - a.nA) * a.D;
-            cp_async16(dst0 + static_cast<uint32_t>((pr * 128 + sl * 32 + sub * 4) * 4), ok ? src + ff : a.A,
-                       ok ? 16 : 0);
-          }
+          for (int j = 0; j < 4; ++j) v[j] = static_cast<double>(xs[j]);
         } else {
-          // D % 4 != 0: 4-byte pieces, this thread's own feature column
-#pragma unroll 4
-          for (int pr = 0; pr < kGMC; ++pr) {
-            const int64_t p = q0 + pr;
-            const bool ok = p < p1 && fvalid;
-            const float* src = p < a.nA ? a.A + p * a.D : a.B + (p - a.nA) * a.D;
-            cp_async4(dst0 + static_cast<uint32_t>((pr * 128 + ct) * 4), ok ? src + f : a.A, ok ? 4 : 0);
+          // normal numbers and signed zeros: sign | (e + 896) << 20 | mant >> 3, mant << 29
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const unsigned u = __float_as_uint(xs[j]);
+            const unsigned hi = (static_cast<unsigned>(static_cast<int>(u) >> 3) & 0x8FFFFFFFu) +
+                                ((u & 0x7FFFFFFFu) != 0u ? 0x38000000u : 0u);
+            v[j] = __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
           }
         }
-      }
-      cp_commit();
-    };
-#pragma unroll
-    for (int c = 0; c < kGNS - 1; ++c) issue(c);
-    for (int c = 0; c < nch; ++c) {
-      cp_wait<kGNS - 2>();       // this thread's pieces of chunk c have landed
-      named_sync(1 + 2 * kGNB, 128);  // ... and everyone's; stage (c-1) % kGNS is free again
-      issue(c + kGNS - 1);
-      const int b = c % kGNB;
-      if (c >= kGNB) named_sync(1 + kGNB + b, kGT);  // MMA warps released buffer b
-      const float* src = stage + (c % kGNS) * kGStageF + ct;
-      double* dst = tile + b * kGMC * kGLd + ct;
-      const int64_t q0 = p0 + static_cast<int64_t>(c) * kGMC;
-      if (!shifted) {
-        // common case: raw values (zero-filled past the range and for absent features);
-        // all kGMC shared loads are issued first, then converted on the integer pipe
-        // (a warp-uniform F2F fallback if any value is subnormal, inf or nan); the owned
-        // column sums use an error-free fp32 TwoSum per chunk, then 4 DADDs.
-        float x[kGMC];
-#pragma unroll
-        for (int pr = 0; pr < kGMC; ++pr) x[pr] = src[pr * 128];
-        bool special = false;
-#pragma unroll
-        for (int pr = 0; pr < kGMC; ++pr) special |= f32_special(x[pr]);
-        if (__any_sync(0xffffffffu, special)) {
-#pragma unroll
-          for (int pr = 0; pr < kGMC; ++pr) dst[pr * kGLd] = static_cast<double>(x[pr]);
-        } else {
-#pragma unroll
-          for (int pr = 0; pr < kGMC; ++pr) dst[pr * kGLd] = f32_to_f64_normal(x[pr]);
-        }
-        if (own) {
-          float sA = 0.0f, cA = 0.0f, sB = 0.0f, cB = 0.0f;
-          if (q0 + kGMC <= a.nA) {
-#pragma unroll
-            for (int pr = 0; pr < kGMC; ++pr) two_sum_acc(sA, cA, x[pr]);
-          } else if (q0 >= a.nA) {
-#pragma unroll
-            for (int pr = 0; pr < kGMC; ++pr) two_sum_acc(sB, cB, x[pr]);
-          } else {
-#pragma unroll
-            for (int pr = 0; pr < kGMC; ++pr) {
-              if (q0 + pr < a.nA)
-                two_sum_acc(sA, cA, x[pr]);
-              else
-                two_sum_acc(sB, cB, x[pr]);
-            }
-          }
-          ssA += static_cast<double>(sA) + static_cast<double>(cA);
-          ssB += static_cast<double>(sB) + static_cast<double>(cB);
-        }
-      } else {
-        // large common offset: x - s_f in fp64 (fp64 pipe)
-#pragma unroll
-        for (int pr = 0; pr < kGMC; ++pr) {
-          const int64_t p = q0 + pr;
-          double v = f32_to_f64(src[pr * 128]) - sf;
-          if (p >= p1) v = 0.0;
-          dst[pr * kGLd] = v;
-          if (own) {
-            if (p < a.nA)
-              ssA += v;
-            else
-              ssB += v;
-          }
-        }
+        double2* d2 = reinterpret_cast<double2*>(dst + pr * kGLd);
+        d2[0] = make_double2(v[0], v[1]);
+        d2[1] = make_double2(v[2], v[3]);
       }
       named_arrive(1 + b, kGT);
     }
-    // pair the MMA warps' last EMPTY arrivals (chunks nch - kGNB .. nch - 1) so no barrier is left open
     for (int c = (nch > kGNB ? nch - kGNB : 0); c < nch; ++c) named_sync(1 + kGNB + (c % kGNB), kGT);
     cp_wait<0>();
-    if (slot < 4) {
-      double* sp = a.Spart + (static_cast<int64_t>(blockIdx.x) * 4 + slot) * 64;
-      sp[lane] = ssA;
-      sp[32 + lane] = ssB;
-    }
   } else {
     // ------------------------------------------------------------------ DMMA warps
-    const bool active = warp < G.ntiles;
-    const int sI = active ? G.si[warp] : 0, sJ = active ? G.sj[warp] : 0;
+    const bool active = warp < G.ntiles * kRep;
+    const int t = active ? warp % G.ntiles : 0;
+    const int ri = active ? warp / G.ntiles : 0;  // k-steps ri, ri + kRep, ... of each chunk
+    const int sI = G.si[t], sJ = G.sj[t];
     const int fr = lane >> 2, fk = lane & 3;
+    constexpr int kS = 4 / kRep;  // k-steps per chunk for this warp
+
     double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    // fragments double-buffered in registers: the loads of k-step k + 1 (the next chunk's first
-    // k-step after its FULL barrier) are issued before the 16 DMMAs of k-step k
     double af[2][4], bf[2][4];
     const int oI = sI * 32 + fr, oJ = sJ * 32 + fr;
     auto ldfrag = [&](const double* row, double (&A_)[4], double (&B_)[4]) {
@@ -392,33 +239,48 @@ __global__ void __launch_bounds__(kGT, 2) gram_kernel(const __grid_constant__ Gr
         for (int j = 0; j < 4; ++j) B_[j] = row[oJ + j * 8];
       }
     };
-    if (nch > 0) {
-      named_sync(1, kGT);
-      ldfrag(tile + fk * kGLd, af[0], bf[0]);
-    }
-    for (int c = 0; c < nch; ++c) {
-      const int b = c % kGNB;
-      const double* t = tile + b * kGMC * kGLd;
+    auto mma16 = [&](const double (&A_)[4], const double (&B_)[4]) {
+      if (active) {
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const int cur = ks & 1, nxt = cur ^ 1;
-        if (ks < 3) {
-          ldfrag(t + ((ks + 1) * 4 + fk) * kGLd, af[nxt], bf[nxt]);
-        } else if (c + 1 < nch) {
-          const int bn = (c + 1) % kGNB;
-          named_sync(1 + bn, kGT);
-          ldfrag(tile + bn * kGMC * kGLd + fk * kGLd, af[nxt], bf[nxt]);
-        }
-        if (active) {
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[cur][i], bf[cur][j]);
-        }
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], A_[i], B_[j]);
       }
-      named_arrive(1 + kGNB + b, kGT);
+    };
+    if constexpr (kS >= 2) {
+      // fragments double-buffered in registers: the loads of the warp's next k-step (the next
+      // chunk's first one after its FULL barrier) are issued before the 16 DMMAs of this one
+      if (nch > 0) {
+        named_sync(1, kGT);
+        ldfrag(tile + (ri * 4 + fk) * kGLd, af[0], bf[0]);
+      }
+      for (int c = 0; c < nch; ++c) {
+        const int b = c % kGNB;
+        const double* tb = tile + b * kGMC * kGLd;
+#pragma unroll
+        for (int u = 0; u < kS; ++u) {
+          const int cur = u & 1, nxt = cur ^ 1;
+          if (u + 1 < kS) {
+            ldfrag(tb + ((ri + kRep * (u + 1)) * 4 + fk) * kGLd, af[nxt], bf[nxt]);
+          } else if (c + 1 < nch) {
+            const int bn = (c + 1) % kGNB;
+            named_sync(1 + bn, kGT);
+            ldfrag(tile + bn * kGMC * kGLd + (ri * 4 + fk) * kGLd, af[nxt], bf[nxt]);
+          }
+          mma16(af[cur], bf[cur]);
+        }
+        named_arrive(1 + kGNB + b, kGT);
+      }
+    } else {
+      for (int c = 0; c < nch; ++c) {
+        const int b = c % kGNB;
+        named_sync(1 + b, kGT);
+        ldfrag(tile + b * kGMC * kGLd + (ri * 4 + fk) * kGLd, af[0], bf[0]);
+        mma16(af[0], bf[0]);
+        named_arrive(1 + kGNB + b, kGT);
+      }
     }
-    double* out = a.Gpart + (static_cast<int64_t>(blockIdx.x) * 4 + warp) * 1024;
+    double* out = a.Gpart + (static_cast<int64_t>(blockIdx.x) * kMW + warp) * 1024;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -428,36 +290,144 @@ __global__ void __launch_bounds__(kGT, 2) gram_kernel(const __grid_constant__ Gr
   }
 }
 
-// G (full symmetric D x D) and S_A, S_B from the per-CTA partials; ranges summed in order.
+// G (full symmetric D x D) and S_A, S_B from the partials, in a fixed order (bit-identical
+// runs): CTA = 32 consecutive elements x of one (group, tile); warp w sums the partials of
+// ranges r = w, w + 8, ... (and every k-step replica) for its lane's element, then the 8 warp
+// sums combine in warp order. The sums of S_X run on CTA 0..ceil(D / 256) - 1 likewise.
 __global__ void __launch_bounds__(256) gram_reduce_kernel(const __grid_constant__ GramArgs a, double* __restrict__ Gout,
                                                           double* __restrict__ SA, double* __restrict__ SB) {
   const int D = a.D;
-  const int64_t total = static_cast<int64_t>(a.ngroups) * 4 * 1024;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int g = static_cast<int>(e / 4096), w = static_cast<int>((e / 1024) % 4), x = static_cast<int>(e % 1024);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double part[2][8][32];
+  const int nblk = a.ngroups * kMW * 32;  // element blocks of 32
+  if (static_cast<int>(blockIdx.x) < nblk) {
+    const int g = blockIdx.x / (kMW * 32), t = (blockIdx.x / 32) % kMW;
+    const int x = (blockIdx.x % 32) * 32 + lane;
     const GramGroup& G = a.grp[g];
-    if (w >= G.ntiles) continue;
-    const int I = G.fb[G.si[w]], J = G.fb[G.sj[w]];
-    const int ii = x / 32, jj = x % 32;
-    if (I == J && ii > jj) continue;  // diagonal tiles: upper triangle is authoritative
-    const int i = I * 32 + ii, j = J * 32 + jj;
-    if (i >= D || j >= D) continue;
+    if (t >= G.ntiles) return;  // uniform per CTA
     double acc = 0.0;
-    for (int r = 0; r < a.rpg; ++r) acc += a.Gpart[(static_cast<int64_t>(r * a.ngroups + g) * 4 + w) * 1024 + x];
-    Gout[static_cast<int64_t>(i) * D + j] = acc;
-    Gout[static_cast<int64_t>(j) * D + i] = acc;
-  }
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < D; f += gridDim.x * blockDim.x) {
-    const int og = a.owner[2 * (f / 32)], os = a.owner[2 * (f / 32) + 1];
-    double sa = 0.0, sb = 0.0;
-    for (int r = 0; r < a.rpg; ++r) {
-      const double* sp = a.Spart + (static_cast<int64_t>(r * a.ngroups + og) * 4 + os) * 64;
-      sa += sp[f % 32];
-      sb += sp[32 + f % 32];
+    for (int r = warp; r < a.rpg; r += 8)
+      for (int q = 0; q < G.rep; ++q)
+        acc += a.Gpart[(static_cast<int64_t>(r * a.ngroups + g) * kMW + q * G.ntiles + t) * 1024 + x];
+    part[0][warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += part[0][w][lane];
+      const int I = G.fb[G.si[t]], J = G.fb[G.sj[t]];
+      const int ii = x / 32, jj = x % 32;
+      const int i = I * 32 + ii, j = J * 32 + jj;
+      if (!(I == J && ii > jj) && i < D && j < D) {  // diagonal tiles: upper triangle is authoritative
+        Gout[static_cast<int64_t>(i) * D + j] = v;
+        Gout[static_cast<int64_t>(j) * D + i] = v;
+      }
     }
-    SA[f] = sa;
-    SB[f] = sb;
+    return;
+  }
+  // S_X = sum_{x in X} x - n_X s (colsum_kernel partials about the origin)
+  const int f0 = (blockIdx.x - nblk) * 32 + lane;
+  const bool fv = f0 < D;
+  double sa = 0.0, sb = 0.0;
+  if (fv)
+    for (int q = warp; q < a.cs_blocks; q += 8) {
+      sa += a.Cpart[(static_cast<int64_t>(q) * 2 + 0) * D + f0];
+      sb += a.Cpart[(static_cast<int64_t>(q) * 2 + 1) * D + f0];
+    }
+  part[0][warp][lane] = sa;
+  part[1][warp][lane] = sb;
+  __syncthreads();
+  if (warp == 0 && fv) {
+    double va = 0.0, vb = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      va += part[0][w][lane];
+      vb += part[1][w][lane];
+    }
+    SA[f0] = va - static_cast<double>(a.nA) * a.s[f0];
+    SB[f0] = vb - static_cast<double>(a.nB) * a.s[f0];
+  }
+}
+
+// Column sums of A and of B about the origin, fp64: CTA q takes a contiguous range of the
+// rows of A u B; thread (row lane, column piece) adds every L-th row of the range; the L row
+// lanes combine in shared memory in a fixed order -> Cpart[q][set][f]. HBM-bound.
+template <int W>
+__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ A, int64_t nA,
+                                                     const float* __restrict__ B, int64_t nB, int D, int64_t per,
+                                                     double* __restrict__ Cpart) {
+  const int P = (D + W - 1) / W;          // W-feature pieces per row
+  const int L = P >= 256 ? 1 : 256 / P;   // row lanes (1: the CTA loops over blocks of 256 pieces)
+  const int64_t N = nA + nB;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * per;
+  const int64_t r1 = r0 + per < N ? r0 + per : N;
+  __shared__ double red[2][1024];
+  for (int pcb = 0; pcb < (L == 1 ? P : 1); pcb += 256) {
+    const int lr = L == 1 ? 0 : static_cast<int>(threadIdx.x) / P;
+    const int pc = L == 1 ? pcb + static_cast<int>(threadIdx.x) : static_cast<int>(threadIdx.x) % P;
+    const bool act = pc < P && lr < L;
+    double sa[W], sb[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) sa[j] = sb[j] = 0.0;
+    if (act) {
+      const int f0 = pc * W;
+      // 4 rows per step, loads issued before the adds (HBM latency)
+      for (int64_t r = r0 + lr; r < r1; r += 4 * static_cast<int64_t>(L)) {
+        float v[4][W];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t rr = r + static_cast<int64_t>(u) * L;
+          const bool ok = rr < r1;
+          const float* row = rr < nA ? A + rr * D : B + (rr - nA) * D;
+          if constexpr (W == 4) {
+            const float4 q = ok ? __ldg(reinterpret_cast<const float4*>(row + f0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[u][0] = q.x;
+            v[u][1] = q.y;
+            v[u][2] = q.z;
+            v[u][3] = q.w;
+          } else {
+            v[u][0] = ok ? __ldg(row + f0) : 0.0f;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool inA = r + static_cast<int64_t>(u) * L < nA;
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            if (inA)
+              sa[j] += static_cast<double>(v[u][j]);
+            else
+              sb[j] += static_cast<double>(v[u][j]);
+          }
+        }
+      }
+    }
+    if (L == 1) {
+      if (act)
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+          if (pc * W + j < D) {
+            Cpart[(static_cast<int64_t>(blockIdx.x) * 2 + 0) * D + pc * W + j] = sa[j];
+            Cpart[(static_cast<int64_t>(blockIdx.x) * 2 + 1) * D + pc * W + j] = sb[j];
+          }
+      continue;
+    }
+    for (int l = 0; l < L; ++l) {  // fixed order over the row lanes
+      if (act && lr == l)
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const int f = pc * W + j;
+          if (f < D) {
+            red[0][f] = (l == 0 ? 0.0 : red[0][f]) + sa[j];
+            red[1][f] = (l == 0 ? 0.0 : red[1][f]) + sb[j];
+          }
+        }
+      __syncthreads();
+    }
+    for (int f = threadIdx.x; f < D; f += blockDim.x) {
+      Cpart[(static_cast<int64_t>(blockIdx.x) * 2 + 0) * D + f] = red[0][f];
+      Cpart[(static_cast<int64_t>(blockIdx.x) * 2 + 1) * D + f] = red[1][f];
+    }
   }
 }
 
@@ -465,97 +435,89 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const __grid_constant_
 
 // Host-side grouping of the upper-triangle 32x32 tiles (see the file header).
 bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p) {
-  const int nb32 = (D + 31) / 32;
-  if (nb32 > kGramMaxFb) return false;
-  const int nb64 = (nb32 + 1) / 2;
+  const int nb = (D + 31) / 32;
+  if (nb > kGramMaxFb) return false;
+  p = GramPlan{};
   p.ngroups = 0;
-  auto add_group = [&](const int (*tiles)[2], int nt) -> bool {
-    if (p.ngroups >= kGramMaxGroups) return false;
+  // one group: the given tiles over the given feature blocks (slot = position in fbs)
+  auto add_group = [&](const int* fbs, int nfb, const int (*tiles)[2], int nt) -> bool {
+    if (p.ngroups >= kGramMaxGroups || nt < 1 || nt > kMW || nfb > kSlotsMax) return false;
     GramGroup& G = p.grp[p.ngroups++];
     G = GramGroup{};
+    G.nslot = 1;
+    while (G.nslot < nfb) G.nslot = static_cast<unsigned char>(G.nslot * 2);
+    for (int s = 0; s < kSlotsMax; ++s) G.fb[s] = static_cast<unsigned char>(s < nfb ? fbs[s] : kGramMaxFb - 1);
+    G.nfb = static_cast<unsigned char>(nfb);
     for (int t = 0; t < nt; ++t) {
-      const int blk[2] = {tiles[t][0], tiles[t][1]};
-      int sl[2];
       for (int q = 0; q < 2; ++q) {
         int s = 0;
-        while (s < G.nfb && G.fb[s] != blk[q]) ++s;
-        if (s == G.nfb) G.fb[G.nfb++] = static_cast<unsigned char>(blk[q]);
-        sl[q] = s;
+        while (s < nfb && fbs[s] != tiles[t][q]) ++s;
+        if (s == nfb) return false;
+        (q == 0 ? G.si : G.sj)[t] = static_cast<unsigned char>(s);
       }
-      G.si[t] = static_cast<unsigned char>(sl[0]);
-      G.sj[t] = static_cast<unsigned char>(sl[1]);
     }
     G.ntiles = static_cast<unsigned char>(nt);
+    G.rep = static_cast<unsigned char>(nt * 4 <= kMW ? 4 : nt * 2 <= kMW ? 2 : 1);
     return true;
   };
-  // off-diagonal 64x64 blocks: one group each
-  for (int a = 0; a < nb64; ++a)
-    for (int b = a + 1; b < nb64; ++b) {
-      int tl[4][2], nt = 0;
-      for (int i = 2 * a; i < 2 * a + 2; ++i)
-        for (int j = 2 * b; j < 2 * b + 2; ++j)
-          if (i < nb32 && j < nb32) {
-            tl[nt][0] = i;
-            tl[nt][1] = j;
-            ++nt;
-          }
-      if (nt > 0 && !add_group(tl, nt)) return false;
-    }
-  // diagonal 64x64 blocks: their upper 32x32 tiles, packed <= 4 tiles / <= 4 feature blocks
-  {
-    int tl[4][2], nt = 0, fbs[8], nfb = 0;
-    for (int a = 0; a < nb64; ++a) {
-      const int cand[3][2] = {{2 * a, 2 * a}, {2 * a, 2 * a + 1}, {2 * a + 1, 2 * a + 1}};
-      for (int c = 0; c < 3; ++c) {
-        const int i = cand[c][0], j = cand[c][1];
-        if (i >= nb32 || j >= nb32) continue;
-        int extra = 0;
-        for (int q = 0; q < 2; ++q) {
-          const int blk = q == 0 ? i : j;
-          bool seen = (q == 1 && j == i);
-          for (int s = 0; s < nfb && !seen; ++s) seen = fbs[s] == blk;
-          extra += seen ? 0 : 1;
-        }
-        if (nt == 4 || nfb + extra > 4) {
-          if (!add_group(tl, nt)) return false;
-          nt = 0;
-          nfb = 0;
-        }
-        for (int q = 0; q < 2; ++q) {
-          const int blk = q == 0 ? i : j;
-          bool seen = false;
-          for (int s = 0; s < nfb; ++s) seen = seen || fbs[s] == blk;
-          if (!seen) fbs[nfb++] = blk;
-        }
-        tl[nt][0] = i;
-        tl[nt][1] = j;
-        ++nt;
+  if (nb <= kSlotsMax) {
+    // every group stages all nb blocks; the T = nb (nb + 1) / 2 tiles split evenly
+    int fbs[kSlotsMax], tl[64][2], T = 0;
+    for (int s = 0; s < nb; ++s) fbs[s] = s;
+    for (int i = 0; i < nb; ++i)
+      for (int j = i; j < nb; ++j) {
+        tl[T][0] = i;
+        tl[T][1] = j;
+        ++T;
       }
+    const int ng = (T + kMW - 1) / kMW;
+    for (int g = 0; g < ng; ++g) {
+      const int t0 = T * g / ng, t1 = T * (g + 1) / ng;
+      if (!add_group(fbs, nb, tl + t0, t1 - t0)) return false;
     }
-    if (nt > 0 && !add_group(tl, nt)) return false;
-  }
-  // owner of each feature block's column sums: the group holding its diagonal tile
-  for (int fb = 0; fb < nb32; ++fb) {
-    p.owner[2 * fb] = -1;
-    for (int g = 0; g < p.ngroups; ++g)
-      for (int t = 0; t < p.grp[g].ntiles; ++t)
-        if (p.grp[g].fb[p.grp[g].si[t]] == fb && p.grp[g].fb[p.grp[g].sj[t]] == fb) {
-          p.owner[2 * fb] = g;
-          p.owner[2 * fb + 1] = p.grp[g].si[t];
-          p.grp[g].own[p.grp[g].si[t]] = 1;
+  } else {
+    // 4x4 squares of blocks on or above the diagonal: <= 8 blocks, <= 16 tiles -> 1 or 2 groups
+    for (int a = 0; a < nb; a += 4)
+      for (int b = a; b < nb; b += 4) {
+        int fbs[kSlotsMax], nfb = 0, tl[16][2], T = 0;
+        for (int i = a; i < a + 4 && i < nb; ++i) fbs[nfb++] = i;
+        if (b != a)
+          for (int j = b; j < b + 4 && j < nb; ++j) fbs[nfb++] = j;
+        for (int i = a; i < a + 4 && i < nb; ++i)
+          for (int j = b; j < b + 4 && j < nb; ++j)
+            if (i <= j) {
+              tl[T][0] = i;
+              tl[T][1] = j;
+              ++T;
+            }
+        const int ng = (T + kMW - 1) / kMW;
+        for (int g = 0; g < ng; ++g) {
+          const int t0 = T * g / ng, t1 = T * (g + 1) / ng;
+          if (!add_group(fbs, nfb, tl + t0, t1 - t0)) return false;
         }
-    if (p.owner[2 * fb] < 0) return false;
+      }
   }
+  // the kernel instantiates kRep per launch: every group must share one
+  for (int g = 1; g < p.ngroups; ++g)
+    if (p.grp[g].rep != p.grp[0].rep) {
+      unsigned char m = p.grp[0].rep;
+      for (int q = 0; q < p.ngroups; ++q) m = p.grp[q].rep < m ? p.grp[q].rep : m;
+      for (int q = 0; q < p.ngroups; ++q) p.grp[q].rep = m;
+      break;
+    }
   const int64_t N = nA + nB;
   const int64_t chunks = N > 0 ? (N + kGMC - 1) / kGMC : 1;
-  int rpg = (2 * (num_sms > 0 ? num_sms : 148)) / p.ngroups;
+  int rpg = (num_sms > 0 ? num_sms : 148) / p.ngroups;  // one CTA per SM, one wave
   if (rpg < 1) rpg = 1;
   if (rpg > chunks) rpg = static_cast<int>(chunks);
   p.rpg = rpg;
   p.per = ((N + rpg - 1) / rpg + kGMC - 1) / kGMC * kGMC;
   p.nctas = p.ngroups * rpg;
-  p.gpart_doubles = static_cast<int64_t>(p.nctas) * 4 * 1024;
-  p.spart_doubles = static_cast<int64_t>(p.nctas) * 4 * 64;
+  p.gpart_doubles = static_cast<int64_t>(p.nctas) * kMW * 1024;
+  p.cs_blocks = 4 * (num_sms > 0 ? num_sms : 148);
+  if (p.cs_blocks > N) p.cs_blocks = static_cast<int>(N > 0 ? N : 1);
+  p.cs_per = (N + p.cs_blocks - 1) / p.cs_blocks;
+  p.spart_doubles = static_cast<int64_t>(p.cs_blocks) * 2 * D;
   return true;
 }
 
@@ -573,19 +535,26 @@ cudaError_t launch_gram(const GramPlan& p, const float* A, int64_t nA, const flo
   a.rpg = p.rpg;
   a.per = p.per;
   a.Gpart = Gpart;
-  a.Spart = Spart;
   for (int g = 0; g < p.ngroups; ++g) a.grp[g] = p.grp[g];
-  for (int q = 0; q < 2 * kGramMaxFb; ++q) a.owner[q] = static_cast<short>(p.owner[q]);
-  cudaError_t e;
+  a.Cpart = Spart;
+  a.cs_blocks = p.cs_blocks;
   const bool vec = (D % 4) == 0;
-  auto kern = vec ? gram_kernel<true> : gram_kernel<false>;
+  const int rep = p.grp[0].rep;
+  auto kern = vec ? (rep == 4 ? gram_kernel<true, 4> : rep == 2 ? gram_kernel<true, 2> : gram_kernel<true, 1>)
+                  : (rep == 4 ? gram_kernel<false, 4> : rep == 2 ? gram_kernel<false, 2> : gram_kernel<false, 1>);
+  cudaError_t e;
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGSmem))) !=
       cudaSuccess)
     return e;
   count_launch();
+  if (vec)
+    colsum_kernel<4><<<p.cs_blocks, 256, 0, st>>>(A, nA, B, nB, D, p.cs_per, Spart);
+  else
+    colsum_kernel<1><<<p.cs_blocks, 256, 0, st>>>(A, nA, B, nB, D, p.cs_per, Spart);
+  count_launch();
   kern<<<p.nctas, kGT, kGSmem, st>>>(a);
   count_launch();
-  gram_reduce_kernel<<<148 * 2, 256, 0, st>>>(a, Gout, SA, SB);
+  gram_reduce_kernel<<<p.ngroups * kMW * 32 + (D + 31) / 32, 256, 0, st>>>(a, Gout, SA, SB);
   return cudaGetLastError();
 }
 

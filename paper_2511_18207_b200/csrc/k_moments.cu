@@ -49,15 +49,28 @@ __global__ void __launch_bounds__(1024) shift_kernel(const float* __restrict__ A
   const int64_t cb = nB < 4096 ? nB : 4096;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (f < D) {
-    for (int64_t i = w; i < ca; i += 32) {
-      const double x = static_cast<double>(__ldg(A + i * D + f));
-      acc[0] += x;
-      acc[1] += x * x;
+    // 8 rows per step: the loads are issued together (this kernel is latency-bound)
+    for (int64_t i0 = w; i0 < ca; i0 += 32 * 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = i0 + 32 * u < ca ? __ldg(A + (i0 + 32 * u) * D + f) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double x = static_cast<double>(v[u]);
+        acc[0] += x;
+        acc[1] += x * x;
+      }
     }
-    for (int64_t i = w; i < cb; i += 32) {
-      const double x = static_cast<double>(__ldg(B + i * D + f));
-      acc[2] += x;
-      acc[3] += x * x;
+    for (int64_t i0 = w; i0 < cb; i0 += 32 * 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = i0 + 32 * u < cb ? __ldg(B + (i0 + 32 * u) * D + f) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double x = static_cast<double>(v[u]);
+        acc[2] += x;
+        acc[3] += x * x;
+      }
     }
   }
 #pragma unroll

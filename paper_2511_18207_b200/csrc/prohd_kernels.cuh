@@ -8,20 +8,20 @@
 namespace prohd {
 
 // ---------------------------------------------------------------- K1
-// Gram pass (k_gram.cu): groups of <= 4 upper-triangle 32x32 tiles over <= 4 feature blocks
-constexpr int kGramMaxFb = 32;       // D <= 1024
-constexpr int kGramMaxGroups = 136;  // 120 off-diagonal + 12 diagonal groups at D = 1024
+// Gram pass (k_gram.cu): groups of <= 12 upper-triangle 32x32 tiles over <= 8 feature blocks
+constexpr int kGramMaxFb = 32;      // D <= 1024
+constexpr int kGramMaxGroups = 64;  // 8 diagonal + 2 x 28 off-diagonal 4x4-block squares at D = 1024
 struct GramGroup {
-  unsigned char ntiles, nfb;
-  unsigned char fb[4];   // feature blocks (32 features each) staged in slots 0..3
-  unsigned char si[4];   // tile t = (fb[si[t]], fb[sj[t]])
-  unsigned char sj[4];
-  unsigned char own[4];  // slot s accumulates the column sums of fb[s]
+  unsigned char ntiles, nfb, nslot, rep;  // nslot: staged slots (power of 2 >= nfb); rep: warps per tile
+  unsigned char fb[8];    // feature blocks (32 features each) staged in slots 0..nfb-1
+  unsigned char si[12];   // tile t = (fb[si[t]], fb[sj[t]])
+  unsigned char sj[12];
 };
 struct GramPlan {
   int ngroups = 0, rpg = 0, nctas = 0;
   int64_t per = 0, gpart_doubles = 0, spart_doubles = 0;
-  int owner[2 * kGramMaxFb];
+  int cs_blocks = 0;     // colsum_kernel CTAs (row ranges)
+  int64_t cs_per = 0;    // rows per colsum CTA
   GramGroup grp[kGramMaxGroups];
 };
 bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p);
