@@ -21,6 +21,8 @@
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
 
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 
 namespace prohd {
@@ -39,38 +41,39 @@ constexpr int kFB = 64;       // feature block
 // at full size (tools/dir_accuracy.py): cfg4 (ratio 31.7, top-16 gaps down to 1.1e-4)
 // gives PC sin-angles of 2.7e-12 unshifted vs 1.2e-13 shifted, against a selection
 // margin of 5e-8; linear in the ratio, the 1024 bound keeps them below ~1e-10.
-__global__ void __launch_bounds__(1024) shift_kernel(const float* __restrict__ A, int64_t nA,
-                                                     const float* __restrict__ B, int64_t nB, int D,
-                                                     double* __restrict__ s) {
+// One 8-CTA cluster per 32 features: CTA q of the cluster takes rows [512 q, 512 q + 512) of
+// the first <= 4096 rows of each set (warp w: rows 512 q + w + 32 u), the 32 warps combine in a
+// fixed tree, and CTA 0 adds the 8 CTA partials in rank order through distributed shared
+// memory (latency-bound kernel: 8x the memory-level parallelism of one CTA per 32 features).
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(1024) shift_kernel(const float* __restrict__ A, int64_t nA,
+                                                                               const float* __restrict__ B, int64_t nB,
+                                                                               int D, double* __restrict__ s) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
   __shared__ double part[4][32][33];  // sum and sum of squares, of A and of B
+  __shared__ double clpart[8][4][32];  // CTA partials (used in rank 0)
+  const int rank = static_cast<int>(cl.block_rank());
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane;
+  const int f = (blockIdx.x / 8) * 32 + lane;
   const int64_t ca = nA < 4096 ? nA : 4096;
   const int64_t cb = nB < 4096 ? nB : 4096;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (f < D) {
-    // 8 rows per step: the loads are issued together (this kernel is latency-bound)
-    for (int64_t i0 = w; i0 < ca; i0 += 32 * 8) {
-      float v[8];
+    const int64_t r0 = 512 * rank + w;
+    float va[16], vb[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = i0 + 32 * u < ca ? __ldg(A + (i0 + 32 * u) * D + f) : 0.0f;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double x = static_cast<double>(v[u]);
-        acc[0] += x;
-        acc[1] += x * x;
-      }
+    for (int u = 0; u < 16; ++u) {
+      const int64_t r = r0 + 32 * u;
+      va[u] = r < ca ? __ldg(A + r * D + f) : 0.0f;
+      vb[u] = r < cb ? __ldg(B + r * D + f) : 0.0f;
     }
-    for (int64_t i0 = w; i0 < cb; i0 += 32 * 8) {
-      float v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = i0 + 32 * u < cb ? __ldg(B + (i0 + 32 * u) * D + f) : 0.0f;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double x = static_cast<double>(v[u]);
-        acc[2] += x;
-        acc[3] += x * x;
-      }
+    for (int u = 0; u < 16; ++u) {
+      const double x = static_cast<double>(va[u]), y = static_cast<double>(vb[u]);
+      acc[0] += x;
+      acc[1] += x * x;
+      acc[2] += y;
+      acc[3] += y * y;
     }
   }
 #pragma unroll
@@ -82,12 +85,18 @@ __global__ void __launch_bounds__(1024) shift_kernel(const float* __restrict__ A
       for (int q = 0; q < 4; ++q) part[q][w][lane] += part[q][w + o][lane];
     __syncthreads();
   }
-  if (w == 0 && f < D) {
+  if (w < 4) *cl.map_shared_rank(&clpart[rank][w][lane], 0) = part[w][0][lane];
+  cl.sync();
+  if (rank == 0 && w == 0 && f < D) {
+    double t[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) t[k] += clpart[q][k][lane];
     // per-set sums added last: the same bits for (A, B) and (B, A)
     const double cnt = static_cast<double>(ca + cb);
-    const double m = (part[0][0][lane] + part[2][0][lane]) / cnt;
+    const double m = (t[0] + t[2]) / cnt;
     s[f] = m;
-    s[D + f] = fmax((part[1][0][lane] + part[3][0][lane]) / cnt - m * m, 0.0);
+    s[D + f] = fmax((t[1] + t[3]) / cnt - m * m, 0.0);
   }
 }
 
@@ -411,14 +420,14 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
 cudaError_t launch_centre(const float* X, int64_t nX, const float* Y, int64_t nY, int D, double* c,
                           cudaStream_t st) {
   count_launch();
-  shift_kernel<<<(D + 31) / 32, 1024, 0, st>>>(X, nX, Y, nY, D, c);
+  shift_kernel<<<8 * ((D + 31) / 32), 1024, 0, st>>>(X, nX, Y, nY, D, c);
   return cudaGetLastError();
 }
 
 cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB, int D, double* s,
                          cudaStream_t st) {
   count_launch();
-  shift_kernel<<<(D + 31) / 32, 1024, 0, st>>>(A, nA, B, nB, D, s);
+  shift_kernel<<<8 * ((D + 31) / 32), 1024, 0, st>>>(A, nA, B, nB, D, s);
   count_launch();
   const char* fe = getenv("PROHD_SHIFT");  // dev A/B only: 0 = never shift, 1 = always
   const int force = (fe != nullptr && (fe[0] == '0' || fe[0] == '1')) ? fe[0] - '0' : -1;
