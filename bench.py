@@ -194,7 +194,8 @@ def run_ours(args, rank: int, world: int):
     from paper_2511_18207_b200 import Context
     from paper_2511_18207_b200.dist import CudaPhases, row_range, sharded_directed_hd, sharded_prohd_estimate
 
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; the modulo only matters for functional multi-rank runs on fewer GPUs
+    local_rank = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     c = datagen.CONFIGS[args.config]
@@ -251,10 +252,12 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
+    lc0 = ctx.launch_count()
     g0.record(stream)
     recs = [step() for _ in range(args.steps)]
     g1.record(stream)
     torch.cuda.synchronize()
+    lc1 = ctx.launch_count()
     if world > 1:
         tdist.barrier()
     clk = clocks.stop()
@@ -283,11 +286,44 @@ def run_ours(args, rank: int, world: int):
     tf32_peak = pk["bf16_tflops"] * NOMINAL_TF32_OVER_BF16
     tf32_peak_sustained = pk["bf16_tflops_sustained"] * NOMINAL_TF32_OVER_BF16
     tpp, tsrc = k6_traffic_per_pair(D)
-    launches = sum((r[2]["kernel_launches"] if r[2] else 0) + (r[3]["kernel_launches"] if r[3] else 0) for r in recs)
+    # our kernels launched inside the timed region, summed over the ranks (library-wide counter)
+    lt = torch.tensor([float(lc1 - lc0)], dtype=torch.float64, device=dev)
     if world > 1:
-        launches = None  # sharded step: phase calls on every rank plus witness kernels on the owner rank
+        tdist.all_reduce(lt, op=tdist.ReduceOp.SUM)
+    launches = int(lt.item())
     # ------------------------------------------------------------ end to end (host buffers through the ABI)
     e2e = None
+    if world > 1 and not args.no_e2e:
+        # every step: H2D of this rank's ProHD row shards of A and B and of the replicated B (the
+        # exact kernel's column set) from pinned host memory, the sharded step, results to host
+        Alh = torch.from_numpy(Ah[lo:hi]).pin_memory()
+        Blh = torch.from_numpy(Bh[lb:hb]).pin_memory()
+        Bfh = torch.from_numpy(Bh).pin_memory()
+        torch.cuda.synchronize()
+        tdist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        d2h = 0
+        for _ in range(args.steps):
+            A_d = Alh.to(dev, non_blocking=True)
+            B_d = Blh.to(dev, non_blocking=True)
+            Bf_d = Bfh.to(dev, non_blocking=True)
+            ee = sharded_prohd_estimate(A_d, lo, n, B_d, lb, n, k, m, phases, device=dev)
+            sharded_directed_hd(A_d, lo, Bf_d, local_fn, phases.witness_fn, device=dev)
+            d2h += 256
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tdist.barrier()
+        et = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+        tdist.all_reduce(et, op=tdist.ReduceOp.MAX)
+        e_ms = float(et.item())
+        hb_t = torch.tensor([float(Alh.numel() * 4 + Blh.numel() * 4 + Bfh.numel() * 4)], dtype=torch.float64,
+                            device=dev)
+        tdist.all_reduce(hb_t, op=tdist.ReduceOp.SUM)
+        e2e = {"value": pairs_step / (e_ms / 1e3) / 1e9, "unit": "Gpair/s",
+               "h2d_bytes_per_step": int(hb_t.item()), "d2h_bytes_per_step": int(d2h / args.steps) * world,
+               "ms_per_step": e_ms}
     if world == 1 and not args.no_e2e:
         Ap = torch.from_numpy(Ah).pin_memory()
         Bp = torch.from_numpy(Bh).pin_memory()
@@ -358,10 +394,11 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
         import torch.distributed as tdist
-        backend = "gloo" if args.impl == "reference" else "nccl"
+        # PROHD_BENCH_BACKEND=gloo: functional multi-rank check on a box with fewer GPUs than ranks
+        backend = "gloo" if args.impl == "reference" else os.environ.get("PROHD_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             import torch
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count()))
         tdist.init_process_group(backend=backend)
     try:
         if args.impl == "reference":

@@ -72,6 +72,9 @@ int prohd_set_stream(prohd_ctx* ctx, void* cuda_stream);
 const char* prohd_last_error(const prohd_ctx* ctx);
 /* Library version string, e.g. "prohd-b200 0.1 sm_100a". Never NULL. */
 const char* prohd_version(void);
+/* Kernels this process has launched through the library so far (all contexts; tracing and
+ * the benchmark's gpu_launches). *out (HOST) receives the count; PROHD_E_INVALID if NULL. */
+int prohd_launch_count(int64_t* out);
 
 /* Bytes of device workspace any call below needs for these sizes (max over
  * directed_hd, hausdorff and prohd_estimate). Pure host arithmetic. */

@@ -90,6 +90,12 @@ class Context:
         self._check(self.lib.prohd_set_stream(self.h, C.c_void_p(stream)))
         return A, B
 
+    def launch_count(self) -> int:
+        """prohd_launch_count: kernels this process has launched through the library."""
+        v = C.c_int64(0)
+        self._check(self.lib.prohd_launch_count(C.byref(v)))
+        return int(v.value)
+
     def enable_timing(self, on: bool = True):
         """Record per-phase CUDA events inside every following call (prohd_enable_timing)."""
         self._check(self.lib.prohd_enable_timing(self.h, 1 if on else 0))

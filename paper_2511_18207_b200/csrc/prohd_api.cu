@@ -25,6 +25,12 @@ extern "C" {
 
 const char* prohd_version(void) { return "prohd-b200 0.1 sm_100a"; }
 
+int prohd_launch_count(int64_t* out) {
+  if (out == nullptr) return PROHD_E_INVALID;
+  *out = static_cast<int64_t>(prohd::launch_counter().load());
+  return PROHD_OK;
+}
+
 int prohd_create(int device, void* cuda_stream, prohd_ctx** out) {
   if (out == nullptr) return PROHD_E_INVALID;
   *out = nullptr;
