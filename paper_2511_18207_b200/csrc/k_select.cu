@@ -211,13 +211,27 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const float* __restrict
   const unsigned pre0 = state[(l * 2 + 0) * 4 + 0], msk0 = state[(l * 2 + 0) * 4 + 1];
   const unsigned pre1 = state[(l * 2 + 1) * 4 + 0], msk1 = state[(l * 2 + 1) * 4 + 1];
   const float* p = P32 + static_cast<int64_t>(l) * n;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const unsigned kt = order_key(__ldg(p + i));
+  auto add = [&](float x) {
+    const unsigned kt = order_key(x);
     const unsigned kb = ~kt;
     if ((kt & msk0) == pre0) atomicAdd(&sh[0][(kt >> shift) & binmask], 1u);
     if ((kb & msk1) == pre1) atomicAdd(&sh[1][(kb >> shift) & binmask], 1u);
+  };
+  // 16-B loads over the aligned middle of the row, scalar head and tail
+  const int64_t head = min(n, static_cast<int64_t>(((16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15) / 4));
+  const int64_t nv = (n - head) / 4;
+  const float4* p4 = reinterpret_cast<const float4*>(p + head);
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (tid < head) add(__ldg(p + tid));
+  for (int64_t q = tid; q < nv; q += stride) {
+    const float4 v = __ldg(p4 + q);
+    add(v.x);
+    add(v.y);
+    add(v.z);
+    add(v.w);
   }
+  for (int64_t i = head + 4 * nv + tid; i < n; i += stride) add(__ldg(p + i));
   __syncthreads();
   unsigned* g = hist + (static_cast<int64_t>(round) * L + l) * 2 * kRadixBins;
   for (int i = threadIdx.x; i < 2 * kRadixBins; i += blockDim.x) {
@@ -310,26 +324,64 @@ __global__ void __launch_bounds__(256) collect_kernel(const float* __restrict__ 
   const double hi_bot = all ? inf : Tbot + 2.0 * eps;   // bottom candidates: pi <= hi_bot
   const float* p = P32 + static_cast<int64_t>(l) * n;
   const int lane = threadIdx.x & 31;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n;
+  // every lane takes 4 consecutive points per step (16-B loads where the row is aligned); the
+  // warp reserves its candidates of each tail with one atomicAdd and an exclusive lane scan
+  const int64_t head = min(n, static_cast<int64_t>(((16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15) / 4));
+  const int64_t nq = head + (n - head + 3) / 4;  // head singletons, then groups of 4
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < nq;
        base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const double v = i < n ? static_cast<double>(__ldg(p + i)) : 0.0;
-    const bool ct = i < n && v >= lo_top;
-    const bool cb = i < n && v <= hi_bot;
+    const int64_t q = base + threadIdx.x;
+    float v[4];
+    int64_t i0 = 0;
+    int nvalid = 0;
+    if (q < head) {
+      i0 = q;
+      nvalid = 1;
+      v[0] = __ldg(p + q);
+    } else if (q < nq) {
+      i0 = head + 4 * (q - head);
+      nvalid = n - i0 < 4 ? static_cast<int>(n - i0) : 4;
+      if (nvalid == 4) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(p + i0));
+        v[0] = w.x;
+        v[1] = w.y;
+        v[2] = w.z;
+        v[3] = w.w;
+      } else {
+        for (int j = 0; j < nvalid; ++j) v[j] = __ldg(p + i0 + j);
+      }
+    }
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-      const bool c = t == 0 ? ct : cb;
-      const unsigned bal = __ballot_sync(0xffffffffu, c);
-      if (bal == 0u) continue;
+      unsigned mask = 0u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double x = static_cast<double>(v[j]);
+        const bool c = j < nvalid && (t == 0 ? x >= lo_top : x <= hi_bot);
+        mask |= c ? 1u << j : 0u;
+      }
+      const unsigned cnt = __popc(mask);
+      unsigned incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+      if (total == 0u) continue;
       unsigned pos0 = 0;
-      if (lane == 0) pos0 = atomicAdd(&ccount[l * 2 + t], __popc(bal));
-      pos0 = __shfl_sync(0xffffffffu, pos0, 0);
-      if (c) {
-        const unsigned pos = pos0 + __popc(bal & ((1u << lane) - 1u));
-        if (pos < cap)
-          cand[(static_cast<int64_t>(l) * 2 + t) * cap + pos] = static_cast<int>(i);
-        else
-          *overflow = 1;
+      if (lane == 31) pos0 = atomicAdd(&ccount[l * 2 + t], total);
+      pos0 = __shfl_sync(0xffffffffu, pos0, 31);
+      unsigned pos = pos0 + incl - cnt;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (mask & (1u << j)) {
+          if (pos < cap)
+            cand[(static_cast<int64_t>(l) * 2 + t) * cap + pos] = static_cast<int>(i0 + j);
+          else
+            *overflow = 1;
+          ++pos;
+        }
       }
     }
   }
@@ -369,16 +421,34 @@ __global__ void __launch_bounds__(256) rank_kernel(int L, const int* n_dirs, con
   const int64_t cnt = min(static_cast<int64_t>(ccount[lt]), cap);
   const int* ci = cand + static_cast<int64_t>(lt) * cap;
   const double* cv = cval + static_cast<int64_t>(lt) * cap;
+  constexpr int kStage = 3072;  // candidates staged in shared memory (the band is usually ~m + a few)
+  __shared__ double sv[kStage];
+  __shared__ int si[kStage];
+  const bool staged = cnt <= kStage;
+  if (staged) {
+    for (int64_t o = threadIdx.x; o < cnt; o += blockDim.x) {
+      sv[o] = cv[o];
+      si[o] = ci[o];
+    }
+    __syncthreads();
+  }
   for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < cnt;
        c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double v = cv[c];
-    const int i = ci[c];
+    const double v = staged ? sv[c] : cv[c];
+    const int i = staged ? si[c] : ci[c];
     int64_t rank = 0;
-    for (int64_t o = 0; o < cnt; ++o) {
-      const double w = cv[o];
-      const int j = ci[o];
-      const bool better = (t == 0) ? (w > v || (w == v && j < i)) : (w < v || (w == v && j < i));
-      rank += better ? 1 : 0;
+    if (staged) {
+      for (int o = 0; o < static_cast<int>(cnt); ++o) {
+        const double w = sv[o];
+        const int j = si[o];
+        rank += ((t == 0) ? (w > v || (w == v && j < i)) : (w < v || (w == v && j < i))) ? 1 : 0;
+      }
+    } else {
+      for (int64_t o = 0; o < cnt; ++o) {
+        const double w = cv[o];
+        const int j = ci[o];
+        rank += ((t == 0) ? (w > v || (w == v && j < i)) : (w < v || (w == v && j < i))) ? 1 : 0;
+      }
     }
     if (rank < m) {
       if (lists != nullptr) lists[static_cast<int64_t>(lt) * m + rank] = i;
@@ -391,26 +461,53 @@ __global__ void __launch_bounds__(256) rank_kernel(int L, const int* n_dirs, con
   }
 }
 
-// single-CTA compaction of the bitmap into the sorted unique union
-__global__ void __launch_bounds__(1024) compact_kernel(const unsigned* __restrict__ bitmap, int64_t nwords,
-                                                       long long* uidx, unsigned* ucount) {
-  __shared__ unsigned part[1024];
-  const int tid = threadIdx.x;
-  const int64_t per = (nwords + 1023) / 1024;
-  const int64_t w0 = tid * per, w1 = min(nwords, w0 + per);
+// K5 compaction of the n-bit bitmap into the sorted unique union, two launches over kCB
+// CTAs, each owning a contiguous word range: (a) per-CTA popcounts, (b) each CTA adds the
+// counts of the CTAs before it, scans its threads' counts and writes its indices in order.
+constexpr int kCB = kCompactBlocks;
+__global__ void __launch_bounds__(256) compact_count_kernel(const unsigned* __restrict__ bitmap, int64_t nwords,
+                                                            unsigned* __restrict__ bcount) {
+  const int64_t per = (nwords + kCB - 1) / kCB;
+  const int64_t w0 = blockIdx.x * per, w1 = min(nwords, w0 + per);
   unsigned c = 0;
-  for (int64_t w = w0; w < w1; ++w) c += __popc(bitmap[w]);
-  part[tid] = c;
+  for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) c += __popc(bitmap[w]);
+  __shared__ unsigned red[256];
+  red[threadIdx.x] = c;
   __syncthreads();
-  // inclusive scan (Hillis-Steele)
-  for (int o = 1; o < 1024; o <<= 1) {
-    const unsigned v = tid >= o ? part[tid - o] : 0u;
-    __syncthreads();
-    part[tid] += v;
+  for (int o = 128; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  unsigned pos = part[tid] - c;
-  for (int64_t w = w0; w < w1; ++w) {
+  if (threadIdx.x == 0) bcount[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(256) compact_write_kernel(const unsigned* __restrict__ bitmap, int64_t nwords,
+                                                            const unsigned* __restrict__ bcount, long long* uidx,
+                                                            unsigned* ucount) {
+  __shared__ unsigned part[256];
+  __shared__ unsigned base;
+  if (threadIdx.x == 0) {
+    unsigned b = 0;
+    for (int q = 0; q < static_cast<int>(blockIdx.x); ++q) b += bcount[q];
+    base = b;
+    if (blockIdx.x == kCB - 1) *ucount = b + bcount[kCB - 1];
+  }
+  const int64_t per = (nwords + kCB - 1) / kCB;
+  const int64_t w0 = blockIdx.x * per, w1 = min(nwords, w0 + per);
+  const int64_t tper = (w1 - w0 + 255) / 256;  // contiguous words per thread
+  const int64_t t0 = min(w1, w0 + threadIdx.x * tper), t1 = min(w1, t0 + tper);
+  unsigned c = 0;
+  for (int64_t w = t0; w < t1; ++w) c += __popc(bitmap[w]);
+  part[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {  // inclusive scan (Hillis-Steele)
+    const unsigned v = static_cast<int>(threadIdx.x) >= o ? part[threadIdx.x - o] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned pos = base + part[threadIdx.x] - c;
+  for (int64_t w = t0; w < t1; ++w) {
     unsigned bits = bitmap[w];
     while (bits) {
       const int b = __ffs(bits) - 1;
@@ -418,7 +515,6 @@ __global__ void __launch_bounds__(1024) compact_kernel(const unsigned* __restric
       bits &= bits - 1;
     }
   }
-  if (tid == 1023) *ucount = part[1023];
 }
 
 __global__ void iota_kernel(long long* idx, unsigned* count, int64_t n) {
@@ -600,7 +696,9 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   // K5
   if (last) {
     count_launch();
-    compact_kernel<<<1, 1024, 0, st>>>(b.bitmap, (n + 31) / 32, b.uidx, b.ucount);
+    compact_count_kernel<<<kCB, 256, 0, st>>>(b.bitmap, (n + 31) / 32, b.ucount + 1);
+    count_launch();
+    compact_write_kernel<<<kCB, 256, 0, st>>>(b.bitmap, (n + 31) / 32, b.ucount + 1, b.uidx, b.ucount);
   }
   return cudaGetLastError();
 }
@@ -659,7 +757,9 @@ cudaError_t launch_merge_union(const double* cval, const long long* cidx, int G,
   count_launch();
   merge_rank_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(cval, cidx, G, L, n_dirs, m, bitmap);
   count_launch();
-  compact_kernel<<<1, 1024, 0, st>>>(bitmap, (n_total + 31) / 32, uidx, ucount);
+  compact_count_kernel<<<kCB, 256, 0, st>>>(bitmap, (n_total + 31) / 32, ucount + 1);
+  count_launch();
+  compact_write_kernel<<<kCB, 256, 0, st>>>(bitmap, (n_total + 31) / 32, ucount + 1, uidx, ucount);
   return cudaGetLastError();
 }
 

@@ -55,7 +55,7 @@ static void carve_select(Carver& c, SelectBufs& b, int64_t n, int L, int64_t m) 
   b.bitmap = c.take<unsigned>((n + 31) / 32);
   const int64_t capU = n < 2 * m * L ? n : 2 * m * L;
   b.uidx = c.take<long long>(capU > n ? n : (2 * m >= n ? n : capU));
-  b.ucount = c.take<unsigned>(1);
+  b.ucount = c.take<unsigned>(1 + kCompactBlocks);  // count, then compaction scratch
   b.overflow = c.take<int>(1);
 }
 

@@ -82,6 +82,7 @@ cudaError_t launch_dirs_to_f32(const double* U64, float* U32, int rows, int D, c
 
 // ---------------------------------------------------------------- K3/K4/K5 (one point set)
 constexpr int kRadixBins = 2048;
+constexpr int kCompactBlocks = 128;  // K5 compaction CTAs
 struct SelectBufs {
   float* P32;             // [L][n] fp32 projections, direction-major
   unsigned* maxnorm2;     // float bits of max ||x||^2 (atomicMax)
@@ -93,7 +94,7 @@ struct SelectBufs {
   int* lists;             // [L][2][m]
   unsigned* bitmap;       // [ceil(n/32)]
   long long* uidx;        // sorted unique union (capacity min(n, 2mL))
-  unsigned* ucount;       // union size
+  unsigned* ucount;       // union size, then kCompactBlocks words of compaction scratch
   int* overflow;          // guard-band overflow flag
   int64_t cap;            // candidates per list
 };
@@ -121,7 +122,8 @@ cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offse
 // Merge G ranks' lists [G][L][2][m] into the global top/bottom-m per list (same total
 // order) and the sorted unique union of their global indices (bitmap over n_total rows).
 cudaError_t launch_merge_union(const double* cval, const long long* cidx, int G, int L, int64_t m, int64_t n_total,
-                               unsigned* bitmap, long long* uidx, unsigned* ucount, const int* n_dirs,
+                               unsigned* bitmap, long long* uidx, unsigned* ucount /* 1 + kCompactBlocks */,
+                               const int* n_dirs,
                                cudaStream_t st);
 // rows_out[i] = X_local[idx[lo + i] - row_offset] for i < cnt
 cudaError_t launch_gather_offset(const float* X, int D, const long long* idx, int64_t lo, int64_t cnt,

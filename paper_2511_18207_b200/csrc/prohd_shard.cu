@@ -72,7 +72,7 @@ static size_t carve_shard(Carver& c, ShardWs& w, int64_t nA, int64_t nB, int64_t
   b.ccount = c.take<unsigned>(static_cast<int64_t>(L) * 2);
   b.overflow = c.take<int>(1);
   w.bitmap = c.take<unsigned>((n_total + 31) / 32 + 1);
-  w.ucount = c.take<unsigned>(1);
+  w.ucount = c.take<unsigned>(1 + kCompactBlocks);  // count, then compaction scratch
   return c.off;
 }
 
