@@ -39,6 +39,7 @@ constexpr int kT = 256;      // threads per CTA
 constexpr int kWarps = kT / 32;
 constexpr int kMaxD = 256;
 constexpr int kRows = kMaxD / kCl;  // rows per CTA (max)
+constexpr int kLuStride = 6 * kMaxD + kMaxD / 8;  // doubles of inverse-iteration scratch per warp
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -46,14 +47,27 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// number of eigenvalues of T (d, e2 = e^2) strictly less than x (Sturm count)
+// 1/q for |q| >= DBL_MIN (normal): hardware approximation + 2 Newton steps (<= 1 ulp), a
+// quarter of the latency of the IEEE division sequence on the serial chains below
+__device__ __forceinline__ double rcp_normal(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rcp_safe(double q) { return fabs(q) >= 0x1p-1000 ? rcp_normal(q) : 1.0 / q; }
+
+// number of eigenvalues of T (d, e2 = e^2) strictly less than x (Sturm count); |q| >= pivmin
+// (> DBL_MIN) at every division, so the reciprocal is taken on normal numbers
 __device__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
   int cnt = 0;
   double q = d[0] - x;
   if (fabs(q) < pivmin) q = -pivmin;
   if (q < 0) ++cnt;
   for (int i = 1; i < n; ++i) {
-    q = d[i] - x - e2[i - 1] / q;
+    q = d[i] - x - e2[i - 1] * rcp_normal(q);
     if (fabs(q) < pivmin) q = -pivmin;
     if (q < 0) ++cnt;
   }
@@ -74,10 +88,12 @@ struct EigArgs {
   double* de;     // [2][kMaxD]: diagonal d, then off-diagonal e of T (global hand-off)
 };
 
-// inverse iteration for eigenvalue `lam` of T (one warp; lane 0 runs the serial solve)
+// inverse iteration for eigenvalue `lam` of T (one warp; lane 0 runs the serial solve on the
+// warp's shared-memory vector x; the result is copied to xout)
 __device__ void inverse_iteration(const double* d, const double* e, int D, double lam, double tnorm, double pivmin,
-                                  double* x, double* u0, double* u1, double* u2, const double* X, const int* prev,
-                                  int nprev, int w, int lane) {
+                                  double* xout, double* x, double* u0, double* u1, double* u2, double* mlt,
+                                  double* inv0, unsigned char* piv, const double* X, const int* prev, int nprev,
+                                  int w, int lane) {
   for (int i = lane; i < D; i += 32) {
     unsigned h = static_cast<unsigned>(i) * 2654435761u ^ (static_cast<unsigned>(w) * 40503u + 17u);
     h ^= h >> 13;
@@ -89,38 +105,66 @@ __device__ void inverse_iteration(const double* d, const double* e, int D, doubl
   const double eps_p = DBL_EPSILON * tnorm + pivmin;
   for (int iter = 0; iter < 3; ++iter) {
     if (lane == 0) {
-      // (T - lam I) y = x, Gaussian elimination with partial pivoting (tridiagonal, fill u2)
-      double dd = d[0] - lam, ee = (D > 1) ? e[0] : 0.0;
+      // (T - lam I) y = x by Gaussian elimination with partial pivoting (tridiagonal, fill u2);
+      // the factorisation (multipliers, row swaps, reciprocal pivots) is formed in the first
+      // iteration and reused by the next two, which only run the substitutions
+      if (iter == 0) {
+        double dd = d[0] - lam, ee = (D > 1) ? e[0] : 0.0;
+        for (int i = 0; i < D - 1; ++i) {
+          const double sub = e[i];
+          const double dn = d[i + 1] - lam;
+          const double en = (i + 2 < D) ? e[i + 1] : 0.0;
+          if (fabs(dd) >= fabs(sub)) {
+            if (dd == 0.0) dd = eps_p;
+            const double rd = rcp_safe(dd);
+            const double m = sub * rd;
+            u0[i] = dd;
+            inv0[i] = rd;
+            u1[i] = ee;
+            u2[i] = 0.0;
+            mlt[i] = m;
+            piv[i] = 0;
+            dd = dn - m * ee;
+            ee = en;
+          } else {
+            const double m = dd * rcp_safe(sub);
+            u0[i] = sub;
+            inv0[i] = rcp_safe(sub);
+            u1[i] = dn;
+            u2[i] = en;
+            mlt[i] = m;
+            piv[i] = 1;
+            dd = ee - m * dn;
+            ee = -m * en;
+          }
+        }
+        if (dd == 0.0) dd = eps_p;
+        u0[D - 1] = dd;
+        inv0[D - 1] = rcp_safe(dd);
+      }
+      // forward: the row operations of the elimination on the right-hand side
+      double xn = x[0];
       for (int i = 0; i < D - 1; ++i) {
-        const double sub = e[i];
-        const double dn = d[i + 1] - lam;
-        const double en = (i + 2 < D) ? e[i + 1] : 0.0;
-        if (fabs(dd) >= fabs(sub)) {
-          if (dd == 0.0) dd = eps_p;
-          const double mlt = sub / dd;
-          u0[i] = dd;
-          u1[i] = ee;
-          u2[i] = 0.0;
-          x[i + 1] -= mlt * x[i];
-          dd = dn - mlt * ee;
-          ee = en;
+        const double xi1 = x[i + 1];
+        if (piv[i] == 0) {
+          x[i] = xn;
+          xn = xi1 - mlt[i] * xn;
         } else {
-          const double mlt = dd / sub;
-          u0[i] = sub;
-          u1[i] = dn;
-          u2[i] = en;
-          const double t = x[i];
-          x[i] = x[i + 1];
-          x[i + 1] = t - mlt * x[i + 1];
-          dd = ee - mlt * dn;
-          ee = -mlt * en;
+          x[i] = xi1;
+          xn = xn - mlt[i] * xi1;
         }
       }
-      if (dd == 0.0) dd = eps_p;
-      u0[D - 1] = dd;
-      x[D - 1] /= u0[D - 1];
-      if (D >= 2) x[D - 2] = (x[D - 2] - u1[D - 2] * x[D - 1]) / u0[D - 2];
-      for (int i = D - 3; i >= 0; --i) x[i] = (x[i] - u1[i] * x[i + 1] - u2[i] * x[i + 2]) / u0[i];
+      x[D - 1] = xn;
+      // back substitution with the reciprocal pivots
+      x[D - 1] *= inv0[D - 1];
+      if (D >= 2) x[D - 2] = (x[D - 2] - u1[D - 2] * x[D - 1]) * inv0[D - 2];
+      double x1 = D >= 2 ? x[D - 2] : 0.0, x2 = x[D - 1];  // x[i + 1], x[i + 2] in registers
+      for (int i = D - 3; i >= 0; --i) {
+        const double xi = (x[i] - u1[i] * x1 - u2[i] * x2) * inv0[i];
+        x[i] = xi;
+        x2 = x1;
+        x1 = xi;
+      }
     }
     __syncwarp();
     // modified Gram-Schmidt against the earlier vectors of the same cluster, then normalise
@@ -139,6 +183,8 @@ __device__ void inverse_iteration(const double* d, const double* e, int D, doubl
     for (int i = lane; i < D; i += 32) x[i] *= inv;
     __syncwarp();
   }
+  for (int i = lane; i < D; i += 32) xout[i] = x[i];
+  __syncwarp();
 }
 
 // Householder tridiagonalisation T = Q^T C Q on one 8-CTA cluster (Golub & Van Loan
@@ -255,7 +301,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
   cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
   extern __shared__ double dyn[];
-  double* lu = dyn;  // [kWarps][3][kMaxD] LU scratch
+  double* lu = dyn;  // per warp: u0, u1, u2, x, multipliers, 1/u0 (kMaxD doubles each), swap flags
   __shared__ double d[kMaxD], e[kMaxD], e2[kMaxD], lamv[kMaxD];
   __shared__ int s_prev[kWarps][16];
   const int D = a.D;
@@ -278,23 +324,40 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
   const double tnorm = fmax(fabs(gl), fabs(gu));
   const double pivmin = fmax(DBL_MIN, 1e-300 * tnorm) + DBL_MIN;
   const int kk = a.k < D ? a.k : D;
-  // one warp per eigenvalue across the whole cluster (warp slot rank * kWarps + warp)
-  for (int w = rank * kWarps + warp; w < kk; w += kCl * kWarps) {
-    const int target = D - 1 - w;  // the eigenvalue with exactly `target` eigenvalues below it
+  // G warps per eigenvalue (32 G probes per multisection step; G = 4 for k <= 16 spreads the
+  // 8 x 8 warps of the cluster over the eigenvalues), the G warps of a group in one CTA
+  const int G = kk <= (kCl * kWarps) / 4 ? 4 : kk <= (kCl * kWarps) / 2 ? 2 : 1;
+  const int gpc = kWarps / G;                 // groups per CTA
+  const int grp = warp / G, gj = warp % G;    // group in this CTA, warp within the group
+  const int P = 32 * G;                       // probes per step
+  __shared__ int gnb[2][kWarps];              // per-step probe counts, double-buffered
+  for (int base = 0; base < kk; base += kCl * gpc) {
+    // every group runs the same number of outer iterations (named barriers inside)
+    const int w = base + rank * gpc + grp;
+    const bool live = w < kk;
+    const int target = D - 1 - (live ? w : 0);  // the eigenvalue with exactly `target` eigenvalues below it
     double lo = gl - 1e-12 * tnorm - pivmin, hi = gu + 1e-12 * tnorm + pivmin;
     for (int it = 0; it < 64; ++it) {
       const double width = hi - lo;
-      if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
-      const double x = lo + width * (lane + 1) / 33.0;
+      if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;  // uniform per group
+      const double x = lo + width * (gj * 32 + lane + 1) / static_cast<double>(P + 1);
       const int cnt = sturm_count(d, e2, D, x, pivmin);
       const unsigned below = __ballot_sync(0xffffffffu, cnt <= target);
-      const int nb = __popc(below);  // monotone: probes 0..nb-1 are at or below the eigenvalue
-      const double nlo = (nb == 0) ? lo : lo + width * nb / 33.0;
-      const double nhi = (nb == 32) ? hi : lo + width * (nb + 1) / 33.0;
+      if (G > 1) {
+        if (lane == 0) gnb[it & 1][warp] = __popc(below);
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * G) : "memory");
+      }
+      int nb = __popc(below);  // monotone: probes 0..nb-1 are at or below the eigenvalue
+      if (G > 1) {
+        nb = 0;
+        for (int q = 0; q < G; ++q) nb += gnb[it & 1][grp * G + q];
+      }
+      const double nlo = (nb == 0) ? lo : lo + width * nb / static_cast<double>(P + 1);
+      const double nhi = (nb == P) ? hi : lo + width * (nb + 1) / static_cast<double>(P + 1);
       lo = nlo;
       hi = nhi;
     }
-    if (lane < kCl) *cl.map_shared_rank(&lamv[w], lane) = 0.5 * (lo + hi);
+    if (live && gj == 0 && lane < kCl) *cl.map_shared_rank(&lamv[w], lane) = 0.5 * (lo + hi);
   }
   cl.sync();
   if (a.stop == 2) return;
@@ -314,11 +377,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
       while (end < kk && fabs(lamv[end - 1] - lamv[end]) <= clus) ++end;
       const int slot = c % (kCl * kWarps);
       if (slot / kWarps == rank && slot % kWarps == warp) {
-        double* u0 = lu + warp * 3 * kMaxD;
+        double* u0 = lu + warp * kLuStride;
         int nprev = 0;
         for (int w = start; w < end; ++w) {
-          inverse_iteration(d, e, D, lamv[w], tnorm, pivmin, a.X + static_cast<int64_t>(w) * D, u0, u0 + kMaxD,
-                            u0 + 2 * kMaxD, a.X, s_prev[warp], nprev, w, lane);
+          inverse_iteration(d, e, D, lamv[w], tnorm, pivmin, a.X + static_cast<int64_t>(w) * D, u0 + 3 * kMaxD, u0,
+                            u0 + kMaxD, u0 + 2 * kMaxD, u0 + 4 * kMaxD, u0 + 5 * kMaxD,
+                            reinterpret_cast<unsigned char*>(u0 + 6 * kMaxD), a.X, s_prev[warp], nprev, w, lane);
           if (lane == 0 && nprev < 16) s_prev[warp][nprev] = w;
           __syncwarp();
           if (nprev < 16) ++nprev;
@@ -422,7 +486,7 @@ cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, dou
     return e;
   count_launch();
   eigen_reduce_cluster_kernel<<<kCl, kT, smem, st>>>(a);
-  const size_t smem3 = sizeof(double) * static_cast<size_t>(kWarps) * 3 * kMaxD;
+  const size_t smem3 = sizeof(double) * static_cast<size_t>(kWarps) * kLuStride;
   if ((e = cudaFuncSetAttribute(eigen_vectors_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem3))) != cudaSuccess)
     return e;
