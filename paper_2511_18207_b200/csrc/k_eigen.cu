@@ -203,6 +203,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
   extern __shared__ double dyn[];
   double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/8)*D])
   __shared__ double colbuf2[2][kMaxD], pbuf[kMaxD];  // colbuf double-buffered: step j uses [j & 1]
+  __shared__ double vbuf[kMaxD], wbuf[kMaxD];        // v and w = p - K v of the current step
   __shared__ double vpart[kCl * kWarps];
   __shared__ double s_d;
   const int D = a.D;
@@ -248,38 +249,55 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
       cl.sync();      // everyone is done reading colbuf before step j+1 scatters into it
       continue;
     }
-    // p_r = 2 M[r][j+1:] . v for own rows r > j (warp per row); v.p partial per warp
-    double vp = 0.0;
-    for (int i = warp; i < nloc; i += kWarps) {
+    // v once per CTA in shared memory (every warp formed the same scalars)
+    for (int c = j + 1 + tid; c < D; c += kT) vbuf[c] = vc(c);
+    __syncthreads();
+    // p_r = 2 M[r][j+1:] . v for own rows r > j (warp per row, <= 4 rows per warp, the row
+    // dot products formed together and reduced together); v.p partial per warp
+    constexpr int kRW = kRows / kWarps;  // rows per warp (4)
+    double ps[kRW];
+#pragma unroll
+    for (int q = 0; q < kRW; ++q) {
+      const int i = warp + kWarps * q;
       const int r = rank + kCl * i;
-      if (r <= j) continue;
-      const double* row = M + i * D;
-      double s0 = 0.0, s1 = 0.0;
-      int c = j + 1 + lane;
-      for (; c + 32 < D; c += 64) {
-        s0 = fma(row[c], vc(c), s0);
-        s1 = fma(row[c + 32], vc(c + 32), s1);
+      double s0 = 0.0;
+      if (i < nloc && r > j) {
+        const double* row = M + i * D;
+        for (int c = j + 1 + lane; c < D; c += 32) s0 = fma(row[c], vbuf[c], s0);
       }
-      if (c < D) s0 = fma(row[c], vc(c), s0);
-      const double pr = 2.0 * warp_sum(s0 + s1);
-      if (lane < kCl) *cl.map_shared_rank(&pbuf[r], lane) = pr;
-      vp += pr * vc(r);
+      ps[q] = s0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < kRW; ++q) ps[q] += __shfl_xor_sync(0xffffffffu, ps[q], o);
+    double vp = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRW; ++q) {
+      const int i = warp + kWarps * q;
+      const int r = rank + kCl * i;
+      if (i < nloc && r > j) {
+        const double pr = 2.0 * ps[q];
+        if (lane < kCl) *cl.map_shared_rank(&pbuf[r], lane) = pr;
+        vp += pr * vbuf[r];
+      }
     }
     if (lane < kCl) *cl.map_shared_rank(&vpart[rank * kWarps + warp], lane) = vp;
     cl.sync();
-    // C. K = v.p; M[r][c] -= v_r w_c + w_r v_c with w = p - K v, on own rows
+    // C. K = v.p; w = p - K v once per CTA; M[r][c] -= v_r w_c + w_r v_c on own rows
     double K = 0.0;
     for (int q = lane; q < kCl * kWarps; q += 32) K += vpart[q];
     K = warp_sum(K);
-    for (int i = warp; i < nloc; i += kWarps) {
+    for (int c = j + 1 + tid; c < D; c += kT) wbuf[c] = pbuf[c] - K * vbuf[c];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kRW; ++q) {
+      const int i = warp + kWarps * q;
       const int r = rank + kCl * i;
-      if (r <= j) continue;
+      if (i >= nloc || r <= j) continue;
       double* row = M + i * D;
-      const double vr = vc(r), wr = pbuf[r] - K * vr;
-      for (int c = j + 1 + lane; c < D; c += 32) {
-        const double v = vc(c);
-        row[c] -= vr * (pbuf[c] - K * v) + wr * v;
-      }
+      const double vr = vbuf[r], wr = wbuf[r];
+      for (int c = j + 1 + lane; c < D; c += 32) row[c] -= fma(vr, wbuf[c], wr * vbuf[c]);
     }
     __syncthreads();
   }
