@@ -86,3 +86,24 @@ def test_gram_shifted(ctx):
     B = (rng.standard_normal((15000, D)) + 4096.5).astype(np.float32)
     s = np.concatenate([A[:4096], B[:4096]]).astype(np.float64).mean(0)
     _check(ctx, A, B, s)
+
+
+@pytest.mark.parametrize("nA,nB,D", [(3001, 2999, 300), (2000, 1500, 513), (1200, 1100, 1000), (777, 5000, 33),
+                                     (5000, 1, 260)])
+def test_gram_wide_and_ragged(ctx, nA, nB, D):
+    """D > 256 (groups over 4x4 squares of 32-feature blocks, the column-sum pass looping over
+    piece blocks) and D % 4 != 0 (4-byte copies, scalar column sums), against the fp64 sums."""
+    rng = np.random.default_rng(D)
+    A = (rng.standard_normal((nA, D)) * rng.uniform(0.1, 3, D)).astype(np.float32)
+    B = (rng.standard_t(4, (nB, D)) + 0.25).astype(np.float32)
+    _check(ctx, A, B, np.zeros(D))
+
+
+def test_gram_replicated_ksteps(ctx):
+    """Small D: each 32x32 tile runs on 4 (D <= 32) or 2 warps taking alternate k-steps, and
+    the replicas' partials are summed by the reduce kernel."""
+    rng = np.random.default_rng(17)
+    for D, n in [(8, 40001), (32, 30000), (64, 20011), (96, 10000)]:
+        A = rng.standard_normal((n, D)).astype(np.float32)
+        B = (rng.standard_normal((n // 2 + 3, D)) * 2 - 1).astype(np.float32)
+        _check(ctx, A, B, np.zeros(D))
