@@ -98,8 +98,9 @@ struct Carver {
 // Operands of one point set for the distance kernel.
 struct SetOps {
   const float* x = nullptr;  // device copy of the fp32 input (D stride)
-  float* hi = nullptr;
-  float* lo = nullptr;
+  float* hi = nullptr;      // TF32-truncated fp32 (K0)
+  uint32_t* pr = nullptr;  // bf16 pairs (hi, lo): row-operand role
+  uint32_t* pc = nullptr;  // bf16 pairs (lo, hi): column-operand role
   float* norms = nullptr;  // padded to kBN with +inf
   int64_t n = 0;
 };
@@ -123,7 +124,8 @@ inline void carve_set(Carver& c, SetOps& s, int64_t n, int D) {
   const int Dp = pad_dim(D);
   s.n = n;
   s.hi = c.take<float>(n * Dp);
-  s.lo = c.take<float>(n * Dp);
+  s.pr = c.take<uint32_t>(n * Dp);
+  s.pc = c.take<uint32_t>(n * Dp);
   s.norms = c.take<float>(round_up(n, kBN));
 }
 
@@ -262,7 +264,7 @@ inline int prep_set(prohd_ctx* ctx, const float* X, int64_t n, int D, SetOps& s,
                     const double* centre) {
   s.x = X;
   const int t0 = tmark(ctx);
-  CK(launch_prep(X, n, D, pad_dim(D), round_up(n, kBN), centre, s.hi, s.lo, s.norms, bad, ctx->stream));
+  CK(launch_prep(X, n, D, pad_dim(D), round_up(n, kBN), centre, s.hi, s.pr, s.pc, s.norms, bad, ctx->stream));
   tspan(ctx, PH_PREP, t0);
   return PROHD_OK;
 }
@@ -274,9 +276,10 @@ inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, flo
   char err[256];
   const int Dp = pad_dim(D);
   if (!make_tmap_2d(&maps[0], R.hi, R.n, Dp, kBM, err, sizeof err) ||
-      !make_tmap_2d(&maps[1], R.lo, R.n, Dp, kBM, err, sizeof err) ||
+      !make_tmap_2d(&maps[1], reinterpret_cast<const float*>(R.pr), R.n, Dp, kBM, err, sizeof err) ||
       !make_tmap_2d(&maps[2], C.hi, C.n, Dp, dist_b_box_rows(D, colmin != nullptr), err, sizeof err) ||
-      !make_tmap_2d(&maps[3], C.lo, C.n, Dp, dist_b_box_rows(D, colmin != nullptr), err, sizeof err))
+      !make_tmap_2d(&maps[3], reinterpret_cast<const float*>(C.pc), C.n, Dp, dist_b_box_rows(D, colmin != nullptr),
+                    err, sizeof err))
     return fail(ctx, PROHD_E_CUDA, "%s", err);
   DistArgs a;
   a.maps = maps;

@@ -21,19 +21,14 @@ constexpr int kBK = 32;   // fp32 K elements per pipeline chunk (one 128-B swizz
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int pad_dim(int D) { return static_cast<int>(round_up(D, 4)); }  // 16-B TMA row stride
 
-// K0: split points, translated by a common centre c (fp64, D; nullptr = none), into TF32
-// hi/lo operands + fp32 norms: y = x - c in fp64, hi = fp32(y) with the low 13 mantissa
-// bits cleared (exact TF32), lo = fp32(y - hi), ||y||^2 accumulated in fp64. Distances
-// are translation invariant, and centring keeps ||a||^2 + ||b||^2 - 2 a.b from cancelling
-// when the data sit far from the origin. hi/lo rows have stride Dp (zero padded);
-// norms[i] = ||y_i||^2 for i < n and +inf for n <= i < n_pad. *bad = 1 if any x or norm
-// is not finite.
+// K0: split points, translated by a common centre c (fp64, D; nullptr = none), into the K6
+// operands: y = x - c in fp64, hi = fp32(y) with the low 13 mantissa bits cleared (exact
+// TF32), lo = fp32(y - hi), pr[f] = bf16 pair (hi_f, lo_f) and pc[f] = (lo_f, hi_f) (element
+// 2f at the lower address), and ||y||^2 accumulated in fp64. hi/pr/pc rows have stride Dp
+// (zero padded); norms[i] = ||y_i||^2 for i < n and +inf for n <= i < n_pad. *bad = 1 if any
+// x or norm is not finite.
 cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, const double* centre, float* hi,
-                        float* lo, float* norms, int* bad, cudaStream_t st);
-// Same, for a gathered subset: rows X[idx[i]] for i < n (subset operands).
-cudaError_t launch_prep_gather(const float* X, const int64_t* idx, int64_t n, int D, int Dp, int64_t n_pad,
-                               const double* centre, float* hi, float* lo, float* norms, int* bad,
-                               cudaStream_t st);
+                        uint32_t* pr, uint32_t* pc, float* norms, int* bad, cudaStream_t st);
 // Common centre of a pair (X, Y): fp64 mean of the first min(nX, 4096) rows of X and the
 // first min(nY, 4096) rows of Y (either count may be 0), summed per set and then added,
 // so centre(X, Y) == centre(Y, X) bit for bit. c: 2D doubles (the second half is scratch).
@@ -41,7 +36,7 @@ cudaError_t launch_centre(const float* X, int64_t nX, const float* Y, int64_t nY
                           cudaStream_t st);
 
 struct DistArgs {
-  const CUtensorMap* maps;  // [A_hi, A_lo, B_hi, B_lo]
+  const CUtensorMap* maps;  // [A_hi, A_pr, B_hi, B_pc]
   int64_t nA, nB;
   int D;
   const float* na;  // row-operand norms

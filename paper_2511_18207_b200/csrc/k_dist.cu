@@ -6,18 +6,27 @@
 // which is min_j ||a_i - b_j||^2 (Eq. (1), inner min). The
 // n_A x n_B distance matrix never leaves TMEM/registers.
 //
-// 3xTF32 (SURVEY.md §8(a) "shared fused distance kernel"): with x = hi + lo,
-//   a.b ~= hi_a.hi_b + hi_a.lo_b + lo_a.hi_b
-// (lo.lo ~ 2^-22 |a||b| dropped); all three products accumulate into one fp32
-// TMEM accumulator.
+// Split products (SURVEY.md §8(a) "shared fused distance kernel"): with x = hi + lo,
+// hi the TF32-truncated value and lo = x - hi (|lo| < 2^-10 |x|),
+//   a.b ~= hi_a.hi_b                      one kind::tf32 MMA per 8 features
+//        + [hi_a lo_a].[lo_b hi_b]        one kind::f16 MMA (bf16) per 8 features,
+// the second over interleaved bf16 pairs (K doubled) so that a single instruction forms both
+// correction terms hi_a.lo_b + lo_a.hi_b. Both accumulate into one fp32 TMEM accumulator.
+// Error per product: lo.lo dropped (< 2^-20 |a_i||b_i|) and the bf16 rounding of hi and lo in
+// the correction terms (< 2 x 2^-9 x 2^-10 each), so |a.b - dot| <= 2^-17 sum |a_i||b_i| <=
+// 2^-17 ||a|| ||b|| and |d2 - d2_exact| <= 2^-17 (||a||^2 + ||b||^2) = 7.6e-6 of the norms, inside
+// the 1e-5 budget of BASELINE.json (Q17) with the centring of K0 shrinking the norms further.
+// Against 3xTF32 (three TF32 MMAs) the tensor time per pair drops from 6D/P_tf32 to
+// 2D/P_tf32 + 4D/P_bf16 (P_bf16 ~ 2 P_tf32): ~1.5x.
 //
 // Structure (persistent, 1 CTA per SM, warp-specialised, 192 threads):
 //   warp 0      TMA producer: per K-chunk (32 fp32 = one 128-B swizzle row) it
-//               loads A_hi/A_lo [128 x 32] and B_hi/B_lo [256 x 32] into a
-//               2-stage ring (96 KB per stage) with SWIZZLE_128B.
+//               loads A_hi/A_pr [128 x 32] and B_hi/B_pc [256 x 32] (pr/pc: 32 bf16
+//               pairs = 128 B per row) into a 2-stage ring (96 KB per stage), SWIZZLE_128B.
 //   warp 1      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
 //               and single-thread MMA issuer: tcgen05.mma.cta_group::1.kind::tf32
-//               M=128, N=256, K=8, 3 MMAs per K-step, commit -> smem slot free,
+//               M=128, N=256: per 8 features one TF32 MMA (K=8) and one bf16 MMA
+//               (K=16 over the pairs), commit -> smem slot free,
 //               commit -> accumulator full.
 //   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 (one TMEM lane = one row per
 //               thread), v = fma(-2, acc, ||b||^2), running min in a register
@@ -146,6 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
+      constexpr uint32_t idesc16 = idesc_bf16(kBM, kBN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -172,9 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t dal = smem_desc_k_sw128(al + off);
               const uint64_t dbh = smem_desc_k_sw128(bh + off);
               const uint64_t dbl = smem_desc_k_sw128(bl + off);
-              mma_tf32(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);
-              mma_tf32(d, dah, dbl, idesc, 1u);
-              mma_tf32(d, dal, dbh, idesc, 1u);
+              mma_tf32(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
+              mma_bf16(d, dal, dbl, idesc16, 1u);                   // [hi lo]_a . [lo hi]_b
             }
             mma_commit(&empty[stage]);
             if (++stage == kStages) {
@@ -365,6 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       constexpr uint32_t idesc = idesc_tf32(256, kBN);
+      constexpr uint32_t idesc16 = idesc_bf16(256, kBN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -391,9 +401,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const uint64_t dal = smem_desc_k_sw128(al + off);
               const uint64_t dbh = smem_desc_k_sw128(bh + off);
               const uint64_t dbl = smem_desc_k_sw128(bl + off);
-              mma_tf32_2sm(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);
-              mma_tf32_2sm(d, dah, dbl, idesc, 1u);
-              mma_tf32_2sm(d, dal, dbh, idesc, 1u);
+              mma_tf32_2sm(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
+              mma_bf16_2sm(d, dal, dbl, idesc16, 1u);                   // [hi lo]_a . [lo hi]_b
             }
             mma_commit_2sm_mc(&empty[stage], 0x3);
             if (++stage == kStages2) {

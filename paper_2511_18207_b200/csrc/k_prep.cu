@@ -4,7 +4,11 @@
 // common centre), hi = trunc_tf32(fp32(y)) (low 13 mantissa bits cleared, so the
 // tensor core reads hi exactly whatever its fp32->tf32 conversion mode),
 // lo = fp32(y - hi), and ||y||^2 accumulated in fp64 then rounded to fp32 (without
-// a centre: y = x and lo = x - hi exactly). One warp per row; HBM-bound.
+// a centre: y = x and lo = x - hi exactly). K6 takes a.b = hi_a.hi_b (TF32 MMA) +
+// [hi_a lo_a].[lo_b hi_b] (one bf16 MMA over interleaved pairs), so K0 writes hi (fp32) and
+// the bf16 pairs in both orders: pr[f] = (bf16(hi_f), bf16(lo_f)) for the row role and
+// pc[f] = (bf16(lo_f), bf16(hi_f)) for the column role (element 2f at the lower address).
+// One warp per row; HBM-bound.
 //
 // K7: the directed maximum over row minima packed as
 //   key = (float_bits(d2) << 32) | (0xFFFFFFFF - row)
@@ -13,6 +17,8 @@
 // direct form sum_k (a_k - b_k)^2 over all of B (lowest index on exact ties),
 // matching the oracle's definition (Eq. (1)).
 #include "internal.cuh"
+
+#include <cuda_bf16.h>
 
 #include <cfloat>
 #include <cmath>
@@ -23,11 +29,18 @@ __device__ __forceinline__ float tf32_trunc(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
+__device__ __forceinline__ uint32_t bf16_pair(float first, float second) {
+  const uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(first));
+  const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(second));
+  return a | (b << 16);
+}
+
 template <bool kGather, bool kCentre>
 __global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, const int64_t* __restrict__ idx,
                                                    int64_t n, int D, int Dp, int64_t n_pad,
                                                    const double* __restrict__ centre, float* __restrict__ hi,
-                                                   float* __restrict__ lo, float* __restrict__ norms, int* bad) {
+                                                   uint32_t* __restrict__ pr, uint32_t* __restrict__ pc,
+                                                   float* __restrict__ norms, int* bad) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -39,20 +52,25 @@ __global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, 
     const int64_t src = kGather ? idx[r] : r;
     const float* x = X + src * static_cast<int64_t>(D);
     float* h = hi + r * static_cast<int64_t>(Dp);
-    float* l = lo + r * static_cast<int64_t>(Dp);
+    uint32_t* qr = pr + r * static_cast<int64_t>(Dp);
+    uint32_t* qc = pc + r * static_cast<int64_t>(Dp);
     double s = 0.0;
     for (int c = lane; c < Dp; c += 32) {
       const float v = c < D ? __ldg(x + c) : 0.0f;
       if (kCentre) {
         const double y = c < D ? static_cast<double>(v) - __ldg(centre + c) : 0.0;
         const float vh = tf32_trunc(static_cast<float>(y));
+        const float vl = static_cast<float>(y - static_cast<double>(vh));
         h[c] = vh;
-        l[c] = static_cast<float>(y - static_cast<double>(vh));
+        qr[c] = bf16_pair(vh, vl);
+        qc[c] = bf16_pair(vl, vh);
         s = fma(y, y, s);
       } else {
         const float vh = tf32_trunc(v);
+        const float vl = v - vh;
         h[c] = vh;
-        l[c] = v - vh;
+        qr[c] = bf16_pair(vh, vl);
+        qc[c] = bf16_pair(vl, vh);
         s = fma(static_cast<double>(v), static_cast<double>(v), s);
       }
     }
@@ -74,27 +92,14 @@ static int grid_for_rows(int64_t rows) {
 }
 
 cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, const double* centre, float* hi,
-                        float* lo, float* norms, int* bad, cudaStream_t st) {
+                        uint32_t* pr, uint32_t* pc, float* norms, int* bad, cudaStream_t st) {
   count_launch();
   if (centre)
-    prep_kernel<false, true><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, centre, hi, lo,
+    prep_kernel<false, true><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, centre, hi, pr, pc,
                                                                     norms, bad);
   else
-    prep_kernel<false, false><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, nullptr, hi, lo,
-                                                                     norms, bad);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_prep_gather(const float* X, const int64_t* idx, int64_t n, int D, int Dp, int64_t n_pad,
-                               const double* centre, float* hi, float* lo, float* norms, int* bad,
-                               cudaStream_t st) {
-  count_launch();
-  if (centre)
-    prep_kernel<true, true><<<grid_for_rows(n_pad), 256, 0, st>>>(X, idx, n, D, Dp, n_pad, centre, hi, lo, norms,
-                                                                   bad);
-  else
-    prep_kernel<true, false><<<grid_for_rows(n_pad), 256, 0, st>>>(X, idx, n, D, Dp, n_pad, nullptr, hi, lo, norms,
-                                                                    bad);
+    prep_kernel<false, false><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, nullptr, hi, pr,
+                                                                     pc, norms, bad);
   return cudaGetLastError();
 }
 
