@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ unsigned colbuf[2][kBN];  // kBidir: per-accumulator column minima (float bits)
+  __shared__ __align__(16) float nbuf[2][kBN];  // column norms of the tile in each accumulator
   __shared__ unsigned tilecnt[2];
 
   const int warp = threadIdx.x >> 5;
@@ -214,10 +215,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       // kBidir: this row's ||a||^2, or +inf for rows past nA (excluded from column minima)
       const float narow = kBidir ? (row < s.nA ? __ldg(na + row) : __int_as_float(0x7f800000)) : 0.0f;
       for (int t = t0; t < t1; ++t) {
-        mbar_wait(&tfull[acc], aphase);
+        // the tile's column norms: loaded before the accumulator wait, staged in shared memory
+        // (one 16-B piece per thread per accumulator buffer), read back as broadcasts
+        {
+          const int e = q * 32 + lane;  // 0..127: two floats each
+          const float2 n2 = __ldg(reinterpret_cast<const float2*>(nb + static_cast<int64_t>(t) * kBN) + e);
+          mbar_wait(&tfull[acc], aphase);
+          reinterpret_cast<float2*>(nbuf[acc])[e] = n2;
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+        }
         tc_fence_after();
         const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(acc * kBN);
-        const float4* nbp = reinterpret_cast<const float4*>(nb + static_cast<int64_t>(t) * kBN);
+        const float4* nbp = reinterpret_cast<const float4*>(nbuf[acc]);
 #pragma unroll 1
         for (int cc = 0; cc < kBN / 32; ++cc) {
           float v[32];
@@ -225,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 n4 = __ldg(nbp + cc * 8 + i);
+            const float4 n4 = nbp[cc * 8 + i];
             v[4 * i + 0] = fmaf(-2.0f, v[4 * i + 0], n4.x);
             v[4 * i + 1] = fmaf(-2.0f, v[4 * i + 1], n4.y);
             v[4 * i + 2] = fmaf(-2.0f, v[4 * i + 2], n4.z);
@@ -307,6 +316,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kStages2;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ __align__(16) float nbuf[2][kBN];  // column norms of the tile in each accumulator
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -430,10 +440,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int t1 = min(s.nt, t0 + s.tps);
       float rmin = __int_as_float(0x7f800000);
       for (int t = t0; t < t1; ++t) {
-        mbar_wait(&tfull[acc], aphase);
+        // the tile's column norms: loaded before the accumulator wait, staged in shared memory
+        // (one 16-B piece per thread per accumulator buffer), read back as broadcasts
+        {
+          const int e = q * 32 + lane;  // 0..127: two floats each
+          const float2 n2 = __ldg(reinterpret_cast<const float2*>(nb + static_cast<int64_t>(t) * kBN) + e);
+          mbar_wait(&tfull[acc], aphase);
+          reinterpret_cast<float2*>(nbuf[acc])[e] = n2;
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+        }
         tc_fence_after();
         const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(acc * kBN);
-        const float4* nbp = reinterpret_cast<const float4*>(nb + static_cast<int64_t>(t) * kBN);
+        const float4* nbp = reinterpret_cast<const float4*>(nbuf[acc]);
 #pragma unroll 1
         for (int cc = 0; cc < kBN / 32; ++cc) {
           float v[32];
@@ -441,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 n4 = __ldg(nbp + cc * 8 + i);
+            const float4 n4 = nbp[cc * 8 + i];
             rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 0], n4.x));
             rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 1], n4.y));
             rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 2], n4.z));
