@@ -227,11 +227,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(acc * kBN);
         const float4* nbp = reinterpret_cast<const float4*>(nbuf[acc]);
-#pragma unroll 1
-        for (int cc = 0; cc < kBN / 32; ++cc) {
-          float v[32];
-          tmem_ld32(taddr + cc * 32, v);
-          tmem_wait_ld();
+        // two 32-column chunks per TMEM wait; the 32 values of a chunk reduce as a tree
+        auto chunk = [&](float (&v)[32], int cc) {
+          float m[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float4 n4 = nbp[cc * 8 + i];
@@ -239,14 +237,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[4 * i + 1] = fmaf(-2.0f, v[4 * i + 1], n4.y);
             v[4 * i + 2] = fmaf(-2.0f, v[4 * i + 2], n4.z);
             v[4 * i + 3] = fmaf(-2.0f, v[4 * i + 3], n4.w);
-            rmin = fminf(rmin, fminf(fminf(v[4 * i + 0], v[4 * i + 1]), fminf(v[4 * i + 2], v[4 * i + 3])));
+            m[i] = fminf(fminf(v[4 * i + 0], v[4 * i + 1]), fminf(v[4 * i + 2], v[4 * i + 3]));
           }
+          rmin = fminf(rmin, fminf(fminf(fminf(m[0], m[1]), fminf(m[2], m[3])),
+                                   fminf(fminf(m[4], m[5]), fminf(m[6], m[7]))));
           if (kBidir) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + narow, 0.0f);
             warp_colmin32(v, lane);
             atomicMin(&colbuf[acc][cc * 32 + lane], __float_as_uint(v[0]));
           }
+        };
+#pragma unroll 1
+        for (int cc = 0; cc < kBN / 32; cc += 2) {
+          float v0[32], v1[32];
+          tmem_ld32(taddr + cc * 32, v0);
+          tmem_ld32(taddr + (cc + 1) * 32, v1);
+          tmem_wait_ld();
+          chunk(v0, cc);
+          chunk(v1, cc + 1);
         }
         tc_fence_before();
         __syncwarp();
