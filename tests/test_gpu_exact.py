@@ -174,3 +174,35 @@ def test_bidirectional_pass_matches_oracle(ctx, shape):
     d = ctx.directed_hd(torch.from_numpy(B).cuda(), torch.from_numpy(A).cuda())
     tol = 1e-5 * (float((B[d["a"]].astype(np.float64) ** 2).sum()) + float((A[d["b"]].astype(np.float64) ** 2).sum()))
     assert abs(h["ba"]["dist2"] - d["dist2"]) <= tol
+
+
+@pytest.mark.parametrize("kind", ["positive", "heavy", "offset"])
+def test_split_product_error_bound(ctx, kind):
+    """K6 forms a.b as hi.hi (TF32) + [hi lo].[lo hi] (one bf16 MMA), whose error is at most
+    2^-17 (||a - c||^2 + ||b - c||^2) on the centred operands (c = fp64 mean of the first <= 4096
+    rows of B, K0 / DESIGN.md 7.1, 7.3). Inputs chosen so the rounding errors of the split
+    products tend to align: all-positive data with every mantissa bit in play, heavy tails, and a
+    large common offset."""
+    rng = np.random.default_rng({"positive": 1, "heavy": 2, "offset": 3}[kind])
+    nA, nB, D = 1536, 2048, 256
+    if kind == "positive":
+        A = (1.0 + rng.random((nA, D)) * 0.999).astype(np.float32)
+        B = (1.0 + rng.random((nB, D)) * 0.999).astype(np.float32)
+    elif kind == "heavy":
+        A = (rng.standard_t(2, (nA, D)) * 3).astype(np.float32)
+        B = (rng.standard_t(2, (nB, D)) * 3 + 0.5).astype(np.float32)
+    else:
+        A = (rng.standard_normal((nA, D)) + 1000.0).astype(np.float32)
+        B = (rng.standard_normal((nB, D)) + 1000.25).astype(np.float32)
+    rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    ref, arg = oracle.row_minima(A, B)
+    c = B[: min(nB, 4096)].astype(np.float64).mean(0)
+    na = ((A.astype(np.float64) - c) ** 2).sum(1)
+    nb = ((B.astype(np.float64)[arg] - c) ** 2).sum(1)
+    err = np.abs(rm.astype(np.float64) - ref)
+    # fp32 accumulation and the fp32 norms add a few 2^-24 of the norms on top of the products
+    bound = (2.0 ** -17 + 64 * 2.0 ** -24) * (na + nb)
+    assert np.all(err <= bound), f"max err / bound {np.max(err / bound):.3f}"
+    raw = (A.astype(np.float64) ** 2).sum(1) + (B.astype(np.float64)[arg] ** 2).sum(1)
+    assert np.all(err <= TOL * raw)
+    print(f"{kind}: max err / (centred bound) = {np.max(err / bound):.3e}")
