@@ -206,3 +206,14 @@ def test_split_product_error_bound(ctx, kind):
     raw = (A.astype(np.float64) ** 2).sum(1) + (B.astype(np.float64)[arg] ** 2).sum(1)
     assert np.all(err <= TOL * raw)
     print(f"{kind}: max err / (centred bound) = {np.max(err / bound):.3e}")
+
+
+@pytest.mark.parametrize("shape", [(333, 1000, 300), (200, 700, 513), (129, 300, 1000)])
+def test_rowmin_wide(ctx, shape):
+    """D > 256 (several passes of the K-chunk loop, zero-padded ragged last chunk)."""
+    nA, nB, D = shape
+    rng = np.random.default_rng(D)
+    A = rng.standard_normal((nA, D)).astype(np.float32)
+    B = (rng.standard_normal((nB, D)) + 0.1).astype(np.float32)
+    rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    _check_rowmins(A, B, rm)
