@@ -39,7 +39,6 @@
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
 
-#include <cstdlib>
 
 namespace prohd {
 namespace {
