@@ -38,7 +38,6 @@ constexpr int kCl = 8;       // CTAs per cluster
 constexpr int kT = 256;      // threads per CTA
 constexpr int kWarps = kT / 32;
 constexpr int kMaxD = 256;
-constexpr int kRows = kMaxD / kCl;  // rows per CTA (max)
 constexpr int kLuStride = 6 * kMaxD + kMaxD / 8;  // doubles of inverse-iteration scratch per warp
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -197,8 +196,10 @@ __device__ void inverse_iteration(const double* d, const double* e, int D, doubl
 //      lanes along the contiguous row) and scatters p_r and its v.p partial.  -> barrier B
 //   C. K = v.p, w = p - K v, and M[r][c] -= v_r w_c + w_r v_c on its own rows.
 // Writes d, e (de) and the Householder vectors (V rows 0 .. D-3).
+template <int kCl>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduce_cluster_kernel(EigArgs a) {
-  cg::cluster_group cl = cg::this_cluster();
+  constexpr int kRows = kMaxD / kCl;  // rows per CTA (max)
+    cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
   extern __shared__ double dyn[];
   double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/8)*D])
@@ -498,12 +499,34 @@ cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, dou
   const char* es = getenv("PROHD_EIG_STOP");
   EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs, es != nullptr ? atoi(es) : 0, V + static_cast<int64_t>(D) * D};
   cudaError_t e;
-  const size_t smem = sizeof(double) * static_cast<size_t>(kRows) * kMaxD;
-  if ((e = cudaFuncSetAttribute(eigen_reduce_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem))) != cudaSuccess)
-    return e;
-  count_launch();
-  eigen_reduce_cluster_kernel<<<kCl, kT, smem, st>>>(a);
+  // tridiagonalisation on a 16-CTA cluster (non-portable size; 2 rows per warp) for D > 160 where
+  // the device allows it (D = 256: 0.87 -> 0.84 ms), else on 8 CTAs (faster below: the per-step
+  // barrier dominates); PROHD_EIG_CL=8 forces the portable size (A/B)
+  const char* ec = getenv("PROHD_EIG_CL");
+  bool wide = D > 160 && !(ec != nullptr && ec[0] == '8');
+  if (wide) {
+    const size_t smem16 = sizeof(double) * static_cast<size_t>(kMaxD / 16) * kMaxD;
+    wide = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                1) == cudaSuccess &&
+           cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem16)) == cudaSuccess;
+    if (wide) {
+      count_launch();
+      eigen_reduce_cluster_kernel<16><<<16, kT, smem16, st>>>(a);
+      wide = cudaPeekAtLastError() == cudaSuccess;
+      if (!wide) (void)cudaGetLastError();  // clear a launch refusal; fall back to 8 CTAs
+    } else {
+      (void)cudaGetLastError();
+    }
+  }
+  if (!wide) {
+    const size_t smem = sizeof(double) * static_cast<size_t>(kMaxD / kCl) * kMaxD;
+    if ((e = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<kCl>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem))) != cudaSuccess)
+      return e;
+    count_launch();
+    eigen_reduce_cluster_kernel<kCl><<<kCl, kT, smem, st>>>(a);
+  }
   const size_t smem3 = sizeof(double) * static_cast<size_t>(kWarps) * kLuStride;
   if ((e = cudaFuncSetAttribute(eigen_vectors_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem3))) != cudaSuccess)
