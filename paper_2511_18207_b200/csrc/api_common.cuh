@@ -59,7 +59,7 @@ inline PFN_encodeTiled get_encode() {
 }
 
 inline bool make_tmap_2d(CUtensorMap* map, const float* base, int64_t rows, int Dp, int box_rows, char* err,
-                  size_t errlen) {
+                  size_t errlen, int box_inner = kBK) {
   PFN_encodeTiled enc = get_encode();
   if (enc == nullptr) {
     snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
@@ -67,10 +67,12 @@ inline bool make_tmap_2d(CUtensorMap* map, const float* base, int64_t rows, int 
   }
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(Dp), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(Dp) * 4};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   box_inner * 4 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     snprintf(err, errlen, "cuTensorMapEncodeTiled failed (%d) rows=%lld Dp=%d box=%d", static_cast<int>(r),
@@ -275,11 +277,11 @@ inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, flo
   CUtensorMap maps[4];
   char err[256];
   const int Dp = pad_dim(D);
-  if (!make_tmap_2d(&maps[0], R.hi, R.n, Dp, kBM, err, sizeof err) ||
-      !make_tmap_2d(&maps[1], reinterpret_cast<const float*>(R.pr), R.n, Dp, kBM, err, sizeof err) ||
-      !make_tmap_2d(&maps[2], C.hi, C.n, Dp, dist_b_box_rows(D, colmin != nullptr), err, sizeof err) ||
-      !make_tmap_2d(&maps[3], reinterpret_cast<const float*>(C.pc), C.n, Dp, dist_b_box_rows(D, colmin != nullptr),
-                    err, sizeof err))
+  const int bi = dist_box_inner(D, colmin != nullptr), br = dist_b_box_rows(D, colmin != nullptr);
+  if (!make_tmap_2d(&maps[0], R.hi, R.n, Dp, kBM, err, sizeof err, bi) ||
+      !make_tmap_2d(&maps[1], reinterpret_cast<const float*>(R.pr), R.n, Dp, kBM, err, sizeof err, bi) ||
+      !make_tmap_2d(&maps[2], C.hi, C.n, Dp, br, err, sizeof err, bi) ||
+      !make_tmap_2d(&maps[3], reinterpret_cast<const float*>(C.pc), C.n, Dp, br, err, sizeof err, bi))
     return fail(ctx, PROHD_E_CUDA, "%s", err);
   DistArgs a;
   a.maps = maps;

@@ -49,6 +49,8 @@ struct DistArgs {
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st);
 // rows per TMA box of the column operand for the selected K6 variant (256: 1-SM, 128: 2-SM pair)
 int dist_b_box_rows(int D, bool bidir);
+// fp32 features per TMA box row of the selected K6 variant (32: SWIZZLE_128B; 16: SWIZZLE_64B)
+int dist_box_inner(int D, bool bidir);
 
 // K7a: packed max key over rows: (bits(d2) << 32) | (0xFFFFFFFF - (row + row_offset)).
 cudaError_t launch_rowmax_key(const float* rowmin, int64_t n, int64_t row_offset, unsigned long long* key,
@@ -64,7 +66,9 @@ cudaError_t launch_nn64_from_key(const float* X, int64_t x_offset, int64_t nX, c
                                  double* out_d, long long* out_j, cudaStream_t st);
 constexpr int kNNBlocks = 592;  // 4 x 148 SMs
 
-// TMA descriptor for a row-major fp32 matrix [rows x Dp], box {kBK, box_rows}, SWIZZLE_128B.
-bool make_tmap_2d(CUtensorMap* map, const float* base, int64_t rows, int Dp, int box_rows, char* err, size_t errlen);
+// TMA descriptor for a row-major fp32 matrix [rows x Dp], box {box_inner, box_rows}, SWIZZLE_128B for
+// box_inner = 32 (128-B rows) and SWIZZLE_64B for box_inner = 16.
+bool make_tmap_2d(CUtensorMap* map, const float* base, int64_t rows, int Dp, int box_rows, char* err, size_t errlen,
+                  int box_inner);
 
 }  // namespace prohd

@@ -54,7 +54,8 @@ constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + 1024 
 
 struct Sched {
   int64_t nA, nB;
-  int nrb, nt, nsplit, tps, nk, ks_last;
+  int nrb, nt, nsplit, tps, nk, ks_last;  // nk, ks_last: 32-feature chunks
+  int nk1, ks_last1;                      // 16-feature chunks (two-A-block variant)
   int atomic_out;
 };
 
@@ -500,27 +501,226 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ============================================================================
+// Two-A-block variant (directed sweep only): one CTA computes TWO 128-row blocks of A against
+// each 256-column tile of B, one fp32 accumulator each (all 512 TMEM columns, so the epilogue of
+// a tile is not overlapped with the next tile's MMAs). Stages of 16 features (SWIZZLE_64B rows):
+// A1 and A2 hi/pr 4 x 8 KB + B hi/pc 2 x 16 KB = 64 KB, three in flight. Per pair and feature the
+// operand stream drops from 96 KB / (128 x 256 x 32) to 64 KB / (256 x 256 x 16): 2/3.
+// ============================================================================
+constexpr int kBK2 = 16;
+constexpr int kThreadsA2 = 320;  // TMA, MMA, 8 epilogue warps
+constexpr int kStagesA2 = 3;
+constexpr uint32_t kA2Tile = 128 * kBK2 * 4;                    // 8 KB
+constexpr uint32_t kB2Tile = kBN * kBK2 * 4;                    // 16 KB
+constexpr uint32_t kStageA2Bytes = 4 * kA2Tile + 2 * kB2Tile;   // 64 KB
+constexpr size_t kSmemA2 = static_cast<size_t>(kStagesA2) * kStageA2Bytes + 1024 + 256;
+
+__global__ void __launch_bounds__(kThreadsA2, 1)
+    dist_rowmin_2a_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
+                          const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
+                          const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin) {
+  using namespace sm100;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStagesA2 * kStageA2Bytes);
+  uint64_t* empty = full + kStagesA2;
+  uint64_t* tfull = empty + kStagesA2;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  __shared__ __align__(16) float nbuf[2][kBN];  // column norms, double-buffered by tile parity
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStagesA2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 8);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tAh);
+    tma_prefetch(&tAl);
+    tma_prefetch(&tBh);
+    tma_prefetch(&tBl);
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int units = s.nrb * s.nsplit;  // nrb counts 256-row block pairs here
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int pb = u / s.nsplit, sp = u % s.nsplit;
+        const int t0 = sp * s.tps;
+        const int t1 = min(s.nt, t0 + s.tps);
+        for (int t = t0; t < t1; ++t) {
+          for (int c = 0; c < s.nk1; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            uint8_t* st = smem + stage * kStageA2Bytes;
+            mbar_arrive_expect_tx(&full[stage], kStageA2Bytes);
+            tma_load_2d(st, &tAh, c * kBK2, pb * 256, &full[stage]);
+            tma_load_2d(st + kA2Tile, &tAl, c * kBK2, pb * 256, &full[stage]);
+            tma_load_2d(st + 2 * kA2Tile, &tAh, c * kBK2, pb * 256 + 128, &full[stage]);
+            tma_load_2d(st + 3 * kA2Tile, &tAl, c * kBK2, pb * 256 + 128, &full[stage]);
+            tma_load_2d(st + 4 * kA2Tile, &tBh, c * kBK2, t * kBN, &full[stage]);
+            tma_load_2d(st + 4 * kA2Tile + kB2Tile, &tBl, c * kBK2, t * kBN, &full[stage]);
+            if (++stage == kStagesA2) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
+      constexpr uint32_t idesc16 = idesc_bf16(kBM, kBN);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t tph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int sp = u % s.nsplit;
+        const int t0 = sp * s.tps;
+        const int t1 = min(s.nt, t0 + s.tps);
+        for (int t = t0; t < t1; ++t) {
+          mbar_wait(&tempty[0], tph ^ 1u);  // the epilogue has drained both accumulators
+          tc_fence_after();
+          const uint32_t d0 = tmem_base, d1 = tmem_base + static_cast<uint32_t>(kBN);
+          for (int c = 0; c < s.nk1; ++c) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a1h = smem_u32(smem + stage * kStageA2Bytes);
+            const uint32_t a1l = a1h + kA2Tile, a2h = a1h + 2 * kA2Tile, a2l = a1h + 3 * kA2Tile;
+            const uint32_t bh = a1h + 4 * kA2Tile, bl = bh + kB2Tile;
+            const int ks = (c == s.nk1 - 1) ? s.ks_last1 : (kBK2 / 8);
+            for (int kk = 0; kk < ks; ++kk) {
+              const uint32_t off = static_cast<uint32_t>(kk * 32);
+              const uint64_t dbh = smem_desc_k_sw64(bh + off), dbl = smem_desc_k_sw64(bl + off);
+              const uint32_t acc = (c | kk) != 0 ? 1u : 0u;
+              mma_tf32(d0, smem_desc_k_sw64(a1h + off), dbh, idesc, acc);
+              mma_bf16(d0, smem_desc_k_sw64(a1l + off), dbl, idesc16, 1u);
+              mma_tf32(d1, smem_desc_k_sw64(a2h + off), dbh, idesc, acc);
+              mma_bf16(d1, smem_desc_k_sw64(a2l + off), dbl, idesc16, 1u);
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == kStagesA2) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          mma_commit(&tfull[0]);
+          tph ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------------------------------- epilogue
+    // 8 warps: warps 2-5 drain accumulator 0 (rows of A block 1), warps 6-9 accumulator 1
+    const int q = warp & 3;
+    const int a2 = (warp - 2) >> 2;
+    const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+    const int e = (warp - 2) * 32 + lane;  // 0..255: one column norm each
+    uint32_t tph = 0;
+    int tb = 0;  // nbuf parity
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int pb = u / s.nsplit, sp = u % s.nsplit;
+      const int t0 = sp * s.tps;
+      const int t1 = min(s.nt, t0 + s.tps);
+      float rm = __int_as_float(0x7f800000);
+      for (int t = t0; t < t1; ++t) {
+        {
+          const float n1 = __ldg(nb + static_cast<int64_t>(t) * kBN + e);
+          mbar_wait(&tfull[0], tph);
+          nbuf[tb][e] = n1;
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+        }
+        tc_fence_after();
+        const float4* nbp = reinterpret_cast<const float4*>(nbuf[tb]);
+        const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(a2 * kBN);
+#pragma unroll 1
+        for (int cc = 0; cc < kBN / 32; cc += 2) {
+          float v0[32], v1[32];
+          tmem_ld32(taddr + cc * 32, v0);
+          tmem_ld32(taddr + (cc + 1) * 32, v1);
+          tmem_wait_ld();
+          float m[16];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 n0 = nbp[cc * 8 + i], n1 = nbp[(cc + 1) * 8 + i];
+            m[i] = fminf(fminf(fmaf(-2.0f, v0[4 * i + 0], n0.x), fmaf(-2.0f, v0[4 * i + 1], n0.y)),
+                         fminf(fmaf(-2.0f, v0[4 * i + 2], n0.z), fmaf(-2.0f, v0[4 * i + 3], n0.w)));
+            m[8 + i] = fminf(fminf(fmaf(-2.0f, v1[4 * i + 0], n1.x), fmaf(-2.0f, v1[4 * i + 1], n1.y)),
+                             fminf(fmaf(-2.0f, v1[4 * i + 2], n1.z), fmaf(-2.0f, v1[4 * i + 3], n1.w)));
+          }
+#pragma unroll
+          for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+            for (int i = 0; i < w; ++i) m[i] = fminf(m[i], m[i + w]);
+          rm = fminf(rm, m[0]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[0]);
+        tph ^= 1u;
+        tb ^= 1;
+      }
+      const int64_t row = static_cast<int64_t>(pb) * 256 + a2 * 128 + q * 32 + lane;
+      if (row < s.nA) {
+        const float d2 = fmaxf(rm + __ldg(na + row), 0.0f);
+        if (s.atomic_out)
+          atomicMin(reinterpret_cast<int*>(rowmin + row), __float_as_int(d2));
+        else
+          rowmin[row] = d2;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
 }  // namespace
 
-// Variant (measured r01 on one B200): in 30-40 ms runs the 2-SM pair is faster at D=256
-// (507 vs 464 Gpair/s, tools/time_exact.py) but slower at D <= 128 (epilogue-bound). In the
-// sustained, power-capped regime of the benchmark (8 s launches at cfg5) the pair drops to a
-// 1425 MHz median SM clock against 1575 MHz for the single-CTA kernel and loses
-// (474 vs 491 Gpair/s, same box, alternated twice): it is faster per clock but spends more
-// energy per pair. The single-CTA kernel is therefore the default for every D;
-// PROHD_K6_VARIANT=2sm selects the pair (A/B testing).
+// Variants (one B200, tools/time_exact.py). The 2-SM pair (cta_group::2) was faster per clock
+// with three TF32 MMAs but lost in the sustained, power-capped benchmark; with the TF32 + bf16
+// MMAs it measures the same as the single-CTA kernel (547 vs 549 Gpair/s) and stays opt-in.
+// Directed sweeps use the two-A-block kernel for D >= 128 (65536 x 262144, D = 256: 549 -> 627
+// Gpair/s; D = 128: 1048 -> 1126) and the single-block kernel below (faster at small D, where the
+// epilogue is not hidden behind fewer MMAs: D = 64 2118 vs 1896). The fused bidirectional sweep
+// always uses the single-block kernel. PROHD_K6_VARIANT = 1 | 2a | 2sm forces a variant (A/B).
 static int dist_variant(int D) {
-  (void)D;
   const char* e = getenv("PROHD_K6_VARIANT");
-  if (e != nullptr && e[0] == '2') return 2;
-  return 1;
+  if (e != nullptr && e[0] == '2' && e[1] == 's') return 2;  // "2sm": CTA pair
+  if (e != nullptr && e[0] == '2' && e[1] == 'a') return 3;  // "2a": two A blocks per CTA
+  if (e != nullptr && e[0] == '1') return 1;
+  return D >= 128 ? 3 : 1;
 }
 
 int dist_b_box_rows(int D, bool bidir) { return (!bidir && dist_variant(D) == 2) ? 128 : kBN; }
+int dist_box_inner(int D, bool bidir) { return (!bidir && dist_variant(D) == 3) ? kBK2 : kBK; }
 
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   const bool pair = dist_variant(a.D) == 2 && a.num_sms >= 2 && a.colmin == nullptr;
-  const int rows_per_unit = pair ? 256 : kBM;
+  const bool twoa = dist_variant(a.D) == 3 && a.colmin == nullptr;
+  const int rows_per_unit = (pair || twoa) ? 256 : kBM;
   const int ctas_per_unit = pair ? 2 : 1;
   Sched s{};
   s.nA = a.nA;
@@ -529,6 +729,8 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   s.nt = static_cast<int>((a.nB + kBN - 1) / kBN);
   s.nk = (a.D + kBK - 1) / kBK;
   s.ks_last = ((a.D - (s.nk - 1) * kBK) + 7) / 8;
+  s.nk1 = (a.D + kBK2 - 1) / kBK2;
+  s.ks_last1 = ((a.D - (s.nk1 - 1) * kBK2) + 7) / 8;
   const int slots = a.num_sms / ctas_per_unit;  // concurrent units
   // enough units to fill the machine twice when A is small (subset HD)
   const int want = 2 * slots;
@@ -544,6 +746,15 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   }
   const int units = s.nrb * s.nsplit;
   const int nunits = units < slots ? units : slots;
+  if (twoa) {
+    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_2a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemA2));
+    if (e != cudaSuccess) return e;
+    count_launch();
+    dist_rowmin_2a_kernel<<<nunits, kThreadsA2, kSmemA2, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na,
+                                                             a.nb, a.rowmin);
+    return cudaGetLastError();
+  }
   if (pair) {
     cudaError_t e = cudaFuncSetAttribute(dist_rowmin_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kSmem2));

@@ -162,6 +162,16 @@ __device__ __forceinline__ uint64_t smem_desc_k_sw128(uint32_t saddr) {
   d |= static_cast<uint64_t>(2u) << 61;              // SWIZZLE_128B
   return d;
 }
+// K-major operand tile with SWIZZLE_64B: rows of 64 B, 8-row (512 B) atoms (SBO = 512 B).
+__device__ __forceinline__ uint64_t smem_desc_k_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;              // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(512u >> 4) << 32;       // SBO
+  d |= static_cast<uint64_t>(1u) << 46;              // version (sm_100)
+  d |= static_cast<uint64_t>(4u) << 61;              // SWIZZLE_64B
+  return d;
+}
 __host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
