@@ -517,10 +517,13 @@ constexpr uint32_t kB2Tile = kBN * kBK2 * 4;                    // 16 KB
 constexpr uint32_t kStageA2Bytes = 4 * kA2Tile + 2 * kB2Tile;   // 64 KB
 constexpr size_t kSmemA2 = static_cast<size_t>(kStagesA2) * kStageA2Bytes + 1024 + 256;
 
+// kBidir: column minima too (as the single-block kernel), combined over the tile's 256 rows
+template <bool kBidir>
 __global__ void __launch_bounds__(kThreadsA2, 1)
     dist_rowmin_2a_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                           const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
-                          const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin) {
+                          const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin,
+                          float* __restrict__ colmin) {
   using namespace sm100;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -530,9 +533,15 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   __shared__ __align__(16) float nbuf[2][kBN];  // column norms, double-buffered by tile parity
+  __shared__ unsigned colbuf[2][kBN];            // kBidir: the tile's column minima (float bits)
+  __shared__ unsigned tilecnt[2];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (kBidir) {
+    for (int i = threadIdx.x; i < 2 * kBN; i += blockDim.x) (&colbuf[0][0])[i] = 0x7F800000u;
+    if (threadIdx.x < 2) tilecnt[threadIdx.x] = 0u;
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStagesA2; ++i) {
       mbar_init(&full[i], 1);
@@ -642,6 +651,9 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
       const int t0 = sp * s.tps;
       const int t1 = min(s.nt, t0 + s.tps);
       float rm = __int_as_float(0x7f800000);
+      const int64_t myrow = static_cast<int64_t>(pb) * 256 + a2 * 128 + q * 32 + lane;
+      // kBidir: this row's ||a||^2, or +inf for rows past nA (excluded from column minima)
+      const float narow = kBidir ? (myrow < s.nA ? __ldg(na + myrow) : __int_as_float(0x7f800000)) : 0.0f;
       for (int t = t0; t < t1; ++t) {
         {
           const float n1 = __ldg(nb + static_cast<int64_t>(t) * kBN + e);
@@ -652,29 +664,54 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
         tc_fence_after();
         const float4* nbp = reinterpret_cast<const float4*>(nbuf[tb]);
         const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(a2 * kBN);
+        auto chunk = [&](float (&v)[32], int cc) {
+          float m[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 n4 = nbp[cc * 8 + i];
+            v[4 * i + 0] = fmaf(-2.0f, v[4 * i + 0], n4.x);
+            v[4 * i + 1] = fmaf(-2.0f, v[4 * i + 1], n4.y);
+            v[4 * i + 2] = fmaf(-2.0f, v[4 * i + 2], n4.z);
+            v[4 * i + 3] = fmaf(-2.0f, v[4 * i + 3], n4.w);
+            m[i] = fminf(fminf(v[4 * i + 0], v[4 * i + 1]), fminf(v[4 * i + 2], v[4 * i + 3]));
+          }
+          rm = fminf(rm, fminf(fminf(fminf(m[0], m[1]), fminf(m[2], m[3])),
+                               fminf(fminf(m[4], m[5]), fminf(m[6], m[7]))));
+          if (kBidir) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + narow, 0.0f);
+            warp_colmin32(v, lane);
+            atomicMin(&colbuf[tb][cc * 32 + lane], __float_as_uint(v[0]));
+          }
+        };
 #pragma unroll 1
         for (int cc = 0; cc < kBN / 32; cc += 2) {
           float v0[32], v1[32];
           tmem_ld32(taddr + cc * 32, v0);
           tmem_ld32(taddr + (cc + 1) * 32, v1);
           tmem_wait_ld();
-          float m[16];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 n0 = nbp[cc * 8 + i], n1 = nbp[(cc + 1) * 8 + i];
-            m[i] = fminf(fminf(fmaf(-2.0f, v0[4 * i + 0], n0.x), fmaf(-2.0f, v0[4 * i + 1], n0.y)),
-                         fminf(fmaf(-2.0f, v0[4 * i + 2], n0.z), fmaf(-2.0f, v0[4 * i + 3], n0.w)));
-            m[8 + i] = fminf(fminf(fmaf(-2.0f, v1[4 * i + 0], n1.x), fmaf(-2.0f, v1[4 * i + 1], n1.y)),
-                             fminf(fmaf(-2.0f, v1[4 * i + 2], n1.z), fmaf(-2.0f, v1[4 * i + 3], n1.w)));
-          }
-#pragma unroll
-          for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-            for (int i = 0; i < w; ++i) m[i] = fminf(m[i], m[i + w]);
-          rm = fminf(rm, m[0]);
+          chunk(v0, cc);
+          chunk(v1, cc + 1);
         }
         tc_fence_before();
         __syncwarp();
+        if (kBidir) {
+          __threadfence_block();
+          unsigned old = 0;
+          if (lane == 0) old = atomicAdd(&tilecnt[tb], 1u);
+          old = __shfl_sync(0xffffffffu, old, 0);
+          if (old == 7u) {  // last of the 8 epilogue warps: flush the tile's column minima
+            __threadfence_block();
+            for (int j = lane; j < kBN; j += 32) {
+              const unsigned val = atomicExch(&colbuf[tb][j], 0x7F800000u);
+              const int64_t col = static_cast<int64_t>(t) * kBN + j;
+              if (col < s.nB) atomicMin(reinterpret_cast<unsigned*>(colmin) + col, val);
+            }
+            if (lane == 0) tilecnt[tb] = 0u;
+            __threadfence_block();
+          }
+          __syncwarp();
+        }
         if (lane == 0) mbar_arrive(&tempty[0]);
         tph ^= 1u;
         tb ^= 1;
@@ -705,7 +742,9 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
 // Directed sweeps use the two-A-block kernel for D >= 128 (65536 x 262144, D = 256: 549 -> 627
 // Gpair/s; D = 128: 1048 -> 1126) and the single-block kernel below (faster at small D, where the
 // epilogue is not hidden behind fewer MMAs: D = 64 2118 vs 1896). The fused bidirectional sweep
-// always uses the single-block kernel. PROHD_K6_VARIANT = 1 | 2a | 2sm forces a variant (A/B).
+// keeps the single-block kernel: its column-minimum epilogue is heavier and, not overlapped in the
+// two-A kernel, made it slower (D = 256: 34.5 vs 31.5 ms for 65536 x 262144; the two-A kBidir
+// instantiation is kept for A/B). PROHD_K6_VARIANT = 1 | 2a | 2sm forces a variant (2sm: directed).
 static int dist_variant(int D) {
   const char* e = getenv("PROHD_K6_VARIANT");
   if (e != nullptr && e[0] == '2' && e[1] == 's') return 2;  // "2sm": CTA pair
@@ -715,11 +754,15 @@ static int dist_variant(int D) {
 }
 
 int dist_b_box_rows(int D, bool bidir) { return (!bidir && dist_variant(D) == 2) ? 128 : kBN; }
-int dist_box_inner(int D, bool bidir) { return (!bidir && dist_variant(D) == 3) ? kBK2 : kBK; }
+static bool bidir_2a() {
+  const char* e = getenv("PROHD_K6_BIDIR_2A");  // dev A/B: fused bidirectional sweep on the two-A kernel
+  return e != nullptr && e[0] == '1';
+}
+int dist_box_inner(int D, bool bidir) { return ((!bidir || bidir_2a()) && dist_variant(D) == 3) ? kBK2 : kBK; }
 
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   const bool pair = dist_variant(a.D) == 2 && a.num_sms >= 2 && a.colmin == nullptr;
-  const bool twoa = dist_variant(a.D) == 3 && a.colmin == nullptr;
+  const bool twoa = dist_variant(a.D) == 3 && (a.colmin == nullptr || bidir_2a());
   const int rows_per_unit = (pair || twoa) ? 256 : kBM;
   const int ctas_per_unit = pair ? 2 : 1;
   Sched s{};
@@ -747,12 +790,16 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   const int units = s.nrb * s.nsplit;
   const int nunits = units < slots ? units : slots;
   if (twoa) {
-    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_2a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemA2));
+    if (a.colmin != nullptr) {
+      cudaError_t e = cudaMemsetAsync(a.colmin, 0x7F, sizeof(float) * a.nB, st);
+      if (e != cudaSuccess) return e;
+    }
+    auto kern = a.colmin != nullptr ? dist_rowmin_2a_kernel<true> : dist_rowmin_2a_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemA2));
     if (e != cudaSuccess) return e;
     count_launch();
-    dist_rowmin_2a_kernel<<<nunits, kThreadsA2, kSmemA2, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na,
-                                                             a.nb, a.rowmin);
+    kern<<<nunits, kThreadsA2, kSmemA2, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na, a.nb, a.rowmin,
+                                             a.colmin);
     return cudaGetLastError();
   }
   if (pair) {
