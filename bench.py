@@ -367,7 +367,8 @@ def run_ours(args, rank: int, world: int):
                                                           "total_ms")}},
         "exact": {"dist": ex["dist"], "a": ex["a"], "b": ex["b"], "Gpair_s_kernel": pairs_launch / k6_ms / 1e6},
         "roofline": {"bound": "tensor",
-                     "kernel": "K6 dist_rowmin_kernel (tcgen05 kind::tf32 hi.hi + kind::f16 bf16 pair correction)",
+                     "kernel": ("K6 dist_rowmin_2a_kernel (two 128-row A blocks per CTA; tcgen05 kind::tf32 "
+                                "hi.hi + kind::f16 bf16 pair correction)"),
                      "achieved": k6_tflops, "peak": tf32_peak, "unit": "TFLOP/s", "frac": k6_tflops / tf32_peak,
                      "traffic": (tpp * pairs_launch) if tpp else None,
                      "note": ("achieved = 6*D executed tensor flops per pair (2*D TF32 + 4*D bf16) x pairs per "
