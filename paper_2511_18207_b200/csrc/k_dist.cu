@@ -45,7 +45,8 @@ namespace prohd {
 namespace {
 
 constexpr int kStages = 2;
-constexpr int kThreads = 192;
+constexpr int kThreads = 192;   // 2-SM kernel: TMA, MMA, 4 epilogue warps
+constexpr int kThreads1 = 320;  // single-block kernel: TMA, MMA, 8 epilogue warps (two column halves)
 constexpr uint32_t kATile = kBM * kBK * 4;                  // 16 KB
 constexpr uint32_t kBTile = kBN * kBK * 4;                  // 32 KB
 constexpr uint32_t kStageBytes = 2 * kATile + 2 * kBTile;   // 96 KB
@@ -79,7 +80,7 @@ __device__ __forceinline__ void warp_colmin32(float (&v)[32], int lane) {
 // reduces its 32 rows with a butterfly reduce-scatter, the 4 warps combine in shared
 // memory, and the last warp of the tile flushes the 256 minima with global atomicMin.
 template <bool kBidir>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads1, 1)
     dist_rowmin_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                        const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
                        const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin,
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ unsigned colbuf[2][kBN];  // kBidir: per-accumulator column minima (float bits)
   __shared__ __align__(16) float nbuf[2][kBN];  // column norms of the tile in each accumulator
   __shared__ unsigned tilecnt[2];
+  __shared__ float rbuf[kBM];  // row minima of the second column half, combined at the unit's end
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 8);
     }
     fence_mbar_init();
   }
@@ -202,9 +204,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // -------------------------------------------------------------- epilogue
+    // 8 warps: warps 2-5 take columns 0-127 of each tile, warps 6-9 columns 128-255, each for
+    // its TMEM lane quarter (warp % 4); the two halves' row minima meet in shared memory at the
+    // end of the unit
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;
     const int row_local = q * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+    const int e = (warp - 2) * 32 + lane;  // 0..255: one column norm each
     int acc = 0;
     uint32_t aphase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -216,14 +223,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // kBidir: this row's ||a||^2, or +inf for rows past nA (excluded from column minima)
       const float narow = kBidir ? (row < s.nA ? __ldg(na + row) : __int_as_float(0x7f800000)) : 0.0f;
       for (int t = t0; t < t1; ++t) {
-        // the tile's column norms: loaded before the accumulator wait, staged in shared memory
-        // (one 16-B piece per thread per accumulator buffer), read back as broadcasts
+        // the tile's column norms: loaded before the accumulator wait, staged in shared memory,
+        // read back as broadcasts
         {
-          const int e = q * 32 + lane;  // 0..127: two floats each
-          const float2 n2 = __ldg(reinterpret_cast<const float2*>(nb + static_cast<int64_t>(t) * kBN) + e);
+          const float n1 = __ldg(nb + static_cast<int64_t>(t) * kBN + e);
           mbar_wait(&tfull[acc], aphase);
-          reinterpret_cast<float2*>(nbuf[acc])[e] = n2;
-          asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+          nbuf[acc][e] = n1;
+          asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
         }
         tc_fence_after();
         const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(acc * kBN);
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         };
 #pragma unroll 1
-        for (int cc = 0; cc < kBN / 32; cc += 2) {
+        for (int cc = half * 4; cc < half * 4 + 4; cc += 2) {
           float v0[32], v1[32];
           tmem_ld32(taddr + cc * 32, v0);
           tmem_ld32(taddr + (cc + 1) * 32, v1);
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           unsigned old = 0;
           if (lane == 0) old = atomicAdd(&tilecnt[acc], 1u);
           old = __shfl_sync(0xffffffffu, old, 0);
-          if (old == 3u) {  // last of the 4 epilogue warps: flush the tile's column minima
+          if (old == 7u) {  // last of the 8 epilogue warps: flush the tile's column minima
             __threadfence_block();
             for (int j = lane; j < kBN; j += 32) {
               const unsigned val = atomicExch(&colbuf[acc][j], 0x7F800000u);
@@ -281,8 +287,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc ^= 1;
         if (acc == 0) aphase ^= 1u;
       }
-      if (row < s.nA) {
-        const float d2 = fmaxf(rmin + __ldg(na + row), 0.0f);
+      if (half == 1) rbuf[row_local] = rmin;
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      if (half == 0 && row < s.nA) {
+        const float d2 = fmaxf(fminf(rmin, rbuf[row_local]) + __ldg(na + row), 0.0f);
         if (s.atomic_out)
           atomicMin(reinterpret_cast<int*>(rowmin + row), __float_as_int(d2));
         else
@@ -818,7 +826,7 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
                              static_cast<int>(kSmemBytes));
     if (e != cudaSuccess) return e;
     count_launch();
-    dist_rowmin_kernel<true><<<nunits, kThreads, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
+    dist_rowmin_kernel<true><<<nunits, kThreads1, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
                                                                     a.na, a.nb, a.rowmin, a.colmin);
     return cudaGetLastError();
   }
@@ -828,7 +836,7 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   }
   count_launch();
-  dist_rowmin_kernel<false><<<nunits, kThreads, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
+  dist_rowmin_kernel<false><<<nunits, kThreads1, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
                                                                    a.na, a.nb, a.rowmin, nullptr);
   return cudaGetLastError();
 }
