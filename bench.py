@@ -370,6 +370,10 @@ def run_ours(args, rank: int, world: int):
                      "kernel": ("K6 dist_rowmin_2a_kernel (two 128-row A blocks per CTA; tcgen05 kind::tf32 "
                                 "hi.hi + kind::f16 bf16 pair correction)"),
                      "achieved": k6_tflops, "peak": tf32_peak, "unit": "TFLOP/s", "frac": k6_tflops / tf32_peak,
+                     # the north star's yardstick: 3xTF32-equivalent work (6D TF32 flops per pair) against
+                     # the dense TF32 peak; above 1 because the kernel forms the split product with one
+                     # TF32 and one bf16 MMA instead of three TF32 MMAs
+                     "frac_vs_3xtf32_roofline": k6_tflops / (pk["bf16_tflops"] * NOMINAL_TF32_OVER_BF16),
                      "traffic": (tpp * pairs_launch) if tpp else None,
                      "note": ("achieved = 6*D executed tensor flops per pair (2*D TF32 + 4*D bf16) x pairs per "
                               "launch / mean launch time from CUDA events on the launch stream; peak = the mixed "
