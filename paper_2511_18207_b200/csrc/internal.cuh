@@ -29,6 +29,9 @@ inline int pad_dim(int D) { return static_cast<int>(round_up(D, 4)); }  // 16-B 
 // x or norm is not finite.
 cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, const double* centre, float* hi,
                         uint32_t* pr, uint32_t* pc, float* norms, int* bad, cudaStream_t st);
+// PROHD_K6_SPLIT=3xtf32: the north star's literal 3xTF32 form (hi.hi + hi.lo + lo.hi, three TF32
+// MMAs); K0 then writes lo (fp32) into pr and pc instead of the bf16 pairs. Default: off.
+bool k6_split3();
 // Common centre of a pair (X, Y): fp64 mean of the first min(nX, 4096) rows of X and the
 // first min(nY, 4096) rows of Y (either count may be 0), summed per set and then added,
 // so centre(X, Y) == centre(Y, X) bit for bit. c: 2D doubles (the second half is scratch).

@@ -54,6 +54,7 @@ constexpr uint32_t kTmemCols = 512;
 constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + 1024 + 256;
 
 struct Sched {
+  int split3;  // k6_split3(): three TF32 MMAs (hi.hi, hi.lo, lo.hi) on fp32 lo tiles
   int64_t nA, nB;
   int nrb, nt, nsplit, tps, nk, ks_last;  // nk, ks_last: 32-feature chunks
   int nk1, ks_last1;                      // 16-feature chunks (two-A-block variant)
@@ -187,7 +188,12 @@ __global__ void __launch_bounds__(kThreads1, 1)
               const uint64_t dbh = smem_desc_k_sw128(bh + off);
               const uint64_t dbl = smem_desc_k_sw128(bl + off);
               mma_tf32(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
-              mma_bf16(d, dal, dbl, idesc16, 1u);                   // [hi lo]_a . [lo hi]_b
+              if (s.split3) {
+                mma_tf32(d, dah, dbl, idesc, 1u);  // hi_a . lo_b
+                mma_tf32(d, dal, dbh, idesc, 1u);  // lo_a . hi_b
+              } else {
+                mma_bf16(d, dal, dbl, idesc16, 1u);  // [hi lo]_a . [lo hi]_b
+              }
             }
             mma_commit(&empty[stage]);
             if (++stage == kStages) {
@@ -430,7 +436,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const uint64_t dbh = smem_desc_k_sw128(bh + off);
               const uint64_t dbl = smem_desc_k_sw128(bl + off);
               mma_tf32_2sm(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
-              mma_bf16_2sm(d, dal, dbl, idesc16, 1u);                   // [hi lo]_a . [lo hi]_b
+              if (s.split3) {
+                mma_tf32_2sm(d, dah, dbl, idesc, 1u);
+                mma_tf32_2sm(d, dal, dbh, idesc, 1u);
+              } else {
+                mma_bf16_2sm(d, dal, dbl, idesc16, 1u);  // [hi lo]_a . [lo hi]_b
+              }
             }
             mma_commit_2sm_mc(&empty[stage], 0x3);
             if (++stage == kStages2) {
@@ -628,10 +639,19 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
               const uint32_t off = static_cast<uint32_t>(kk * 32);
               const uint64_t dbh = smem_desc_k_sw64(bh + off), dbl = smem_desc_k_sw64(bl + off);
               const uint32_t acc = (c | kk) != 0 ? 1u : 0u;
-              mma_tf32(d0, smem_desc_k_sw64(a1h + off), dbh, idesc, acc);
-              mma_bf16(d0, smem_desc_k_sw64(a1l + off), dbl, idesc16, 1u);
-              mma_tf32(d1, smem_desc_k_sw64(a2h + off), dbh, idesc, acc);
-              mma_bf16(d1, smem_desc_k_sw64(a2l + off), dbl, idesc16, 1u);
+              const uint64_t da1h = smem_desc_k_sw64(a1h + off), da1l = smem_desc_k_sw64(a1l + off);
+              const uint64_t da2h = smem_desc_k_sw64(a2h + off), da2l = smem_desc_k_sw64(a2l + off);
+              mma_tf32(d0, da1h, dbh, idesc, acc);
+              mma_tf32(d1, da2h, dbh, idesc, acc);
+              if (s.split3) {
+                mma_tf32(d0, da1h, dbl, idesc, 1u);
+                mma_tf32(d0, da1l, dbh, idesc, 1u);
+                mma_tf32(d1, da2h, dbl, idesc, 1u);
+                mma_tf32(d1, da2l, dbh, idesc, 1u);
+              } else {
+                mma_bf16(d0, da1l, dbl, idesc16, 1u);
+                mma_bf16(d1, da2l, dbl, idesc16, 1u);
+              }
             }
             mma_commit(&empty[stage]);
             if (++stage == kStagesA2) {
@@ -762,6 +782,11 @@ static int dist_variant(int D) {
 }
 
 int dist_b_box_rows(int D, bool bidir) { return (!bidir && dist_variant(D) == 2) ? 128 : kBN; }
+bool k6_split3() {
+  const char* e = getenv("PROHD_K6_SPLIT");
+  return e != nullptr && e[0] == '3';
+}
+
 static bool bidir_2a() {
   const char* e = getenv("PROHD_K6_BIDIR_2A");  // dev A/B: fused bidirectional sweep on the two-A kernel
   return e != nullptr && e[0] == '1';
@@ -774,6 +799,7 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   const int rows_per_unit = (pair || twoa) ? 256 : kBM;
   const int ctas_per_unit = pair ? 2 : 1;
   Sched s{};
+  s.split3 = k6_split3() ? 1 : 0;
   s.nA = a.nA;
   s.nB = a.nB;
   s.nrb = static_cast<int>((a.nA + rows_per_unit - 1) / rows_per_unit);

@@ -35,7 +35,7 @@ __device__ __forceinline__ uint32_t bf16_pair(float first, float second) {
   return a | (b << 16);
 }
 
-template <bool kGather, bool kCentre>
+template <bool kGather, bool kCentre, bool kSplit3>
 __global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, const int64_t* __restrict__ idx,
                                                    int64_t n, int D, int Dp, int64_t n_pad,
                                                    const double* __restrict__ centre, float* __restrict__ hi,
@@ -62,15 +62,15 @@ __global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, 
         const float vh = tf32_trunc(static_cast<float>(y));
         const float vl = static_cast<float>(y - static_cast<double>(vh));
         h[c] = vh;
-        qr[c] = bf16_pair(vh, vl);
-        qc[c] = bf16_pair(vl, vh);
+        qr[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vh, vl);
+        qc[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vl, vh);
         s = fma(y, y, s);
       } else {
         const float vh = tf32_trunc(v);
         const float vl = v - vh;
         h[c] = vh;
-        qr[c] = bf16_pair(vh, vl);
-        qc[c] = bf16_pair(vl, vh);
+        qr[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vh, vl);
+        qc[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vl, vh);
         s = fma(static_cast<double>(v), static_cast<double>(v), s);
       }
     }
@@ -94,12 +94,16 @@ static int grid_for_rows(int64_t rows) {
 cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, const double* centre, float* hi,
                         uint32_t* pr, uint32_t* pc, float* norms, int* bad, cudaStream_t st) {
   count_launch();
-  if (centre)
-    prep_kernel<false, true><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, centre, hi, pr, pc,
-                                                                    norms, bad);
+  const int g = grid_for_rows(n_pad);
+  const bool s3 = k6_split3();
+  if (centre && s3)
+    prep_kernel<false, true, true><<<g, 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, centre, hi, pr, pc, norms, bad);
+  else if (centre)
+    prep_kernel<false, true, false><<<g, 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, centre, hi, pr, pc, norms, bad);
+  else if (s3)
+    prep_kernel<false, false, true><<<g, 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, nullptr, hi, pr, pc, norms, bad);
   else
-    prep_kernel<false, false><<<grid_for_rows(n_pad), 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, nullptr, hi, pr,
-                                                                     pc, norms, bad);
+    prep_kernel<false, false, false><<<g, 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, nullptr, hi, pr, pc, norms, bad);
   return cudaGetLastError();
 }
 

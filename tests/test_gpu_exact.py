@@ -217,3 +217,30 @@ def test_rowmin_wide(ctx, shape):
     B = (rng.standard_normal((nB, D)) + 0.1).astype(np.float32)
     rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
     _check_rowmins(A, B, rm)
+
+
+@pytest.fixture
+def split3():
+    """PROHD_K6_SPLIT=3xtf32: the north star's literal 3xTF32 form (three TF32 MMAs on fp32 hi/lo)."""
+    import os
+    old = os.environ.get("PROHD_K6_SPLIT")
+    os.environ["PROHD_K6_SPLIT"] = "3xtf32"
+    yield
+    if old is None:
+        del os.environ["PROHD_K6_SPLIT"]
+    else:
+        os.environ["PROHD_K6_SPLIT"] = old
+
+
+@pytest.mark.parametrize("shape", [(300, 513, 16), (1000, 3000, 64), (513, 1100, 256), (2000, 2500, 128)])
+def test_rowmin_literal_3xtf32(ctx, split3, shape):
+    nA, nB, D = shape
+    rng = np.random.default_rng(nA + D)
+    A = rng.standard_normal((nA, D)).astype(np.float32)
+    B = (rng.standard_normal((nB, D)) * 1.5 + 0.25).astype(np.float32)
+    rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    _check_rowmins(A, B, rm)
+    h = ctx.hausdorff(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    ref = oracle.hausdorff(A, B)
+    _check_directed(A, B, h["ab"], ref["ab"])
+    _check_directed(B, A, h["ba"], ref["ba"])
