@@ -238,3 +238,25 @@ def test_special_values(ctx, D):
     A[::13, 3] = np.float32(3e-40)   # subnormal
     B[::5, 0] = np.float32(-2e-39)   # subnormal
     _check_layers(ctx, A, B, 3, 9)
+
+
+@pytest.mark.parametrize("bad", ["nan_a", "inf_b", "neg_inf_a"])
+def test_nonfinite_wide(ctx, bad):
+    """Non-finite input at D = 256 (DMMA Gram with the F2F fallback, tcgen05 projection, K6):
+    every entry point reports PROHD_E_DATA instead of returning a number."""
+    from paper_2511_18207_b200 import ProHDError
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((3000, 256)).astype(np.float32)
+    B = rng.standard_normal((2500, 256)).astype(np.float32)
+    if bad == "nan_a":
+        A[1234, 77] = np.nan
+    elif bad == "inf_b":
+        B[17, 200] = np.inf
+    else:
+        A[2999, 0] = -np.inf
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    for call in (lambda: ctx.prohd_estimate(At, Bt, 8, 50), lambda: ctx.directed_hd(At, Bt),
+                 lambda: ctx.hausdorff(At, Bt)):
+        with pytest.raises(ProHDError) as e:
+            call()
+        assert e.value.code == 3
