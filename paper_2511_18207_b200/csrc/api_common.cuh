@@ -37,6 +37,9 @@ struct prohd_ctx {
   int t_total = -1;
   long long launches0 = 0;
   prohd_timings last{};
+  // second stream for independent per-set work (the two sets' selection chains overlap)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace prohd {

@@ -49,6 +49,9 @@ int prohd_create(int device, void* cuda_stream, prohd_ctx** out) {
 int prohd_destroy(prohd_ctx* ctx) {
   if (ctx == nullptr) return PROHD_OK;
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
   delete ctx;
   return PROHD_OK;
 }

@@ -184,23 +184,35 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   const float* X[2] = {A, B};
   const int64_t n[2] = {nA, nB};
   const int t_sel = tmark(ctx);
+  // set B's chain runs on the context's second stream, set A's on the caller's: the low-occupancy
+  // tail of one set's selection (collect, re-rank, compaction) overlaps the other's projection
+  if (ctx->aux == nullptr) {
+    CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
+  if (counts && L > 1) CK(launch_minus_one(w.n_dirs, w.n_dirs1, st));  // shared by both sets
+  CK(cudaEventRecord(ctx->ev_fork, st));
+  CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
   for (int s = 0; s < 2; ++s) {
     // projections run for every point (also when 2m >= n) so non-finite input is always detected
+    cudaStream_t sst = s == 0 ? st : ctx->aux;
     SelectBufs& b = w.sel[s];
     const int64_t m0 = counts ? counts[2 * s] : m;      // centroid axis
     const int64_t m1 = counts ? counts[2 * s + 1] : m;  // principal directions
     const bool all = 2 * m0 >= n[s] || (L > 1 && 2 * m1 >= n[s]);
     if (all) {
-      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, st));  // finiteness pass
-      CK(launch_iota(b.uidx, b.ucount, n[s], st));
+      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, sst));  // finiteness pass
+      CK(launch_iota(b.uidx, b.ucount, n[s], sst));
     } else if (m0 == m1 || L == 1) {
-      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, st));
+      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst));
     } else {  // two direction groups with different per-tail counts, one shared union bitmap
-      CK(launch_select(X[s], n[s], D, w.U64, w.U32, 1, w.n_dirs, m0, b, st, true, false));
-      CK(launch_minus_one(w.n_dirs, w.n_dirs1, st));
-      CK(launch_select(X[s], n[s], D, w.U64 + D, w.U32 + D, L - 1, w.n_dirs1, m1, b, st, false, true));
+      CK(launch_select(X[s], n[s], D, w.U64, w.U32, 1, w.n_dirs, m0, b, sst, true, false));
+      CK(launch_select(X[s], n[s], D, w.U64 + D, w.U32 + D, L - 1, w.n_dirs1, m1, b, sst, false, true));
     }
   }
+  CK(cudaEventRecord(ctx->ev_join, ctx->aux));
+  CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
   tspan(ctx, PH_SELECT, t_sel);
   unsigned ucount[2];
   int ndirs = 0, ovf[2] = {0, 0};
