@@ -12,8 +12,12 @@
 // square of blocks on or above the diagonal gives one or two groups. A group with fewer
 // than 12 tiles runs each tile on kRep = 2 or 4 warps that take alternate k-steps (partial
 // accumulators summed by the reduce kernel), so small D still fills the MMA warps.
-// CTA = (point range r, group g), blockIdx = r * ngroups + g, ONE CTA per SM, one wave: the
-// ngroups CTAs reading the same rows are adjacent in launch order and share them through L2.
+// A diagonal tile issues only its 10 8x8 blocks on or above the diagonal (A = B fragments).
+// The diagonal tiles go four to a group, on warps 0-3 (one per SM sub-partition, whose DMMA
+// pipe its 3 warps share), and each group gets CTAs in proportion to its busiest
+// sub-partition's DMMA count: D = 256 has groups of 4+8, 4+8 and 0+12 tiles (42, 42 and 48
+// DMMAs per k-step) over 47, 47 and 54 point ranges, against 48 x 49 when every tile was full.
+// CTA = (group g, point range r), blockIdx = grp[g].cta0 + r, ONE CTA per SM, one wave.
 //
 // CTA = 16 warps:
 //   warps 12-15 (loaders): thread ct owns 16-B pieces (4 features) of fixed column 4 (ct % P)
@@ -60,8 +64,7 @@ struct GramArgs {
   int64_t nA, nB;
   int D;
   const double* s;
-  int ngroups, rpg;
-  int64_t per;      // points per range (multiple of kGMC)
+  int ngroups;
   double* Gpart;    // [cta][kMW warps][32][32]
   const double* Cpart;  // colsum_kernel partials [cs_blocks][2 sets][D]
   int cs_blocks;
@@ -97,12 +100,13 @@ __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ Gr
   extern __shared__ __align__(16) uint8_t gsm[];
   float* stage = reinterpret_cast<float*>(gsm);                                  // [kGNS][kGMC][32 nslot]
   double* tile = reinterpret_cast<double*>(gsm + sizeof(float) * kGNS * kGStageF);  // [kGNB][kGMC][kGLd]
-  const int g = blockIdx.x % a.ngroups;
-  const int r = blockIdx.x / a.ngroups;
+  int g = 0;
+  while (g + 1 < a.ngroups && static_cast<int>(blockIdx.x) >= a.grp[g + 1].cta0) ++g;
   const GramGroup& G = a.grp[g];
+  const int r = blockIdx.x - G.cta0;
   const int64_t N = a.nA + a.nB;
-  const int64_t p0 = static_cast<int64_t>(r) * a.per;
-  const int64_t p1 = p0 + a.per < N ? p0 + a.per : N;
+  const int64_t p0 = static_cast<int64_t>(r) * G.per;
+  const int64_t p1 = p0 + G.per < N ? p0 + G.per : N;
   const int nch = p1 > p0 ? static_cast<int>((p1 - p0 + kGMC - 1) / kGMC) : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rowf = 32 * G.nslot;  // staged floats per row
@@ -220,6 +224,7 @@ __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ Gr
     const int t = active ? warp % G.ntiles : 0;
     const int ri = active ? warp / G.ntiles : 0;  // k-steps ri, ri + kRep, ... of each chunk
     const int sI = G.si[t], sJ = G.sj[t];
+    const bool dg = sI == sJ;  // diagonal tile: the 10 8x8 blocks on or above its diagonal, A = B fragments
     const int fr = lane >> 2, fk = lane & 3;
     constexpr int kS = 4 / kRep;  // k-steps per chunk for this warp
 
@@ -234,16 +239,24 @@ __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ Gr
       if (active) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) A_[i] = row[oI + i * 8];
+        if (!dg)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) B_[j] = row[oJ + j * 8];
+          for (int j = 0; j < 4; ++j) B_[j] = row[oJ + j * 8];
       }
     };
     auto mma16 = [&](const double (&A_)[4], const double (&B_)[4]) {
       if (active) {
+        if (dg) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma(acc[i][j], A_[i], B_[j]);
+            for (int j = i; j < 4; ++j) dmma(acc[i][j], A_[i], A_[j]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma(acc[i][j], A_[i], B_[j]);
+        }
       }
     };
     if constexpr (kS >= 2) {
@@ -305,9 +318,9 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const __grid_constant_
     const GramGroup& G = a.grp[g];
     if (t >= G.ntiles) return;  // uniform per CTA
     double acc = 0.0;
-    for (int r = warp; r < a.rpg; r += 8)
+    for (int r = warp; r < G.rpg; r += 8)
       for (int q = 0; q < G.rep; ++q)
-        acc += a.Gpart[(static_cast<int64_t>(r * a.ngroups + g) * kMW + q * G.ntiles + t) * 1024 + x];
+        acc += a.Gpart[(static_cast<int64_t>(G.cta0 + r) * kMW + q * G.ntiles + t) * 1024 + x];
     part[0][warp][lane] = acc;
     __syncthreads();
     if (warp == 0) {
@@ -460,19 +473,41 @@ bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p) {
     return true;
   };
   if (nb <= kSlotsMax) {
-    // every group stages all nb blocks; the T = nb (nb + 1) / 2 tiles split evenly
-    int fbs[kSlotsMax], tl[64][2], T = 0;
+    // every group stages all nb blocks; the T = nb (nb + 1) / 2 tiles split evenly over the
+    // groups, the nb diagonal tiles (10 of 16 DMMAs per k-step) dealt out four per group first
+    // and placed on warps 0-3 (one per SM sub-partition, whose DMMA pipe the warps share)
+    int fbs[kSlotsMax], dl[kSlotsMax][2], ol[64][2], nd = 0, no = 0;
     for (int s = 0; s < nb; ++s) fbs[s] = s;
     for (int i = 0; i < nb; ++i)
       for (int j = i; j < nb; ++j) {
-        tl[T][0] = i;
-        tl[T][1] = j;
-        ++T;
+        int(*l)[2] = i == j ? dl : ol;
+        int& c = i == j ? nd : no;
+        l[c][0] = i;
+        l[c][1] = j;
+        ++c;
       }
+    const int T = nd + no;
     const int ng = (T + kMW - 1) / kMW;
+    int di = 0, oi = 0;
     for (int g = 0; g < ng; ++g) {
-      const int t0 = T * g / ng, t1 = T * (g + 1) / ng;
-      if (!add_group(fbs, nb, tl + t0, t1 - t0)) return false;
+      const int sz = T * (g + 1) / ng - T * g / ng;
+      int tl[kMW][2], n = 0;
+      while (n < sz && n < 4 && di < nd) {
+        tl[n][0] = dl[di][0];
+        tl[n][1] = dl[di][1];
+        ++n, ++di;
+      }
+      while (n < sz && oi < no) {
+        tl[n][0] = ol[oi][0];
+        tl[n][1] = ol[oi][1];
+        ++n, ++oi;
+      }
+      while (n < sz && di < nd) {
+        tl[n][0] = dl[di][0];
+        tl[n][1] = dl[di][1];
+        ++n, ++di;
+      }
+      if (!add_group(fbs, nb, tl, n)) return false;
     }
   } else {
     // 4x4 squares of blocks on or above the diagonal: <= 8 blocks, <= 16 tiles -> 1 or 2 groups
@@ -482,13 +517,14 @@ bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p) {
         for (int i = a; i < a + 4 && i < nb; ++i) fbs[nfb++] = i;
         if (b != a)
           for (int j = b; j < b + 4 && j < nb; ++j) fbs[nfb++] = j;
-        for (int i = a; i < a + 4 && i < nb; ++i)
-          for (int j = b; j < b + 4 && j < nb; ++j)
-            if (i <= j) {
-              tl[T][0] = i;
-              tl[T][1] = j;
-              ++T;
-            }
+        for (int pass = 0; pass < 2; ++pass)  // diagonal tiles first (warps 0-3)
+          for (int i = a; i < a + 4 && i < nb; ++i)
+            for (int j = b; j < b + 4 && j < nb; ++j)
+              if (i <= j && (i == j) == (pass == 0)) {
+                tl[T][0] = i;
+                tl[T][1] = j;
+                ++T;
+              }
         const int ng = (T + kMW - 1) / kMW;
         for (int g = 0; g < ng; ++g) {
           const int t0 = T * g / ng, t1 = T * (g + 1) / ng;
@@ -504,14 +540,48 @@ bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p) {
       for (int q = 0; q < p.ngroups; ++q) p.grp[q].rep = m;
       break;
     }
+  // Cost model: warp w runs on SM sub-partition w % 4 and issues 16 (10 on a diagonal tile)
+  // DMMAs per k-step; a group's CTA time per point is set by its busiest sub-partition. The
+  // one-wave CTA budget is split over the groups in proportion to that load (largest
+  // remaining time per range first), and every group cuts A u B into its own rpg ranges.
   const int64_t N = nA + nB;
   const int64_t chunks = N > 0 ? (N + kGMC - 1) / kGMC : 1;
-  int rpg = (num_sms > 0 ? num_sms : 148) / p.ngroups;  // one CTA per SM, one wave
-  if (rpg < 1) rpg = 1;
-  if (rpg > chunks) rpg = static_cast<int>(chunks);
-  p.rpg = rpg;
-  p.per = ((N + rpg - 1) / rpg + kGMC - 1) / kGMC * kGMC;
-  p.nctas = p.ngroups * rpg;
+  const int budget = num_sms > 0 ? num_sms : 148;
+  for (int g = 0; g < p.ngroups; ++g) {
+    GramGroup& G = p.grp[g];
+    int sp[4] = {0, 0, 0, 0};
+    for (int w = 0; w < G.ntiles * G.rep && w < kMW; ++w) {
+      const int t = w % G.ntiles;
+      sp[w % 4] += G.si[t] == G.sj[t] ? 10 : 16;
+    }
+    G.load = sp[0];
+    for (int q = 1; q < 4; ++q) G.load = sp[q] > G.load ? sp[q] : G.load;
+    if (G.load < 1) G.load = 1;
+    G.rpg = 1;
+  }
+  // beta: a per-point cost outside the DMMA pipe, in DMMA units (dev A/B: PROHD_K1_BETA)
+  double beta = 0.0;
+  if (const char* e = getenv("PROHD_K1_BETA")) beta = atof(e);
+  for (int used = p.ngroups; used < budget; ++used) {
+    int best = -1;
+    double bt = 0.0;
+    for (int g = 0; g < p.ngroups; ++g) {
+      const double t = (p.grp[g].load + beta) / p.grp[g].rpg;
+      if (p.grp[g].rpg < chunks && t > bt) {
+        bt = t;
+        best = g;
+      }
+    }
+    if (best < 0) break;
+    ++p.grp[best].rpg;
+  }
+  p.nctas = 0;
+  for (int g = 0; g < p.ngroups; ++g) {
+    GramGroup& G = p.grp[g];
+    G.per = ((N + G.rpg - 1) / G.rpg + kGMC - 1) / kGMC * kGMC;
+    G.cta0 = p.nctas;
+    p.nctas += G.rpg;
+  }
   p.gpart_doubles = static_cast<int64_t>(p.nctas) * kMW * 1024;
   p.cs_blocks = 4 * (num_sms > 0 ? num_sms : 148);
   if (p.cs_blocks > N) p.cs_blocks = static_cast<int>(N > 0 ? N : 1);
@@ -531,8 +601,6 @@ cudaError_t launch_gram(const GramPlan& p, const float* A, int64_t nA, const flo
   a.D = D;
   a.s = s;
   a.ngroups = p.ngroups;
-  a.rpg = p.rpg;
-  a.per = p.per;
   a.Gpart = Gpart;
   for (int g = 0; g < p.ngroups; ++g) a.grp[g] = p.grp[g];
   a.Cpart = Spart;

@@ -14,12 +14,15 @@ constexpr int kGramMaxGroups = 64;  // 8 diagonal + 2 x 28 off-diagonal 4x4-bloc
 struct GramGroup {
   unsigned char ntiles, nfb, nslot, rep;  // nslot: staged slots (power of 2 >= nfb); rep: warps per tile
   unsigned char fb[8];    // feature blocks (32 features each) staged in slots 0..nfb-1
-  unsigned char si[12];   // tile t = (fb[si[t]], fb[sj[t]])
+  unsigned char si[12];   // tile t = (fb[si[t]], fb[sj[t]]); si == sj: a diagonal tile (upper 8x8 blocks only)
   unsigned char sj[12];
+  int rpg, cta0;          // the group's point ranges (CTAs cta0 .. cta0 + rpg - 1)
+  int64_t per;            // points per range (multiple of 16)
+  int load;               // DMMAs per k-step on the busiest SM sub-partition (plan_gram's cost model)
 };
 struct GramPlan {
-  int ngroups = 0, rpg = 0, nctas = 0;
-  int64_t per = 0, gpart_doubles = 0, spart_doubles = 0;
+  int ngroups = 0, nctas = 0;
+  int64_t gpart_doubles = 0, spart_doubles = 0;
   int cs_blocks = 0;     // colsum_kernel CTAs (row ranges)
   int64_t cs_per = 0;    // rows per colsum CTA
   GramGroup grp[kGramMaxGroups];

@@ -1,6 +1,6 @@
+# K1 (diagonal-tile skip, load-balanced groups) and K3 (6 TMA boxes + 4 xl tiles) check:
+# parity of moments / selection / ProHD, K3 ring A/B, per-config timings
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_moments.py -x -q > gpurun_out/pytest_k1.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_k1.log
-timeout 300 python tools/time_prohd.py 5 4 3 2 > gpurun_out/time_k1.txt 2>&1
-for c in 5 3 2; do
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:"gram|colsum|shift|finalize|covariance" python tools/prof_prohd.py $c > gpurun_out/k1_launch_cfg$c.csv 2>&1
-done
+for r in 8 6 8 6; do PROHD_K3_RING=$r timeout 120 python tools/time_project.py >> gpurun_out/k3_ring.log 2>&1; echo "ring=$r" >> gpurun_out/k3_ring.log; done
+timeout 900 python -m pytest tests/test_gpu_moments.py tests/test_gpu_select.py tests/test_gpu_prohd.py -m gpu -q -x > gpurun_out/k1_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/k1_pytest.log
+timeout 600 python tools/report_configs.py 2 3 4 5 > gpurun_out/k1_configs.md 2> gpurun_out/k1_configs.err
