@@ -37,11 +37,12 @@
 // points, and the reduce kernel forms S_X = sum x - n_X s.
 // Three MMA warps per SM sub-partition keep the DMMA pipe fed through the fragment-load and
 // barrier gaps that left it 26% idle with two (the 8-warp, 2-CTA/SM version).
-// Buffer hand-off with named barriers: FULL[b] (loaders arrive, MMA warps sync) and
-// EMPTY[b] (MMA warps arrive, loaders sync). Every warp writes its own partial slot;
+// Buffer hand-off with mbarriers: full[b] (loader warps arrive, MMA warps wait) and
+// empty[b] (MMA warps arrive, loaders wait). Every warp writes its own partial slot;
 // gram_reduce_kernel sums the slots in a fixed order (deterministic, bit-identical runs).
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
+#include "sm100.cuh"
 
 
 namespace prohd {
@@ -76,12 +77,6 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void named_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
 }
@@ -94,7 +89,6 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// barrier ids: FULL[b] = 1 + b, EMPTY[b] = 1 + kGNB + b, loaders only = 1 + 2 kGNB
 template <bool kVec, int kRep>
 __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ GramArgs a) {
   extern __shared__ __align__(16) uint8_t gsm[];
@@ -110,6 +104,18 @@ __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ Gr
   const int nch = p1 > p0 ? static_cast<int>((p1 - p0 + kGMC - 1) / kGMC) : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rowf = 32 * G.nslot;  // staged floats per row
+  // full[b]: the 4 loader warps wrote buffer b; empty[b]: the 12 MMA warps have its fragments
+  // in registers. mbarriers rather than bar.sync: an MMA warp ahead of the others runs on
+  // into the next buffers instead of meeting them at every chunk.
+  __shared__ uint64_t full[kGNB], empty[kGNB];
+  if (tid == 0) {
+    for (int i = 0; i < kGNB; ++i) {
+      sm100::mbar_init(&full[i], kGT / 32 - kMW);
+      sm100::mbar_init(&empty[i], kMW);
+    }
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
 
   if (warp >= kMW) {
     // ------------------------------------------------------------------ loaders
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ Gr
       special = __any_sync(0xffffffffu, special);
       const int64_t q0 = p0 + static_cast<int64_t>(c) * kGMC;
       const int b = c % kGNB;
-      if (c >= kGNB) named_sync(1 + kGNB + b, kGT);  // MMA warps released buffer b
+      if (c >= kGNB) sm100::mbar_wait(&empty[b], ((c / kGNB) - 1) & 1);  // MMA warps released buffer b
       double* dst = tile + b * kGMC * kGLd + col;
 #pragma unroll
       for (int it = 0; it < kSlotsMax; ++it) {
@@ -214,9 +220,9 @@ __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ Gr
         d2[0] = make_double2(v[0], v[1]);
         d2[1] = make_double2(v[2], v[3]);
       }
-      named_arrive(1 + b, kGT);
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&full[b]);
     }
-    for (int c = (nch > kGNB ? nch - kGNB : 0); c < nch; ++c) named_sync(1 + kGNB + (c % kGNB), kGT);
     cp_wait<0>();
   } else {
     // ------------------------------------------------------------------ DMMA warps
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ Gr
       // fragments double-buffered in registers: the loads of the warp's next k-step (the next
       // chunk's first one after its FULL barrier) are issued before the 16 DMMAs of this one
       if (nch > 0) {
-        named_sync(1, kGT);
+        sm100::mbar_wait(&full[0], 0);
         ldfrag(tile + (ri * 4 + fk) * kGLd, af[0], bf[0]);
       }
       for (int c = 0; c < nch; ++c) {
@@ -276,20 +282,22 @@ __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ Gr
             ldfrag(tb + ((ri + kRep * (u + 1)) * 4 + fk) * kGLd, af[nxt], bf[nxt]);
           } else if (c + 1 < nch) {
             const int bn = (c + 1) % kGNB;
-            named_sync(1 + bn, kGT);
+            sm100::mbar_wait(&full[bn], ((c + 1) / kGNB) & 1);
             ldfrag(tile + bn * kGMC * kGLd + (ri * 4 + fk) * kGLd, af[nxt], bf[nxt]);
           }
           mma16(af[cur], bf[cur]);
         }
-        named_arrive(1 + kGNB + b, kGT);
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&empty[b]);
       }
     } else {
       for (int c = 0; c < nch; ++c) {
         const int b = c % kGNB;
-        named_sync(1 + b, kGT);
+        sm100::mbar_wait(&full[b], (c / kGNB) & 1);
         ldfrag(tile + b * kGMC * kGLd + (ri * 4 + fk) * kGLd, af[0], bf[0]);
         mma16(af[0], bf[0]);
-        named_arrive(1 + kGNB + b, kGT);
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&empty[b]);
       }
     }
     double* out = a.Gpart + (static_cast<int64_t>(blockIdx.x) * kMW + warp) * 1024;
