@@ -813,9 +813,30 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   s.nk1 = (a.D + kBK2 - 1) / kBK2;
   s.ks_last1 = ((a.D - (s.nk1 - 1) * kBK2) + 7) / 8;
   const int slots = a.num_sms / ctas_per_unit;  // concurrent units
-  // enough units to fill the machine twice when A is small (subset HD)
-  const int want = 2 * slots;
-  int nsplit = (want + s.nrb - 1) / s.nrb;
+  // Column splits: units (row block, column range) are dealt round-robin to the persistent
+  // CTAs, so the sweep takes ceil(units / slots) rounds of (tps + ~0.5) tile times (the half
+  // tile: a unit's pipeline fill / drain and row-minimum merge). Small A (subset HD: 100-250
+  // row blocks) needs splits to fill 148 SMs, and the split count decides the last round's
+  // occupancy: pick the cheapest of 1..64 splits (ties to fewer: fewer atomic merges).
+  int nsplit = 1;
+  {
+    const char* e = getenv("PROHD_K6_SPLITS");  // dev A/B: "2x" = the old fill-twice rule
+    if (e != nullptr && e[0] == '2') {
+      nsplit = (2 * slots + s.nrb - 1) / s.nrb;
+    } else {
+      double best = 0.0;
+      for (int ns = 1; ns <= 64 && ns <= s.nt; ++ns) {
+        const int tps = (s.nt + ns - 1) / ns;
+        const int nsa = (s.nt + tps - 1) / tps;
+        const int64_t u = static_cast<int64_t>(s.nrb) * nsa;
+        const double cost = static_cast<double>((u + slots - 1) / slots) * (tps + 0.5);
+        if (ns == 1 || cost < best * 0.995) {
+          best = cost;
+          nsplit = nsa;
+        }
+      }
+    }
+  }
   if (nsplit < 1) nsplit = 1;
   if (nsplit > s.nt) nsplit = s.nt;
   s.tps = (s.nt + nsplit - 1) / nsplit;
