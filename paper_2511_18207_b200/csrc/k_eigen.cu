@@ -13,13 +13,12 @@
 //      entry positive, lowest index on ties), rank drop
 //      (lambda <= D 2^-52 lambda_1).
 //
-// Layout: ONE thread-block cluster of 8 CTAs. The matrix is kept on chip: row r
-// lives in CTA r % 8 (cyclic, so every CTA keeps work as the trailing block
-// shrinks), <= 32 rows x 256 fp64 = 64 KB of shared memory per CTA. Each
-// Householder step needs three cluster barriers: (1) column norm partials,
-// (2) the Householder vector v, (3) p = 2 A v and v^T p; the vectors are
-// exchanged by direct stores into every CTA's shared memory (DSMEM).
-// Latency-bound: ~3 x (D-2) cluster barriers.
+// Layout: ONE thread-block cluster of 8 (16 for D > 160) CTAs. The matrix is kept on chip:
+// row r lives in CTA r % kCl (cyclic, so every CTA keeps work as the trailing block shrinks),
+// <= 32 rows x 256 fp64 = 64 KB of shared memory per CTA. Each Householder step exchanges
+// p = 2 A v, the pre-update next column and the v.p partials by direct stores into every
+// CTA's shared memory (DSMEM) and needs ONE cluster barrier; every CTA forms v and the
+// updated next column itself. Latency-bound: ~(D-2) cluster barriers.
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
 
@@ -186,47 +185,51 @@ __device__ void inverse_iteration(const double* d, const double* e, int D, doubl
   __syncwarp();
 }
 
-// Householder tridiagonalisation T = Q^T C Q on one 8-CTA cluster (Golub & Van Loan
-// 8.3.1). Row r of C lives in CTA r % 8 as a full row in shared memory (<= 32 rows x 256
-// fp64). Step j, with two cluster barriers:
-//   A. every CTA scatters its rows' column-j entries (r > j) into every CTA's colbuf
-//      (DSMEM stores); the owner of row j scatters d_j.               -> barrier A
-//   B. each CTA forms the norm, alpha and v = (x - alpha e1)/||.|| redundantly from the
-//      full column, computes p_r = 2 sum_c M[r][c] v_c for its rows (warp per row,
-//      lanes along the contiguous row) and scatters p_r and its v.p partial.  -> barrier B
-//   C. K = v.p, w = p - K v, and M[r][c] -= v_r w_c + w_r v_c on its own rows.
-// Writes d, e (de) and the Householder vectors (V rows 0 .. D-3).
+// Householder tridiagonalisation T = Q^T C Q on one cluster of kCl CTAs (Golub & Van Loan
+// 8.3.1). Row r of C lives in CTA r % kCl as a full row in shared memory. ONE cluster barrier
+// per step j (buffers double-buffered on j & 1):
+//   B. every CTA holds column j (rows >= j, d_j at index j) in colbuf; each warp forms the
+//      norm, alpha and v = (x - alpha e1)/||.|| from it, the CTA computes p_r = 2 sum_c
+//      M[r][c] v_c for its rows r > j and scatters p_r, the PRE-update entry M[r][j+1] and
+//      its v.p partial into every CTA.                                      -> cluster barrier
+//   C. K = v.p, w = p - K v, M[r][c] -= v_r w_c + w_r v_c on its own rows, and every CTA
+//      forms the whole updated column j+1 itself, M[r][j+1] - (v_r w_{j+1} + w_r v_{j+1})
+//      (the same expression, so bit-identical to the owner's row), as step j+1's colbuf.
+// The second barrier of a scatter-the-updated-column scheme is gone; the scatter volume is the
+// same. Writes d, e (de) and the Householder vectors (V rows 0 .. D-3).
 template <int kCl>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduce_cluster_kernel(EigArgs a) {
   constexpr int kRows = kMaxD / kCl;  // rows per CTA (max)
     cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
   extern __shared__ double dyn[];
-  double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/8)*D])
-  __shared__ double colbuf2[2][kMaxD], pbuf[kMaxD];  // colbuf double-buffered: step j uses [j & 1]
-  __shared__ double vbuf[kMaxD], wbuf[kMaxD];        // v and w = p - K v of the current step
-  __shared__ double vpart[kCl * kWarps];
-  __shared__ double s_d;
+  double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/kCl)*D])
+  __shared__ double colbuf2[2][kMaxD];                 // column j (rows >= j) of step j: [j & 1]
+  __shared__ double pbuf2[2][kMaxD], cpre2[2][kMaxD];  // scattered p_r and pre-update M[r][j+1]
+  __shared__ double vbuf[kMaxD], wbuf[kMaxD];          // v and w = p - K v of the current step
+  __shared__ double vpart2[2][kCl * kWarps];
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nloc = (D - rank + kCl - 1) / kCl;  // rows r = rank + 8*i, i < nloc
+  const int nloc = (D - rank + kCl - 1) / kCl;  // rows r = rank + kCl*i, i < nloc
   for (int t = tid; t < nloc * D; t += kT) {
     const int i = t / D, c = t % D;
     M[i * D + c] = a.C[static_cast<int64_t>(rank + kCl * i) * D + c];
   }
   __syncthreads();
+  // column 0 (with d_0 at index 0) into every CTA
+  {
+    const int i = tid / kCl, q = tid % kCl;  // own row slot i, target CTA q
+    if (i < nloc) *cl.map_shared_rank(&colbuf2[0][rank + kCl * i], q) = M[i * D];
+  }
+  cl.sync();
   double* dg = a.de;
   double* eg = a.de + kMaxD;
   for (int j = 0; j + 2 < D; ++j) {
-    double* colbuf = colbuf2[j & 1];  // step j+1 may scatter while a slow CTA still reads step j's
-    // A. scatter column j (rows > j) and d_j into every CTA
-    {
-      const int i = tid / kCl, q = tid % kCl;  // own row slot i, target CTA q
-      const int r = rank + kCl * i;
-      if (i < nloc && r > j) *cl.map_shared_rank(&colbuf[r], q) = M[i * D + j];
-      if (j % kCl == rank && tid < kCl) *cl.map_shared_rank(&s_d, tid) = M[(j / kCl) * D + j];
-    }
-    cl.sync();
+    const int b = j & 1;
+    const double* colbuf = colbuf2[b];
+    double* pbuf = pbuf2[b];
+    double* cpre = cpre2[b];
+    double* vpart = vpart2[b];
     // B. every warp forms ||x||, alpha and the scale itself (no CTA barrier); v_c is
     // recomputed on the fly as vc(c) = (c == j+1 ? x0 - alpha : colbuf[c]) * sc
     double ss = 0.0;
@@ -237,25 +240,23 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
     const double alpha = (x0 > 0.0) ? -nrm : nrm;
     const double v0 = x0 - alpha;
     const double vn2 = nrm2 - x0 * x0 + v0 * v0;
+    // sc == 0: the column is already zero below the subdiagonal, H = I (v = 0, p = 0, K = 0:
+    // the update below is then a no-op and the next column comes out unchanged)
     const double sc = (vn2 > 0.0 && nrm > 0.0) ? 1.0 / sqrt(vn2) : 0.0;
     auto vc = [&](int c) { return (c == j + 1 ? v0 : colbuf[c]) * sc; };
     if (rank == 0) {
       if (tid == 0) {
-        dg[j] = s_d;
+        dg[j] = colbuf[j];
         eg[j] = (sc != 0.0) ? alpha : 0.0;
       }
       for (int c = j + 1 + tid; c < D; c += kT) a.V[static_cast<int64_t>(j) * D + c] = vc(c);
-    }
-    if (sc == 0.0) {  // column already zero below the subdiagonal: H = I (uniform decision)
-      cl.sync();      // everyone is done reading colbuf before step j+1 scatters into it
-      continue;
     }
     // v once per CTA in shared memory (every warp formed the same scalars)
     for (int c = j + 1 + tid; c < D; c += kT) vbuf[c] = vc(c);
     __syncthreads();
     // p_r = 2 M[r][j+1:] . v for own rows r > j (warp per row, <= 4 rows per warp, the row
     // dot products formed together and reduced together); v.p partial per warp
-    constexpr int kRW = kRows / kWarps;  // rows per warp (4)
+    constexpr int kRW = kRows / kWarps;  // rows per warp
     double ps[kRW];
 #pragma unroll
     for (int q = 0; q < kRW; ++q) {
@@ -279,13 +280,17 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
       const int r = rank + kCl * i;
       if (i < nloc && r > j) {
         const double pr = 2.0 * ps[q];
-        if (lane < kCl) *cl.map_shared_rank(&pbuf[r], lane) = pr;
+        if (lane < kCl) {
+          *cl.map_shared_rank(&pbuf[r], lane) = pr;
+          *cl.map_shared_rank(&cpre[r], lane) = M[i * D + j + 1];
+        }
         vp += pr * vbuf[r];
       }
     }
     if (lane < kCl) *cl.map_shared_rank(&vpart[rank * kWarps + warp], lane) = vp;
     cl.sync();
-    // C. K = v.p; w = p - K v once per CTA; M[r][c] -= v_r w_c + w_r v_c on own rows
+    // C. K = v.p; w = p - K v once per CTA; M[r][c] -= v_r w_c + w_r v_c on own rows; the
+    // updated column j+1 (rows >= j+1) into the other colbuf
     double K = 0.0;
     for (int q = lane; q < kCl * kWarps; q += 32) K += vpart[q];
     K = warp_sum(K);
@@ -299,6 +304,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
       double* row = M + i * D;
       const double vr = vbuf[r], wr = wbuf[r];
       for (int c = j + 1 + lane; c < D; c += 32) row[c] -= fma(vr, wbuf[c], wr * vbuf[c]);
+    }
+    {
+      double* nxt = colbuf2[b ^ 1];
+      const double vj = vbuf[j + 1], wj = wbuf[j + 1];
+      for (int r = j + 1 + tid; r < D; r += kT) nxt[r] = cpre[r] - fma(vbuf[r], wj, wbuf[r] * vj);
     }
     __syncthreads();
   }
