@@ -67,7 +67,10 @@ struct GramArgs {
   const double* s;
   int ngroups;
   double* Gpart;    // [cta][kMW warps][32][32]
-  const double* Cpart;  // colsum_kernel partials [cs_blocks][2 sets][D]
+  int ngram;        // Gram CTAs; CTAs ngram .. ngram + cs_ctas - 1 take the column sums
+  int cs_ctas;
+  int64_t cs_per;   // rows per column-sum CTA
+  double* Cpart;        // column-sum partials [cs_blocks][2 sets][D]
   int cs_blocks;
   GramGroup grp[kGramMaxGroups];
 };
@@ -89,9 +92,100 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Column sums inside the Gram launch (D % 4 == 0): the last cs_ctas CTAs (one per SM, like
+// the Gram CTAs) each stream a contiguous row range of A u B through shared memory with 1-D
+// bulk copies (kCsBuf x 64 KB in flight; a chunk never straddles the A/B boundary) and add
+// it up in fp64 on their own SMs' fp64 pipes, concurrently with the DMMA-bound Gram CTAs.
+// Thread t sums column t % D over rows t / D, t / D + H, ... (H = 512 / D row phases);
+// partial slot (q H + h) of Cpart, combined in a fixed order by gram_reduce_kernel.
+constexpr int kCsBuf = 3;
+constexpr uint32_t kCsBytes = 65536;
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sm100::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(sm100::smem_u32(bar))
+               : "memory");
+}
+__device__ __noinline__ void colsum_role(const GramArgs& a, uint8_t* gsm) {
+  __shared__ uint64_t cbar[kCsBuf];
+  const int tid = threadIdx.x;
+  const int D = a.D;
+  const int q = blockIdx.x - a.ngram;
+  const int64_t N = a.nA + a.nB;
+  const int64_t r0 = static_cast<int64_t>(q) * a.cs_per;
+  const int64_t r1 = r0 + a.cs_per < N ? r0 + a.cs_per : N;
+  const int64_t rpc = kCsBytes / (4 * D);  // rows per chunk
+  // chunk k of this range: rows [c0, c1), cut at nA
+  auto chunk = [&](int64_t& c0, int64_t& c1, int64_t at) {
+    c0 = at;
+    c1 = c0 + rpc < r1 ? c0 + rpc : r1;
+    if (c0 < a.nA && c1 > a.nA) c1 = a.nA;
+  };
+  if (tid == 0) {
+    for (int i = 0; i < kCsBuf; ++i) sm100::mbar_init(&cbar[i], 1);
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
+  const int H = kGT / D > 0 ? kGT / D : 1;
+  const int c = tid % D, h = tid / D;
+  const bool act = D <= kGT ? h < H : true;
+  double sa = 0.0, sb = 0.0;
+  // thread 0 keeps the ring full: chunk starts are sequential, so it walks them itself
+  int64_t next = r0;
+  auto issue = [&](int buf) {
+    if (next >= r1) return;
+    int64_t c0, c1;
+    chunk(c0, c1, next);
+    const float* src = c0 < a.nA ? a.A + c0 * D : a.B + (c0 - a.nA) * D;
+    const uint32_t bytes = static_cast<uint32_t>((c1 - c0) * D * 4);
+    sm100::mbar_arrive_expect_tx(&cbar[buf], bytes);
+    bulk_g2s(gsm + static_cast<size_t>(buf) * kCsBytes, src, bytes, &cbar[buf]);
+    next = c1;
+  };
+  if (tid == 0)
+    for (int i = 0; i < kCsBuf; ++i) issue(i);
+  int64_t at = r0;
+  for (int k = 0; at < r1; ++k) {
+    int64_t c0, c1;
+    chunk(c0, c1, at);
+    const int buf = k % kCsBuf;
+    sm100::mbar_wait(&cbar[buf], (k / kCsBuf) & 1);
+    const float* x = reinterpret_cast<const float*>(gsm + static_cast<size_t>(buf) * kCsBytes);
+    const int rows = static_cast<int>(c1 - c0);
+    double s = 0.0;
+    if (act && c < D) {
+      // 4 independent chains (fp64 add latency), combined in a fixed order
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      int rr = h;
+      for (; rr + 3 * H < rows; rr += 4 * H) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s4[u] += static_cast<double>(x[(rr + u * H) * D + c]);
+      }
+      for (; rr < rows; rr += H) s4[0] += static_cast<double>(x[rr * D + c]);
+      s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
+    if (c0 < a.nA)
+      sa += s;
+    else
+      sb += s;
+    __syncthreads();  // everyone is done with buf
+    if (tid == 0) issue(buf);
+    at = c1;
+  }
+  if (act && c < D) {
+    double* cp = a.Cpart + static_cast<int64_t>(q * H + h) * 2 * D;
+    cp[c] = sa;
+    cp[D + c] = sb;
+  }
+}
+
 template <bool kVec, int kRep>
 __global__ void __launch_bounds__(kGT, 1) gram_kernel(const __grid_constant__ GramArgs a) {
   extern __shared__ __align__(16) uint8_t gsm[];
+  if (static_cast<int>(blockIdx.x) >= a.ngram) {
+    colsum_role(a, gsm);
+    return;
+  }
   float* stage = reinterpret_cast<float*>(gsm);                                  // [kGNS][kGMC][32 nslot]
   double* tile = reinterpret_cast<double*>(gsm + sizeof(float) * kGNS * kGStageF);  // [kGNB][kGMC][kGLd]
   int g = 0;
@@ -554,7 +648,19 @@ bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p) {
   // remaining time per range first), and every group cuts A u B into its own rpg ranges.
   const int64_t N = nA + nB;
   const int64_t chunks = N > 0 ? (N + kGMC - 1) / kGMC : 1;
-  const int budget = num_sms > 0 ? num_sms : 148;
+  // Column sums in the same launch on cs_ctas SMs of their own when the Gram is slow enough per
+  // byte to hide them: a column-sum SM streams ~66 GB/s (measured), so 7 of them match the
+  // DMMA-bound Gram on the other 141 at D = 256 (cfg5 moments 9.27 -> 8.91 ms; 8: 9.11, 6: 10.19)
+  // but not at D = 128, where the Gram costs half as much per byte (cfg3 0.80 -> 1.36 ms). D >= 224,
+  // D % 4 == 0, enough rows; PROHD_K1_CS_SMS overrides the count (0 = the colsum_kernel pass).
+  p.cs_ctas = 0;
+  {
+    int cs = D >= 224 ? 7 : 0;
+    if (const char* e = getenv("PROHD_K1_CS_SMS")) cs = atoi(e);
+    const int sms = num_sms > 0 ? num_sms : 148;
+    if (cs > 0 && D % 4 == 0 && D <= kGT && N >= static_cast<int64_t>(64) * sms && cs < sms / 2) p.cs_ctas = cs;
+  }
+  const int budget = (num_sms > 0 ? num_sms : 148) - p.cs_ctas;
   for (int g = 0; g < p.ngroups; ++g) {
     GramGroup& G = p.grp[g];
     int sp[4] = {0, 0, 0, 0};
@@ -591,9 +697,15 @@ bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p) {
     p.nctas += G.rpg;
   }
   p.gpart_doubles = static_cast<int64_t>(p.nctas) * kMW * 1024;
-  p.cs_blocks = 4 * (num_sms > 0 ? num_sms : 148);
-  if (p.cs_blocks > N) p.cs_blocks = static_cast<int>(N > 0 ? N : 1);
-  p.cs_per = (N + p.cs_blocks - 1) / p.cs_blocks;
+  if (p.cs_ctas > 0) {
+    const int H = kGT / D > 0 ? kGT / D : 1;
+    p.cs_per = (N + p.cs_ctas - 1) / p.cs_ctas;
+    p.cs_blocks = p.cs_ctas * H;
+  } else {
+    p.cs_blocks = 4 * (num_sms > 0 ? num_sms : 148);
+    if (p.cs_blocks > N) p.cs_blocks = static_cast<int>(N > 0 ? N : 1);
+    p.cs_per = (N + p.cs_blocks - 1) / p.cs_blocks;
+  }
   p.spart_doubles = static_cast<int64_t>(p.cs_blocks) * 2 * D;
   return true;
 }
@@ -613,6 +725,9 @@ cudaError_t launch_gram(const GramPlan& p, const float* A, int64_t nA, const flo
   for (int g = 0; g < p.ngroups; ++g) a.grp[g] = p.grp[g];
   a.Cpart = Spart;
   a.cs_blocks = p.cs_blocks;
+  a.ngram = p.nctas;
+  a.cs_ctas = p.cs_ctas;
+  a.cs_per = p.cs_per;
   const bool vec = (D % 4) == 0;
   const int rep = p.grp[0].rep;
   auto kern = vec ? (rep == 4 ? gram_kernel<true, 4> : rep == 2 ? gram_kernel<true, 2> : gram_kernel<true, 1>)
@@ -621,13 +736,15 @@ cudaError_t launch_gram(const GramPlan& p, const float* A, int64_t nA, const flo
   if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGSmem))) !=
       cudaSuccess)
     return e;
+  if (p.cs_ctas == 0) {
+    count_launch();
+    if (vec)
+      colsum_kernel<4><<<p.cs_blocks, 256, 0, st>>>(A, nA, B, nB, D, p.cs_per, Spart);
+    else
+      colsum_kernel<1><<<p.cs_blocks, 256, 0, st>>>(A, nA, B, nB, D, p.cs_per, Spart);
+  }
   count_launch();
-  if (vec)
-    colsum_kernel<4><<<p.cs_blocks, 256, 0, st>>>(A, nA, B, nB, D, p.cs_per, Spart);
-  else
-    colsum_kernel<1><<<p.cs_blocks, 256, 0, st>>>(A, nA, B, nB, D, p.cs_per, Spart);
-  count_launch();
-  kern<<<p.nctas, kGT, kGSmem, st>>>(a);
+  kern<<<p.nctas + p.cs_ctas, kGT, kGSmem, st>>>(a);
   count_launch();
   gram_reduce_kernel<<<p.ngroups * kMW * 32 + (D + 31) / 32, 256, 0, st>>>(a, Gout, SA, SB);
   return cudaGetLastError();

@@ -23,8 +23,9 @@ struct GramGroup {
 struct GramPlan {
   int ngroups = 0, nctas = 0;
   int64_t gpart_doubles = 0, spart_doubles = 0;
-  int cs_blocks = 0;     // colsum_kernel CTAs (row ranges)
+  int cs_blocks = 0;     // column-sum partial slots (colsum_kernel CTAs, or in-launch CTAs x row phases)
   int64_t cs_per = 0;    // rows per colsum CTA
+  int cs_ctas = 0;       // > 0: the Gram launch carries this many column-sum CTAs after its nctas
   GramGroup grp[kGramMaxGroups];
 };
 bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p);
