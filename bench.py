@@ -150,6 +150,13 @@ def _oracle_seconds_per_row(A, B, rows_all) -> float:
     return max((time.perf_counter() - t0) / 256, 1e-6)
 
 
+def workload_config(c, world: int) -> dict:
+    """The `config` both arms report (same workload string and keys)."""
+    return {"workload": f"cfg{c.cfg} {c.name}: nA=nB={c.n}, D={c.D}, k={c.k}, m={c.m()} (prohd_estimate + "
+                        f"directed_hd per step)",
+            "nA": c.n, "nB": c.n, "D": c.D, "k": c.k, "m": c.m(), "parallelism": f"rows-of-A x{world}"}
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args, rank: int, world: int):
     if rank != 0:
@@ -178,8 +185,8 @@ def run_reference(args, rank: int, world: int):
            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen cfg%d, seed 0)" % args.config,
            "impl": "reference",
-           "config": {"workload": f"cfg{c.cfg} {c.name} n={c.n} D={c.D} k={c.k} m={c.m()}", "nA": c.n, "nB": c.n,
-                      "D": c.D, "sample_rows_per_step": nrows},
+           "config": dict(workload_config(c, world), parallelism="host cores (oracle)",
+                          sample_rows_per_step=nrows),
            "cpu_baseline": {"value": value, "unit": "Gpair/s", "cores": int(threads), "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": value, "unit": "Gpair/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -356,10 +363,8 @@ def run_ours(args, rank: int, world: int):
         "metric": METRIC, "value": value, "unit": "Gpair/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": f"synthetic (datagen cfg{args.config}, seed 0)",
-        "config": {"workload": f"cfg{c.cfg} {c.name}: nA=nB={n}, D={D}, k={k}, m={m} (prohd_estimate + "
-                               f"directed_hd per step)",
-                   "nA": n, "nB": n, "D": D, "k": k, "m": m, "parallelism": f"rows-of-A x{world}",
-                   "l2": "inputs larger than L2 (2 x %.1f GB), no flush" % (Ah.nbytes / 1e9)},
+        "config": dict(workload_config(c, world),
+                       l2="inputs larger than L2 (2 x %.1f GB), no flush" % (Ah.nbytes / 1e9)),
         "prohd_ms": statistics.mean(prohd_ms), "exact_ms": statistics.mean(exact_ms),
         "prohd": {"value": est["value"], "size_a": est["size_a"], "size_b": est["size_b"],
                   "n_dirs": est["n_dirs"], "phases_ms": {kk: est_t[kk] for kk in
