@@ -79,6 +79,24 @@ __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
                : "memory");
 }
 
+// warp-wide MMA issue: every lane runs the issuer loop (so descriptors and addresses stay
+// warp-uniform and can live in uniform registers); elect.sync picks the one lane that issues
+__device__ __forceinline__ void mma_tf32_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          sm100::smem_u32(bar))
+      : "memory");
+}
+
 __global__ void __launch_bounds__(kPThreads, 1)
     project_tc_kernel(const __grid_constant__ CUtensorMap tX, int64_t n, int D, const float* __restrict__ U32, int L,
                       float* __restrict__ P32, unsigned* maxnorm2) {
@@ -153,8 +171,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
+    {
+      // ------------------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
       constexpr uint32_t id64 = idesc_p(128, 64), id32 = idesc_p(128, 32);
       const uint32_t u0 = smem_u32(ubase);
       int stage = 0;
@@ -175,18 +193,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t off = static_cast<uint32_t>(kk * 32);  // 8 tf32 along K
             const uint32_t accum = (c | kk) != 0 ? 1u : 0u;
-            mma_tf32(d, smem_desc_k_sw128(xh + off), smem_desc_k_sw128(ub + off), id64, accum);       // xh.[uh;ul]
-            mma_tf32(d + 64, smem_desc_k_sw128(xl + off), smem_desc_k_sw128(ub + off), id32, accum);  // xl.uh
+            mma_tf32_w(d, smem_desc_k_sw128(xh + off), smem_desc_k_sw128(ub + off), id64, accum);       // xh.[uh;ul]
+            mma_tf32_w(d + 64, smem_desc_k_sw128(xl + off), smem_desc_k_sw128(ub + off), id32, accum);  // xl.uh
           }
-          mma_commit(&empty[stage]);
-          mma_commit(&loempty[lslot]);
+          mma_commit_w(&empty[stage]);
+          mma_commit_w(&loempty[lslot]);
           lslot = lslot + 1 == kLoSlots ? 0 : lslot + 1;
           if (++stage == kStagesP) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        mma_commit(&tfull[acc]);
+        mma_commit_w(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) aphase ^= 1u;
       }
