@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
+    {
+      // ------------------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
       constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
       constexpr uint32_t idesc16 = idesc_bf16(kBM, kBN);
       int stage = 0;
@@ -187,21 +187,21 @@ __global__ void __launch_bounds__(kThreads1, 1)
               const uint64_t dal = smem_desc_k_sw128(al + off);
               const uint64_t dbh = smem_desc_k_sw128(bh + off);
               const uint64_t dbl = smem_desc_k_sw128(bl + off);
-              mma_tf32(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
+              mma_tf32_w(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
               if (s.split3) {
-                mma_tf32(d, dah, dbl, idesc, 1u);  // hi_a . lo_b
-                mma_tf32(d, dal, dbh, idesc, 1u);  // lo_a . hi_b
+                mma_tf32_w(d, dah, dbl, idesc, 1u);  // hi_a . lo_b
+                mma_tf32_w(d, dal, dbh, idesc, 1u);  // lo_a . hi_b
               } else {
-                mma_bf16(d, dal, dbl, idesc16, 1u);  // [hi lo]_a . [lo hi]_b
+                mma_bf16_w(d, dal, dbl, idesc16, 1u);  // [hi lo]_a . [lo hi]_b
               }
             }
-            mma_commit(&empty[stage]);
+            mma_commit_w(&empty[stage]);
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
             }
           }
-          mma_commit(&tfull[acc]);
+          mma_commit_w(&tfull[acc]);
           acc ^= 1;
           if (acc == 0) aphase ^= 1u;
         }
@@ -613,8 +613,8 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
+    {
+      // ------------------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
       constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
       constexpr uint32_t idesc16 = idesc_bf16(kBM, kBN);
       int stage = 0;
@@ -644,26 +644,26 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
               if (!s.split3) {
                 // issue order matters for power: alternating kinds per accumulator ran at a 1490 MHz
                 // median clock in the power-capped benchmark, both TF32 MMAs first at 1035 MHz
-                mma_tf32(d0, da1h, dbh, idesc, acc);
-                mma_bf16(d0, da1l, dbl, idesc16, 1u);
-                mma_tf32(d1, da2h, dbh, idesc, acc);
-                mma_bf16(d1, da2l, dbl, idesc16, 1u);
+                mma_tf32_w(d0, da1h, dbh, idesc, acc);
+                mma_bf16_w(d0, da1l, dbl, idesc16, 1u);
+                mma_tf32_w(d1, da2h, dbh, idesc, acc);
+                mma_bf16_w(d1, da2l, dbl, idesc16, 1u);
               } else {
-                mma_tf32(d0, da1h, dbh, idesc, acc);
-                mma_tf32(d0, da1h, dbl, idesc, 1u);
-                mma_tf32(d0, da1l, dbh, idesc, 1u);
-                mma_tf32(d1, da2h, dbh, idesc, acc);
-                mma_tf32(d1, da2h, dbl, idesc, 1u);
-                mma_tf32(d1, da2l, dbh, idesc, 1u);
+                mma_tf32_w(d0, da1h, dbh, idesc, acc);
+                mma_tf32_w(d0, da1h, dbl, idesc, 1u);
+                mma_tf32_w(d0, da1l, dbh, idesc, 1u);
+                mma_tf32_w(d1, da2h, dbh, idesc, acc);
+                mma_tf32_w(d1, da2h, dbl, idesc, 1u);
+                mma_tf32_w(d1, da2l, dbh, idesc, 1u);
               }
             }
-            mma_commit(&empty[stage]);
+            mma_commit_w(&empty[stage]);
             if (++stage == kStagesA2) {
               stage = 0;
               phase ^= 1u;
             }
           }
-          mma_commit(&tfull[0]);
+          mma_commit_w(&tfull[0]);
           tph ^= 1u;
         }
       }

@@ -79,24 +79,6 @@ __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
                : "memory");
 }
 
-// warp-wide MMA issue: every lane runs the issuer loop (so descriptors and addresses stay
-// warp-uniform and can live in uniform registers); elect.sync picks the one lane that issues
-__device__ __forceinline__ void mma_tf32_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-          sm100::smem_u32(bar))
-      : "memory");
-}
-
 __global__ void __launch_bounds__(kPThreads, 1)
     project_tc_kernel(const __grid_constant__ CUtensorMap tX, int64_t n, int D, const float* __restrict__ U32, int L,
                       float* __restrict__ P32, unsigned* maxnorm2) {
