@@ -80,7 +80,7 @@ __device__ __forceinline__ void warp_colmin32(float (&v)[32], int lane) {
 // colmin[j] = min_i ||a_i - b_j||^2 (the B->A direction). Per 32-column chunk each warp
 // reduces its 32 rows with a butterfly reduce-scatter, the 4 warps combine in shared
 // memory, and the last warp of the tile flushes the 256 minima with global atomicMin.
-template <bool kBidir>
+template <bool kBidir, bool kElect>
 __global__ void __launch_bounds__(kThreads1, 1)
     dist_rowmin_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                        const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
@@ -157,8 +157,19 @@ __global__ void __launch_bounds__(kThreads1, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    {
-      // ------------------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
+    // kElect: warp-wide issue with an elected lane (sm100.cuh mma_*_w); else lane 0 issues
+    // (measured faster for the fused bidirectional sweep at D = 128, §7.1)
+    auto mtf32 = [](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t ac) {
+      if constexpr (kElect) mma_tf32_w(d, a, b, id, ac); else mma_tf32(d, a, b, id, ac);
+    };
+    auto mbf16 = [](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t ac) {
+      if constexpr (kElect) mma_bf16_w(d, a, b, id, ac); else mma_bf16(d, a, b, id, ac);
+    };
+    auto mcommit = [](uint64_t* bar) {
+      if constexpr (kElect) mma_commit_w(bar); else mma_commit(bar);
+    };
+    if (kElect || lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
       constexpr uint32_t idesc16 = idesc_bf16(kBM, kBN);
       int stage = 0;
@@ -187,21 +198,21 @@ __global__ void __launch_bounds__(kThreads1, 1)
               const uint64_t dal = smem_desc_k_sw128(al + off);
               const uint64_t dbh = smem_desc_k_sw128(bh + off);
               const uint64_t dbl = smem_desc_k_sw128(bl + off);
-              mma_tf32_w(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
+              mtf32(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
               if (s.split3) {
-                mma_tf32_w(d, dah, dbl, idesc, 1u);  // hi_a . lo_b
-                mma_tf32_w(d, dal, dbh, idesc, 1u);  // lo_a . hi_b
+                mtf32(d, dah, dbl, idesc, 1u);  // hi_a . lo_b
+                mtf32(d, dal, dbh, idesc, 1u);  // lo_a . hi_b
               } else {
-                mma_bf16_w(d, dal, dbl, idesc16, 1u);  // [hi lo]_a . [lo hi]_b
+                mbf16(d, dal, dbl, idesc16, 1u);  // [hi lo]_a . [lo hi]_b
               }
             }
-            mma_commit_w(&empty[stage]);
+            mcommit(&empty[stage]);
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1u;
             }
           }
-          mma_commit_w(&tfull[acc]);
+          mcommit(&tfull[acc]);
           acc ^= 1;
           if (acc == 0) aphase ^= 1u;
         }
@@ -873,21 +884,22 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   if (a.colmin != nullptr) {
     cudaError_t e = cudaMemsetAsync(a.colmin, 0x7F, sizeof(float) * a.nB, st);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(dist_rowmin_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSmemBytes));
+    // lane-0 MMA issue below D = 192 (D = 128 undirected cfg3: 255 -> 243 ms), elected above
+    auto kern = a.D < 192 ? dist_rowmin_kernel<true, false> : dist_rowmin_kernel<true, true>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     if (e != cudaSuccess) return e;
     count_launch();
-    dist_rowmin_kernel<true><<<nunits, kThreads1, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
-                                                                    a.na, a.nb, a.rowmin, a.colmin);
+    kern<<<nunits, kThreads1, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na, a.nb, a.rowmin,
+                                                a.colmin);
     return cudaGetLastError();
   }
   {
-    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kSmemBytes));
     if (e != cudaSuccess) return e;
   }
   count_launch();
-  dist_rowmin_kernel<false><<<nunits, kThreads1, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
+  dist_rowmin_kernel<false, true><<<nunits, kThreads1, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
                                                                    a.na, a.nb, a.rowmin, nullptr);
   return cudaGetLastError();
 }
