@@ -124,9 +124,27 @@ def k6_traffic_per_pair(D: int):
     return e["dram_bytes"] / e["pairs"], e["source"]
 
 
-def cpu_baseline(A, B, budget_s: float = 15.0) -> dict:
-    """The fp64 oracle's exact-HD row minima on a bounded row sample, host cores."""
+def host_info() -> dict:
+    """CPU model, sockets and logical cores of the box the oracle runs on."""
+    model, sockets = None, set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name") and model is None:
+                    model = ln.split(":", 1)[1].strip()
+                elif ln.startswith("physical id"):
+                    sockets.add(ln.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    return {"cpu_model": model, "sockets": max(1, len(sockets)), "logical_cores": os.cpu_count()}
+
+
+def cpu_baseline(A, B, k: int, m: int, budget_s: float = 15.0, prohd: bool = True) -> dict:
+    """The fp64 oracle on the host cores: exact-HD row minima on a bounded row
+    sample (value = its pair rate, plus the extrapolated full directed time) and, unless disabled,
+    ProHD O1-O9 end to end on the full sets."""
     import oracle
+    from oracle import prohd as OP
     rows_all = datagen.sample_rows(A.shape[0], 4096, seed=7)
     per_row = _oracle_seconds_per_row(A, B, rows_all)
     nrows = int(max(8, min(4096, budget_s / per_row)))
@@ -136,10 +154,19 @@ def cpu_baseline(A, B, budget_s: float = 15.0) -> dict:
     dt = time.perf_counter() - t0
     pairs = nrows * B.shape[0]
     threads = os.environ.get("OMP_NUM_THREADS") or os.environ.get("OPENBLAS_NUM_THREADS") or str(os.cpu_count())
-    return {"value": pairs / dt / 1e9, "unit": "Gpair/s", "cores": int(threads), "kind": "oracle",
-            "sample": f"exact-HD row minima (fp64, oracle/hausdorff.py) of {nrows} seeded rows of A against "
-                      f"all {B.shape[0]} rows of B: {pairs:.3e} pairs in {dt:.1f} s",
-            "seconds": dt}
+    out = {"value": pairs / dt / 1e9, "unit": "Gpair/s", "cores": int(threads), "kind": "oracle",
+           "sample": f"exact-HD row minima (fp64, oracle/hausdorff.py) of {nrows} seeded rows of A against "
+                     f"all {B.shape[0]} rows of B: {pairs:.3e} pairs in {dt:.1f} s",
+           "seconds": dt, **host_info(),
+           "exact_directed_s_extrapolated": dt / nrows * A.shape[0],
+           "exact_extrapolation": f"measured seconds x nA / {nrows} rows (extrapolated, not run)"}
+    if prohd:
+        t0 = time.perf_counter()
+        r = OP.estimate(A, B, k, m)
+        out["prohd_s"] = time.perf_counter() - t0
+        out["prohd_value"] = r["value"]
+        out["prohd_sample"] = "ProHD O1-O9 (oracle/prohd.py estimate) end to end on the full sets, excluding generation"
+    return out
 
 
 def _oracle_seconds_per_row(A, B, rows_all) -> float:
@@ -148,6 +175,46 @@ def _oracle_seconds_per_row(A, B, rows_all) -> float:
     t0 = time.perf_counter()
     oracle.row_minima(A, B, rows=rows_all[:256])
     return max((time.perf_counter() - t0) / 256, 1e-6)
+
+
+def phase_rooflines(c, t_est: dict, t_ex: dict, est: dict, pk: dict) -> dict:
+    """Per-kernel (phase) roofline fractions from the library's CUDA events:
+    achieved = ALGORITHMIC bytes or flops of the phase (§8(d4)) / its measured time."""
+    n, D, L = c.n, c.D, c.k + 1
+    N = 2 * n  # points of A u B
+    hbm = pk["hbm_gbs"]
+    bf16 = pk["bf16_tflops"]
+    tf32 = bf16 * NOMINAL_TF32_OVER_BF16
+    out = {}
+
+    def hb(name, nbytes, ms, what):
+        gbs = nbytes / (ms / 1e3) / 1e9 if ms and ms > 0 else None
+        out[name] = {"bound": "hbm", "ms": ms, "bytes": nbytes, "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                     "frac": gbs / hbm if gbs else None, "what": what}
+
+    mom = t_est.get("moments_ms")
+    gram_flops = 2.0 * N * D * D
+    out["K1_moments"] = {"bound": "tensor", "ms": mom, "flops": gram_flops,
+                         "achieved": gram_flops / (mom / 1e3) / 1e12 if mom else None, "unit": "TFLOP/s",
+                         "peak": tf32, "frac": (gram_flops / (mom / 1e3) / 1e12) / tf32 if mom else None,
+                         "hbm_frac": (N * D * 4 / (mom / 1e3) / 1e9) / hbm if mom else None,
+                         "what": "useful Gram flops 2 (nA+nB) D^2 against the TF32 tensor peak (SURVEY §8(d3)); "
+                                 "hbm_frac: one read of A u B (4D B per point) over the phase time"}
+    hb("K3K4K5_select", N * (D * 4 + 2 * L * 4), t_est.get("select_ms"),
+       "per point: read 4D B (projection), write 4(k+1) B, read 4(k+1) B (selection): the one-pass floor")
+    out["K2_eigen"] = {"bound": "latency", "ms": t_est.get("eigen_ms")}
+    sub_ms = t_est.get("subset_ms")
+    sp = float(est["size_a"]) * float(est["size_b"])
+    out["K6_subset"] = {"bound": "tensor", "ms": sub_ms, "pairs": sp,
+                        "note": "fused bidirectional sweep over |I_A| x |I_B| pairs (both directions) plus K0/K7"}
+    hb("K0_prep_exact", N * (12 * D + 4), t_ex.get("prep_ms"),
+       "K0 of the exact call: read 4D B, write hi 4D + pairs 8D... (12D + 4 B per point of A and B)")
+    floor_ms = 2 * N * D * 4 / (hbm * 1e9) * 1e3
+    tot = t_est.get("total_ms")
+    out["prohd"] = {"ms": tot, "floor_ms": floor_ms, "frac": floor_ms / tot if tot else None,
+                    "floor": "two HBM reads of A u B (moments, projection) at the measured HBM peak; the Gram, "
+                             "eigen-solve and subset HD are not in it (SURVEY §8(d5) floor 1.9-2.9 ms at cfg5)"}
+    return out
 
 
 def workload_config(c, world: int) -> dict:
@@ -168,17 +235,17 @@ def run_reference(args, rank: int, world: int):
     rows_all = datagen.sample_rows(A.shape[0], 4096, seed=11)
     per_row = _oracle_seconds_per_row(A, B, rows_all)
     nrows = int(max(4, min(1024, 6.0 / per_row)))  # ~6 s of CPU work per step
-    times = []
+    times, pairs = [], 0
     for s in range(args.warmup + args.steps):
-        rows = rows_all[(s * nrows) % 4096:][:nrows]
+        rows = rows_all[(s * nrows + np.arange(nrows)) % len(rows_all)]  # wraps: always nrows rows
         t0 = time.perf_counter()
         oracle.row_minima(A, B, rows=rows)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
-    pairs = nrows * B.shape[0]
+            pairs += len(rows) * B.shape[0]
     ms = 1e3 * sum(times) / len(times)
-    value = pairs / (ms / 1e3) / 1e9
+    value = pairs / (sum(times)) / 1e9
     threads = os.environ.get("OMP_NUM_THREADS") or os.environ.get("OPENBLAS_NUM_THREADS") or str(os.cpu_count())
     sample = f"exact-HD row minima of {nrows} seeded rows of A vs all {B.shape[0]} rows of B per step (fp64 oracle)"
     out = {"metric": METRIC, "value": value, "unit": "Gpair/s", "n_gpus": world, "steps": args.steps,
@@ -198,8 +265,9 @@ def run_ours(args, rank: int, world: int):
     import torch
     import torch.distributed as tdist
 
-    from paper_2511_18207_b200 import Context
-    from paper_2511_18207_b200.dist import CudaPhases, row_range, sharded_directed_hd, sharded_prohd_estimate
+    from paper_2511_18207_b200 import Context, option
+    from paper_2511_18207_b200.dist import (CudaPhases, row_range, sharded_directed_hd, sharded_hausdorff,
+                                            sharded_prohd_estimate)
 
     # one rank per GPU; the modulo only matters for functional multi-rank runs on fewer GPUs
     local_rank = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
@@ -301,6 +369,42 @@ def run_ours(args, rank: int, world: int):
     if world > 1:
         tdist.all_reduce(lt, op=tdist.ReduceOp.SUM)
     launches = int(lt.item())
+    # ------------------------------------------------------------ outside the timed region
+    # undirected exact H once (the fused bidirectional sweep at N=1; both directions row-sharded at N>1)
+    torch.cuda.synchronize()
+    u0 = torch.cuda.Event(enable_timing=True)
+    u1 = torch.cuda.Event(enable_timing=True)
+    u0.record(stream)
+    if world == 1:
+        und = ctx.hausdorff(A, B)
+    else:
+        und = sharded_hausdorff(A, B, rank, world, phases.local_fn, phases.witness_fn, centre=ctx.centre(A, B),
+                                device=dev)
+    u1.record(stream)
+    torch.cuda.synchronize()
+    ut = torch.tensor([u0.elapsed_time(u1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(ut, op=tdist.ReduceOp.MAX)
+    und_ms = float(ut.item())
+    undirected = {"value": und["value"], "ms": und_ms, "eff_Gpair_s": 2.0 * n * n / (und_ms / 1e3) / 1e9,
+                  "ab": {kk: und["ab"][kk] for kk in ("dist", "a", "b")},
+                  "ba": {kk: und["ba"][kk] for kk in ("dist", "a", "b")},
+                  "note": "effective rate = 2 nA nB / time (both directions)"}
+    # the north star's literal 3xTF32 K6 (option k6_split3) on a row slice, N=1 only
+    lit = None
+    if world == 1:
+        rows = min(n, 262144)
+        with option("k6_split3", 1):
+            ctx.directed_hd(A[:rows], B)
+            lt0 = ctx.last_timings()
+        lit = {"rows": rows, "cols": n, "kernel_ms": lt0["dist_ms"],
+               "Gpair_s": rows * float(n) / (lt0["dist_ms"] / 1e3) / 1e9,
+               "tflops_tf32": 6.0 * D * rows * float(n) / (lt0["dist_ms"] / 1e3) / 1e12}
+    # per-kernel roofline fractions of the ProHD phases (N=1: the library's own CUDA events)
+    kernels = None
+    if world == 1 and recs[-1][2]:
+        kernels = phase_rooflines(c, recs[-1][2], recs[-1][3], est, peaks())
+
     # ------------------------------------------------------------ end to end (host buffers through the ABI)
     e2e = None
     if world > 1 and not args.no_e2e:
@@ -355,7 +459,7 @@ def run_ours(args, rank: int, world: int):
                "d2h_bytes_per_step": int(d2h / args.steps), "ms_per_step": e_ms}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(Ah, Bh, budget_s=args.cpu_budget)
+        cpu = cpu_baseline(Ah, Bh, k, m, budget_s=args.cpu_budget, prohd=not args.no_cpu_prohd)
     if rank != 0:
         return
     est_t = recs[-1][2] or {kk: None for kk in ("moments_ms", "eigen_ms", "select_ms", "subset_ms", "total_ms")}
@@ -371,23 +475,28 @@ def run_ours(args, rank: int, world: int):
                                                          ("moments_ms", "eigen_ms", "select_ms", "subset_ms",
                                                           "total_ms")}},
         "exact": {"dist": ex["dist"], "a": ex["a"], "b": ex["b"], "Gpair_s_kernel": pairs_launch / k6_ms / 1e6},
+        "undirected": undirected, "k6_literal_3xtf32": lit, "kernels": kernels,
         "roofline": {"bound": "tensor",
                      "kernel": ("K6 dist_rowmin_2a_kernel (two 128-row A blocks per CTA; tcgen05 kind::tf32 "
                                 "hi.hi + kind::f16 bf16 pair correction)"),
-                     "achieved": k6_tflops, "peak": tf32_peak, "unit": "TFLOP/s", "frac": k6_tflops / tf32_peak,
+                     "achieved": k6_tflops, "peak": tf32_peak_sustained, "peak_kind": "sustained",
+                     "unit": "TFLOP/s", "frac": k6_tflops / tf32_peak_sustained,
+                     "peak_burst": tf32_peak, "frac_burst": k6_tflops / tf32_peak,
                      # the north star's yardstick: 3xTF32-equivalent work (6D TF32 flops per pair) against
-                     # the dense TF32 peak; above 1 because the kernel forms the split product with one
-                     # TF32 and one bf16 MMA instead of three TF32 MMAs
+                     # the dense TF32 peak. The kernel executes 2D TF32 + 4D bf16 flops per pair (one TF32
+                     # and one bf16 MMA instead of three TF32 MMAs), so this ratio is NOT a utilisation and
+                     # may exceed 1; `frac` (executed work / mixed peak) is.
                      "frac_vs_3xtf32_roofline": k6_tflops / (pk["bf16_tflops"] * NOMINAL_TF32_OVER_BF16),
                      "traffic": (tpp * pairs_launch) if tpp else None,
+                     "traffic_note": ("DRAM bytes per launch from the ncu capture; the compulsory operand bytes are "
+                                      "~8D B per point of A and B (hi + pairs), B is re-streamed once per wave of "
+                                      "row blocks (L2 holds 126 MB), harmless to a tensor-bound kernel"),
                      "note": ("achieved = 6*D executed tensor flops per pair (2*D TF32 + 4*D bf16) x pairs per "
                               "launch / mean launch time from CUDA events on the launch stream; peak = the mixed "
                               "rate 6/(2/P_tf32 + 4/P_bf16) with P_bf16 = "
-                              f"{pk['source']} bf16 burst {pk['bf16_tflops']} and P_tf32 = P_bf16 x nominal "
-                              f"{NOMINAL_TF32_OVER_BF16:.4f} (the larger, conservative denominator: the sustained "
-                              f"bf16 figure {pk['bf16_tflops_sustained']} gives {tf32_peak_sustained:.1f} TFLOP/s and "
-                              f"frac {k6_tflops / tf32_peak_sustained:.3f}); traffic = DRAM bytes per pair from "
-                              f"{tsrc or 'n/a'} x pairs per launch"),
+                              f"{pk['source']} bf16 SUSTAINED {pk['bf16_tflops_sustained']} (K6 is one multi-second "
+                              f"launch inside the step) and P_tf32 = P_bf16 x nominal {NOMINAL_TF32_OVER_BF16:.4f}; "
+                              f"against the burst figure {pk['bf16_tflops']}: peak_burst / frac_burst"),
                      "launch_ms": k6_ms},
         "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }
@@ -404,9 +513,23 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-prohd", action="store_true", help="skip the oracle's end-to-end ProHD timing")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without a launcher: re-run under torch.distributed.run, one rank per GPU
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        log("launching " + " ".join(cmd))
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (one rank per GPU)")
     if world > 1:
         import torch.distributed as tdist
         # PROHD_BENCH_BACKEND=gloo: functional multi-rank check on a box with fewer GPUs than ranks
@@ -414,7 +537,11 @@ def main():
         if backend == "nccl":
             import torch
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count()))
+            # communicator init lines (nranks, NVLS/NVLink transport) on stderr for the rank check
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         tdist.init_process_group(backend=backend)
+        log(f"[rank {rank}] process group: backend={backend} world={tdist.get_world_size()}")
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)

@@ -21,6 +21,11 @@
  *     context's device) or HOST pointers; host inputs are copied into the
  *     workspace inside the call (cudaMemcpyAsync on the context stream), so the
  *     workspace must have been sized with PROHD_WS_HOST_INPUTS.
+ *   - Alignment: when D % 4 == 0, DEVICE point-cloud pointers must be 16-byte
+ *     aligned (the kernels read rows with 16-byte vector loads, bulk copies and
+ *     TMA); a misaligned device pointer returns PROHD_E_INVALID before any launch.
+ *     torch / cudaMalloc buffers and whole-row offsets of them always qualify;
+ *     host inputs are staged into the (aligned) workspace and may be unaligned.
  *   - Ownership: the caller owns every input/output buffer and the workspace;
  *     the library never frees caller memory and allocates no device memory of
  *     its own beyond its context (TMA descriptors live in kernel parameters).
@@ -75,6 +80,23 @@ const char* prohd_version(void);
 /* Kernels this process has launched through the library so far (all contexts; tracing and
  * the benchmark's gpu_launches). *out (HOST) receives the count; PROHD_E_INVALID if NULL. */
 int prohd_launch_count(int64_t* out);
+/* Variant options (process-wide, all contexts). Each forces another DEVICE variant of the same
+ * computation for A/B measurement and tests; none is a CPU path, and the defaults (value -1,
+ * "unset") are the measured-best variants. They are only ever set through this call (the
+ * library reads no environment variables). Names and values:
+ *   "k6_variant"    1 single 128-row A block per CTA, 2 two-SM pair (directed), 3 two A blocks
+ *   "k6_split3"     1: literal 3xTF32 distance products (three TF32 MMAs on fp32 hi/lo)
+ *   "k6_bidir_2a"   1: fused bidirectional sweep on the two-A kernel
+ *   "k6_splits_2x"  1: the earlier fill-twice column-split rule
+ *   "k1_path"       0 fp64 DMMA Gram, 1 int8 tcgen05 Gram, 2 legacy tile moments kernel
+ *   "k1_ctas", "k1_cs_sms", "k1_beta_milli"   Gram scheduling knobs
+ *   "shift"         0 never / 1 always shift the Gram by the sample mean
+ *   "k3_simt"       1: SIMT projection kernel instead of tcgen05
+ *   "eig_stop"      1|2|3: stop the eigen-solver after that stage (timing prefixes only)
+ *   "eig_cl"        8: portable 8-CTA tridiagonalisation cluster
+ * value < 0 restores the default. PROHD_E_INVALID for an unknown name or NULL pointer. */
+int prohd_set_option(const char* name, int64_t value);
+int prohd_get_option(const char* name, int64_t* value);
 
 /* Bytes of device workspace any call below needs for these sizes (max over
  * directed_hd, hausdorff and prohd_estimate). Pure host arithmetic. */

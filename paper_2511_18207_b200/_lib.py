@@ -25,6 +25,8 @@ STATUS_NAMES = {0: "PROHD_OK", 2: "PROHD_E_INVALID", 3: "PROHD_E_DATA", 4: "PROH
 EXPORTED = [
     "prohd_create", "prohd_destroy", "prohd_set_stream", "prohd_last_error", "prohd_version",
     "prohd_launch_count",
+    "prohd_set_option",
+    "prohd_get_option",
     "prohd_workspace_bytes", "prohd_set_workspace", "directed_hd", "hausdorff", "directed_hd_rowmin",
     "prohd_estimate", "prohd_estimate_certified", "prohd_estimate_alpha", "hausdorff_subsets",
     "prohd_estimate_with_dirs", "prohd_bounds", "directed_hd_local", "prohd_centre", "directed_hd_witness",
@@ -76,6 +78,8 @@ def load() -> C.CDLL:
     lib.prohd_last_error.restype = C.c_char_p
     lib.prohd_version.restype = C.c_char_p
     lib.prohd_launch_count.argtypes = [C.POINTER(C.c_int64)]
+    lib.prohd_set_option.argtypes = [C.c_char_p, i64]
+    lib.prohd_get_option.argtypes = [C.c_char_p, C.POINTER(C.c_int64)]
     lib.prohd_workspace_bytes.argtypes = [i64, i64, i32, i32, i64, C.c_uint32]
     lib.prohd_workspace_bytes.restype = C.c_size_t
     lib.prohd_set_workspace.argtypes = [vp, vp, C.c_size_t]

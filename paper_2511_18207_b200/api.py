@@ -352,6 +352,39 @@ class Context:
 _default: dict[int, Context] = {}
 
 
+def set_option(name: str, value: int) -> None:
+    """prohd_set_option: force a device variant (process-wide; value < 0 = default)."""
+    lib = L.load()
+    rc = lib.prohd_set_option(name.encode(), int(value))
+    if rc != L.PROHD_OK:
+        raise ProHDError(rc, f"unknown option {name!r}")
+
+
+def get_option(name: str) -> int:
+    lib = L.load()
+    v = C.c_int64(0)
+    rc = lib.prohd_get_option(name.encode(), C.byref(v))
+    if rc != L.PROHD_OK:
+        raise ProHDError(rc, f"unknown option {name!r}")
+    return int(v.value)
+
+
+class option:
+    """Context manager: `with option("k6_split3", 1): ...` restores the previous value on exit."""
+
+    def __init__(self, name: str, value: int):
+        self.name, self.value, self.old = name, int(value), None
+
+    def __enter__(self):
+        self.old = get_option(self.name)
+        set_option(self.name, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, self.old)
+        return False
+
+
 def context(device: int | None = None) -> Context:
     dev = torch.cuda.current_device() if device is None else int(device)
     if dev not in _default:

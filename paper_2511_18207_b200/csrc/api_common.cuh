@@ -245,6 +245,16 @@ inline int check_sets(prohd_ctx* ctx, const float* A, int64_t nA, const float* B
   return PROHD_OK;
 }
 
+// Device inputs with D % 4 == 0 feed 16-byte vector loads, cp.async / bulk copies and TMA
+// (K1, K3, K4), which need 16-byte aligned bases (row strides 4D are then multiples of 16).
+// torch allocations are 256-byte aligned; a pointer offset by a partial row is rejected
+// here with PROHD_E_INVALID instead of faulting inside a kernel (prohd.h "Alignment").
+inline int check_aligned(prohd_ctx* ctx, const void* p, int32_t D, const char* what) {
+  if (p != nullptr && D % 4 == 0 && (reinterpret_cast<uintptr_t>(p) & 15u) != 0)
+    return fail(ctx, PROHD_E_INVALID, "%s must be 16-byte aligned when D %% 4 == 0", what);
+  return PROHD_OK;
+}
+
 // Make device copies of A/B available (staging host inputs through the workspace).
 inline int stage_inputs(prohd_ctx* ctx, const float*& A, int64_t nA, const float*& B, int64_t nB, int32_t D,
                         float* stA, float* stB, bool& host_inputs) {
@@ -262,7 +272,9 @@ inline int stage_inputs(prohd_ctx* ctx, const float*& A, int64_t nA, const float
     B = stB;
   }
   if (host_inputs) tspan(ctx, PH_H2D, t0);
-  return PROHD_OK;
+  int rc = check_aligned(ctx, A, D, "A");
+  if (rc == PROHD_OK) rc = check_aligned(ctx, B, D, "B");
+  return rc;
 }
 
 inline int prep_set(prohd_ctx* ctx, const float* X, int64_t n, int D, SetOps& s, int* bad,

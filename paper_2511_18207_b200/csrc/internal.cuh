@@ -14,6 +14,35 @@ inline std::atomic<long long>& launch_counter() {
 }
 inline void count_launch(int n = 1) { launch_counter().fetch_add(n, std::memory_order_relaxed); }
 
+// Variant options (prohd_set_option, include/prohd.h). Each forces another device variant of
+// the SAME computation for A/B measurement; -1 = unset (the measured-best default). They are set
+// explicitly through the ABI (never read from the environment), process-wide.
+enum OptId {
+  OPT_K6_VARIANT,    // 1 single A block, 2 two-SM pair (directed), 3 two A blocks per CTA
+  OPT_K6_SPLIT3,     // 1: literal 3xTF32 (three TF32 MMAs on fp32 hi/lo)
+  OPT_K6_BIDIR_2A,   // 1: fused bidirectional sweep on the two-A kernel
+  OPT_K6_SPLITS_2X,  // 1: the old fill-twice column-split rule
+  OPT_K1_PATH,       // 0 fp64 DMMA Gram, 1 int8 tcgen05 Gram, 2 legacy 64x64-tile moments kernel
+  OPT_K1_CTAS,       // legacy moments kernel: resident CTAs per SM (3 or 4)
+  OPT_K1_CS_SMS,     // DMMA Gram: column-sum SMs inside the launch (0 = separate pass)
+  OPT_K1_BETA_MILLI, // DMMA Gram: CTA allocation by (load + beta/1000)
+  OPT_SHIFT,         // 0 never / 1 always shift the Gram
+  OPT_K3_SIMT,       // 1: SIMT projection kernel instead of tcgen05
+  OPT_EIG_STOP,      // stop K2 after stage 1|2|3 (timing prefixes)
+  OPT_EIG_CL,        // 8: portable 8-CTA tridiagonalisation cluster
+  OPT_COUNT
+};
+inline std::atomic<long long>* option_table() {
+  static std::atomic<long long> t[OPT_COUNT] = {};
+  static bool init = [] {
+    for (auto& v : t) v.store(-1);
+    return true;
+  }();
+  (void)init;
+  return t;
+}
+inline long long opt(OptId id) { return option_table()[id].load(std::memory_order_relaxed); }
+
 constexpr int kBM = 128;  // rows of the row operand per CTA tile (UMMA M)
 constexpr int kBN = 256;  // columns (points of the column operand) per tile (UMMA N)
 constexpr int kBK = 32;   // fp32 K elements per pipeline chunk (one 128-B swizzle row)
@@ -22,14 +51,14 @@ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int pad_dim(int D) { return static_cast<int>(round_up(D, 4)); }  // 16-B TMA row stride
 
 // K0: split points, translated by a common centre c (fp64, D; nullptr = none), into the K6
-// operands: y = x - c in fp64, hi = fp32(y) with the low 13 mantissa bits cleared (exact
-// TF32), lo = fp32(y - hi), pr[f] = bf16 pair (hi_f, lo_f) and pc[f] = (lo_f, hi_f) (element
+// operands: y = x - c in fp64, hi = fp32(y) rounded to nearest TF32 (low 13 mantissa bits
+// zero), lo = fp32(y - hi), pr[f] = bf16 pair (hi_f, lo_f) and pc[f] = (lo_f, hi_f) (element
 // 2f at the lower address), and ||y||^2 accumulated in fp64. hi/pr/pc rows have stride Dp
 // (zero padded); norms[i] = ||y_i||^2 for i < n and +inf for n <= i < n_pad. *bad = 1 if any
 // x or norm is not finite.
 cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, const double* centre, float* hi,
                         uint32_t* pr, uint32_t* pc, float* norms, int* bad, cudaStream_t st);
-// PROHD_K6_SPLIT=3xtf32: the north star's literal 3xTF32 form (hi.hi + hi.lo + lo.hi, three TF32
+// option k6_split3 = 1: the north star's literal 3xTF32 form (hi.hi + hi.lo + lo.hi, three TF32
 // MMAs); K0 then writes lo (fp32) into pr and pc instead of the bf16 pairs. Default: off.
 bool k6_split3();
 // Common centre of a pair (X, Y): fp64 mean of the first min(nX, 4096) rows of X and the

@@ -7,31 +7,41 @@
 // n_A x n_B distance matrix never leaves TMEM/registers.
 //
 // Split products (SURVEY.md §8(a) "shared fused distance kernel"): with x = hi + lo,
-// hi the TF32-truncated value and lo = x - hi (|lo| < 2^-10 |x|),
+// hi = x rounded to nearest TF32 (11 significant bits, K0) and lo = x - hi (|lo| <= 2^-11 |x|),
 //   a.b ~= hi_a.hi_b                      one kind::tf32 MMA per 8 features
 //        + [hi_a lo_a].[lo_b hi_b]        one kind::f16 MMA (bf16) per 8 features,
 // the second over interleaved bf16 pairs (K doubled) so that a single instruction forms both
 // correction terms hi_a.lo_b + lo_a.hi_b. Both accumulate into one fp32 TMEM accumulator.
-// Error per product: lo.lo dropped (< 2^-20 |a_i||b_i|) and the bf16 rounding of hi and lo in
-// the correction terms (< 2 x 2^-9 x 2^-10 each), so |a.b - dot| <= 2^-17 sum |a_i||b_i| <=
-// 2^-17 ||a|| ||b|| and |d2 - d2_exact| <= 2^-17 (||a||^2 + ||b||^2) = 7.6e-6 of the norms, inside
-// the 1e-5 budget of BASELINE.json (Q17) with the centring of K0 shrinking the norms further.
+// Error per product a_i b_i (hi.hi and the bf16 products are exact; bf16 unit roundoff
+// u = 2^-8, applied to hi and to lo in each correction term):
+//   |hi_a lo_b - bf16(hi_a) bf16(lo_b)| <= (2u + u^2)|hi_a||lo_b| <= (2^-7 + 2^-16)(1 + 2^-11) 2^-11 |a_i||b_i|
+// twice, plus the dropped lo_a.lo_b <= 2^-22 |a_i||b_i|: in all <= 7.9e-6 |a_i||b_i| (an
+// exhaustive emulation over all 2^23 mantissas of a_i = b_i gives at most 5.9e-6). So
+// |a.b - dot| <= 7.9e-6 ||a|| ||b|| and |d2 - d2_exact| <= 7.9e-6 (||a||^2 + ||b||^2) plus the
+// fp32 accumulation (<= ~1.9e-6 of the same norms for D/8 accumulator updates at D = 256 in the
+// aligned worst case), inside the 1e-5 budget of BASELINE.json (Q17); the centring of K0 shrinks
+// the norms further. (With truncated hi, |lo| < 2^-10 |x|, the worst case was 1.22e-5 of the
+// product: tests/test_gpu_exact.py::test_split_worst_case_mantissas.)
 // Against 3xTF32 (three TF32 MMAs) the tensor time per pair drops from 6D/P_tf32 to
 // 2D/P_tf32 + 4D/P_bf16 (P_bf16 ~ 2 P_tf32): ~1.5x.
 //
-// Structure (persistent, 1 CTA per SM, warp-specialised, 192 threads):
-//   warp 0      TMA producer: per K-chunk (32 fp32 = one 128-B swizzle row) it
-//               loads A_hi/A_pr [128 x 32] and B_hi/B_pc [256 x 32] (pr/pc: 32 bf16
-//               pairs = 128 B per row) into a 2-stage ring (96 KB per stage), SWIZZLE_128B.
-//   warp 1      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
-//               and single-thread MMA issuer: tcgen05.mma.cta_group::1.kind::tf32
-//               M=128, N=256: per 8 features one TF32 MMA (K=8) and one bf16 MMA
-//               (K=16 over the pairs), commit -> smem slot free,
+// Structure (persistent, 1 CTA per SM, warp-specialised; 320 threads for the single-block and
+// two-A kernels, 192 for the opt-in 2-SM pair):
+//   warp 0      TMA producer: per K-chunk it loads the A and B hi / pair tiles into a smem
+//               ring (single block: 32 fp32 = one 128-B swizzle row, [128 x 32] A and [256 x 32]
+//               B, 2 stages of 96 KB; two-A: 16-feature SWIZZLE_64B stages x3).
+//   warp 1      TMEM allocator (512 columns) and MMA issuer: all 32 lanes run the issue loop and
+//               an elect.sync predicate inside the tcgen05.mma / commit asm picks the issuing
+//               lane (kElect; the fused bidirectional sweep below D = 192 keeps a lane-0 issuer).
+//               tcgen05.mma.cta_group::1 M=128, N=256: per 8 features one kind::tf32 MMA (K=8)
+//               and one kind::f16 bf16 MMA (K=16 over the pairs); commit -> smem slot free,
 //               commit -> accumulator full.
-//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 (one TMEM lane = one row per
-//               thread), v = fma(-2, acc, ||b||^2), running min in a register
-//               across all B tiles of the unit; the accumulator is double
-//               buffered so the epilogue of tile t overlaps the MMAs of t+1.
+//   warps 2-9   epilogue (8 warps): tcgen05.ld 32x32b.x32 (one TMEM lane = one row per thread;
+//               two warps per lane quarter, each one 128-column half of the tile in the single-
+//               block kernel, one accumulator per group of 4 warps in the two-A kernel),
+//               v = fma(-2, acc, ||b||^2), running min in a register across all B tiles of the
+//               unit; the single-block accumulator is double buffered so the epilogue of tile t
+//               overlaps the MMAs of t+1.
 // Work unit = (128-row block of A, contiguous range of B tiles). With one range
 // the row minimum is stored; with several (small n_A) it is combined with an
 // integer atomicMin on the float bits (valid since d2 >= 0).
@@ -787,24 +797,20 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
 // epilogue is not hidden behind fewer MMAs: D = 64 2118 vs 1896). The fused bidirectional sweep
 // keeps the single-block kernel: its column-minimum epilogue is heavier and, not overlapped in the
 // two-A kernel, made it slower (D = 256: 34.5 vs 31.5 ms for 65536 x 262144; the two-A kBidir
-// instantiation is kept for A/B). PROHD_K6_VARIANT = 1 | 2a | 2sm forces a variant (2sm: directed).
+// instantiation is kept for A/B). option k6_variant = 1 | 3 (two-A) | 2 (2-SM pair, directed) forces a variant.
 static int dist_variant(int D) {
-  const char* e = getenv("PROHD_K6_VARIANT");
-  if (e != nullptr && e[0] == '2' && e[1] == 's') return 2;  // "2sm": CTA pair
-  if (e != nullptr && e[0] == '2' && e[1] == 'a') return 3;  // "2a": two A blocks per CTA
-  if (e != nullptr && e[0] == '1') return 1;
+  const long long v = opt(OPT_K6_VARIANT);  // 2: CTA pair, 3: two A blocks per CTA, 1: single
+  if (v >= 1 && v <= 3) return static_cast<int>(v);
   return D >= 128 ? 3 : 1;
 }
 
 int dist_b_box_rows(int D, bool bidir) { return (!bidir && dist_variant(D) == 2) ? 128 : kBN; }
 bool k6_split3() {
-  const char* e = getenv("PROHD_K6_SPLIT");
-  return e != nullptr && e[0] == '3';
+  return opt(OPT_K6_SPLIT3) == 1;
 }
 
 static bool bidir_2a() {
-  const char* e = getenv("PROHD_K6_BIDIR_2A");  // dev A/B: fused bidirectional sweep on the two-A kernel
-  return e != nullptr && e[0] == '1';
+  return opt(OPT_K6_BIDIR_2A) == 1;  // dev A/B: fused bidirectional sweep on the two-A kernel
 }
 int dist_box_inner(int D, bool bidir) { return ((!bidir || bidir_2a()) && dist_variant(D) == 3) ? kBK2 : kBK; }
 
@@ -831,8 +837,7 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   // occupancy: pick the cheapest of 1..64 splits (ties to fewer: fewer atomic merges).
   int nsplit = 1;
   {
-    const char* e = getenv("PROHD_K6_SPLITS");  // dev A/B: "2x" = the old fill-twice rule
-    if (e != nullptr && e[0] == '2') {
+    if (opt(OPT_K6_SPLITS_2X) == 1) {  // dev A/B: the old fill-twice rule
       nsplit = (2 * slots + s.nrb - 1) / s.nrb;
     } else {
       double best = 0.0;

@@ -82,7 +82,7 @@ struct EigArgs {
   float* out32;   // U32 rows
   double* lam;    // [k] eigenvalues (desc)
   int* n_dirs;    // 1 + kept
-  int stop;       // dev timing only (PROHD_EIG_STOP): return after phase `stop` (0 = run all)
+  int stop;       // dev timing only (option eig_stop): return after phase `stop` (0 = run all)
   double* de;     // [2][kMaxD]: diagonal d, then off-diagonal e of T (global hand-off)
 };
 
@@ -506,14 +506,13 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
 cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, double* out64, float* out32,
                               double* lam, int* n_dirs, cudaStream_t st) {
   if (D > kMaxD) return cudaErrorInvalidValue;
-  const char* es = getenv("PROHD_EIG_STOP");
-  EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs, es != nullptr ? atoi(es) : 0, V + static_cast<int64_t>(D) * D};
+  const int stop = opt(OPT_EIG_STOP) > 0 ? static_cast<int>(opt(OPT_EIG_STOP)) : 0;
+  EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs, stop, V + static_cast<int64_t>(D) * D};
   cudaError_t e;
   // tridiagonalisation on a 16-CTA cluster (non-portable size; 2 rows per warp) for D > 160 where
   // the device allows it (D = 256: 0.87 -> 0.84 ms), else on 8 CTAs (faster below: the per-step
-  // barrier dominates); PROHD_EIG_CL=8 forces the portable size (A/B)
-  const char* ec = getenv("PROHD_EIG_CL");
-  bool wide = D > 160 && !(ec != nullptr && ec[0] == '8');
+  // barrier dominates); option eig_cl = 8 forces the portable size (A/B)
+  bool wide = D > 160 && opt(OPT_EIG_CL) != 8;
   if (wide) {
     const size_t smem16 = sizeof(double) * static_cast<size_t>(kMaxD / 16) * kMaxD;
     wide = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed,

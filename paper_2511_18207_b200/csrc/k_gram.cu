@@ -30,11 +30,13 @@
 //   warps 0-11 (MMA): warp w runs tile w % ntiles on k-steps (w / ntiles) + kRep u; per
 //            k-step it loads 4 A and 4 B fragments (8 LDS.64, issued one k-step ahead) and
 //            issues 16 DMMA.8x8x4 into a 32x32 fp64 register accumulator (64 regs).
-// The column sums are NOT taken here: any fp64 add in this kernel runs on the adder the DMMAs
-// share and was measured to cost far more than its count suggests (fp64 adds in the loaders:
-// 9.6 -> 12.6-13.1 ms; one extra DMMA per k-step against an indicator operand: 9.6 -> 11.1 ms).
-// colsum_kernel takes them in a separate HBM-bound pass (~0.65 ms at cfg5) over the raw
-// points, and the reduce kernel forms S_X = sum x - n_X s.
+// The column sums are NOT taken by the Gram warps: any fp64 add in a Gram CTA runs on the adder
+// the DMMAs share and was measured to cost far more than its count suggests (fp64 adds in the
+// loaders: 9.6 -> 12.6-13.1 ms; one extra DMMA per k-step against an indicator operand: 9.6 ->
+// 11.1 ms). At D >= 224 the launch's last CTAs (colsum_role, one per SM of their own) stream the
+// rows with 1-D bulk copies and add them up while the Gram CTAs run; below that colsum_kernel
+// takes them in a separate HBM-bound pass (~0.65 ms at cfg5). The reduce kernel forms
+// S_X = sum x - n_X s.
 // Three MMA warps per SM sub-partition keep the DMMA pipe fed through the fragment-load and
 // barrier gaps that left it 26% idle with two (the 8-warp, 2-CTA/SM version).
 // Buffer hand-off with mbarriers: full[b] (loader warps arrive, MMA warps wait) and
@@ -652,11 +654,11 @@ bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p) {
   // byte to hide them: a column-sum SM streams ~66 GB/s (measured), so 7 of them match the
   // DMMA-bound Gram on the other 141 at D = 256 (cfg5 moments 9.27 -> 8.91 ms; 8: 9.11, 6: 10.19)
   // but not at D = 128, where the Gram costs half as much per byte (cfg3 0.80 -> 1.36 ms). D >= 224,
-  // D % 4 == 0, enough rows; PROHD_K1_CS_SMS overrides the count (0 = the colsum_kernel pass).
+  // D % 4 == 0, enough rows; option k1_cs_sms overrides the count (0 = the colsum_kernel pass).
   p.cs_ctas = 0;
   {
     int cs = D >= 224 ? 7 : 0;
-    if (const char* e = getenv("PROHD_K1_CS_SMS")) cs = atoi(e);
+    if (opt(OPT_K1_CS_SMS) >= 0) cs = static_cast<int>(opt(OPT_K1_CS_SMS));
     const int sms = num_sms > 0 ? num_sms : 148;
     if (cs > 0 && D % 4 == 0 && D <= kGT && N >= static_cast<int64_t>(64) * sms && cs < sms / 2) p.cs_ctas = cs;
   }
@@ -673,9 +675,9 @@ bool plan_gram(int64_t nA, int64_t nB, int D, int num_sms, GramPlan& p) {
     if (G.load < 1) G.load = 1;
     G.rpg = 1;
   }
-  // beta: a per-point cost outside the DMMA pipe, in DMMA units (dev A/B: PROHD_K1_BETA)
+  // beta: a per-point cost outside the DMMA pipe, in DMMA units (dev A/B: option k1_beta_milli)
   double beta = 0.0;
-  if (const char* e = getenv("PROHD_K1_BETA")) beta = atof(e);
+  if (opt(OPT_K1_BETA_MILLI) >= 0) beta = 1e-3 * static_cast<double>(opt(OPT_K1_BETA_MILLI));
   for (int used = p.ngroups; used < budget; ++used) {
     int best = -1;
     double bt = 0.0;

@@ -161,10 +161,9 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
 constexpr int kLds = 132;
 constexpr int kMT = 128;    // threads per CTA (4 warps)
 constexpr int kMC = 32;     // points per chunk
-// resident CTAs per SM (register-limited: 160 regs at 3, 128 at 4). PROHD_K1_CTAS=3|4 (dev A/B).
+// resident CTAs per SM (register-limited: 160 regs at 3, 128 at 4). option k1_ctas = 3|4 (dev A/B).
 static int mom_ctas_per_sm() {
-  const char* e = getenv("PROHD_K1_CTAS");
-  return (e != nullptr && e[0] == '3') ? 3 : 4;
+  return opt(OPT_K1_CTAS) == 3 ? 3 : 4;
 }
 
 // CTA -> (bi, bj, pair index, slot). Pairs (bi <= bj) are enumerated row-major; row r
@@ -399,16 +398,14 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
   p.nslots = cd > p.c_off ? cd : p.c_off;
   p.gpart_doubles = static_cast<int64_t>(p.npairs) * p.nslots * kFB * kFB;
   p.spart_doubles = static_cast<int64_t>(p.nb) * p.c_diag * 2 * kFB;
-  const char* leg = getenv("PROHD_K1_LEGACY");
-  p.gram = !(leg != nullptr && leg[0] == '1') && plan_gram(nA, nB, D, num_sms, p.gp);
+  p.gram = opt(OPT_K1_PATH) != 2 && plan_gram(nA, nB, D, num_sms, p.gp);
   if (p.gram) {
     if (p.gp.gpart_doubles > p.gpart_doubles) p.gpart_doubles = p.gp.gpart_doubles;
     if (p.gp.spart_doubles > p.spart_doubles) p.spart_doubles = p.gp.spart_doubles;
   }
-  // The int8 tensor-core Gram (k_gram_i8.cu) is opt-in (PROHD_K1_I8=1): correct, but measured
+  // The int8 tensor-core Gram (k_gram_i8.cu) is opt-in (option k1_path = 1): correct, but measured
   // slower at cfg5 (22.4 vs 12.2 ms) because its 128x64 tiles are L2-bound.
-  const char* i8e = getenv("PROHD_K1_I8");
-  p.i8 = (i8e != nullptr && i8e[0] == '1') && plan_gram_i8(nA, nB, D, num_sms, p.ip);
+  p.i8 = opt(OPT_K1_PATH) == 1 && plan_gram_i8(nA, nB, D, num_sms, p.ip);
   if (p.i8) {
     if (p.ip.gpart_doubles > p.gpart_doubles) p.gpart_doubles = p.ip.gpart_doubles;
     p.i8_bytes = round_up(static_cast<int64_t>(D) * 4, 256) + round_up(p.ip.spart_doubles * 8, 256) +
@@ -429,8 +426,8 @@ cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB,
   count_launch();
   shift_kernel<<<8 * ((D + 31) / 32), 1024, 0, st>>>(A, nA, B, nB, D, s);
   count_launch();
-  const char* fe = getenv("PROHD_SHIFT");  // dev A/B only: 0 = never shift, 1 = always
-  const int force = (fe != nullptr && (fe[0] == '0' || fe[0] == '1')) ? fe[0] - '0' : -1;
+  const long long fo = opt(OPT_SHIFT);  // dev A/B only: 0 = never shift, 1 = always
+  const int force = (fo == 0 || fo == 1) ? static_cast<int>(fo) : -1;
   shift_decide_kernel<<<1, 256, 0, st>>>(s, D, force);
   return cudaGetLastError();
 }

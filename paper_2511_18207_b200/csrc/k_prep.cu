@@ -1,9 +1,10 @@
 // k_prep.cu — K0 operand preparation, K7 row-max key and fp64 witness search.
 //
 // K0 (SURVEY.md §2f, §8(a) "Centering"): per point, y = x - c (fp64, c the pair's
-// common centre), hi = trunc_tf32(fp32(y)) (low 13 mantissa bits cleared, so the
-// tensor core reads hi exactly whatever its fp32->tf32 conversion mode),
-// lo = fp32(y - hi), and ||y||^2 accumulated in fp64 then rounded to fp32 (without
+// common centre), hi = rn_tf32(fp32(y)) (rounded to nearest, ties to even, to 11
+// significant bits with the low 13 mantissa bits zero, so the tensor core reads hi
+// exactly whatever its fp32->tf32 conversion mode, and |lo| <= 2^-11 |y|),
+// lo = fp32(y - hi) (exact in fp32), and ||y||^2 accumulated in fp64 then rounded to fp32 (without
 // a centre: y = x and lo = x - hi exactly). K6 takes a.b = hi_a.hi_b (TF32 MMA) +
 // [hi_a lo_a].[lo_b hi_b] (one bf16 MMA over interleaved pairs), so K0 writes hi (fp32) and
 // the bf16 pairs in both orders: pr[f] = (bf16(hi_f), bf16(lo_f)) for the row role and
@@ -25,8 +26,14 @@
 
 namespace prohd {
 
-__device__ __forceinline__ float tf32_trunc(float x) {
-  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+// Round to nearest TF32 (ties to even) by integer carry into bit 13; a value that would
+// round past FLT_MAX (to the inf pattern) keeps its truncation instead, so a finite x
+// always gives a finite hi. NaN/inf pass through truncated (they are flagged by the norm).
+__device__ __forceinline__ float tf32_rn(float x) {
+  const uint32_t b = __float_as_uint(x);
+  const uint32_t r = (b + 0xFFFu + ((b >> 13) & 1u)) & 0xFFFFE000u;
+  const bool keep = ((b & 0x7F800000u) == 0x7F800000u) || ((r & 0x7F800000u) == 0x7F800000u);
+  return __uint_as_float(keep ? (b & 0xFFFFE000u) : r);
 }
 
 __device__ __forceinline__ uint32_t bf16_pair(float first, float second) {
@@ -59,14 +66,14 @@ __global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, 
       const float v = c < D ? __ldg(x + c) : 0.0f;
       if (kCentre) {
         const double y = c < D ? static_cast<double>(v) - __ldg(centre + c) : 0.0;
-        const float vh = tf32_trunc(static_cast<float>(y));
+        const float vh = tf32_rn(static_cast<float>(y));
         const float vl = static_cast<float>(y - static_cast<double>(vh));
         h[c] = vh;
         qr[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vh, vl);
         qc[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vl, vh);
         s = fma(y, y, s);
       } else {
-        const float vh = tf32_trunc(v);
+        const float vh = tf32_rn(v);
         const float vl = v - vh;
         h[c] = vh;
         qr[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vh, vl);

@@ -281,8 +281,7 @@ double project_tc_eps_coef(int D) {
 }
 
 bool project_tc_supported(int64_t n, int D, int L) {
-  const char* e = getenv("PROHD_K3_SIMT");  // dev A/B: the SIMT tile kernel
-  if (e != nullptr && e[0] == '1') return false;
+  if (opt(OPT_K3_SIMT) == 1) return false;  // dev A/B: the SIMT tile kernel
   return n >= 1 && D % 4 == 0 && D <= 32 * kPMaxChunks && L >= 1 && L <= 32 && n <= 0x7FFFFFFFll;
 }
 

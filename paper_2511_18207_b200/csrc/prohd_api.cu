@@ -25,6 +25,30 @@ extern "C" {
 
 const char* prohd_version(void) { return "prohd-b200 0.1 sm_100a"; }
 
+static const char* const kOptNames[prohd::OPT_COUNT] = {
+    "k6_variant", "k6_split3", "k6_bidir_2a", "k6_splits_2x", "k1_path", "k1_ctas",
+    "k1_cs_sms",  "k1_beta_milli", "shift", "k3_simt", "eig_stop", "eig_cl"};
+
+int prohd_set_option(const char* name, int64_t value) {
+  if (name == nullptr) return PROHD_E_INVALID;
+  for (int i = 0; i < prohd::OPT_COUNT; ++i)
+    if (std::strcmp(name, kOptNames[i]) == 0) {
+      prohd::option_table()[i].store(value < 0 ? -1 : value);
+      return PROHD_OK;
+    }
+  return PROHD_E_INVALID;
+}
+
+int prohd_get_option(const char* name, int64_t* value) {
+  if (name == nullptr || value == nullptr) return PROHD_E_INVALID;
+  for (int i = 0; i < prohd::OPT_COUNT; ++i)
+    if (std::strcmp(name, kOptNames[i]) == 0) {
+      *value = prohd::option_table()[i].load();
+      return PROHD_OK;
+    }
+  return PROHD_E_INVALID;
+}
+
 int prohd_launch_count(int64_t* out) {
   if (out == nullptr) return PROHD_E_INVALID;
   *out = static_cast<int64_t>(prohd::launch_counter().load());
@@ -255,6 +279,7 @@ int prohd_project(prohd_ctx* ctx, const float* X, int64_t n, int32_t D, const do
   if (n < 1 || D < 1 || L < 1 || L > 32) return fail(ctx, PROHD_E_INVALID, "bad sizes");
   if (!is_device_ptr(X) || !is_device_ptr(dirs) || !is_device_ptr(proj_out))
     return fail(ctx, PROHD_E_INVALID, "prohd_project takes device pointers");
+  if ((rc = check_aligned(ctx, X, D, "X"))) return rc;
   Carver dry{nullptr, 0, 0, true};
   dry.take<float>(static_cast<int64_t>(L) * D);
   dry.take<unsigned>(1);

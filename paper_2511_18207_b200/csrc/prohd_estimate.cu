@@ -194,25 +194,37 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   if (counts && L > 1) CK(launch_minus_one(w.n_dirs, w.n_dirs1, st));  // shared by both sets
   CK(cudaEventRecord(ctx->ev_fork, st));
   CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
-  for (int s = 0; s < 2; ++s) {
-    // projections run for every point (also when 2m >= n) so non-finite input is always detected
-    cudaStream_t sst = s == 0 ? st : ctx->aux;
-    SelectBufs& b = w.sel[s];
-    const int64_t m0 = counts ? counts[2 * s] : m;      // centroid axis
-    const int64_t m1 = counts ? counts[2 * s + 1] : m;  // principal directions
-    const bool all = 2 * m0 >= n[s] || (L > 1 && 2 * m1 >= n[s]);
-    if (all) {
-      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, sst));  // finiteness pass
-      CK(launch_iota(b.uidx, b.ucount, n[s], sst));
-    } else if (m0 == m1 || L == 1) {
-      CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst));
-    } else {  // two direction groups with different per-tail counts, one shared union bitmap
-      CK(launch_select(X[s], n[s], D, w.U64, w.U32, 1, w.n_dirs, m0, b, sst, true, false));
-      CK(launch_select(X[s], n[s], D, w.U64 + D, w.U32 + D, L - 1, w.n_dirs1, m1, b, sst, false, true));
+  // the chains are enqueued by a helper so that an error in either still joins the aux stream
+  // back into the caller's before returning (no kernel of this call is left unordered against
+  // the caller's stream and workspace)
+  auto enqueue_chains = [&]() -> cudaError_t {
+    for (int s = 0; s < 2; ++s) {
+      // projections run for every point (also when 2m >= n) so non-finite input is always detected
+      cudaStream_t sst = s == 0 ? st : ctx->aux;
+      SelectBufs& b = w.sel[s];
+      const int64_t m0 = counts ? counts[2 * s] : m;      // centroid axis
+      const int64_t m1 = counts ? counts[2 * s + 1] : m;  // principal directions
+      const bool all = 2 * m0 >= n[s] || (L > 1 && 2 * m1 >= n[s]);
+      cudaError_t e;
+      if (all) {
+        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, sst)) != cudaSuccess) return e;
+        if ((e = launch_iota(b.uidx, b.ucount, n[s], sst)) != cudaSuccess) return e;
+      } else if (m0 == m1 || L == 1) {
+        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst)) != cudaSuccess) return e;
+      } else {  // two direction groups with different per-tail counts, one shared union bitmap
+        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, 1, w.n_dirs, m0, b, sst, true, false)) != cudaSuccess)
+          return e;
+        if ((e = launch_select(X[s], n[s], D, w.U64 + D, w.U32 + D, L - 1, w.n_dirs1, m1, b, sst, false, true)) !=
+            cudaSuccess)
+          return e;
+      }
     }
-  }
+    return cudaSuccess;
+  };
+  const cudaError_t e_chain = enqueue_chains();
   CK(cudaEventRecord(ctx->ev_join, ctx->aux));
   CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+  CK(e_chain);
   tspan(ctx, PH_SELECT, t_sel);
   unsigned ucount[2];
   int ndirs = 0, ovf[2] = {0, 0};

@@ -148,6 +148,9 @@ int prohd_local_moments(prohd_ctx* ctx, const float* A_local, int64_t nA_local, 
       B_local = w.stageB;
     }
   }
+  if ((rc = check_aligned(ctx, nA_local > 0 ? A_local : nullptr, D, "A_local")) ||
+      (rc = check_aligned(ctx, nB_local > 0 ? B_local : nullptr, D, "B_local")))
+    return rc;
   CK(cudaMemcpyAsync(w.mom.s, shift, sizeof(double) * D, cudaMemcpyHostToDevice, st));
   const int t0 = tmark(ctx);
   CK(cudaMemsetAsync(w.mom.SA, 0, sizeof(double) * D, st));
@@ -227,6 +230,7 @@ int prohd_local_candidates(prohd_ctx* ctx, const float* X_local, int64_t n_local
     CK(cudaMemcpyAsync(w.stageA, X_local, sizeof(float) * n_local * D, cudaMemcpyHostToDevice, st));
     X_local = w.stageA;
   }
+  if ((rc = check_aligned(ctx, n_local > 0 ? X_local : nullptr, D, "X_local"))) return rc;
   CK(cudaMemcpyAsync(w.U64, dirs, sizeof(double) * n_dirs * D, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(w.n_dirs, &n_dirs, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(launch_dirs_to_f32(w.U64, w.U32, n_dirs, D, st));

@@ -64,6 +64,26 @@ def sharded_directed_hd(A_local, row_offset: int, B, local_fn, witness_fn, devic
     return {"dist": float(np.sqrt(d2)), "dist2": d2, "a": row, "b": b, "dist2_tc": d2_tc, "key": gkey}
 
 
+def sharded_hausdorff(A, B, rank: int, world: int, local_fn, witness_fn, centre=None, device=None,
+                      group=None) -> dict:
+    """H(A,B) = max(h(A,B), h(B,A)) with both sets replicated on every rank.
+
+    A->B shards the rows of A (B replicated), B->A shards the rows of B (A replicated), each
+    side combined by one MAX all-reduce of the packed key plus the witness exchange of
+    `sharded_directed_hd`. With `centre` (e.g. prohd_centre(A, B), the centre `hausdorff()`
+    uses) both sides prepare their operands about the same point, so the result is
+    bit-identical for every rank count. local_fn(A_local, row_offset, B, centre) -> key.
+    """
+    res = {}
+    for side, (R, Cm) in {"ab": (A, B), "ba": (B, A)}.items():
+        lo, hi = row_range(R.shape[0], rank, world)
+        loc = (lambda A_l, off, Bm: local_fn(A_l, off, Bm, centre))
+        res[side] = sharded_directed_hd(R[lo:hi], lo, Cm, loc, witness_fn, device=device, group=group)
+    ab, ba = res["ab"], res["ba"]
+    value = ab["dist"] if ab["dist2"] >= ba["dist2"] else ba["dist"]  # A->B witness on equality (Q15)
+    return {"value": value, "ab": ab, "ba": ba}
+
+
 def _all_gather_rows(rows: torch.Tensor, D: int, device, group=None) -> torch.Tensor:
     """Concatenate every rank's rows (variable counts) in rank order (C3)."""
     world = dist.get_world_size(group)

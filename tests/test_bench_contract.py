@@ -28,3 +28,24 @@ def test_reference_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["value"] == d["value"] and cb["cores"] >= 1 and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": "Gpair/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_gpus_flag_forms_the_process_group():
+    """`bench.py --gpus 2` without a launcher re-runs itself under torch.distributed.run with two
+    ranks (--gpus was ignored); the reference arm then reports n_gpus = 2 from
+    rank 0 alone, and a --gpus / WORLD_SIZE mismatch is refused."""
+    env = dict(os.environ, OMP_NUM_THREADS="2", OPENBLAS_NUM_THREADS="2")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "1", "--steps", "1",
+                          "--warmup", "1", "--gpus", "2"], cwd=ROOT, env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    assert "world=2" in out.stderr
+    bad = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "1", "--gpus", "4"],
+                         cwd=ROOT, env=dict(env, WORLD_SIZE="1", RANK="0"), capture_output=True, text=True,
+                         timeout=120)
+    assert bad.returncode != 0 and "WORLD_SIZE" in bad.stderr

@@ -14,7 +14,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_2511_18207_b200.dist import pack_key, row_range, sharded_directed_hd, unpack_key
+from paper_2511_18207_b200.dist import pack_key, row_range, sharded_directed_hd, sharded_hausdorff, unpack_key
 
 
 def _free_port():
@@ -25,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, A, B, q):
+def _worker(rank, world, port, A, B, q, mode):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -41,16 +41,19 @@ def _worker(rank, world, port, A, B, q):
         rmin, arg = oracle.row_minima(a.reshape(1, -1), Bm)
         return {"b": int(arg[0]), "dist2": float(rmin[0])}
 
-    r = sharded_directed_hd(A[lo:hi], lo, B, local_fn, witness_fn)
+    if mode == "directed":
+        r = sharded_directed_hd(A[lo:hi], lo, B, local_fn, witness_fn)
+    else:
+        r = sharded_hausdorff(A, B, rank, world, lambda Al, off, Bm, c: local_fn(Al, off, Bm), witness_fn)
     q.put((rank, r))
     dist.destroy_process_group()
 
 
-def _run(A, B, world=2):
+def _run(A, B, world=2, mode="directed"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, A, B, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, A, B, q, mode)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=120) for _ in ps]
@@ -82,3 +85,18 @@ def test_sharded_equals_unsharded(ties):
     for rank, r in res.items():
         assert r["a"] == ref["a"] and r["b"] == ref["b"], (rank, r, ref)
         assert r["dist2"] == ref["dist2"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_hausdorff_equals_unsharded(world):
+    """Both directions sharded (rows of A for A->B, rows of B for B->A), one MAX all-reduce each:
+    the value, both witnesses and the A->B-on-equality rule match the unsharded oracle."""
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((157, 5)).astype(np.float32)
+    B = (rng.standard_normal((211, 5)) + 0.3).astype(np.float32)
+    ref = oracle.hausdorff(A, B)
+    for rank, r in _run(A, B, world=world, mode="undirected").items():
+        for side in ("ab", "ba"):
+            assert (r[side]["a"], r[side]["b"]) == (ref[side]["a"], ref[side]["b"]), (rank, side)
+            assert r[side]["dist2"] == ref[side]["dist2"]
+        assert r["value"] == ref["value"]

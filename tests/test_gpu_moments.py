@@ -3,7 +3,7 @@
 same fp32 inputs (the oracle's definition, O1/O3, written out with numpy).
 
 The default Gram is the fp64 DMMA pass (k_gram.cu, products of fp32 values exact in fp64,
-subtraction only when s != 0); PROHD_K1_I8=1 selects the opt-in int8 tensor-core pass for
+subtraction only when s != 0); option k1_path = 1 selects the opt-in int8 tensor-core pass for
 s = 0 (k_gram_i8.cu: exact integer slice products, pairs t + u <= 7 kept). Both must agree
 with the fp64 sums to 1e-12 of sum_p |x_pi - s_i| |x_pj - s_j| (the scale of the
 accumulation; fp64 accumulation over 1e5 points, or the int8 path's dropped slice pairs,
@@ -47,13 +47,9 @@ def _check(ctx, A, B, s, rtol=1e-12):
 
 @pytest.fixture(params=["dmma", "i8"])
 def gram_path(request):
-    old = os.environ.get("PROHD_K1_I8")
-    os.environ["PROHD_K1_I8"] = "1" if request.param == "i8" else "0"
-    yield request.param
-    if old is None:
-        del os.environ["PROHD_K1_I8"]
-    else:
-        os.environ["PROHD_K1_I8"] = old
+    from paper_2511_18207_b200 import option
+    with option("k1_path", 1 if request.param == "i8" else 0):
+        yield request.param
 
 
 @pytest.mark.parametrize("nA,nB,D", [(1, 1, 3), (63, 65, 16), (1000, 777, 64), (4099, 2051, 100),

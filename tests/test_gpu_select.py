@@ -66,15 +66,9 @@ def test_projection_variants_agree(ctx):
     X = rng.standard_normal((50_000, 256)).astype(np.float32)
     U = _dirs(256, 17, 7)
     tc = _check(ctx, X, U)
-    old = os.environ.get("PROHD_K3_SIMT")
-    os.environ["PROHD_K3_SIMT"] = "1"
-    try:
+    from paper_2511_18207_b200 import option
+    with option("k3_simt", 1):
         simt = _check(ctx, X, U)
-    finally:
-        if old is None:
-            del os.environ["PROHD_K3_SIMT"]
-        else:
-            os.environ["PROHD_K3_SIMT"] = old
     print(f"tcgen05 {tc[0]:.2e} (bound {tc[1]:.2e}); SIMT {simt[0]:.2e} (bound {simt[1]:.2e})")
 
 

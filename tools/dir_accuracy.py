@@ -1,7 +1,10 @@
 """Dev check: GPU directions vs the fp64 oracle's at a config's full size (angles, C residuals,
-selection equality). Run with PROHD_SHIFT=0/1 to compare the Gram paths."""
+selection equality). Run with PROHD_OPT_SHIFT=0/1 to compare the Gram paths."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _opts  # noqa: E402
+_opts.apply_env()
 import numpy as np
 import torch
 import datagen
@@ -18,6 +21,6 @@ U, R, C = g["U"], ref["U"], ref["C"]
 cn = np.linalg.norm(C, 2)
 ang = [float(np.linalg.norm(U[:, l] - (U[:, l] @ R[:, l]) * R[:, l])) for l in range(U.shape[1])]
 res = [float(np.linalg.norm(C @ U[:, l] - (U[:, l] @ C @ U[:, l]) * U[:, l]) / cn) for l in range(1, U.shape[1])]
-print(f"cfg{cfg} shift={os.environ.get('PROHD_SHIFT', 'auto')}: max sin-angle {max(ang):.3e}, max residual/||C|| "
+print(f"cfg{cfg} shift={os.environ.get('PROHD_OPT_SHIFT', 'auto')}: max sin-angle {max(ang):.3e}, max residual/||C|| "
       f"{max(res):.3e}, sets equal {np.array_equal(g['IA'], ref['IA']) and np.array_equal(g['IB'], ref['IB'])}, "
       f"H^ {g['value']:.9f} vs {ref['value']:.9f}", flush=True)

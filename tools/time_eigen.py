@@ -1,7 +1,10 @@
-"""Dev timing of K2 through prohd_directions on a prescribed spectrum; PROHD_EIG_STOP=1|2|3
+"""Dev timing of K2 through prohd_directions on a prescribed spectrum; PROHD_OPT_EIG_STOP=1|2|3
 stops after tridiagonalisation | bisection | inverse iteration (timing prefixes)."""
 import os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _opts  # noqa: E402
+_opts.apply_env()
 import numpy as np
 import torch
 from paper_2511_18207_b200 import Context
@@ -17,5 +20,5 @@ for D, k in [(64, 8), (128, 8), (256, 16), (256, 1)]:
     for _ in range(6):
         ctx.directions(mom, 500, 500, D, k, np.zeros(D))
         ts.append(ctx.last_timings()["eigen_ms"])
-    print(f"D={D} k={k} stop={os.environ.get('PROHD_EIG_STOP', '0')}: eigen {statistics.median(ts[1:]):.3f} ms",
+    print(f"D={D} k={k} stop={os.environ.get('PROHD_OPT_EIG_STOP', '0')}: eigen {statistics.median(ts[1:]):.3f} ms",
           flush=True)

@@ -1,6 +1,9 @@
 """Dev timing: prohd_estimate phases (in-library CUDA events) per config, median of 5 runs."""
 import os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _opts  # noqa: E402
+_opts.apply_env()
 import torch
 import datagen
 from paper_2511_18207_b200 import Context

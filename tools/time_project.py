@@ -1,6 +1,9 @@
 """Dev timing: K3 alone through the prohd_project hook, 2M x 256 points, 17 directions (cfg5 shape)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _opts  # noqa: E402
+_opts.apply_env()
 import numpy as np
 import torch
 from paper_2511_18207_b200 import Context
@@ -16,5 +19,5 @@ ts = []
 for _ in range(10):
     e0.record(); ctx.project(X, U); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
 t = sorted(ts)[len(ts) // 2]
-print(f"dbg={os.environ.get('PROHD_K3_DBG', '0')} simt={os.environ.get('PROHD_K3_SIMT', '0')}: {t:.3f} ms "
+print(f"dbg={os.environ.get('PROHD_OPT_K3_DBG', '0')} simt={os.environ.get('PROHD_OPT_K3_SIMT', '0')}: {t:.3f} ms "
       f"(call incl. U conversion + readback), {n * D * 4 / t / 1e6:.0f} GB/s", flush=True)
