@@ -352,17 +352,12 @@ def run_ours(args, rank: int, world: int):
     dist_ms = [r[3]["dist_ms"] / max(1, r[3]["dist_launches"]) for r in recs]
     k6_ms = sum(dist_ms) / len(dist_ms)
     pairs_launch = float(hi - lo) * float(n)
-    # K6 executes, per pair, 2D TF32 flops (hi.hi) and 4D bf16 flops ([hi lo].[lo hi], K doubled);
-    # its tensor roofline is the mixed rate 6 / (2 / P_tf32 + 4 / P_bf16) TFLOP/s
+    # K6 executes, per pair, three fp16 MMAs per feature pair (hi.hi + hi.lo + lo.hi, kind::f16):
+    # 6D dense fp16 tensor flops, whose peak is the bf16/fp16 dense rate
     k6_tflops = 6.0 * D * pairs_launch / (k6_ms / 1e3) / 1e12
     pk = peaks()
-    # Denominators from the BURST bf16 figure (TF32 = bf16 x the nominal ratio), the larger of the two
-    # admissible peaks (so the smaller, conservative fraction): K6 runs seconds inside the step under
-    # sw_power_cap, where the sustained bf16 figure (MEASURED_PEAKS median 1312 MHz) under-states it.
-    def mixed_peak(bf16):
-        return 6.0 / (2.0 / (bf16 * NOMINAL_TF32_OVER_BF16) + 4.0 / bf16)
-    tf32_peak = mixed_peak(pk["bf16_tflops"])
-    tf32_peak_sustained = mixed_peak(pk["bf16_tflops_sustained"])
+    tf32_peak = pk["bf16_tflops"]  # fp16 = bf16 dense rate (B200_PROFILING.md)
+    tf32_peak_sustained = pk["bf16_tflops_sustained"]
     tpp, tsrc = k6_traffic_per_pair(D)
     # our kernels launched inside the timed region, summed over the ranks (library-wide counter)
     lt = torch.tensor([float(lc1 - lc0)], dtype=torch.float64, device=dev)
@@ -477,26 +472,24 @@ def run_ours(args, rank: int, world: int):
         "exact": {"dist": ex["dist"], "a": ex["a"], "b": ex["b"], "Gpair_s_kernel": pairs_launch / k6_ms / 1e6},
         "undirected": undirected, "k6_literal_3xtf32": lit, "kernels": kernels,
         "roofline": {"bound": "tensor",
-                     "kernel": ("K6 dist_rowmin_2a_kernel (two 128-row A blocks per CTA; tcgen05 kind::tf32 "
-                                "hi.hi + kind::f16 bf16 pair correction)"),
+                     "kernel": ("K6 dist_rowmin_2a_kernel (two 128-row A blocks per CTA; tcgen05 kind::f16, "
+                                "three fp16 MMAs hi.hi + hi.lo + lo.hi on power-of-two-scaled split operands)"),
                      "achieved": k6_tflops, "peak": tf32_peak_sustained, "peak_kind": "sustained",
                      "unit": "TFLOP/s", "frac": k6_tflops / tf32_peak_sustained,
                      "peak_burst": tf32_peak, "frac_burst": k6_tflops / tf32_peak,
                      # the north star's yardstick: 3xTF32-equivalent work (6D TF32 flops per pair) against
-                     # the dense TF32 peak. The kernel executes 2D TF32 + 4D bf16 flops per pair (one TF32
-                     # and one bf16 MMA instead of three TF32 MMAs), so this ratio is NOT a utilisation and
-                     # may exceed 1; `frac` (executed work / mixed peak) is.
+                     # the dense TF32 peak. The kernel executes the same 3-term split on fp16 MMAs (twice the
+                     # TF32 rate), so this ratio is NOT a utilisation and may exceed 1; `frac` is.
                      "frac_vs_3xtf32_roofline": k6_tflops / (pk["bf16_tflops"] * NOMINAL_TF32_OVER_BF16),
                      "traffic": (tpp * pairs_launch) if tpp else None,
                      "traffic_note": ("DRAM bytes per launch from the ncu capture; the compulsory operand bytes are "
                                       "~8D B per point of A and B (hi + pairs), B is re-streamed once per wave of "
                                       "row blocks (L2 holds 126 MB), harmless to a tensor-bound kernel"),
-                     "note": ("achieved = 6*D executed tensor flops per pair (2*D TF32 + 4*D bf16) x pairs per "
-                              "launch / mean launch time from CUDA events on the launch stream; peak = the mixed "
-                              "rate 6/(2/P_tf32 + 4/P_bf16) with P_bf16 = "
-                              f"{pk['source']} bf16 SUSTAINED {pk['bf16_tflops_sustained']} (K6 is one multi-second "
-                              f"launch inside the step) and P_tf32 = P_bf16 x nominal {NOMINAL_TF32_OVER_BF16:.4f}; "
-                              f"against the burst figure {pk['bf16_tflops']}: peak_burst / frac_burst"),
+                     "note": ("achieved = 6*D executed fp16 tensor flops per pair (3 MMAs x 2D) x pairs per "
+                              "launch / mean launch time from CUDA events on the launch stream; peak = "
+                              f"{pk['source']} bf16 (= fp16 dense rate) SUSTAINED {pk['bf16_tflops_sustained']} (K6 is "
+                              f"one multi-second launch inside the step); against the burst figure "
+                              f"{pk['bf16_tflops']}: peak_burst / frac_burst"),
                      "launch_ms": k6_ms},
         "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }

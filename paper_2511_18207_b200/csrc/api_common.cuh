@@ -100,14 +100,16 @@ struct Carver {
   }
 };
 
-// Operands of one point set for the distance kernel.
+// Operands of one point set for the distance kernel (K0 output).
 struct SetOps {
-  const float* x = nullptr;  // device copy of the fp32 input (D stride)
-  float* hi = nullptr;      // TF32-truncated fp32 (K0)
-  uint32_t* pr = nullptr;  // bf16 pairs (hi, lo): row-operand role
-  uint32_t* pc = nullptr;  // bf16 pairs (lo, hi): column-operand role
-  float* norms = nullptr;  // padded to kBN with +inf
+  const float* x = nullptr;     // device copy of the fp32 input (D stride)
+  void* H = nullptr;            // split hi (fp16 of the scaled coordinates, or fp32 RN-TF32)
+  void* L = nullptr;            // split lo
+  float* norms = nullptr;       // ||y||^2, padded to kBN with +inf
+  float* scale = nullptr;       // per-row power-of-two scale (F16), padded to kBN
+  PrepStats* stats = nullptr;   // max |y|, min ||y||^2 of the set
   int64_t n = 0;
+  bool f16 = true;
 };
 
 struct ExactWs {
@@ -126,12 +128,13 @@ struct ExactWs {
 };
 
 inline void carve_set(Carver& c, SetOps& s, int64_t n, int D) {
-  const int Dp = pad_dim(D);
+  const int Dp = k6_stride_f32(D);  // room for either format (fp16 uses half)
   s.n = n;
-  s.hi = c.take<float>(n * Dp);
-  s.pr = c.take<uint32_t>(n * Dp);
-  s.pc = c.take<uint32_t>(n * Dp);
+  s.H = c.take<float>(n * Dp);
+  s.L = c.take<float>(n * Dp);
   s.norms = c.take<float>(round_up(n, kBN));
+  s.scale = c.take<float>(round_up(n, kBN));
+  s.stats = c.take<PrepStats>(1);
 }
 
 inline size_t carve_exact(Carver& c, ExactWs& w, int64_t nA, int64_t nB, int D, bool host_inputs) {
@@ -277,11 +280,28 @@ inline int stage_inputs(prohd_ctx* ctx, const float*& A, int64_t nA, const float
   return rc;
 }
 
-inline int prep_set(prohd_ctx* ctx, const float* X, int64_t n, int D, SetOps& s, int* bad,
-                    const double* centre) {
-  s.x = X;
+// K0 for the two sets of a pair (the sets a K6 sweep will meet): stats of both first (the F16
+// scale mode depends on both), then the split arrays of each. The sets' operands may be used in
+// either role (row or column) against each other.
+inline int prep_pair(prohd_ctx* ctx, const float* X, int64_t nX, const float* Y, int64_t nY, int D, SetOps& sx,
+                     SetOps& sy, int* bad, const double* centre) {
+  const bool f16 = !k6_split3();
+  SetOps* ops[2] = {&sx, &sy};
+  const float* src[2] = {X, Y};
+  const int64_t n[2] = {nX, nY};
   const int t0 = tmark(ctx);
-  CK(launch_prep(X, n, D, pad_dim(D), round_up(n, kBN), centre, s.hi, s.pr, s.pc, s.norms, bad, ctx->stream));
+  for (int i = 0; i < 2; ++i) {
+    ops[i]->x = src[i];
+    ops[i]->n = n[i];
+    ops[i]->f16 = f16;
+    CK(cudaMemsetAsync(&ops[i]->stats->maxabs, 0, sizeof(unsigned), ctx->stream));
+    CK(cudaMemsetAsync(&ops[i]->stats->minnorm2, 0x7F, sizeof(unsigned), ctx->stream));  // 3.39e38
+    CK(launch_prep_stats(src[i], nullptr, n[i], D, round_up(n[i], kBN), centre, ops[i]->norms, ops[i]->stats, bad,
+                         ctx->stream));
+  }
+  for (int i = 0; i < 2; ++i)
+    CK(launch_prep_write(src[i], nullptr, n[i], D, round_up(n[i], kBN), centre, ops[i]->stats, ops[1 - i]->stats,
+                         f16, ops[i]->H, ops[i]->L, ops[i]->scale, ctx->stream));
   tspan(ctx, PH_PREP, t0);
   return PROHD_OK;
 }
@@ -291,20 +311,25 @@ inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, flo
                     float* colmin = nullptr) {
   CUtensorMap maps[4];
   char err[256];
-  const int Dp = pad_dim(D);
-  const int bi = dist_box_inner(D, colmin != nullptr), br = dist_b_box_rows(D, colmin != nullptr);
-  if (!make_tmap_2d(&maps[0], R.hi, R.n, Dp, kBM, err, sizeof err, bi) ||
-      !make_tmap_2d(&maps[1], reinterpret_cast<const float*>(R.pr), R.n, Dp, kBM, err, sizeof err, bi) ||
-      !make_tmap_2d(&maps[2], C.hi, C.n, Dp, br, err, sizeof err, bi) ||
-      !make_tmap_2d(&maps[3], reinterpret_cast<const float*>(C.pc), C.n, Dp, br, err, sizeof err, bi))
+  // 64-byte TMA box rows (SWIZZLE_64B) over the split arrays, described as fp32 columns
+  const int cols = R.f16 ? k6_stride_f16(D) / 2 : k6_stride_f32(D);
+  if (!make_tmap_2d(&maps[0], reinterpret_cast<const float*>(R.H), R.n, cols, kBM, err, sizeof err, 16) ||
+      !make_tmap_2d(&maps[1], reinterpret_cast<const float*>(R.L), R.n, cols, kBM, err, sizeof err, 16) ||
+      !make_tmap_2d(&maps[2], reinterpret_cast<const float*>(C.H), C.n, cols, kBN, err, sizeof err, 16) ||
+      !make_tmap_2d(&maps[3], reinterpret_cast<const float*>(C.L), C.n, cols, kBN, err, sizeof err, 16))
     return fail(ctx, PROHD_E_CUDA, "%s", err);
   DistArgs a;
   a.maps = maps;
   a.nA = R.n;
   a.nB = C.n;
   a.D = D;
+  a.f16 = R.f16;
   a.na = R.norms;
   a.nb = C.norms;
+  a.sa = R.scale;
+  a.sb = C.scale;
+  a.sta = R.stats;
+  a.stb = C.stats;
   a.rowmin = rowmin;
   a.num_sms = ctx->num_sms;
   a.colmin = colmin;

@@ -50,16 +50,46 @@ constexpr int kBK = 32;   // fp32 K elements per pipeline chunk (one 128-B swizz
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int pad_dim(int D) { return static_cast<int>(round_up(D, 4)); }  // 16-B TMA row stride
 
-// K0: split points, translated by a common centre c (fp64, D; nullptr = none), into the K6
-// operands: y = x - c in fp64, hi = fp32(y) rounded to nearest TF32 (low 13 mantissa bits
-// zero), lo = fp32(y - hi), pr[f] = bf16 pair (hi_f, lo_f) and pc[f] = (lo_f, hi_f) (element
-// 2f at the lower address), and ||y||^2 accumulated in fp64. hi/pr/pc rows have stride Dp
-// (zero padded); norms[i] = ||y_i||^2 for i < n and +inf for n <= i < n_pad. *bad = 1 if any
-// x or norm is not finite.
-cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, const double* centre, float* hi,
-                        uint32_t* pr, uint32_t* pc, float* norms, int* bad, cudaStream_t st);
-// option k6_split3 = 1: the north star's literal 3xTF32 form (hi.hi + hi.lo + lo.hi, three TF32
-// MMAs); K0 then writes lo (fp32) into pr and pc instead of the bf16 pairs. Default: off.
+// K0 (k_prep.cu): the K6 operands of one point set. y = x - c (fp64, c the pair's common centre,
+// nullptr = none); three-term split arrays H (hi) and L (lo), row stride k6_stride_*(D) elements,
+// zero padded:
+//   F16  (default):          hi = fp16_rn(s y), lo = fp16_rn(s y - hi), s = scale[i] (power of two)
+//   TF32 (option k6_split3): hi = rn_tf32(y), lo = fp32(y - hi), scale[i] = 1
+// norms[i] = ||y_i||^2 (fp32 from fp64) for i < n, +inf for n <= i < n_pad. *bad = 1 if any x or
+// norm is not finite. The stats pass must run on BOTH sets of a pair before either write pass
+// (the F16 scale mode depends on both).
+struct PrepStats {
+  unsigned maxabs;    // float bits of max_i,f |y_if| (0 = none yet)
+  unsigned minnorm2;  // float bits of min_i ||y_i||^2 (+inf = none yet)
+};
+inline int k6_stride_f16(int D) { return static_cast<int>(round_up(D, 8)); }  // halfs: 16-B row stride
+inline int k6_stride_f32(int D) { return static_cast<int>(round_up(D, 4)); }  // floats
+// power-of-two scale putting max |y| into (2^13, 2^14] (1 for 0 / non-finite; clamped to 2^+-60)
+__host__ __device__ inline float prep_scale_for(float M) {
+  if (!(M > 0.0f) || !(M < 3.0e38f)) return 1.0f;
+  int e = 0;
+  (void)frexpf(M, &e);  // M = m 2^e, m in [0.5, 1)
+  int k = 14 - e;
+  k = k < -60 ? -60 : (k > 60 ? 60 : k);
+  return ldexpf(1.0f, k);
+}
+// F16 scale mode of a pair: ONE scale per set (s_X from the set's max |y|) unless some row is so
+// small against the pair's largest coordinate M that the fp16 subnormal floor (2^-25 / s_X per
+// coordinate, <= 2^-38 M) could cost more than 3e-6 of the pair's ||a||^2 + ||b||^2:
+// rows need sqrt(||a||^2+||b||^2) >= 2^-37 sqrt(2D) M / 3e-6 = 2.43e-6 sqrt(2D) M. Otherwise one
+// scale per ROW (every row at the top of the fp16 range; K6's epilogue then rescales per column).
+__device__ __forceinline__ bool prep_mode_perrow(const PrepStats* a, const PrepStats* b, int D) {
+  const float M = fmaxf(__uint_as_float(a->maxabs), __uint_as_float(b->maxabs));
+  const float mn2 = fminf(__uint_as_float(a->minnorm2), __uint_as_float(b->minnorm2));
+  return !(sqrtf(mn2) >= 2.43e-6f * sqrtf(2.0f * static_cast<float>(D)) * M);
+}
+cudaError_t launch_prep_stats(const float* X, const long long* idx, int64_t n, int D, int64_t n_pad,
+                              const double* centre, float* norms, PrepStats* st, int* bad, cudaStream_t stream);
+cudaError_t launch_prep_write(const float* X, const long long* idx, int64_t n, int D, int64_t n_pad,
+                              const double* centre, const PrepStats* self, const PrepStats* other, bool f16, void* H,
+                              void* L, float* scale, cudaStream_t stream);
+// option k6_split3 = 1: the north star's literal 3xTF32 form (fp32 hi/lo, three TF32 MMAs)
+// instead of the default three fp16 MMAs on scaled fp16 hi/lo.
 bool k6_split3();
 // Common centre of a pair (X, Y): fp64 mean of the first min(nX, 4096) rows of X and the
 // first min(nY, 4096) rows of Y (either count may be 0), summed per set and then added,
@@ -68,21 +98,22 @@ cudaError_t launch_centre(const float* X, int64_t nX, const float* Y, int64_t nY
                           cudaStream_t st);
 
 struct DistArgs {
-  const CUtensorMap* maps;  // [A_hi, A_pr, B_hi, B_pc]
+  const CUtensorMap* maps;  // [A_H, A_L, B_H, B_L]: 64-B box rows (32 fp16 or 16 fp32 features)
   int64_t nA, nB;
   int D;
-  const float* na;  // row-operand norms
-  const float* nb;  // column-operand norms, padded to a multiple of kBN with +inf
-  float* rowmin;    // out: min_j d2(i, j), clamped >= 0
+  bool f16;                 // operand format (K0): F16 (scaled fp16) or TF32
+  const float* na;          // row-operand norms
+  const float* nb;          // column-operand norms, padded to a multiple of kBN with +inf
+  const float* sa;          // row-operand scales (K0), n_pad
+  const float* sb;          // column-operand scales, padded to a multiple of kBN
+  const PrepStats* sta;     // stats of both sets (F16 scale mode)
+  const PrepStats* stb;
+  float* rowmin;            // out: min_j d2(i, j), clamped >= 0
   int num_sms;
   float* colmin = nullptr;  // optional out (fused bidirectional pass): min_i d2(i, j), clamped >= 0
 };
-// K6: fused 3xTF32 tcgen05 distance + row-min kernel.
+// K6: fused split-precision tcgen05 distance + row-min kernel.
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st);
-// rows per TMA box of the column operand for the selected K6 variant (256: 1-SM, 128: 2-SM pair)
-int dist_b_box_rows(int D, bool bidir);
-// fp32 features per TMA box row of the selected K6 variant (32: SWIZZLE_128B; 16: SWIZZLE_64B)
-int dist_box_inner(int D, bool bidir);
 
 // K7a: packed max key over rows: (bits(d2) << 32) | (0xFFFFFFFF - (row + row_offset)).
 cudaError_t launch_rowmax_key(const float* rowmin, int64_t n, int64_t row_offset, unsigned long long* key,

@@ -1,50 +1,47 @@
-// k_dist.cu — K6: fused 3xTF32 tcgen05 distance + row-minimum kernel.
+// k_dist.cu — K6: fused split-precision tcgen05 distance + row-minimum kernel.
 //
 // Computes, for every row a_i of the row operand A and all columns b_j of B,
-//     v_ij = ||b_j||^2 - 2 a_i . b_j        (a_i . b_j on tcgen05, 3xTF32)
+//     v_ij = ||b_j||^2 - 2 a_i . b_j        (a_i . b_j on tcgen05)
 //     rowmin_i = max(0, ||a_i||^2 + min_j v_ij)
 // which is min_j ||a_i - b_j||^2 (Eq. (1), inner min). The
 // n_A x n_B distance matrix never leaves TMEM/registers.
 //
-// Split products (SURVEY.md §8(a) "shared fused distance kernel"): with x = hi + lo,
-// hi = x rounded to nearest TF32 (11 significant bits, K0) and lo = x - hi (|lo| <= 2^-11 |x|),
-//   a.b ~= hi_a.hi_b                      one kind::tf32 MMA per 8 features
-//        + [hi_a lo_a].[lo_b hi_b]        one kind::f16 MMA (bf16) per 8 features,
-// the second over interleaved bf16 pairs (K doubled) so that a single instruction forms both
-// correction terms hi_a.lo_b + lo_a.hi_b. Both accumulate into one fp32 TMEM accumulator.
-// Error per product a_i b_i (hi.hi and the bf16 products are exact; bf16 unit roundoff
-// u = 2^-8, applied to hi and to lo in each correction term):
-//   |hi_a lo_b - bf16(hi_a) bf16(lo_b)| <= (2u + u^2)|hi_a||lo_b| <= (2^-7 + 2^-16)(1 + 2^-11) 2^-11 |a_i||b_i|
-// twice, plus the dropped lo_a.lo_b <= 2^-22 |a_i||b_i|: in all <= 7.9e-6 |a_i||b_i| (an
-// exhaustive emulation over all 2^23 mantissas of a_i = b_i gives at most 5.9e-6). So
-// |a.b - dot| <= 7.9e-6 ||a|| ||b|| and |d2 - d2_exact| <= 7.9e-6 (||a||^2 + ||b||^2) plus the
-// fp32 accumulation (<= ~1.9e-6 of the same norms for D/8 accumulator updates at D = 256 in the
-// aligned worst case), inside the 1e-5 budget of BASELINE.json (Q17); the centring of K0 shrinks
-// the norms further. (With truncated hi, |lo| < 2^-10 |x|, the worst case was 1.22e-5 of the
-// product: tests/test_gpu_exact.py::test_split_worst_case_mantissas.)
-// Against 3xTF32 (three TF32 MMAs) the tensor time per pair drops from 6D/P_tf32 to
-// 2D/P_tf32 + 4D/P_bf16 (P_bf16 ~ 2 P_tf32): ~1.5x.
+// Split products (SURVEY.md §8(a) "shared fused distance kernel"): K0 writes each coordinate y
+// (centred) as hi + lo on two arrays H and L, and each 32-byte K-step issues THREE MMAs into
+// one fp32 TMEM accumulator, hi_a.hi_b + hi_a.lo_b + lo_a.hi_b (lo.lo dropped):
+//   F16 (default):  kind::f16 on fp16 hi/lo of the power-of-two-scaled coordinates s*y, 16
+//                   features per K-step. hi has 11 significant bits and lo the next 11, the same
+//                   split as 3xTF32, at twice the TF32 tensor rate and half its operand bytes.
+//                   Error per product <= 3 2^-22 |a_i||b_i| (lo's fp16 rounding on both sides,
+//                   the dropped lo.lo), plus the fp16 subnormal floor 2^-25/s per coordinate that
+//                   K0's scale mode keeps below 3e-6 of ||a||^2+||b||^2 (internal.cuh).
+//   TF32 (option k6_split3, the literal north-star 3xTF32): kind::tf32 on fp32 hi (RN to TF32)
+//                   and lo, 8 features per K-step.
+// The accumulator is scaled by s_i s_j (row and column scales, powers of two, exact): the
+// epilogue forms v_ij = fma(-2 / (s_i s_j), acc_ij, ||b_j||^2) — with one scale per set that is
+// a per-row constant (the same two instructions per element as unscaled); with per-row scales
+// (K0's wide-dynamic-range mode) one extra multiply by 1/s_j per element.
+// fp32 accumulation (the tensor core truncates each MMA's sum to the accumulator's precision)
+// adds up to ~2^-23 |acc| per MMA; measured on constant-mantissa rows (tools/split_probe.py)
+// this is the dominant term at D = 256.
 //
-// Structure (persistent, 1 CTA per SM, warp-specialised; 320 threads for the single-block and
-// two-A kernels, 192 for the opt-in 2-SM pair):
-//   warp 0      TMA producer: per K-chunk it loads the A and B hi / pair tiles into a smem
-//               ring (single block: 32 fp32 = one 128-B swizzle row, [128 x 32] A and [256 x 32]
-//               B, 2 stages of 96 KB; two-A: 16-feature SWIZZLE_64B stages x3).
-//   warp 1      TMEM allocator (512 columns) and MMA issuer: all 32 lanes run the issue loop and
-//               an elect.sync predicate inside the tcgen05.mma / commit asm picks the issuing
+// Structure (persistent, 1 CTA per SM, warp-specialised, 320 threads):
+//   warp 0      TMA producer: 64-byte box rows (32 fp16 or 16 fp32 features), SWIZZLE_64B,
+//               H and L tiles of A and B per stage.
+//   warp 1      TMEM allocator (512 columns) and MMA issuer: all 32 lanes run the issue loop
+//               and an elect.sync predicate inside the tcgen05.mma / commit asm picks the issuing
 //               lane (kElect; the fused bidirectional sweep below D = 192 keeps a lane-0 issuer).
-//               tcgen05.mma.cta_group::1 M=128, N=256: per 8 features one kind::tf32 MMA (K=8)
-//               and one kind::f16 bf16 MMA (K=16 over the pairs); commit -> smem slot free,
-//               commit -> accumulator full.
-//   warps 2-9   epilogue (8 warps): tcgen05.ld 32x32b.x32 (one TMEM lane = one row per thread;
-//               two warps per lane quarter, each one 128-column half of the tile in the single-
-//               block kernel, one accumulator per group of 4 warps in the two-A kernel),
-//               v = fma(-2, acc, ||b||^2), running min in a register across all B tiles of the
-//               unit; the single-block accumulator is double buffered so the epilogue of tile t
-//               overlaps the MMAs of t+1.
-// Work unit = (128-row block of A, contiguous range of B tiles). With one range
-// the row minimum is stored; with several (small n_A) it is combined with an
-// integer atomicMin on the float bits (valid since d2 >= 0).
+//   warps 2-9   epilogue (8 warps): tcgen05.ld 32x32b.x32 (one TMEM lane = one row per thread),
+//               v = fma(k_i, acc, ||b||^2), running min in a register across all B tiles of the
+//               unit.
+// Two kernels: the single-block kernel (one 128-row block of A per CTA, M=128 N=256, the
+// accumulator double-buffered so the epilogue of tile t overlaps the MMAs of t+1; 4 stages of
+// 48 KB) and the two-A kernel (two 128-row blocks against each B tile, both accumulators = all
+// 512 TMEM columns, 3 stages of 64 KB: 2/3 of the operand bytes per pair), used for directed
+// sweeps at D >= 128.
+// Work unit = (row block, contiguous range of B tiles). With one range the row minimum is
+// stored; with several (small n_A) it is combined with an integer atomicMin on the float bits
+// (valid since d2 >= 0).
 #include "internal.cuh"
 #include "sm100.cuh"
 
@@ -54,22 +51,54 @@
 namespace prohd {
 namespace {
 
-constexpr int kStages = 2;
-constexpr int kThreads = 192;   // 2-SM kernel: TMA, MMA, 4 epilogue warps
-constexpr int kThreads1 = 320;  // single-block kernel: TMA, MMA, 8 epilogue warps (two column halves)
-constexpr uint32_t kATile = kBM * kBK * 4;                  // 16 KB
-constexpr uint32_t kBTile = kBN * kBK * 4;                  // 32 KB
-constexpr uint32_t kStageBytes = 2 * kATile + 2 * kBTile;   // 96 KB
+constexpr uint32_t kRowBytes = 64;                      // one SWIZZLE_64B box row
+constexpr uint32_t kATile = kBM * kRowBytes;           // 8 KB: 128 rows
+constexpr uint32_t kBTile = kBN * kRowBytes;           // 16 KB: 256 rows
 constexpr uint32_t kTmemCols = 512;
-constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + 1024 + 256;
+constexpr int kThreads1 = 320;  // TMA, MMA, 8 epilogue warps
+constexpr int kStages1 = 4;
+constexpr uint32_t kStage1Bytes = 2 * kATile + 2 * kBTile;  // 48 KB: A_H, A_L, B_H, B_L
+constexpr size_t kSmem1 = static_cast<size_t>(kStages1) * kStage1Bytes + 1024 + 256;
+constexpr int kThreadsA2 = 320;
+constexpr int kStagesA2 = 3;
+constexpr uint32_t kStageA2Bytes = 4 * kATile + 2 * kBTile;  // 64 KB: A1_H, A1_L, A2_H, A2_L, B_H, B_L
+constexpr size_t kSmemA2 = static_cast<size_t>(kStagesA2) * kStageA2Bytes + 1024 + 256;
 
 struct Sched {
-  int split3;  // k6_split3(): three TF32 MMAs (hi.hi, hi.lo, lo.hi) on fp32 lo tiles
   int64_t nA, nB;
-  int nrb, nt, nsplit, tps, nk, ks_last;  // nk, ks_last: 32-feature chunks
-  int nk1, ks_last1;                      // 16-feature chunks (two-A-block variant)
+  int nrb, nt, nsplit, tps;
+  int nk, ks_last;  // 64-byte stages over the features, 32-byte K-steps in the last stage
   int atomic_out;
+  int D;
 };
+
+// the three split MMAs of one 32-byte K-step into accumulator d
+template <bool kF16, bool kElect>
+__device__ __forceinline__ void mma3(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl, uint32_t acc) {
+  using namespace sm100;
+  constexpr uint32_t id = kF16 ? idesc_f16(kBM, kBN) : idesc_tf32(kBM, kBN);
+  if constexpr (kF16) {
+    if constexpr (kElect) {
+      mma_bf16_w(d, ah, bh, id, acc);  // kind::f16; the idesc selects fp16 operands
+      mma_bf16_w(d, ah, bl, id, 1u);
+      mma_bf16_w(d, al, bh, id, 1u);
+    } else {
+      mma_bf16(d, ah, bh, id, acc);
+      mma_bf16(d, ah, bl, id, 1u);
+      mma_bf16(d, al, bh, id, 1u);
+    }
+  } else {
+    if constexpr (kElect) {
+      mma_tf32_w(d, ah, bh, id, acc);
+      mma_tf32_w(d, ah, bl, id, 1u);
+      mma_tf32_w(d, al, bh, id, 1u);
+    } else {
+      mma_tf32(d, ah, bh, id, acc);
+      mma_tf32(d, ah, bl, id, 1u);
+      mma_tf32(d, al, bh, id, 1u);
+    }
+  }
+}
 
 // butterfly reduce-scatter: lane L ends with min over the warp's 32 lanes of v[L] in v[0]
 __device__ __forceinline__ void warp_colmin32(float (&v)[32], int lane) {
@@ -86,26 +115,68 @@ __device__ __forceinline__ void warp_colmin32(float (&v)[32], int lane) {
   }
 }
 
+// Epilogue helpers. Scale factors: global mode k = -2 / (s_i s_B) per row; per-row mode
+// k = -2 / s_i and u_j = 1 / s_j per column (staged with the column norms).
+struct EpiScale {
+  bool perrow;
+  float k;  // this thread's row factor
+};
+__device__ __forceinline__ EpiScale epi_scale(bool f16, const PrepStats* sta, const PrepStats* stb, const float* sa,
+                                              const float* sb, int64_t row, int64_t nA, int D) {
+  EpiScale e{false, -2.0f};
+  if (!f16) return e;
+  e.perrow = prep_mode_perrow(sta, stb, D);
+  const float si = row < nA ? __ldg(sa + row) : 1.0f;
+  e.k = e.perrow ? -2.0f / si : (-2.0f / si) / __ldg(sb);
+  return e;
+}
+
+// v[0..31] <- fma(k, acc (* u_j), ||b_j||^2) for one 32-column chunk; returns the chunk minimum
+template <bool kPerRow>
+__device__ __forceinline__ float epi_chunk(float (&v)[32], float k, const float4* nbp, const float4* ubp) {
+  float m[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 n4 = nbp[i];
+    if constexpr (kPerRow) {
+      const float4 u4 = ubp[i];
+      v[4 * i + 0] = fmaf(k, v[4 * i + 0] * u4.x, n4.x);
+      v[4 * i + 1] = fmaf(k, v[4 * i + 1] * u4.y, n4.y);
+      v[4 * i + 2] = fmaf(k, v[4 * i + 2] * u4.z, n4.z);
+      v[4 * i + 3] = fmaf(k, v[4 * i + 3] * u4.w, n4.w);
+    } else {
+      v[4 * i + 0] = fmaf(k, v[4 * i + 0], n4.x);
+      v[4 * i + 1] = fmaf(k, v[4 * i + 1], n4.y);
+      v[4 * i + 2] = fmaf(k, v[4 * i + 2], n4.z);
+      v[4 * i + 3] = fmaf(k, v[4 * i + 3], n4.w);
+    }
+    m[i] = fminf(fminf(v[4 * i + 0], v[4 * i + 1]), fminf(v[4 * i + 2], v[4 * i + 3]));
+  }
+  return fminf(fminf(fminf(m[0], m[1]), fminf(m[2], m[3])), fminf(fminf(m[4], m[5]), fminf(m[6], m[7])));
+}
+
 // kBidir: the same sweep also produces column minima
 // colmin[j] = min_i ||a_i - b_j||^2 (the B->A direction). Per 32-column chunk each warp
-// reduces its 32 rows with a butterfly reduce-scatter, the 4 warps combine in shared
+// reduces its 32 rows with a butterfly reduce-scatter, the warps combine in shared
 // memory, and the last warp of the tile flushes the 256 minima with global atomicMin.
-template <bool kBidir, bool kElect>
+template <bool kBidir, bool kElect, bool kF16>
 __global__ void __launch_bounds__(kThreads1, 1)
     dist_rowmin_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                        const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
-                       const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin,
-                       float* __restrict__ colmin) {
+                       const float* __restrict__ na, const float* __restrict__ nb, const float* __restrict__ sa,
+                       const float* __restrict__ sb, const PrepStats* sta, const PrepStats* stb,
+                       float* __restrict__ rowmin, float* __restrict__ colmin) {
   using namespace sm100;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages1 * kStage1Bytes);
+  uint64_t* empty = full + kStages1;
+  uint64_t* tfull = empty + kStages1;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ unsigned colbuf[2][kBN];  // kBidir: per-accumulator column minima (float bits)
   __shared__ __align__(16) float nbuf[2][kBN];  // column norms of the tile in each accumulator
+  __shared__ __align__(16) float ubuf[2][kBN];  // per-row scale mode: 1 / s_j of the tile's columns
   __shared__ unsigned tilecnt[2];
   __shared__ float rbuf[kBM];  // row minima of the second column half, combined at the unit's end
 
@@ -116,7 +187,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     if (threadIdx.x < 2) tilecnt[threadIdx.x] = 0u;
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kStages1; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -151,13 +222,13 @@ __global__ void __launch_bounds__(kThreads1, 1)
         for (int t = t0; t < t1; ++t) {
           for (int c = 0; c < s.nk; ++c) {
             mbar_wait(&empty[stage], phase ^ 1u);
-            uint8_t* st = smem + stage * kStageBytes;
-            mbar_arrive_expect_tx(&full[stage], kStageBytes);
-            tma_load_2d(st, &tAh, c * kBK, rb * kBM, &full[stage]);
-            tma_load_2d(st + kATile, &tAl, c * kBK, rb * kBM, &full[stage]);
-            tma_load_2d(st + 2 * kATile, &tBh, c * kBK, t * kBN, &full[stage]);
-            tma_load_2d(st + 2 * kATile + kBTile, &tBl, c * kBK, t * kBN, &full[stage]);
-            if (++stage == kStages) {
+            uint8_t* st = smem + stage * kStage1Bytes;
+            mbar_arrive_expect_tx(&full[stage], kStage1Bytes);
+            tma_load_2d(st, &tAh, c * 16, rb * kBM, &full[stage]);
+            tma_load_2d(st + kATile, &tAl, c * 16, rb * kBM, &full[stage]);
+            tma_load_2d(st + 2 * kATile, &tBh, c * 16, t * kBN, &full[stage]);
+            tma_load_2d(st + 2 * kATile + kBTile, &tBl, c * 16, t * kBN, &full[stage]);
+            if (++stage == kStages1) {
               stage = 0;
               phase ^= 1u;
             }
@@ -169,19 +240,11 @@ __global__ void __launch_bounds__(kThreads1, 1)
   } else if (warp == 1) {
     // kElect: warp-wide issue with an elected lane (sm100.cuh mma_*_w); else lane 0 issues
     // (measured faster for the fused bidirectional sweep at D = 128, §7.1)
-    auto mtf32 = [](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t ac) {
-      if constexpr (kElect) mma_tf32_w(d, a, b, id, ac); else mma_tf32(d, a, b, id, ac);
-    };
-    auto mbf16 = [](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t ac) {
-      if constexpr (kElect) mma_bf16_w(d, a, b, id, ac); else mma_bf16(d, a, b, id, ac);
-    };
     auto mcommit = [](uint64_t* bar) {
       if constexpr (kElect) mma_commit_w(bar); else mma_commit(bar);
     };
     if (kElect || lane == 0) {
       // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
-      constexpr uint32_t idesc16 = idesc_bf16(kBM, kBN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -197,27 +260,18 @@ __global__ void __launch_bounds__(kThreads1, 1)
           for (int c = 0; c < s.nk; ++c) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t ah = smem_u32(smem + stage * kStageBytes);
+            const uint32_t ah = smem_u32(smem + stage * kStage1Bytes);
             const uint32_t al = ah + kATile;
             const uint32_t bh = ah + 2 * kATile;
             const uint32_t bl = bh + kBTile;
-            const int ks = (c == s.nk - 1) ? s.ks_last : (kBK / 8);
+            const int ks = (c == s.nk - 1) ? s.ks_last : 2;
             for (int kk = 0; kk < ks; ++kk) {
-              const uint32_t off = static_cast<uint32_t>(kk * 32);  // 8 tf32 = 32 B along K
-              const uint64_t dah = smem_desc_k_sw128(ah + off);
-              const uint64_t dal = smem_desc_k_sw128(al + off);
-              const uint64_t dbh = smem_desc_k_sw128(bh + off);
-              const uint64_t dbl = smem_desc_k_sw128(bl + off);
-              mtf32(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
-              if (s.split3) {
-                mtf32(d, dah, dbl, idesc, 1u);  // hi_a . lo_b
-                mtf32(d, dal, dbh, idesc, 1u);  // lo_a . hi_b
-              } else {
-                mbf16(d, dal, dbl, idesc16, 1u);  // [hi lo]_a . [lo hi]_b
-              }
+              const uint32_t off = static_cast<uint32_t>(kk * 32);  // 16 fp16 / 8 tf32 along K
+              mma3<kF16, kElect>(d, smem_desc_k_sw64(ah + off), smem_desc_k_sw64(al + off),
+                                 smem_desc_k_sw64(bh + off), smem_desc_k_sw64(bl + off), (c | kk) != 0 ? 1u : 0u);
             }
             mcommit(&empty[stage]);
-            if (++stage == kStages) {
+            if (++stage == kStages1) {
               stage = 0;
               phase ^= 1u;
             }
@@ -239,6 +293,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     const int row_local = q * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
     const int e = (warp - 2) * 32 + lane;  // 0..255: one column norm each
+    const bool perrow = kF16 && prep_mode_perrow(sta, stb, s.D);
     int acc = 0;
     uint32_t aphase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -247,34 +302,29 @@ __global__ void __launch_bounds__(kThreads1, 1)
       const int t1 = min(s.nt, t0 + s.tps);
       float rmin = __int_as_float(0x7f800000);
       const int64_t row = static_cast<int64_t>(rb) * kBM + row_local;
+      const EpiScale es = epi_scale(kF16, sta, stb, sa, sb, row, s.nA, s.D);
       // kBidir: this row's ||a||^2, or +inf for rows past nA (excluded from column minima)
       const float narow = kBidir ? (row < s.nA ? __ldg(na + row) : __int_as_float(0x7f800000)) : 0.0f;
       for (int t = t0; t < t1; ++t) {
-        // the tile's column norms: loaded before the accumulator wait, staged in shared memory,
-        // read back as broadcasts
+        // the tile's column norms (and per-row-mode column factors): loaded before the
+        // accumulator wait, staged in shared memory, read back as broadcasts
         {
-          const float n1 = __ldg(nb + static_cast<int64_t>(t) * kBN + e);
+          const int64_t col = static_cast<int64_t>(t) * kBN + e;
+          const float n1 = __ldg(nb + col);
+          const float u1 = perrow ? 1.0f / __ldg(sb + col) : 1.0f;
           mbar_wait(&tfull[acc], aphase);
           nbuf[acc][e] = n1;
+          ubuf[acc][e] = u1;
           asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
         }
         tc_fence_after();
         const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(acc * kBN);
         const float4* nbp = reinterpret_cast<const float4*>(nbuf[acc]);
-        // two 32-column chunks per TMEM wait; the 32 values of a chunk reduce as a tree
+        const float4* ubp = reinterpret_cast<const float4*>(ubuf[acc]);
         auto chunk = [&](float (&v)[32], int cc) {
-          float m[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 n4 = nbp[cc * 8 + i];
-            v[4 * i + 0] = fmaf(-2.0f, v[4 * i + 0], n4.x);
-            v[4 * i + 1] = fmaf(-2.0f, v[4 * i + 1], n4.y);
-            v[4 * i + 2] = fmaf(-2.0f, v[4 * i + 2], n4.z);
-            v[4 * i + 3] = fmaf(-2.0f, v[4 * i + 3], n4.w);
-            m[i] = fminf(fminf(v[4 * i + 0], v[4 * i + 1]), fminf(v[4 * i + 2], v[4 * i + 3]));
-          }
-          rmin = fminf(rmin, fminf(fminf(fminf(m[0], m[1]), fminf(m[2], m[3])),
-                                   fminf(fminf(m[4], m[5]), fminf(m[6], m[7]))));
+          const float m = perrow ? epi_chunk<true>(v, es.k, nbp + cc * 8, ubp + cc * 8)
+                                 : epi_chunk<false>(v, es.k, nbp + cc * 8, ubp + cc * 8);
+          rmin = fminf(rmin, m);
           if (kBidir) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + narow, 0.0f);
@@ -334,236 +384,18 @@ __global__ void __launch_bounds__(kThreads1, 1)
 }
 
 // ============================================================================
-// 2-SM variant (cta_group::2): a CTA pair computes a 256-row block of A against
-// 256-column tiles of B with one M=256, N=256 MMA per K-step. Each CTA stages its
-// own 128 rows of A and its 128-column half of the B tile (64 KB per stage with
-// hi+lo, 3 stages), so per SM the operand traffic per pair drops from 24 B to
-// 16 B and the tensor core reads half as much of each SM's shared memory.
-// Barriers: full[] lives in the leader (rank 0) and counts both CTAs' TMA bytes
-// (2-SM TMA); empty[] and tfull[] exist in both CTAs and are signalled by the
-// leader's multicast tcgen05.commit; tempty[] lives in the leader and counts the
-// 8 epilogue warps of the pair.
+// Two-A-block variant: one CTA computes TWO 128-row blocks of A against each 256-column tile
+// of B, one fp32 accumulator each (all 512 TMEM columns, so the epilogue of a tile is not
+// overlapped with the next tile's MMAs). Stages of 64-byte rows: A1 and A2 H/L 4 x 8 KB + B H/L
+// 2 x 16 KB = 64 KB, three in flight: 2/3 of the single-block kernel's operand bytes per pair.
 // ============================================================================
-constexpr int kStages2 = 3;
-constexpr uint32_t kHalf = 128 * kBK * 4;     // 16 KB: 128 rows x 32 fp32
-constexpr uint32_t kStage2Bytes = 4 * kHalf;  // A_hi, A_lo, B_hi, B_lo halves
-constexpr size_t kSmem2 = static_cast<size_t>(kStages2) * kStage2Bytes + 1024 + 256;
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    dist_rowmin_2sm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
-                           const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
-                           const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin) {
-  using namespace sm100;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStage2Bytes);
-  uint64_t* empty = full + kStages2;
-  uint64_t* tfull = empty + kStages2;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ __align__(16) float nbuf[2][kBN];  // column norms of the tile in each accumulator
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int cid = static_cast<int>(cluster_id_x());
-  const int ncl = static_cast<int>(nclusters_x());
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages2; ++i) {
-      mbar_init(&full[i], 2);
-      mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tAh);
-    tma_prefetch(&tAl);
-    tma_prefetch(&tBh);
-    tma_prefetch(&tBl);
-  }
-  if (warp == 1) tmem_alloc_2sm<kTmemCols>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int units = s.nrb * s.nsplit;  // nrb counts 256-row blocks here
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = cid; u < units; u += ncl) {
-        const int pb = u / s.nsplit, sp = u % s.nsplit;
-        const int t0 = sp * s.tps;
-        const int t1 = min(s.nt, t0 + s.tps);
-        const int arow = pb * 256 + static_cast<int>(rank) * 128;
-        for (int t = t0; t < t1; ++t) {
-          const int brow = t * kBN + static_cast<int>(rank) * 128;
-          for (int c = 0; c < s.nk; ++c) {
-            mbar_wait(&empty[stage], phase ^ 1u);
-            const uint32_t fl = mapa(smem_u32(&full[stage]), 0);
-            if (leader)
-              mbar_arrive_expect_tx(&full[stage], 2 * kStage2Bytes);
-            else
-              mbar_arrive_cluster(fl);
-            uint8_t* st = smem + stage * kStage2Bytes;
-            tma_load_2d_2sm(st, &tAh, c * kBK, arow, fl);
-            tma_load_2d_2sm(st + kHalf, &tAl, c * kBK, arow, fl);
-            tma_load_2d_2sm(st + 2 * kHalf, &tBh, c * kBK, brow, fl);
-            tma_load_2d_2sm(st + 3 * kHalf, &tBl, c * kBK, brow, fl);
-            if (++stage == kStages2) {
-              stage = 0;
-              phase ^= 1u;
-            }
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      constexpr uint32_t idesc = idesc_tf32(256, kBN);
-      constexpr uint32_t idesc16 = idesc_bf16(256, kBN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t aphase = 0;
-      for (int u = cid; u < units; u += ncl) {
-        const int sp = u % s.nsplit;
-        const int t0 = sp * s.tps;
-        const int t1 = min(s.nt, t0 + s.tps);
-        for (int t = t0; t < t1; ++t) {
-          mbar_wait(&tempty[acc], aphase ^ 1u);
-          tc_fence_after();
-          const uint32_t d = tmem_base + static_cast<uint32_t>(acc * kBN);
-          for (int c = 0; c < s.nk; ++c) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t ah = smem_u32(smem + stage * kStage2Bytes);
-            const uint32_t al = ah + kHalf;
-            const uint32_t bh = ah + 2 * kHalf;
-            const uint32_t bl = ah + 3 * kHalf;
-            const int ks = (c == s.nk - 1) ? s.ks_last : (kBK / 8);
-            for (int kk = 0; kk < ks; ++kk) {
-              const uint32_t off = static_cast<uint32_t>(kk * 32);
-              const uint64_t dah = smem_desc_k_sw128(ah + off);
-              const uint64_t dal = smem_desc_k_sw128(al + off);
-              const uint64_t dbh = smem_desc_k_sw128(bh + off);
-              const uint64_t dbl = smem_desc_k_sw128(bl + off);
-              mma_tf32_2sm(d, dah, dbh, idesc, (c | kk) != 0 ? 1u : 0u);  // hi_a . hi_b
-              if (s.split3) {
-                mma_tf32_2sm(d, dah, dbl, idesc, 1u);
-                mma_tf32_2sm(d, dal, dbh, idesc, 1u);
-              } else {
-                mma_bf16_2sm(d, dal, dbl, idesc16, 1u);  // [hi lo]_a . [lo hi]_b
-              }
-            }
-            mma_commit_2sm_mc(&empty[stage], 0x3);
-            if (++stage == kStages2) {
-              stage = 0;
-              phase ^= 1u;
-            }
-          }
-          mma_commit_2sm_mc(&tfull[acc], 0x3);
-          acc ^= 1;
-          if (acc == 0) aphase ^= 1u;
-        }
-      }
-    }
-    __syncwarp();
-  } else {
-    const int q = warp & 3;
-    const int row_local = q * 32 + lane;
-    const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t te[2] = {mapa(smem_u32(&tempty[0]), 0), mapa(smem_u32(&tempty[1]), 0)};
-    int acc = 0;
-    uint32_t aphase = 0;
-    for (int u = cid; u < units; u += ncl) {
-      const int pb = u / s.nsplit, sp = u % s.nsplit;
-      const int t0 = sp * s.tps;
-      const int t1 = min(s.nt, t0 + s.tps);
-      float rmin = __int_as_float(0x7f800000);
-      for (int t = t0; t < t1; ++t) {
-        // the tile's column norms: loaded before the accumulator wait, staged in shared memory
-        // (one 16-B piece per thread per accumulator buffer), read back as broadcasts
-        {
-          const int e = q * 32 + lane;  // 0..127: two floats each
-          const float2 n2 = __ldg(reinterpret_cast<const float2*>(nb + static_cast<int64_t>(t) * kBN) + e);
-          mbar_wait(&tfull[acc], aphase);
-          reinterpret_cast<float2*>(nbuf[acc])[e] = n2;
-          asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
-        }
-        tc_fence_after();
-        const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(acc * kBN);
-        const float4* nbp = reinterpret_cast<const float4*>(nbuf[acc]);
-#pragma unroll 1
-        for (int cc = 0; cc < kBN / 32; ++cc) {
-          float v[32];
-          tmem_ld32(taddr + cc * 32, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 n4 = nbp[cc * 8 + i];
-            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 0], n4.x));
-            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 1], n4.y));
-            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 2], n4.z));
-            rmin = fminf(rmin, fmaf(-2.0f, v[4 * i + 3], n4.w));
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(te[acc]);
-        acc ^= 1;
-        if (acc == 0) aphase ^= 1u;
-      }
-      const int64_t row = static_cast<int64_t>(pb) * 256 + static_cast<int64_t>(rank) * 128 + row_local;
-      if (row < s.nA) {
-        const float d2 = fmaxf(rmin + __ldg(na + row), 0.0f);
-        if (s.atomic_out)
-          atomicMin(reinterpret_cast<int*>(rowmin + row), __float_as_int(d2));
-        else
-          rowmin[row] = d2;
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc_2sm<kTmemCols>(tmem_base);
-  }
-}
-
-
-// ============================================================================
-// Two-A-block variant (directed sweep only): one CTA computes TWO 128-row blocks of A against
-// each 256-column tile of B, one fp32 accumulator each (all 512 TMEM columns, so the epilogue of
-// a tile is not overlapped with the next tile's MMAs). Stages of 16 features (SWIZZLE_64B rows):
-// A1 and A2 hi/pr 4 x 8 KB + B hi/pc 2 x 16 KB = 64 KB, three in flight. Per pair and feature the
-// operand stream drops from 96 KB / (128 x 256 x 32) to 64 KB / (256 x 256 x 16): 2/3.
-// ============================================================================
-constexpr int kBK2 = 16;
-constexpr int kThreadsA2 = 320;  // TMA, MMA, 8 epilogue warps
-constexpr int kStagesA2 = 3;
-constexpr uint32_t kA2Tile = 128 * kBK2 * 4;                    // 8 KB
-constexpr uint32_t kB2Tile = kBN * kBK2 * 4;                    // 16 KB
-constexpr uint32_t kStageA2Bytes = 4 * kA2Tile + 2 * kB2Tile;   // 64 KB
-constexpr size_t kSmemA2 = static_cast<size_t>(kStagesA2) * kStageA2Bytes + 1024 + 256;
-
-// kBidir: column minima too (as the single-block kernel), combined over the tile's 256 rows
-template <bool kBidir>
+template <bool kBidir, bool kF16>
 __global__ void __launch_bounds__(kThreadsA2, 1)
     dist_rowmin_2a_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                           const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
-                          const float* __restrict__ na, const float* __restrict__ nb, float* __restrict__ rowmin,
-                          float* __restrict__ colmin) {
+                          const float* __restrict__ na, const float* __restrict__ nb, const float* __restrict__ sa,
+                          const float* __restrict__ sb, const PrepStats* sta, const PrepStats* stb,
+                          float* __restrict__ rowmin, float* __restrict__ colmin) {
   using namespace sm100;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -573,6 +405,7 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   __shared__ __align__(16) float nbuf[2][kBN];  // column norms, double-buffered by tile parity
+  __shared__ __align__(16) float ubuf[2][kBN];  // per-row scale mode: 1 / s_j
   __shared__ unsigned colbuf[2][kBN];            // kBidir: the tile's column minima (float bits)
   __shared__ unsigned tilecnt[2];
 
@@ -614,16 +447,16 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
         const int t0 = sp * s.tps;
         const int t1 = min(s.nt, t0 + s.tps);
         for (int t = t0; t < t1; ++t) {
-          for (int c = 0; c < s.nk1; ++c) {
+          for (int c = 0; c < s.nk; ++c) {
             mbar_wait(&empty[stage], phase ^ 1u);
             uint8_t* st = smem + stage * kStageA2Bytes;
             mbar_arrive_expect_tx(&full[stage], kStageA2Bytes);
-            tma_load_2d(st, &tAh, c * kBK2, pb * 256, &full[stage]);
-            tma_load_2d(st + kA2Tile, &tAl, c * kBK2, pb * 256, &full[stage]);
-            tma_load_2d(st + 2 * kA2Tile, &tAh, c * kBK2, pb * 256 + 128, &full[stage]);
-            tma_load_2d(st + 3 * kA2Tile, &tAl, c * kBK2, pb * 256 + 128, &full[stage]);
-            tma_load_2d(st + 4 * kA2Tile, &tBh, c * kBK2, t * kBN, &full[stage]);
-            tma_load_2d(st + 4 * kA2Tile + kB2Tile, &tBl, c * kBK2, t * kBN, &full[stage]);
+            tma_load_2d(st, &tAh, c * 16, pb * 256, &full[stage]);
+            tma_load_2d(st + kATile, &tAl, c * 16, pb * 256, &full[stage]);
+            tma_load_2d(st + 2 * kATile, &tAh, c * 16, pb * 256 + 128, &full[stage]);
+            tma_load_2d(st + 3 * kATile, &tAl, c * 16, pb * 256 + 128, &full[stage]);
+            tma_load_2d(st + 4 * kATile, &tBh, c * 16, t * kBN, &full[stage]);
+            tma_load_2d(st + 4 * kATile + kBTile, &tBl, c * 16, t * kBN, &full[stage]);
             if (++stage == kStagesA2) {
               stage = 0;
               phase ^= 1u;
@@ -636,8 +469,6 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
   } else if (warp == 1) {
     {
       // ------------------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
-      constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
-      constexpr uint32_t idesc16 = idesc_bf16(kBM, kBN);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tph = 0;
@@ -649,34 +480,19 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
           mbar_wait(&tempty[0], tph ^ 1u);  // the epilogue has drained both accumulators
           tc_fence_after();
           const uint32_t d0 = tmem_base, d1 = tmem_base + static_cast<uint32_t>(kBN);
-          for (int c = 0; c < s.nk1; ++c) {
+          for (int c = 0; c < s.nk; ++c) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t a1h = smem_u32(smem + stage * kStageA2Bytes);
-            const uint32_t a1l = a1h + kA2Tile, a2h = a1h + 2 * kA2Tile, a2l = a1h + 3 * kA2Tile;
-            const uint32_t bh = a1h + 4 * kA2Tile, bl = bh + kB2Tile;
-            const int ks = (c == s.nk1 - 1) ? s.ks_last1 : (kBK2 / 8);
+            const uint32_t a1l = a1h + kATile, a2h = a1h + 2 * kATile, a2l = a1h + 3 * kATile;
+            const uint32_t bh = a1h + 4 * kATile, bl = bh + kBTile;
+            const int ks = (c == s.nk - 1) ? s.ks_last : 2;
             for (int kk = 0; kk < ks; ++kk) {
               const uint32_t off = static_cast<uint32_t>(kk * 32);
               const uint64_t dbh = smem_desc_k_sw64(bh + off), dbl = smem_desc_k_sw64(bl + off);
               const uint32_t acc = (c | kk) != 0 ? 1u : 0u;
-              const uint64_t da1h = smem_desc_k_sw64(a1h + off), da1l = smem_desc_k_sw64(a1l + off);
-              const uint64_t da2h = smem_desc_k_sw64(a2h + off), da2l = smem_desc_k_sw64(a2l + off);
-              if (!s.split3) {
-                // issue order matters for power: alternating kinds per accumulator ran at a 1490 MHz
-                // median clock in the power-capped benchmark, both TF32 MMAs first at 1035 MHz
-                mma_tf32_w(d0, da1h, dbh, idesc, acc);
-                mma_bf16_w(d0, da1l, dbl, idesc16, 1u);
-                mma_tf32_w(d1, da2h, dbh, idesc, acc);
-                mma_bf16_w(d1, da2l, dbl, idesc16, 1u);
-              } else {
-                mma_tf32_w(d0, da1h, dbh, idesc, acc);
-                mma_tf32_w(d0, da1h, dbl, idesc, 1u);
-                mma_tf32_w(d0, da1l, dbh, idesc, 1u);
-                mma_tf32_w(d1, da2h, dbh, idesc, acc);
-                mma_tf32_w(d1, da2h, dbl, idesc, 1u);
-                mma_tf32_w(d1, da2l, dbh, idesc, 1u);
-              }
+              mma3<kF16, true>(d0, smem_desc_k_sw64(a1h + off), smem_desc_k_sw64(a1l + off), dbh, dbl, acc);
+              mma3<kF16, true>(d1, smem_desc_k_sw64(a2h + off), smem_desc_k_sw64(a2l + off), dbh, dbl, acc);
             }
             mma_commit_w(&empty[stage]);
             if (++stage == kStagesA2) {
@@ -697,6 +513,7 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
     const int a2 = (warp - 2) >> 2;
     const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
     const int e = (warp - 2) * 32 + lane;  // 0..255: one column norm each
+    const bool perrow = kF16 && prep_mode_perrow(sta, stb, s.D);
     uint32_t tph = 0;
     int tb = 0;  // nbuf parity
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -705,31 +522,27 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
       const int t1 = min(s.nt, t0 + s.tps);
       float rm = __int_as_float(0x7f800000);
       const int64_t myrow = static_cast<int64_t>(pb) * 256 + a2 * 128 + q * 32 + lane;
+      const EpiScale es = epi_scale(kF16, sta, stb, sa, sb, myrow, s.nA, s.D);
       // kBidir: this row's ||a||^2, or +inf for rows past nA (excluded from column minima)
       const float narow = kBidir ? (myrow < s.nA ? __ldg(na + myrow) : __int_as_float(0x7f800000)) : 0.0f;
       for (int t = t0; t < t1; ++t) {
         {
-          const float n1 = __ldg(nb + static_cast<int64_t>(t) * kBN + e);
+          const int64_t col = static_cast<int64_t>(t) * kBN + e;
+          const float n1 = __ldg(nb + col);
+          const float u1 = perrow ? 1.0f / __ldg(sb + col) : 1.0f;
           mbar_wait(&tfull[0], tph);
           nbuf[tb][e] = n1;
+          ubuf[tb][e] = u1;
           asm volatile("bar.sync 1, 256;" ::: "memory");
         }
         tc_fence_after();
         const float4* nbp = reinterpret_cast<const float4*>(nbuf[tb]);
+        const float4* ubp = reinterpret_cast<const float4*>(ubuf[tb]);
         const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(a2 * kBN);
         auto chunk = [&](float (&v)[32], int cc) {
-          float m[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 n4 = nbp[cc * 8 + i];
-            v[4 * i + 0] = fmaf(-2.0f, v[4 * i + 0], n4.x);
-            v[4 * i + 1] = fmaf(-2.0f, v[4 * i + 1], n4.y);
-            v[4 * i + 2] = fmaf(-2.0f, v[4 * i + 2], n4.z);
-            v[4 * i + 3] = fmaf(-2.0f, v[4 * i + 3], n4.w);
-            m[i] = fminf(fminf(v[4 * i + 0], v[4 * i + 1]), fminf(v[4 * i + 2], v[4 * i + 3]));
-          }
-          rm = fminf(rm, fminf(fminf(fminf(m[0], m[1]), fminf(m[2], m[3])),
-                               fminf(fminf(m[4], m[5]), fminf(m[6], m[7]))));
+          const float m = perrow ? epi_chunk<true>(v, es.k, nbp + cc * 8, ubp + cc * 8)
+                                 : epi_chunk<false>(v, es.k, nbp + cc * 8, ubp + cc * 8);
+          rm = fminf(rm, m);
           if (kBidir) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + narow, 0.0f);
@@ -769,13 +582,12 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
         tph ^= 1u;
         tb ^= 1;
       }
-      const int64_t row = static_cast<int64_t>(pb) * 256 + a2 * 128 + q * 32 + lane;
-      if (row < s.nA) {
-        const float d2 = fmaxf(rm + __ldg(na + row), 0.0f);
+      if (myrow < s.nA) {
+        const float d2 = fmaxf(rm + __ldg(na + myrow), 0.0f);
         if (s.atomic_out)
-          atomicMin(reinterpret_cast<int*>(rowmin + row), __float_as_int(d2));
+          atomicMin(reinterpret_cast<int*>(rowmin + myrow), __float_as_int(d2));
         else
-          rowmin[row] = d2;
+          rowmin[myrow] = d2;
       }
     }
   }
@@ -787,69 +599,63 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
   }
 }
 
+template <typename K>
+cudaError_t launch_k(K kern, int grid, int threads, size_t smem, cudaStream_t st, const DistArgs& a, const Sched& s) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  count_launch();
+  kern<<<grid, threads, smem, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na, a.nb, a.sa, a.sb, a.sta,
+                                    a.stb, a.rowmin, a.colmin);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
-// Variants (one B200, tools/time_exact.py). The 2-SM pair (cta_group::2) was faster per clock
-// with three TF32 MMAs but lost in the sustained, power-capped benchmark; with the TF32 + bf16
-// MMAs it measures the same as the single-CTA kernel (547 vs 549 Gpair/s) and stays opt-in.
-// Directed sweeps use the two-A-block kernel for D >= 128 (65536 x 262144, D = 256: 549 -> 627
-// Gpair/s; D = 128: 1048 -> 1126) and the single-block kernel below (faster at small D, where the
-// epilogue is not hidden behind fewer MMAs: D = 64 2118 vs 1896). The fused bidirectional sweep
-// keeps the single-block kernel: its column-minimum epilogue is heavier and, not overlapped in the
-// two-A kernel, made it slower (D = 256: 34.5 vs 31.5 ms for 65536 x 262144; the two-A kBidir
-// instantiation is kept for A/B). option k6_variant = 1 | 3 (two-A) | 2 (2-SM pair, directed) forces a variant.
+// Variants (one B200). Directed sweeps use the two-A-block kernel for D >= 128 and the
+// single-block kernel below (faster at small D, where the epilogue is not hidden behind fewer
+// MMAs). The fused bidirectional sweep keeps the single-block kernel (its column-minimum
+// epilogue is heavier and is not overlapped in the two-A kernel). option k6_variant = 1 | 3
+// forces the single-block / two-A kernel; k6_bidir_2a = 1 runs the bidirectional sweep two-A.
 static int dist_variant(int D) {
-  const long long v = opt(OPT_K6_VARIANT);  // 2: CTA pair, 3: two A blocks per CTA, 1: single
-  if (v >= 1 && v <= 3) return static_cast<int>(v);
+  const long long v = opt(OPT_K6_VARIANT);
+  if (v == 1 || v == 3) return static_cast<int>(v);
   return D >= 128 ? 3 : 1;
 }
 
-int dist_b_box_rows(int D, bool bidir) { return (!bidir && dist_variant(D) == 2) ? 128 : kBN; }
-bool k6_split3() {
-  return opt(OPT_K6_SPLIT3) == 1;
-}
-
-static bool bidir_2a() {
-  return opt(OPT_K6_BIDIR_2A) == 1;  // dev A/B: fused bidirectional sweep on the two-A kernel
-}
-int dist_box_inner(int D, bool bidir) { return ((!bidir || bidir_2a()) && dist_variant(D) == 3) ? kBK2 : kBK; }
+bool k6_split3() { return opt(OPT_K6_SPLIT3) == 1; }
 
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
-  const bool pair = dist_variant(a.D) == 2 && a.num_sms >= 2 && a.colmin == nullptr;
-  const bool twoa = dist_variant(a.D) == 3 && (a.colmin == nullptr || bidir_2a());
-  const int rows_per_unit = (pair || twoa) ? 256 : kBM;
-  const int ctas_per_unit = pair ? 2 : 1;
+  const bool twoa = dist_variant(a.D) == 3 && (a.colmin == nullptr || opt(OPT_K6_BIDIR_2A) == 1);
+  const int rows_per_unit = twoa ? 256 : kBM;
   Sched s{};
-  s.split3 = k6_split3() ? 1 : 0;
   s.nA = a.nA;
   s.nB = a.nB;
+  s.D = a.D;
   s.nrb = static_cast<int>((a.nA + rows_per_unit - 1) / rows_per_unit);
   s.nt = static_cast<int>((a.nB + kBN - 1) / kBN);
-  s.nk = (a.D + kBK - 1) / kBK;
-  s.ks_last = ((a.D - (s.nk - 1) * kBK) + 7) / 8;
-  s.nk1 = (a.D + kBK2 - 1) / kBK2;
-  s.ks_last1 = ((a.D - (s.nk1 - 1) * kBK2) + 7) / 8;
-  const int slots = a.num_sms / ctas_per_unit;  // concurrent units
+  const int fps = a.f16 ? 32 : 16;  // features per 64-byte stage row
+  const int fpk = fps / 2;          // features per 32-byte K-step
+  s.nk = (a.D + fps - 1) / fps;
+  s.ks_last = (a.D - (s.nk - 1) * fps + fpk - 1) / fpk;
+  const int slots = a.num_sms;  // concurrent units
   // Column splits: units (row block, column range) are dealt round-robin to the persistent
   // CTAs, so the sweep takes ceil(units / slots) rounds of (tps + ~0.5) tile times (the half
   // tile: a unit's pipeline fill / drain and row-minimum merge). Small A (subset HD: 100-250
   // row blocks) needs splits to fill 148 SMs, and the split count decides the last round's
   // occupancy: pick the cheapest of 1..64 splits (ties to fewer: fewer atomic merges).
   int nsplit = 1;
-  {
-    if (opt(OPT_K6_SPLITS_2X) == 1) {  // dev A/B: the old fill-twice rule
-      nsplit = (2 * slots + s.nrb - 1) / s.nrb;
-    } else {
-      double best = 0.0;
-      for (int ns = 1; ns <= 64 && ns <= s.nt; ++ns) {
-        const int tps = (s.nt + ns - 1) / ns;
-        const int nsa = (s.nt + tps - 1) / tps;
-        const int64_t u = static_cast<int64_t>(s.nrb) * nsa;
-        const double cost = static_cast<double>((u + slots - 1) / slots) * (tps + 0.5);
-        if (ns == 1 || cost < best * 0.995) {
-          best = cost;
-          nsplit = nsa;
-        }
+  if (opt(OPT_K6_SPLITS_2X) == 1) {  // dev A/B: the old fill-twice rule
+    nsplit = (2 * slots + s.nrb - 1) / s.nrb;
+  } else {
+    double best = 0.0;
+    for (int ns = 1; ns <= 64 && ns <= s.nt; ++ns) {
+      const int tps = (s.nt + ns - 1) / ns;
+      const int nsa = (s.nt + tps - 1) / tps;
+      const int64_t u = static_cast<int64_t>(s.nrb) * nsa;
+      const double cost = static_cast<double>((u + slots - 1) / slots) * (tps + 0.5);
+      if (ns == 1 || cost < best * 0.995) {
+        best = cost;
+        nsplit = nsa;
       }
     }
   }
@@ -862,51 +668,30 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(a.rowmin, 0x7F, sizeof(float) * a.nA, st);  // 3.39e38 (finite, > any d2)
     if (e != cudaSuccess) return e;
   }
-  const int units = s.nrb * s.nsplit;
-  const int nunits = units < slots ? units : slots;
-  if (twoa) {
-    if (a.colmin != nullptr) {
-      cudaError_t e = cudaMemsetAsync(a.colmin, 0x7F, sizeof(float) * a.nB, st);
-      if (e != cudaSuccess) return e;
-    }
-    auto kern = a.colmin != nullptr ? dist_rowmin_2a_kernel<true> : dist_rowmin_2a_kernel<false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemA2));
-    if (e != cudaSuccess) return e;
-    count_launch();
-    kern<<<nunits, kThreadsA2, kSmemA2, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na, a.nb, a.rowmin,
-                                             a.colmin);
-    return cudaGetLastError();
-  }
-  if (pair) {
-    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmem2));
-    if (e != cudaSuccess) return e;
-    count_launch();
-    dist_rowmin_2sm_kernel<<<2 * nunits, kThreads, kSmem2, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
-                                                                   a.na, a.nb, a.rowmin);
-    return cudaGetLastError();
-  }
   if (a.colmin != nullptr) {
     cudaError_t e = cudaMemsetAsync(a.colmin, 0x7F, sizeof(float) * a.nB, st);
     if (e != cudaSuccess) return e;
+  }
+  const int units = s.nrb * s.nsplit;
+  const int grid = units < slots ? units : slots;
+  const bool bidir = a.colmin != nullptr;
+  if (twoa) {
+    if (bidir)
+      return a.f16 ? launch_k(dist_rowmin_2a_kernel<true, true>, grid, kThreadsA2, kSmemA2, st, a, s)
+                   : launch_k(dist_rowmin_2a_kernel<true, false>, grid, kThreadsA2, kSmemA2, st, a, s);
+    return a.f16 ? launch_k(dist_rowmin_2a_kernel<false, true>, grid, kThreadsA2, kSmemA2, st, a, s)
+                 : launch_k(dist_rowmin_2a_kernel<false, false>, grid, kThreadsA2, kSmemA2, st, a, s);
+  }
+  if (bidir) {
     // lane-0 MMA issue below D = 192 (D = 128 undirected cfg3: 255 -> 243 ms), elected above
-    auto kern = a.D < 192 ? dist_rowmin_kernel<true, false> : dist_rowmin_kernel<true, true>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-    if (e != cudaSuccess) return e;
-    count_launch();
-    kern<<<nunits, kThreads1, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s, a.na, a.nb, a.rowmin,
-                                                a.colmin);
-    return cudaGetLastError();
+    if (a.D < 192)
+      return a.f16 ? launch_k(dist_rowmin_kernel<true, false, true>, grid, kThreads1, kSmem1, st, a, s)
+                   : launch_k(dist_rowmin_kernel<true, false, false>, grid, kThreads1, kSmem1, st, a, s);
+    return a.f16 ? launch_k(dist_rowmin_kernel<true, true, true>, grid, kThreads1, kSmem1, st, a, s)
+                 : launch_k(dist_rowmin_kernel<true, true, false>, grid, kThreads1, kSmem1, st, a, s);
   }
-  {
-    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemBytes));
-    if (e != cudaSuccess) return e;
-  }
-  count_launch();
-  dist_rowmin_kernel<false, true><<<nunits, kThreads1, kSmemBytes, st>>>(a.maps[0], a.maps[1], a.maps[2], a.maps[3], s,
-                                                                   a.na, a.nb, a.rowmin, nullptr);
-  return cudaGetLastError();
+  return a.f16 ? launch_k(dist_rowmin_kernel<false, true, true>, grid, kThreads1, kSmem1, st, a, s)
+               : launch_k(dist_rowmin_kernel<false, true, false>, grid, kThreads1, kSmem1, st, a, s);
 }
 
 }  // namespace prohd

@@ -1,15 +1,20 @@
 // k_prep.cu — K0 operand preparation, K7 row-max key and fp64 witness search.
 //
-// K0 (SURVEY.md §2f, §8(a) "Centering"): per point, y = x - c (fp64, c the pair's
-// common centre), hi = rn_tf32(fp32(y)) (rounded to nearest, ties to even, to 11
-// significant bits with the low 13 mantissa bits zero, so the tensor core reads hi
-// exactly whatever its fp32->tf32 conversion mode, and |lo| <= 2^-11 |y|),
-// lo = fp32(y - hi) (exact in fp32), and ||y||^2 accumulated in fp64 then rounded to fp32 (without
-// a centre: y = x and lo = x - hi exactly). K6 takes a.b = hi_a.hi_b (TF32 MMA) +
-// [hi_a lo_a].[lo_b hi_b] (one bf16 MMA over interleaved pairs), so K0 writes hi (fp32) and
-// the bf16 pairs in both orders: pr[f] = (bf16(hi_f), bf16(lo_f)) for the row role and
-// pc[f] = (bf16(lo_f), bf16(hi_f)) for the column role (element 2f at the lower address).
-// One warp per row; HBM-bound.
+// K0 (SURVEY.md §2f, §8(a) "Centering"): the distance kernel K6 forms
+// a.b with the three-term split a.b ~= hi_a.hi_b + hi_a.lo_b + lo_a.hi_b (lo.lo dropped) on
+// two operand arrays per set, H (hi) and L (lo). Per point y = x - c (fp64, c the pair's
+// common centre; y = x without one). Two formats:
+//   F16 (default): y is scaled by a power of two s (exact), hi = fp16_rn(s y), lo =
+//        fp16_rn(s y - hi); 11 + 11 significant bits like 3xTF32, at the fp16 tensor rate and
+//        half the operand bytes. s keeps |s y| <= 2^14 (no overflow): one scale per SET (the
+//        set's max |y| -> (2^13, 2^14]) when the pair's dynamic range allows it, else one per
+//        ROW (prep_mode below). scale[i] = s of row i.
+//   TF32 (option k6_split3, the literal north-star form): hi = rn_tf32(fp32(y)) (low 13
+//        mantissa bits zero, read exactly by the tensor core), lo = fp32(y - hi), s = 1.
+// ||y||^2 is accumulated in fp64 and stored in fp32 (padded rows: +inf, so K6 needs no column
+// masks). Rows are zero-padded to the array stride. A stats pass (warp per row) records each
+// set's max |y| and min ||y||^2 (PrepStats) before the write pass, whose scale depends on both
+// sets of the pair. One warp per row; HBM-bound.
 //
 // K7: the directed maximum over row minima packed as
 //   key = (float_bits(d2) << 32) | (0xFFFFFFFF - row)
@@ -19,7 +24,7 @@
 // matching the oracle's definition (Eq. (1)).
 #include "internal.cuh"
 
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cfloat>
 #include <cmath>
@@ -36,21 +41,24 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float(keep ? (b & 0xFFFFE000u) : r);
 }
 
-__device__ __forceinline__ uint32_t bf16_pair(float first, float second) {
-  const uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(first));
-  const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(second));
-  return a | (b << 16);
+template <bool kGather, bool kCentre>
+__device__ __forceinline__ double coord(const float* __restrict__ x, const double* __restrict__ centre, int c, int D) {
+  if (c >= D) return 0.0;
+  const double v = static_cast<double>(__ldg(x + c));
+  return kCentre ? v - __ldg(centre + c) : v;
 }
 
-template <bool kGather, bool kCentre, bool kSplit3>
-__global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, const int64_t* __restrict__ idx,
-                                                   int64_t n, int D, int Dp, int64_t n_pad,
-                                                   const double* __restrict__ centre, float* __restrict__ hi,
-                                                   uint32_t* __restrict__ pr, uint32_t* __restrict__ pc,
-                                                   float* __restrict__ norms, int* bad) {
+// stats pass: norms (fp32, +inf padding), the set's max |y| and min ||y||^2 (float bits, atomics)
+template <bool kGather, bool kCentre>
+__global__ void __launch_bounds__(256) prep_stats_kernel(const float* __restrict__ X, const long long* __restrict__ idx,
+                                                         int64_t n, int D, int64_t n_pad,
+                                                         const double* __restrict__ centre, float* __restrict__ norms,
+                                                         PrepStats* st, int* bad) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  __shared__ unsigned smax[8], smin[8];
+  unsigned wmax = 0u, wmin = 0x7F800000u;
   for (int64_t r = warp; r < n_pad; r += nwarps) {
     if (r >= n) {
       if (lane == 0) norms[r] = __int_as_float(0x7f800000);
@@ -58,35 +66,91 @@ __global__ void __launch_bounds__(256) prep_kernel(const float* __restrict__ X, 
     }
     const int64_t src = kGather ? idx[r] : r;
     const float* x = X + src * static_cast<int64_t>(D);
-    float* h = hi + r * static_cast<int64_t>(Dp);
-    uint32_t* qr = pr + r * static_cast<int64_t>(Dp);
-    uint32_t* qc = pc + r * static_cast<int64_t>(Dp);
-    double s = 0.0;
-    for (int c = lane; c < Dp; c += 32) {
-      const float v = c < D ? __ldg(x + c) : 0.0f;
-      if (kCentre) {
-        const double y = c < D ? static_cast<double>(v) - __ldg(centre + c) : 0.0;
-        const float vh = tf32_rn(static_cast<float>(y));
-        const float vl = static_cast<float>(y - static_cast<double>(vh));
-        h[c] = vh;
-        qr[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vh, vl);
-        qc[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vl, vh);
-        s = fma(y, y, s);
-      } else {
-        const float vh = tf32_rn(v);
-        const float vl = v - vh;
-        h[c] = vh;
-        qr[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vh, vl);
-        qc[c] = kSplit3 ? __float_as_uint(vl) : bf16_pair(vl, vh);
-        s = fma(static_cast<double>(v), static_cast<double>(v), s);
-      }
+    double s = 0.0, mx = 0.0;
+    for (int c = lane; c < D; c += 32) {
+      const double y = coord<kGather, kCentre>(x, centre, c, D);
+      s = fma(y, y, s);
+      mx = fmax(mx, fabs(y));
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      const float f = static_cast<float>(s);
-      norms[r] = f;
-      if (!isfinite(s) || !isfinite(f)) atomicExch(bad, 1);
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const float f = static_cast<float>(s);
+    const float fm = static_cast<float>(mx);
+    if (lane == 0) norms[r] = f;
+    if (!isfinite(s) || !isfinite(f) || !isfinite(fm)) {
+      if (lane == 0) atomicExch(bad, 1);
+    } else {
+      wmax = max(wmax, __float_as_uint(fm));
+      wmin = min(wmin, __float_as_uint(f));
+    }
+  }
+  if (lane == 0) {
+    smax[threadIdx.x >> 5] = wmax;
+    smin[threadIdx.x >> 5] = wmin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned bm = 0u, bn = 0x7F800000u;
+    for (int i = 0; i < 8; ++i) {
+      bm = max(bm, smax[i]);
+      bn = min(bn, smin[i]);
+    }
+    if (bm != 0u) atomicMax(&st->maxabs, bm);
+    if (bn != 0x7F800000u) atomicMin(&st->minnorm2, bn);
+  }
+}
+
+// write pass: H, L and the per-row scale (F16) or fp32 hi / lo (TF32)
+template <bool kGather, bool kCentre, bool kF16>
+__global__ void __launch_bounds__(256) prep_write_kernel(const float* __restrict__ X,
+                                                         const long long* __restrict__ idx, int64_t n, int D,
+                                                         int Dh, int64_t n_pad, const double* __restrict__ centre,
+                                                         const PrepStats* self, const PrepStats* other,
+                                                         void* __restrict__ Hv, void* __restrict__ Lv,
+                                                         float* __restrict__ scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool perrow = kF16 && prep_mode_perrow(self, other, D);
+  const float sset = kF16 ? prep_scale_for(__uint_as_float(self->maxabs)) : 1.0f;
+  for (int64_t r = warp; r < n_pad; r += nwarps) {
+    if (r >= n) {
+      if (lane == 0) scale[r] = sset;
+      continue;
+    }
+    const int64_t src = kGather ? idx[r] : r;
+    const float* x = X + src * static_cast<int64_t>(D);
+    float sc = sset;
+    if (perrow) {
+      double mx = 0.0;
+      for (int c = lane; c < D; c += 32) mx = fmax(mx, fabs(coord<kGather, kCentre>(x, centre, c, D)));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      sc = prep_scale_for(static_cast<float>(mx));
+    }
+    if (lane == 0) scale[r] = sc;
+    if constexpr (kF16) {
+      __half* h = reinterpret_cast<__half*>(Hv) + r * static_cast<int64_t>(Dh);
+      __half* l = reinterpret_cast<__half*>(Lv) + r * static_cast<int64_t>(Dh);
+      const double s64 = static_cast<double>(sc);
+      for (int c = lane; c < Dh; c += 32) {
+        const double y = coord<kGather, kCentre>(x, centre, c, D) * s64;  // exact: power-of-two scale
+        const __half vh = __double2half(y);
+        h[c] = vh;
+        l[c] = __double2half(y - static_cast<double>(__half2float(vh)));
+      }
+    } else {
+      float* h = reinterpret_cast<float*>(Hv) + r * static_cast<int64_t>(Dh);
+      float* l = reinterpret_cast<float*>(Lv) + r * static_cast<int64_t>(Dh);
+      for (int c = lane; c < Dh; c += 32) {
+        const double y = coord<kGather, kCentre>(x, centre, c, D);
+        const float vh = tf32_rn(static_cast<float>(y));
+        h[c] = vh;
+        l[c] = static_cast<float>(y - static_cast<double>(vh));
+      }
     }
   }
 }
@@ -98,19 +162,39 @@ static int grid_for_rows(int64_t rows) {
   return static_cast<int>(blocks);
 }
 
-cudaError_t launch_prep(const float* X, int64_t n, int D, int Dp, int64_t n_pad, const double* centre, float* hi,
-                        uint32_t* pr, uint32_t* pc, float* norms, int* bad, cudaStream_t st) {
+cudaError_t launch_prep_stats(const float* X, const long long* idx, int64_t n, int D, int64_t n_pad,
+                              const double* centre, float* norms, PrepStats* st, int* bad, cudaStream_t st_) {
   count_launch();
   const int g = grid_for_rows(n_pad);
-  const bool s3 = k6_split3();
-  if (centre && s3)
-    prep_kernel<false, true, true><<<g, 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, centre, hi, pr, pc, norms, bad);
-  else if (centre)
-    prep_kernel<false, true, false><<<g, 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, centre, hi, pr, pc, norms, bad);
-  else if (s3)
-    prep_kernel<false, false, true><<<g, 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, nullptr, hi, pr, pc, norms, bad);
-  else
-    prep_kernel<false, false, false><<<g, 256, 0, st>>>(X, nullptr, n, D, Dp, n_pad, nullptr, hi, pr, pc, norms, bad);
+#define PS(G, C) prep_stats_kernel<G, C><<<g, 256, 0, st_>>>(X, idx, n, D, n_pad, centre, norms, st, bad)
+  if (idx && centre) PS(true, true);
+  else if (idx) PS(true, false);
+  else if (centre) PS(false, true);
+  else PS(false, false);
+#undef PS
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_write(const float* X, const long long* idx, int64_t n, int D, int64_t n_pad,
+                              const double* centre, const PrepStats* self, const PrepStats* other, bool f16, void* H,
+                              void* L, float* scale, cudaStream_t st) {
+  count_launch();
+  const int g = grid_for_rows(n_pad);
+  const int Dh = f16 ? k6_stride_f16(D) : k6_stride_f32(D);
+#define PW(G, C, F) \
+  prep_write_kernel<G, C, F><<<g, 256, 0, st>>>(X, idx, n, D, Dh, n_pad, centre, self, other, H, L, scale)
+  if (f16) {
+    if (idx && centre) PW(true, true, true);
+    else if (idx) PW(true, false, true);
+    else if (centre) PW(false, true, true);
+    else PW(false, false, true);
+  } else {
+    if (idx && centre) PW(true, true, false);
+    else if (idx) PW(true, false, false);
+    else if (centre) PW(false, true, false);
+    else PW(false, false, false);
+  }
+#undef PW
   return cudaGetLastError();
 }
 

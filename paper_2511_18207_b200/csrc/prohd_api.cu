@@ -156,8 +156,7 @@ static int exact_common(prohd_ctx* ctx, const float* A, int64_t nA, const float*
     CK(launch_centre(A, nA, B, nB, D, w.centre, ctx->stream));
   else
     CK(launch_centre(nullptr, 0, B, nB, D, w.centre, ctx->stream));
-  if ((rc = prep_set(ctx, A, nA, D, w.A, w.bad, w.centre))) return rc;
-  if ((rc = prep_set(ctx, B, nB, D, w.B, w.bad, w.centre))) return rc;
+  if ((rc = prep_pair(ctx, A, nA, B, nB, D, w.A, w.B, w.bad, w.centre))) return rc;
   return PROHD_OK;
 }
 
@@ -413,8 +412,7 @@ int hausdorff_subsets(prohd_ctx* ctx, const float* A, int64_t nA, const int64_t*
   CK(launch_gather_offset(B, D, dib, 0, kB, 0, xb, st));
   CK(cudaMemsetAsync(w.bad, 0, sizeof(int), st));
   CK(launch_centre(xa, kA, xb, kB, D, w.centre, st));
-  if ((rc = prep_set(ctx, xa, kA, D, w.A, w.bad, w.centre))) return rc;
-  if ((rc = prep_set(ctx, xb, kB, D, w.B, w.bad, w.centre))) return rc;
+  if ((rc = prep_pair(ctx, xa, kA, xb, kB, D, w.A, w.B, w.bad, w.centre))) return rc;
   if ((rc = bidir_on_ops(ctx, w.A, w.B, D, w))) return rc;
   ExactHost h;
   if ((rc = fetch(ctx, w, h))) return rc;

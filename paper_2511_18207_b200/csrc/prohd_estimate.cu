@@ -253,10 +253,9 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   // one common centre for every operand of the subset HD: centre(A_sel, B_sel) (symmetric;
   // the sharded driver computes the same from the all-gathered subsets)
   CK(launch_centre(w.Xs[0], ucount[0], w.Xs[1], ucount[1], D, w.centre, st));
-  for (int s = 0; s < 2; ++s) {
-    w.ops[s].n = ucount[s];
-    if ((rc = prep_set(ctx, w.Xs[s], ucount[s], D, w.ops[s], w.bad, w.centre))) return rc;
-  }
+  if (!certified && (rc = prep_pair(ctx, w.Xs[0], ucount[0], w.Xs[1], ucount[1], D, w.ops[0], w.ops[1], w.bad,
+                                     w.centre)))
+    return rc;
   ExactWs ew;
   ew.rowmin = w.rowmin;
   ew.colmin = w.colmin;
@@ -269,8 +268,9 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
     if ((rc = bidir_on_ops(ctx, w.ops[0], w.ops[1], D, ew))) return rc;  // Alg. 3 line 6, both directions
   } else {
     // certified mode (SPEC.md:279 subset-full): rows of each subset against the FULL other set
-    if ((rc = prep_set(ctx, A, nA, D, w.full[0], w.bad, w.centre))) return rc;
-    if ((rc = prep_set(ctx, B, nB, D, w.full[1], w.bad, w.centre))) return rc;
+    // two pairs, each prepared together: (A_sel, B) and (B_sel, A)
+    if ((rc = prep_pair(ctx, w.Xs[0], ucount[0], B, nB, D, w.ops[0], w.full[1], w.bad, w.centre))) return rc;
+    if ((rc = prep_pair(ctx, w.Xs[1], ucount[1], A, nA, D, w.ops[1], w.full[0], w.bad, w.centre))) return rc;
     if ((rc = directed_on_ops(ctx, w.ops[0], w.full[1], D, ew, 0))) return rc;
     if ((rc = directed_on_ops(ctx, w.ops[1], w.full[0], D, ew, 1))) return rc;
   }

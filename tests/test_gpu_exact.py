@@ -176,13 +176,16 @@ def test_bidirectional_pass_matches_oracle(ctx, shape):
     assert abs(h["ba"]["dist2"] - d["dist2"]) <= tol
 
 
+@pytest.mark.parametrize("split3", [0, 1])
 @pytest.mark.parametrize("kind", ["positive", "heavy", "offset"])
-def test_split_product_error_bound(ctx, kind):
-    """K6 forms a.b as hi.hi (TF32) + [hi lo].[lo hi] (one bf16 MMA), whose error is at most
-    7.9e-6 (||a - c||^2 + ||b - c||^2) on the centred operands (c = fp64 mean of the first <= 4096
-    rows of B, K0 / DESIGN.md 7.1, 7.3). Inputs chosen so the rounding errors of the split
-    products tend to align: all-positive data with every mantissa bit in play, heavy tails, and a
-    large common offset."""
+def test_split_product_error_bound(ctx, kind, split3):
+    """K6 forms a.b as hi.hi + hi.lo + lo.hi on K0's split operands (fp16 of the power-of-two-scaled
+    coordinates by default, RN-TF32 fp32 with option k6_split3): 11 + 11 significant bits, error per
+    product <= 3 2^-22 |a_i||b_i|, plus the tensor core's fp32 accumulation (<= ~2^-23 |acc| per
+    MMA, 3 D / 16 or 3 D / 8 MMAs) -- on the centred operands (c = fp64 mean of the first <= 4096
+    rows of B). Inputs chosen so the rounding errors tend to align: all-positive
+    data with every mantissa bit in play, heavy tails, and a large common offset."""
+    from paper_2511_18207_b200 import option
     rng = np.random.default_rng({"positive": 1, "heavy": 2, "offset": 3}[kind])
     nA, nB, D = 1536, 2048, 256
     if kind == "positive":
@@ -194,63 +197,65 @@ def test_split_product_error_bound(ctx, kind):
     else:
         A = (rng.standard_normal((nA, D)) + 1000.0).astype(np.float32)
         B = (rng.standard_normal((nB, D)) + 1000.25).astype(np.float32)
-    rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    with option("k6_split3", split3):
+        rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
     ref, arg = oracle.row_minima(A, B)
     c = B[: min(nB, 4096)].astype(np.float64).mean(0)
     na = ((A.astype(np.float64) - c) ** 2).sum(1)
     nb = ((B.astype(np.float64)[arg] - c) ** 2).sum(1)
     err = np.abs(rm.astype(np.float64) - ref)
-    # fp32 accumulation and the fp32 norms add a few 2^-24 of the norms on top of the products
-    bound = (7.9e-6 + 64 * 2.0 ** -24) * (na + nb)
+    nmma = 3 * D / (8 if split3 else 16)
+    bound = (3 * 2.0 ** -22 + nmma / 2 * 2.0 ** -23 + 4 * 2.0 ** -24) * (na + nb)
     assert np.all(err <= bound), f"max err / bound {np.max(err / bound):.3f}"
     raw = (A.astype(np.float64) ** 2).sum(1) + (B.astype(np.float64)[arg] ** 2).sum(1)
     assert np.all(err <= TOL * raw)
-    print(f"{kind}: max err / (centred bound) = {np.max(err / bound):.3e}")
+    print(f"{kind} split3={split3}: max err / (centred bound) = {np.max(err / bound):.3e}")
 
 
-def _bf16_rn(x):
-    b = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
-    return ((b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000).astype(np.uint32).view(np.float32)
-
-
-def _tf32_rn(x):
-    b = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
-    return ((b + 0xFFF + ((b >> 13) & 1)) & 0xFFFFE000).astype(np.uint32).view(np.float32)
-
-
-def _split_product_rel_err(x):
-    """CPU emulation of K0's split (hi = RN-TF32, lo = x - hi, both bf16-rounded in the correction
-    MMA) for the product x.x with exact products: (approx - x^2) / x^2."""
-    hi = _tf32_rn(x)
-    lo = (x - hi).astype(np.float32)
-    bh, bl = _bf16_rn(hi).astype(np.float64), _bf16_rn(lo).astype(np.float64)
-    x64 = x.astype(np.float64)
-    return (hi.astype(np.float64) ** 2 + 2 * bh * bl - x64 ** 2) / x64 ** 2
+def _fp16_split_rel_err(x):
+    """CPU emulation of K0's default split for the product x.x (one power-of-two scale putting
+    max |x| into (2^13, 2^14], hi = fp16(s x), lo = fp16(s x - hi), exact products, lo.lo dropped)."""
+    m = float(np.max(np.abs(x)))
+    s = 2.0 ** (14 - np.frexp(m)[1])
+    y = x.astype(np.float64) * s
+    hi = y.astype(np.float16).astype(np.float64)
+    lo = (y - hi).astype(np.float16).astype(np.float64)
+    return (hi * hi + 2 * hi * lo - y * y) / (y * y)
 
 
 def test_split_worst_case_mantissas(ctx):
     """Adversarial split-precision case: rows of D = 256 equal coordinates
-    x, so every product's rounding error has the same sign and the d^2 error of the pair (x.1, x.1)
-    is 2 D err(x.x) x^2 against the Q17 budget 1e-5 (2 D x^2). The mantissas are the 24 worst of an
-    exhaustive emulation of K0's split over all 2^23 mantissas, plus the worst case of the earlier
-    truncated split (x = 1.0048771f, 1.22e-5 of the product, i.e. 1.22x the budget), at three binades
-    and both signs. B = {x.1, -x.1} so the centre K0 subtracts is exactly 0."""
+    x, so every product's rounding error and every accumulator truncation has the same sign and
+    the d^2 error of the pair (x.1, x.1) is 2 D err(x.x) x^2 + the accumulation error, against the
+    Q17 budget 1e-5 (2 D x^2). Mantissas: the 16 worst of the earlier TF32 + bf16-pair split (the
+    worst case 1.0048771f was 1.22e-5 of the product alone), the 16 worst of an exhaustive
+    emulation of the current fp16 split, and 32 random ones, at three binades and both signs.
+    B = {x.1, -x.1} per x so the centre K0 subtracts is exactly 0. Checked for the default split and
+    for the literal 3xTF32 option."""
+    from paper_2511_18207_b200 import option
     m = np.arange(1 << 23, dtype=np.uint32)
     xs = (m | np.uint32(127 << 23)).view(np.float32)
-    err = _split_product_rel_err(xs)
-    assert np.abs(err).max() <= 7.9e-6
-    worst = xs[np.argsort(-np.abs(err))[:24]]
-    vals = np.concatenate([worst, np.array([1.0048771], np.float32)])
+    e16 = _fp16_split_rel_err(xs)
+    assert np.abs(e16).max() <= 3 * 2.0 ** -22
+    old = np.array([1.0048771, 1.0043917, 1.0043879, 1.0112314, 1.0200167, 1.0200129, 1.0268564], np.float32)
+    rng = np.random.default_rng(0)
+    vals = np.concatenate([old, xs[np.argsort(-np.abs(e16))[:16]], xs[rng.integers(0, 1 << 23, 32)]])
     vals = np.concatenate([vals * np.float32(s) for s in (0.125, 1.0, 32.0)] +
                           [-vals * np.float32(4.0)]).astype(np.float32)
     D = 256
-    A = np.repeat(vals[:, None], D, axis=1).astype(np.float32)
-    B = np.empty((2 * len(vals), D), np.float32)
-    B[0::2] = A
-    B[1::2] = -A
-    rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
-    worst_frac = _check_rowmins(A, B, rm) / TOL
-    print(f"worst-case mantissas: max |d2 err| / Q17 budget = {worst_frac:.3f}")
+    worst = {}
+    for split3 in (0, 1):
+        errs = []
+        with option("k6_split3", split3):
+            for x in vals:  # one x per call: the self pair is the row's only near neighbour
+                A = np.full((1, D), x, np.float32)
+                B = np.concatenate([A, -A])
+                rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+                errs.append(float(rm[0]) / (2 * D * float(x) ** 2))  # exact d2 = 0
+        worst[split3] = max(errs)
+        assert worst[split3] <= TOL, (split3, worst[split3], vals[int(np.argmax(errs))])
+    print(f"worst-case mantissas: max |d2 err| / Q17 budget: default {worst[0] / TOL:.3f}, "
+          f"3xTF32 {worst[1] / TOL:.3f}")
 
 
 @pytest.mark.parametrize("shape", [(333, 1000, 300), (200, 700, 513), (129, 300, 1000)])

@@ -11,7 +11,7 @@ import torch
 from paper_2511_18207_b200 import Context, option
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
-from test_gpu_exact import _split_product_rel_err  # noqa: E402
+from test_gpu_exact import _fp16_split_rel_err as _split_product_rel_err  # noqa: E402
 
 ctx = Context(0)
 m = np.arange(1 << 23, dtype=np.uint32)
@@ -35,7 +35,7 @@ def run(D, variant=None, split3=None):
 
 for D in (8, 16, 64, 256):
     for name, opts in (("default", {}), ("split3", {"k6_split3": 1}), ("v1", {"k6_variant": 1}),
-                       ("v3", {"k6_variant": 3})):
+                       ("v3", {"k6_variant": 3}), ("v1split3", {"k6_variant": 1, "k6_split3": 1})):
         cms = [option(k, v) for k, v in opts.items()]
         for c in cms:
             c.__enter__()
