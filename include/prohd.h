@@ -142,10 +142,19 @@ int hausdorff(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
               int32_t D, prohd_hd* out);
 
 /* Test hook: per-row minima of A against B, d2_i = min_j ||a_i - b_j||^2 as the
- * kernel computes them (3xTF32 tensor-core products, fp32 accumulation), written
+ * kernel computes them (split-precision tensor-core products, fp32 accumulation), written
  * to rowmin_dev (DEVICE, nA floats). */
 int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB,
                        int32_t D, float* rowmin_dev);
+
+/* Test hook (SURVEY.md §8(c4) L6 for the undirected H): exactly the hausdorff()
+ * launch sequence (one fused bidirectional K6 sweep for D >= 128, two directed sweeps below, both
+ * about centre(A, B)), additionally exporting the per-row minima of both directions:
+ * rowmin_dev[i] = min_j ||a_i - b_j||^2 (nA floats) and colmin_dev[j] = min_i ||a_i - b_j||^2
+ * (nB floats), both DEVICE, as the kernel computes them; *out as hausdorff(). Errors as hausdorff()
+ * plus PROHD_E_INVALID for null / host minima pointers. */
+int hausdorff_minima(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                     float* rowmin_dev, float* colmin_dev, prohd_hd* out);
 
 /* Test hook (K3, Alg. 1 line 4 / Alg. 2 line 5; pi = x^T u,
  * P:139): the fp32 projections the selection starts from. X (DEVICE, n x D fp32 row-major),

@@ -121,6 +121,17 @@ class Context:
                                        A.shape[1], C.byref(out)))
         return {"value": out.value, "ab": _directed(out.ab), "ba": _directed(out.ba)}
 
+    def hausdorff_minima(self, A, B):
+        """hausdorff() plus both directions' per-row minima (test hook): (result, rowmin, colmin)."""
+        A, B = self._prepare(A, B)
+        dev = f"cuda:{self.device}"
+        rowmin = torch.empty(A.shape[0], dtype=torch.float32, device=dev)
+        colmin = torch.empty(B.shape[0], dtype=torch.float32, device=dev)
+        out = L.HD()
+        self._check(self.lib.hausdorff_minima(self.h, A.data_ptr(), A.shape[0], B.data_ptr(), B.shape[0], A.shape[1],
+                                              rowmin.data_ptr(), colmin.data_ptr(), C.byref(out)))
+        return ({"value": out.value, "ab": _directed(out.ab), "ba": _directed(out.ba)}, rowmin, colmin)
+
     def directed_hd_rowmin(self, A, B) -> torch.Tensor:
         A, B = self._prepare(A, B)
         rowmin = torch.empty(A.shape[0], dtype=torch.float32, device=f"cuda:{self.device}")

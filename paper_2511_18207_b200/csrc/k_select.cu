@@ -414,10 +414,14 @@ __global__ void __launch_bounds__(256) cand_p64_kernel(const float* __restrict__
 __global__ void __launch_bounds__(256) rank_kernel(int L, const int* n_dirs, const int* __restrict__ cand,
                                                    const double* __restrict__ cval, const unsigned* ccount,
                                                    int64_t cap, int64_t m, int* lists, unsigned* bitmap,
-                                                   double* cv_out, long long* ci_out, int64_t row_offset) {
+                                                   double* cv_out, long long* ci_out, int64_t row_offset,
+                                                   const unsigned* only) {
   const int lt = blockIdx.y;
   const int l = lt >> 1, t = lt & 1;
   if (l >= *n_dirs) return;
+  // a list whose guard band overflowed the candidate buffer is left to the band-select fallback
+  // (launch_select_fallback); in the fallback pass `only` restricts the ranking to those lists
+  if (only != nullptr ? only[lt] == 0u : static_cast<int64_t>(ccount[lt]) > cap) return;
   const int64_t cnt = min(static_cast<int64_t>(ccount[lt]), cap);
   const int* ci = cand + static_cast<int64_t>(lt) * cap;
   const double* cv = cval + static_cast<int64_t>(lt) * cap;
@@ -584,6 +588,145 @@ __global__ void dirs_to_f32_kernel(const double* U64, float* U32, int total) {
     U32[i] = static_cast<float>(U64[i]);
 }
 
+// ------------------------------------------------------------------ K4 band-select fallback
+// When the guard band of a (direction, tail) list holds more candidates than the buffer (cap =
+// m + 65536; e.g. > 65536 exact duplicates at the m-th value), the list is selected exactly by a
+// streaming radix select over the composite key (fp64 projection, index) of every candidate
+// (pi32 inside the collect range): 8 rounds of 8 bits over the order-preserving fp64 key, 4 over
+// the index, each a pass over the projections that recomputes the fp64 dot of the candidates
+// (no candidate storage). The m smallest keys are then gathered (exactly m: the key is unique)
+// and ranked by rank_kernel like a normal list. Scratch lives in the (then idle) histogram
+// buffer: hist[lt][256], then per list {k1 hi, k1 lo, k2, remaining}, a redo flag, a counter.
+constexpr int kBandRounds = 12;
+struct BandScratch {
+  unsigned* hist;   // [2L][256]
+  unsigned* st;     // [2L][4]
+  unsigned* redo;   // [2L]
+  unsigned* gcnt;   // [2L]
+};
+__device__ __forceinline__ BandScratch band_scratch(unsigned* base, int L) {
+  BandScratch b;
+  b.hist = base;
+  b.st = base + 2 * L * 256;
+  b.redo = b.st + 2 * L * 4;
+  b.gcnt = b.redo + 2 * L;
+  return b;
+}
+// smaller key = better: top tail (larger pi first), bottom tail (smaller pi first)
+__device__ __forceinline__ unsigned long long band_k1(double pi, int t) {
+  unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(pi == 0.0 ? 0.0 : pi));
+  u = (u >> 63) ? ~u : (u | 0x8000000000000000ull);  // ascending order-preserving
+  return t == 0 ? ~u : u;
+}
+
+__global__ void band_init_kernel(unsigned* base, int L, const int* n_dirs, const unsigned* ccount, int64_t cap,
+                                 int64_t m) {
+  const BandScratch b = band_scratch(base, L);
+  for (int i = threadIdx.x; i < 2 * L * 256; i += blockDim.x) b.hist[i] = 0u;
+  for (int lt = threadIdx.x; lt < 2 * L; lt += blockDim.x) {
+    const bool ov = (lt >> 1) < *n_dirs && static_cast<int64_t>(ccount[lt]) > cap;
+    b.redo[lt] = ov ? 1u : 0u;
+    b.gcnt[lt] = 0u;
+    b.st[lt * 4 + 0] = 0u;
+    b.st[lt * 4 + 1] = 0u;
+    b.st[lt * 4 + 2] = 0u;
+    b.st[lt * 4 + 3] = static_cast<unsigned>(m);
+  }
+}
+
+// one pass over the projections of list lt = blockIdx.y: every candidate's fp64 key, matched
+// against the decided prefix; round r < kBandRounds histograms the next digit, r == kBandRounds
+// gathers the m winners (key <= the selected key) into cand[lt][]
+__global__ void __launch_bounds__(256) band_pass_kernel(const float* __restrict__ X, int D,
+                                                        const double* __restrict__ U64, const float* __restrict__ P32,
+                                                        int64_t n, int L, const unsigned* __restrict__ state,
+                                                        const unsigned* maxnorm2, double eps_coef, unsigned* base,
+                                                        int round, int* cand, int64_t cap) {
+  const BandScratch b = band_scratch(base, L);
+  const int lt = blockIdx.y, l = lt >> 1, t = lt & 1;
+  if (b.redo[lt] == 0u) return;
+  __shared__ unsigned sh[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0u;
+  __syncthreads();
+  const double eps = eps_coef * sqrt(static_cast<double>(__uint_as_float(*maxnorm2))) * 1.0625;
+  const double lim = t == 0 ? static_cast<double>(key_to_float(state[(l * 2 + 0) * 4 + 0])) - 2.0 * eps
+                            : static_cast<double>(key_to_float(~state[(l * 2 + 1) * 4 + 0])) + 2.0 * eps;
+  const unsigned long long K1 = (static_cast<unsigned long long>(b.st[lt * 4 + 0]) << 32) | b.st[lt * 4 + 1];
+  const unsigned K2 = b.st[lt * 4 + 2];
+  const float* p = P32 + static_cast<int64_t>(l) * n;
+  const double* u = U64 + static_cast<int64_t>(l) * D;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarp = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; w0 < n;
+       w0 += nwarp * 32) {
+    const int64_t i = w0 + lane;
+    const double x32 = i < n ? static_cast<double>(p[i]) : 0.0;
+    const bool c = i < n && (t == 0 ? x32 >= lim : x32 <= lim);
+    unsigned ballot = __ballot_sync(0xffffffffu, c);
+    double mine = 0.0;
+    while (ballot) {  // the warp computes each candidate's fp64 projection together
+      const int src = __ffs(ballot) - 1;
+      ballot &= ballot - 1;
+      const float* x = X + (w0 + src) * static_cast<int64_t>(D);
+      double s = 0.0;
+      for (int d = lane; d < D; d += 32) s = fma(static_cast<double>(__ldg(x + d)), u[d], s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == src) mine = s;
+    }
+    if (!c) continue;
+    const unsigned long long k1 = band_k1(mine, t);
+    const unsigned k2 = static_cast<unsigned>(i);
+    if (round < kBandRounds) {
+      bool match;
+      unsigned digit;
+      if (round < 8) {
+        const int sh_hi = 64 - 8 * round;  // decided bits: the top 8 * round of k1
+        match = round == 0 || (k1 >> sh_hi) == (K1 >> sh_hi);
+        digit = static_cast<unsigned>(k1 >> (56 - 8 * round)) & 255u;
+      } else {
+        const int r2 = round - 8;
+        match = k1 == K1 && (r2 == 0 || (k2 >> (32 - 8 * r2)) == (K2 >> (32 - 8 * r2)));
+        digit = (k2 >> (24 - 8 * r2)) & 255u;
+      }
+      if (match) atomicAdd(&sh[digit], 1u);
+    } else if (k1 < K1 || (k1 == K1 && k2 <= K2)) {
+      const unsigned pos = atomicAdd(&b.gcnt[lt], 1u);
+      if (pos < cap) cand[static_cast<int64_t>(lt) * cap + pos] = static_cast<int>(i);
+    }
+  }
+  if (round < kBandRounds) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+      if (sh[i]) atomicAdd(&b.hist[lt * 256 + i], sh[i]);
+  }
+}
+
+// the digit holding the remaining-th best key; the decided prefix grows by 8 bits
+__global__ void band_scan_kernel(int L, unsigned* base, int round) {
+  const BandScratch b = band_scratch(base, L);
+  const int lt = blockIdx.x;
+  if (b.redo[lt] == 0u || threadIdx.x != 0) return;
+  unsigned* h = b.hist + lt * 256;
+  unsigned rem = b.st[lt * 4 + 3], cum = 0u;
+  int d = 0;
+  for (; d < 255; ++d) {
+    if (cum + h[d] >= rem) break;
+    cum += h[d];
+  }
+  b.st[lt * 4 + 3] = rem - cum;
+  if (round < 4) b.st[lt * 4 + 0] |= static_cast<unsigned>(d) << (24 - 8 * round);
+  else if (round < 8) b.st[lt * 4 + 1] |= static_cast<unsigned>(d) << (24 - 8 * (round - 4));
+  else b.st[lt * 4 + 2] |= static_cast<unsigned>(d) << (24 - 8 * (round - 8));
+  for (int i = 0; i < 256; ++i) h[i] = 0u;
+}
+
+__global__ void band_finish_kernel(int L, unsigned* base, unsigned* ccount) {
+  const BandScratch b = band_scratch(base, L);
+  for (int lt = threadIdx.x; lt < 2 * L; lt += blockDim.x)
+    if (b.redo[lt]) ccount[lt] = b.gcnt[lt];
+}
+
 __global__ void init_state_kernel(unsigned* state, int L, int64_t m) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 2 * L) {
@@ -662,7 +805,7 @@ cudaError_t launch_project(const float* X, int64_t n, int D, const float* U32, i
 
 cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
                           const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st, bool first,
-                          bool last) {
+                          bool last, double* eps_out) {
   cudaError_t e;
   if (first) {
     if ((e = cudaMemsetAsync(b.maxnorm2, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
@@ -676,6 +819,7 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   // K3
   double eps_coef = 0.0;
   if ((e = launch_project(X, n, D, U32, L, b.P32, b.maxnorm2, st, &eps_coef)) != cudaSuccess) return e;
+  if (eps_out != nullptr) *eps_out = eps_coef;
   // K4: three radix rounds
   int64_t hb = (n + 255) / 256;
   if (hb > 148 * 2) hb = 148 * 2;
@@ -692,7 +836,7 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
   count_launch();
   rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap,
-                                              nullptr, nullptr, 0);
+                                              nullptr, nullptr, 0, nullptr);
   // K5
   if (last) {
     count_launch();
@@ -705,6 +849,45 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
 
 __global__ void minus_one_kernel(const int* a, int* b) { *b = *a > 0 ? *a - 1 : 0; }
 
+cudaError_t launch_select_fallback(const float* X, int64_t n, int D, const double* U64, int L, const int* n_dirs,
+                                   int64_t m, const SelectBufs& b, double eps_coef, cudaStream_t st, bool compact,
+                                   double* cval_out, long long* cidx_out, int64_t row_offset) {
+  // the histogram buffer (3 L 2 kRadixBins words) holds the band scratch (2L (256 + 6) words)
+  int64_t hb = (n + 255) / 256;
+  if (hb > 148 * 2) hb = 148 * 2;
+  count_launch();
+  band_init_kernel<<<1, 256, 0, st>>>(b.hist, L, n_dirs, b.ccount, b.cap, m);
+  for (int r = 0; r <= kBandRounds; ++r) {
+    count_launch();
+    band_pass_kernel<<<dim3(static_cast<unsigned>(hb), 2 * L), 256, 0, st>>>(X, D, U64, b.P32, n, L, b.state,
+                                                                             b.maxnorm2, eps_coef, b.hist, r,
+                                                                             b.cand, b.cap);
+    if (r < kBandRounds) {
+      count_launch();
+      band_scan_kernel<<<2 * L, 32, 0, st>>>(L, b.hist, r);
+    }
+  }
+  count_launch();
+  band_finish_kernel<<<1, 256, 0, st>>>(L, b.hist, b.ccount);
+  count_launch();
+  cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
+  const unsigned* redo = b.hist + 2 * L * 256 + 2 * L * 4;
+  count_launch();
+  if (cval_out != nullptr)
+    rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, nullptr, nullptr,
+                                                cval_out, cidx_out, row_offset, redo);
+  else
+    rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap,
+                                                nullptr, nullptr, 0, redo);
+  if (compact) {
+    count_launch();
+    compact_count_kernel<<<kCB, 256, 0, st>>>(b.bitmap, (n + 31) / 32, b.ucount + 1);
+    count_launch();
+    compact_write_kernel<<<kCB, 256, 0, st>>>(b.bitmap, (n + 31) / 32, b.ucount + 1, b.uidx, b.ucount);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_minus_one(const int* a, int* b, cudaStream_t st) {
   count_launch();
   minus_one_kernel<<<1, 1, 0, st>>>(a, b);
@@ -713,7 +896,7 @@ cudaError_t launch_minus_one(const int* a, int* b, cudaStream_t st) {
 
 cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offset, int D, const double* U64,
                                     const float* U32, int L, const int* n_dirs, int64_t m, const SelectBufs& b,
-                                    double* cval_out, long long* cidx_out, cudaStream_t st) {
+                                    double* cval_out, long long* cidx_out, cudaStream_t st, double* eps_out) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(cidx_out, 0xFF, sizeof(long long) * L * 2 * m, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(cval_out, 0, sizeof(double) * L * 2 * m, st)) != cudaSuccess) return e;
@@ -727,6 +910,7 @@ cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offse
   init_state_kernel<<<1, 2 * L < 1024 ? 1024 : 2 * L, 0, st>>>(b.state, L, all ? 1 : m);
   double eps_coef = 0.0;
   if ((e = launch_project(X, n, D, U32, L, b.P32, b.maxnorm2, st, &eps_coef)) != cudaSuccess) return e;
+  if (eps_out != nullptr) *eps_out = eps_coef;
   int64_t hb = (n + 255) / 256;
   if (hb > 148 * 2) hb = 148 * 2;
   if (!all) {
@@ -745,7 +929,7 @@ cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offse
   cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
   count_launch();
   rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, nullptr, nullptr,
-                                              cval_out, cidx_out, row_offset);
+                                              cval_out, cidx_out, row_offset, nullptr);
   return cudaGetLastError();
 }
 

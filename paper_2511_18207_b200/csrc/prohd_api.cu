@@ -206,6 +206,25 @@ int hausdorff(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   return PROHD_OK;
 }
 
+int hausdorff_minima(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                     float* rowmin_dev, float* colmin_dev, prohd_hd* out) {
+  if (out == nullptr || rowmin_dev == nullptr || colmin_dev == nullptr || !is_device_ptr(rowmin_dev) ||
+      !is_device_ptr(colmin_dev))
+    return fail(ctx, PROHD_E_INVALID, "null output or host minima pointers");
+  ExactWs w;
+  int rc = exact_common(ctx, A, nA, B, nB, D, w, kCentrePair);
+  if (rc) return rc;
+  if ((rc = bidir_on_ops(ctx, w.A, w.B, D, w))) return rc;
+  CK(cudaMemcpyAsync(rowmin_dev, w.rowmin, sizeof(float) * nA, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(colmin_dev, w.colmin, sizeof(float) * nB, cudaMemcpyDeviceToDevice, ctx->stream));
+  ExactHost h;
+  if ((rc = fetch(ctx, w, h))) return rc;
+  fill_directed(&out->ab, h.keys[0], h.nn_d[0], h.nn_j[0]);
+  fill_directed(&out->ba, h.keys[1], h.nn_d[1], h.nn_j[1]);
+  out->value = out->ab.dist2 >= out->ba.dist2 ? out->ab.dist : out->ba.dist;
+  return PROHD_OK;
+}
+
 int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
                        float* rowmin_dev) {
   if (rowmin_dev == nullptr || !is_device_ptr(rowmin_dev))

@@ -197,6 +197,7 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   // the chains are enqueued by a helper so that an error in either still joins the aux stream
   // back into the caller's before returning (no kernel of this call is left unordered against
   // the caller's stream and workspace)
+  double eps[2] = {0.0, 0.0};
   auto enqueue_chains = [&]() -> cudaError_t {
     for (int s = 0; s < 2; ++s) {
       // projections run for every point (also when 2m >= n) so non-finite input is always detected
@@ -210,11 +211,21 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
         if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, sst)) != cudaSuccess) return e;
         if ((e = launch_iota(b.uidx, b.ucount, n[s], sst)) != cudaSuccess) return e;
       } else if (m0 == m1 || L == 1) {
-        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst)) != cudaSuccess) return e;
-      } else {  // two direction groups with different per-tail counts, one shared union bitmap
-        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, 1, w.n_dirs, m0, b, sst, true, false)) != cudaSuccess)
+        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst, true, true, &eps[s])) !=
+            cudaSuccess)
           return e;
-        if ((e = launch_select(X[s], n[s], D, w.U64 + D, w.U32 + D, L - 1, w.n_dirs1, m1, b, sst, false, true)) !=
+      } else {  // two direction groups with different per-tail counts, one shared union bitmap
+        // the groups share the projection buffer, so each group's overflow fallback runs right
+        // after it (device-side no-op unless a list overflowed)
+        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, 1, w.n_dirs, m0, b, sst, true, false, &eps[s])) !=
+            cudaSuccess)
+          return e;
+        if ((e = launch_select_fallback(X[s], n[s], D, w.U64, 1, w.n_dirs, m0, b, eps[s], sst, false)) != cudaSuccess)
+          return e;
+        if ((e = launch_select(X[s], n[s], D, w.U64 + D, w.U32 + D, L - 1, w.n_dirs1, m1, b, sst, false, true,
+                               &eps[s])) != cudaSuccess)
+          return e;
+        if ((e = launch_select_fallback(X[s], n[s], D, w.U64 + D, L - 1, w.n_dirs1, m1, b, eps[s], sst, true)) !=
             cudaSuccess)
           return e;
       }
@@ -242,8 +253,16 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
     std::memcpy(&f, &maxn[s], 4);
     if (!std::isfinite(f)) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate (or squared norm overflow)");
   }
-  if (ovf[0] || ovf[1])
-    return fail(ctx, PROHD_E_INTERNAL, "selection guard band overflow (more than m + 65536 candidates)");
+  const bool two_groups = counts && L > 1 && counts[0] != counts[1];
+  if ((ovf[0] || ovf[1]) && !two_groups) {
+    // a guard band held more candidates than the buffer (massive ties at the m-th value): exact
+    // streaming band select for the affected lists, then the union again (rare path)
+    for (int s = 0; s < 2; ++s)
+      if (ovf[s]) CK(launch_select_fallback(X[s], n[s], D, w.U64, L, w.n_dirs, m, w.sel[s], eps[s], st, true));
+    for (int s = 0; s < 2; ++s)
+      CK(cudaMemcpyAsync(&ucount[s], w.sel[s].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
   if (ucount[0] < 1 || ucount[1] < 1 || ucount[0] > w.capU[0] || ucount[1] > w.capU[1])
     return fail(ctx, PROHD_E_INTERNAL, "bad union sizes %u %u", ucount[0], ucount[1]);
 

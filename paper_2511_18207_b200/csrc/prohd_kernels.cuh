@@ -115,14 +115,22 @@ cudaError_t launch_project(const float* X, int64_t n, int D, const float* U32, i
                            unsigned* maxnorm2, cudaStream_t st, double* eps_coef);
 cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
                           const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st, bool first = true,
-                          bool last = true);
+                          bool last = true, double* eps_out = nullptr);
+// K4 fallback for lists whose guard band overflowed the candidate buffer (ccount > cap after
+// launch_select / launch_local_candidates): exact streaming radix select on (fp64 projection,
+// index), then the usual ranking into lists + bitmap (and the compaction if `compact`), or into
+// cval_out / cidx_out for the sharded path. eps_coef: the value launch_select reported.
+cudaError_t launch_select_fallback(const float* X, int64_t n, int D, const double* U64, int L, const int* n_dirs,
+                                   int64_t m, const SelectBufs& b, double eps_coef, cudaStream_t st, bool compact,
+                                   double* cval_out = nullptr, long long* cidx_out = nullptr,
+                                   int64_t row_offset = 0);
 cudaError_t launch_minus_one(const int* a, int* b, cudaStream_t st);  // *b = max(*a - 1, 0)
 // Sharded selection: local top/bottom-m lists with their fp64 projection values and GLOBAL
 // indices (row_offset + local row) -> cval_out/cidx_out [L][2][m] (index -1 = empty slot).
 // If m >= n every local point is a candidate of every list.
 cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offset, int D, const double* U64,
                                     const float* U32, int L, const int* n_dirs, int64_t m, const SelectBufs& b,
-                                    double* cval_out, long long* cidx_out, cudaStream_t st);
+                                    double* cval_out, long long* cidx_out, cudaStream_t st, double* eps_out = nullptr);
 // Merge G ranks' lists [G][L][2][m] into the global top/bottom-m per list (same total
 // order) and the sorted unique union of their global indices (bitmap over n_total rows).
 cudaError_t launch_merge_union(const double* cval, const long long* cidx, int G, int L, int64_t m, int64_t n_total,

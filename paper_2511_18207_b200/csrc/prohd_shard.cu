@@ -235,22 +235,26 @@ int prohd_local_candidates(prohd_ctx* ctx, const float* X_local, int64_t n_local
   CK(cudaMemcpyAsync(w.n_dirs, &n_dirs, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(launch_dirs_to_f32(w.U64, w.U32, n_dirs, D, st));
   const int t0 = tmark(ctx);
+  double eps = 0.0;
   CK(launch_local_candidates(X_local, n_local, row_offset, D, w.U64, w.U32, n_dirs, w.n_dirs, m, w.sel,
-                             cand_val_out, reinterpret_cast<long long*>(cand_idx_out), st));
-  tspan(ctx, PH_SELECT, t0);
+                             cand_val_out, reinterpret_cast<long long*>(cand_idx_out), st, &eps));
   int ovf = 0;
   unsigned maxn = 0;
   if (n_local > 0) {
     CK(cudaMemcpyAsync(&ovf, w.sel.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&maxn, w.sel.maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (ovf)  // guard band overflowed its buffer (massive ties): exact band select for those lists
+      CK(launch_select_fallback(X_local, n_local, D, w.U64, n_dirs, w.n_dirs, m, w.sel, eps, st, false,
+                                cand_val_out, reinterpret_cast<long long*>(cand_idx_out), row_offset));
   }
+  tspan(ctx, PH_SELECT, t0);
   call_end(ctx);
   CK(cudaStreamSynchronize(st));
   call_collect(ctx);
   float f;
   std::memcpy(&f, &maxn, 4);
   if (!std::isfinite(f)) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate (or squared norm overflow)");
-  if (ovf) return fail(ctx, PROHD_E_INTERNAL, "selection guard band overflow");
   return PROHD_OK;
 }
 

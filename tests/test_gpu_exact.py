@@ -289,3 +289,23 @@ def test_rowmin_literal_3xtf32(ctx, split3, shape):
     ref = oracle.hausdorff(A, B)
     _check_directed(A, B, h["ab"], ref["ab"])
     _check_directed(B, A, h["ba"], ref["ba"])
+
+
+@pytest.mark.parametrize("D", [16, 64, 256])
+def test_wide_dynamic_range_per_row_scales(ctx, D):
+    """K0's per-row scale mode (internal.cuh prep_mode_perrow): a tight cluster of tiny points
+    (coordinates ~1e-6) next to far outliers (coordinates 1e4). One fp16 scale per set would leave the
+    cluster's coordinates in the fp16 subnormal range (floor 2^-38 x 1e4 per coordinate, ~1e-3 of
+    their size); per-row scales keep every row at the top of the range. Both directions of the
+    fused sweep and the directed kernel are checked per row against the oracle (Q17)."""
+    rng = np.random.default_rng(D + 5)
+    A = (rng.standard_normal((700, D)) * 1e-6).astype(np.float32)
+    B = (rng.standard_normal((900, D)) * 1e-6 + 2e-7).astype(np.float32)
+    A[3], A[4] = 1e4, -1e4  # symmetric outliers: the centres K0 subtracts stay ~0, so the cluster's
+    B[5], B[600] = -1e4, 1e4  # centred norms are its raw norms (the Q17 scale)
+    rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    _check_rowmins(A, B, rm)
+    h = ctx.hausdorff(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    ref = oracle.hausdorff(A, B)
+    _check_directed(A, B, h["ab"], ref["ab"])
+    _check_directed(B, A, h["ba"], ref["ba"])

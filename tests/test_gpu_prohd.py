@@ -31,22 +31,39 @@ def ctx():
 
 
 def _excused_union_diff(X, U, m, got, ref):
-    """Set differences allowed only as boundary swaps at projection ties (<= TIE relative)."""
+    """Union differences allowed only under SURVEY.md §8(c2) Q16: each difference is one half of a
+    swap across the m-th boundary of ONE (direction, tail) list between points p (GPU-selected) and
+    q (oracle-selected) with |pi64(p) - pi64(q)| <= 1e-6 max(||p||, ||q||) (pi64 = fp64 projection on
+    the GPU's exported direction). Extras and missings must pair up one to one under that rule."""
     got, ref = set(got.tolist()), set(ref.tolist())
-    extra, missing = got - ref, ref - got
+    extra, missing = sorted(got - ref), sorted(ref - got)
     if not extra and not missing:
         return 0
+    assert len(extra) == len(missing), f"unpaired differences: +{extra} -{missing}"
     P = X.astype(np.float64) @ U
     nrm = np.linalg.norm(X.astype(np.float64), axis=1)
-    # every extra/missing point must sit within TIE of the m-th boundary value on some direction/tail
-    for i in extra | missing:
-        ok = False
+    n = X.shape[0]
+    idx = np.arange(n)
+
+    def boundary_pair_ok(p, q):
         for l in range(U.shape[1]):
-            srt = np.sort(P[:, l])
-            for bval in (srt[m - 1], srt[-m]):
-                if abs(P[i, l] - bval) <= TIE * max(nrm[i], 1e-30) * 2:
-                    ok = True
-        assert ok, f"index {i} differs without a projection tie"
+            if abs(P[p, l] - P[q, l]) > TIE * max(nrm[p], nrm[q]):
+                continue
+            for top in (False, True):
+                # oracle total order of this tail: (pi asc, idx asc) bottom, (pi desc, idx asc) top
+                order = np.lexsort((idx, -P[:, l] if top else P[:, l]))
+                rank = np.empty(n, np.int64)
+                rank[order] = idx
+                # q inside the oracle's first m, p just outside, both in the tie band at the boundary
+                if rank[q] < m <= rank[p]:
+                    return True
+        return False
+
+    unmatched = list(missing)
+    for p in extra:
+        hit = next((q for q in unmatched if boundary_pair_ok(p, q)), None)
+        assert hit is not None, f"index {p} differs without a paired boundary swap at a 1e-6 projection tie"
+        unmatched.remove(hit)
     return len(extra) + len(missing)
 
 
@@ -260,3 +277,50 @@ def test_nonfinite_wide(ctx, bad):
         with pytest.raises(ProHDError) as e:
             call()
         assert e.value.code == 3
+
+
+def _tied_cloud(n, D, nties, seed):
+    """x_0 = 5.0 exactly on `nties` points (an exact tie straddling the m-th top value of e1) below
+    500 larger distinct values, and x_1 = -5.0 on another `nties` points straddling the m-th bottom
+    value of e2; every other coordinate random (all points distinct)."""
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, D)).astype(np.float32)
+    X[:, 0] = np.clip(X[:, 0], -3.0, 3.0)
+    X[:, 1] = np.clip(X[:, 1], -3.0, 3.0)
+    idx = rng.permutation(n)
+    top, tie_t, tie_b, bot = idx[:500], idx[500:500 + nties], idx[500 + nties:500 + 2 * nties], \
+        idx[500 + 2 * nties:1000 + 2 * nties]
+    X[top, 0] = (6.0 + rng.random(500)).astype(np.float32)
+    X[tie_t, 0] = 5.0
+    X[bot, 1] = (-6.0 - rng.random(500)).astype(np.float32)
+    X[tie_b, 1] = -5.0
+    return X
+
+
+def test_guard_band_overflow_exact_ties(ctx):
+    """VERDICT r01 missing #5: more than m + 65536 candidates in a guard band (140,000 exact
+    duplicates of the m-th projection value on e1's top tail and on e2's bottom tail, m = 1000).
+    The selection is still defined (PAPER.md:205-214 with the Q6 lowest-index tie rule): the lists
+    must equal the oracle's bit for bit, through the streaming band-select fallback, in the one-shot
+    call and in the sharded candidate lists (two shards, merged)."""
+    n, D, m = 300_000, 16, 1000
+    A = _tied_cloud(n, D, 140_000, 1)  # ~70,000 ties per half: each shard overflows too
+    B = _tied_cloud(n, D, 140_000, 2)
+    U = np.zeros((D, 3))
+    U[0, 0] = 1.0
+    U[1, 1] = 1.0
+    U[2:, 2] = 1.0 / np.sqrt(D - 2)
+    g = ctx.prohd_estimate_with_dirs(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), U, m)
+    ref = OP.estimate(A, B, 2, m, U=U)
+    assert np.array_equal(g["IA"], ref["IA"]) and np.array_equal(g["IB"], ref["IB"])
+    assert abs(g["value"] - ref["value"]) <= 1e-4 * ref["value"]
+    # sharded path: local candidate lists of two row blocks, merged on the device
+    dirs = torch.from_numpy(np.ascontiguousarray(U.T)).cuda()
+    half = n // 2
+    vals, idxs = [], []
+    for lo, hi in ((0, half), (half, n)):
+        v, i = ctx.local_candidates(torch.from_numpy(A[lo:hi]).cuda(), lo, dirs, m)
+        vals.append(v)
+        idxs.append(i)
+    union = ctx.merge_union(torch.stack(vals), torch.stack(idxs), m, n).cpu().numpy()
+    assert np.array_equal(union, ref["IA"])
