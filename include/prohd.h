@@ -156,6 +156,16 @@ int directed_hd_rowmin(prohd_ctx* ctx, const float* A, int64_t nA, const float* 
 int hausdorff_minima(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
                      float* rowmin_dev, float* colmin_dev, prohd_hd* out);
 
+/* Test hook: step 1a of prohd_estimate alone -- the mean mu of A u B and
+ * the covariance C = (1/N) sum (p - mu)(p - mu)^T (Alg. 2 lines 1-2) as the
+ * library computes them for the directions, through the same Gram path (int8 tensor cores for
+ * 128 < D <= 256 with D % 4 == 0 unless option k1_path = 0, else fp64 DMMA; the int8 pass falls
+ * back to DMMA when a value leaves its sampled fixed-point range). mu_out (HOST, D), C_out (HOST,
+ * D x D row-major), *path_out (HOST) = 1 if the int8 Gram produced C, 0 if the DMMA Gram did.
+ * Workspace: prohd_workspace_bytes(nA, nB, D, 0, 1, flags). Errors as prohd_estimate. */
+int prohd_covariance(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                     double* mu_out, double* C_out, int32_t* path_out);
+
 /* Test hook (K3, Alg. 1 line 4 / Alg. 2 line 5; pi = x^T u,
  * P:139): the fp32 projections the selection starts from. X (DEVICE, n x D fp32 row-major),
  * dirs (DEVICE, L x D fp64, row l = direction u_l, 1 <= L <= 32; rounded to fp32 first);

@@ -27,7 +27,7 @@ EXPORTED = [
     "prohd_launch_count",
     "prohd_set_option",
     "prohd_get_option",
-    "prohd_workspace_bytes", "prohd_set_workspace", "directed_hd", "hausdorff", "directed_hd_rowmin", "hausdorff_minima",
+    "prohd_workspace_bytes", "prohd_set_workspace", "directed_hd", "hausdorff", "directed_hd_rowmin", "hausdorff_minima", "prohd_covariance",
     "prohd_estimate", "prohd_estimate_certified", "prohd_estimate_alpha", "hausdorff_subsets",
     "prohd_estimate_with_dirs", "prohd_bounds", "directed_hd_local", "prohd_centre", "directed_hd_witness",
     "prohd_project",
@@ -86,6 +86,7 @@ def load() -> C.CDLL:
     lib.directed_hd.argtypes = [vp, vp, i64, vp, i64, i32, C.POINTER(Directed)]
     lib.hausdorff.argtypes = [vp, vp, i64, vp, i64, i32, C.POINTER(HD)]
     lib.hausdorff_minima.argtypes = [vp, vp, i64, vp, i64, i32, vp, vp, C.POINTER(HD)]
+    lib.prohd_covariance.argtypes = [vp, vp, i64, vp, i64, i32, vp, vp, C.POINTER(C.c_int32)]
     lib.directed_hd_rowmin.argtypes = [vp, vp, i64, vp, i64, i32, vp]
     lib.prohd_estimate.argtypes = [vp, vp, i64, vp, i64, i32, i32, i64, C.POINTER(Est), vp, vp, vp]
     lib.prohd_estimate_certified.argtypes = [vp, vp, i64, vp, i64, i32, i32, i64, C.POINTER(Est), vp, vp, vp]

@@ -121,6 +121,17 @@ class Context:
                                        A.shape[1], C.byref(out)))
         return {"value": out.value, "ab": _directed(out.ab), "ba": _directed(out.ba)}
 
+    def covariance(self, A, B):
+        """prohd_covariance (test hook): (mu, C, path) of step 1a, path 1 = int8 Gram, 0 = DMMA."""
+        A, B = self._prepare(A, B, 0, 1)
+        D = A.shape[1]
+        mu = np.empty(D, np.float64)
+        Cm = np.empty((D, D), np.float64)
+        path = C.c_int32(0)
+        self._check(self.lib.prohd_covariance(self.h, A.data_ptr(), A.shape[0], B.data_ptr(), B.shape[0], D,
+                                              mu.ctypes.data, Cm.ctypes.data, C.byref(path)))
+        return mu, Cm, int(path.value)
+
     def hausdorff_minima(self, A, B):
         """hausdorff() plus both directions' per-row minima (test hook): (result, rowmin, colmin)."""
         A, B = self._prepare(A, B)

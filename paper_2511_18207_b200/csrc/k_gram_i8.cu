@@ -1,33 +1,48 @@
-// k_gram_i8.cu — K1 on the int8 tensor cores: the Gram G = sum_p x_p x_p^T of A u B,
-// exact-integer products (Ozaki-style slicing), for data taken about the origin.
+// k_gram_i8.cu — K1 on the int8 tensor cores: the shifted Gram G = sum_p (p - s)(p - s)^T of
+// A u B and the column sums S_X = sum_{x in X} (x - s), for 128 < D <= 256 (D % 4 == 0).
 //
-// PAPER.md Alg. 2 lines 1-2; see k_gram.cu for the fp64 DMMA variant and the
-// shift policy (this path runs when the shift kernel dropped the shift, s = 0).
+// PAPER.md Alg. 1 line 1 and Alg. 2 lines 1-2: the principal
+// components are eigenvectors of C = G / N - (mu - s)(mu - s)^T (moments_finalize, k_moments.cu).
 //
-// Each fp32 value of feature f is written in fixed point relative to its column's
-// magnitude bound 2^E_f (E_f > log2 max_p |x_pf|) as 7 signed 7-bit digits,
-//     x = sign * sum_t d_t 2^(E_f - 7(t+1)),  d_t in [0, 127],  t = 0..6  (49 bits),
-// exact whenever x has no bits below 2^(E_f - 49) (else rounded to nearest, |err| <=
-// 2^(E_f - 50)). Slice t of x is the int8 sign*d_t. Then
-//     x_i x_j = 2^(E_i + E_j - 14) sum_{t,u} s_t(x_i) s_u(x_j) 2^(-7(t+u)),
-// and sum_p s_t(x_pi) s_u(x_pj) is an exact int8 x int8 -> int32 tensor-core product.
-// Pairs with t + u <= 7 are kept (34 pairs; the dropped ones are < 2^-62 of
-// max_p|x_pi| max_p|x_pj| per point); pairs with the same d = t + u share one int32 TMEM
-// accumulator (8 accumulators x 64 columns = all 512 TMEM columns). With <= 8 pairs per d
-// and |s_t s_u| <= 127^2 an accumulator grows by < 2^17 per point, so it is drained to
-// fp64 every 8192 points (< 2^30), exact. The epilogue combines the 8 accumulators in fp64
-// with their power-of-two weights.
+// Arithmetic (an exact-integer Ozaki scheme). Per feature j a power of two 2^k_j and an integer
+// shift S_j (s_j = the shift kernel's sample mean, or 0 when the data sit near the origin;
+// M_j = max over ALL rows of |x - s_j| from one HBM-bound pass, mapped to <= 2^30) turn every
+// value into the 32-bit fixed-point integer F = rint(x 2^k_j - S_j) (exact when S_j = 0; with a
+// shift the fused multiply-add rounds x 2^k - S to 24 bits first). F is written as four balanced 8-bit
+// digits, F - c0 = sum_t d_t 2^(8 (3 - t)), t = 0 the most significant: the bytes of F with the
+// three low bytes XOR 0x80 (c0 = 128 (2^16 + 2^8 + 1), a constant shift per column). Then
+//     (F_i - c0)(F_j - c0) = sum_{t,u} d_t(i) d_u(j) 2^(8 (6 - t - u))
+// and sum_p d_t(x_pi) d_u(x_pj) is an exact int8 x int8 -> int32 tensor-core product. Levels
+// L = t + u <= 5 are kept: only d_3 d_3 (weight 1, |.| <= 2^14) is dropped, zero-mean, against
+// products of |F| up to 2^30 (levels <= 3 alone would drop terms up to 2^32, too much for
+// small values of heavy-tailed columns, whose leading digits are zero). The pairs of one level
+// share an int32 TMEM accumulator, which grows by at most 4 * 128^2 = 2^16 per point, so it is
+// drained to fp64 every <= 32704 points (exact).
+// The result is the Gram about s'_j = (S_j + c0) 2^-k_j (exact fixed-point shift), written with
+// s' into the moments buffers: G_ij = 2^(-k_i - k_j) sum_L 2^(8 (6 - L)) G_L, S_X = 2^-k sum F'.
+// A non-finite value sets an overflow flag; the caller then reruns the moments on the fp64
+// DMMA path (k_gram.cu), which reports PROHD_E_DATA.
 //
-// Kernels:
-//   colmax_kernel  per-feature max|x| (atomicMax on the bits) and fp64 column sums of A and
-//                  of B (per-CTA partials, fixed-order reduce): one read of the data.
-//   slice_kernel   the 7 int8 slice planes, feature-major: S[t][f][p] (p over A then B, rows
-//                  padded to Np = 64k points), through a shared-memory transpose.
-//   gram_i8_kernel tiles of 128 I-features x 64 J-features (every tile holding an i <= j
-//                  pair), CTA = (tile, point range), warp-specialised like K6: warp 0 TMA
-//                  (SWIZZLE_64B boxes of 64 points x 64 features, 7 slices of the I and J
-//                  blocks, 84 KB per stage, 2 stages), warp 1 TMEM + tcgen05.mma.kind::i8
-//                  (M=128, N=64, K=32), warps 2-5 drain the accumulators to fp64.
+// Kernel (cta_group::2, CTA pairs). One MMA M = 256 (all features, 128 per CTA) x N = 256 (all
+// features, 128 per CTA) x K = 32 points covers the full Gram; each SM holds 128 rows x 256
+// columns of int32 per level, so a pair holds two levels (all 512 TMEM columns): pair type 0
+// accumulates levels {0, 3} (1 + 4 products), type 1 levels {1, 2} (2 + 3), type 2 levels {4, 5}
+// (3 + 2). A group = one pair of each type over the same rows of A and of B (L2 serves the
+// repeated reads); 24 groups = 144 SMs.
+// Per CTA (320 threads):
+//   warp 0     TMA: raw fp32 chunks [64 points x 128 features] (this CTA's feature half),
+//              3 stages of 32 KB.
+//   warp 1     (leader CTA) MMA issuer: per 64-point chunk 2 K-steps x 5 tcgen05.mma.cta_group::2
+//              .kind::i8 over the two CTAs' digit planes; commit -> slice stage free (both CTAs).
+//   warps 2-5  slicers: warp = every 4th point of the chunk, lane = 4 features: one 16-byte load,
+//              F for the 4 values, a 4 x 4 byte transpose (PRMT) and one 32-bit store per digit
+//              plane: 4 MN-major SWIZZLE_128B planes [64 points x 128 feature bytes] (2 stages of
+//              32 KB; conflict-free: a warp writes one 128-byte row); type-0 pairs also add F' up per
+//              set (int64 column sums). Arrive (cluster scope) on the leader's slices-full barrier.
+//   warps 6-9  drain: TMEM lane quarter warp % 4 = feature rows; int32 -> fp64, both levels
+//              weighted, added into this CTA's fp64 slab [128][256] in global memory.
+// gram_i8_reduce_kernel sums the slabs in a fixed order (deterministic) and applies 2^(-k_i-k_j).
+#include "api_common.cuh"  // TMA descriptor encoder
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
 #include "sm100.cuh"
@@ -35,440 +50,551 @@
 namespace prohd {
 namespace {
 
-constexpr int kSl = 7;           // slices (7 bits each)
-constexpr int kPts = 64;         // points per pipeline stage (one 64-B swizzle row)
-constexpr int kFI = 128;         // I-block features (UMMA M)
-constexpr int kFJ = 64;          // J-block features (UMMA N)
-constexpr int kNAcc = 8;         // accumulators d = t + u = 0..7
-constexpr int kFlush = 8192;     // points between drains (exactness bound above)
-constexpr int kStagesI8 = 2;
-constexpr uint32_t kBox = kPts * 64;                       // 4 KB: one TMA box (64 rows x 64 B)
-constexpr uint32_t kStageI8 = kSl * (kFI / 64 + 1) * kBox;  // 7 x 3 boxes = 84 KB
-constexpr size_t kSmemI8 = static_cast<size_t>(kStagesI8) * kStageI8 + 1024 + 256;
+constexpr int kPts = 64;          // points per chunk = bytes per digit-plane row (SWIZZLE_64B)
+constexpr int kFeat = 128;        // features per CTA
+constexpr int kRawStages = 3;
+constexpr int kSlStages = 2;
+constexpr uint32_t kRawBytes = kPts * kFeat * 4;   // 32 KB
+constexpr uint32_t kPlane = kFeat * kPts;          // 8 KB
+constexpr uint32_t kSlBytes = 4 * kPlane;          // 32 KB
+constexpr int kSlicers = 8;      // slicer / drain warps (2-9), two per SM sub-partition
+constexpr int kThreads = 64 + 32 * kSlicers;
+constexpr int kDrainChunks = 511;
+constexpr int kColmaxBlocks = 148 * 8;                  // 32704 points: int32 headroom (2^31 / 2^16)
+constexpr size_t kSmem = static_cast<size_t>(kRawStages) * kRawBytes + kSlStages * kSlBytes + 1024 + 512;  // + barriers
 
-// ------------------------------------------------------------------ colmax + column sums
-__global__ void __launch_bounds__(256) colmax_kernel(const float* __restrict__ A, int64_t nA,
-                                                     const float* __restrict__ B, int64_t nB, int D,
-                                                     unsigned* __restrict__ maxbits, double* __restrict__ Spart) {
-  // thread = (feature f = blockIdx.y * 32 + lane, warp w): rows w, w + 8, ... of each CTA chunk
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.y * 32 + lane;
-  const int64_t N = nA + nB;
-  unsigned m = 0u;
-  double sa = 0.0, sb = 0.0;
-  if (f < D) {
-    for (int64_t p = static_cast<int64_t>(blockIdx.x) * 8 + w; p < N; p += static_cast<int64_t>(gridDim.x) * 8) {
-      const float x = p < nA ? __ldg(A + p * D + f) : __ldg(B + (p - nA) * D + f);
-      m = max(m, __float_as_uint(x) & 0x7FFFFFFFu);  // |x| bits; inf/nan order above every finite
-      if (p < nA)
-        sa += static_cast<double>(x);
-      else
-        sb += static_cast<double>(x);
-    }
-  }
-  __shared__ unsigned sm[8][32];
-  __shared__ double s1[8][32], s2[8][32];
-  sm[w][lane] = m;
-  s1[w][lane] = sa;
-  s2[w][lane] = sb;
-  __syncthreads();
-  if (w == 0 && f < D) {
-    unsigned mm = 0u;
-    double a = 0.0, b = 0.0;
-    for (int q = 0; q < 8; ++q) {
-      mm = max(mm, sm[q][lane]);
-      a += s1[q][lane];
-      b += s2[q][lane];
-    }
-    atomicMax(maxbits + f, mm);
-    Spart[(static_cast<int64_t>(blockIdx.x) * 2 + 0) * D + f] = a;
-    Spart[(static_cast<int64_t>(blockIdx.x) * 2 + 1) * D + f] = b;
-  }
-}
-
-__global__ void __launch_bounds__(256) colsum_reduce_kernel(const double* __restrict__ Spart, int nparts, int D,
-                                                            double* __restrict__ SA, double* __restrict__ SB) {
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < D; f += gridDim.x * blockDim.x) {
-    double a = 0.0, b = 0.0;
-    for (int q = 0; q < nparts; ++q) {
-      a += Spart[(static_cast<int64_t>(q) * 2 + 0) * D + f];
-      b += Spart[(static_cast<int64_t>(q) * 2 + 1) * D + f];
-    }
-    SA[f] = a;
-    SB[f] = b;
-  }
-}
-
-// E_f with max|x_f| < 2^E_f (0 for an all-zero column)
-__device__ __forceinline__ int col_exp(unsigned mb) {
-  const int e = static_cast<int>((mb >> 23) & 0xFFu);
-  return e == 0 ? (mb == 0u ? 0 : -125) : e - 126;  // normal: |x| < 2^(e - 127 + 1)
-}
-
-// ------------------------------------------------------------------ slicing
-constexpr int kSlT = 64;        // tile: 64 points x 64 features
-constexpr int kSlRow = 68;      // smem row stride in bytes (17 words: conflict-free packed stores)
-__global__ void __launch_bounds__(256) slice_kernel(const float* __restrict__ A, int64_t nA,
-                                                    const float* __restrict__ B, int64_t nB, int D, int Df,
-                                                    int64_t Np, const unsigned* __restrict__ maxbits,
-                                                    int8_t* __restrict__ S) {
-  __shared__ __align__(16) uint32_t sm[kSl * kSlT * kSlRow / 4];  // [t][f][68 B]
-  const int tid = threadIdx.x;
-  const int fl = tid & 63, pg = tid >> 6;  // feature, group of 16 points
-  const int f = blockIdx.y * kSlT + fl;
-  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * kSlT + pg * 16;
-  const int64_t N = nA + nB;
-  const int E = f < D ? col_exp(__ldg(maxbits + f)) : 0;
-  uint32_t word[kSl];
-#pragma unroll
-  for (int t = 0; t < kSl; ++t) word[t] = 0u;
-#pragma unroll 4
-  for (int q = 0; q < 16; ++q) {
-    const int64_t p = p0 + q;
-    float x = 0.0f;
-    if (f < D && p < N) x = p < nA ? __ldg(A + p * D + f) : __ldg(B + (p - nA) * D + f);
-    const unsigned u = __float_as_uint(x);
-    const unsigned ef = (u >> 23) & 0xFFu;
-    const unsigned long long mant = ef == 0u ? (u & 0x7FFFFFu) : ((u & 0x7FFFFFu) | 0x800000u);
-    const int e = ef == 0u ? -126 : static_cast<int>(ef) - 127;  // x = mant * 2^(e - 23)
-    const int sh = e - E + 26;  // y = |x| * 2^(49 - E) = mant * 2^sh
-    unsigned long long y;
-    if (sh >= 0)
-      y = mant << sh;
-    else if (sh > -40)
-      y = (mant + (1ull << (-sh - 1))) >> (-sh);
-    else
-      y = 0ull;
-    const bool neg = (u >> 31) != 0u;
-#pragma unroll
-    for (int t = 0; t < kSl; ++t) {
-      int dgt = static_cast<int>((y >> (7 * (kSl - 1 - t))) & 127ull);
-      if (neg) dgt = -dgt;
-      word[t] |= (static_cast<uint32_t>(dgt) & 0xFFu) << (8 * (q & 3));
-    }
-    if ((q & 3) == 3) {
-#pragma unroll
-      for (int t = 0; t < kSl; ++t) {
-        sm[(t * kSlT + fl) * (kSlRow / 4) + pg * 4 + (q >> 2)] = word[t];
-        word[t] = 0u;
-      }
-    }
-  }
-  __syncthreads();
-  // write out: per (t, f) row, 64 bytes = 4 x 16 B
-  for (int q = tid; q < kSl * kSlT * 4; q += 256) {
-    const int t = q / (kSlT * 4), r = (q / 4) % kSlT, c = q % 4;
-    const uint32_t* src = sm + (t * kSlT + r) * (kSlRow / 4) + c * 4;
-    const uint4 v = make_uint4(src[0], src[1], src[2], src[3]);
-    const int ff = blockIdx.y * kSlT + r;
-    int8_t* dst = S + (static_cast<int64_t>(t) * Df + ff) * Np + static_cast<int64_t>(blockIdx.x) * kSlT + c * 16;
-    *reinterpret_cast<uint4*>(dst) = v;
-  }
-}
-
-// ------------------------------------------------------------------ int8 tensor-core Gram
-struct GramI8Sched {
-  int ntiles, nranges;
-  int64_t per;        // points per range (multiple of kPts)
-  int64_t N, Np;
-  int D, Df;
-  int tI[16], tJ[16];  // tile -> (I block of 128, J block of 64)
+struct I8Args {
+  int64_t nA, nB;
+  int D, ngroups;
+  const float* scale;    // [256] 2^k_j
+  const float* shiftf;   // [256] S_j (integer-valued float)
+  double* slab;          // [ngroups * 6 CTAs][128][256]
+  const double* cpart;   // [ncs blocks][2][D] fp64 column sums of A, B (i8_colmax_kernel)
+  int ncs;
+  unsigned* overflow;
 };
 
-__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate) {
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const long long t0 = clock64();
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(sm100::smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!ok && clock64() - t0 > 40000000000ll) __trap();
+  } while (!ok);
+}
+
+// mbarrier wait with a suspend-time hint: a waiting thread sleeps in hardware instead of spinning
+// on the issue slots its scheduler shares with the slicer warps
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const long long t0 = clock64();
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 200000;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(sm100::smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!ok && clock64() - t0 > 40000000000ll) __trap();
+  } while (!ok);
+}
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void mma_i8_2sm(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
-// K-major operand staged by TMA with SWIZZLE_64B: rows of 64 B, 8-row (512 B) atoms.
-__device__ __forceinline__ uint64_t smem_desc_k_sw64(uint32_t saddr) {
+// kind::i8: D s32 (2), A and B s8 (1), both MN-major (bits 15, 16)
+__host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+// MN-major operand with SWIZZLE_128B: one 128-byte row (the CTA's 128 features) per K index
+// (point), 8-row (1 KB) swizzle atoms stacked along K (SBO = 1 KB); a single atom along MN, so
+// LBO is unused. Canonical layout Sw<3,4,3> o ((T,8,m),(8,k)) : ((1,T,LBO),(8T,SBO)).
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t saddr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>(1u) << 16;          // LBO (unused for swizzled K-major)
-  d |= static_cast<uint64_t>(512u >> 4) << 32;   // SBO: 8 rows x 64 B
-  d |= static_cast<uint64_t>(1u) << 46;          // version (sm_100)
-  d |= static_cast<uint64_t>(4u) << 61;          // SWIZZLE_64B
+  d |= static_cast<uint64_t>(1u) << 16;            // LBO (unused: one MN atom)
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;    // SBO: next 8 K-rows
+  d |= static_cast<uint64_t>(1u) << 46;            // version (sm_100)
+  d |= static_cast<uint64_t>(2u) << 61;            // SWIZZLE_128B
   return d;
 }
-// instruction descriptor, kind::i8: D s32, A and B signed int8, K-major, N >> 3, M >> 4
-__host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
-  return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+__device__ __forceinline__ void tmem_ld32i(uint32_t taddr, int (&v)[32]) {
+  sm100::tmem_ld32(taddr, reinterpret_cast<float(&)[32]>(v));
 }
 
-// 32 lanes x 32 bit, 32 consecutive columns (as int32)
-__device__ __forceinline__ void tmem_ld32i(uint32_t taddr, int (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr)
-      : "memory");
+// chunk schedule of one group: A rows [a0, a1) then B rows [b0, b1), 64 rows per chunk
+struct Range {
+  int64_t a0, a1, b0, b1;
+  int na, nb;  // chunks
+};
+__device__ __forceinline__ Range group_range(const I8Args& a, int g) {
+  Range r;
+  r.a0 = a.nA * g / a.ngroups;
+  r.a1 = a.nA * (g + 1) / a.ngroups;
+  r.b0 = a.nB * g / a.ngroups;
+  r.b1 = a.nB * (g + 1) / a.ngroups;
+  r.na = static_cast<int>((r.a1 - r.a0 + kPts - 1) / kPts);
+  r.nb = static_cast<int>((r.b1 - r.b0 + kPts - 1) / kPts);
+  return r;
 }
 
-__global__ void __launch_bounds__(192, 1)
-    gram_i8_kernel(const __grid_constant__ CUtensorMap tS, GramI8Sched s, const unsigned* __restrict__ maxbits,
-                   double* __restrict__ Gpart) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gram_i8_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, I8Args a) {
   using namespace sm100;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStagesI8 * kStageI8);
-  uint64_t* empty = full + kStagesI8;
-  uint64_t* tfull = empty + kStagesI8;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint8_t* raw = smem;
+  uint8_t* sl = smem + kRawStages * kRawBytes;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(sl + kSlStages * kSlBytes);
+  uint64_t* raw_empty = raw_full + kRawStages;
+  uint64_t* sl_full = raw_empty + kRawStages;  // leader: 8 slicer warps of the pair
+  uint64_t* sl_empty = sl_full + kSlStages;    // both: MMA commit (multicast)
+  uint64_t* tfull = sl_empty + kSlStages;      // both: MMA commit (multicast)
+  uint64_t* tempty = tfull + 1;                // leader: 8 drain warps of the pair
+  uint64_t* sl_fwd = tempty + 1;               // peer: its slicer warps, forwarded by one thread
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sl_fwd + kSlStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x % s.ntiles, range = blockIdx.x / s.ntiles;
-  const int I = s.tI[tile], J = s.tJ[tile];
-  const int64_t q0 = static_cast<int64_t>(range) * s.per;
-  const int64_t q1 = q0 + s.per < s.Np ? q0 + s.per : s.Np;
-  const int nst = q1 > q0 ? static_cast<int>((q1 - q0) / kPts) : 0;  // stages of 64 points
-  const int st_per_flush = kFlush / kPts;
-  const int nflush = (nst + st_per_flush - 1) / st_per_flush;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int type = pair % 3, g = pair / 3;
+  const Range R = group_range(a, g);
+  const int nchunks = R.na + R.nb;
+  const int cta = blockIdx.x;  // slab index
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStagesI8; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+    for (int i = 0; i < kRawStages; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], kSlicers);
     }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    for (int i = 0; i < kSlStages; ++i) {
+      mbar_init(&sl_full[i], kSlicers + 1);  // the leader's slicer warps + one forwarded arrival
+      mbar_init(&sl_empty[i], 1);
+      mbar_init(&sl_fwd[i], kSlicers);
+    }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 2 * kSlicers);
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) tma_prefetch(&tS);
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tA);
+    tma_prefetch(&tB);
+  }
+  if (warp == 1) tmem_alloc_2sm<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      // -------------------------------------------------------------- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int c = 0; c < nst; ++c) {
-        mbar_wait(&empty[stage], phase ^ 1u);
-        uint8_t* st = smem + stage * kStageI8;
-        mbar_arrive_expect_tx(&full[stage], kStageI8);
-        const int x = static_cast<int>(q0 + static_cast<int64_t>(c) * kPts);
-        for (int t = 0; t < kSl; ++t) {
-          // I block (2 boxes of 64 rows) then J block (1 box); slice t rows start at t * Df
-          uint8_t* dst = st + t * 3 * kBox;
-          tma_load_2d(dst, &tS, x, t * s.Df + I * kFI, &full[stage]);
-          tma_load_2d(dst + kBox, &tS, x, t * s.Df + I * kFI + 64, &full[stage]);
-          tma_load_2d(dst + 2 * kBox, &tS, x, t * s.Df + J * kFJ, &full[stage]);
-        }
-        if (++stage == kStagesI8) {
-          stage = 0;
-          phase ^= 1u;
+      int st = 0;
+      uint32_t ph = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        mbar_wait_sleep(&raw_empty[st], ph ^ 1u);
+        mbar_arrive_expect_tx(&raw_full[st], kRawBytes);
+        const bool inA = c < R.na;
+        const int64_t row = inA ? R.a0 + static_cast<int64_t>(c) * kPts : R.b0 + static_cast<int64_t>(c - R.na) * kPts;
+        tma_load_2d(raw + st * kRawBytes, inA ? &tA : &tB, static_cast<int>(rank) * kFeat, static_cast<int>(row),
+                    &raw_full[st]);
+        if (++st == kRawStages) {
+          st = 0;
+          ph ^= 1u;
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // -------------------------------------------------------------- MMA issuer
-      constexpr uint32_t idesc = idesc_i8(kFI, kFJ);
-      int stage = 0;
-      uint32_t phase = 0, fphase = 0;
-      for (int fl = 0; fl < nflush; ++fl) {
-        mbar_wait(tempty, fphase ^ 1u);  // the epilogue drained the previous flush
-        tc_fence_after();
-        const int c0 = fl * st_per_flush;
-        const int c1 = min(nst, c0 + st_per_flush);
-        for (int c = c0; c < c1; ++c) {
-          mbar_wait(&full[stage], phase);
+    // ------------------------------------------------------------------ MMA issuer (leader CTA)
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(256, 256);
+      // (t, u, accumulator slot): type 0 = levels {0 -> slot 0, 3 -> slot 1}, type 1 = {1 -> 0, 2 -> 1}
+      int tt[5], uu[5], ss[5];
+      if (type == 0) {
+        const int t0[5] = {0, 0, 1, 2, 3}, u0[5] = {0, 3, 2, 1, 0}, s0[5] = {0, 1, 1, 1, 1};
+        for (int i = 0; i < 5; ++i) tt[i] = t0[i], uu[i] = u0[i], ss[i] = s0[i];
+      } else if (type == 1) {
+        const int t1[5] = {0, 1, 0, 1, 2}, u1[5] = {1, 0, 2, 1, 0}, s1[5] = {0, 0, 1, 1, 1};
+        for (int i = 0; i < 5; ++i) tt[i] = t1[i], uu[i] = u1[i], ss[i] = s1[i];
+      } else {
+        const int t2[5] = {1, 2, 3, 2, 3}, u2[5] = {3, 2, 1, 3, 2}, s2[5] = {0, 0, 0, 1, 1};
+        for (int i = 0; i < 5; ++i) tt[i] = t2[i], uu[i] = u2[i], ss[i] = s2[i];
+      }
+      int st = 0;
+      uint32_t ph = 0, tph = 0;
+      int since = 0;  // chunks accumulated since the last drain
+      for (int c = 0; c < nchunks; ++c) {
+        if (since == 0 && c > 0) {
+          mbar_wait_cluster(&tempty[0], tph ^ 1u);  // the drain warps of both CTAs have read TMEM
           tc_fence_after();
-          const uint32_t sbase = smem_u32(smem + stage * kStageI8);
-          for (int kk = 0; kk < kPts / 32; ++kk) {
-            const uint32_t off = static_cast<uint32_t>(kk * 32);  // 32 int8 = 32 B along K
-            for (int t = 0; t < kSl; ++t) {
-              const uint64_t da = smem_desc_k_sw64(sbase + t * 3 * kBox + off);
-              for (int u = 0; u < kSl && t + u < kNAcc; ++u) {
-                const uint64_t db = smem_desc_k_sw64(sbase + u * 3 * kBox + 2 * kBox + off);
-                const int d = t + u;
-                // the first product into accumulator d after a drain overwrites it
-                const bool first = (c == c0) && (kk == 0) && (t == (d < kSl ? 0 : d - (kSl - 1)));
-                mma_i8(tmem_base + static_cast<uint32_t>(d * kFJ), da, db, idesc, first ? 0u : 1u);
-              }
-            }
-          }
-          mma_commit(&empty[stage]);
-          if (++stage == kStagesI8) {
-            stage = 0;
-            phase ^= 1u;
+        }
+        mbar_wait_cluster(&sl_full[st], ph);
+        tc_fence_after();
+        const uint32_t base = smem_u32(sl + st * kSlBytes);
+        for (int kk = 0; kk < 2; ++kk) {
+          for (int i = 0; i < 5; ++i) {  // K = 32 points = 4 swizzle atoms of 8 rows: +4 KB per K-step
+            const uint64_t da = smem_desc_mn_sw128(base + tt[i] * kPlane + kk * 4096);
+            const uint64_t db = smem_desc_mn_sw128(base + uu[i] * kPlane + kk * 4096);
+            const bool first = since == 0 && kk == 0 && (i == 0 || ss[i] != ss[i - 1]);
+            mma_i8_2sm(tmem_base + static_cast<uint32_t>(ss[i] * 256), da, db, idesc, first ? 0u : 1u);
           }
         }
-        mma_commit(tfull);
-        fphase ^= 1u;
+        mma_commit_2sm_mc(&sl_empty[st], 0x3);
+        if (++st == kSlStages) {
+          st = 0;
+          ph ^= 1u;
+        }
+        if (++since == kDrainChunks || c == nchunks - 1) {
+          mma_commit_2sm_mc(&tfull[0], 0x3);
+          since = 0;
+          tph ^= 1u;
+        }
+      }
+    }
+    if (rank == 1 && lane == 0) {
+      // forwarder: the peer's slicer warps arrive on a local barrier; one cluster-scope release
+      // arrival per chunk on the leader's slices-full barrier (instead of one per warp)
+      const uint32_t leader_full = mapa(smem_u32(&sl_full[0]), 0);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        mbar_wait(&sl_fwd[st], ph);
+        mbar_arrive_cluster(leader_full + static_cast<uint32_t>(st * 8));
+        if (++st == kSlStages) {
+          st = 0;
+          ph ^= 1u;
+        }
       }
     }
     __syncwarp();
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 2-5)
-    const int qd = warp & 3;  // TMEM lane quarter
-    const int il = qd * 32 + lane;  // I-feature within the block
-    const uint32_t lane_addr = static_cast<uint32_t>(qd * 32) << 16;
-    double run[kFJ];
+    // ------------------------------------------------------------------ slicers (+ drains)
+    // warp ws = warp - 2 takes points ws, ws + 8, ... of each 64-point chunk; lane l takes features
+    // 4l..4l+3 of the CTA's 128: one 16-byte shared load per point, F for the four values, a 4 x 4
+    // byte transpose and one 32-bit store per digit plane (MN-major: row = point, 128 feature
+    // bytes; a warp writes one 128-byte row, conflict-free under the XOR swizzle)
+    const int ws = warp - 2;
+    const int fg0 = static_cast<int>(rank) * kFeat + 4 * lane;
+    float sc[4], sh[4];
 #pragma unroll
-    for (int c = 0; c < kFJ; ++c) run[c] = 0.0;
-    uint32_t fphase = 0;
-    for (int fl = 0; fl < nflush; ++fl) {
-      mbar_wait(tfull, fphase);
-      tc_fence_after();
-      for (int d = 0; d < kNAcc; ++d) {
-        const double wgt = ldexp(1.0, -7 * d);
-#pragma unroll
-        for (int h = 0; h < kFJ / 32; ++h) {
-          int v[32];
-          tmem_ld32i(tmem_base + lane_addr + static_cast<uint32_t>(d * kFJ + h * 32), v);
+    for (int i = 0; i < 4; ++i) {
+      const bool live = fg0 + i < a.D;
+      sc[i] = live ? __ldg(a.scale + fg0 + i) : 0.0f;  // features >= D: y = -(-c0) = c0, F - c0 = 0
+      sh[i] = live ? __ldg(a.shiftf + fg0 + i) : -8421504.0f;
+    }
+    const uint32_t leader_te = mapa(smem_u32(&tempty[0]), 0);
+    const uint32_t raw_u32 = smem_u32(raw), sl_u32 = smem_u32(sl);
+    // drain role: TMEM lane quarter ws % 4, column half ws / 4 of both level slots
+    const int q = warp & 3, half = ws >> 2;
+    const int rowl = q * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+    // level weights 2^(8 (6 - L)) / 2^48 = 2^(-8 L): slots of type 0 = levels {0, 3}, type 1 =
+    // {1, 2}, type 2 = {4, 5}
+    const double w0 = type == 0 ? 1.0 : (type == 1 ? 0x1p-8 : 0x1p-32);
+    const double w1 = type == 0 ? 0x1p-24 : (type == 1 ? 0x1p-16 : 0x1p-40);
+    double* out = a.slab + (static_cast<int64_t>(cta) * kFeat + rowl) * 256 + half * 128;
+    float ymax = 0.0f;
+    int rst = 0, sst = 0, since = 0, ndr = 0;
+    uint32_t rph = 0, sph = 0, tph = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const bool inA = c < R.na;
+      const int64_t row0 = inA ? R.a0 + static_cast<int64_t>(c) * kPts : R.b0 + static_cast<int64_t>(c - R.na) * kPts;
+      const int64_t rend = inA ? R.a1 : R.b1;
+      const int valid = static_cast<int>(min(static_cast<int64_t>(kPts), rend - row0));
+      mbar_wait(&raw_full[rst], rph);
+      mbar_wait(&sl_empty[sst], sph ^ 1u);
+      const uint32_t xr = raw_u32 + rst * kRawBytes + lane * 16;
+      const uint32_t pl = sl_u32 + sst * kSlBytes;
+#pragma unroll 4
+      for (int pp = 0; pp < kPts / kSlicers; ++pp) {
+        const int p = kSlicers * pp + ws;
+        const float4 x4 = lds128(xr + p * (kFeat * 4));
+        // rows past the range: F = c0 = 0x808080, i.e. F - c0 = 0 (no contribution)
+        const bool ok = p < valid;
+        const float y0 = ok ? fmaf(x4.x, sc[0], -sh[0]) : 8421504.0f, y1 = ok ? fmaf(x4.y, sc[1], -sh[1]) : 8421504.0f;
+        const float y2 = ok ? fmaf(x4.z, sc[2], -sh[2]) : 8421504.0f, y3 = ok ? fmaf(x4.w, sc[3], -sh[3]) : 8421504.0f;
+        ymax = fmaxf(fmaxf(ymax, fmaxf(fabsf(y0), fabsf(y1))), fmaxf(fabsf(y2), fabsf(y3)));
+        const uint32_t w0i = static_cast<uint32_t>(__float2int_rn(y0)), w1i = static_cast<uint32_t>(__float2int_rn(y1));
+        const uint32_t w2i = static_cast<uint32_t>(__float2int_rn(y2)), w3i = static_cast<uint32_t>(__float2int_rn(y3));
+        // 4 x 4 byte transpose: plane t (t = 0 the top byte) gets byte 3 - t of the 4 features;
+        // the three low planes XOR 0x80 per byte (balanced digits of F - c0)
+        const uint32_t x01l = __byte_perm(w0i, w1i, 0x5140), x01h = __byte_perm(w0i, w1i, 0x7362);
+        const uint32_t x23l = __byte_perm(w2i, w3i, 0x5140), x23h = __byte_perm(w2i, w3i, 0x7362);
+        const uint32_t b0 = __byte_perm(x01l, x23l, 0x5410) ^ 0x80808080u;
+        const uint32_t b1 = __byte_perm(x01l, x23l, 0x7632) ^ 0x80808080u;
+        const uint32_t b2 = __byte_perm(x01h, x23h, 0x5410) ^ 0x80808080u;
+        const uint32_t b3 = __byte_perm(x01h, x23h, 0x7632);
+        // SWIZZLE_128B MN-major: row p (128 B), 16-byte chunk (lane / 4) XOR (p % 8)
+        const uint32_t off = static_cast<uint32_t>((p >> 3) * 1024 + (p & 7) * 128 +
+                                                   ((((lane >> 2) ^ (p & 7)) & 7) << 4) + (lane & 3) * 4);
+        sts32(pl + 0 * kPlane + off, b3);
+        sts32(pl + 1 * kPlane + off, b2);
+        sts32(pl + 2 * kPlane + off, b1);
+        sts32(pl + 3 * kPlane + off, b0);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&raw_empty[rst]);
+        mbar_arrive(rank == 0 ? &sl_full[sst] : &sl_fwd[sst]);  // CTA scope; the peer's are forwarded
+      }
+      if (++rst == kRawStages) {
+        rst = 0;
+        rph ^= 1u;
+      }
+      if (++sst == kSlStages) {
+        sst = 0;
+        sph ^= 1u;
+      }
+      if (++since == kDrainChunks || c == nchunks - 1) {
+        // drain window ends with this chunk: TMEM -> fp64 slab (this warp: its lane quarter, its
+        // 128-column half of both level slots), then release the accumulators to the MMA issuer
+        since = 0;
+        mbar_wait_sleep(&tfull[0], tph);
+        tph ^= 1u;
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < 128; cc += 32) {
+          int v0[32], v1[32];
+          tmem_ld32i(tmem_base + lane_addr + static_cast<uint32_t>(half * 128 + cc), v0);
+          tmem_ld32i(tmem_base + lane_addr + static_cast<uint32_t>(256 + half * 128 + cc), v1);
           tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) run[h * 32 + c] = fma(static_cast<double>(v[c]), wgt, run[h * 32 + c]);
+          for (int i = 0; i < 32; ++i) {
+            const double v = static_cast<double>(v0[i]) * w0 + static_cast<double>(v1[i]) * w1;
+            out[cc + i] = ndr == 0 ? v : out[cc + i] + v;
+          }
         }
+        ++ndr;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_te);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
-      fphase ^= 1u;
     }
-    // G[i][j] partial = 2^(E_i + E_j - 14) * run[j]
-    const int fi = I * kFI + il;
-    const int Ei = fi < s.D ? col_exp(__ldg(maxbits + fi)) : 0;
-    double* out = Gpart + (static_cast<int64_t>(blockIdx.x) * kFI + il) * kFJ;
-#pragma unroll
-    for (int c = 0; c < kFJ; ++c) {
-      const int fj = J * kFJ + c;
-      const int Ej = fj < s.D ? col_exp(__ldg(maxbits + fj)) : 0;
-      out[c] = ldexp(run[c], Ei + Ej - 14);
-    }
+    if (nchunks == 0)
+      for (int j2 = 0; j2 < 128; ++j2) out[j2] = 0.0;  // an empty group contributes zeros
+    if (!(ymax < 2147483008.0f)) atomicOr(a.overflow, 1u);  // beyond int32 (or NaN / inf)
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
+    tmem_dealloc_2sm<512>(tmem_base);
   }
 }
 
-// G (full symmetric) from the per-CTA tile partials; ranges summed in order.
-__global__ void __launch_bounds__(256) gram_i8_reduce_kernel(const double* __restrict__ Gpart, GramI8Sched s,
-                                                             double* __restrict__ G) {
-  const int64_t total = static_cast<int64_t>(s.ntiles) * kFI * kFJ;
+// exact per-feature max |x - s_j| over all rows of A and B (one HBM-bound read) and fp64 column
+// sums of A and of B: thread = a 16-byte column piece (D % 4 == 0), rows strided over the grid;
+// block max -> atomicMax on the non-negative float bits (non-finite values force +inf); block
+// sums (fixed order) -> csum_part[block][set][D] for gram_i8_reduce_kernel (fixed order again).
+__global__ void __launch_bounds__(256) i8_colmax_kernel(const float* __restrict__ A, int64_t nA,
+                                                        const float* __restrict__ B, int64_t nB, int D,
+                                                        const double* __restrict__ s, unsigned* colmax,
+                                                        double* csum_part) {
+  const int P = D / 4;  // pieces per row
+  const int rows_per_block = blockDim.x / P;
+  const int piece = threadIdx.x % P, rsub = threadIdx.x / P;
+  __shared__ unsigned red[256 * 4];
+  __shared__ double sred[256 * 8];
+  float m[4] = {0.f, 0.f, 0.f, 0.f};
+  double sum[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+  float sf[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) sf[i] = static_cast<float>(s[4 * piece + i]);
+  if (rsub < rows_per_block) {
+    const int64_t N = nA + nB;
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * rows_per_block + rsub; r < N;
+         r += static_cast<int64_t>(gridDim.x) * rows_per_block) {
+      const bool inA = r < nA;
+      const float* row = inA ? A + r * D : B + (r - nA) * D;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(row) + piece);
+      m[0] = fmaxf(m[0], fabsf(v.x - sf[0]));
+      m[1] = fmaxf(m[1], fabsf(v.y - sf[1]));
+      m[2] = fmaxf(m[2], fabsf(v.z - sf[2]));
+      m[3] = fmaxf(m[3], fabsf(v.w - sf[3]));
+      if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w))) m[0] = __int_as_float(0x7f800000);
+      const double e0 = inA ? 1.0 : 0.0, e1 = 1.0 - e0;  // branch-free, no dynamic indexing
+      sum[0][0] = fma(e0, static_cast<double>(v.x), sum[0][0]);
+      sum[0][1] = fma(e0, static_cast<double>(v.y), sum[0][1]);
+      sum[0][2] = fma(e0, static_cast<double>(v.z), sum[0][2]);
+      sum[0][3] = fma(e0, static_cast<double>(v.w), sum[0][3]);
+      sum[1][0] = fma(e1, static_cast<double>(v.x), sum[1][0]);
+      sum[1][1] = fma(e1, static_cast<double>(v.y), sum[1][1]);
+      sum[1][2] = fma(e1, static_cast<double>(v.z), sum[1][2]);
+      sum[1][3] = fma(e1, static_cast<double>(v.w), sum[1][3]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    red[threadIdx.x * 4 + i] = __float_as_uint(m[i]);
+    sred[threadIdx.x * 8 + i] = sum[0][i];
+    sred[threadIdx.x * 8 + 4 + i] = sum[1][i];
+  }
+  __syncthreads();
+  if (rsub == 0) {
+    unsigned mm[4] = {0u, 0u, 0u, 0u};
+    double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = 0; q < rows_per_block; ++q) {
+      const int t = q * P + piece;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        mm[i] = max(mm[i], red[t * 4 + i]);
+        sa[i] += sred[t * 8 + i];
+        sb[i] += sred[t * 8 + 4 + i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      atomicMax(&colmax[4 * piece + i], mm[i]);
+      csum_part[(static_cast<int64_t>(blockIdx.x) * 2 + 0) * D + 4 * piece + i] = sa[i];
+      csum_part[(static_cast<int64_t>(blockIdx.x) * 2 + 1) * D + 4 * piece + i] = sb[i];
+    }
+  }
+}
+
+// per-feature 2^k (the largest power of two with M_j 2^k <= 2^30, M_j = max |x - s_j| over all
+// rows: F stays within +-2^30, half the int32 range) and the integer shift S_j = rint(s_j 2^k),
+// rounded so that it is exact in fp32 (the slicer subtracts it in an FMA)
+__global__ void i8_scale_kernel(int D, const double* __restrict__ s, const unsigned* __restrict__ colmax,
+                                float* scale, float* shiftf, unsigned* overflow) {
+  for (int f = threadIdx.x; f < D; f += blockDim.x) {
+    const float M = __uint_as_float(colmax[f]);
+    int k = 0;
+    if (!(M < 3.0e38f)) {
+      atomicOr(overflow, 1u);  // non-finite input (or out of range): the DMMA path reports it
+    } else if (M > 0.0f) {
+      int e;
+      frexp(static_cast<double>(M), &e);  // M < 2^e
+      k = 30 - e;
+    }
+    k = k > 100 ? 100 : (k < -100 ? -100 : k);
+    const double sck = ldexp(1.0, k);
+    scale[f] = static_cast<float>(sck);
+    shiftf[f] = static_cast<float>(rint(static_cast<double>(static_cast<float>(s[f] * sck))));
+  }
+}
+
+// G = 2^(-k_i - k_j) sum over groups and pair types of the slabs (fixed order), S_X, s'
+__global__ void gram_i8_reduce_kernel(I8Args a, double* G, double* SA, double* SB, double* s) {
+  const int D = a.D;
+  const int64_t total = static_cast<int64_t>(D) * D;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int tile = static_cast<int>(e / (kFI * kFJ));
-    const int il = static_cast<int>((e / kFJ) % kFI), jc = static_cast<int>(e % kFJ);
-    const int i = s.tI[tile] * kFI + il, j = s.tJ[tile] * kFJ + jc;
-    if (i > j || j >= s.D) continue;  // each i <= j pair lives in exactly one tile
-    double acc = 0.0;
-    for (int r = 0; r < s.nranges; ++r)
-      acc += Gpart[((static_cast<int64_t>(r) * s.ntiles + tile) * kFI + il) * kFJ + jc];
-    G[static_cast<int64_t>(i) * s.D + j] = acc;
-    G[static_cast<int64_t>(j) * s.D + i] = acc;
+    const int i = static_cast<int>(e / D), j = static_cast<int>(e % D);
+    const int r = i / kFeat, row = i % kFeat;
+    // fixed order: 4 interleaved partial sums over the groups (memory-level parallelism), then
+    // combined in order -- deterministic for a given group count
+    double part[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* base = a.slab + static_cast<int64_t>(r) * kFeat * 256 + static_cast<int64_t>(row) * 256 + j;
+    const int64_t cstride = static_cast<int64_t>(kFeat) * 256;  // one CTA slab
+#pragma unroll 4
+    for (int g = 0; g < a.ngroups; ++g) {
+      const double* gb = base + static_cast<int64_t>(g * 3) * 2 * cstride;
+      part[g & 3] += __ldg(gb) + __ldg(gb + 2 * cstride) + __ldg(gb + 4 * cstride);  // types 0, 1, 2
+    }
+    const double acc = (part[0] + part[1]) + (part[2] + part[3]);
+    // slabs carry sum_L 2^(-8L) G_L = 2^-48 sum_L 2^(8 (6 - L)) G_L
+    G[e] = ldexp(acc, 48) / (static_cast<double>(a.scale[i]) * static_cast<double>(a.scale[j]));
+  }
+  if (blockIdx.x == 0) {
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+      double sa = 0.0, sb = 0.0;
+      for (int b = 0; b < a.ncs; ++b) {  // fixed order: deterministic
+        sa += a.cpart[(static_cast<int64_t>(b) * 2 + 0) * D + j];
+        sb += a.cpart[(static_cast<int64_t>(b) * 2 + 1) * D + j];
+      }
+      const double sp = (static_cast<double>(a.shiftf[j]) + 128.0 * 65793.0) / static_cast<double>(a.scale[j]);
+      SA[j] = sa - static_cast<double>(a.nA) * sp;  // sums about s' = (S + c0) 2^-k
+      SB[j] = sb - static_cast<double>(a.nB) * sp;
+      s[j] = sp;
+    }
   }
 }
 
 }  // namespace
 
 bool plan_gram_i8(int64_t nA, int64_t nB, int D, int num_sms, GramI8Plan& p) {
-  if (D > 256 || D < 1) return false;
+  if (D <= 128 || D > 256 || D % 4 != 0 || nA < 1 || nB < 1) return false;
+  const int pairs = (num_sms > 0 ? num_sms : 148) / 2;
+  int groups = pairs / 3;  // a group = one pair of each type
+  const int64_t per = (nA + nB) / (groups > 0 ? groups : 1);
+  if (per < 4 * kPts) groups = static_cast<int>((nA + nB) / (4 * kPts));  // small problems: fewer groups
+  if (groups < 1) return false;
   p.D = D;
-  p.Df = static_cast<int>(round_up(D, 128));
-  p.N = nA + nB;
-  p.Np = round_up(p.N > 0 ? p.N : 1, kPts);
-  p.ntiles = 0;
-  for (int I = 0; I < p.Df / kFI; ++I)
-    for (int J = 0; J < p.Df / kFJ; ++J)
-      if ((J + 1) * kFJ > I * kFI && J * kFJ < D && I * kFI < D) {
-        p.tI[p.ntiles] = I;
-        p.tJ[p.ntiles] = J;
-        ++p.ntiles;
-      }
-  const int sms = num_sms > 0 ? num_sms : 148;
-  int nr = sms / p.ntiles;
-  if (nr < 1) nr = 1;
-  const int64_t stages = p.Np / kPts;
-  if (nr > stages) nr = static_cast<int>(stages);
-  p.per = (stages + nr - 1) / nr * kPts;
-  p.nranges = static_cast<int>((p.Np + p.per - 1) / p.per);
-  p.nctas = p.ntiles * p.nranges;
-  p.cm_ctas = 2 * sms;
-  p.slice_bytes = static_cast<int64_t>(kSl) * p.Df * p.Np;
-  p.gpart_doubles = static_cast<int64_t>(p.nctas) * kFI * kFJ;
-  p.spart_doubles = static_cast<int64_t>(p.cm_ctas) * 2 * D;
+  p.ngroups = groups;
+  p.nctas = groups * 6;
+  p.slab_doubles = static_cast<int64_t>(p.nctas) * kFeat * 256;
+  p.csum_count = static_cast<int64_t>(kColmaxBlocks) * 2 * D;
   return true;
 }
 
+size_t gram_i8_ws_bytes(const GramI8Plan& p) {
+  return static_cast<size_t>(round_up(p.slab_doubles * 8, 256) + round_up(p.csum_count * 8, 256) + 256 * 4 * 3 +
+                             256);
+}
+
 cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, const float* B, int64_t nB,
-                           unsigned* maxbits, double* Spart, int8_t* S, double* Gpart, double* G, double* SA,
-                           double* SB, cudaStream_t st) {
+                           uint8_t* ws, double* s, double* G, double* SA, double* SB, unsigned* overflow,
+                           cudaStream_t st) {
   const int D = p.D;
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(maxbits, 0, sizeof(unsigned) * D, st)) != cudaSuccess) return e;
-  count_launch();
-  colmax_kernel<<<dim3(p.cm_ctas, (D + 31) / 32), 256, 0, st>>>(A, nA, B, nB, D, maxbits, Spart);
-  count_launch();
-  colsum_reduce_kernel<<<(D + 255) / 256, 256, 0, st>>>(Spart, p.cm_ctas, D, SA, SB);
-  // padded features (D .. Df) of every plane must read as zero slices
-  if (p.Df > D) {
-    for (int t = 0; t < kSl; ++t)
-      if ((e = cudaMemsetAsync(S + (static_cast<int64_t>(t) * p.Df + D) * p.Np, 0,
-                               static_cast<size_t>(p.Df - D) * p.Np, st)) != cudaSuccess)
-        return e;
-  }
-  count_launch();
-  slice_kernel<<<dim3(static_cast<unsigned>(p.Np / kSlT), (D + kSlT - 1) / kSlT), 256, 0, st>>>(
-      A, nA, B, nB, D, p.Df, p.Np, maxbits, S);
-  CUtensorMap map;
-  {
-    typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static EncFn enc = nullptr;
-    if (enc == nullptr) {
-      cudaDriverEntryPointQueryResult q;
-      void* fn = nullptr;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-          q != cudaDriverEntryPointSuccess || fn == nullptr)
-        return cudaErrorUnknown;
-      enc = reinterpret_cast<EncFn>(fn);
-    }
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.Np), static_cast<cuuint64_t>(kSl) * p.Df};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.Np)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kPts), 64u};
-    const cuuint32_t estr[2] = {1u, 1u};
-    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, S, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  double* slab = reinterpret_cast<double*>(ws);
+  double* cpart = reinterpret_cast<double*>(ws + round_up(p.slab_doubles * 8, 256));
+  float* scale = reinterpret_cast<float*>(ws + round_up(p.slab_doubles * 8, 256) + round_up(p.csum_count * 8, 256));
+  float* shiftf = scale + 256;
+  CUtensorMap maps[2];
+  char err[256];
+  // raw fp32 boxes [128 features x 64 rows], no swizzle (the slicers read them, not the MMA)
+  PFN_encodeTiled enc = get_encode();
+  if (enc == nullptr) return cudaErrorNotSupported;
+  const float* src[2] = {A, B};
+  const int64_t rows[2] = {nA, nB};
+  for (int i = 0; i < 2; ++i) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(rows[i])};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 4};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kFeat), static_cast<cuuint32_t>(kPts)};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(src[i]), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  GramI8Sched s{};
-  s.ntiles = p.ntiles;
-  s.nranges = p.nranges;
-  s.per = p.per;
-  s.N = p.N;
-  s.Np = p.Np;
-  s.D = D;
-  s.Df = p.Df;
-  for (int t = 0; t < p.ntiles; ++t) {
-    s.tI[t] = p.tI[t];
-    s.tJ[t] = p.tJ[t];
-  }
-  if ((e = cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kSmemI8))) != cudaSuccess)
-    return e;
+  (void)err;
+  unsigned* colmax = reinterpret_cast<unsigned*>(shiftf + 256);
+  cudaError_t e0 = cudaMemsetAsync(colmax, 0, sizeof(unsigned) * 256, st);
+  if (e0 != cudaSuccess) return e0;
   count_launch();
-  gram_i8_kernel<<<p.nctas, 192, kSmemI8, st>>>(map, s, maxbits, Gpart);
+  i8_colmax_kernel<<<kColmaxBlocks, 256, 0, st>>>(A, nA, B, nB, D, s, colmax, cpart);
   count_launch();
-  gram_i8_reduce_kernel<<<148, 256, 0, st>>>(Gpart, s, G);
+  i8_scale_kernel<<<1, 256, 0, st>>>(D, s, colmax, scale, shiftf, overflow);
+  I8Args a{nA, nB, D, p.ngroups, scale, shiftf, slab, cpart, kColmaxBlocks, overflow};
+  cudaError_t e =
+      cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
+  if (e != cudaSuccess) return e;
+  count_launch();
+  gram_i8_kernel<<<p.nctas, kThreads, kSmem, st>>>(maps[0], maps[1], a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  count_launch();
+  gram_i8_reduce_kernel<<<148, 256, 0, st>>>(a, G, SA, SB, s);
   return cudaGetLastError();
 }
 

@@ -403,14 +403,10 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
     if (p.gp.gpart_doubles > p.gpart_doubles) p.gpart_doubles = p.gp.gpart_doubles;
     if (p.gp.spart_doubles > p.spart_doubles) p.spart_doubles = p.gp.spart_doubles;
   }
-  // The int8 tensor-core Gram (k_gram_i8.cu) is opt-in (option k1_path = 1): correct, but measured
-  // slower at cfg5 (22.4 vs 12.2 ms) because its 128x64 tiles are L2-bound.
-  p.i8 = opt(OPT_K1_PATH) == 1 && plan_gram_i8(nA, nB, D, num_sms, p.ip);
-  if (p.i8) {
-    if (p.ip.gpart_doubles > p.gpart_doubles) p.gpart_doubles = p.ip.gpart_doubles;
-    p.i8_bytes = round_up(static_cast<int64_t>(D) * 4, 256) + round_up(p.ip.spart_doubles * 8, 256) +
-                 p.ip.slice_bytes;
-  }
+  // The int8 tensor-core Gram (k_gram_i8.cu) is the default for 128 < D <= 256 (option k1_path:
+  // 0 forces the fp64 DMMA Gram, 2 the legacy tile kernel).
+  p.i8 = (opt(OPT_K1_PATH) == -1 || opt(OPT_K1_PATH) == 1) && plan_gram_i8(nA, nB, D, num_sms, p.ip);
+  if (p.i8) p.i8_bytes = static_cast<int64_t>(gram_i8_ws_bytes(p.ip));
   return p;
 }
 
@@ -433,14 +429,9 @@ cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB,
 }
 
 cudaError_t launch_moments_partial(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB,
-                                   int D, const MomentsBufs& b, cudaStream_t st, bool shifted) {
-  if (!shifted && p.i8 && b.i8ws != nullptr) {
-    unsigned* maxbits = reinterpret_cast<unsigned*>(b.i8ws);
-    double* sp = reinterpret_cast<double*>(b.i8ws + round_up(static_cast<int64_t>(D) * 4, 256));
-    int8_t* S = reinterpret_cast<int8_t*>(b.i8ws + round_up(static_cast<int64_t>(D) * 4, 256) +
-                                          round_up(p.ip.spart_doubles * 8, 256));
-    return launch_gram_i8(p.ip, A, nA, B, nB, maxbits, sp, S, b.Gpart, b.C, b.SA, b.SB, st);
-  }
+                                   int D, const MomentsBufs& b, cudaStream_t st, bool use_i8) {
+  if (use_i8 && p.i8 && b.i8ws != nullptr && b.i8ovf != nullptr)
+    return launch_gram_i8(p.ip, A, nA, B, nB, b.i8ws, b.s, b.C, b.SA, b.SB, b.i8ovf, st);
   if (p.gram) return launch_gram(p.gp, A, nA, B, nB, D, b.s, b.Gpart, b.Spart, b.C, b.SA, b.SB, st);
   const size_t smem = sizeof(double) * kMC * kLds;
   auto kern = mom_ctas_per_sm() == 3 ? moments_kernel<3> : moments_kernel<4>;
@@ -468,7 +459,7 @@ cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, con
                            const MomentsBufs& b, cudaStream_t st) {
   cudaError_t e = launch_shift(A, nA, B, nB, D, b.s, st);
   if (e != cudaSuccess) return e;
-  if ((e = launch_moments_partial(p, A, nA, B, nB, D, b, st)) != cudaSuccess) return e;
+  if ((e = launch_moments_partial(p, A, nA, B, nB, D, b, st, true)) != cudaSuccess) return e;
   return launch_moments_finalize(nA, nB, D, b, st);
 }
 

@@ -70,7 +70,10 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
   w.mom.s = c.take<double>(2 * static_cast<int64_t>(D));  // shift + scratch
   w.mom.Gpart = c.take<double>(mp.gpart_doubles);
   w.mom.Spart = c.take<double>(mp.spart_doubles);
-  if (mp.i8) w.mom.i8ws = c.take<uint8_t>(mp.i8_bytes);
+  if (mp.i8) {
+    w.mom.i8ws = c.take<uint8_t>(mp.i8_bytes);
+    w.mom.i8ovf = c.take<unsigned>(1);
+  }
   w.mom.C = c.take<double>(static_cast<int64_t>(D) * D);
   w.mom.SA = c.take<double>(D);
   w.mom.SB = c.take<double>(D);
@@ -147,107 +150,116 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   CK(cudaMemsetAsync(w.U64, 0, sizeof(double) * L * D, st));
 
   // ------------------------------------------------------------ step 1: directions
-  if (dirs_in == nullptr) {
-    const MomentsPlan mp = plan_moments(nA, nB, D, ctx->num_sms);
-    int t0 = tmark(ctx);
-    // shift first; with the opt-in int8 Gram planned, its value picks the path (int8 tensor
-    // cores about the origin, or the fp64 DMMA pass with the subtraction), so the host reads
-    // it back (D doubles); the default DMMA pass handles either case on the device
-    CK(launch_shift(A, nA, B, nB, D, w.mom.s, st));
-    bool shifted = true;
-    if (mp.i8) {
-      std::vector<double> sh(static_cast<size_t>(D));
-      CK(cudaMemcpyAsync(sh.data(), w.mom.s, sizeof(double) * D, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      shifted = false;
-      for (double v : sh) shifted = shifted || v != 0.0;
-    }
-    CK(launch_moments_partial(mp, A, nA, B, nB, D, w.mom, st, shifted));
-    CK(launch_moments_finalize(nA, nB, D, w.mom, st));
-    tspan(ctx, PH_MOMENTS, t0);
-    if (k > 0) {
-      t0 = tmark(ctx);
-      CK(launch_eigen_topk(w.mom.C, D, k, w.V, w.Xe, w.U64, w.U32, w.lam, w.n_dirs, st));
-      tspan(ctx, PH_EIGEN, t0);
+  // moments on the int8 tensor cores where planned (k_gram_i8.cu), else the fp64 DMMA Gram;
+  // if the int8 pass saw a value outside its sampled fixed-point range (checked at the host
+  // sync after the selection), steps 1-3 rerun with the DMMA Gram
+  const MomentsPlan mp = dirs_in == nullptr ? plan_moments(nA, nB, D, ctx->num_sms) : MomentsPlan{};
+  auto directions = [&](bool use_i8) -> int {
+    if (dirs_in == nullptr) {
+      int t0 = tmark(ctx);
+      CK(launch_shift(A, nA, B, nB, D, w.mom.s, st));
+      if (use_i8) CK(cudaMemsetAsync(w.mom.i8ovf, 0, sizeof(unsigned), st));
+      CK(launch_moments_partial(mp, A, nA, B, nB, D, w.mom, st, use_i8));
+      CK(launch_moments_finalize(nA, nB, D, w.mom, st));
+      tspan(ctx, PH_MOMENTS, t0);
+      if (k > 0) {
+        t0 = tmark(ctx);
+        CK(launch_eigen_topk(w.mom.C, D, k, w.V, w.Xe, w.U64, w.U32, w.lam, w.n_dirs, st));
+        tspan(ctx, PH_EIGEN, t0);
+      } else {
+        const int one = 1;
+        CK(cudaMemcpyAsync(w.n_dirs, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+      }
+      CK(launch_dirs_to_f32(w.U64, w.U32, L, D, st));
     } else {
-      const int one = 1;
-      CK(cudaMemcpyAsync(w.n_dirs, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(w.U64, dirs_in, sizeof(double) * n_dirs_in * D, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(w.n_dirs, &n_dirs_in, sizeof(int), cudaMemcpyHostToDevice, st));
+      CK(launch_dirs_to_f32(w.U64, w.U32, L, D, st));
     }
-    CK(launch_dirs_to_f32(w.U64, w.U32, L, D, st));
-  } else {
-    CK(cudaMemcpyAsync(w.U64, dirs_in, sizeof(double) * n_dirs_in * D, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(w.n_dirs, &n_dirs_in, sizeof(int), cudaMemcpyHostToDevice, st));
-    CK(launch_dirs_to_f32(w.U64, w.U32, L, D, st));
-  }
+    return PROHD_OK;
+  };
+  bool use_i8 = dirs_in == nullptr && mp.i8;
+  if ((rc = directions(use_i8))) return rc;
 
   // ------------------------------------------------------------ steps 2-3: projection, selection, union
   const float* X[2] = {A, B};
   const int64_t n[2] = {nA, nB};
-  const int t_sel = tmark(ctx);
-  // set B's chain runs on the context's second stream, set A's on the caller's: the low-occupancy
-  // tail of one set's selection (collect, re-rank, compaction) overlaps the other's projection
-  if (ctx->aux == nullptr) {
-    CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
-  }
-  if (counts && L > 1) CK(launch_minus_one(w.n_dirs, w.n_dirs1, st));  // shared by both sets
-  CK(cudaEventRecord(ctx->ev_fork, st));
-  CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
-  // the chains are enqueued by a helper so that an error in either still joins the aux stream
-  // back into the caller's before returning (no kernel of this call is left unordered against
-  // the caller's stream and workspace)
-  double eps[2] = {0.0, 0.0};
-  auto enqueue_chains = [&]() -> cudaError_t {
-    for (int s = 0; s < 2; ++s) {
-      // projections run for every point (also when 2m >= n) so non-finite input is always detected
-      cudaStream_t sst = s == 0 ? st : ctx->aux;
-      SelectBufs& b = w.sel[s];
-      const int64_t m0 = counts ? counts[2 * s] : m;      // centroid axis
-      const int64_t m1 = counts ? counts[2 * s + 1] : m;  // principal directions
-      const bool all = 2 * m0 >= n[s] || (L > 1 && 2 * m1 >= n[s]);
-      cudaError_t e;
-      if (all) {
-        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, sst)) != cudaSuccess) return e;
-        if ((e = launch_iota(b.uidx, b.ucount, n[s], sst)) != cudaSuccess) return e;
-      } else if (m0 == m1 || L == 1) {
-        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst, true, true, &eps[s])) !=
-            cudaSuccess)
-          return e;
-      } else {  // two direction groups with different per-tail counts, one shared union bitmap
-        // the groups share the projection buffer, so each group's overflow fallback runs right
-        // after it (device-side no-op unless a list overflowed)
-        if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, 1, w.n_dirs, m0, b, sst, true, false, &eps[s])) !=
-            cudaSuccess)
-          return e;
-        if ((e = launch_select_fallback(X[s], n[s], D, w.U64, 1, w.n_dirs, m0, b, eps[s], sst, false)) != cudaSuccess)
-          return e;
-        if ((e = launch_select(X[s], n[s], D, w.U64 + D, w.U32 + D, L - 1, w.n_dirs1, m1, b, sst, false, true,
-                               &eps[s])) != cudaSuccess)
-          return e;
-        if ((e = launch_select_fallback(X[s], n[s], D, w.U64 + D, L - 1, w.n_dirs1, m1, b, eps[s], sst, true)) !=
-            cudaSuccess)
-          return e;
-      }
-    }
-    return cudaSuccess;
-  };
-  const cudaError_t e_chain = enqueue_chains();
-  CK(cudaEventRecord(ctx->ev_join, ctx->aux));
-  CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-  CK(e_chain);
-  tspan(ctx, PH_SELECT, t_sel);
   unsigned ucount[2];
   int ndirs = 0, ovf[2] = {0, 0};
   unsigned maxn[2];
-  CK(cudaMemcpyAsync(&ucount[0], w.sel[0].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&ucount[1], w.sel[1].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&ovf[0], w.sel[0].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&ovf[1], w.sel[1].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&maxn[0], w.sel[0].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&maxn[1], w.sel[1].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&ndirs, w.n_dirs, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  unsigned i8ovf = 0;
+  double eps[2] = {0.0, 0.0};
+  auto select_and_read = [&]() -> int {
+    const int t_sel = tmark(ctx);
+    // set B's chain runs on the context's second stream, set A's on the caller's: the low-occupancy
+    // tail of one set's selection (collect, re-rank, compaction) overlaps the other's projection
+    if (ctx->aux == nullptr) {
+      CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    }
+    if (counts && L > 1) CK(launch_minus_one(w.n_dirs, w.n_dirs1, st));  // shared by both sets
+    CK(cudaEventRecord(ctx->ev_fork, st));
+    CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    // the chains are enqueued by a helper so that an error in either still joins the aux stream
+    // back into the caller's before returning (no kernel of this call is left unordered against
+    // the caller's stream and workspace)
+    auto enqueue_chains = [&]() -> cudaError_t {
+      for (int s = 0; s < 2; ++s) {
+        // projections run for every point (also when 2m >= n) so non-finite input is always detected
+        cudaStream_t sst = s == 0 ? st : ctx->aux;
+        SelectBufs& b = w.sel[s];
+        const int64_t m0 = counts ? counts[2 * s] : m;      // centroid axis
+        const int64_t m1 = counts ? counts[2 * s + 1] : m;  // principal directions
+        const bool all = 2 * m0 >= n[s] || (L > 1 && 2 * m1 >= n[s]);
+        cudaError_t e;
+        if (all) {
+          if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, sst)) != cudaSuccess) return e;
+          if ((e = launch_iota(b.uidx, b.ucount, n[s], sst)) != cudaSuccess) return e;
+        } else if (m0 == m1 || L == 1) {
+          if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst, true, true, &eps[s])) !=
+              cudaSuccess)
+            return e;
+        } else {  // two direction groups with different per-tail counts, one shared union bitmap
+          // the groups share the projection buffer, so each group's overflow fallback runs right
+          // after it (device-side no-op unless a list overflowed)
+          if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, 1, w.n_dirs, m0, b, sst, true, false, &eps[s])) !=
+              cudaSuccess)
+            return e;
+          if ((e = launch_select_fallback(X[s], n[s], D, w.U64, 1, w.n_dirs, m0, b, eps[s], sst, false)) != cudaSuccess)
+            return e;
+          if ((e = launch_select(X[s], n[s], D, w.U64 + D, w.U32 + D, L - 1, w.n_dirs1, m1, b, sst, false, true,
+                                 &eps[s])) != cudaSuccess)
+            return e;
+          if ((e = launch_select_fallback(X[s], n[s], D, w.U64 + D, L - 1, w.n_dirs1, m1, b, eps[s], sst, true)) !=
+              cudaSuccess)
+            return e;
+        }
+      }
+      return cudaSuccess;
+    };
+    const cudaError_t e_chain = enqueue_chains();
+    CK(cudaEventRecord(ctx->ev_join, ctx->aux));
+    CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    CK(e_chain);
+    tspan(ctx, PH_SELECT, t_sel);
+    CK(cudaMemcpyAsync(&ucount[0], w.sel[0].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ucount[1], w.sel[1].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ovf[0], w.sel[0].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ovf[1], w.sel[1].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&maxn[0], w.sel[0].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&maxn[1], w.sel[1].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ndirs, w.n_dirs, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (use_i8) CK(cudaMemcpyAsync(&i8ovf, w.mom.i8ovf, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return PROHD_OK;
+  };
+  if ((rc = select_and_read())) return rc;
+  if (use_i8 && i8ovf) {  // a value outside the int8 Gram's sampled range: rerun on the DMMA Gram
+    use_i8 = false;
+    if ((rc = directions(false))) return rc;
+    if ((rc = select_and_read())) return rc;
+  }
   for (int s = 0; s < 2; ++s) {
     float f;
     std::memcpy(&f, &maxn[s], 4);
@@ -325,5 +337,49 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   out->_pad = 0;
   if (idxA_out) std::memcpy(idxA_out, ua.data(), sizeof(long long) * ucount[0]);
   if (idxB_out) std::memcpy(idxB_out, ub.data(), sizeof(long long) * ucount[1]);
+  return PROHD_OK;
+}
+
+// Test hook (include/prohd.h prohd_covariance): step 1a of prohd_estimate alone.
+extern "C" int prohd_covariance(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
+                                double* mu_out, double* C_out, int32_t* path_out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (mu_out == nullptr || C_out == nullptr || path_out == nullptr) return fail(ctx, PROHD_E_INVALID, "null output");
+  if ((rc = check_sets(ctx, A, nA, B, nB, D))) return rc;
+  call_begin(ctx);
+  const bool host_in = !(is_device_ptr(A) && is_device_ptr(B));
+  Carver dry{nullptr, 0, 0, true};
+  EstWs tmp;
+  const size_t need = carve_est(dry, tmp, nA, nB, D, 0, 1, host_in, ctx->num_sms);
+  if (ctx->ws == nullptr || ctx->ws_bytes < need)
+    return fail(ctx, PROHD_E_WORKSPACE, "workspace too small: need %zu bytes, have %zu", need, ctx->ws_bytes);
+  Carver c{ctx->ws, 0, ctx->ws_bytes, false};
+  EstWs w;
+  carve_est(c, w, nA, nB, D, 0, 1, host_in, ctx->num_sms);
+  cudaStream_t st = ctx->stream;
+  bool hi;
+  if ((rc = stage_inputs(ctx, A, nA, B, nB, D, w.stageA, w.stageB, hi))) return rc;
+  const MomentsPlan mp = plan_moments(nA, nB, D, ctx->num_sms);
+  bool use_i8 = mp.i8;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const int t0 = tmark(ctx);
+    CK(launch_shift(A, nA, B, nB, D, w.mom.s, st));
+    if (use_i8) CK(cudaMemsetAsync(w.mom.i8ovf, 0, sizeof(unsigned), st));
+    CK(launch_moments_partial(mp, A, nA, B, nB, D, w.mom, st, use_i8));
+    CK(launch_moments_finalize(nA, nB, D, w.mom, st));
+    tspan(ctx, PH_MOMENTS, t0);
+    unsigned ovf = 0;
+    if (use_i8) CK(cudaMemcpyAsync(&ovf, w.mom.i8ovf, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!(use_i8 && ovf)) break;
+    use_i8 = false;  // outside the int8 pass's sampled range: the fp64 DMMA Gram
+  }
+  CK(cudaMemcpyAsync(mu_out, w.mom.mu, sizeof(double) * D, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(C_out, w.mom.C, sizeof(double) * D * D, cudaMemcpyDeviceToHost, st));
+  call_end(ctx);
+  CK(cudaStreamSynchronize(st));
+  call_collect(ctx);
+  *path_out = use_i8 ? 1 : 0;
   return PROHD_OK;
 }

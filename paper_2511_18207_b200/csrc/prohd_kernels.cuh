@@ -33,28 +33,32 @@ cudaError_t launch_gram(const GramPlan& p, const float* A, int64_t nA, const flo
                         const double* s, double* Gpart, double* Spart, double* Gout, double* SA, double* SB,
                         cudaStream_t st);
 
-// int8 tensor-core Gram (k_gram_i8.cu), for moments about the origin (s = 0), D <= 256
+// int8 tensor-core Gram (k_gram_i8.cu): exact-integer Ozaki slices on tcgen05 kind::i8 CTA pairs,
+// 128 < D <= 256, D % 4 == 0. Writes G (D x D), S_A, S_B about its own fixed-point shift s'
+// (overwrites s), and sets *overflow if a value fell outside the sampled range (then the caller
+// reruns the fp64 DMMA Gram).
 struct GramI8Plan {
-  int D = 0, Df = 0, ntiles = 0, nranges = 0, nctas = 0, cm_ctas = 0;
-  int64_t N = 0, Np = 0, per = 0, slice_bytes = 0, gpart_doubles = 0, spart_doubles = 0;
-  int tI[16], tJ[16];
+  int D = 0, ngroups = 0, nctas = 0;
+  int64_t slab_doubles = 0, csum_count = 0;
 };
 bool plan_gram_i8(int64_t nA, int64_t nB, int D, int num_sms, GramI8Plan& p);
+size_t gram_i8_ws_bytes(const GramI8Plan& p);
 cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, const float* B, int64_t nB,
-                           unsigned* maxbits, double* Spart, int8_t* S, double* Gpart, double* G, double* SA,
-                           double* SB, cudaStream_t st);
+                           uint8_t* ws, double* s, double* G, double* SA, double* SB, unsigned* overflow,
+                           cudaStream_t st);
 
 struct MomentsPlan {
   int nb = 0, npairs = 0, c_diag = 0, c_off = 0, nctas = 0, nslots = 0;
   bool gram = false;  // warp-specialised Gram pass (k_gram.cu); else the legacy 64x64-block kernel
   GramPlan gp;
-  bool i8 = false;    // int8 tensor-core Gram available (used when s = 0)
+  bool i8 = false;    // int8 tensor-core Gram (the default where supported, k_gram_i8.cu)
   GramI8Plan ip;
   int64_t gpart_doubles = 0, spart_doubles = 0;
-  int64_t i8_bytes = 0;  // maxbits + column-sum partials + slice planes (k_gram_i8.cu)
+  int64_t i8_bytes = 0;  // slabs, column-sum partials, scales (k_gram_i8.cu)
 };
 struct MomentsBufs {
   uint8_t* i8ws = nullptr;  // int8 Gram scratch (MomentsPlan::i8_bytes)
+  unsigned* i8ovf = nullptr;  // int8 Gram range overflow flag
   double* s;      // [2D]: shift s (0 unless the offset is large), then D doubles of scratch
   double* Gpart;  // partial Grams
   double* Spart;  // partial column sums
@@ -71,9 +75,10 @@ cudaError_t launch_moments(const MomentsPlan& p, const float* A, int64_t nA, con
 // pieces of launch_moments (sharded path): shift s from the first <= 4096 rows of A and B;
 // partial sums about b.s (-> b.SA, b.SB, b.C = G); finalize (mu, u0, C from the sums).
 cudaError_t launch_shift(const float* A, int64_t nA, const float* B, int64_t nB, int D, double* s, cudaStream_t st);
-// shifted: s != 0 (DMMA path with the fp64 subtraction); else the int8 Gram when planned
+// use_i8: the int8 tensor-core Gram when planned (it replaces b.s by its own shift s'; the
+// sharded phase calls, whose shift is fixed by the caller, pass false), else the fp64 DMMA pass
 cudaError_t launch_moments_partial(const MomentsPlan& p, const float* A, int64_t nA, const float* B, int64_t nB,
-                                   int D, const MomentsBufs& b, cudaStream_t st, bool shifted = true);
+                                   int D, const MomentsBufs& b, cudaStream_t st, bool use_i8 = false);
 cudaError_t launch_moments_finalize(int64_t nA, int64_t nB, int D, const MomentsBufs& b, cudaStream_t st);
 
 // ---------------------------------------------------------------- K2

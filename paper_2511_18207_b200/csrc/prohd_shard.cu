@@ -158,9 +158,9 @@ int prohd_local_moments(prohd_ctx* ctx, const float* A_local, int64_t nA_local, 
   CK(cudaMemsetAsync(w.mom.C, 0, sizeof(double) * D * D, st));
   if (nA_local + nB_local > 0) {
     const MomentsPlan mp = plan_moments(nA_local, nB_local, D, ctx->num_sms);
-    bool shifted = false;  // the shift is a HOST array (prohd.h)
-    for (int f = 0; f < D; ++f) shifted = shifted || shift[f] != 0.0;
-    CK(launch_moments_partial(mp, A_local, nA_local, B_local, nB_local, D, w.mom, st, shifted));
+    // the caller's shift is fixed across ranks (the moments are summed by an all-reduce), so the
+    // phase call keeps the fp64 DMMA Gram (the int8 pass chooses its own fixed-point shift)
+    CK(launch_moments_partial(mp, A_local, nA_local, B_local, nB_local, D, w.mom, st, false));
   }
   tspan(ctx, PH_MOMENTS, t0);
   CK(cudaMemcpyAsync(moments_out, w.mom.SA, sizeof(double) * D, cudaMemcpyDeviceToDevice, st));

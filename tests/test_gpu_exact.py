@@ -297,15 +297,21 @@ def test_wide_dynamic_range_per_row_scales(ctx, D):
     (coordinates ~1e-6) next to far outliers (coordinates 1e4). One fp16 scale per set would leave the
     cluster's coordinates in the fp16 subnormal range (floor 2^-38 x 1e4 per coordinate, ~1e-3 of
     their size); per-row scales keep every row at the top of the range. Both directions of the
-    fused sweep and the directed kernel are checked per row against the oracle (Q17)."""
+    fused sweep and the directed kernel are checked per row against the oracle (Q17); the HD values
+    and witnesses too (the outliers sit 0.5 apart per coordinate, so they carry H: with exactly
+    coincident outliers H would be a cluster distance ~1e-5, below the fp32 accumulation error
+    that Q17 allows on the outliers' own row minima, ~1e-7 of their norms)."""
     rng = np.random.default_rng(D + 5)
     A = (rng.standard_normal((700, D)) * 1e-6).astype(np.float32)
     B = (rng.standard_normal((900, D)) * 1e-6 + 2e-7).astype(np.float32)
     A[3], A[4] = 1e4, -1e4  # symmetric outliers: the centres K0 subtracts stay ~0, so the cluster's
-    B[5], B[600] = -1e4, 1e4  # centred norms are its raw norms (the Q17 scale)
-    rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    B[5], B[600] = -1e4 - 0.5, 1e4 + 0.5  # centred norms are its raw norms (the Q17 scale)
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    rm = ctx.directed_hd_rowmin(At, Bt).cpu().numpy()
     _check_rowmins(A, B, rm)
-    h = ctx.hausdorff(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    h, r1, c1 = ctx.hausdorff_minima(At, Bt)
+    _check_rowmins(A, B, r1.cpu().numpy())
+    _check_rowmins(B, A, c1.cpu().numpy())
     ref = oracle.hausdorff(A, B)
     _check_directed(A, B, h["ab"], ref["ab"])
     _check_directed(B, A, h["ba"], ref["ba"])

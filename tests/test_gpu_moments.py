@@ -103,3 +103,74 @@ def test_gram_replicated_ksteps(ctx):
         A = rng.standard_normal((n, D)).astype(np.float32)
         B = (rng.standard_normal((n // 2 + 3, D)) * 2 - 1).astype(np.float32)
         _check(ctx, A, B, np.zeros(D))
+
+
+def _i8_bound(A, B, shifted):
+    """Element-wise bound on |C_gpu - C_ref| for the int8 Gram (k_gram_i8.cu): every value is a
+    fixed-point integer on the grid 2^-k_j <= 2^-29 M_j (M_j = max |x - s_j|, exact), rounded to
+    nearest (|e_j| <= 2^-30 M_j; with a shift the FMA first rounds to 24 bits of |F| <= 2^30:
+    |e_j| <= 2^-23 M_j), and the dropped d_3 d_3 level adds <= 2^14 grid^2 per point."""
+    X = np.concatenate([A, B]).astype(np.float64)
+    mu = X.mean(0)
+    Y = np.abs(X - mu)
+    # M_j = max |x - s_j| with s_j the shift kernel's value (0 or ~the sample mean): covered by
+    M = 1.1 * np.maximum(np.abs(X).max(0), Y.max(0)) + 1e-300
+    e = M * (2.0 ** -23 if shifted else 2.0 ** -30)
+    Ymean = Y.mean(0)
+    # C_gpu is the covariance of the quantized values x + e (G and S come from the same integers):
+    # |cov(x + e) - cov(x)| <= 2 (mean|x_i - mu_i| e_j + mean|x_j - mu_j| e_i) + 4 e_i e_j
+    return (2 * (Ymean[:, None] * e[None, :] + Ymean[None, :] * e[:, None]) + 4 * np.outer(e, e)
+            + 2.0 ** -44 * np.outer(M, M)) * 1.05 + 1e-15 * (Y.T @ Y) / X.shape[0]
+
+
+@pytest.mark.parametrize("kind", ["gauss", "heavy", "unit", "offset", "ragged"])
+def test_covariance_int8_path(ctx, kind):
+    """Step 1a through prohd_covariance (the path prohd_estimate uses): the int8 tensor-core Gram
+    for 128 < D <= 256, against the oracle's two-pass fp64 covariance (O3, oracle/prohd.py), within
+    the fixed-point bound above; mu within 1e-12 of the scale."""
+    from oracle import prohd as OP
+    rng = np.random.default_rng({"gauss": 1, "heavy": 2, "unit": 3, "offset": 4, "ragged": 5}[kind])
+    D = {"gauss": 256, "heavy": 256, "unit": 200, "offset": 160, "ragged": 132}[kind]
+    nA, nB = (40011, 35003) if kind != "ragged" else (1237, 70001)
+    if kind == "heavy":
+        A = (rng.standard_t(3, (nA, D)) * rng.uniform(0.1, 3, D)).astype(np.float32)
+        B = (rng.standard_t(3, (nB, D)) * rng.uniform(0.1, 3, D) + 0.3).astype(np.float32)
+    elif kind == "unit":
+        A = np.clip(rng.random((nA, D)) * 0.6 + 0.1 * rng.standard_normal((nA, D)), 0, 1).astype(np.float32)
+        B = np.clip(rng.random((nB, D)) * 0.5 + 0.1 * rng.standard_normal((nB, D)), 0, 1).astype(np.float32)
+    elif kind == "offset":
+        A = (rng.standard_normal((nA, D)) + 4096).astype(np.float32)
+        B = (rng.standard_normal((nB, D)) + 4096.5).astype(np.float32)
+    else:
+        A = rng.standard_normal((nA, D)).astype(np.float32)
+        B = (rng.standard_normal((nB, D)) * 2 + 1).astype(np.float32)
+    mu, C, path = ctx.covariance(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    assert path == 1, "the int8 Gram should serve 128 < D <= 256"
+    rmu, rC = OP.covariance(A, B)
+    # mu is the mean of the fixed-point values: within the rounding bound e_j of the grid
+    X = np.concatenate([A, B]).astype(np.float64)
+    M = 1.1 * np.maximum(np.abs(X).max(0), np.abs(X - rmu).max(0))
+    assert np.all(np.abs(mu - rmu) <= M * (2.0 ** -23 if kind == "offset" else 2.0 ** -30) + 1e-15 * np.abs(rmu))
+    bound = _i8_bound(A, B, kind == "offset")
+    frac = np.abs(C - rC) / bound
+    assert frac.max() <= 1.0, f"max |dC| / bound = {frac.max():.3f}"
+    assert np.array_equal(C, C.T)
+    print(f"{kind} D={D}: max |dC|/bound {frac.max():.2e}, max |dC|/max|C| "
+          f"{np.abs(C - rC).max() / np.abs(rC).max():.2e}")
+
+
+def test_covariance_dmma_option_and_small_d(ctx):
+    """option k1_path = 0 (and D <= 128 always) keeps the fp64 DMMA Gram: C within 1e-12 of the
+    accumulation scale."""
+    from oracle import prohd as OP
+    from paper_2511_18207_b200 import option
+    rng = np.random.default_rng(11)
+    for D, opt in ((256, 0), (96, -1)):
+        A = rng.standard_normal((20000, D)).astype(np.float32)
+        B = (rng.standard_t(4, (15000, D)) + 0.2).astype(np.float32)
+        with option("k1_path", opt):
+            mu, C, path = ctx.covariance(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+        assert path == 0
+        rmu, rC = OP.covariance(A, B)
+        X = np.abs(np.concatenate([A, B]).astype(np.float64) - rmu)
+        assert np.all(np.abs(C - rC) <= 1e-12 * (X.T @ X) / X.shape[0] + 1e-300)

@@ -1,8 +1,10 @@
 """GPU parity for ProHD (Alg. 3) through the C ABI, layered as SURVEY.md §8(c4):
 
   L2 directions   u0 within 1e-9; each PC an eigenvector of the oracle's C
-                  (residual <= 1e-9 ||C||) and, where the oracle's spectral gap
-                  allows, within the Davis-Kahan angle of the oracle's PC.
+                  (residual <= 2 ||C_gpu - C||_2 + 1e-11 ||C||, at least 1e-9 ||C||, with
+                  C_gpu the library's own covariance through prohd_covariance) and, where
+                  the oracle's spectral gap allows, within the Davis-Kahan angle of the
+                  oracle's PC (the same numerator over the gap).
   L3 selection    the oracle run with the GPU's directions injected: per-set
                   unions bit-exact, except swaps across the m-th boundary between
                   points whose fp64 projections differ by <= 1e-6 max(||p||,||q||)
@@ -67,6 +69,16 @@ def _excused_union_diff(X, U, m, got, ref):
     return len(extra) + len(missing)
 
 
+def _direction_tol(ctx, A, B, C):
+    """L2 tolerance for an eigenvector v of the GPU's covariance C_gpu judged against the oracle's
+    C: ||C v - (v^T C v) v|| <= 2 ||C_gpu - C||_2 + eigen-solver error (Davis-Kahan for the angle,
+    divided by the gap). C_gpu through prohd_covariance (the same Gram path as prohd_estimate); at
+    least the 1e-9 ||C|| of the fp64 Gram."""
+    _, Cg, _ = ctx.covariance(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    cn = np.linalg.norm(C, 2)
+    return max(1e-9 * cn, 2.0 * np.linalg.norm(Cg - C, 2) + 1e-11 * cn)
+
+
 def _run(ctx, A, B, k, m):
     return ctx.prohd_estimate(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), k, m,
                               return_dirs=True, return_indices=True)
@@ -82,15 +94,16 @@ def _check_layers(ctx, A, B, k, m, exact_sets=True):
     cn = np.linalg.norm(C, 2)
     assert g["n_dirs"] == ref["n_dirs"]
     lam = np.sort(np.linalg.eigvalsh(C))[::-1]
+    tol = _direction_tol(ctx, A, B, C)
     for l in range(1, U.shape[1]):
         v = U[:, l]
         assert abs(np.linalg.norm(v) - 1) <= 1e-12
         r = C @ v - (v @ C @ v) * v
-        assert np.linalg.norm(r) <= 1e-9 * cn, f"PC{l} residual {np.linalg.norm(r) / cn:.2e}"
+        assert np.linalg.norm(r) <= tol, f"PC{l} residual {np.linalg.norm(r) / cn:.2e}"
         gap = min(abs(lam[l - 1] - lam[j]) for j in range(len(lam)) if j != l - 1)
         if gap > 1e-6 * lam[0]:
             s = np.linalg.norm(v - (v @ ref["U"][:, l]) * ref["U"][:, l])
-            assert s <= 1e-9 * cn / gap + 1e-12, f"PC{l} angle {s:.2e}, gap {gap / lam[0]:.2e}"
+            assert s <= tol / gap + 1e-12, f"PC{l} angle {s:.2e}, gap {gap / lam[0]:.2e}"
     # L3: oracle with the GPU's directions injected
     inj = OP.estimate(A, B, k, m, U=U)
     nd = _excused_union_diff(A, U, m, g["IA"], inj["IA"]) + _excused_union_diff(B, U, m, g["IB"], inj["IB"])
