@@ -94,6 +94,7 @@ int prohd_launch_count(int64_t* out);
  *   "k3_simt"       1: SIMT projection kernel instead of tcgen05
  *   "eig_stop"      1|2|3: stop the eigen-solver after that stage (timing prefixes only)
  *   "eig_cl"        8: portable 8-CTA tridiagonalisation cluster
+ *   "k1_ablate"     1|2: int8 Gram timing ablations (skip slicing / MMAs; WRONG results, dev only)
  * value < 0 restores the default. PROHD_E_INVALID for an unknown name or NULL pointer. */
 int prohd_set_option(const char* name, int64_t value);
 int prohd_get_option(const char* name, int64_t* value);

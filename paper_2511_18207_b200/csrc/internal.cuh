@@ -30,6 +30,7 @@ enum OptId {
   OPT_K3_SIMT,       // 1: SIMT projection kernel instead of tcgen05
   OPT_EIG_STOP,      // stop K2 after stage 1|2|3 (timing prefixes)
   OPT_EIG_CL,        // 8: portable 8-CTA tridiagonalisation cluster
+  OPT_K1_ABLATE,     // int8 Gram timing ablations (wrong results): 1 no slicing work, 2 no MMAs
   OPT_COUNT
 };
 inline std::atomic<long long>* option_table() {

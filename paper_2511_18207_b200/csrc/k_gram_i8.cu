@@ -53,12 +53,13 @@ namespace {
 constexpr int kPts = 64;          // points per chunk = bytes per digit-plane row (SWIZZLE_64B)
 constexpr int kFeat = 128;        // features per CTA
 constexpr int kRawStages = 3;
-constexpr int kSlStages = 2;
+constexpr int kSlStages = 4;
 constexpr uint32_t kRawBytes = kPts * kFeat * 4;   // 32 KB
 constexpr uint32_t kPlane = kFeat * kPts;          // 8 KB
 constexpr uint32_t kSlBytes = 4 * kPlane;          // 32 KB
 constexpr int kSlicers = 8;      // slicer / drain warps (2-9), two per SM sub-partition
 constexpr int kThreads = 64 + 32 * kSlicers;
+constexpr int kDrainWarps = 8;   // slicer warps 0-7 also drain: 4 TMEM lane quarters x 2 column halves
 constexpr int kDrainChunks = 511;
 constexpr int kColmaxBlocks = 148 * 8;                  // 32704 points: int32 headroom (2^31 / 2^16)
 constexpr size_t kSmem = static_cast<size_t>(kRawStages) * kRawBytes + kSlStages * kSlBytes + 1024 + 512;  // + barriers
@@ -72,6 +73,7 @@ struct I8Args {
   const double* cpart;   // [ncs blocks][2][D] fp64 column sums of A, B (i8_colmax_kernel)
   int ncs;
   unsigned* overflow;
+  int ablate;            // dev timing only (option k1_ablate): 1 skip the slicing work, 2 skip the MMAs
 };
 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
@@ -190,7 +192,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&sl_fwd[i], kSlicers);
     }
     mbar_init(&tfull[0], 1);
-    mbar_init(&tempty[0], 2 * kSlicers);
+    mbar_init(&tempty[0], 2 * kDrainWarps);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -210,12 +212,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int st = 0;
       uint32_t ph = 0;
       for (int c = 0; c < nchunks; ++c) {
-        mbar_wait_sleep(&raw_empty[st], ph ^ 1u);
+        mbar_wait(&raw_empty[st], ph ^ 1u);
         mbar_arrive_expect_tx(&raw_full[st], kRawBytes);
         const bool inA = c < R.na;
         const int64_t row = inA ? R.a0 + static_cast<int64_t>(c) * kPts : R.b0 + static_cast<int64_t>(c - R.na) * kPts;
-        tma_load_2d(raw + st * kRawBytes, inA ? &tA : &tB, static_cast<int>(rank) * kFeat, static_cast<int>(row),
-                    &raw_full[st]);
+        // four [32 features x 64 rows] SWIZZLE_128B boxes (128-byte rows): the whole 128-feature half
+        for (int bx = 0; bx < 4; ++bx)
+          tma_load_2d(raw + st * kRawBytes + bx * (kRawBytes / 4), inA ? &tA : &tB,
+                      static_cast<int>(rank) * kFeat + bx * 32, static_cast<int>(row), &raw_full[st]);
         if (++st == kRawStages) {
           st = 0;
           ph ^= 1u;
@@ -225,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer (leader CTA)
-    if (rank == 0 && lane == 0) {
+    if (rank == 0 && lane == 0 && a.ablate < 4) {
       constexpr uint32_t idesc = idesc_i8(256, 256);
       // (t, u, accumulator slot): type 0 = levels {0 -> slot 0, 3 -> slot 1}, type 1 = {1 -> 0, 2 -> 1}
       int tt[5], uu[5], ss[5];
@@ -250,7 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait_cluster(&sl_full[st], ph);
         tc_fence_after();
         const uint32_t base = smem_u32(sl + st * kSlBytes);
-        for (int kk = 0; kk < 2; ++kk) {
+        for (int kk = 0; kk < (a.ablate >= 2 ? 0 : 2); ++kk) {
           for (int i = 0; i < 5; ++i) {  // K = 32 points = 4 swizzle atoms of 8 rows: +4 KB per K-step
             const uint64_t da = smem_desc_mn_sw128(base + tt[i] * kPlane + kk * 4096);
             const uint64_t db = smem_desc_mn_sw128(base + uu[i] * kPlane + kk * 4096);
@@ -270,7 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (rank == 1 && lane == 0) {
+    if (rank == 1 && lane == 0 && a.ablate < 4) {
       // forwarder: the peer's slicer warps arrive on a local barrier; one cluster-scope release
       // arrival per chunk on the leader's slices-full barrier (instead of one per warp)
       const uint32_t leader_full = mapa(smem_u32(&sl_full[0]), 0);
@@ -312,7 +316,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const double w0 = type == 0 ? 1.0 : (type == 1 ? 0x1p-8 : 0x1p-32);
     const double w1 = type == 0 ? 0x1p-24 : (type == 1 ? 0x1p-16 : 0x1p-40);
     double* out = a.slab + (static_cast<int64_t>(cta) * kFeat + rowl) * 256 + half * 128;
-    float ymax = 0.0f;
     int rst = 0, sst = 0, since = 0, ndr = 0;
     uint32_t rph = 0, sph = 0, tph = 0;
     for (int c = 0; c < nchunks; ++c) {
@@ -321,22 +324,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int64_t rend = inA ? R.a1 : R.b1;
       const int valid = static_cast<int>(min(static_cast<int64_t>(kPts), rend - row0));
       mbar_wait(&raw_full[rst], rph);
-      mbar_wait(&sl_empty[sst], sph ^ 1u);
-      const uint32_t xr = raw_u32 + rst * kRawBytes + lane * 16;
+      if (a.ablate < 4) mbar_wait(&sl_empty[sst], sph ^ 1u);
+      // raw box (lane / 8) holds features 32 (lane / 8) ..; row p, 16-byte chunk (lane % 8) ^ (p % 8)
+      const uint32_t xr = raw_u32 + rst * kRawBytes + (lane >> 3) * (kRawBytes / 4);
       const uint32_t pl = sl_u32 + sst * kSlBytes;
-#pragma unroll 4
-      for (int pp = 0; pp < kPts / kSlicers; ++pp) {
-        const int p = kSlicers * pp + ws;
-        const float4 x4 = lds128(xr + p * (kFeat * 4));
-        // rows past the range: F = c0 = 0x808080, i.e. F - c0 = 0 (no contribution)
-        const bool ok = p < valid;
+      // all of this warp's points of the chunk are loaded first (8 independent 16-byte loads in
+      // flight), then converted: the shared-memory latency is not on each point's dependency chain
+      constexpr int kPer = kPts / kSlicers;
+      float4 xs[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int p = ws + kSlicers * u;
+        xs[u] = lds128(xr + p * 128 + ((((lane & 7) ^ (p & 7)) & 7) << 4));
+      }
+      // one 4-point group: y = x 2^k - S (rows past the range: F = c0, i.e. F - c0 = 0), F, the four
+      // digit bytes per feature, 4 x 4 byte transpose, one 32-bit store per digit plane
+      auto slice_point = [&](int u, bool ok) {
+        const int p = ws + kSlicers * u;
+        const float4 x4 = xs[u];
         const float y0 = ok ? fmaf(x4.x, sc[0], -sh[0]) : 8421504.0f, y1 = ok ? fmaf(x4.y, sc[1], -sh[1]) : 8421504.0f;
         const float y2 = ok ? fmaf(x4.z, sc[2], -sh[2]) : 8421504.0f, y3 = ok ? fmaf(x4.w, sc[3], -sh[3]) : 8421504.0f;
-        ymax = fmaxf(fmaxf(ymax, fmaxf(fabsf(y0), fabsf(y1))), fmaxf(fabsf(y2), fabsf(y3)));
         const uint32_t w0i = static_cast<uint32_t>(__float2int_rn(y0)), w1i = static_cast<uint32_t>(__float2int_rn(y1));
         const uint32_t w2i = static_cast<uint32_t>(__float2int_rn(y2)), w3i = static_cast<uint32_t>(__float2int_rn(y3));
-        // 4 x 4 byte transpose: plane t (t = 0 the top byte) gets byte 3 - t of the 4 features;
-        // the three low planes XOR 0x80 per byte (balanced digits of F - c0)
+        // plane t (t = 0 the top byte) gets byte 3 - t of the 4 features; the three low planes XOR
+        // 0x80 per byte (balanced digits of F - c0)
         const uint32_t x01l = __byte_perm(w0i, w1i, 0x5140), x01h = __byte_perm(w0i, w1i, 0x7362);
         const uint32_t x23l = __byte_perm(w2i, w3i, 0x5140), x23h = __byte_perm(w2i, w3i, 0x7362);
         const uint32_t b0 = __byte_perm(x01l, x23l, 0x5410) ^ 0x80808080u;
@@ -350,12 +361,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         sts32(pl + 1 * kPlane + off, b2);
         sts32(pl + 2 * kPlane + off, b1);
         sts32(pl + 3 * kPlane + off, b0);
+      };
+      if (!(a.ablate & 1)) {
+        if (valid == kPts) {
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) slice_point(u, true);
+        } else {  // the last, ragged chunk of a set
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) slice_point(u, ws + kSlicers * u < valid);
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&raw_empty[rst]);
-        mbar_arrive(rank == 0 ? &sl_full[sst] : &sl_fwd[sst]);  // CTA scope; the peer's are forwarded
+        if (a.ablate < 4) mbar_arrive(rank == 0 ? &sl_full[sst] : &sl_fwd[sst]);  // CTA scope; the peer's are forwarded
       }
       if (++rst == kRawStages) {
         rst = 0;
@@ -365,7 +385,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         sst = 0;
         sph ^= 1u;
       }
-      if (++since == kDrainChunks || c == nchunks - 1) {
+      if (a.ablate >= 4) continue;
+      if ((++since == kDrainChunks || c == nchunks - 1) && ws >= kDrainWarps) {
+        since = 0;
+      } else if (since == kDrainChunks || c == nchunks - 1) {
         // drain window ends with this chunk: TMEM -> fp64 slab (this warp: its lane quarter, its
         // 128-column half of both level slots), then release the accumulators to the MMA issuer
         since = 0;
@@ -390,9 +413,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive_cluster(leader_te);
       }
     }
-    if (nchunks == 0)
+    if (nchunks == 0 && ws < kDrainWarps)
       for (int j2 = 0; j2 < 128; ++j2) out[j2] = 0.0;  // an empty group contributes zeros
-    if (!(ymax < 2147483008.0f)) atomicOr(a.overflow, 1u);  // beyond int32 (or NaN / inf)
+    // |y| <= 2^30 by the exact column max; non-finite input is flagged by the pre-pass
   }
   tc_fence_before();
   __syncthreads();
@@ -407,6 +430,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // sums of A and of B: thread = a 16-byte column piece (D % 4 == 0), rows strided over the grid;
 // block max -> atomicMax on the non-negative float bits (non-finite values force +inf); block
 // sums (fixed order) -> csum_part[block][set][D] for gram_i8_reduce_kernel (fixed order again).
+// Non-finite input propagates into the sums and is flagged there.
 __global__ void __launch_bounds__(256) i8_colmax_kernel(const float* __restrict__ A, int64_t nA,
                                                         const float* __restrict__ B, int64_t nB, int D,
                                                         const double* __restrict__ s, unsigned* colmax,
@@ -423,8 +447,38 @@ __global__ void __launch_bounds__(256) i8_colmax_kernel(const float* __restrict_
   for (int i = 0; i < 4; ++i) sf[i] = static_cast<float>(s[4 * piece + i]);
   if (rsub < rows_per_block) {
     const int64_t N = nA + nB;
-    for (int64_t r = static_cast<int64_t>(blockIdx.x) * rows_per_block + rsub; r < N;
-         r += static_cast<int64_t>(gridDim.x) * rows_per_block) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * rows_per_block;
+    int64_t r = static_cast<int64_t>(blockIdx.x) * rows_per_block + rsub;
+    // four rows in flight per iteration (memory-level parallelism: the register budget limits the
+    // resident threads), then the remainder one at a time
+    for (; r + 3 * stride < N; r += 4 * stride) {
+      float4 vv[4];
+      bool ia[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t ru = r + u * stride;
+        ia[u] = ru < nA;
+        vv[u] = __ldg(reinterpret_cast<const float4*>(ia[u] ? A + ru * D : B + (ru - nA) * D) + piece);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 v = vv[u];
+        m[0] = fmaxf(m[0], fabsf(v.x - sf[0]));
+        m[1] = fmaxf(m[1], fabsf(v.y - sf[1]));
+        m[2] = fmaxf(m[2], fabsf(v.z - sf[2]));
+        m[3] = fmaxf(m[3], fabsf(v.w - sf[3]));
+        const double e0 = ia[u] ? 1.0 : 0.0, e1 = 1.0 - e0;
+        sum[0][0] = fma(e0, static_cast<double>(v.x), sum[0][0]);
+        sum[0][1] = fma(e0, static_cast<double>(v.y), sum[0][1]);
+        sum[0][2] = fma(e0, static_cast<double>(v.z), sum[0][2]);
+        sum[0][3] = fma(e0, static_cast<double>(v.w), sum[0][3]);
+        sum[1][0] = fma(e1, static_cast<double>(v.x), sum[1][0]);
+        sum[1][1] = fma(e1, static_cast<double>(v.y), sum[1][1]);
+        sum[1][2] = fma(e1, static_cast<double>(v.z), sum[1][2]);
+        sum[1][3] = fma(e1, static_cast<double>(v.w), sum[1][3]);
+      }
+    }
+    for (; r < N; r += stride) {
       const bool inA = r < nA;
       const float* row = inA ? A + r * D : B + (r - nA) * D;
       const float4 v = __ldg(reinterpret_cast<const float4*>(row) + piece);
@@ -432,7 +486,6 @@ __global__ void __launch_bounds__(256) i8_colmax_kernel(const float* __restrict_
       m[1] = fmaxf(m[1], fabsf(v.y - sf[1]));
       m[2] = fmaxf(m[2], fabsf(v.z - sf[2]));
       m[3] = fmaxf(m[3], fabsf(v.w - sf[3]));
-      if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w))) m[0] = __int_as_float(0x7f800000);
       const double e0 = inA ? 1.0 : 0.0, e1 = 1.0 - e0;  // branch-free, no dynamic indexing
       sum[0][0] = fma(e0, static_cast<double>(v.x), sum[0][0]);
       sum[0][1] = fma(e0, static_cast<double>(v.y), sum[0][1]);
@@ -494,19 +547,17 @@ __global__ void i8_scale_kernel(int D, const double* __restrict__ s, const unsig
   }
 }
 
-// G = 2^(-k_i - k_j) sum over groups and pair types of the slabs (fixed order), S_X, s'
-__global__ void gram_i8_reduce_kernel(I8Args a, double* G, double* SA, double* SB, double* s) {
+// G = 2^(-k_i - k_j) sum over groups and pair types of the slabs (fixed order), S_X, s'.
+// Block = one row i of G, thread = column j: every slab row is read coalesced (2 KB), and the
+// 3 x ngroups loads of a thread are independent (memory-level parallelism).
+__global__ void __launch_bounds__(256) gram_i8_reduce_kernel(I8Args a, double* G, double* SA, double* SB, double* s) {
   const int D = a.D;
-  const int64_t total = static_cast<int64_t>(D) * D;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int i = static_cast<int>(e / D), j = static_cast<int>(e % D);
+  const int i = blockIdx.x, j = threadIdx.x;
+  if (i < D && j < D) {
     const int r = i / kFeat, row = i % kFeat;
-    // fixed order: 4 interleaved partial sums over the groups (memory-level parallelism), then
-    // combined in order -- deterministic for a given group count
-    double part[4] = {0.0, 0.0, 0.0, 0.0};
-    const double* base = a.slab + static_cast<int64_t>(r) * kFeat * 256 + static_cast<int64_t>(row) * 256 + j;
     const int64_t cstride = static_cast<int64_t>(kFeat) * 256;  // one CTA slab
+    const double* base = a.slab + static_cast<int64_t>(r) * cstride + static_cast<int64_t>(row) * 256 + j;
+    double part[4] = {0.0, 0.0, 0.0, 0.0};  // fixed interleave over groups: deterministic
 #pragma unroll 4
     for (int g = 0; g < a.ngroups; ++g) {
       const double* gb = base + static_cast<int64_t>(g * 3) * 2 * cstride;
@@ -514,7 +565,8 @@ __global__ void gram_i8_reduce_kernel(I8Args a, double* G, double* SA, double* S
     }
     const double acc = (part[0] + part[1]) + (part[2] + part[3]);
     // slabs carry sum_L 2^(-8L) G_L = 2^-48 sum_L 2^(8 (6 - L)) G_L
-    G[e] = ldexp(acc, 48) / (static_cast<double>(a.scale[i]) * static_cast<double>(a.scale[j]));
+    G[static_cast<int64_t>(i) * D + j] =
+        ldexp(acc, 48) / (static_cast<double>(a.scale[i]) * static_cast<double>(a.scale[j]));
   }
   if (blockIdx.x == 0) {
     for (int j = threadIdx.x; j < D; j += blockDim.x) {
@@ -523,6 +575,7 @@ __global__ void gram_i8_reduce_kernel(I8Args a, double* G, double* SA, double* S
         sa += a.cpart[(static_cast<int64_t>(b) * 2 + 0) * D + j];
         sb += a.cpart[(static_cast<int64_t>(b) * 2 + 1) * D + j];
       }
+      if (!isfinite(sa) || !isfinite(sb)) atomicOr(a.overflow, 1u);  // non-finite input: the DMMA path reports it
       const double sp = (static_cast<double>(a.shiftf[j]) + 128.0 * 65793.0) / static_cast<double>(a.scale[j]);
       SA[j] = sa - static_cast<double>(a.nA) * sp;  // sums about s' = (S + c0) 2^-k
       SB[j] = sb - static_cast<double>(a.nB) * sp;
@@ -563,7 +616,7 @@ cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, cons
   float* shiftf = scale + 256;
   CUtensorMap maps[2];
   char err[256];
-  // raw fp32 boxes [128 features x 64 rows], no swizzle (the slicers read them, not the MMA)
+  // raw fp32 boxes [32 features x 64 rows], SWIZZLE_128B (four per chunk and CTA)
   PFN_encodeTiled enc = get_encode();
   if (enc == nullptr) return cudaErrorNotSupported;
   const float* src[2] = {A, B};
@@ -571,10 +624,10 @@ cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, cons
   for (int i = 0; i < 2; ++i) {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(rows[i])};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 4};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(kFeat), static_cast<cuuint32_t>(kPts)};
+    cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(kPts)};
     cuuint32_t estr[2] = {1, 1};
     if (enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(src[i]), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
@@ -586,7 +639,8 @@ cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, cons
   i8_colmax_kernel<<<kColmaxBlocks, 256, 0, st>>>(A, nA, B, nB, D, s, colmax, cpart);
   count_launch();
   i8_scale_kernel<<<1, 256, 0, st>>>(D, s, colmax, scale, shiftf, overflow);
-  I8Args a{nA, nB, D, p.ngroups, scale, shiftf, slab, cpart, kColmaxBlocks, overflow};
+  I8Args a{nA, nB, D, p.ngroups, scale, shiftf, slab, cpart, kColmaxBlocks, overflow,
+           opt(OPT_K1_ABLATE) > 0 ? static_cast<int>(opt(OPT_K1_ABLATE)) : 0};
   cudaError_t e =
       cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
   if (e != cudaSuccess) return e;
@@ -594,7 +648,7 @@ cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, cons
   gram_i8_kernel<<<p.nctas, kThreads, kSmem, st>>>(maps[0], maps[1], a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   count_launch();
-  gram_i8_reduce_kernel<<<148, 256, 0, st>>>(a, G, SA, SB, s);
+  gram_i8_reduce_kernel<<<D, 256, 0, st>>>(a, G, SA, SB, s);
   return cudaGetLastError();
 }
 
