@@ -194,21 +194,43 @@ def phase_rooflines(c, t_est: dict, t_ex: dict, est: dict, pk: dict) -> dict:
 
     mom = t_est.get("moments_ms")
     gram_flops = 2.0 * N * D * D
-    out["K1_moments"] = {"bound": "tensor", "ms": mom, "flops": gram_flops,
-                         "achieved": gram_flops / (mom / 1e3) / 1e12 if mom else None, "unit": "TFLOP/s",
-                         "peak": tf32, "frac": (gram_flops / (mom / 1e3) / 1e12) / tf32 if mom else None,
-                         "hbm_frac": (N * D * 4 / (mom / 1e3) / 1e9) / hbm if mom else None,
-                         "what": "useful Gram flops 2 (nA+nB) D^2 against the TF32 tensor peak (SURVEY §8(d3)); "
-                                 "hbm_frac: one read of A u B (4D B per point) over the phase time"}
+    i8 = 128 < D <= 256 and D % 4 == 0  # the int8 tensor-core Gram (k_gram_i8.cu); else fp64 DMMA
+    if i8 and mom:
+        # executed: 15 slice-pair products of the full 256 x 256 Gram per point (cta_group::2 M=N=256)
+        i8_ops = N * 15 * 2.0 * 256 * 256
+        i8_peak = 2.0 * bf16  # int8 dense = 2x the bf16 rate (B200_PROFILING.md nominal 4.5 vs 2.25 PF)
+        out["K1_moments"] = {"bound": "tensor", "path": "int8 tcgen05 (exact-integer Ozaki)", "ms": mom,
+                             "executed_int8_ops": i8_ops, "achieved": i8_ops / (mom / 1e3) / 1e12,
+                             "unit": "TOP/s (int8)", "peak": i8_peak,
+                             "frac": i8_ops / (mom / 1e3) / 1e12 / i8_peak,
+                             "useful_tflops": gram_flops / (mom / 1e3) / 1e12,
+                             "useful_frac_tf32": gram_flops / (mom / 1e3) / 1e12 / tf32,
+                             "hbm_frac": (2 * N * D * 4 / (mom / 1e3) / 1e9) / hbm,
+                             "what": "whole moments phase (column-max pass, int8 Gram, reduce, finalize): executed "
+                                     "int8 MMA ops (15 digit-pair products x 2 x 256^2 per point) against the int8 "
+                                     "dense peak (2 x bf16 burst); useful = 2 (nA+nB) D^2 fp64-grade Gram flops; "
+                                     "hbm_frac: two reads of A u B (column max, Gram)"}
+    else:
+        out["K1_moments"] = {"bound": "tensor", "path": "fp64 DMMA", "ms": mom, "flops": gram_flops,
+                             "achieved": gram_flops / (mom / 1e3) / 1e12 if mom else None, "unit": "TFLOP/s",
+                             "peak": tf32, "frac": (gram_flops / (mom / 1e3) / 1e12) / tf32 if mom else None,
+                             "hbm_frac": (N * D * 4 / (mom / 1e3) / 1e9) / hbm if mom else None,
+                             "what": "useful Gram flops 2 (nA+nB) D^2 against the TF32 tensor peak (SURVEY §8(d3)); "
+                                     "hbm_frac: one read of A u B (4D B per point) over the phase time"}
     hb("K3K4K5_select", N * (D * 4 + 2 * L * 4), t_est.get("select_ms"),
        "per point: read 4D B (projection), write 4(k+1) B, read 4(k+1) B (selection): the one-pass floor")
     out["K2_eigen"] = {"bound": "latency", "ms": t_est.get("eigen_ms")}
     sub_ms = t_est.get("subset_ms")
     sp = float(est["size_a"]) * float(est["size_b"])
     out["K6_subset"] = {"bound": "tensor", "ms": sub_ms, "pairs": sp,
-                        "note": "fused bidirectional sweep over |I_A| x |I_B| pairs (both directions) plus K0/K7"}
-    hb("K0_prep_exact", N * (12 * D + 4), t_ex.get("prep_ms"),
-       "K0 of the exact call: read 4D B, write hi 4D + pairs 8D... (12D + 4 B per point of A and B)")
+                        "achieved": 6.0 * D * sp / (sub_ms / 1e3) / 1e12 if sub_ms else None,
+                        "unit": "TFLOP/s (fp16)", "peak": bf16,
+                        "frac": 6.0 * D * sp / (sub_ms / 1e3) / 1e12 / bf16 if sub_ms else None,
+                        "note": "fused bidirectional sweep over |I_A| x |I_B| pairs (both directions, 6D fp16 "
+                                "flops per pair) over the whole subset phase (gather, centre, K0, K6, K7)"}
+    hb("K0_prep_exact", N * (12 * D + 12), t_ex.get("prep_ms"),
+       "K0 of the exact call: stats pass (read 4D B) + write pass (read 4D B, write fp16 hi + lo 4D B, "
+       "norm + scale 8 B): 12D + 12 B per point of A and B")
     floor_ms = 2 * N * D * 4 / (hbm * 1e9) * 1e3
     tot = t_est.get("total_ms")
     out["prohd"] = {"ms": tot, "floor_ms": floor_ms, "frac": floor_ms / tot if tot else None,

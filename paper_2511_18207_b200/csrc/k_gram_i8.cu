@@ -467,15 +467,17 @@ __global__ void __launch_bounds__(256) i8_colmax_kernel(const float* __restrict_
         m[1] = fmaxf(m[1], fabsf(v.y - sf[1]));
         m[2] = fmaxf(m[2], fabsf(v.z - sf[2]));
         m[3] = fmaxf(m[3], fabsf(v.w - sf[3]));
-        const double e0 = ia[u] ? 1.0 : 0.0, e1 = 1.0 - e0;
-        sum[0][0] = fma(e0, static_cast<double>(v.x), sum[0][0]);
-        sum[0][1] = fma(e0, static_cast<double>(v.y), sum[0][1]);
-        sum[0][2] = fma(e0, static_cast<double>(v.z), sum[0][2]);
-        sum[0][3] = fma(e0, static_cast<double>(v.w), sum[0][3]);
-        sum[1][0] = fma(e1, static_cast<double>(v.x), sum[1][0]);
-        sum[1][1] = fma(e1, static_cast<double>(v.y), sum[1][1]);
-        sum[1][2] = fma(e1, static_cast<double>(v.z), sum[1][2]);
-        sum[1][3] = fma(e1, static_cast<double>(v.w), sum[1][3]);
+        if (ia[u]) {  // warp-uniform: a warp's lanes read pieces of the same row
+          sum[0][0] += static_cast<double>(v.x);
+          sum[0][1] += static_cast<double>(v.y);
+          sum[0][2] += static_cast<double>(v.z);
+          sum[0][3] += static_cast<double>(v.w);
+        } else {
+          sum[1][0] += static_cast<double>(v.x);
+          sum[1][1] += static_cast<double>(v.y);
+          sum[1][2] += static_cast<double>(v.z);
+          sum[1][3] += static_cast<double>(v.w);
+        }
       }
     }
     for (; r < N; r += stride) {
@@ -486,15 +488,17 @@ __global__ void __launch_bounds__(256) i8_colmax_kernel(const float* __restrict_
       m[1] = fmaxf(m[1], fabsf(v.y - sf[1]));
       m[2] = fmaxf(m[2], fabsf(v.z - sf[2]));
       m[3] = fmaxf(m[3], fabsf(v.w - sf[3]));
-      const double e0 = inA ? 1.0 : 0.0, e1 = 1.0 - e0;  // branch-free, no dynamic indexing
-      sum[0][0] = fma(e0, static_cast<double>(v.x), sum[0][0]);
-      sum[0][1] = fma(e0, static_cast<double>(v.y), sum[0][1]);
-      sum[0][2] = fma(e0, static_cast<double>(v.z), sum[0][2]);
-      sum[0][3] = fma(e0, static_cast<double>(v.w), sum[0][3]);
-      sum[1][0] = fma(e1, static_cast<double>(v.x), sum[1][0]);
-      sum[1][1] = fma(e1, static_cast<double>(v.y), sum[1][1]);
-      sum[1][2] = fma(e1, static_cast<double>(v.z), sum[1][2]);
-      sum[1][3] = fma(e1, static_cast<double>(v.w), sum[1][3]);
+      if (inA) {  // warp-uniform: a warp's lanes read pieces of the same row
+        sum[0][0] += static_cast<double>(v.x);
+        sum[0][1] += static_cast<double>(v.y);
+        sum[0][2] += static_cast<double>(v.z);
+        sum[0][3] += static_cast<double>(v.w);
+      } else {
+        sum[1][0] += static_cast<double>(v.x);
+        sum[1][1] += static_cast<double>(v.y);
+        sum[1][2] += static_cast<double>(v.z);
+        sum[1][3] += static_cast<double>(v.w);
+      }
     }
   }
 #pragma unroll
