@@ -572,19 +572,34 @@ __global__ void __launch_bounds__(256) gram_i8_reduce_kernel(I8Args a, double* G
     G[static_cast<int64_t>(i) * D + j] =
         ldexp(acc, 48) / (static_cast<double>(a.scale[i]) * static_cast<double>(a.scale[j]));
   }
-  if (blockIdx.x == 0) {
-    for (int j = threadIdx.x; j < D; j += blockDim.x) {
-      double sa = 0.0, sb = 0.0;
-      for (int b = 0; b < a.ncs; ++b) {  // fixed order: deterministic
-        sa += a.cpart[(static_cast<int64_t>(b) * 2 + 0) * D + j];
-        sb += a.cpart[(static_cast<int64_t>(b) * 2 + 1) * D + j];
-      }
-      if (!isfinite(sa) || !isfinite(sb)) atomicOr(a.overflow, 1u);  // non-finite input: the DMMA path reports it
-      const double sp = (static_cast<double>(a.shiftf[j]) + 128.0 * 65793.0) / static_cast<double>(a.scale[j]);
-      SA[j] = sa - static_cast<double>(a.nA) * sp;  // sums about s' = (S + c0) 2^-k
-      SB[j] = sb - static_cast<double>(a.nB) * sp;
-      s[j] = sp;
+  // column sums of feature i (this block's row index): thread t adds partials t, t + 256, ... of
+  // A and of B, then a fixed tree over the block -- deterministic, and the 1184 partials are read
+  // by 256 threads instead of one sequential chain
+  __shared__ double red[2][256];
+  double sa = 0.0, sb = 0.0;
+  if (i < D)
+    for (int b = j; b < a.ncs; b += blockDim.x) {
+      sa += a.cpart[(static_cast<int64_t>(b) * 2 + 0) * D + i];
+      sb += a.cpart[(static_cast<int64_t>(b) * 2 + 1) * D + i];
     }
+  red[0][j] = sa;
+  red[1][j] = sb;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (j < o) {
+      red[0][j] += red[0][j + o];
+      red[1][j] += red[1][j + o];
+    }
+    __syncthreads();
+  }
+  if (j == 0 && i < D) {
+    sa = red[0][0];
+    sb = red[1][0];
+    if (!isfinite(sa) || !isfinite(sb)) atomicOr(a.overflow, 1u);  // non-finite input: the DMMA path reports it
+    const double sp = (static_cast<double>(a.shiftf[i]) + 128.0 * 65793.0) / static_cast<double>(a.scale[i]);
+    SA[i] = sa - static_cast<double>(a.nA) * sp;  // sums about s' = (S + c0) 2^-k
+    SB[i] = sb - static_cast<double>(a.nB) * sp;
+    s[i] = sp;
   }
 }
 
