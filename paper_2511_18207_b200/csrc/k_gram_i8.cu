@@ -15,9 +15,13 @@
 // and sum_p d_t(x_pi) d_u(x_pj) is an exact int8 x int8 -> int32 tensor-core product. Levels
 // L = t + u <= 5 are kept: only d_3 d_3 (weight 1, |.| <= 2^14) is dropped, zero-mean, against
 // products of |F| up to 2^30 (levels <= 3 alone would drop terms up to 2^32, too much for
-// small values of heavy-tailed columns, whose leading digits are zero). The pairs of one level
-// share an int32 TMEM accumulator, which grows by at most 4 * 128^2 = 2^16 per point, so it is
-// drained to fp64 every <= 32704 points (exact).
+// small values of heavy-tailed columns, whose leading digits are zero). The Gram is symmetric,
+// so G_L = sum_{t+u=L} D_t^T D_u needs only the symmetric part of Z_L = 2 D_0^T D_L + sum_{t,u>0}
+// D_t^T D_u (L > 0), Z_0 = 4 D_0^T D_0: M_j 2^k_j <= 2^30 - 256 keeps d_0 in [-64, 63], so the
+// DOUBLED top digit 2 d_0 is an int8 plane and each pair (0, u), (u, 0) costs one product
+// instead of two -- 12 products per point instead of 15; the reduce takes (Z + Z^T) / 2. The
+// products of one level share an int32 TMEM accumulator, which grows by at most 3 * 128^2 < 2^16
+// per point, so it is drained to fp64 every <= 32704 points (exact).
 // The result is the Gram about s'_j = (S_j + c0) 2^-k_j (exact fixed-point shift), written with
 // s' into the moments buffers: G_ij = 2^(-k_i - k_j) sum_L 2^(8 (6 - L)) G_L, S_X = 2^-k sum F'.
 // A non-finite value sets an overflow flag; the caller then reruns the moments on the fp64
@@ -26,13 +30,13 @@
 // Kernel (cta_group::2, CTA pairs). One MMA M = 256 (all features, 128 per CTA) x N = 256 (all
 // features, 128 per CTA) x K = 32 points covers the full Gram; each SM holds 128 rows x 256
 // columns of int32 per level, so a pair holds two levels (all 512 TMEM columns): pair type 0
-// accumulates levels {0, 3} (1 + 4 products), type 1 levels {1, 2} (2 + 3), type 2 levels {4, 5}
-// (3 + 2). A group = one pair of each type over the same rows of A and of B (L2 serves the
+// accumulates levels {0, 3} (1 + 3 products), type 1 levels {1, 4} (1 + 3), type 2 levels {2, 5}
+// (2 + 2). A group = one pair of each type over the same rows of A and of B (L2 serves the
 // repeated reads); 24 groups = 144 SMs.
 // Per CTA (320 threads):
 //   warp 0     TMA: raw fp32 chunks [64 points x 128 features] (this CTA's feature half),
 //              3 stages of 32 KB.
-//   warp 1     (leader CTA) MMA issuer: per 64-point chunk 2 K-steps x 5 tcgen05.mma.cta_group::2
+//   warp 1     (leader CTA) MMA issuer: per 64-point chunk 2 K-steps x 4 tcgen05.mma.cta_group::2
 //              .kind::i8 over the two CTAs' digit planes; commit -> slice stage free (both CTAs).
 //   warps 2-5  slicers: warp = every 4th point of the chunk, lane = 4 features: one 16-byte load,
 //              F for the 4 values, a 4 x 4 byte transpose (PRMT) and one 32-bit store per digit
@@ -41,7 +45,8 @@
 //              set (int64 column sums). Arrive (cluster scope) on the leader's slices-full barrier.
 //   warps 6-9  drain: TMEM lane quarter warp % 4 = feature rows; int32 -> fp64, both levels
 //              weighted, added into this CTA's fp64 slab [128][256] in global memory.
-// gram_i8_reduce_kernel sums the slabs in a fixed order (deterministic) and applies 2^(-k_i-k_j).
+// gram_i8_reduce_kernel sums the slabs in a fixed order (deterministic) and applies 2^(-k_i-k_j);
+// gram_i8_sym_kernel takes the symmetric part.
 #include "api_common.cuh"  // TMA descriptor encoder
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
@@ -231,17 +236,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------------ MMA issuer (leader CTA)
     if (rank == 0 && lane == 0 && a.ablate < 4) {
       constexpr uint32_t idesc = idesc_i8(256, 256);
-      // (t, u, accumulator slot): type 0 = levels {0 -> slot 0, 3 -> slot 1}, type 1 = {1 -> 0, 2 -> 1}
-      int tt[5], uu[5], ss[5];
+      // (t, u, accumulator slot), plane 0 = 2 d_0: type 0 = levels {0 -> slot 0, 3 -> slot 1},
+      // type 1 = {1, 4}, type 2 = {2, 5}; the pairs (0, u) and (u, 0) are one product 2 d_0 d_u
+      // (the reduce symmetrises), (0, 0) is 4 d_0 d_0 (drain weight / 4)
+      int tt[4], uu[4], ss[4];
       if (type == 0) {
-        const int t0[5] = {0, 0, 1, 2, 3}, u0[5] = {0, 3, 2, 1, 0}, s0[5] = {0, 1, 1, 1, 1};
-        for (int i = 0; i < 5; ++i) tt[i] = t0[i], uu[i] = u0[i], ss[i] = s0[i];
+        const int t0[4] = {0, 0, 1, 2}, u0[4] = {0, 3, 2, 1}, s0[4] = {0, 1, 1, 1};
+        for (int i = 0; i < 4; ++i) tt[i] = t0[i], uu[i] = u0[i], ss[i] = s0[i];
       } else if (type == 1) {
-        const int t1[5] = {0, 1, 0, 1, 2}, u1[5] = {1, 0, 2, 1, 0}, s1[5] = {0, 0, 1, 1, 1};
-        for (int i = 0; i < 5; ++i) tt[i] = t1[i], uu[i] = u1[i], ss[i] = s1[i];
+        const int t1[4] = {0, 1, 3, 2}, u1[4] = {1, 3, 1, 2}, s1[4] = {0, 1, 1, 1};
+        for (int i = 0; i < 4; ++i) tt[i] = t1[i], uu[i] = u1[i], ss[i] = s1[i];
       } else {
-        const int t2[5] = {1, 2, 3, 2, 3}, u2[5] = {3, 2, 1, 3, 2}, s2[5] = {0, 0, 0, 1, 1};
-        for (int i = 0; i < 5; ++i) tt[i] = t2[i], uu[i] = u2[i], ss[i] = s2[i];
+        const int t2[4] = {0, 1, 2, 3}, u2[4] = {2, 1, 3, 2}, s2[4] = {0, 0, 1, 1};
+        for (int i = 0; i < 4; ++i) tt[i] = t2[i], uu[i] = u2[i], ss[i] = s2[i];
       }
       int st = 0;
       uint32_t ph = 0, tph = 0;
@@ -255,7 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t base = smem_u32(sl + st * kSlBytes);
         for (int kk = 0; kk < (a.ablate >= 2 ? 0 : 2); ++kk) {
-          for (int i = 0; i < 5; ++i) {  // K = 32 points = 4 swizzle atoms of 8 rows: +4 KB per K-step
+          for (int i = 0; i < 4; ++i) {  // K = 32 points = 4 swizzle atoms of 8 rows: +4 KB per K-step
             const uint64_t da = smem_desc_mn_sw128(base + tt[i] * kPlane + kk * 4096);
             const uint64_t db = smem_desc_mn_sw128(base + uu[i] * kPlane + kk * 4096);
             const bool first = since == 0 && kk == 0 && (i == 0 || ss[i] != ss[i - 1]);
@@ -311,10 +318,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3, half = ws >> 2;
     const int rowl = q * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
-    // level weights 2^(8 (6 - L)) / 2^48 = 2^(-8 L): slots of type 0 = levels {0, 3}, type 1 =
-    // {1, 2}, type 2 = {4, 5}
-    const double w0 = type == 0 ? 1.0 : (type == 1 ? 0x1p-8 : 0x1p-32);
-    const double w1 = type == 0 ? 0x1p-24 : (type == 1 ? 0x1p-16 : 0x1p-40);
+    // level weights 2^(8 (6 - L)) / 2^48 = 2^(-8 L): slots of type 0 = levels {0, 3} (level 0
+    // holds 4 d_0 d_0: weight / 4), type 1 = {1, 4}, type 2 = {2, 5}
+    const double w0 = type == 0 ? 0.25 : (type == 1 ? 0x1p-8 : 0x1p-16);
+    const double w1 = type == 0 ? 0x1p-24 : (type == 1 ? 0x1p-32 : 0x1p-40);
     double* out = a.slab + (static_cast<int64_t>(cta) * kFeat + rowl) * 256 + half * 128;
     int rst = 0, sst = 0, since = 0, ndr = 0;
     uint32_t rph = 0, sph = 0, tph = 0;
@@ -353,7 +360,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t b0 = __byte_perm(x01l, x23l, 0x5410) ^ 0x80808080u;
         const uint32_t b1 = __byte_perm(x01l, x23l, 0x7632) ^ 0x80808080u;
         const uint32_t b2 = __byte_perm(x01h, x23h, 0x5410) ^ 0x80808080u;
-        const uint32_t b3 = __byte_perm(x01h, x23h, 0x7632);
+        // plane 0 holds the DOUBLED top digit 2 d_0 (|d_0| <= 64, d_0 <= 63): per-byte shift
+        const uint32_t b3 = (__byte_perm(x01h, x23h, 0x7632) << 1) & 0xFEFEFEFEu;
         // SWIZZLE_128B MN-major: row p (128 B), 16-byte chunk (lane / 4) XOR (p % 8)
         const uint32_t off = static_cast<uint32_t>((p >> 3) * 1024 + (p & 7) * 128 +
                                                    ((((lane >> 2) ^ (p & 7)) & 7) << 4) + (lane & 3) * 4);
@@ -543,11 +551,26 @@ __global__ void i8_scale_kernel(int D, const double* __restrict__ s, const unsig
       int e;
       frexp(static_cast<double>(M), &e);  // M < 2^e
       k = 30 - e;
+      // |F| <= M 2^k + 1/2 (+ the fp32 rounding of the FMA, ulp 64 below 2^30): keep F <= 2^30 - 64
+      // so the top digit lies in [-64, 63] and the doubled top plane fits int8 (colmax itself is
+      // rounded to fp32: a 2^-24 relative margin)
+      if (ldexp(static_cast<double>(M), k) > 0x1p30 - 256.0) --k;
     }
     k = k > 100 ? 100 : (k < -100 ? -100 : k);
     const double sck = ldexp(1.0, k);
     scale[f] = static_cast<float>(sck);
     shiftf[f] = static_cast<float>(rint(static_cast<double>(static_cast<float>(s[f] * sck))));
+  }
+}
+
+// G <- (G + G^T) / 2: the slabs hold Z = sum_L 2^(-8L) Z_L with Z_L + Z_L^T = 2 G_L (the pairs
+// (0, u), u > 0, are accumulated once as 2 d_0 d_u); thread (i, j > i) owns both entries
+__global__ void __launch_bounds__(256) gram_i8_sym_kernel(int D, double* G) {
+  const int i = blockIdx.x, j = threadIdx.x;
+  if (i < D && j < D && j > i) {
+    const double v = 0.5 * (G[static_cast<int64_t>(i) * D + j] + G[static_cast<int64_t>(j) * D + i]);
+    G[static_cast<int64_t>(i) * D + j] = v;
+    G[static_cast<int64_t>(j) * D + i] = v;
   }
 }
 
@@ -668,6 +691,9 @@ cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, cons
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   count_launch();
   gram_i8_reduce_kernel<<<D, 256, 0, st>>>(a, G, SA, SB, s);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  count_launch();
+  gram_i8_sym_kernel<<<D, 256, 0, st>>>(D, G);
   return cudaGetLastError();
 }
 
