@@ -20,8 +20,8 @@
 // D_t^T D_u (L > 0), Z_0 = 4 D_0^T D_0: M_j 2^k_j <= 2^30 - 256 keeps d_0 in [-64, 63], so the
 // DOUBLED top digit 2 d_0 is an int8 plane and each pair (0, u), (u, 0) costs one product
 // instead of two -- 12 products per point instead of 15; the reduce takes (Z + Z^T) / 2. The
-// products of one level share an int32 TMEM accumulator, which grows by at most 3 * 128^2 < 2^16
-// per point, so it is drained to fp64 every <= 32704 points (exact).
+// products of one level share an int32 TMEM accumulator, which grows by at most 3 * 128^2 per
+// point, so it is drained to fp64 every <= 43648 points (exact).
 // The result is the Gram about s'_j = (S_j + c0) 2^-k_j (exact fixed-point shift), written with
 // s' into the moments buffers: G_ij = 2^(-k_i - k_j) sum_L 2^(8 (6 - L)) G_L, S_X = 2^-k sum F'.
 // A non-finite value sets an overflow flag; the caller then reruns the moments on the fp64
@@ -65,8 +65,8 @@ constexpr uint32_t kSlBytes = 4 * kPlane;          // 32 KB
 constexpr int kSlicers = 8;      // slicer / drain warps (2-9), two per SM sub-partition
 constexpr int kThreads = 64 + 32 * kSlicers;
 constexpr int kDrainWarps = 8;   // slicer warps 0-7 also drain: 4 TMEM lane quarters x 2 column halves
-constexpr int kDrainChunks = 511;
-constexpr int kColmaxBlocks = 148 * 8;                  // 32704 points: int32 headroom (2^31 / 2^16)
+constexpr int kDrainChunks = 682;  // 43648 points x 3 products x 2^14 < 2^31: int32 headroom
+constexpr int kColmaxBlocks = 148 * 8;
 constexpr size_t kSmem = static_cast<size_t>(kRawStages) * kRawBytes + kSlStages * kSlBytes + 1024 + 512;  // + barriers
 
 struct I8Args {
@@ -322,7 +322,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // holds 4 d_0 d_0: weight / 4), type 1 = {1, 4}, type 2 = {2, 5}
     const double w0 = type == 0 ? 0.25 : (type == 1 ? 0x1p-8 : 0x1p-16);
     const double w1 = type == 0 ? 0x1p-24 : (type == 1 ? 0x1p-32 : 0x1p-40);
-    double* out = a.slab + (static_cast<int64_t>(cta) * kFeat + rowl) * 256 + half * 128;
+    // slab layout [column 256][row 128]: a warp's 32 lanes (rows) store 256 contiguous bytes
+    double* out = a.slab + static_cast<int64_t>(cta) * kFeat * 256 + half * 128 * kFeat + rowl;
     int rst = 0, sst = 0, since = 0, ndr = 0;
     uint32_t rph = 0, sph = 0, tph = 0;
     for (int c = 0; c < nchunks; ++c) {
@@ -412,7 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const double v = static_cast<double>(v0[i]) * w0 + static_cast<double>(v1[i]) * w1;
-            out[cc + i] = ndr == 0 ? v : out[cc + i] + v;
+            out[(cc + i) * kFeat] = ndr == 0 ? v : out[(cc + i) * kFeat] + v;
           }
         }
         ++ndr;
@@ -422,7 +423,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
     if (nchunks == 0 && ws < kDrainWarps)
-      for (int j2 = 0; j2 < 128; ++j2) out[j2] = 0.0;  // an empty group contributes zeros
+      for (int j2 = 0; j2 < 128; ++j2) out[j2 * kFeat] = 0.0;  // an empty group contributes zeros
     // |y| <= 2^30 by the exact column max; non-finite input is flagged by the pre-pass
   }
   tc_fence_before();
@@ -574,16 +575,17 @@ __global__ void __launch_bounds__(256) gram_i8_sym_kernel(int D, double* G) {
   }
 }
 
-// G = 2^(-k_i - k_j) sum over groups and pair types of the slabs (fixed order), S_X, s'.
-// Block = one row i of G, thread = column j: every slab row is read coalesced (2 KB), and the
-// 3 x ngroups loads of a thread are independent (memory-level parallelism).
+// G^T = 2^(-k_i - k_j) sum over groups and pair types of the slabs (fixed order), S_X, s'.
+// Block = slab column i, thread = feature row j: every slab column is read coalesced (1 KB per
+// CTA half), and the 3 x ngroups loads of a thread are independent (memory-level parallelism).
+// The transpose is immaterial: gram_i8_sym_kernel takes the symmetric part.
 __global__ void __launch_bounds__(256) gram_i8_reduce_kernel(I8Args a, double* G, double* SA, double* SB, double* s) {
   const int D = a.D;
   const int i = blockIdx.x, j = threadIdx.x;
   if (i < D && j < D) {
-    const int r = i / kFeat, row = i % kFeat;
+    const int r = j / kFeat, row = j % kFeat;
     const int64_t cstride = static_cast<int64_t>(kFeat) * 256;  // one CTA slab
-    const double* base = a.slab + static_cast<int64_t>(r) * cstride + static_cast<int64_t>(row) * 256 + j;
+    const double* base = a.slab + static_cast<int64_t>(r) * cstride + static_cast<int64_t>(i) * kFeat + row;
     double part[4] = {0.0, 0.0, 0.0, 0.0};  // fixed interleave over groups: deterministic
 #pragma unroll 4
     for (int g = 0; g < a.ngroups; ++g) {

@@ -123,16 +123,18 @@ def _i8_bound(A, B, shifted):
             + 2.0 ** -44 * np.outer(M, M)) * 1.05 + 1e-15 * (Y.T @ Y) / X.shape[0]
 
 
-@pytest.mark.parametrize("kind", ["gauss", "heavy", "unit", "offset", "ragged"])
+@pytest.mark.parametrize("kind", ["gauss", "heavy", "unit", "offset", "ragged", "windows"])
 def test_covariance_int8_path(ctx, kind):
     """Step 1a through prohd_covariance (the path prohd_estimate uses): the int8 tensor-core Gram
     for 128 < D <= 256, against the oracle's two-pass fp64 covariance (O3, oracle/prohd.py), within
     the fixed-point bound above; mu within 1e-12 of the scale."""
     from oracle import prohd as OP
-    rng = np.random.default_rng({"gauss": 1, "heavy": 2, "unit": 3, "offset": 4, "ragged": 5}[kind])
-    D = {"gauss": 256, "heavy": 256, "unit": 200, "offset": 160, "ragged": 132}[kind]
-    nA, nB = (40011, 35003) if kind != "ragged" else (1237, 70001)
-    if kind == "heavy":
+    rng = np.random.default_rng({"gauss": 1, "heavy": 2, "unit": 3, "offset": 4, "ragged": 5, "windows": 6}[kind])
+    D = {"gauss": 256, "heavy": 256, "unit": 200, "offset": 160, "ragged": 132, "windows": 256}[kind]
+    # "windows": > 682 chunks of 64 points per group (24 groups), so every TMEM accumulator is
+    # drained to the fp64 slabs mid-sweep and accumulated again
+    nA, nB = {"ragged": (1237, 70001), "windows": (560000, 560003)}.get(kind, (40011, 35003))
+    if kind in ("heavy", "windows"):
         A = (rng.standard_t(3, (nA, D)) * rng.uniform(0.1, 3, D)).astype(np.float32)
         B = (rng.standard_t(3, (nB, D)) * rng.uniform(0.1, 3, D) + 0.3).astype(np.float32)
     elif kind == "unit":
