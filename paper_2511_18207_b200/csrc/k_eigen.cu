@@ -190,9 +190,9 @@ __device__ void inverse_iteration(const double* d, const double* e, int D, doubl
 // per step j (buffers double-buffered on j & 1):
 //   B. every CTA holds column j (rows >= j, d_j at index j) in colbuf; each warp forms the
 //      norm, alpha and v = (x - alpha e1)/||.|| from it, the CTA computes p_r = 2 sum_c
-//      M[r][c] v_c for its rows r > j and scatters p_r, the PRE-update entry M[r][j+1] and
-//      its v.p partial into every CTA.                                      -> cluster barrier
-//   C. K = v.p, w = p - K v, M[r][c] -= v_r w_c + w_r v_c on its own rows, and every CTA
+//      M[r][c] v_c for its rows r > j and scatters (p_r, the PRE-update entry M[r][j+1]) as one
+//      16-byte store into every CTA.                                        -> cluster barrier
+//   C. K = v.p (from the full p), w = p - K v, M[r][c] -= v_r w_c + w_r v_c on its own rows, and every CTA
 //      forms the whole updated column j+1 itself, M[r][j+1] - (v_r w_{j+1} + w_r v_{j+1})
 //      (the same expression, so bit-identical to the owner's row), as step j+1's colbuf.
 // The second barrier of a scatter-the-updated-column scheme is gone; the scatter volume is the
@@ -205,9 +205,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
   extern __shared__ double dyn[];
   double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/kCl)*D])
   __shared__ double colbuf2[2][kMaxD];                 // column j (rows >= j) of step j: [j & 1]
-  __shared__ double pbuf2[2][kMaxD], cpre2[2][kMaxD];  // scattered p_r and pre-update M[r][j+1]
+  __shared__ double2 pc2[2][kMaxD];                    // scattered (p_r, pre-update M[r][j+1])
   __shared__ double vbuf[kMaxD], wbuf[kMaxD];          // v and w = p - K v of the current step
-  __shared__ double vpart2[2][kCl * kWarps];
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nloc = (D - rank + kCl - 1) / kCl;  // rows r = rank + kCl*i, i < nloc
@@ -227,9 +226,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
   for (int j = 0; j + 2 < D; ++j) {
     const int b = j & 1;
     const double* colbuf = colbuf2[b];
-    double* pbuf = pbuf2[b];
-    double* cpre = cpre2[b];
-    double* vpart = vpart2[b];
+    double2* pc = pc2[b];
     // B. every warp forms ||x||, alpha and the scale itself (no CTA barrier); v_c is
     // recomputed on the fly as vc(c) = (c == j+1 ? x0 - alpha : colbuf[c]) * sc
     double ss = 0.0;
@@ -244,13 +241,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
     // the update below is then a no-op and the next column comes out unchanged)
     const double sc = (vn2 > 0.0 && nrm > 0.0) ? 1.0 / sqrt(vn2) : 0.0;
     auto vc = [&](int c) { return (c == j + 1 ? v0 : colbuf[c]) * sc; };
-    if (rank == 0) {
-      if (tid == 0) {
-        dg[j] = colbuf[j];
-        eg[j] = (sc != 0.0) ? alpha : 0.0;
-      }
-      for (int c = j + 1 + tid; c < D; c += kT) a.V[static_cast<int64_t>(j) * D + c] = vc(c);
-    }
     // v once per CTA in shared memory (every warp formed the same scalars)
     for (int c = j + 1 + tid; c < D; c += kT) vbuf[c] = vc(c);
     __syncthreads();
@@ -273,28 +263,34 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int q = 0; q < kRW; ++q) ps[q] += __shfl_xor_sync(0xffffffffu, ps[q], o);
-    double vp = 0.0;
 #pragma unroll
     for (int q = 0; q < kRW; ++q) {
       const int i = warp + kWarps * q;
       const int r = rank + kCl * i;
-      if (i < nloc && r > j) {
-        const double pr = 2.0 * ps[q];
-        if (lane < kCl) {
-          *cl.map_shared_rank(&pbuf[r], lane) = pr;
-          *cl.map_shared_rank(&cpre[r], lane) = M[i * D + j + 1];
-        }
-        vp += pr * vbuf[r];
-      }
+      // one 16-byte DSMEM store per row and target CTA
+      if (i < nloc && r > j && lane < kCl)
+        *cl.map_shared_rank(&pc[r], lane) = make_double2(2.0 * ps[q], M[i * D + j + 1]);
     }
-    if (lane < kCl) *cl.map_shared_rank(&vpart[rank * kWarps + warp], lane) = vp;
-    cl.sync();
+    // split cluster barrier: the release covers the DSMEM stores above; this step's global
+    // outputs (d_j, e_j, Householder vector j) are stored between arrive and wait, so their
+    // latency is not on the barrier's path (the next step's release finds them long done)
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if (rank == 0) {
+      if (tid == 0) {
+        dg[j] = colbuf[j];
+        eg[j] = (sc != 0.0) ? alpha : 0.0;
+      }
+      for (int c = j + 1 + tid; c < D; c += kT) a.V[static_cast<int64_t>(j) * D + c] = vbuf[c];
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     // C. K = v.p; w = p - K v once per CTA; M[r][c] -= v_r w_c + w_r v_c on own rows; the
     // updated column j+1 (rows >= j+1) into the other colbuf
+    // K from the full p every CTA now holds (no partial sums to exchange); same order in every
+    // warp and CTA, so every copy of w is identical
     double K = 0.0;
-    for (int q = lane; q < kCl * kWarps; q += 32) K += vpart[q];
+    for (int c = j + 1 + lane; c < D; c += 32) K = fma(vbuf[c], pc[c].x, K);
     K = warp_sum(K);
-    for (int c = j + 1 + tid; c < D; c += kT) wbuf[c] = pbuf[c] - K * vbuf[c];
+    for (int c = j + 1 + tid; c < D; c += kT) wbuf[c] = pc[c].x - K * vbuf[c];
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kRW; ++q) {
@@ -308,7 +304,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
     {
       double* nxt = colbuf2[b ^ 1];
       const double vj = vbuf[j + 1], wj = wbuf[j + 1];
-      for (int r = j + 1 + tid; r < D; r += kT) nxt[r] = cpre[r] - fma(vbuf[r], wj, wbuf[r] * vj);
+      for (int r = j + 1 + tid; r < D; r += kT) nxt[r] = pc[r].y - fma(vbuf[r], wj, wbuf[r] * vj);
     }
     __syncthreads();
   }

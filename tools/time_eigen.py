@@ -1,5 +1,6 @@
 """Dev timing of K2 through prohd_directions on a prescribed spectrum; PROHD_OPT_EIG_STOP=1|2|3
-stops after tridiagonalisation | bisection | inverse iteration (timing prefixes)."""
+stops after tridiagonalisation | bisection | inverse iteration (timing prefixes).
+Optional arguments: D k (one case only)."""
 import os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -10,7 +11,8 @@ import torch
 from paper_2511_18207_b200 import Context
 ctx = Context(0)
 ctx.enable_timing(True)
-for D, k in [(64, 8), (128, 8), (256, 16), (256, 1)]:
+CASES = [(int(sys.argv[1]), int(sys.argv[2]))] if len(sys.argv) > 2 else [(64, 8), (128, 8), (256, 16), (256, 1)]
+for D, k in CASES:
     rng = np.random.default_rng(D)
     q, r = np.linalg.qr(rng.standard_normal((D, D)))
     lam = np.sort(rng.uniform(0.1, 10, D))[::-1]
