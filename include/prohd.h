@@ -95,6 +95,10 @@ int prohd_launch_count(int64_t* out);
  *   "eig_stop"      1|2|3: stop the eigen-solver after that stage (timing prefixes only)
  *   "eig_cl"        8: portable 8-CTA tridiagonalisation cluster
  *   "k1_ablate"     1|2: int8 Gram timing ablations (skip slicing / MMAs; WRONG results, dev only)
+ *   "k4_sampled"    0: radix K4 over all projections; 1: sampled-threshold K4 wherever it applies
+ *                   (default: sampled for n >= 262144, same selected indices either way);
+ *                   2|3: timing ablations of the fused K3 epilogue (no tests / no appends; the
+ *                   lists then fail certification and the radix K4 reruns)
  * value < 0 restores the default. PROHD_E_INVALID for an unknown name or NULL pointer. */
 int prohd_set_option(const char* name, int64_t value);
 int prohd_get_option(const char* name, int64_t* value);

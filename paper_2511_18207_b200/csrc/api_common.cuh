@@ -62,14 +62,14 @@ inline PFN_encodeTiled get_encode() {
 }
 
 inline bool make_tmap_2d(CUtensorMap* map, const float* base, int64_t rows, int Dp, int box_rows, char* err,
-                  size_t errlen, int box_inner = kBK) {
+                  size_t errlen, int box_inner = kBK, int64_t row_stride = 0) {
   PFN_encodeTiled enc = get_encode();
   if (enc == nullptr) {
     snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
     return false;
   }
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(Dp), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(Dp) * 4};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride > 0 ? row_stride : Dp) * 4};  // bytes, % 16 == 0
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,

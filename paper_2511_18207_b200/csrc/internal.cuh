@@ -31,6 +31,7 @@ enum OptId {
   OPT_EIG_STOP,      // stop K2 after stage 1|2|3 (timing prefixes)
   OPT_EIG_CL,        // 8: portable 8-CTA tridiagonalisation cluster
   OPT_K1_ABLATE,     // int8 Gram timing ablations (wrong results): 1 no slicing work, 2 no MMAs
+  OPT_K4_SAMPLED,    // 0 radix K4 over all projections, 1 sampled-threshold K4 wherever it applies
   OPT_COUNT
 };
 inline std::atomic<long long>* option_table() {
@@ -131,8 +132,8 @@ cudaError_t launch_nn64_from_key(const float* X, int64_t x_offset, int64_t nX, c
 constexpr int kNNBlocks = 592;  // 4 x 148 SMs
 
 // TMA descriptor for a row-major fp32 matrix [rows x Dp], box {box_inner, box_rows}, SWIZZLE_128B for
-// box_inner = 32 (128-B rows) and SWIZZLE_64B for box_inner = 16.
+// box_inner = 32 (128-B rows) and SWIZZLE_64B for box_inner = 16; row_stride in floats (0 = Dp).
 bool make_tmap_2d(CUtensorMap* map, const float* base, int64_t rows, int Dp, int box_rows, char* err, size_t errlen,
-                  int box_inner);
+                  int box_inner, int64_t row_stride);
 
 }  // namespace prohd

@@ -39,7 +39,9 @@
 //              tiles and accumulates ||x||^2 (fp32, halves combined by one shuffle per tile);
 //              fence.proxy.async, then one arrive per warp.
 //   warps 10-13 epilogue: tcgen05.ld of the 96 columns (row = point), pi_l = c_l + c_{32+l}
-//              + c_{64+l}, stored direction-major P32[l * n + p] (coalesced per l).
+//              + c_{64+l}, stored direction-major P32[l * n + p] (coalesced per l); or, with the
+//              sampled K4 (k_select.cu launch_select_sampled), (index, pi_l) appended to the
+//              list of every (direction, tail) whose sample threshold the point passes.
 // The directions are written once per CTA into shared memory in the UMMA K-major SWIZZLE_128B
 // layout: per K-chunk a 64-row tile, rows 0-31 uh and rows 32-63 ul (zero past L and D).
 #include "api_common.cuh"
@@ -81,7 +83,7 @@ __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
 
 __global__ void __launch_bounds__(kPThreads, 1)
     project_tc_kernel(const __grid_constant__ CUtensorMap tX, int64_t n, int D, const float* __restrict__ U32, int L,
-                      float* __restrict__ P32, unsigned* maxnorm2) {
+                      float* __restrict__ P32, unsigned* maxnorm2, ProjectFuse fz) {
   using namespace sm100;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -96,6 +98,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ unsigned bmax;
+  __shared__ float sthr[64];  // fused selection: per (direction, tail) sample threshold
+  __shared__ unsigned wcnt[4][64];  // fused selection: fill counts of the epilogue warps' slabs
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -111,6 +115,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const uint32_t piece = (((k >> 2) ^ (r & 7)) << 4) + (k & 3) * 4;  // (r + 32) & 7 == r & 7
     *reinterpret_cast<float*>(ubase + c * kUChunk + r * 128 + piece) = uh;
     *reinterpret_cast<float*>(ubase + c * kUChunk + (32 + r) * 128 + piece) = u - uh;
+  }
+  if (fz.state != nullptr) {
+    for (int i = threadIdx.x; i < 2 * L; i += blockDim.x) sthr[i] = __uint_as_float(fz.state[i * 4 + 0]);
+    for (int i = threadIdx.x; i < 4 * 64; i += blockDim.x) (&wcnt[0][0])[i] = 0u;
   }
   if (threadIdx.x == 0) {
     bmax = 0u;
@@ -242,6 +250,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
     int acc = 0;
     uint32_t aphase = 0;
+    const int slab = blockIdx.x * 4 + (warp - 10);  // fused selection: this warp's slab
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
@@ -251,17 +260,86 @@ __global__ void __launch_bounds__(kPThreads, 1)
       tmem_ld32(ta + 32, a1);
       tmem_ld32(ta + 64, a2);
       tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       const int64_t p = t * 128 + q * 32 + lane;
-      if (p < n) {
+      if (fz.state == nullptr) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (p < n) {
 #pragma unroll
-        for (int l = 0; l < 32; ++l)
-          if (l < L) P32[static_cast<int64_t>(l) * n + p] = (a0[l] + a1[l]) + a2[l];
+          for (int l = 0; l < 32; ++l)
+            if (l < L) P32[static_cast<int64_t>(l) * n + p] = (a0[l] + a1[l]) + a2[l];
+        }
+      } else {
+        // fused K4 pre-selection: (index, pi32) of every point beyond its list's sample
+        // threshold, appended to this warp's private slab of the list (P32 is not written).
+        // Pass 1 (unrolled, a few instructions per direction): the lists this lane's point
+        // enters, as bits of (lo, hi) = lists 0-31, 32-63. Pass 2 only if the warp has any: a
+        // rolled loop over the warp's lists that reloads the direction's three accumulator
+        // columns from TMEM (the accumulator is released after it), a ballot, the fill count
+        // (lane 0, shared memory) and the stores. Small executed code: the converters' loop
+        // keeps the instruction cache.
+        const bool ok = p < n;
+        unsigned bits_lo = 0, bits_hi = 0;
+        if (fz.ablate != 1) {
+#pragma unroll
+          for (int l = 0; l < 32; ++l)
+            if (l < L) {
+              const float v = (a0[l] + a1[l]) + a2[l];
+              const unsigned b2 = (ok && v >= sthr[2 * l] ? 1u : 0u) | (ok && v <= sthr[2 * l + 1] ? 2u : 0u);
+              if (2 * l < 32)
+                bits_lo |= b2 << (2 * l);
+              else
+                bits_hi |= b2 << (2 * l - 32);
+            }
+        }
+        const unsigned wlo = __reduce_or_sync(0xffffffffu, bits_lo), whi = __reduce_or_sync(0xffffffffu, bits_hi);
+        if ((wlo | whi) != 0u && fz.ablate != 2) {
+          unsigned* wc = wcnt[warp - 10];
+          const unsigned below = (1u << lane) - 1u;
+          const int64_t sbase = static_cast<int64_t>(slab) * 2 * L;
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            unsigned wb = half == 0 ? wlo : whi;
+            const unsigned mine = half == 0 ? bits_lo : bits_hi;
+#pragma unroll 1
+            while (wb != 0u) {
+              const int bit = __ffs(wb) - 1;
+              wb &= wb - 1u;
+              const int lt = 32 * half + bit, l = lt >> 1;
+              const bool pr = (mine >> bit) & 1u;
+              const unsigned bal = __ballot_sync(0xffffffffu, pr);
+              float c0, c1, c2;
+              asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=f"(c0) : "r"(ta + l));
+              asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=f"(c1) : "r"(ta + 32 + l));
+              asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=f"(c2) : "r"(ta + 64 + l));
+              tmem_wait_ld();
+              const float v = (c0 + c1) + c2;  // pass 1's value (same operations, same order)
+              unsigned base = 0;
+              if (lane == 0) {
+                base = wc[lt];
+                wc[lt] = base + __popc(bal);
+              }
+              base = __shfl_sync(0xffffffffu, base, 0);
+              const unsigned pos = base + __popc(bal & below);
+              if (pr && pos < static_cast<unsigned>(fz.capw)) {
+                const int64_t e = (sbase + lt) * fz.capw + pos;
+                fz.sidx[e] = static_cast<int>(p);
+                fz.sval[e] = v;
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
       }
       acc ^= 1;
       if (acc == 0) aphase ^= 1u;
+    }
+    if (fz.state != nullptr) {  // slab fill counts (may exceed capw: the filter then fails the list)
+      __syncwarp();
+      for (int i = lane; i < 2 * L; i += 32) fz.wcount[slab * 2 * L + i] = wcnt[warp - 10][i];
     }
   }
   tc_fence_before();
@@ -286,17 +364,19 @@ bool project_tc_supported(int64_t n, int D, int L) {
 }
 
 cudaError_t launch_project_tc(const float* X, int64_t n, int D, const float* U32, int L, float* P32,
-                              unsigned* maxnorm2, int num_sms, cudaStream_t st) {
+                              unsigned* maxnorm2, int num_sms, cudaStream_t st, const ProjectFuse* fuse,
+                              int64_t row_stride) {
   CUtensorMap map;
   char err[256];
-  if (!make_tmap_2d(&map, X, n, D, 128, err, sizeof(err))) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&map, X, n, D, 128, err, sizeof(err), kBK, row_stride)) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(project_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kPSmem));
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (n + 127) / 128;
   const int grid = static_cast<int>(ntiles < num_sms ? ntiles : num_sms);
   count_launch();
-  project_tc_kernel<<<grid, kPThreads, kPSmem, st>>>(map, n, D, U32, L, P32, maxnorm2);
+  project_tc_kernel<<<grid, kPThreads, kPSmem, st>>>(map, n, D, U32, L, P32, maxnorm2,
+                                                     fuse != nullptr ? *fuse : ProjectFuse{});
   return cudaGetLastError();
 }
 

@@ -25,6 +25,7 @@
 #include "prohd_kernels.cuh"
 
 #include <cfloat>
+#include <cmath>
 #include <cstdlib>
 
 namespace prohd {
@@ -387,6 +388,256 @@ __global__ void __launch_bounds__(256) collect_kernel(const float* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ K4, sampled-threshold variant
+// (launch_select_sampled). The radix select above reads all L n projections four times (three
+// histogram rounds and the collection). Here a sample of s rows fixes, per (direction, tail), a
+// threshold thr that about 5 m of the n points pass; K3's epilogue then appends (index, pi32) of
+// exactly those points (P32 is not written), and one CTA per list finds the m-th best value T
+// among them, CHECKS that the guard band [T - 2 eps, inf) lies inside [thr, inf) (then every
+// point of the band was appended, so T and the band are exactly those of the radix path) and
+// writes the band as the candidate list. A list that cannot be certified (fewer than m appended,
+// band not inside, raw buffer full) sets sfail and the caller reruns the radix path.
+
+// the rank-th largest key (1-based) among cnt keys key(v[i], tail) (top: order_key, bottom: its
+// complement), one block of kSelThreads threads, 1 <= rank <= cnt. Radix digits of
+// (key - min key) from the top bit of (max - min) down, 8 bits per round (adaptive: the values'
+// own key range, not the full float range, so the first round already spreads them); warp-private
+// histograms (shared atomics without return: a warp's clustered values serialise only within
+// the warp); warp 0 scans the 256 bins. v: shared memory or global (L2-resident) values; hbuf:
+// kSelHistWords words of (dynamic) shared memory.
+constexpr int kSelThreads = 1024;
+constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kSelBins = 256;
+constexpr int kSelHistWords = kSelWarps * kSelBins;
+__device__ unsigned block_select_key(const float* v, int64_t cnt, unsigned rank, int t, unsigned* hbuf) {
+  __shared__ unsigned tot[kSelBins];
+  __shared__ unsigned wmin[kSelWarps], wmax[kSelWarps];
+  __shared__ unsigned s_prefix, s_mask, s_rem;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  unsigned* hw = hbuf + w * kSelBins;
+  auto key = [&](int64_t i) {
+    const unsigned k0 = order_key(v[i]);
+    return t == 0 ? k0 : ~k0;
+  };
+  unsigned kmin = 0xFFFFFFFFu, kmax = 0u;
+  for (int64_t i = tid; i < cnt; i += kSelThreads) {
+    const unsigned k = key(i);
+    kmin = min(kmin, k);
+    kmax = max(kmax, k);
+  }
+  kmin = __reduce_min_sync(0xffffffffu, kmin);
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if (lane == 0) {
+    wmin[w] = kmin;
+    wmax[w] = kmax;
+  }
+  if (tid == 0) {
+    s_prefix = 0u;
+    s_mask = 0u;
+    s_rem = rank;
+  }
+  __syncthreads();
+  kmin = wmin[0];
+  kmax = wmax[0];
+  for (int i = 1; i < kSelWarps; ++i) {
+    kmin = min(kmin, wmin[i]);
+    kmax = max(kmax, wmax[i]);
+  }
+  int rb = 32 - __clz(kmax - kmin);  // bits left to resolve
+  while (rb > 0) {
+    const int shift = rb > 8 ? rb - 8 : 0;
+    const unsigned binmask = (1u << (rb - shift)) - 1u;
+    for (int b = lane; b < kSelBins; b += 32) hw[b] = 0u;
+    __syncwarp();
+    const unsigned prefix = s_prefix, mask = s_mask;
+    for (int64_t i = tid; i < cnt; i += kSelThreads) {
+      const unsigned d = key(i) - kmin;
+      if ((d & mask) == prefix) atomicAdd(&hw[(d >> shift) & binmask], 1u);
+    }
+    __syncthreads();
+    if (tid < kSelBins) {
+      unsigned c = 0;
+      for (int j = 0; j < kSelWarps; ++j) c += hbuf[j * kSelBins + tid];
+      tot[tid] = c;
+    }
+    __syncthreads();
+    if (w == 0) {  // descending: lane owns bins 255 - 8 lane .. 248 - 8 lane
+      unsigned hv[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        hv[j] = tot[kSelBins - 1 - (8 * lane + j)];
+        sum += hv[j];
+      }
+      unsigned inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const unsigned rem = s_rem;
+      unsigned cum = inc - sum;
+      int hit = -1;
+      unsigned cum_hit = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int pos = 8 * lane + j;  // descending position; bin = 255 - pos
+        if (hit < 0 && cum + hv[j] >= rem && kSelBins - 1 - pos <= static_cast<int>(binmask)) {
+          hit = pos;
+          cum_hit = cum;
+        }
+        cum += hv[j];
+      }
+      const unsigned hm = __ballot_sync(0xffffffffu, hit >= 0);
+      // rem <= the count of this round's candidates: some lane hits (bins above binmask are empty)
+      if (hm != 0u && lane == __ffs(hm) - 1) {
+        s_prefix = prefix | (static_cast<unsigned>(kSelBins - 1 - hit) << shift);
+        s_mask = mask | (binmask << shift);
+        s_rem = rem - cum_hit;
+      }
+    }
+    __syncthreads();
+    rb = shift;
+  }
+  return kmin + s_prefix;
+}
+
+constexpr int kSampleMax = 32768;  // sample rows (their projections staged in shared memory)
+constexpr int kFilterStage = 16384;  // appended entries per list (shared memory, values + indices)
+constexpr int kSlabCap = 64;         // entries per (epilogue warp, list) slab
+
+// stage cnt floats into shared memory: 8 independent loads in flight per thread (one block
+// streams from L2; a load-store loop would be one L2 latency per element)
+__device__ __forceinline__ void stage_floats(float* dst, const float* __restrict__ src, int64_t cnt) {
+  const int64_t nb = blockDim.x;
+  for (int64_t base = threadIdx.x; base < cnt; base += 8 * nb) {
+    float r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = base + k * nb < cnt ? __ldg(src + base + k * nb) : 0.0f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (base + k * nb < cnt) dst[base + k * nb] = r[k];
+  }
+  __syncthreads();
+}
+
+// per list lt = 2 l + tail: the threshold = the r-th best sample projection -> state[lt * 4 + 0]
+// (float bits), raw count state[lt * 4 + 1] = 0
+__global__ void __launch_bounds__(kSelThreads) sample_thresh_kernel(const float* __restrict__ S, int s, const int* n_dirs,
+                                                            unsigned r, unsigned* state) {
+  extern __shared__ float sv[];  // [s] values, then the selection histograms
+  const int lt = blockIdx.x, l = lt >> 1, t = lt & 1;
+  if (l >= *n_dirs) {  // a dropped direction: nothing passes (K3 appends nothing)
+    if (threadIdx.x == 0) {
+      state[lt * 4 + 0] = __float_as_uint(t == 0 ? __int_as_float(0x7f800000) : __int_as_float(0xff800000));
+      state[lt * 4 + 1] = 0u;
+    }
+    return;
+  }
+  stage_floats(sv, S + static_cast<int64_t>(l) * s, s);
+  const unsigned k = block_select_key(sv, s, r, t, reinterpret_cast<unsigned*>(sv + s));
+  if (threadIdx.x == 0) {
+    state[lt * 4 + 0] = __float_as_uint(key_to_float(t == 0 ? k : ~k));
+    state[lt * 4 + 1] = 0u;
+  }
+}
+
+// per list: the slabs' entries gathered into shared memory, T = the m-th best of them,
+// certification, the guard band as candidates (the same band as collect_kernel)
+__global__ void __launch_bounds__(kSelThreads) cand_filter_kernel(const int* n_dirs, const unsigned* __restrict__ state,
+                                                          const int* __restrict__ sidx, const float* __restrict__ sval,
+                                                          const unsigned* __restrict__ wcount, int nslabs, int L,
+                                                          int capw, int64_t m, const unsigned* maxnorm2,
+                                                          double eps_coef, int* cand, unsigned* ccount, int64_t cap,
+                                                          int* overflow, int* sfail) {
+  extern __shared__ float sv[];
+  int* si = reinterpret_cast<int*>(sv + kFilterStage);
+  __shared__ unsigned wsum[kSelWarps];
+  const int lt = blockIdx.x, l = lt >> 1, t = lt & 1;
+  if (l >= *n_dirs) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  int mybad = 0;
+  // slabs [tid * per, (tid + 1) * per) (per <= 4): counts, exclusive block scan of the totals
+  const int per = (nslabs + kSelThreads - 1) / kSelThreads;
+  unsigned cs[4];
+  unsigned tot = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int sl = tid * per + j;
+    cs[j] = (j < per && sl < nslabs) ? __ldg(wcount + static_cast<int64_t>(sl) * 2 * L + lt) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (cs[j] > static_cast<unsigned>(capw)) mybad = 1;
+    tot += cs[j];
+  }
+  unsigned inc = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[w] = inc;
+  const int bad = __syncthreads_or(mybad);
+  unsigned off = inc - tot;
+  for (int i = 0; i < w; ++i) off += wsum[i];
+  unsigned total = 0;
+  for (int i = 0; i < kSelWarps; ++i) total += wsum[i];
+  if (bad || total > static_cast<unsigned>(kFilterStage) || total < m) {
+    if (tid == 0) atomicOr(sfail, 1);
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int sl = tid * per + j;
+    const unsigned c = cs[j];
+    const int64_t e0 = (static_cast<int64_t>(sl) * 2 * L + lt) * capw;
+    for (unsigned k0 = 0; k0 < c; k0 += 8) {  // 16 independent loads in flight
+      float rv[8];
+      int ri[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        rv[k] = k0 + k < c ? __ldg(sval + e0 + k0 + k) : 0.0f;
+        ri[k] = k0 + k < c ? __ldg(sidx + e0 + k0 + k) : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k0 + k < c) {
+          sv[off + k0 + k] = rv[k];
+          si[off + k0 + k] = ri[k];
+        }
+    }
+    off += c;
+  }
+  __syncthreads();
+  const unsigned key = block_select_key(sv, total, static_cast<unsigned>(m), t,
+                                        reinterpret_cast<unsigned*>(si + kFilterStage));
+  const double T = static_cast<double>(key_to_float(t == 0 ? key : ~key));
+  const double thr = static_cast<double>(__uint_as_float(state[lt * 4 + 0]));
+  const double eps = eps_coef * sqrt(static_cast<double>(__uint_as_float(*maxnorm2))) * 1.0625;
+  const double lo = T - 2.0 * eps, hi = T + 2.0 * eps;
+  if (!(t == 0 ? lo >= thr : hi <= thr)) {  // the band reaches past the threshold (or NaN)
+    if (tid == 0) atomicOr(sfail, 1);
+    return;
+  }
+  for (unsigned base = 0; base < total; base += blockDim.x) {
+    const unsigned i = base + tid;
+    const double x = i < total ? static_cast<double>(sv[i]) : 0.0;
+    const bool keep = i < total && (t == 0 ? x >= lo : x <= hi);
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (bal == 0u) continue;
+    unsigned pos0 = 0;
+    if (lane == 0) pos0 = atomicAdd(&ccount[lt], static_cast<unsigned>(__popc(bal)));
+    pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+    const unsigned pos = pos0 + __popc(bal & ((1u << lane) - 1u));
+    if (keep) {
+      if (pos < cap)
+        cand[static_cast<int64_t>(lt) * cap + pos] = si[i];
+      else
+        *overflow = 1;
+    }
+  }
+}
+
 // fp64 projection of every candidate: one warp per candidate
 __global__ void __launch_bounds__(256) cand_p64_kernel(const float* __restrict__ X, int D,
                                                        const double* __restrict__ U64, int L, const int* n_dirs,
@@ -436,25 +687,32 @@ __global__ void __launch_bounds__(256) rank_kernel(int L, const int* n_dirs, con
     }
     __syncthreads();
   }
-  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < cnt;
-       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double v = staged ? sv[c] : cv[c];
-    const int i = staged ? si[c] : ci[c];
+  // four lanes per candidate, each counting over a quarter of the list (warp-uniform trip
+  // counts: the loop runs to the warp's largest candidate slot, extra slots count nothing)
+  const int q = threadIdx.x & 3;
+  const int64_t per_pass = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 2);
+  for (int64_t c0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 2); c0 < cnt; c0 += per_pass) {
+    const int64_t c = c0 + (threadIdx.x >> 2);
+    const bool live = c < cnt;
+    const double v = live ? (staged ? sv[c] : cv[c]) : 0.0;
+    const int i = live ? (staged ? si[c] : ci[c]) : 0;
     int64_t rank = 0;
     if (staged) {
-      for (int o = 0; o < static_cast<int>(cnt); ++o) {
+      for (int o = q; o < static_cast<int>(cnt); o += 4) {
         const double w = sv[o];
         const int j = si[o];
         rank += ((t == 0) ? (w > v || (w == v && j < i)) : (w < v || (w == v && j < i))) ? 1 : 0;
       }
     } else {
-      for (int64_t o = 0; o < cnt; ++o) {
+      for (int64_t o = q; o < cnt; o += 4) {
         const double w = cv[o];
         const int j = ci[o];
         rank += ((t == 0) ? (w > v || (w == v && j < i)) : (w < v || (w == v && j < i))) ? 1 : 0;
       }
     }
-    if (rank < m) {
+    rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+    rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+    if (live && q == 0 && rank < m) {
       if (lists != nullptr) lists[static_cast<int64_t>(lt) * m + rank] = i;
       if (bitmap != nullptr) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
       if (cv_out != nullptr) {
@@ -835,7 +1093,7 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
   count_launch();
   cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
   count_launch();
-  rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap,
+  rank_kernel<<<dim3(32, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap,
                                               nullptr, nullptr, 0, nullptr);
   // K5
   if (last) {
@@ -844,6 +1102,96 @@ cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, c
     count_launch();
     compact_write_kernel<<<kCB, 256, 0, st>>>(b.bitmap, (n + 31) / 32, b.ucount + 1, b.uidx, b.ucount);
   }
+  return cudaGetLastError();
+}
+
+bool select_sampled_plan(int64_t n, int D, int L, int64_t m, int* s_out, unsigned* r_out) {
+  const long long o = opt(OPT_K4_SAMPLED);
+  if (o == 0 || (o < 0 && n < 262144)) return false;
+  if (!project_tc_supported(n, D, L) || m < 1 || 2 * m >= n) return false;
+  const int s = static_cast<int>(n < kSampleMax ? n : kSampleMax);
+  // about mu of the s sample points lie beyond the true m-th value; the r-th best sample value
+  // is then passed by ~(r / mu) m points (r / mu ~ 3.5 at cfg5, 2.4 at cfg2), and by fewer than
+  // m only if the sample holds r >= 2 mu + 4 sqrt(mu) + 8 points beyond the m-th value (Poisson
+  // tail < 1e-13 for mu >= 16); the filter certifies every list anyway
+  const double mu = static_cast<double>(s) * static_cast<double>(m) / static_cast<double>(n);
+  const double r = std::ceil(2.0 * mu + 4.0 * std::sqrt(mu)) + 8.0;
+  if (r > s / 8) return false;  // not a tail: the radix path
+  // about r n / s points pass the threshold: they must fit the filter's shared-memory stage
+  if (r * static_cast<double>(n / s) > kFilterStage / 2) return false;
+  *s_out = s;
+  *r_out = static_cast<unsigned>(r);
+  return true;
+}
+
+cudaError_t launch_select_sampled(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
+                                  const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st,
+                                  double* eps_out, bool* used) {
+  *used = false;
+  int s = 0;
+  unsigned r = 0;
+  if (b.sfail == nullptr || !select_sampled_plan(n, D, L, m, &s, &r)) return cudaSuccess;
+  int sms = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                cudaSuccess || sms <= 0)
+    sms = 148;
+  // the appended slabs and the sample projections live in the P32 buffer (L n floats), which this
+  // path does not otherwise use: per epilogue warp (4 per K3 CTA) and list kSlabCap indices and
+  // values, then the fill counts
+  const int64_t ntiles = (n + 127) / 128;
+  // K3 CTAs: one per SM, fewer for small n so that the slabs fit the buffer (sample-size tests)
+  int64_t ctas = ntiles < sms ? ntiles : sms;
+  const int64_t fit = static_cast<int64_t>(L) * n / (8 * L * (2 * kSlabCap + 1));
+  if (ctas > fit) ctas = fit;
+  if (ctas > 1024) ctas = 1024;  // cand_filter_kernel: <= 4 slabs per thread
+  if (ctas < 1) return cudaSuccess;
+  const int nslabs = 4 * static_cast<int>(ctas);
+  *used = true;
+  ProjectFuse fz;
+  fz.state = b.state;
+  fz.capw = kSlabCap;
+  fz.ablate = opt(OPT_K4_SAMPLED) >= 2 ? static_cast<int>(opt(OPT_K4_SAMPLED)) - 1 : 0;
+  fz.sidx = reinterpret_cast<int*>(b.P32);
+  fz.sval = b.P32 + static_cast<int64_t>(nslabs) * 2 * L * kSlabCap;
+  fz.wcount = reinterpret_cast<unsigned*>(b.P32 + static_cast<int64_t>(nslabs) * 2 * L * kSlabCap * 2);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(b.maxnorm2, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.bitmap, 0, sizeof(unsigned) * ((n + 31) / 32), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.overflow, 0, sizeof(int), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.sfail, 0, sizeof(int), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.ccount, 0, sizeof(unsigned) * 2 * L, st)) != cudaSuccess) return e;
+  // sample projections: K3 itself on rows 0, step, 2 step, ... (a strided TMA view), into the
+  // P32 buffer (consumed by sample_thresh_kernel before K3 proper writes the raw lists there)
+  const int64_t step = n / s;
+  float* S = b.P32;
+  if ((e = launch_project_tc(X, s, D, U32, L, S, b.maxnorm2, sms, st, nullptr, step * D)) != cudaSuccess) return e;
+  const size_t tsmem = sizeof(float) * static_cast<size_t>(s) + sizeof(unsigned) * kSelHistWords;
+  const size_t fsmem = (sizeof(float) + sizeof(int)) * static_cast<size_t>(kFilterStage) +
+                       sizeof(unsigned) * kSelHistWords;
+  if ((e = cudaFuncSetAttribute(sample_thresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(tsmem))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(cand_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(fsmem))) != cudaSuccess)
+    return e;
+  count_launch();
+  sample_thresh_kernel<<<2 * L, kSelThreads, tsmem, st>>>(S, s, n_dirs, r, b.state);
+  const double eps_coef = project_tc_eps_coef(D);
+  if (eps_out != nullptr) *eps_out = eps_coef;
+  if ((e = launch_project_tc(X, n, D, U32, L, b.P32, b.maxnorm2, static_cast<int>(ctas), st, &fz)) != cudaSuccess)
+    return e;
+  count_launch();
+  cand_filter_kernel<<<2 * L, kSelThreads, fsmem, st>>>(n_dirs, b.state, fz.sidx, fz.sval, fz.wcount, nslabs, L, kSlabCap,
+                                                m, b.maxnorm2, eps_coef, b.cand, b.ccount, b.cap, b.overflow,
+                                                b.sfail);
+  count_launch();
+  cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
+  count_launch();
+  rank_kernel<<<dim3(32, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap,
+                                              nullptr, nullptr, 0, nullptr);
+  count_launch();
+  compact_count_kernel<<<kCB, 256, 0, st>>>(b.bitmap, (n + 31) / 32, b.ucount + 1);
+  count_launch();
+  compact_write_kernel<<<kCB, 256, 0, st>>>(b.bitmap, (n + 31) / 32, b.ucount + 1, b.uidx, b.ucount);
   return cudaGetLastError();
 }
 
@@ -874,10 +1222,10 @@ cudaError_t launch_select_fallback(const float* X, int64_t n, int D, const doubl
   const unsigned* redo = b.hist + 2 * L * 256 + 2 * L * 4;
   count_launch();
   if (cval_out != nullptr)
-    rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, nullptr, nullptr,
+    rank_kernel<<<dim3(32, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, nullptr, nullptr,
                                                 cval_out, cidx_out, row_offset, redo);
   else
-    rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap,
+    rank_kernel<<<dim3(32, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, b.lists, b.bitmap,
                                                 nullptr, nullptr, 0, redo);
   if (compact) {
     count_launch();
@@ -928,7 +1276,7 @@ cudaError_t launch_local_candidates(const float* X, int64_t n, int64_t row_offse
   count_launch();
   cand_p64_kernel<<<dim3(16, 2 * L), 256, 0, st>>>(X, D, U64, L, n_dirs, b.cand, b.ccount, b.cap, b.cval);
   count_launch();
-  rank_kernel<<<dim3(8, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, nullptr, nullptr,
+  rank_kernel<<<dim3(32, 2 * L), 256, 0, st>>>(L, n_dirs, b.cand, b.cval, b.ccount, b.cap, m, nullptr, nullptr,
                                               cval_out, cidx_out, row_offset, nullptr);
   return cudaGetLastError();
 }

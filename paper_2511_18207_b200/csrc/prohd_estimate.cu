@@ -57,6 +57,7 @@ static void carve_select(Carver& c, SelectBufs& b, int64_t n, int L, int64_t m) 
   b.uidx = c.take<long long>(capU > n ? n : (2 * m >= n ? n : capU));
   b.ucount = c.take<unsigned>(1 + kCompactBlocks);  // count, then compaction scratch
   b.overflow = c.take<int>(1);
+  b.sfail = c.take<int>(1);
 }
 
 static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int k, int64_t m, bool host_inputs,
@@ -189,7 +190,11 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   unsigned maxn[2];
   unsigned i8ovf = 0;
   double eps[2] = {0.0, 0.0};
+  bool sampled[2] = {false, false};
+  int64_t msel[2] = {m, m};
+  int sfail[2] = {0, 0};
   auto select_and_read = [&]() -> int {
+    sampled[0] = sampled[1] = false;
     const int t_sel = tmark(ctx);
     // set B's chain runs on the context's second stream, set A's on the caller's: the low-occupancy
     // tail of one set's selection (collect, re-rank, compaction) overlaps the other's projection
@@ -217,8 +222,17 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
           if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, 1, b, sst)) != cudaSuccess) return e;
           if ((e = launch_iota(b.uidx, b.ucount, n[s], sst)) != cudaSuccess) return e;
         } else if (m0 == m1 || L == 1) {
-          if ((e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst, true, true, &eps[s])) !=
+          // sampled-threshold K4 where it applies (certification failures rerun the radix path
+          // after the host sync below), else the radix K4
+          bool used = false;
+          if ((e = launch_select_sampled(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst, &eps[s], &used)) !=
               cudaSuccess)
+            return e;
+          sampled[s] = used;
+          msel[s] = m0;
+          if (!used &&
+              (e = launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, m0, b, sst, true, true, &eps[s])) !=
+                  cudaSuccess)
             return e;
         } else {  // two direction groups with different per-tail counts, one shared union bitmap
           // the groups share the projection buffer, so each group's overflow fallback runs right
@@ -251,7 +265,23 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
     CK(cudaMemcpyAsync(&maxn[1], w.sel[1].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&ndirs, w.n_dirs, sizeof(int), cudaMemcpyDeviceToHost, st));
     if (use_i8) CK(cudaMemcpyAsync(&i8ovf, w.mom.i8ovf, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    for (int s = 0; s < 2; ++s) {
+      sfail[s] = 0;
+      if (sampled[s]) CK(cudaMemcpyAsync(&sfail[s], w.sel[s].sfail, sizeof(int), cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaStreamSynchronize(st));
+    if (sfail[0] || sfail[1]) {
+      // a sampled threshold could not be certified for some list (ties or a sample far off the
+      // tail): the radix K4 for that set, from the projections again
+      for (int s = 0; s < 2; ++s) {
+        if (!sfail[s]) continue;
+        CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, msel[s], w.sel[s], st, true, true, &eps[s]));
+        CK(cudaMemcpyAsync(&ucount[s], w.sel[s].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&ovf[s], w.sel[s].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&maxn[s], w.sel[s].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      }
+      CK(cudaStreamSynchronize(st));
+    }
     return PROHD_OK;
   };
   if ((rc = select_and_read())) return rc;

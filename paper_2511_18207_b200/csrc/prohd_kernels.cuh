@@ -106,14 +106,29 @@ struct SelectBufs {
   unsigned* ucount;       // union size, then kCompactBlocks words of compaction scratch
   int* overflow;          // guard-band overflow flag
   int64_t cap;            // candidates per list
+  int* sfail = nullptr;   // sampled K4 could not certify a list: rerun launch_select (nullptr: no sampled K4)
 };
 // first: reset the union bitmap/flags; last: compact the bitmap into the sorted union. Two calls
 // (first=true,last=false then first=false,last=true) select with different m per direction group.
 // K3 on the tensor cores (k_project_tc.cu): D % 4 == 0, D <= 256, 1 <= L <= 32
 bool project_tc_supported(int64_t n, int D, int L);
 double project_tc_eps_coef(int D);  // |pi32 - pi64| <= coef * ||x||
+// fused pre-selection in K3's epilogue (sampled K4): state[lt * 4 + 0] = float bits of the
+// threshold of list lt = 2 l + tail (top: pi >= thr, bottom: pi <= thr); every epilogue warp w
+// (= 4 CTA + warp, 4 per CTA) appends (index, pi32) to its private slab sidx / sval
+// [w][2L][capw] and stores its fill counts wcount[w][2L] (possibly > capw) at the end
+struct ProjectFuse {
+  const unsigned* state = nullptr;
+  int* sidx = nullptr;
+  float* sval = nullptr;
+  unsigned* wcount = nullptr;
+  int capw = 0;
+  int ablate = 0;  // dev timing only (option k4_sampled 2 | 3): 1 no tests, 2 no appends
+};
+// row_stride (floats, 0 = D): rows of X at that pitch (the sampled K4 projects every (n/s)-th row)
 cudaError_t launch_project_tc(const float* X, int64_t n, int D, const float* U32, int L, float* P32,
-                              unsigned* maxnorm2, int num_sms, cudaStream_t st);
+                              unsigned* maxnorm2, int num_sms, cudaStream_t st, const ProjectFuse* fuse = nullptr,
+                              int64_t row_stride = 0);
 // K3 dispatch (tensor-core kernel, else SIMT): P32 = direction-major projections, atomicMax of
 // max ||x||^2 bits into *maxnorm2 (zeroed by the caller); *eps_coef: |pi32 - pi64| <= coef ||x||
 cudaError_t launch_project(const float* X, int64_t n, int D, const float* U32, int L, float* P32,
@@ -121,6 +136,14 @@ cudaError_t launch_project(const float* X, int64_t n, int D, const float* U32, i
 cudaError_t launch_select(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
                           const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st, bool first = true,
                           bool last = true, double* eps_out = nullptr);
+// K4 with a sampled threshold and K3's fused pre-selection (k_select.cu): the same candidate
+// lists, union and bitmap as launch_select (first = last = true) for one direction group; *used
+// = false (nothing launched) where it does not apply (option k4_sampled, n, m, K3 variant, or
+// b.sfail == nullptr). A list it cannot certify sets *b.sfail: rerun launch_select.
+bool select_sampled_plan(int64_t n, int D, int L, int64_t m, int* s_out, unsigned* r_out);
+cudaError_t launch_select_sampled(const float* X, int64_t n, int D, const double* U64, const float* U32, int L,
+                                  const int* n_dirs, int64_t m, const SelectBufs& b, cudaStream_t st,
+                                  double* eps_out, bool* used);
 // K4 fallback for lists whose guard band overflowed the candidate buffer (ccount > cap after
 // launch_select / launch_local_candidates): exact streaming radix select on (fp64 projection,
 // index), then the usual ranking into lists + bitmap (and the compaction if `compact`), or into

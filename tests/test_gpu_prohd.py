@@ -337,3 +337,59 @@ def test_guard_band_overflow_exact_ties(ctx):
         idxs.append(i)
     union = ctx.merge_union(torch.stack(vals), torch.stack(idxs), m, n).cpu().numpy()
     assert np.array_equal(union, ref["IA"])
+
+
+@pytest.mark.parametrize("cfg,n", [(2, 20000), (3, 65536), (5, 65536)])
+def test_sampled_select_layers(ctx, cfg, n):
+    """K4 with a sampled threshold and K3's fused pre-selection (k_select.cu
+    launch_select_sampled; the default from n = 262,144 on), forced at the reduced sizes: the
+    same L2-L5 layers as the radix K4 (exact unions)."""
+    from paper_2511_18207_b200 import option
+    c = datagen.CONFIGS[cfg]
+    A, B = datagen.generate(cfg, n=n)
+    with option("k4_sampled", 1):
+        g, ref, inj = _check_layers(ctx, A, B, c.k, c.m(n))
+    if np.array_equal(g["IA"], ref["IA"]) and np.array_equal(g["IB"], ref["IB"]):
+        assert abs(g["value"] - ref["value"]) <= 1e-4 * ref["value"]
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_sampled_equals_radix(ctx, cfg):
+    """At 300,000 points per set (sampled K4 by default) the selected unions, the estimate and its
+    witnesses are identical to the radix K4's (option k4_sampled 0): the certified band is the
+    radix path's band (same m-th value T, same eps), so the candidate set is the same."""
+    from paper_2511_18207_b200 import option
+    c = datagen.CONFIGS[cfg]
+    n = 300_000
+    A, B = datagen.generate(cfg, n=n)
+    m = c.m(n)
+    tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    g1 = ctx.prohd_estimate(tA, tB, c.k, m, return_dirs=True, return_indices=True)
+    with option("k4_sampled", 0):
+        g0 = ctx.prohd_estimate(tA, tB, c.k, m, return_dirs=True, return_indices=True)
+    assert np.array_equal(g0["U"], g1["U"])
+    assert np.array_equal(g0["IA"], g1["IA"]) and np.array_equal(g0["IB"], g1["IB"])
+    assert g0["value"] == g1["value"]
+    for side in ("ab", "ba"):
+        assert (g0[side]["a"], g0[side]["b"]) == (g1[side]["a"], g1[side]["b"])
+
+
+def test_sampled_select_uncertified_reruns(ctx):
+    """Lists the sampled K4 cannot certify: 50,000 exact duplicates of the m-th value on e1's top
+    tail (and on e2's bottom tail), so the sample threshold IS the m-th value T and the guard band
+    [T - 2 eps, inf) reaches below it (within the raw capacity, so this is the certification check,
+    not an overflow). The radix rerun gives the oracle's lists; so does the radix K4 alone."""
+    from paper_2511_18207_b200 import option
+    n, D, m = 300_000, 16, 1000
+    A = _tied_cloud(n, D, 50_000, 5)
+    B = _tied_cloud(n, D, 50_000, 6)
+    U = np.zeros((D, 3))
+    U[0, 0] = 1.0
+    U[1, 1] = 1.0
+    U[2:, 2] = 1.0 / np.sqrt(D - 2)
+    ref = OP.estimate(A, B, 2, m, U=U)
+    for opt in (1, 0):
+        with option("k4_sampled", opt):
+            g = ctx.prohd_estimate_with_dirs(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), U, m)
+        assert np.array_equal(g["IA"], ref["IA"]) and np.array_equal(g["IB"], ref["IB"])
+        assert abs(g["value"] - ref["value"]) <= 1e-4 * ref["value"]

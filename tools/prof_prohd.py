@@ -1,6 +1,9 @@
 """ncu target: one prohd_estimate at cfg5 (n=2M, D=256, k=16, m=1000)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _opts  # noqa: E402
+_opts.apply_env()
 import torch
 import datagen
 from paper_2511_18207_b200 import Context
