@@ -88,7 +88,8 @@ int prohd_launch_count(int64_t* out);
  *   "k6_split3"     1: literal 3xTF32 distance products (three TF32 MMAs on fp32 hi/lo)
  *   "k6_bidir_2a"   1: fused bidirectional sweep on the two-A kernel
  *   "k6_splits_2x"  1: the earlier fill-twice column-split rule
- *   "k1_path"       0 fp64 DMMA Gram, 1 int8 tcgen05 Gram, 2 legacy tile moments kernel
+ *   "k1_path"       0 fp64 DMMA Gram, 1 int8 tcgen05 Gram (the default for D <= 256, D % 4 == 0),
+ *                   2 legacy tile moments kernel
  *   "k1_ctas", "k1_cs_sms", "k1_beta_milli"   Gram scheduling knobs
  *   "shift"         0 never / 1 always shift the Gram by the sample mean
  *   "k3_simt"       1: SIMT projection kernel instead of tcgen05
@@ -99,6 +100,7 @@ int prohd_launch_count(int64_t* out);
  *                   (default: sampled for n >= 262144, same selected indices either way);
  *                   2|3: timing ablations of the fused K3 epilogue (no tests / no appends; the
  *                   lists then fail certification and the radix K4 reruns)
+ *   "k1_i8_ctas"    n > 0: at most n CTAs in the int8 Gram (tests force mid-sweep drains with it)
  * value < 0 restores the default. PROHD_E_INVALID for an unknown name or NULL pointer. */
 int prohd_set_option(const char* name, int64_t value);
 int prohd_get_option(const char* name, int64_t* value);
@@ -164,7 +166,7 @@ int hausdorff_minima(prohd_ctx* ctx, const float* A, int64_t nA, const float* B,
 /* Test hook: step 1a of prohd_estimate alone -- the mean mu of A u B and
  * the covariance C = (1/N) sum (p - mu)(p - mu)^T (Alg. 2 lines 1-2) as the
  * library computes them for the directions, through the same Gram path (int8 tensor cores for
- * 128 < D <= 256 with D % 4 == 0 unless option k1_path = 0, else fp64 DMMA; the int8 pass falls
+ * D <= 256 with D % 4 == 0 unless option k1_path = 0, else fp64 DMMA; the int8 pass falls
  * back to DMMA when a value leaves its sampled fixed-point range). mu_out (HOST, D), C_out (HOST,
  * D x D row-major), *path_out (HOST) = 1 if the int8 Gram produced C, 0 if the DMMA Gram did.
  * Workspace: prohd_workspace_bytes(nA, nB, D, 0, 1, flags). Errors as prohd_estimate. */
@@ -277,7 +279,8 @@ int directed_hd_witness(prohd_ctx* ctx, const float* a, const float* B, int64_t 
  * Alg. 3 with the rows of A and of B split across ranks. The caller
  * (paper_2511_18207_b200/dist.py) runs the collectives between the calls:
  *   s = prohd_shift(rank 0's first rows)            -> broadcast s
- *   prohd_local_moments(own rows, s)                -> all_reduce(SUM)      (C1)
+ *   prohd_local_colmax(own rows, s)                 -> all_reduce(MAX)      (C0, int8 Gram)
+ *   prohd_local_moments[_i8](own rows, s[, colmax]) -> all_reduce(SUM)      (C1)
  *   prohd_directions(reduced moments)               (replicated, deterministic)
  *   prohd_local_candidates(own rows, global offset) -> all_gather           (C2)
  *   prohd_merge_union(all lists)                    (replicated)
@@ -299,6 +302,22 @@ int prohd_shift(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int6
  * (full, row-major). n_local may be 0. */
 int prohd_local_moments(prohd_ctx* ctx, const float* A_local, int64_t nA_local, const float* B_local,
                         int64_t nB_local, int32_t D, const double* shift, double* moments_out);
+/* The same moments on the int8 tensor cores (the Gram prohd_estimate uses, k_gram_i8.cu), in two
+ * calls around one MAX all-reduce so that every rank quantises on the same fixed-point grid
+ * (Alg. 2 lines 1-2; SURVEY.md §8(e) "shard the Gram and centroid sums"):
+ *   prohd_local_colmax: colmax_out (DEVICE, D fp32) = max over own A and B rows of |x_f - s_f|
+ *     (+inf for non-finite input; 0 without rows)                 -> all_reduce(MAX)
+ *   prohd_local_moments_i8: moments_out (DEVICE, 2D + D*D fp64) exactly as prohd_local_moments,
+ *     from the int8 Gram on the grid of colmax (DEVICE, D fp32, the all-reduced maxima), re-expressed
+ *     about s. A non-finite colmax entry selects the fp64 DMMA Gram (whose sums then carry the
+ *     non-finite value to prohd_directions: PROHD_E_DATA there).
+ * Both need D <= 256 and D % 4 == 0 (else PROHD_E_NOTIMPL: use prohd_local_moments); shift is
+ * HOST (D fp64, the broadcast prohd_shift). n_local may be 0. Blocking. */
+int prohd_local_colmax(prohd_ctx* ctx, const float* A_local, int64_t nA_local, const float* B_local,
+                       int64_t nB_local, int32_t D, const double* shift, float* colmax_out);
+int prohd_local_moments_i8(prohd_ctx* ctx, const float* A_local, int64_t nA_local, const float* B_local,
+                           int64_t nB_local, int32_t D, const double* shift, const float* colmax,
+                           double* moments_out);
 /* Directions from the all-reduced moments (DEVICE) of nA + nB points: dirs_out (DEVICE,
  * (k+1) x D fp64, row l = direction l, row 0 = centroid axis), *n_dirs_out (HOST). */
 int prohd_directions(prohd_ctx* ctx, const double* moments, int64_t nA, int64_t nB, int32_t D, int32_t k,

@@ -32,7 +32,8 @@ EXPORTED = [
     "prohd_estimate_with_dirs", "prohd_bounds", "directed_hd_local", "prohd_centre", "directed_hd_witness",
     "prohd_project",
     "prohd_enable_timing", "prohd_last_timings",
-    "prohd_shard_workspace_bytes", "prohd_shift", "prohd_local_moments", "prohd_directions",
+    "prohd_shard_workspace_bytes", "prohd_shift", "prohd_local_moments", "prohd_local_colmax",
+    "prohd_local_moments_i8", "prohd_directions",
     "prohd_local_candidates", "prohd_merge_union", "prohd_gather_owned",
 ]
 
@@ -103,6 +104,8 @@ def load() -> C.CDLL:
     lib.prohd_shard_workspace_bytes.restype = C.c_size_t
     lib.prohd_shift.argtypes = [vp, vp, i64, vp, i64, i32, vp]
     lib.prohd_local_moments.argtypes = [vp, vp, i64, vp, i64, i32, vp, vp]
+    lib.prohd_local_colmax.argtypes = [vp, vp, i64, vp, i64, i32, vp, vp]
+    lib.prohd_local_moments_i8.argtypes = [vp, vp, i64, vp, i64, i32, vp, vp, vp]
     lib.prohd_directions.argtypes = [vp, vp, i64, i64, i32, i32, vp, vp, C.POINTER(C.c_int32)]
     lib.prohd_local_candidates.argtypes = [vp, vp, i64, i64, i32, vp, i32, i64, vp, vp]
     lib.prohd_merge_union.argtypes = [vp, vp, vp, i32, i32, i64, i64, vp, C.POINTER(C.c_int64)]

@@ -328,6 +328,32 @@ class Context:
                                                  s.ctypes.data, out.data_ptr()))
         return out
 
+    def local_colmax(self, A_local, B_local, shift: np.ndarray) -> torch.Tensor:
+        """prohd_local_colmax: per-feature max |x - s| of this rank's rows (device fp32, D)."""
+        A, B = _as_points(A_local, "A"), _as_points(B_local, "B")
+        D = A.shape[1]
+        self._shard_ws(max(A.shape[0], B.shape[0]), 1, D, 0, 1)
+        s = np.ascontiguousarray(shift, dtype=np.float64)
+        out = torch.empty(D, dtype=torch.float32, device=f"cuda:{self.device}")
+        self._check(self.lib.prohd_local_colmax(self.h, A.data_ptr() if A.numel() else None, A.shape[0],
+                                                B.data_ptr() if B.numel() else None, B.shape[0], D,
+                                                s.ctypes.data, out.data_ptr()))
+        return out
+
+    def local_moments_i8(self, A_local, B_local, shift: np.ndarray, colmax: torch.Tensor) -> torch.Tensor:
+        """prohd_local_moments_i8: [S_A | S_B | G] about s from the int8 Gram on the grid of the
+        all-reduced column maxima `colmax` (device fp32, D)."""
+        A, B = _as_points(A_local, "A"), _as_points(B_local, "B")
+        D = A.shape[1]
+        self._shard_ws(max(A.shape[0], B.shape[0]), 1, D, 0, 1)
+        s = np.ascontiguousarray(shift, dtype=np.float64)
+        cm = colmax.to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
+        out = torch.empty(2 * D + D * D, dtype=torch.float64, device=f"cuda:{self.device}")
+        self._check(self.lib.prohd_local_moments_i8(self.h, A.data_ptr() if A.numel() else None, A.shape[0],
+                                                    B.data_ptr() if B.numel() else None, B.shape[0], D,
+                                                    s.ctypes.data, cm.data_ptr(), out.data_ptr()))
+        return out
+
     def directions(self, moments: torch.Tensor, nA: int, nB: int, D: int, k: int, shift: np.ndarray):
         self._shard_ws(0, 1, D, k, 1)
         s = np.ascontiguousarray(shift, dtype=np.float64)

@@ -32,6 +32,7 @@ enum OptId {
   OPT_EIG_CL,        // 8: portable 8-CTA tridiagonalisation cluster
   OPT_K1_ABLATE,     // int8 Gram timing ablations (wrong results): 1 no slicing work, 2 no MMAs
   OPT_K4_SAMPLED,    // 0 radix K4 over all projections, 1 sampled-threshold K4 wherever it applies
+  OPT_K1_I8_CTAS,    // int8 Gram: cap on the CTA count (tests: mid-sweep drains at small sizes)
   OPT_COUNT
 };
 inline std::atomic<long long>* option_table() {

@@ -186,17 +186,16 @@ __device__ void inverse_iteration(const double* d, const double* e, int D, doubl
 }
 
 // Householder tridiagonalisation T = Q^T C Q on one cluster of kCl CTAs (Golub & Van Loan
-// 8.3.1). Row r of C lives in CTA r % kCl as a full row in shared memory. ONE cluster barrier
-// per step j (buffers double-buffered on j & 1):
-//   B. every CTA holds column j (rows >= j, d_j at index j) in colbuf; each warp forms the
-//      norm, alpha and v = (x - alpha e1)/||.|| from it, the CTA computes p_r = 2 sum_c
-//      M[r][c] v_c for its rows r > j and scatters (p_r, the PRE-update entry M[r][j+1]) as one
-//      16-byte store into every CTA.                                        -> cluster barrier
-//   C. K = v.p (from the full p), w = p - K v, M[r][c] -= v_r w_c + w_r v_c on its own rows, and every CTA
-//      forms the whole updated column j+1 itself, M[r][j+1] - (v_r w_{j+1} + w_r v_{j+1})
-//      (the same expression, so bit-identical to the owner's row), as step j+1's colbuf.
-// The second barrier of a scatter-the-updated-column scheme is gone; the scatter volume is the
-// same. Writes d, e (de) and the Householder vectors (V rows 0 .. D-3).
+// 8.3.1). Row r of C lives in CTA r % kCl as a full row in shared memory. Column j of the
+// current matrix is held in REGISTERS by every warp (lane l: rows l + 32 t), so a step needs no
+// CTA barrier, and ONE cluster barrier (pc double-buffered on j & 1):
+//   B. each warp forms the norm, alpha and v = (x - alpha e1)/||.|| from its copy of column j,
+//      computes p_r = 2 sum_c M[r][c] v_c for its own rows r > j and scatters (p_r, the
+//      PRE-update entry M[r][j+1]) as one 16-byte store into every CTA.  -> cluster barrier
+//   C. K = v.p (from the full p), w = p - K v, M[r][c] -= v_r w_c + w_r v_c on own rows (v_r from
+//      the row's own entry M[r][j]), and every warp forms the updated column j+1 in its registers
+//      with the owner's expression M[r][j+1] - (v_r w_{j+1} + w_r v_{j+1}) (bit-identical).
+// Writes d, e (de) and the Householder vectors (V rows 0 .. D-3).
 template <int kCl>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduce_cluster_kernel(EigArgs a) {
   constexpr int kRows = kMaxD / kCl;  // rows per CTA (max)
@@ -204,9 +203,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
   const int rank = static_cast<int>(cl.block_rank());
   extern __shared__ double dyn[];
   double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/kCl)*D])
-  __shared__ double colbuf2[2][kMaxD];                 // column j (rows >= j) of step j: [j & 1]
-  __shared__ double2 pc2[2][kMaxD];                    // scattered (p_r, pre-update M[r][j+1])
-  __shared__ double vbuf[kMaxD], wbuf[kMaxD];          // v and w = p - K v of the current step
+  __shared__ double2 pc2[2][kMaxD];  // scattered (p_r, pre-update M[r][j+1]): [j & 1]
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nloc = (D - rank + kCl - 1) / kCl;  // rows r = rank + kCl*i, i < nloc
@@ -214,39 +211,52 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
     const int i = t / D, c = t % D;
     M[i * D + c] = a.C[static_cast<int64_t>(rank + kCl * i) * D + c];
   }
-  __syncthreads();
-  // column 0 (with d_0 at index 0) into every CTA
-  {
-    const int i = tid / kCl, q = tid % kCl;  // own row slot i, target CTA q
-    if (i < nloc) *cl.map_shared_rank(&colbuf2[0][rank + kCl * i], q) = M[i * D];
+  // column j of the current matrix, in registers and replicated in every warp: lane l holds rows
+  // c = l + 32 t (t < 8). Column 0 is read from the ROWS (C[c][0]), the entries the row owners
+  // hold: the register column and the owners' rows must agree bit for bit (the update uses v_r
+  // from the row and v_c from the column; with C[0][c] instead, a 1-ulp asymmetry of the input
+  // grew into O(||C||) errors of T, reproduced in a host emulation)
+  constexpr int kTq = kMaxD / 32;
+  double x[kTq];
+#pragma unroll
+  for (int t = 0; t < kTq; ++t) {
+    const int c = lane + 32 * t;
+    x[t] = c < D ? a.C[static_cast<int64_t>(c) * D] : 0.0;
   }
+  __syncthreads();
   cl.sync();
   double* dg = a.de;
   double* eg = a.de + kMaxD;
+  constexpr int kRW = kRows / kWarps;  // own rows per warp
   for (int j = 0; j + 2 < D; ++j) {
-    const int b = j & 1;
-    const double* colbuf = colbuf2[b];
-    double2* pc = pc2[b];
-    // B. every warp forms ||x||, alpha and the scale itself (no CTA barrier); v_c is
-    // recomputed on the fly as vc(c) = (c == j+1 ? x0 - alpha : colbuf[c]) * sc
-    double ss = 0.0;
-    for (int c = j + 1 + lane; c < D; c += 32) ss = fma(colbuf[c], colbuf[c], ss);
+    double2* pc = pc2[j & 1];
+    // B. every warp forms ||x||, alpha and the scale from its register copy of column j (rows
+    // > j); v_c = (c == j+1 ? x0 - alpha : x_c) * sc
+    double ss = 0.0, x0 = 0.0;
+#pragma unroll
+    for (int t = 0; t < kTq; ++t) {
+      const int c = lane + 32 * t;
+      const double xt = (c > j && c < D) ? x[t] : 0.0;
+      ss = fma(xt, xt, ss);
+      x0 = (c == j + 1) ? xt : x0;
+    }
     const double nrm2 = warp_sum(ss);
     const double nrm = sqrt(nrm2);
-    const double x0 = colbuf[j + 1];
+    x0 = __shfl_sync(0xffffffffu, x0, (j + 1) & 31);
     const double alpha = (x0 > 0.0) ? -nrm : nrm;
     const double v0 = x0 - alpha;
     const double vn2 = nrm2 - x0 * x0 + v0 * v0;
     // sc == 0: the column is already zero below the subdiagonal, H = I (v = 0, p = 0, K = 0:
     // the update below is then a no-op and the next column comes out unchanged)
     const double sc = (vn2 > 0.0 && nrm > 0.0) ? 1.0 / sqrt(vn2) : 0.0;
-    auto vc = [&](int c) { return (c == j + 1 ? v0 : colbuf[c]) * sc; };
-    // v once per CTA in shared memory (every warp formed the same scalars)
-    for (int c = j + 1 + tid; c < D; c += kT) vbuf[c] = vc(c);
-    __syncthreads();
-    // p_r = 2 M[r][j+1:] . v for own rows r > j (warp per row, <= 4 rows per warp, the row
-    // dot products formed together and reduced together); v.p partial per warp
-    constexpr int kRW = kRows / kWarps;  // rows per warp
+    double v[kTq];
+#pragma unroll
+    for (int t = 0; t < kTq; ++t) {
+      const int c = lane + 32 * t;
+      v[t] = (c > j && c < D) ? (c == j + 1 ? v0 : x[t]) * sc : 0.0;
+    }
+    // p_r = 2 M[r][j+1:] . v for own rows r > j (warp per row, the row dot products formed
+    // together and reduced together)
     double ps[kRW];
 #pragma unroll
     for (int q = 0; q < kRW; ++q) {
@@ -255,7 +265,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
       double s0 = 0.0;
       if (i < nloc && r > j) {
         const double* row = M + i * D;
-        for (int c = j + 1 + lane; c < D; c += 32) s0 = fma(row[c], vbuf[c], s0);
+#pragma unroll
+        for (int t = 0; t < kTq; ++t) {
+          const int c = lane + 32 * t;
+          if (c > j && c < D) s0 = fma(row[c], v[t], s0);
+        }
       }
       ps[q] = s0;
     }
@@ -275,39 +289,57 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
     // outputs (d_j, e_j, Householder vector j) are stored between arrive and wait, so their
     // latency is not on the barrier's path (the next step's release finds them long done)
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    if (rank == 0) {
-      if (tid == 0) {
-        dg[j] = colbuf[j];
-        eg[j] = (sc != 0.0) ? alpha : 0.0;
+    // d_j from the warp that owns (and last updated) row j: no cross-warp shared-memory hazard
+    if (j % kCl == rank && warp == (j / kCl) % kWarps && lane == 0) dg[j] = M[(j / kCl) * D + j];
+    if (rank == 0 && warp == 0) {
+      if (lane == 0) eg[j] = (sc != 0.0) ? alpha : 0.0;
+#pragma unroll
+      for (int t = 0; t < kTq; ++t) {
+        const int c = lane + 32 * t;
+        if (c > j && c < D) a.V[static_cast<int64_t>(j) * D + c] = v[t];
       }
-      for (int c = j + 1 + tid; c < D; c += kT) a.V[static_cast<int64_t>(j) * D + c] = vbuf[c];
     }
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    // C. K = v.p; w = p - K v once per CTA; M[r][c] -= v_r w_c + w_r v_c on own rows; the
-    // updated column j+1 (rows >= j+1) into the other colbuf
-    // K from the full p every CTA now holds (no partial sums to exchange); same order in every
-    // warp and CTA, so every copy of w is identical
+    // C. K = v.p from the full p (same order in every warp and CTA), w = p - K v; M[r][c] -=
+    // v_r w_c + w_r v_c on own rows; every warp forms the updated column j+1 (rows > j) in its
+    // registers with the owner's expression, M[r][j+1] - (v_r w_{j+1} + w_r v_{j+1})
     double K = 0.0;
-    for (int c = j + 1 + lane; c < D; c += 32) K = fma(vbuf[c], pc[c].x, K);
+#pragma unroll
+    for (int t = 0; t < kTq; ++t) {
+      const int c = lane + 32 * t;
+      if (c > j && c < D) K = fma(v[t], pc[c].x, K);
+    }
     K = warp_sum(K);
-    for (int c = j + 1 + tid; c < D; c += kT) wbuf[c] = pc[c].x - K * vbuf[c];
-    __syncthreads();
+    double w[kTq];
+#pragma unroll
+    for (int t = 0; t < kTq; ++t) {
+      const int c = lane + 32 * t;
+      w[t] = (c > j && c < D) ? pc[c].x - K * v[t] : 0.0;
+    }
 #pragma unroll
     for (int q = 0; q < kRW; ++q) {
       const int i = warp + kWarps * q;
       const int r = rank + kCl * i;
       if (i >= nloc || r <= j) continue;
       double* row = M + i * D;
-      const double vr = vbuf[r], wr = wbuf[r];
-      for (int c = j + 1 + lane; c < D; c += 32) row[c] -= fma(vr, wbuf[c], wr * vbuf[c]);
+      const double vr = (r == j + 1 ? v0 : row[j]) * sc;  // v_r from the row's own column-j entry
+      const double wr = pc[r].x - K * vr;
+#pragma unroll
+      for (int t = 0; t < kTq; ++t) {
+        const int c = lane + 32 * t;
+        if (c > j && c < D) row[c] -= fma(vr, w[t], wr * v[t]);
+      }
     }
     {
-      double* nxt = colbuf2[b ^ 1];
-      const double vj = vbuf[j + 1], wj = wbuf[j + 1];
-      for (int r = j + 1 + tid; r < D; r += kT) nxt[r] = pc[r].y - fma(vbuf[r], wj, wbuf[r] * vj);
+      const double vj = v0 * sc, wj = pc[j + 1].x - K * vj;
+#pragma unroll
+      for (int t = 0; t < kTq; ++t) {
+        const int c = lane + 32 * t;
+        x[t] = (c > j && c < D) ? pc[c].y - fma(v[t], wj, w[t] * vj) : 0.0;
+      }
     }
-    __syncthreads();
   }
+  __syncthreads();  // the last step's row updates (other warps) before the 2x2 block
   // last 2x2 block
   if (D >= 2 && ((D - 2) % kCl) == rank && tid == 0) {
     const int i = (D - 2) / kCl;

@@ -1,5 +1,6 @@
 // k_gram_i8.cu — K1 on the int8 tensor cores: the shifted Gram G = sum_p (p - s)(p - s)^T of
-// A u B and the column sums S_X = sum_{x in X} (x - s), for 128 < D <= 256 (D % 4 == 0).
+// A u B and the column sums S_X = sum_{x in X} (x - s), for D <= 256 (D % 4 == 0): gram_i8_kernel
+// (CTA pairs) for 128 < D <= 256, gram_i8s_kernel (single CTAs, below) for D <= 128.
 //
 // PAPER.md Alg. 1 line 1 and Alg. 2 lines 1-2: the principal
 // components are eigenvectors of C = G / N - (mu - s)(mu - s)^T (moments_finalize, k_moments.cu).
@@ -79,6 +80,8 @@ struct I8Args {
   int ncs;
   unsigned* overflow;
   int ablate;            // dev timing only (option k1_ablate): 1 skip the slicing work, 2 skip the MMAs
+  int small;             // D <= 128: gram_i8s_kernel (one CTA per level set), nt0 + nt1 CTAs
+  int nt0, nt1;          //   CTAs of level set 0 ({0,1,2,3}) and of level set 1 ({4,5})
 };
 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
@@ -151,15 +154,64 @@ struct Range {
   int64_t a0, a1, b0, b1;
   int na, nb;  // chunks
 };
-__device__ __forceinline__ Range group_range(const I8Args& a, int g) {
+__device__ __forceinline__ Range group_range(const I8Args& a, int g, int ngroups) {
   Range r;
-  r.a0 = a.nA * g / a.ngroups;
-  r.a1 = a.nA * (g + 1) / a.ngroups;
-  r.b0 = a.nB * g / a.ngroups;
-  r.b1 = a.nB * (g + 1) / a.ngroups;
+  r.a0 = a.nA * g / ngroups;
+  r.a1 = a.nA * (g + 1) / ngroups;
+  r.b0 = a.nB * g / ngroups;
+  r.b1 = a.nB * (g + 1) / ngroups;
   r.na = static_cast<int>((r.a1 - r.a0 + kPts - 1) / kPts);
   r.nb = static_cast<int>((r.b1 - r.b0 + kPts - 1) / kPts);
   return r;
+}
+
+// Slice one raw chunk into the four digit planes (slicer warp ws, lane = features 4 lane .. +3 of the
+// CTA's 128): xr = the raw stage (four SWIZZLE_128B boxes of 32 features x 64 points; box lane / 8
+// holds features 32 (lane / 8) .., row p, 16-byte chunk (lane % 8) ^ (p % 8)), pl = the slice stage.
+__device__ __forceinline__ void slice_chunk(uint32_t xr, uint32_t pl, int ws, int lane, int valid, const float (&sc)[4],
+                                            const float (&sh)[4]) {
+  // all of this warp's points of the chunk are loaded first (8 independent 16-byte loads in
+  // flight), then converted: the shared-memory latency is not on each point's dependency chain
+  constexpr int kPer = kPts / kSlicers;
+  float4 xs[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int p = ws + kSlicers * u;
+    xs[u] = lds128(xr + p * 128 + ((((lane & 7) ^ (p & 7)) & 7) << 4));
+  }
+  // one 4-point group: y = x 2^k - S (rows past the range: F = c0, i.e. F - c0 = 0), F, the four
+  // digit bytes per feature, 4 x 4 byte transpose, one 32-bit store per digit plane
+  auto slice_point = [&](int u, bool ok) {
+    const int p = ws + kSlicers * u;
+    const float4 x4 = xs[u];
+    const float y0 = ok ? fmaf(x4.x, sc[0], -sh[0]) : 8421504.0f, y1 = ok ? fmaf(x4.y, sc[1], -sh[1]) : 8421504.0f;
+    const float y2 = ok ? fmaf(x4.z, sc[2], -sh[2]) : 8421504.0f, y3 = ok ? fmaf(x4.w, sc[3], -sh[3]) : 8421504.0f;
+    const uint32_t w0i = static_cast<uint32_t>(__float2int_rn(y0)), w1i = static_cast<uint32_t>(__float2int_rn(y1));
+    const uint32_t w2i = static_cast<uint32_t>(__float2int_rn(y2)), w3i = static_cast<uint32_t>(__float2int_rn(y3));
+    // plane t (t = 0 the top byte) gets byte 3 - t of the 4 features; the three low planes XOR
+    // 0x80 per byte (balanced digits of F - c0)
+    const uint32_t x01l = __byte_perm(w0i, w1i, 0x5140), x01h = __byte_perm(w0i, w1i, 0x7362);
+    const uint32_t x23l = __byte_perm(w2i, w3i, 0x5140), x23h = __byte_perm(w2i, w3i, 0x7362);
+    const uint32_t b0 = __byte_perm(x01l, x23l, 0x5410) ^ 0x80808080u;
+    const uint32_t b1 = __byte_perm(x01l, x23l, 0x7632) ^ 0x80808080u;
+    const uint32_t b2 = __byte_perm(x01h, x23h, 0x5410) ^ 0x80808080u;
+    // plane 0 holds the DOUBLED top digit 2 d_0 (|d_0| <= 64, d_0 <= 63): per-byte shift
+    const uint32_t b3 = (__byte_perm(x01h, x23h, 0x7632) << 1) & 0xFEFEFEFEu;
+    // SWIZZLE_128B MN-major: row p (128 B), 16-byte chunk (lane / 4) XOR (p % 8)
+    const uint32_t off = static_cast<uint32_t>((p >> 3) * 1024 + (p & 7) * 128 +
+                                               ((((lane >> 2) ^ (p & 7)) & 7) << 4) + (lane & 3) * 4);
+    sts32(pl + 0 * kPlane + off, b3);
+    sts32(pl + 1 * kPlane + off, b2);
+    sts32(pl + 2 * kPlane + off, b1);
+    sts32(pl + 3 * kPlane + off, b0);
+  };
+  if (valid == kPts) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) slice_point(u, true);
+  } else {  // the last, ragged chunk of a set
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) slice_point(u, ws + kSlicers * u < valid);
+  }
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -182,7 +234,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
   const int type = pair % 3, g = pair / 3;
-  const Range R = group_range(a, g);
+  const Range R = group_range(a, g, a.ngroups);
   const int nchunks = R.na + R.nb;
   const int cta = blockIdx.x;  // slab index
 
@@ -336,50 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // raw box (lane / 8) holds features 32 (lane / 8) ..; row p, 16-byte chunk (lane % 8) ^ (p % 8)
       const uint32_t xr = raw_u32 + rst * kRawBytes + (lane >> 3) * (kRawBytes / 4);
       const uint32_t pl = sl_u32 + sst * kSlBytes;
-      // all of this warp's points of the chunk are loaded first (8 independent 16-byte loads in
-      // flight), then converted: the shared-memory latency is not on each point's dependency chain
-      constexpr int kPer = kPts / kSlicers;
-      float4 xs[kPer];
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int p = ws + kSlicers * u;
-        xs[u] = lds128(xr + p * 128 + ((((lane & 7) ^ (p & 7)) & 7) << 4));
-      }
-      // one 4-point group: y = x 2^k - S (rows past the range: F = c0, i.e. F - c0 = 0), F, the four
-      // digit bytes per feature, 4 x 4 byte transpose, one 32-bit store per digit plane
-      auto slice_point = [&](int u, bool ok) {
-        const int p = ws + kSlicers * u;
-        const float4 x4 = xs[u];
-        const float y0 = ok ? fmaf(x4.x, sc[0], -sh[0]) : 8421504.0f, y1 = ok ? fmaf(x4.y, sc[1], -sh[1]) : 8421504.0f;
-        const float y2 = ok ? fmaf(x4.z, sc[2], -sh[2]) : 8421504.0f, y3 = ok ? fmaf(x4.w, sc[3], -sh[3]) : 8421504.0f;
-        const uint32_t w0i = static_cast<uint32_t>(__float2int_rn(y0)), w1i = static_cast<uint32_t>(__float2int_rn(y1));
-        const uint32_t w2i = static_cast<uint32_t>(__float2int_rn(y2)), w3i = static_cast<uint32_t>(__float2int_rn(y3));
-        // plane t (t = 0 the top byte) gets byte 3 - t of the 4 features; the three low planes XOR
-        // 0x80 per byte (balanced digits of F - c0)
-        const uint32_t x01l = __byte_perm(w0i, w1i, 0x5140), x01h = __byte_perm(w0i, w1i, 0x7362);
-        const uint32_t x23l = __byte_perm(w2i, w3i, 0x5140), x23h = __byte_perm(w2i, w3i, 0x7362);
-        const uint32_t b0 = __byte_perm(x01l, x23l, 0x5410) ^ 0x80808080u;
-        const uint32_t b1 = __byte_perm(x01l, x23l, 0x7632) ^ 0x80808080u;
-        const uint32_t b2 = __byte_perm(x01h, x23h, 0x5410) ^ 0x80808080u;
-        // plane 0 holds the DOUBLED top digit 2 d_0 (|d_0| <= 64, d_0 <= 63): per-byte shift
-        const uint32_t b3 = (__byte_perm(x01h, x23h, 0x7632) << 1) & 0xFEFEFEFEu;
-        // SWIZZLE_128B MN-major: row p (128 B), 16-byte chunk (lane / 4) XOR (p % 8)
-        const uint32_t off = static_cast<uint32_t>((p >> 3) * 1024 + (p & 7) * 128 +
-                                                   ((((lane >> 2) ^ (p & 7)) & 7) << 4) + (lane & 3) * 4);
-        sts32(pl + 0 * kPlane + off, b3);
-        sts32(pl + 1 * kPlane + off, b2);
-        sts32(pl + 2 * kPlane + off, b1);
-        sts32(pl + 3 * kPlane + off, b0);
-      };
-      if (!(a.ablate & 1)) {
-        if (valid == kPts) {
-#pragma unroll
-          for (int u = 0; u < kPer; ++u) slice_point(u, true);
-        } else {  // the last, ragged chunk of a set
-#pragma unroll
-          for (int u = 0; u < kPer; ++u) slice_point(u, ws + kSlicers * u < valid);
-        }
-      }
+      if (!(a.ablate & 1)) slice_chunk(xr, pl, ws, lane, valid, sc, sh);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
@@ -432,6 +441,234 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_2sm<512>(tmem_base);
+  }
+}
+
+__device__ __forceinline__ void mma_i8_1sm(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// D <= 128 (gram_i8s_kernel): the whole Gram is one M = 128 x N = 128 block (features past D have
+// zero digits), so one CTA (cta_group::1) holds four 128-column int32 level accumulators in its
+// 512 TMEM columns. Level set 0 = levels {0, 1, 2, 3}: 1 + 1 + 2 + 3 = 7 products per K-step;
+// level set 1 = levels {4, 5}: 3 + 2 = 5 products. The CTAs of a set split the rows of A u B
+// (the two sets read every row once each), and the sets get CTAs in the ratio 7 : 5.
+// Same roles and stages as gram_i8_kernel: warp 0 TMA (raw chunks, 64 points x 128 features),
+// warp 1 TMEM allocation and the MMA issuer, warps 2-9 slicers and, at the end of a drain window,
+// drains (lane quarter warp % 4, column half (warp - 2) / 4 of every slot) into the CTA's fp64
+// slab [128 columns][128 rows].
+constexpr int kSmallSlab = 128 * 128;  // doubles per CTA slab
+constexpr int kSet0Share = 7, kSetShares = 12;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gram_i8s_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, I8Args a) {
+  using namespace sm100;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* raw = smem;
+  uint8_t* sl = smem + kRawStages * kRawBytes;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(sl + kSlStages * kSlBytes);
+  uint64_t* raw_empty = raw_full + kRawStages;
+  uint64_t* sl_full = raw_empty + kRawStages;  // the 8 slicer warps
+  uint64_t* sl_empty = sl_full + kSlStages;    // MMA commit
+  uint64_t* tfull = sl_empty + kSlStages;      // MMA commit at the end of a drain window
+  uint64_t* tempty = tfull + 1;                // the 8 drain warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int set = static_cast<int>(blockIdx.x) < a.nt0 ? 0 : 1;
+  const int g = set == 0 ? static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x) - a.nt0;
+  const Range R = group_range(a, g, set == 0 ? a.nt0 : a.nt1);
+  const int nchunks = R.na + R.nb;
+  const int nslot = set == 0 ? 4 : 2;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRawStages; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], kSlicers);
+    }
+    for (int i = 0; i < kSlStages; ++i) {
+      mbar_init(&sl_full[i], kSlicers);
+      mbar_init(&sl_empty[i], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], kDrainWarps);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tA);
+    tma_prefetch(&tB);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        mbar_wait(&raw_empty[st], ph ^ 1u);
+        mbar_arrive_expect_tx(&raw_full[st], kRawBytes);
+        const bool inA = c < R.na;
+        const int64_t row = inA ? R.a0 + static_cast<int64_t>(c) * kPts : R.b0 + static_cast<int64_t>(c - R.na) * kPts;
+        for (int bx = 0; bx < 4; ++bx)  // boxes past D are zero-filled by the TMA unit
+          tma_load_2d(raw + st * kRawBytes + bx * (kRawBytes / 4), inA ? &tA : &tB, bx * 32, static_cast<int>(row),
+                      &raw_full[st]);
+        if (++st == kRawStages) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(128, 128);
+      // (t, u, slot); plane 0 = 2 d_0, so (0, u) stands for (0, u) + (u, 0) after the final
+      // symmetrisation and (0, 0) is 4 d_0 d_0
+      int tt[7], uu[7], ss[7];
+      int np;
+      if (set == 0) {
+        const int t0[7] = {0, 0, 0, 1, 0, 1, 2}, u0[7] = {0, 1, 2, 1, 3, 2, 1}, s0[7] = {0, 1, 2, 2, 3, 3, 3};
+        for (int i = 0; i < 7; ++i) tt[i] = t0[i], uu[i] = u0[i], ss[i] = s0[i];
+        np = 7;
+      } else {
+        const int t1[5] = {1, 2, 3, 2, 3}, u1[5] = {3, 2, 1, 3, 2}, s1[5] = {0, 0, 0, 1, 1};
+        for (int i = 0; i < 5; ++i) tt[i] = t1[i], uu[i] = u1[i], ss[i] = s1[i];
+        for (int i = 5; i < 7; ++i) tt[i] = uu[i] = ss[i] = 0;
+        np = 5;
+      }
+      int st = 0;
+      uint32_t ph = 0, tph = 0;
+      int since = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        if (since == 0 && c > 0) {
+          mbar_wait(&tempty[0], tph ^ 1u);  // the drain warps have read TMEM
+          tc_fence_after();
+        }
+        mbar_wait(&sl_full[st], ph);
+        tc_fence_after();
+        const uint32_t base = smem_u32(sl + st * kSlBytes);
+        for (int kk = 0; kk < (a.ablate >= 2 ? 0 : 2); ++kk) {
+          for (int i = 0; i < np; ++i) {
+            const uint64_t da = smem_desc_mn_sw128(base + tt[i] * kPlane + kk * 4096);
+            const uint64_t db = smem_desc_mn_sw128(base + uu[i] * kPlane + kk * 4096);
+            const bool first = since == 0 && kk == 0 && (i == 0 || ss[i] != ss[i - 1]);
+            mma_i8_1sm(tmem_base + static_cast<uint32_t>(ss[i] * 128), da, db, idesc, first ? 0u : 1u);
+          }
+        }
+        mma_commit(&sl_empty[st]);
+        if (++st == kSlStages) {
+          st = 0;
+          ph ^= 1u;
+        }
+        if (++since == kDrainChunks || c == nchunks - 1) {
+          mma_commit(&tfull[0]);
+          since = 0;
+          tph ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ slicers (+ drains)
+    const int ws = warp - 2;
+    const int fg0 = 4 * lane;
+    float sc[4], sh[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool live = fg0 + i < a.D;
+      sc[i] = live ? __ldg(a.scale + fg0 + i) : 0.0f;  // features >= D: F - c0 = 0
+      sh[i] = live ? __ldg(a.shiftf + fg0 + i) : -8421504.0f;
+    }
+    const uint32_t raw_u32 = smem_u32(raw), sl_u32 = smem_u32(sl);
+    const int q = warp & 3, half = ws >> 2;
+    const int rowl = q * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+    // level weights 2^(-8 L) (level 0 holds 4 d_0 d_0: weight / 4)
+    double wt[4];
+    if (set == 0) {
+      wt[0] = 0.25;
+      wt[1] = 0x1p-8;
+      wt[2] = 0x1p-16;
+      wt[3] = 0x1p-24;
+    } else {
+      wt[0] = 0x1p-32;
+      wt[1] = 0x1p-40;
+      wt[2] = wt[3] = 0.0;
+    }
+    double* out = a.slab + static_cast<int64_t>(blockIdx.x) * kSmallSlab + half * 64 * 128 + rowl;
+    int rst = 0, sst = 0, since = 0, ndr = 0;
+    uint32_t rph = 0, sph = 0, tph = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const bool inA = c < R.na;
+      const int64_t row0 = inA ? R.a0 + static_cast<int64_t>(c) * kPts : R.b0 + static_cast<int64_t>(c - R.na) * kPts;
+      const int64_t rend = inA ? R.a1 : R.b1;
+      const int valid = static_cast<int>(min(static_cast<int64_t>(kPts), rend - row0));
+      mbar_wait(&raw_full[rst], rph);
+      mbar_wait(&sl_empty[sst], sph ^ 1u);
+      const uint32_t xr = raw_u32 + rst * kRawBytes + (lane >> 3) * (kRawBytes / 4);
+      const uint32_t pl = sl_u32 + sst * kSlBytes;
+      if (!(a.ablate & 1)) slice_chunk(xr, pl, ws, lane, valid, sc, sh);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&raw_empty[rst]);
+        mbar_arrive(&sl_full[sst]);
+      }
+      if (++rst == kRawStages) {
+        rst = 0;
+        rph ^= 1u;
+      }
+      if (++sst == kSlStages) {
+        sst = 0;
+        sph ^= 1u;
+      }
+      if (++since == kDrainChunks || c == nchunks - 1) {
+        // drain window ends: TMEM -> fp64 slab (this warp: its lane quarter, its 64-column half of
+        // every slot, the slots weighted and added in a fixed order), then release the accumulators
+        since = 0;
+        mbar_wait_sleep(&tfull[0], tph);
+        tph ^= 1u;
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < 64; cc += 32) {
+          double acc[32];
+#pragma unroll 1
+          for (int sl2 = 0; sl2 < nslot; ++sl2) {
+            int v[32];
+            tmem_ld32i(tmem_base + lane_addr + static_cast<uint32_t>(sl2 * 128 + half * 64 + cc), v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = sl2 == 0 ? static_cast<double>(v[i]) * wt[0]
+                                                           : fma(static_cast<double>(v[i]), wt[sl2], acc[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) out[(cc + i) * 128] = ndr == 0 ? acc[i] : out[(cc + i) * 128] + acc[i];
+        }
+        ++ndr;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[0]);
+      }
+    }
+    if (nchunks == 0)
+      for (int j2 = 0; j2 < 64; ++j2) out[j2 * 128] = 0.0;  // an empty range contributes zeros
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
   }
 }
 
@@ -628,20 +865,135 @@ __global__ void __launch_bounds__(256) gram_i8_reduce_kernel(I8Args a, double* G
   }
 }
 
+// Sharded phase (prohd_local_moments_i8): the moments about the fixed-point shift s' re-expressed
+// about the caller's shift s, d = s' - s: sum (x - s)(x - s)^T = G' + d S'^T + S' d^T + N d d^T with
+// S' = S'_A + S'_B, and S_X = S'_X + n_X d (d is below the grid step 2^-k_j; fp64 throughout).
+__global__ void __launch_bounds__(256) i8_reshift_gram_kernel(int D, int64_t N, const double* __restrict__ s_to,
+                                                              const double* __restrict__ s_from,
+                                                              const double* __restrict__ SA,
+                                                              const double* __restrict__ SB, double* G) {
+  const int i = blockIdx.x;
+  const double di = s_from[i] - s_to[i], Si = SA[i] + SB[i];
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    const double dj = s_from[j] - s_to[j], Sj = SA[j] + SB[j];
+    // every term symmetric in (i, j) bit for bit: G stays exactly symmetric
+    G[static_cast<int64_t>(i) * D + j] += (di * Sj + Si * dj) + static_cast<double>(N) * (di * dj);
+  }
+}
+__global__ void i8_reshift_sums_kernel(int D, int64_t nA, int64_t nB, const double* __restrict__ s_to, double* s_from,
+                                       double* SA, double* SB) {
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    const double d = s_from[j] - s_to[j];
+    SA[j] += static_cast<double>(nA) * d;
+    SB[j] += static_cast<double>(nB) * d;
+    s_from[j] = s_to[j];
+  }
+}
+
+// D <= 128: G = 2^(-k_i - k_j) sym(sum over CTA slabs), the symmetric part taken in the same pass
+// (block i reads column i and row i of every slab: 0.5 (sum_c Z_c[i][j] + sum_c Z_c[j][i]) is the
+// same value for blocks i and j). Thread (grp, j) sums the slabs grp, grp + ngrp, ... in order,
+// then thread j adds the groups' partials in order (deterministic); the column sums as in
+// gram_i8_reduce_kernel.
+constexpr int kSRedThreads = 512;
+__global__ void __launch_bounds__(kSRedThreads) gram_i8s_reduce_kernel(I8Args a, double* G, double* SA, double* SB,
+                                                                      double* s) {
+  const int D = a.D;
+  const int i = blockIdx.x, t = threadIdx.x;
+  const int ngrp = kSRedThreads / D;  // D <= 128: >= 4 groups
+  const int grp = t / D, j = t % D;
+  __shared__ double part[2][kSRedThreads];
+  const int nct = a.nt0 + a.nt1;
+  if (grp < ngrp) {
+    const double* col = a.slab + static_cast<int64_t>(i) * 128 + j;  // Z_c[i][j]: slab [column i][row j]
+    const double* row = a.slab + static_cast<int64_t>(j) * 128 + i;  // Z_c[j][i]
+    double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+    int c = grp;
+    for (; c + ngrp < nct; c += 2 * ngrp) {
+      p0 += __ldg(col + static_cast<int64_t>(c) * kSmallSlab);
+      q0 += __ldg(row + static_cast<int64_t>(c) * kSmallSlab);
+      p1 += __ldg(col + static_cast<int64_t>(c + ngrp) * kSmallSlab);
+      q1 += __ldg(row + static_cast<int64_t>(c + ngrp) * kSmallSlab);
+    }
+    if (c < nct) {
+      p0 += __ldg(col + static_cast<int64_t>(c) * kSmallSlab);
+      q0 += __ldg(row + static_cast<int64_t>(c) * kSmallSlab);
+    }
+    part[0][t] = p0 + p1;
+    part[1][t] = q0 + q1;
+  }
+  __syncthreads();
+  if (t < D) {
+    double p = 0.0, q = 0.0;
+    for (int g2 = 0; g2 < ngrp; ++g2) {
+      p += part[0][g2 * D + t];
+      q += part[1][g2 * D + t];
+    }
+    // slabs carry 2^-48 sum_L 2^(8 (6 - L)) G_L; (p + q) / 2 is the symmetric part
+    G[static_cast<int64_t>(i) * D + t] =
+        ldexp(0.5 * (p + q), 48) / (static_cast<double>(a.scale[i]) * static_cast<double>(a.scale[t]));
+  }
+  __syncthreads();
+  double sa = 0.0, sb = 0.0;
+  for (int b = t; b < a.ncs; b += kSRedThreads) {
+    sa += a.cpart[(static_cast<int64_t>(b) * 2 + 0) * D + i];
+    sb += a.cpart[(static_cast<int64_t>(b) * 2 + 1) * D + i];
+  }
+  part[0][t] = sa;
+  part[1][t] = sb;
+  __syncthreads();
+  for (int o = kSRedThreads / 2; o > 0; o >>= 1) {
+    if (t < o) {
+      part[0][t] += part[0][t + o];
+      part[1][t] += part[1][t + o];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    sa = part[0][0];
+    sb = part[1][0];
+    if (!isfinite(sa) || !isfinite(sb)) atomicOr(a.overflow, 1u);
+    const double sp = (static_cast<double>(a.shiftf[i]) + 128.0 * 65793.0) / static_cast<double>(a.scale[i]);
+    SA[i] = sa - static_cast<double>(a.nA) * sp;
+    SB[i] = sb - static_cast<double>(a.nB) * sp;
+    s[i] = sp;
+  }
+}
+
 }  // namespace
 
 bool plan_gram_i8(int64_t nA, int64_t nB, int D, int num_sms, GramI8Plan& p) {
-  if (D <= 128 || D > 256 || D % 4 != 0 || nA < 1 || nB < 1) return false;
-  const int pairs = (num_sms > 0 ? num_sms : 148) / 2;
+  if (D > 256 || D % 4 != 0 || nA < 0 || nB < 0 || nA + nB < 1) return false;  // a shard may hold one set only
+  const int sms = num_sms > 0 ? num_sms : 148;
+  p.D = D;
+  p.csum_count = static_cast<int64_t>(kColmaxBlocks) * 2 * D;
+  if (D <= 128) {
+    // one CTA per SM; at least 4 chunks per CTA (option k1_i8_ctas caps the count: tests force
+    // mid-sweep drains with it)
+    int64_t T = (nA + nB) / (4 * kPts);
+    if (T > sms) T = sms;
+    if (opt(OPT_K1_I8_CTAS) > 0 && T > opt(OPT_K1_I8_CTAS)) T = opt(OPT_K1_I8_CTAS);
+    if (T < 2) T = 2;
+    p.small = true;
+    p.nt0 = static_cast<int>((T * kSet0Share + kSetShares / 2) / kSetShares);
+    if (p.nt0 < 1) p.nt0 = 1;
+    p.nt1 = static_cast<int>(T) - p.nt0;
+    if (p.nt1 < 1) p.nt1 = 1;
+    p.ngroups = 0;
+    p.nctas = p.nt0 + p.nt1;
+    p.slab_doubles = static_cast<int64_t>(p.nctas) * kSmallSlab;
+    return true;
+  }
+  const int pairs = sms / 2;
   int groups = pairs / 3;  // a group = one pair of each type
   const int64_t per = (nA + nB) / (groups > 0 ? groups : 1);
   if (per < 4 * kPts) groups = static_cast<int>((nA + nB) / (4 * kPts));  // small problems: fewer groups
+  if (opt(OPT_K1_I8_CTAS) > 0 && groups * 6 > opt(OPT_K1_I8_CTAS)) groups = static_cast<int>(opt(OPT_K1_I8_CTAS) / 6);
   if (groups < 1) return false;
-  p.D = D;
+  p.small = false;
   p.ngroups = groups;
   p.nctas = groups * 6;
   p.slab_doubles = static_cast<int64_t>(p.nctas) * kFeat * 256;
-  p.csum_count = static_cast<int64_t>(kColmaxBlocks) * 2 * D;
   return true;
 }
 
@@ -652,7 +1004,7 @@ size_t gram_i8_ws_bytes(const GramI8Plan& p) {
 
 cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, const float* B, int64_t nB,
                            uint8_t* ws, double* s, double* G, double* SA, double* SB, unsigned* overflow,
-                           cudaStream_t st) {
+                           cudaStream_t st, const float* colmax_in, const double* s_to) {
   const int D = p.D;
   double* slab = reinterpret_cast<double*>(ws);
   double* cpart = reinterpret_cast<double*>(ws + round_up(p.slab_doubles * 8, 256));
@@ -663,8 +1015,9 @@ cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, cons
   // raw fp32 boxes [32 features x 64 rows], SWIZZLE_128B (four per chunk and CTA)
   PFN_encodeTiled enc = get_encode();
   if (enc == nullptr) return cudaErrorNotSupported;
-  const float* src[2] = {A, B};
-  const int64_t rows[2] = {nA, nB};
+  // a set without rows (a shard of the sharded phase) gets the other set's map: it is never read
+  const float* src[2] = {nA > 0 ? A : B, nB > 0 ? B : A};
+  const int64_t rows[2] = {nA > 0 ? nA : nB, nB > 0 ? nB : nA};
   for (int i = 0; i < 2; ++i) {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(rows[i])};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 4};
@@ -682,21 +1035,47 @@ cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, cons
   count_launch();
   i8_colmax_kernel<<<kColmaxBlocks, 256, 0, st>>>(A, nA, B, nB, D, s, colmax, cpart);
   count_launch();
-  i8_scale_kernel<<<1, 256, 0, st>>>(D, s, colmax, scale, shiftf, overflow);
+  // the grid: this call's own column maxima, or (sharded phase) the MAX over ranks
+  i8_scale_kernel<<<1, 256, 0, st>>>(D, s, colmax_in != nullptr ? reinterpret_cast<const unsigned*>(colmax_in) : colmax,
+                                     scale, shiftf, overflow);
   I8Args a{nA, nB, D, p.ngroups, scale, shiftf, slab, cpart, kColmaxBlocks, overflow,
-           opt(OPT_K1_ABLATE) > 0 ? static_cast<int>(opt(OPT_K1_ABLATE)) : 0};
-  cudaError_t e =
-      cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
+           opt(OPT_K1_ABLATE) > 0 ? static_cast<int>(opt(OPT_K1_ABLATE)) : 0, p.small ? 1 : 0, p.nt0, p.nt1};
+  auto kern = p.small ? gram_i8s_kernel : gram_i8_kernel;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
   if (e != cudaSuccess) return e;
   count_launch();
-  gram_i8_kernel<<<p.nctas, kThreads, kSmem, st>>>(maps[0], maps[1], a);
+  kern<<<p.nctas, kThreads, kSmem, st>>>(maps[0], maps[1], a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  count_launch();
-  gram_i8_reduce_kernel<<<D, 256, 0, st>>>(a, G, SA, SB, s);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  count_launch();
-  gram_i8_sym_kernel<<<D, 256, 0, st>>>(D, G);
+  if (p.small) {
+    count_launch();
+    gram_i8s_reduce_kernel<<<D, kSRedThreads, 0, st>>>(a, G, SA, SB, s);
+  } else {
+    count_launch();
+    gram_i8_reduce_kernel<<<D, 256, 0, st>>>(a, G, SA, SB, s);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    count_launch();
+    gram_i8_sym_kernel<<<D, 256, 0, st>>>(D, G);
+  }
+  if (s_to != nullptr) {
+    count_launch(2);
+    i8_reshift_gram_kernel<<<D, 256, 0, st>>>(D, nA + nB, s_to, s, SA, SB, G);
+    i8_reshift_sums_kernel<<<1, 256, 0, st>>>(D, nA, nB, s_to, s, SA, SB);
+  }
   return cudaGetLastError();
+}
+
+cudaError_t launch_colmax_i8(const GramI8Plan& p, const float* A, int64_t nA, const float* B, int64_t nB,
+                             uint8_t* ws, const double* s, float* colmax_out, cudaStream_t st) {
+  const int D = p.D;
+  double* cpart = reinterpret_cast<double*>(ws + round_up(p.slab_doubles * 8, 256));
+  float* scale = reinterpret_cast<float*>(ws + round_up(p.slab_doubles * 8, 256) + round_up(p.csum_count * 8, 256));
+  unsigned* colmax = reinterpret_cast<unsigned*>(scale + 512);
+  cudaError_t e = cudaMemsetAsync(colmax, 0, sizeof(unsigned) * 256, st);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  i8_colmax_kernel<<<kColmaxBlocks, 256, 0, st>>>(A, nA, B, nB, D, s, colmax, cpart);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cudaMemcpyAsync(colmax_out, colmax, sizeof(float) * D, cudaMemcpyDeviceToDevice, st);
 }
 
 }  // namespace prohd

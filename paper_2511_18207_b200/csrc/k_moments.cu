@@ -403,7 +403,7 @@ MomentsPlan plan_moments(int64_t nA, int64_t nB, int D, int num_sms) {
     if (p.gp.gpart_doubles > p.gpart_doubles) p.gpart_doubles = p.gp.gpart_doubles;
     if (p.gp.spart_doubles > p.spart_doubles) p.spart_doubles = p.gp.spart_doubles;
   }
-  // The int8 tensor-core Gram (k_gram_i8.cu) is the default for 128 < D <= 256 (option k1_path:
+  // The int8 tensor-core Gram (k_gram_i8.cu) is the default for D <= 256, D % 4 == 0 (option k1_path:
   // 0 forces the fp64 DMMA Gram, 2 the legacy tile kernel).
   p.i8 = (opt(OPT_K1_PATH) == -1 || opt(OPT_K1_PATH) == 1) && plan_gram_i8(nA, nB, D, num_sms, p.ip);
   if (p.i8) p.i8_bytes = static_cast<int64_t>(gram_i8_ws_bytes(p.ip));

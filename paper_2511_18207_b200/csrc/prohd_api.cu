@@ -28,7 +28,7 @@ const char* prohd_version(void) { return "prohd-b200 0.1 sm_100a"; }
 static const char* const kOptNames[prohd::OPT_COUNT] = {
     "k6_variant", "k6_split3", "k6_bidir_2a", "k6_splits_2x", "k1_path", "k1_ctas",
     "k1_cs_sms",  "k1_beta_milli", "shift", "k3_simt", "eig_stop", "eig_cl", "k1_ablate",
-    "k4_sampled"};
+    "k4_sampled", "k1_i8_ctas"};
 
 int prohd_set_option(const char* name, int64_t value) {
   if (name == nullptr) return PROHD_E_INVALID;

@@ -34,18 +34,23 @@ cudaError_t launch_gram(const GramPlan& p, const float* A, int64_t nA, const flo
                         cudaStream_t st);
 
 // int8 tensor-core Gram (k_gram_i8.cu): exact-integer Ozaki slices on tcgen05 kind::i8 CTA pairs,
-// 128 < D <= 256, D % 4 == 0. Writes G (D x D), S_A, S_B about its own fixed-point shift s'
+// D <= 256, D % 4 == 0. Writes G (D x D), S_A, S_B about its own fixed-point shift s'
 // (overwrites s), and sets *overflow if a value fell outside the sampled range (then the caller
 // reruns the fp64 DMMA Gram).
 struct GramI8Plan {
   int D = 0, ngroups = 0, nctas = 0;
+  bool small = false;  // D <= 128: gram_i8s_kernel, nt0 + nt1 single CTAs (level sets 0 and 1)
+  int nt0 = 0, nt1 = 0;
   int64_t slab_doubles = 0, csum_count = 0;
 };
 bool plan_gram_i8(int64_t nA, int64_t nB, int D, int num_sms, GramI8Plan& p);
 size_t gram_i8_ws_bytes(const GramI8Plan& p);
 cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, const float* B, int64_t nB,
                            uint8_t* ws, double* s, double* G, double* SA, double* SB, unsigned* overflow,
-                           cudaStream_t st);
+                           cudaStream_t st, const float* colmax_in = nullptr, const double* s_to = nullptr);
+// sharded phase: per-feature max |x - s| of these rows (fp32, non-finite -> +inf) into colmax_out (device)
+cudaError_t launch_colmax_i8(const GramI8Plan& p, const float* A, int64_t nA, const float* B, int64_t nB,
+                             uint8_t* ws, const double* s, float* colmax_out, cudaStream_t st);
 
 struct MomentsPlan {
   int nb = 0, npairs = 0, c_diag = 0, c_off = 0, nctas = 0, nslots = 0;

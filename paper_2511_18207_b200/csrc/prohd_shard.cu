@@ -17,6 +17,7 @@
 #include "prohd_steps.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 namespace prohd {
@@ -47,7 +48,10 @@ static size_t carve_shard(Carver& c, ShardWs& w, int64_t nA, int64_t nB, int64_t
   w.mom.s = c.take<double>(2 * static_cast<int64_t>(D));  // shift + scratch
   w.mom.Gpart = c.take<double>(mp.gpart_doubles);
   w.mom.Spart = c.take<double>(mp.spart_doubles);
-  if (mp.i8) w.mom.i8ws = c.take<uint8_t>(mp.i8_bytes);
+  if (mp.i8) {
+    w.mom.i8ws = c.take<uint8_t>(mp.i8_bytes);
+    w.mom.i8ovf = c.take<unsigned>(1);
+  }
   w.mom.C = c.take<double>(static_cast<int64_t>(D) * D);
   w.mom.SA = c.take<double>(D);
   w.mom.SB = c.take<double>(D);
@@ -96,6 +100,25 @@ static int shard_begin(prohd_ctx* ctx, ShardWs& w, int64_t nA, int64_t nB, int64
   return PROHD_OK;
 }
 
+// host shards are staged through the workspace; device shards must be 16-byte aligned
+static int stage_local(prohd_ctx* ctx, ShardWs& w, const float*& A_local, int64_t nA_local, const float*& B_local,
+                       int64_t nB_local, int D) {
+  cudaStream_t st = ctx->stream;
+  if (nA_local > 0 && !is_device_ptr(A_local)) {
+    CK(cudaMemcpyAsync(w.stageA, A_local, sizeof(float) * nA_local * D, cudaMemcpyHostToDevice, st));
+    A_local = w.stageA;
+  }
+  if (nB_local > 0 && !is_device_ptr(B_local)) {
+    CK(cudaMemcpyAsync(w.stageB, B_local, sizeof(float) * nB_local * D, cudaMemcpyHostToDevice, st));
+    B_local = w.stageB;
+  }
+  int rc;
+  if ((rc = check_aligned(ctx, nA_local > 0 ? A_local : nullptr, D, "A_local")) ||
+      (rc = check_aligned(ctx, nB_local > 0 ? B_local : nullptr, D, "B_local")))
+    return rc;
+  return PROHD_OK;
+}
+
 extern "C" {
 
 size_t prohd_shard_workspace_bytes(int64_t n_local_max, int64_t n_total_max, int32_t D, int32_t k, int64_t m,
@@ -138,19 +161,7 @@ int prohd_local_moments(prohd_ctx* ctx, const float* A_local, int64_t nA_local, 
   ShardWs w;
   if ((rc = shard_begin(ctx, w, nA_local, nB_local, 1, D, 0, 1, host_in))) return rc;
   cudaStream_t st = ctx->stream;
-  if (host_in) {
-    if (nA_local > 0 && !is_device_ptr(A_local)) {
-      CK(cudaMemcpyAsync(w.stageA, A_local, sizeof(float) * nA_local * D, cudaMemcpyHostToDevice, st));
-      A_local = w.stageA;
-    }
-    if (nB_local > 0 && !is_device_ptr(B_local)) {
-      CK(cudaMemcpyAsync(w.stageB, B_local, sizeof(float) * nB_local * D, cudaMemcpyHostToDevice, st));
-      B_local = w.stageB;
-    }
-  }
-  if ((rc = check_aligned(ctx, nA_local > 0 ? A_local : nullptr, D, "A_local")) ||
-      (rc = check_aligned(ctx, nB_local > 0 ? B_local : nullptr, D, "B_local")))
-    return rc;
+  if ((rc = stage_local(ctx, w, A_local, nA_local, B_local, nB_local, D))) return rc;
   CK(cudaMemcpyAsync(w.mom.s, shift, sizeof(double) * D, cudaMemcpyHostToDevice, st));
   const int t0 = tmark(ctx);
   CK(cudaMemsetAsync(w.mom.SA, 0, sizeof(double) * D, st));
@@ -161,6 +172,92 @@ int prohd_local_moments(prohd_ctx* ctx, const float* A_local, int64_t nA_local, 
     // the caller's shift is fixed across ranks (the moments are summed by an all-reduce), so the
     // phase call keeps the fp64 DMMA Gram (the int8 pass chooses its own fixed-point shift)
     CK(launch_moments_partial(mp, A_local, nA_local, B_local, nB_local, D, w.mom, st, false));
+  }
+  tspan(ctx, PH_MOMENTS, t0);
+  CK(cudaMemcpyAsync(moments_out, w.mom.SA, sizeof(double) * D, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(moments_out + D, w.mom.SB, sizeof(double) * D, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(moments_out + 2 * D, w.mom.C, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, st));
+  call_end(ctx);
+  CK(cudaStreamSynchronize(st));
+  call_collect(ctx);
+  return PROHD_OK;
+}
+
+// Sharded int8 moments, step 1: this rank's per-feature max |x - s| (the grid of the int8 Gram).
+int prohd_local_colmax(prohd_ctx* ctx, const float* A_local, int64_t nA_local, const float* B_local,
+                       int64_t nB_local, int32_t D, const double* shift, float* colmax_out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (shift == nullptr || colmax_out == nullptr) return fail(ctx, PROHD_E_INVALID, "null shift or colmax_out");
+  if (D < 1 || nA_local < 0 || nB_local < 0) return fail(ctx, PROHD_E_INVALID, "bad sizes");
+  if ((nA_local > 0 && A_local == nullptr) || (nB_local > 0 && B_local == nullptr))
+    return fail(ctx, PROHD_E_INVALID, "null input");
+  if (D > 256 || D % 4 != 0) return fail(ctx, PROHD_E_NOTIMPL, "the int8 Gram needs D <= 256, D %% 4 == 0");
+  call_begin(ctx);
+  const bool host_in = (nA_local > 0 && !is_device_ptr(A_local)) || (nB_local > 0 && !is_device_ptr(B_local));
+  ShardWs w;
+  if ((rc = shard_begin(ctx, w, nA_local, nB_local, 1, D, 0, 1, host_in))) return rc;
+  cudaStream_t st = ctx->stream;
+  if ((rc = stage_local(ctx, w, A_local, nA_local, B_local, nB_local, D))) return rc;
+  CK(cudaMemcpyAsync(w.mom.s, shift, sizeof(double) * D, cudaMemcpyHostToDevice, st));
+  GramI8Plan ip;
+  if (nA_local + nB_local > 0 && w.mom.i8ws != nullptr && plan_gram_i8(nA_local, nB_local, D, ctx->num_sms, ip)) {
+    const int t0 = tmark(ctx);
+    CK(launch_colmax_i8(ip, A_local, nA_local, B_local, nB_local, w.mom.i8ws, w.mom.s, colmax_out, st));
+    tspan(ctx, PH_MOMENTS, t0);
+  } else {
+    CK(cudaMemsetAsync(colmax_out, 0, sizeof(float) * D, st));  // no rows: the MAX identity
+  }
+  call_end(ctx);
+  CK(cudaStreamSynchronize(st));
+  call_collect(ctx);
+  return PROHD_OK;
+}
+
+// Sharded int8 moments, step 2: prohd_local_moments on the int8 tensor cores with the grid of the
+// all-reduced column maxima (identical on every rank), re-expressed about the caller's shift.
+int prohd_local_moments_i8(prohd_ctx* ctx, const float* A_local, int64_t nA_local, const float* B_local,
+                           int64_t nB_local, int32_t D, const double* shift, const float* colmax,
+                           double* moments_out) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if (shift == nullptr || moments_out == nullptr || colmax == nullptr)
+    return fail(ctx, PROHD_E_INVALID, "null shift, colmax or moments_out");
+  if (D < 1 || nA_local < 0 || nB_local < 0) return fail(ctx, PROHD_E_INVALID, "bad sizes");
+  if ((nA_local > 0 && A_local == nullptr) || (nB_local > 0 && B_local == nullptr))
+    return fail(ctx, PROHD_E_INVALID, "null input");
+  if (D > 256 || D % 4 != 0) return fail(ctx, PROHD_E_NOTIMPL, "the int8 Gram needs D <= 256, D %% 4 == 0");
+  call_begin(ctx);
+  const bool host_in = (nA_local > 0 && !is_device_ptr(A_local)) || (nB_local > 0 && !is_device_ptr(B_local));
+  ShardWs w;
+  if ((rc = shard_begin(ctx, w, nA_local, nB_local, 1, D, 0, 1, host_in))) return rc;
+  cudaStream_t st = ctx->stream;
+  if ((rc = stage_local(ctx, w, A_local, nA_local, B_local, nB_local, D))) return rc;
+  // a non-finite global column max (non-finite input on some rank): the fp64 DMMA Gram, whose
+  // sums carry the non-finite value to prohd_directions (PROHD_E_DATA there)
+  std::vector<float> cm(D);
+  CK(cudaMemcpyAsync(cm.data(), colmax, sizeof(float) * D, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(w.mom.s, shift, sizeof(double) * D, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(w.mom.s + D, shift, sizeof(double) * D, cudaMemcpyHostToDevice, st));  // target shift
+  CK(cudaStreamSynchronize(st));
+  bool finite = true;
+  for (float v : cm) finite = finite && std::isfinite(v) && v < 3.0e38f;
+  const int t0 = tmark(ctx);
+  CK(cudaMemsetAsync(w.mom.SA, 0, sizeof(double) * D, st));
+  CK(cudaMemsetAsync(w.mom.SB, 0, sizeof(double) * D, st));
+  CK(cudaMemsetAsync(w.mom.C, 0, sizeof(double) * D * D, st));
+  if (nA_local + nB_local > 0) {
+    GramI8Plan ip;
+    const bool i8 = finite && w.mom.i8ws != nullptr && w.mom.i8ovf != nullptr &&
+                    plan_gram_i8(nA_local, nB_local, D, ctx->num_sms, ip);
+    if (i8) {
+      CK(cudaMemsetAsync(w.mom.i8ovf, 0, sizeof(unsigned), st));
+      CK(launch_gram_i8(ip, A_local, nA_local, B_local, nB_local, w.mom.i8ws, w.mom.s, w.mom.C, w.mom.SA, w.mom.SB,
+                        w.mom.i8ovf, st, colmax, w.mom.s + D));
+    } else {
+      const MomentsPlan mp = plan_moments(nA_local, nB_local, D, ctx->num_sms);
+      CK(launch_moments_partial(mp, A_local, nA_local, B_local, nB_local, D, w.mom, st, false));
+    }
   }
   tspan(ctx, PH_MOMENTS, t0);
   CK(cudaMemcpyAsync(moments_out, w.mom.SA, sizeof(double) * D, cudaMemcpyDeviceToDevice, st));

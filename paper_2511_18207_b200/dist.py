@@ -107,6 +107,7 @@ def sharded_prohd_estimate(A_local, offA: int, nA: int, B_local, offB: int, nB: 
     blocks in rank order; rank 0 starts at row 0). `phases` provides the per-rank compute
     (CUDA: `CudaPhases(ctx)`): shift, local_moments, directions, local_candidates,
     merge_union, gather_owned, local_fn, witness_fn. Collectives: broadcast of the shift,
+    C0 MAX all-reduce of the column ranges (int8 Gram; skipped when local_colmax returns None),
     C1 SUM all-reduce of the moments, C2 all-gather of the candidate lists, C3 all-gather
     of the selected rows, C4 MAX all-reduce of the subset-HD keys.
     """
@@ -118,8 +119,12 @@ def sharded_prohd_estimate(A_local, offA: int, nA: int, B_local, offB: int, nB: 
         s.copy_(torch.as_tensor(phases.shift(A_local[:4096], B_local[:4096])))
     dist.broadcast(s, src=0, group=group)
     s_np = s.cpu().numpy()
-    # C1: moments
-    mom = phases.local_moments(A_local, B_local, s_np)
+    # C0 (int8 Gram): MAX all-reduce of the per-feature ranges, so every rank quantises on the
+    # same fixed-point grid; C1: SUM all-reduce of the moments
+    colmax = phases.local_colmax(A_local, B_local, s_np)
+    if colmax is not None:
+        dist.all_reduce(colmax, op=dist.ReduceOp.MAX, group=group)
+    mom = phases.local_moments(A_local, B_local, s_np, colmax)
     dist.all_reduce(mom, op=dist.ReduceOp.SUM, group=group)
     dirs, n_dirs = phases.directions(mom, nA, nB, D, k, s_np)
     # C2 + merge + C3 per set
@@ -154,8 +159,9 @@ def sharded_prohd_estimate(A_local, offA: int, nA: int, B_local, offB: int, nB: 
 class CudaPhases:
     """The product phase implementations: every step runs in libprohd.so kernels."""
 
-    def __init__(self, ctx):
+    def __init__(self, ctx, dmma: bool = False):
         self.ctx = ctx
+        self.dmma = dmma  # True: the fp64 DMMA Gram for the moments (one-shot option k1_path = 0)
         self.local_fn, self.witness_fn = cuda_fns(ctx)
 
     def shift(self, A_first, B_first):
@@ -164,8 +170,17 @@ class CudaPhases:
     def centre(self, X, Y):
         return self.ctx.centre(X, Y)
 
-    def local_moments(self, A_local, B_local, s):
-        return self.ctx.local_moments(A_local, B_local, s)
+    def local_colmax(self, A_local, B_local, s):
+        """Column ranges for the int8 Gram (D <= 256, D % 4 == 0), else None (fp64 DMMA Gram)."""
+        D = A_local.shape[1]
+        if D > 256 or D % 4 != 0 or self.dmma:
+            return None
+        return self.ctx.local_colmax(A_local, B_local, s)
+
+    def local_moments(self, A_local, B_local, s, colmax=None):
+        if colmax is None:
+            return self.ctx.local_moments(A_local, B_local, s)
+        return self.ctx.local_moments_i8(A_local, B_local, s, colmax)
 
     def directions(self, moments, nA, nB, D, k, s):
         return self.ctx.directions(moments, nA, nB, D, k, s)

@@ -23,7 +23,10 @@ class OraclePhases:
         X = np.concatenate([np.asarray(Af, np.float64), np.asarray(Bf, np.float64)])
         return X.mean(axis=0)
 
-    def local_moments(self, A_l, B_l, s):
+    def local_colmax(self, A_l, B_l, s):
+        return None  # no fixed-point grid: fp64 moments
+
+    def local_moments(self, A_l, B_l, s, colmax=None):
         A = np.asarray(A_l, np.float64) - s
         B = np.asarray(B_l, np.float64) - s
         G = A.T @ A + B.T @ B

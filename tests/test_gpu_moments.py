@@ -123,37 +123,50 @@ def _i8_bound(A, B, shifted):
             + 2.0 ** -44 * np.outer(M, M)) * 1.05 + 1e-15 * (Y.T @ Y) / X.shape[0]
 
 
-@pytest.mark.parametrize("kind", ["gauss", "heavy", "unit", "offset", "ragged", "windows"])
+_I8_KINDS = ["gauss", "heavy", "unit", "offset", "ragged", "windows",
+             "s_gauss16", "s_heavy128", "s_unit64", "s_offset96", "s_ragged20", "s_windows64", "s_tiny"]
+
+
+@pytest.mark.parametrize("kind", _I8_KINDS)
 def test_covariance_int8_path(ctx, kind):
     """Step 1a through prohd_covariance (the path prohd_estimate uses): the int8 tensor-core Gram
-    for 128 < D <= 256, against the oracle's two-pass fp64 covariance (O3, oracle/prohd.py), within
-    the fixed-point bound above; mu within 1e-12 of the scale."""
+    (gram_i8_kernel for 128 < D <= 256, gram_i8s_kernel for D <= 128: kinds "s_*"), against the
+    oracle's two-pass fp64 covariance (O3, oracle/prohd.py), within the fixed-point bound above;
+    mu within the grid's rounding bound."""
     from oracle import prohd as OP
-    rng = np.random.default_rng({"gauss": 1, "heavy": 2, "unit": 3, "offset": 4, "ragged": 5, "windows": 6}[kind])
-    D = {"gauss": 256, "heavy": 256, "unit": 200, "offset": 160, "ragged": 132, "windows": 256}[kind]
+    from paper_2511_18207_b200 import option
+    rng = np.random.default_rng(_I8_KINDS.index(kind) + 1)
+    D = {"gauss": 256, "heavy": 256, "unit": 200, "offset": 160, "ragged": 132, "windows": 256,
+         "s_gauss16": 16, "s_heavy128": 128, "s_unit64": 64, "s_offset96": 96, "s_ragged20": 20,
+         "s_windows64": 64, "s_tiny": 16}[kind]
     # "windows": > 682 chunks of 64 points per group (24 groups), so every TMEM accumulator is
-    # drained to the fp64 slabs mid-sweep and accumulated again
-    nA, nB = {"ragged": (1237, 70001), "windows": (560000, 560003)}.get(kind, (40011, 35003))
-    if kind in ("heavy", "windows"):
+    # drained to the fp64 slabs mid-sweep and accumulated again; "s_windows64": the same on the
+    # D <= 128 kernel with two CTAs (option k1_i8_ctas), ~2.3 windows per CTA
+    nA, nB = {"ragged": (1237, 70001), "windows": (560000, 560003), "s_ragged20": (1237, 70001),
+              "s_windows64": (50001, 50003), "s_tiny": (3, 5)}.get(kind, (40011, 35003))
+    base = kind[2:] if kind.startswith("s_") else kind
+    base = base.rstrip("0123456789")
+    if base in ("heavy", "windows"):
         A = (rng.standard_t(3, (nA, D)) * rng.uniform(0.1, 3, D)).astype(np.float32)
         B = (rng.standard_t(3, (nB, D)) * rng.uniform(0.1, 3, D) + 0.3).astype(np.float32)
-    elif kind == "unit":
+    elif base == "unit":
         A = np.clip(rng.random((nA, D)) * 0.6 + 0.1 * rng.standard_normal((nA, D)), 0, 1).astype(np.float32)
         B = np.clip(rng.random((nB, D)) * 0.5 + 0.1 * rng.standard_normal((nB, D)), 0, 1).astype(np.float32)
-    elif kind == "offset":
+    elif base == "offset":
         A = (rng.standard_normal((nA, D)) + 4096).astype(np.float32)
         B = (rng.standard_normal((nB, D)) + 4096.5).astype(np.float32)
     else:
         A = rng.standard_normal((nA, D)).astype(np.float32)
         B = (rng.standard_normal((nB, D)) * 2 + 1).astype(np.float32)
-    mu, C, path = ctx.covariance(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
-    assert path == 1, "the int8 Gram should serve 128 < D <= 256"
+    with option("k1_i8_ctas", 2 if kind == "s_windows64" else -1):
+        mu, C, path = ctx.covariance(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    assert path == 1, "the int8 Gram should serve D <= 256 (D % 4 == 0)"
     rmu, rC = OP.covariance(A, B)
     # mu is the mean of the fixed-point values: within the rounding bound e_j of the grid
     X = np.concatenate([A, B]).astype(np.float64)
     M = 1.1 * np.maximum(np.abs(X).max(0), np.abs(X - rmu).max(0))
-    assert np.all(np.abs(mu - rmu) <= M * (2.0 ** -23 if kind == "offset" else 2.0 ** -30) + 1e-15 * np.abs(rmu))
-    bound = _i8_bound(A, B, kind == "offset")
+    assert np.all(np.abs(mu - rmu) <= M * (2.0 ** -23 if base == "offset" else 2.0 ** -30) + 1e-15 * np.abs(rmu))
+    bound = _i8_bound(A, B, base == "offset")
     frac = np.abs(C - rC) / bound
     assert frac.max() <= 1.0, f"max |dC| / bound = {frac.max():.3f}"
     assert np.array_equal(C, C.T)
@@ -162,12 +175,12 @@ def test_covariance_int8_path(ctx, kind):
 
 
 def test_covariance_dmma_option_and_small_d(ctx):
-    """option k1_path = 0 (and D <= 128 always) keeps the fp64 DMMA Gram: C within 1e-12 of the
-    accumulation scale."""
+    """option k1_path = 0 selects the fp64 DMMA Gram (D % 4 != 0 always takes it): C within 1e-12
+    of the accumulation scale."""
     from oracle import prohd as OP
     from paper_2511_18207_b200 import option
     rng = np.random.default_rng(11)
-    for D, opt in ((256, 0), (96, -1)):
+    for D, opt in ((256, 0), (96, 0), (18, -1)):
         A = rng.standard_normal((20000, D)).astype(np.float32)
         B = (rng.standard_t(4, (15000, D)) + 0.2).astype(np.float32)
         with option("k1_path", opt):

@@ -19,15 +19,21 @@ def ctx():
     return Context(0)
 
 
-def _sim_sharded(ctx, A, B, k, m, G):
-    ph = CudaPhases(ctx)
+def _sim_sharded(ctx, A, B, k, m, G, dmma=True):
+    ph = CudaPhases(ctx, dmma=dmma)
     nA, nB, D = A.shape[0], B.shape[0], A.shape[1]
     la = [row_range(nA, g, G) for g in range(G)]
     lb = [row_range(nB, g, G) for g in range(G)]
     s = ph.shift(A[:4096], B[:4096])
+    # C0: MAX over the shards' column ranges (int8 Gram), C1: SUM of the moments
+    colmax = None
+    for g in range(G):
+        cm = ph.local_colmax(A[la[g][0]:la[g][1]], B[lb[g][0]:lb[g][1]], s)
+        if cm is not None:
+            colmax = cm if colmax is None else torch.maximum(colmax, cm)
     mom = None
     for g in range(G):
-        part = ph.local_moments(A[la[g][0]:la[g][1]], B[lb[g][0]:lb[g][1]], s)
+        part = ph.local_moments(A[la[g][0]:la[g][1]], B[lb[g][0]:lb[g][1]], s, colmax)
         mom = part if mom is None else mom + part
     dirs, nd = ph.directions(mom, nA, nB, D, k, s)
     unions, subsets = [], []
@@ -92,3 +98,48 @@ def test_exact_key_invariant_to_shard_count(ctx, G):
     assert row == one["a"] and np.float32(d2) == np.float32(one["dist2_tc"])
     w = ctx.directed_hd_witness(At[row], Bt)
     assert w["b"] == one["b"] and w["dist2"] == one["dist2"]
+
+
+@pytest.mark.parametrize("cfg,n,G", [(1, None, 2), (3, 30000, 3), (5, 65536, 4), (4, 40000, 8)])
+def test_sharded_int8_moments(ctx, cfg, n, G):
+    """The sharded moments on the int8 Gram (prohd_local_colmax -> MAX -> prohd_local_moments_i8
+    -> SUM): every shard quantises on the grid of the global column maxima, the grid the one-shot
+    call picks, so the directions agree with the one-shot int8 call to fp64 rounding and the
+    selections, subsets and estimate are identical (and equal the oracle's)."""
+    c = datagen.CONFIGS[cfg]
+    A, B = datagen.generate(cfg, n=n)
+    m = c.m(A.shape[0])
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    one = ctx.prohd_estimate(At, Bt, c.k, m, return_dirs=True, return_indices=True)
+    sh = _sim_sharded(ctx, At, Bt, c.k, m, G, dmma=False)
+    assert sh["n_dirs"] == one["n_dirs"]
+    assert np.allclose(sh["U"].T, one["U"], rtol=0, atol=1e-9)
+    assert np.array_equal(sh["IA"], one["IA"]) and np.array_equal(sh["IB"], one["IB"])
+    assert sh["value"] == one["value"]
+    ref = OP.estimate(A, B, c.k, m)
+    assert np.array_equal(sh["IA"], ref["IA"]) and np.array_equal(sh["IB"], ref["IB"])
+
+
+def test_sharded_int8_empty_set_shard(ctx):
+    """A shard holding rows of one set only (nB_local = 0) and an empty shard: the int8 phase
+    calls accept them and the summed moments match the one-shot covariance path."""
+    rng = np.random.default_rng(5)
+    D = 64
+    A = rng.standard_normal((3000, D)).astype(np.float32)
+    B = (rng.standard_normal((2000, D)) + 0.5).astype(np.float32)
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    ph = CudaPhases(ctx, dmma=False)
+    s = ph.shift(At[:4096], Bt[:4096])
+    shards = [(At[:1000], Bt[:0]), (At[1000:3000], Bt[:2000]), (At[:0], Bt[:0])]
+    colmax = None
+    for a_, b_ in shards:
+        cm = ph.local_colmax(a_, b_, s)
+        colmax = cm if colmax is None else torch.maximum(colmax, cm)
+    mom = sum(ph.local_moments(a_, b_, s, colmax) for a_, b_ in shards)
+    X = np.concatenate([A, B]).astype(np.float64) - s
+    G = X.T @ X
+    Gd = mom[2 * D:].cpu().numpy().reshape(D, D)
+    scale = np.abs(X).max(0)
+    assert np.all(np.abs(Gd - G) <= 2.0 ** -26 * X.shape[0] * np.outer(scale, scale))
+    assert np.allclose(mom[:D].cpu().numpy(), (np.asarray(A, np.float64) - s).sum(0), rtol=0,
+                       atol=1e-6 * 3000 * scale.max())
