@@ -40,6 +40,19 @@ struct prohd_ctx {
   // second stream for independent per-set work (the two sets' selection chains overlap)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // CUDA-graph replay of prohd_estimate's stream-ordered phases (prohd_estimate.cu): the
+  // library's own capture stream (the caller's may be the legacy default stream, which cannot
+  // be captured), joined to the caller's stream by events, and a small cache of instantiated
+  // graphs keyed by every argument the enqueued work depends on
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  struct GraphEntry {
+    std::vector<uint8_t> key;
+    cudaGraphExec_t exec = nullptr;
+    long long launches = 0;          // kernels in the graph (added to the launch counter per replay)
+    std::vector<uint8_t> host;       // host-side values the enqueue computed (restored on replay)
+  };
+  std::vector<GraphEntry> graphs;
 };
 
 namespace prohd {
@@ -368,6 +381,62 @@ inline int bidir_on_ops(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D,
   CK(launch_nn64_from_key(C.x, 0, C.n, &w.keys[1], R.x, R.n, D, w.blk_d, w.blk_j, kNNBlocks, &w.nn_d[1],
                           &w.nn_j[1], ctx->stream));
   tspan(ctx, PH_REDUCE, t0);
+  return PROHD_OK;
+}
+
+// Enqueue `work` (stream-ordered launches on ctx->stream and ctx->aux only: no host reads, no
+// host-memory copies) through a cached CUDA graph: the first call with this key captures and
+// instantiates it (the launch counter counts its kernels once, at capture), later calls replay it
+// (count_launch(n) per replay). `host` is a byte image of the host-side values the enqueue
+// computes (saved at capture, restored on replay). A capture the runtime refuses falls back to
+// running `work` eagerly; an error inside `work` is returned as is.
+template <class F>
+int graphed(prohd_ctx* ctx, const std::vector<uint8_t>& key, void* host, size_t host_bytes, F&& work) {
+  for (auto& g : ctx->graphs)
+    if (g.key == key) {
+      if (host_bytes) std::memcpy(host, g.host.data(), host_bytes);
+      count_launch(static_cast<int>(g.launches));
+      CK(cudaGraphLaunch(g.exec, ctx->stream));
+      return PROHD_OK;
+    }
+  const long long l0 = launch_counter().load();
+  if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return work();
+  }
+  const int rc = work();
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (e != cudaSuccess || graph == nullptr) {  // capture invalidated: run eagerly
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    ctx->err.clear();
+    launch_counter().store(l0);
+    return work();
+  }
+  if (rc != PROHD_OK) {
+    cudaGraphDestroy(graph);
+    return rc;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) {
+    cudaGetLastError();
+    launch_counter().store(l0);
+    return work();
+  }
+  prohd_ctx::GraphEntry ent;
+  ent.key = key;
+  ent.exec = exec;
+  ent.launches = launch_counter().load() - l0;
+  ent.host.assign(static_cast<const uint8_t*>(host), static_cast<const uint8_t*>(host) + host_bytes);
+  if (ctx->graphs.size() >= 8) {  // small FIFO cache
+    cudaGraphExecDestroy(ctx->graphs.front().exec);
+    ctx->graphs.erase(ctx->graphs.begin());
+  }
+  ctx->graphs.push_back(std::move(ent));
+  CK(cudaGraphLaunch(exec, ctx->stream));
   return PROHD_OK;
 }
 

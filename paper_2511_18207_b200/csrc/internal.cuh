@@ -33,6 +33,7 @@ enum OptId {
   OPT_K1_ABLATE,     // int8 Gram timing ablations (wrong results): 1 no slicing work, 2 no MMAs
   OPT_K4_SAMPLED,    // 0 radix K4 over all projections, 1 sampled-threshold K4 wherever it applies
   OPT_K1_I8_CTAS,    // int8 Gram: cap on the CTA count (tests: mid-sweep drains at small sizes)
+  OPT_GRAPH,         // 0: prohd_estimate launches eagerly (no CUDA-graph replay)
   OPT_COUNT
 };
 inline std::atomic<long long>* option_table() {

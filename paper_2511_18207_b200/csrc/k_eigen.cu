@@ -56,7 +56,26 @@ __device__ __forceinline__ double rcp_normal(double q) {
   return fma(r, e, r);
 }
 __device__ __forceinline__ double rcp_safe(double q) { return fabs(q) >= 0x1p-1000 ? rcp_normal(q) : 1.0 / q; }
+// 1/sqrt(x) for normal x > 0: hardware approximation + 2 Newton steps (~1 ulp); off the IEEE sqrt
+// and division sequences on the Householder step's serial chain. Tiny / zero x: the IEEE path.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  if (!(x >= 0x1p-1000)) return 1.0 / sqrt(x);
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double h = 0.5 * x;
+  r = r * fma(-h * r, r, 1.5);
+  r = r * fma(-h * r, r, 1.5);
+  return r;
+}
 
+// 1/q for the Sturm count: hardware approximation + ONE Newton step (relative error ~2^-44: the
+// count is that of T with the e2 perturbed by ~2^-44 relative, well inside what bisection to
+// 2 eps needs; the q-form recurrence stays backward stable)
+__device__ __forceinline__ double rcp_sturm(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  return fma(r, fma(-q, r, 1.0), r);
+}
 // number of eigenvalues of T (d, e2 = e^2) strictly less than x (Sturm count); |q| >= pivmin
 // (> DBL_MIN) at every division, so the reciprocal is taken on normal numbers
 __device__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
@@ -65,7 +84,7 @@ __device__ int sturm_count(const double* d, const double* e2, int n, double x, d
   if (fabs(q) < pivmin) q = -pivmin;
   if (q < 0) ++cnt;
   for (int i = 1; i < n; ++i) {
-    q = d[i] - x - e2[i - 1] * rcp_normal(q);
+    q = d[i] - x - e2[i - 1] * rcp_sturm(q);
     if (fabs(q) < pivmin) q = -pivmin;
     if (q < 0) ++cnt;
   }
@@ -241,14 +260,14 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
       x0 = (c == j + 1) ? xt : x0;
     }
     const double nrm2 = warp_sum(ss);
-    const double nrm = sqrt(nrm2);
+    const double nrm = nrm2 > 0.0 ? nrm2 * rsqrt_nr(nrm2) : 0.0;
     x0 = __shfl_sync(0xffffffffu, x0, (j + 1) & 31);
     const double alpha = (x0 > 0.0) ? -nrm : nrm;
     const double v0 = x0 - alpha;
     const double vn2 = nrm2 - x0 * x0 + v0 * v0;
     // sc == 0: the column is already zero below the subdiagonal, H = I (v = 0, p = 0, K = 0:
     // the update below is then a no-op and the next column comes out unchanged)
-    const double sc = (vn2 > 0.0 && nrm > 0.0) ? 1.0 / sqrt(vn2) : 0.0;
+    const double sc = (vn2 > 0.0 && nrm > 0.0) ? rsqrt_nr(vn2) : 0.0;
     double v[kTq];
 #pragma unroll
     for (int t = 0; t < kTq; ++t) {
@@ -455,30 +474,57 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
   // ---------------------------------------------------------------- 4. back-transform, sign, output
   for (int w = rank * kWarps + warp; w < kk; w += kCl * kWarps) {
     double* y = a.X + static_cast<int64_t>(w) * D;
-    // y <- H_0 H_1 ... H_{D-3} y with y in registers (lane holds y[lane + 32 t]) and the next
-    // reflector's row prefetched into registers while the current one is applied
+    // y <- H_0 H_1 ... H_{D-3} y with y in registers (lane holds y[lane + 32 t]), H_j = I - 2 v_j v_j^T.
+    // Reflectors are applied in PAIRS with one warp reduction: a = v_j.y, b = v_{j-1}.y and
+    // c = v_{j-1}.v_j reduced together, then y -= 2 a v_j and y -= 2 (b - 2 a c) v_{j-1}
+    // (= v_{j-1}.(H_j y)); the rows of the next two pairs are prefetched into registers, so the
+    // global-memory latency of V is not on the chain.
     constexpr int kYT = kMaxD / 32;
-    double yr[kYT], vn[kYT];
+    double yr[kYT];
+    double p0[kYT], p1[kYT], q0[kYT], q1[kYT], r0[kYT], r1[kYT];
+    auto ldrow = [&](int j, double(&r)[kYT]) {
+#pragma unroll
+      for (int t = 0; t < kYT; ++t) {
+        const int i = lane + 32 * t;
+        r[t] = (j >= 0 && i > j && i < D) ? a.V[static_cast<int64_t>(j) * D + i] : 0.0;  // v_j[i], i > j
+      }
+    };
 #pragma unroll
     for (int t = 0; t < kYT; ++t) {
       const int i = lane + 32 * t;
       yr[t] = i < D ? y[i] : 0.0;
-      vn[t] = (D >= 3 && i < D) ? a.V[static_cast<int64_t>(D - 3) * D + i] : 0.0;
     }
-    for (int j = D - 3; j >= 0; --j) {
-      double vc[kYT];
+    const int J = D - 3;
+    ldrow(J, p0);
+    ldrow(J - 1, p1);
+    ldrow(J - 2, q0);
+    ldrow(J - 3, q1);
+    for (int j = J; j >= 0; j -= 2) {
+      ldrow(j - 4, r0);
+      ldrow(j - 5, r1);
+      double sa = 0.0, sb = 0.0, scc = 0.0;
 #pragma unroll
       for (int t = 0; t < kYT; ++t) {
-        const int i = lane + 32 * t;
-        vc[t] = i > j ? vn[t] : 0.0;  // V row j holds v_j[i] for i > j only
-        if (j > 0 && i < D) vn[t] = a.V[static_cast<int64_t>(j - 1) * D + i];
+        sa = fma(p0[t], yr[t], sa);
+        sb = fma(p1[t], yr[t], sb);
+        scc = fma(p1[t], p0[t], scc);
       }
-      double s = 0.0;
 #pragma unroll
-      for (int t = 0; t < kYT; ++t) s = fma(vc[t], yr[t], s);
-      s = 2.0 * warp_sum(s);
+      for (int o = 16; o > 0; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        scc += __shfl_xor_sync(0xffffffffu, scc, o);
+      }
+      const double s2 = sb - 2.0 * sa * scc;
 #pragma unroll
-      for (int t = 0; t < kYT; ++t) yr[t] = fma(-s, vc[t], yr[t]);
+      for (int t = 0; t < kYT; ++t) {
+        yr[t] = fma(-2.0 * sa, p0[t], yr[t]);
+        yr[t] = fma(-2.0 * s2, p1[t], yr[t]);
+        p0[t] = q0[t];
+        p1[t] = q1[t];
+        q0[t] = r0[t];
+        q1[t] = r1[t];
+      }
     }
 #pragma unroll
     for (int t = 0; t < kYT; ++t) {

@@ -1236,6 +1236,64 @@ cudaError_t launch_select_fallback(const float* X, int64_t n, int D, const doubl
   return cudaGetLastError();
 }
 
+// prohd_estimate's host reads, gathered into one small buffer (one D2H copy per read point):
+// status: [0,1] union sizes, [2,3] overflow flags, [4,5] max squared-norm bits, [6] n_dirs,
+// [7] int8-Gram range flag, [8,9] sampled-threshold certification failures (0 for null sources)
+__global__ void pack_status_kernel(StatusSrc src, unsigned* out) {
+  const int t = threadIdx.x;
+  unsigned v = 0;
+  switch (t) {
+    case 0: v = *src.uc[0]; break;
+    case 1: v = *src.uc[1]; break;
+    case 2: v = static_cast<unsigned>(*src.ovf[0]); break;
+    case 3: v = static_cast<unsigned>(*src.ovf[1]); break;
+    case 4: v = *src.maxn[0]; break;
+    case 5: v = *src.maxn[1]; break;
+    case 6: v = static_cast<unsigned>(*src.ndirs); break;
+    case 7: v = src.i8ovf ? *src.i8ovf : 0u; break;
+    case 8: v = src.sfail[0] ? static_cast<unsigned>(*src.sfail[0]) : 0u; break;
+    case 9: v = src.sfail[1] ? static_cast<unsigned>(*src.sfail[1]) : 0u; break;
+    default: return;
+  }
+  out[t] = v;
+}
+cudaError_t launch_pack_status(const StatusSrc& src, unsigned* out, cudaStream_t st) {
+  count_launch();
+  pack_status_kernel<<<1, 32, 0, st>>>(src, out);
+  return cudaGetLastError();
+}
+
+// the end of prohd_estimate: both directed results with the witness rows mapped to original
+// indices through the unions (uA, uB; null = the columns already are original indices)
+__global__ void pack_result_kernel(const unsigned long long* keys, const double* nn_d, const long long* nn_j,
+                                   const long long* uA, const long long* uB, bool map_cols, EstResultDev* out) {
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < 2; ++s) {
+    const unsigned long long key = keys[s];
+    const long long row = static_cast<long long>(0xFFFFFFFFu - static_cast<unsigned>(key & 0xFFFFFFFFull));
+    const long long* ur = s == 0 ? uA : uB;  // rows: subset of the first set of this direction
+    const long long* uc = s == 0 ? uB : uA;
+    out->key[s] = key;
+    out->d2[s] = nn_d[s];
+    out->a[s] = ur[row];
+    out->b[s] = map_cols ? uc[nn_j[s]] : nn_j[s];
+  }
+}
+cudaError_t launch_pack_result(const unsigned long long* keys, const double* nn_d, const long long* nn_j,
+                               const long long* uA, const long long* uB, bool map_cols, EstResultDev* out,
+                               cudaStream_t st) {
+  count_launch();
+  pack_result_kernel<<<1, 32, 0, st>>>(keys, nn_d, nn_j, uA, uB, map_cols, out);
+  return cudaGetLastError();
+}
+
+__global__ void set_int_kernel(int* a, int v) { *a = v; }
+cudaError_t launch_set_int(int* a, int v, cudaStream_t st) {
+  count_launch();
+  set_int_kernel<<<1, 1, 0, st>>>(a, v);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_minus_one(const int* a, int* b, cudaStream_t st) {
   count_launch();
   minus_one_kernel<<<1, 1, 0, st>>>(a, b);

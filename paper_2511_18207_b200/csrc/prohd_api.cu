@@ -28,7 +28,7 @@ const char* prohd_version(void) { return "prohd-b200 0.1 sm_100a"; }
 static const char* const kOptNames[prohd::OPT_COUNT] = {
     "k6_variant", "k6_split3", "k6_bidir_2a", "k6_splits_2x", "k1_path", "k1_ctas",
     "k1_cs_sms",  "k1_beta_milli", "shift", "k3_simt", "eig_stop", "eig_cl", "k1_ablate",
-    "k4_sampled", "k1_i8_ctas"};
+    "k4_sampled", "k1_i8_ctas", "graph"};
 
 int prohd_set_option(const char* name, int64_t value) {
   if (name == nullptr) return PROHD_E_INVALID;
@@ -77,6 +77,11 @@ int prohd_destroy(prohd_ctx* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  for (auto& g : ctx->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   delete ctx;
   return PROHD_OK;
 }

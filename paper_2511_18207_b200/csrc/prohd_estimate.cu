@@ -5,8 +5,9 @@
 //   step 2   K3 projections onto U = [u0 u1..uk]                     (Alg.1 l.3-4, Alg.2 l.5-7)
 //   step 3   K4 top/bottom-m per direction, K5 union + gather        (Alg.1 l.5-9, Alg.2 l.8-11, Alg.3 l.4-5)
 //   step 4   K0+K6+K7 exact HD on the subsets, both directions       (Alg.3 l.6-7)
-// One host synchronisation (after step 3) reads the subset sizes to size the
-// distance-kernel launches; everything else is stream-ordered.
+// One host synchronisation (after step 3) reads the subset sizes to size the distance-kernel
+// launches (one packed device-to-host copy of every status word); everything else is
+// stream-ordered, and the result comes back in one packed copy.
 #include "api_common.cuh"
 #include "prohd_kernels.cuh"
 #include "prohd_steps.cuh"
@@ -39,6 +40,8 @@ struct EstWs {
   long long* blk_j = nullptr;
   int* bad = nullptr;
   double* centre = nullptr;  // [2D] common centre of the subset pair (K0)
+  unsigned* status = nullptr;  // [kStatusWords] the mid-pipeline host read (pack_status_kernel)
+  EstResultDev* res = nullptr;  // the final host read (pack_result_kernel)
   int64_t capU[2] = {0, 0};
 };
 
@@ -108,6 +111,8 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
   w.blk_j = c.take<long long>(kNNBlocks);
   w.bad = c.take<int>(1);
   w.centre = c.take<double>(2 * static_cast<int64_t>(D));
+  w.status = c.take<unsigned>(kStatusWords);
+  w.res = c.take<EstResultDev>(1);
   return c.off;
 }
 
@@ -144,11 +149,72 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   Carver c{ctx->ws, 0, ctx->ws_bytes, false};
   EstWs w;
   carve_est(c, w, nA, nB, D, k, m, host_in, ctx->num_sms, certified);
-  cudaStream_t st = ctx->stream;
   bool hi;
   if ((rc = stage_inputs(ctx, A, nA, B, nB, D, w.stageA, w.stageB, hi))) return rc;
-  CK(cudaMemsetAsync(w.bad, 0, sizeof(int), st));
-  CK(cudaMemsetAsync(w.U64, 0, sizeof(double) * L * D, st));
+  // the second stream of the selection chains, created outside any capture
+  if (ctx->aux == nullptr) {
+    CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
+  // CUDA-graph replay (api_common.cuh graphed()) of the two stream-ordered stretches of the call:
+  // steps 1-3 up to the status read, and step 4 up to the result read. Used for the plain
+  // estimate on device inputs without tracing; the work runs on the library's capture stream,
+  // ordered after and before the caller's stream by events.
+  const bool use_graph = dirs_in == nullptr && counts == nullptr && !certified && !host_in && !ctx->timing &&
+                         opt(OPT_GRAPH) != 0;
+  if (use_graph && ctx->gstream == nullptr) {
+    CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+  }
+  struct StreamSwap {
+    prohd_ctx* c;
+    cudaStream_t orig;
+    bool on;
+    StreamSwap(prohd_ctx* c_, bool on_) : c(c_), orig(c_->stream), on(on_) {
+      if (!on) return;
+      cudaEventRecord(c->ev_in, orig);
+      cudaStreamWaitEvent(c->gstream, c->ev_in, 0);
+      c->stream = c->gstream;
+    }
+    ~StreamSwap() {
+      if (!on) return;
+      cudaEventRecord(c->ev_out, c->gstream);
+      cudaStreamWaitEvent(orig, c->ev_out, 0);
+      c->stream = orig;
+    }
+  } swap_guard(ctx, use_graph);
+  cudaStream_t st = ctx->stream;
+  struct Key {
+    int phase, use_i8;
+    const void *A, *B, *ws;
+    int64_t nA, nB, m, uc0, uc1;
+    size_t ws_bytes;
+    int D, k, num_sms;
+    long long opts[OPT_COUNT];
+  };
+  auto make_key = [&](int phase, int i8, int64_t uc0, int64_t uc1) {
+    Key kk;
+    std::memset(&kk, 0, sizeof kk);  // padding bytes too: the key is compared as bytes
+    kk.phase = phase;
+    kk.use_i8 = i8;
+    kk.A = A;
+    kk.B = B;
+    kk.ws = ctx->ws;
+    kk.nA = nA;
+    kk.nB = nB;
+    kk.m = m;
+    kk.uc0 = uc0;
+    kk.uc1 = uc1;
+    kk.ws_bytes = ctx->ws_bytes;
+    kk.D = D;
+    kk.k = k;
+    kk.num_sms = ctx->num_sms;
+    for (int i = 0; i < OPT_COUNT; ++i) kk.opts[i] = opt(static_cast<OptId>(i));
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(&kk);
+    return std::vector<uint8_t>(b, b + sizeof kk);
+  };
 
   // ------------------------------------------------------------ step 1: directions
   // moments on the int8 tensor cores where planned (k_gram_i8.cu), else the fp64 DMMA Gram;
@@ -168,8 +234,7 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
         CK(launch_eigen_topk(w.mom.C, D, k, w.V, w.Xe, w.U64, w.U32, w.lam, w.n_dirs, st));
         tspan(ctx, PH_EIGEN, t0);
       } else {
-        const int one = 1;
-        CK(cudaMemcpyAsync(w.n_dirs, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+        CK(launch_set_int(w.n_dirs, 1, st));
       }
       CK(launch_dirs_to_f32(w.U64, w.U32, L, D, st));
     } else {
@@ -180,7 +245,6 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
     return PROHD_OK;
   };
   bool use_i8 = dirs_in == nullptr && mp.i8;
-  if ((rc = directions(use_i8))) return rc;
 
   // ------------------------------------------------------------ steps 2-3: projection, selection, union
   const float* X[2] = {A, B};
@@ -193,16 +257,11 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   bool sampled[2] = {false, false};
   int64_t msel[2] = {m, m};
   int sfail[2] = {0, 0};
-  auto select_and_read = [&]() -> int {
+  auto enqueue_select = [&]() -> int {
     sampled[0] = sampled[1] = false;
     const int t_sel = tmark(ctx);
     // set B's chain runs on the context's second stream, set A's on the caller's: the low-occupancy
     // tail of one set's selection (collect, re-rank, compaction) overlaps the other's projection
-    if (ctx->aux == nullptr) {
-      CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
-    }
     if (counts && L > 1) CK(launch_minus_one(w.n_dirs, w.n_dirs1, st));  // shared by both sets
     CK(cudaEventRecord(ctx->ev_fork, st));
     CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
@@ -257,37 +316,82 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
     CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     CK(e_chain);
     tspan(ctx, PH_SELECT, t_sel);
-    CK(cudaMemcpyAsync(&ucount[0], w.sel[0].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&ucount[1], w.sel[1].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&ovf[0], w.sel[0].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&ovf[1], w.sel[1].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&maxn[0], w.sel[0].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&maxn[1], w.sel[1].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&ndirs, w.n_dirs, sizeof(int), cudaMemcpyDeviceToHost, st));
-    if (use_i8) CK(cudaMemcpyAsync(&i8ovf, w.mom.i8ovf, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    for (int s = 0; s < 2; ++s) {
-      sfail[s] = 0;
-      if (sampled[s]) CK(cudaMemcpyAsync(&sfail[s], w.sel[s].sfail, sizeof(int), cudaMemcpyDeviceToHost, st));
-    }
+    return PROHD_OK;
+  };
+  // every value the host needs after the selection, packed on the device (one D2H copy)
+  auto pack_status = [&](bool with_sfail) -> int {
+    StatusSrc src{{w.sel[0].ucount, w.sel[1].ucount}, {w.sel[0].overflow, w.sel[1].overflow},
+                  {w.sel[0].maxnorm2, w.sel[1].maxnorm2}, w.n_dirs, use_i8 ? w.mom.i8ovf : nullptr,
+                  {with_sfail && sampled[0] ? w.sel[0].sfail : nullptr,
+                   with_sfail && sampled[1] ? w.sel[1].sfail : nullptr}};
+    CK(launch_pack_status(src, w.status, st));
+    return PROHD_OK;
+  };
+  auto read_status = [&]() -> int {
+    unsigned h[kStatusWords];
+    CK(cudaMemcpyAsync(h, w.status, sizeof h, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    for (int q = 0; q < 2; ++q) {
+      ucount[q] = h[q];
+      ovf[q] = static_cast<int>(h[2 + q]);
+      maxn[q] = h[4 + q];
+      sfail[q] = static_cast<int>(h[8 + q]);
+    }
+    ndirs = static_cast<int>(h[6]);
+    i8ovf = h[7];
+    return PROHD_OK;
+  };
+  // steps 1-3 as one stream-ordered stretch (graph-captured when use_graph)
+  auto steps123 = [&]() -> int {
+    int r2;
+    CK(cudaMemsetAsync(w.bad, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(w.U64, 0, sizeof(double) * L * D, st));
+    if ((r2 = directions(use_i8))) return r2;
+    if ((r2 = enqueue_select())) return r2;
+    return pack_status(true);
+  };
+  auto select_and_read = [&]() -> int {
+    if (use_graph) {
+      struct {
+        double eps[2];
+        int64_t msel[2];
+        bool sampled[2];
+      } hv;
+      std::memset(&hv, 0, sizeof hv);
+      const int r2 = graphed(ctx, make_key(1, use_i8 ? 1 : 0, 0, 0), &hv, sizeof hv, [&]() -> int {
+        const int r3 = steps123();
+        for (int q = 0; q < 2; ++q) {
+          hv.eps[q] = eps[q];
+          hv.msel[q] = msel[q];
+          hv.sampled[q] = sampled[q];
+        }
+        return r3;
+      });
+      if (r2) return r2;
+      for (int q = 0; q < 2; ++q) {
+        eps[q] = hv.eps[q];
+        msel[q] = hv.msel[q];
+        sampled[q] = hv.sampled[q];
+      }
+    } else {
+      const int r2 = steps123();
+      if (r2) return r2;
+    }
+    if ((rc = read_status())) return rc;
     if (sfail[0] || sfail[1]) {
       // a sampled threshold could not be certified for some list (ties or a sample far off the
       // tail): the radix K4 for that set, from the projections again
-      for (int s = 0; s < 2; ++s) {
-        if (!sfail[s]) continue;
-        CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, msel[s], w.sel[s], st, true, true, &eps[s]));
-        CK(cudaMemcpyAsync(&ucount[s], w.sel[s].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&ovf[s], w.sel[s].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&maxn[s], w.sel[s].maxnorm2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-      }
-      CK(cudaStreamSynchronize(st));
+      for (int s = 0; s < 2; ++s)
+        if (sfail[s])
+          CK(launch_select(X[s], n[s], D, w.U64, w.U32, L, w.n_dirs, msel[s], w.sel[s], st, true, true, &eps[s]));
+      if ((rc = pack_status(false))) return rc;
+      if ((rc = read_status())) return rc;
     }
     return PROHD_OK;
   };
   if ((rc = select_and_read())) return rc;
-  if (use_i8 && i8ovf) {  // a value outside the int8 Gram's sampled range: rerun on the DMMA Gram
+  if (use_i8 && i8ovf) {  // a value outside the int8 Gram's range (non-finite input): rerun on the DMMA Gram
     use_i8 = false;
-    if ((rc = directions(false))) return rc;
     if ((rc = select_and_read())) return rc;
   }
   for (int s = 0; s < 2; ++s) {
@@ -301,72 +405,76 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
     // streaming band select for the affected lists, then the union again (rare path)
     for (int s = 0; s < 2; ++s)
       if (ovf[s]) CK(launch_select_fallback(X[s], n[s], D, w.U64, L, w.n_dirs, m, w.sel[s], eps[s], st, true));
-    for (int s = 0; s < 2; ++s)
-      CK(cudaMemcpyAsync(&ucount[s], w.sel[s].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    unsigned uc2[2];
+    CK(cudaMemcpyAsync(&uc2[0], w.sel[0].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&uc2[1], w.sel[1].ucount, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    ucount[0] = uc2[0];
+    ucount[1] = uc2[1];
   }
   if (ucount[0] < 1 || ucount[1] < 1 || ucount[0] > w.capU[0] || ucount[1] > w.capU[1])
     return fail(ctx, PROHD_E_INTERNAL, "bad union sizes %u %u", ucount[0], ucount[1]);
 
   // ------------------------------------------------------------ step 4: exact HD on the subsets
-  const int t_sub = tmark(ctx);
-  for (int s = 0; s < 2; ++s) CK(launch_gather(X[s], D, w.sel[s].uidx, w.sel[s].ucount, ucount[s], w.Xs[s], st));
-  // one common centre for every operand of the subset HD: centre(A_sel, B_sel) (symmetric;
-  // the sharded driver computes the same from the all-gathered subsets)
-  CK(launch_centre(w.Xs[0], ucount[0], w.Xs[1], ucount[1], D, w.centre, st));
-  if (!certified && (rc = prep_pair(ctx, w.Xs[0], ucount[0], w.Xs[1], ucount[1], D, w.ops[0], w.ops[1], w.bad,
-                                     w.centre)))
-    return rc;
-  ExactWs ew;
-  ew.rowmin = w.rowmin;
-  ew.colmin = w.colmin;
-  ew.keys = w.keys;
-  ew.nn_d = w.nn_d;
-  ew.nn_j = w.nn_j;
-  ew.blk_d = w.blk_d;
-  ew.blk_j = w.blk_j;
-  if (!certified) {
-    if ((rc = bidir_on_ops(ctx, w.ops[0], w.ops[1], D, ew))) return rc;  // Alg. 3 line 6, both directions
-  } else {
-    // certified mode (SPEC.md:279 subset-full): rows of each subset against the FULL other set
-    // two pairs, each prepared together: (A_sel, B) and (B_sel, A)
-    if ((rc = prep_pair(ctx, w.Xs[0], ucount[0], B, nB, D, w.ops[0], w.full[1], w.bad, w.centre))) return rc;
-    if ((rc = prep_pair(ctx, w.Xs[1], ucount[1], A, nA, D, w.ops[1], w.full[0], w.bad, w.centre))) return rc;
-    if ((rc = directed_on_ops(ctx, w.ops[0], w.full[1], D, ew, 0))) return rc;
-    if ((rc = directed_on_ops(ctx, w.ops[1], w.full[0], D, ew, 1))) return rc;
-  }
-  tspan(ctx, PH_SUBSET, t_sub);
-  unsigned long long keys[2];
-  double nn_d[2];
-  long long nn_j[2];
-  CK(cudaMemcpyAsync(keys, w.keys, sizeof keys, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(nn_d, w.nn_d, sizeof nn_d, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(nn_j, w.nn_j, sizeof nn_j, cudaMemcpyDeviceToHost, st));
-  std::vector<long long> ua(ucount[0]), ub(ucount[1]);
-  CK(cudaMemcpyAsync(ua.data(), w.sel[0].uidx, sizeof(long long) * ucount[0], cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(ub.data(), w.sel[1].uidx, sizeof(long long) * ucount[1], cudaMemcpyDeviceToHost, st));
+  auto step4 = [&]() -> int {
+    int r2;
+    const int t_sub = tmark(ctx);
+    for (int s = 0; s < 2; ++s) CK(launch_gather(X[s], D, w.sel[s].uidx, w.sel[s].ucount, ucount[s], w.Xs[s], st));
+    // one common centre for every operand of the subset HD: centre(A_sel, B_sel) (symmetric;
+    // the sharded driver computes the same from the all-gathered subsets)
+    CK(launch_centre(w.Xs[0], ucount[0], w.Xs[1], ucount[1], D, w.centre, st));
+    if (!certified && (r2 = prep_pair(ctx, w.Xs[0], ucount[0], w.Xs[1], ucount[1], D, w.ops[0], w.ops[1], w.bad,
+                                      w.centre)))
+      return r2;
+    ExactWs ew;
+    ew.rowmin = w.rowmin;
+    ew.colmin = w.colmin;
+    ew.keys = w.keys;
+    ew.nn_d = w.nn_d;
+    ew.nn_j = w.nn_j;
+    ew.blk_d = w.blk_d;
+    ew.blk_j = w.blk_j;
+    if (!certified) {
+      if ((r2 = bidir_on_ops(ctx, w.ops[0], w.ops[1], D, ew))) return r2;  // Alg. 3 line 6, both directions
+    } else {
+      // certified mode (SPEC.md:279 subset-full): rows of each subset against the FULL other set
+      // two pairs, each prepared together: (A_sel, B) and (B_sel, A)
+      if ((r2 = prep_pair(ctx, w.Xs[0], ucount[0], B, nB, D, w.ops[0], w.full[1], w.bad, w.centre))) return r2;
+      if ((r2 = prep_pair(ctx, w.Xs[1], ucount[1], A, nA, D, w.ops[1], w.full[0], w.bad, w.centre))) return r2;
+      if ((r2 = directed_on_ops(ctx, w.ops[0], w.full[1], D, ew, 0))) return r2;
+      if ((r2 = directed_on_ops(ctx, w.ops[1], w.full[0], D, ew, 1))) return r2;
+    }
+    tspan(ctx, PH_SUBSET, t_sub);
+    // witnesses mapped to original indices on the device (one copy of the result below)
+    CK(launch_pack_result(w.keys, w.nn_d, w.nn_j, w.sel[0].uidx, w.sel[1].uidx, !certified, w.res, st));
+    return PROHD_OK;
+  };
+  if (use_graph)
+    rc = graphed(ctx, make_key(2, use_i8 ? 1 : 0, ucount[0], ucount[1]), nullptr, 0, step4);
+  else
+    rc = step4();
+  if (rc) return rc;
+  EstResultDev res;
+  CK(cudaMemcpyAsync(&res, w.res, sizeof res, cudaMemcpyDeviceToHost, st));
+  if (idxA_out)
+    CK(cudaMemcpyAsync(idxA_out, w.sel[0].uidx, sizeof(long long) * ucount[0], cudaMemcpyDeviceToHost, st));
+  if (idxB_out)
+    CK(cudaMemcpyAsync(idxB_out, w.sel[1].uidx, sizeof(long long) * ucount[1], cudaMemcpyDeviceToHost, st));
   if (dirs_out != nullptr)
     CK(cudaMemcpyAsync(dirs_out, w.U64, sizeof(double) * L * D, cudaMemcpyDeviceToHost, st));
   call_end(ctx);
   CK(cudaStreamSynchronize(st));
   call_collect(ctx);
 
-  fill_directed(&out->ab, keys[0], nn_d[0], nn_j[0]);
-  fill_directed(&out->ba, keys[1], nn_d[1], nn_j[1]);
-  // map subset rows to original indices (a in the first argument, b in the second)
-  out->ab.a = ua[out->ab.a];
-  out->ba.a = ub[out->ba.a];
-  if (!certified) {  // certified mode: the columns already are the full sets
-    out->ab.b = ub[out->ab.b];
-    out->ba.b = ua[out->ba.b];
-  }
+  fill_directed(&out->ab, res.key[0], res.d2[0], res.b[0]);
+  fill_directed(&out->ba, res.key[1], res.d2[1], res.b[1]);
+  out->ab.a = res.a[0];  // original indices (a in the first argument, b in the second)
+  out->ba.a = res.a[1];
   out->value = out->ab.dist2 >= out->ba.dist2 ? out->ab.dist : out->ba.dist;
   out->size_a = ucount[0];
   out->size_b = ucount[1];
   out->n_dirs = ndirs;
   out->_pad = 0;
-  if (idxA_out) std::memcpy(idxA_out, ua.data(), sizeof(long long) * ucount[0]);
-  if (idxB_out) std::memcpy(idxB_out, ub.data(), sizeof(long long) * ucount[1]);
   return PROHD_OK;
 }
 

@@ -157,6 +157,25 @@ cudaError_t launch_select_fallback(const float* X, int64_t n, int D, const doubl
                                    int64_t m, const SelectBufs& b, double eps_coef, cudaStream_t st, bool compact,
                                    double* cval_out = nullptr, long long* cidx_out = nullptr,
                                    int64_t row_offset = 0);
+struct StatusSrc {
+  const unsigned* uc[2];
+  const int* ovf[2];
+  const unsigned* maxn[2];
+  const int* ndirs;
+  const unsigned* i8ovf;  // may be null
+  const int* sfail[2];    // may be null
+};
+constexpr int kStatusWords = 10;
+cudaError_t launch_pack_status(const StatusSrc& src, unsigned* out, cudaStream_t st);
+struct EstResultDev {
+  unsigned long long key[2];  // packed (d2 bits, ~row) of h(A_sel, .) and h(B_sel, .)
+  double d2[2];               // fp64 witness distances
+  long long a[2], b[2];       // witnesses as original indices
+};
+cudaError_t launch_pack_result(const unsigned long long* keys, const double* nn_d, const long long* nn_j,
+                               const long long* uA, const long long* uB, bool map_cols, EstResultDev* out,
+                               cudaStream_t st);
+cudaError_t launch_set_int(int* a, int v, cudaStream_t st);  // *a = v (stream-ordered, capturable)
 cudaError_t launch_minus_one(const int* a, int* b, cudaStream_t st);  // *b = max(*a - 1, 0)
 // Sharded selection: local top/bottom-m lists with their fp64 projection values and GLOBAL
 // indices (row_offset + local row) -> cval_out/cidx_out [L][2][m] (index -1 = empty slot).
