@@ -138,6 +138,7 @@ struct ExactWs {
   long long* blk_j = nullptr;
   int* bad = nullptr;
   double* centre = nullptr;  // [2D]: the pair's common centre (K0), then scratch
+  void* res = nullptr;       // ExactResDev: the packed result (prohd_api.cu)
 };
 
 inline void carve_set(Carver& c, SetOps& s, int64_t n, int D) {
@@ -166,6 +167,7 @@ inline size_t carve_exact(Carver& c, ExactWs& w, int64_t nA, int64_t nB, int D, 
   w.blk_j = c.take<long long>(kNNBlocks);
   w.bad = c.take<int>(1);
   w.centre = c.take<double>(2 * static_cast<int64_t>(D));
+  w.res = c.take<uint8_t>(64);
   return c.off;
 }
 
@@ -438,6 +440,51 @@ int graphed(prohd_ctx* ctx, const std::vector<uint8_t>& key, void* host, size_t 
   ctx->graphs.push_back(std::move(ent));
   CK(cudaGraphLaunch(exec, ctx->stream));
   return PROHD_OK;
+}
+
+// The library's capture stream for graphed() work: created on first use; while a GraphStream is
+// alive ctx->stream is the capture stream, ordered after the caller's stream (event) and the
+// caller's stream ordered after it again on destruction.
+inline int ensure_gstream(prohd_ctx* ctx) {
+  if (ctx->gstream != nullptr) return PROHD_OK;
+  CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+  return PROHD_OK;
+}
+struct GraphStream {
+  prohd_ctx* c;
+  cudaStream_t orig;
+  bool on;
+  GraphStream(prohd_ctx* c_, bool on_) : c(c_), orig(c_->stream), on(on_ && c_->gstream != nullptr) {
+    if (!on) return;
+    cudaEventRecord(c->ev_in, orig);
+    cudaStreamWaitEvent(c->gstream, c->ev_in, 0);
+    c->stream = c->gstream;
+  }
+  ~GraphStream() {
+    if (!on) return;
+    cudaEventRecord(c->ev_out, c->gstream);
+    cudaStreamWaitEvent(orig, c->ev_out, 0);
+    c->stream = orig;
+  }
+};
+// Graph-cache key: the raw bytes of every argument the enqueued work depends on, plus the option
+// table and the workspace (pointer, size).
+struct KeyBuf {
+  std::vector<uint8_t> b;
+  template <typename T>
+  KeyBuf& add(const T& v) {
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(&v);
+    b.insert(b.end(), p, p + sizeof(T));
+    return *this;
+  }
+};
+inline KeyBuf graph_key(prohd_ctx* ctx, int tag) {
+  KeyBuf k;
+  k.add(tag).add(ctx->ws).add(ctx->ws_bytes).add(ctx->num_sms);
+  for (int i = 0; i < OPT_COUNT; ++i) k.add(opt(static_cast<OptId>(i)));
+  return k;
 }
 
 inline void fill_directed(prohd_directed* o, unsigned long long key, double d2, long long j) {

@@ -1294,6 +1294,24 @@ cudaError_t launch_set_int(int* a, int v, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+__global__ void pack_exact_kernel(const unsigned long long* keys, const double* nn_d, const long long* nn_j,
+                                  const int* bad, ExactResDev* out) {
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < 2; ++s) {
+    out->key[s] = keys[s];
+    out->d2[s] = nn_d[s];
+    out->j[s] = nn_j[s];
+  }
+  out->bad = *bad;
+  out->_pad = 0;
+}
+cudaError_t launch_pack_exact(const unsigned long long* keys, const double* nn_d, const long long* nn_j,
+                              const int* bad, ExactResDev* out, cudaStream_t st) {
+  count_launch();
+  pack_exact_kernel<<<1, 32, 0, st>>>(keys, nn_d, nn_j, bad, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_minus_one(const int* a, int* b, cudaStream_t st) {
   count_launch();
   minus_one_kernel<<<1, 1, 0, st>>>(a, b);

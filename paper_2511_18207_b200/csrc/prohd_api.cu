@@ -173,39 +173,79 @@ struct ExactHost {
   int bad;
 };
 
-static int fetch(prohd_ctx* ctx, const ExactWs& w, ExactHost& h) {
-  CK(cudaMemcpyAsync(h.keys, w.keys, sizeof h.keys, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(h.nn_d, w.nn_d, sizeof h.nn_d, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(h.nn_j, w.nn_j, sizeof h.nn_j, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(&h.bad, w.bad, sizeof h.bad, cudaMemcpyDeviceToHost, ctx->stream));
+// every result word in ONE device-to-host copy (pack_exact_kernel), then the single sync
+static int fetch(prohd_ctx* ctx, const ExactWs& w, ExactHost& h, bool packed = false) {
+  ExactResDev r;
+  if (!packed)
+    CK(launch_pack_exact(w.keys, w.nn_d, w.nn_j, w.bad, static_cast<ExactResDev*>(w.res), ctx->stream));
+  CK(cudaMemcpyAsync(&r, w.res, sizeof r, cudaMemcpyDeviceToHost, ctx->stream));
   call_end(ctx);
   CK(cudaStreamSynchronize(ctx->stream));
   call_collect(ctx);
+  for (int s = 0; s < 2; ++s) {
+    h.keys[s] = r.key[s];
+    h.nn_d[s] = r.d2[s];
+    h.nn_j[s] = r.j[s];
+  }
+  h.bad = r.bad;
   if (h.bad) return fail(ctx, PROHD_E_DATA, "non-finite input coordinate (or squared norm overflow)");
   return PROHD_OK;
+}
+
+// directed_hd / hausdorff on device inputs without tracing: the whole enqueue (centre, K0, K6, K7,
+// pack) replays a cached CUDA graph on the library's capture stream (api_common.cuh graphed(),
+// prohd_estimate.cu); the host then reads one packed result.
+static int exact_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D, bool bidir,
+                     ExactHost& h) {
+  int rc = enter(ctx);
+  if (rc) return rc;
+  if ((rc = check_sets(ctx, A, nA, B, nB, D))) return rc;
+  const bool dev_in = is_device_ptr(A) && is_device_ptr(B);
+  const bool use_graph = dev_in && !ctx->timing && opt(OPT_GRAPH) != 0;
+  if (use_graph && (rc = ensure_gstream(ctx))) return rc;
+  GraphStream gs(ctx, use_graph);
+  ExactWs w;
+  auto work = [&]() -> int {
+    int r2 = exact_common(ctx, A, nA, B, nB, D, w, bidir ? kCentrePair : kCentreCols);
+    if (r2) return r2;
+    if ((r2 = bidir ? bidir_on_ops(ctx, w.A, w.B, D, w) : directed_on_ops(ctx, w.A, w.B, D, w, 0))) return r2;
+    CK(launch_pack_exact(w.keys, w.nn_d, w.nn_j, w.bad, static_cast<ExactResDev*>(w.res), ctx->stream));
+    return PROHD_OK;
+  };
+  if (use_graph) {
+    KeyBuf kk = graph_key(ctx, bidir ? 2 : 1);
+    kk.add(A).add(B).add(nA).add(nB).add(D);
+    // exact_common's carve fills w inside the capture; on a replay it is not run, so carve here too
+    Carver c{ctx->ws, 0, ctx->ws_bytes, false};
+    if (ctx->ws != nullptr) {
+      Carver dry{nullptr, 0, 0, true};
+      ExactWs tmp;
+      if (carve_exact(dry, tmp, nA, nB, D, false) <= ctx->ws_bytes) carve_exact(c, w, nA, nB, D, false);
+    }
+    call_begin(ctx);
+    rc = graphed(ctx, kk.b, nullptr, 0, work);
+  } else {
+    rc = work();
+  }
+  if (rc) return rc;
+  return fetch(ctx, w, h, true);
 }
 
 int directed_hd(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D,
                 prohd_directed* out) {
   if (out == nullptr) return fail(ctx, PROHD_E_INVALID, "null output");
-  ExactWs w;
-  int rc = exact_common(ctx, A, nA, B, nB, D, w, kCentreCols);
-  if (rc) return rc;
-  if ((rc = directed_on_ops(ctx, w.A, w.B, D, w, 0))) return rc;
   ExactHost h;
-  if ((rc = fetch(ctx, w, h))) return rc;
+  int rc = exact_run(ctx, A, nA, B, nB, D, false, h);
+  if (rc) return rc;
   fill_directed(out, h.keys[0], h.nn_d[0], h.nn_j[0]);
   return PROHD_OK;
 }
 
 int hausdorff(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_t nB, int32_t D, prohd_hd* out) {
   if (out == nullptr) return fail(ctx, PROHD_E_INVALID, "null output");
-  ExactWs w;
-  int rc = exact_common(ctx, A, nA, B, nB, D, w, kCentrePair);
-  if (rc) return rc;
-  if ((rc = bidir_on_ops(ctx, w.A, w.B, D, w))) return rc;  // one fused sweep for both directions
   ExactHost h;
-  if ((rc = fetch(ctx, w, h))) return rc;
+  int rc = exact_run(ctx, A, nA, B, nB, D, true, h);  // one fused sweep for both directions
+  if (rc) return rc;
   fill_directed(&out->ab, h.keys[0], h.nn_d[0], h.nn_j[0]);
   fill_directed(&out->ba, h.keys[1], h.nn_d[1], h.nn_j[1]);
   out->value = out->ab.dist2 >= out->ba.dist2 ? out->ab.dist : out->ba.dist;

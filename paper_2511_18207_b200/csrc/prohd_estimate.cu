@@ -163,57 +163,13 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   // ordered after and before the caller's stream by events.
   const bool use_graph = dirs_in == nullptr && counts == nullptr && !certified && !host_in && !ctx->timing &&
                          opt(OPT_GRAPH) != 0;
-  if (use_graph && ctx->gstream == nullptr) {
-    CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
-  }
-  struct StreamSwap {
-    prohd_ctx* c;
-    cudaStream_t orig;
-    bool on;
-    StreamSwap(prohd_ctx* c_, bool on_) : c(c_), orig(c_->stream), on(on_) {
-      if (!on) return;
-      cudaEventRecord(c->ev_in, orig);
-      cudaStreamWaitEvent(c->gstream, c->ev_in, 0);
-      c->stream = c->gstream;
-    }
-    ~StreamSwap() {
-      if (!on) return;
-      cudaEventRecord(c->ev_out, c->gstream);
-      cudaStreamWaitEvent(orig, c->ev_out, 0);
-      c->stream = orig;
-    }
-  } swap_guard(ctx, use_graph);
+  if (use_graph && (rc = ensure_gstream(ctx))) return rc;
+  GraphStream swap_guard(ctx, use_graph);
   cudaStream_t st = ctx->stream;
-  struct Key {
-    int phase, use_i8;
-    const void *A, *B, *ws;
-    int64_t nA, nB, m, uc0, uc1;
-    size_t ws_bytes;
-    int D, k, num_sms;
-    long long opts[OPT_COUNT];
-  };
   auto make_key = [&](int phase, int i8, int64_t uc0, int64_t uc1) {
-    Key kk;
-    std::memset(&kk, 0, sizeof kk);  // padding bytes too: the key is compared as bytes
-    kk.phase = phase;
-    kk.use_i8 = i8;
-    kk.A = A;
-    kk.B = B;
-    kk.ws = ctx->ws;
-    kk.nA = nA;
-    kk.nB = nB;
-    kk.m = m;
-    kk.uc0 = uc0;
-    kk.uc1 = uc1;
-    kk.ws_bytes = ctx->ws_bytes;
-    kk.D = D;
-    kk.k = k;
-    kk.num_sms = ctx->num_sms;
-    for (int i = 0; i < OPT_COUNT; ++i) kk.opts[i] = opt(static_cast<OptId>(i));
-    const uint8_t* b = reinterpret_cast<const uint8_t*>(&kk);
-    return std::vector<uint8_t>(b, b + sizeof kk);
+    KeyBuf kk = graph_key(ctx, 100 + phase);
+    kk.add(i8).add(A).add(B).add(nA).add(nB).add(m).add(uc0).add(uc1).add(D).add(k);
+    return kk.b;
   };
 
   // ------------------------------------------------------------ step 1: directions

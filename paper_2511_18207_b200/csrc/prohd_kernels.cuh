@@ -175,6 +175,15 @@ struct EstResultDev {
 cudaError_t launch_pack_result(const unsigned long long* keys, const double* nn_d, const long long* nn_j,
                                const long long* uA, const long long* uB, bool map_cols, EstResultDev* out,
                                cudaStream_t st);
+struct ExactResDev {           // directed_hd / hausdorff result, one device-to-host copy
+  unsigned long long key[2];
+  double d2[2];
+  long long j[2];
+  int bad;
+  int _pad;
+};
+cudaError_t launch_pack_exact(const unsigned long long* keys, const double* nn_d, const long long* nn_j,
+                              const int* bad, ExactResDev* out, cudaStream_t st);
 cudaError_t launch_set_int(int* a, int v, cudaStream_t st);  // *a = v (stream-ordered, capturable)
 cudaError_t launch_minus_one(const int* a, int* b, cudaStream_t st);  // *b = max(*a - 1, 0)
 // Sharded selection: local top/bottom-m lists with their fp64 projection values and GLOBAL

@@ -315,3 +315,23 @@ def test_wide_dynamic_range_per_row_scales(ctx, D):
     ref = oracle.hausdorff(A, B)
     _check_directed(A, B, h["ab"], ref["ab"])
     _check_directed(B, A, h["ba"], ref["ba"])
+
+
+def test_graph_replay_exact(ctx):
+    """directed_hd / hausdorff replay a cached CUDA graph of their whole enqueue on device inputs:
+    repeated calls and new values in the same buffers return exactly the eager result (option
+    graph = 0)."""
+    from paper_2511_18207_b200 import option
+    rng = np.random.default_rng(31)
+    A = rng.standard_normal((3001, 64)).astype(np.float32)
+    B = (rng.standard_normal((2500, 64)) + 0.3).astype(np.float32)
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    for data in range(2):
+        if data == 1:
+            At.copy_(torch.from_numpy((A * 2.0 - 1.0).astype(np.float32)))
+            Bt.copy_(torch.from_numpy(np.ascontiguousarray(B[::-1])))
+        with option("graph", 0):
+            d0, h0 = ctx.directed_hd(At, Bt), ctx.hausdorff(At, Bt)
+        for _ in range(3):
+            assert ctx.directed_hd(At, Bt) == d0
+            assert ctx.hausdorff(At, Bt) == h0
