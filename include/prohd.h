@@ -187,8 +187,8 @@ int prohd_project(prohd_ctx* ctx, const float* X, int64_t n, int32_t D, const do
 /* ---------------------------------------------------------------- ProHD   */
 /* Alg. 3 with k principal directions plus the centroid axis and m points per
  * (set, direction, tail). 0 <= k <= D, m >= 1; if 2m >= n_X all of X is kept.
- * The device eigen-solver holds C in one 8-CTA cluster's shared memory: k > 0 needs
- * D <= 256 (else PROHD_E_NOTIMPL); k = 0 (centroid axis only) takes any D.
+ * The device eigen-solver holds C in one thread-block cluster's shared memory (8 or 16 CTAs):
+ * k > 0 needs D <= 512 (else PROHD_E_NOTIMPL); k = 0 (centroid axis only) takes any D.
  * Optional outputs (NULL to skip), HOST pointers:
  *   dirs_out  D x (k+1) fp64, column-major by direction (dirs_out[l*D + d]);
  *             column 0 is the centroid axis; columns >= n_dirs are zero.

@@ -36,8 +36,10 @@ namespace {
 constexpr int kCl = 8;       // CTAs per cluster
 constexpr int kT = 256;      // threads per CTA
 constexpr int kWarps = kT / 32;
-constexpr int kMaxD = 256;
-constexpr int kLuStride = 6 * kMaxD + kMaxD / 8;  // doubles of inverse-iteration scratch per warp
+constexpr int kMaxD = 256;     // the default variant's largest D; D <= 512 takes the MD = 512 variant
+constexpr int kDeStride = 512;  // de = [d (512) | e (512)] for both variants
+template <int MD>
+constexpr int lu_stride() { return 6 * MD + MD / 8; }  // doubles of inverse-iteration scratch per warp
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -102,7 +104,7 @@ struct EigArgs {
   double* lam;    // [k] eigenvalues (desc)
   int* n_dirs;    // 1 + kept
   int stop;       // dev timing only (option eig_stop): return after phase `stop` (0 = run all)
-  double* de;     // [2][kMaxD]: diagonal d, then off-diagonal e of T (global hand-off)
+  double* de;     // [2][kDeStride]: diagonal d, then off-diagonal e of T (global hand-off)
 };
 
 // inverse iteration for eigenvalue `lam` of T (one warp; lane 0 runs the serial solve on the
@@ -215,14 +217,14 @@ __device__ void inverse_iteration(const double* d, const double* e, int D, doubl
 //      the row's own entry M[r][j]), and every warp forms the updated column j+1 in its registers
 //      with the owner's expression M[r][j+1] - (v_r w_{j+1} + w_r v_{j+1}) (bit-identical).
 // Writes d, e (de) and the Householder vectors (V rows 0 .. D-3).
-template <int kCl>
+template <int kCl, int MD>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduce_cluster_kernel(EigArgs a) {
-  constexpr int kRows = kMaxD / kCl;  // rows per CTA (max)
+  constexpr int kRows = MD / kCl;  // rows per CTA (max)
     cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
   extern __shared__ double dyn[];
   double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/kCl)*D])
-  __shared__ double2 pc2[2][kMaxD];  // scattered (p_r, pre-update M[r][j+1]): [j & 1]
+  __shared__ double2 pc2[2][MD];  // scattered (p_r, pre-update M[r][j+1]): [j & 1]
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nloc = (D - rank + kCl - 1) / kCl;  // rows r = rank + kCl*i, i < nloc
@@ -235,7 +237,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
   // hold: the register column and the owners' rows must agree bit for bit (the update uses v_r
   // from the row and v_c from the column; with C[0][c] instead, a 1-ulp asymmetry of the input
   // grew into O(||C||) errors of T, reproduced in a host emulation)
-  constexpr int kTq = kMaxD / 32;
+  constexpr int kTq = MD / 32;
   double x[kTq];
 #pragma unroll
   for (int t = 0; t < kTq; ++t) {
@@ -245,7 +247,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
   __syncthreads();
   cl.sync();
   double* dg = a.de;
-  double* eg = a.de + kMaxD;
+  double* eg = a.de + kDeStride;
   constexpr int kRW = kRows / kWarps;  // own rows per warp
   for (int j = 0; j + 2 < D; ++j) {
     double2* pc = pc2[j & 1];
@@ -373,18 +375,19 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
 
 // Eigenvalues (bisection), eigenvectors of T (inverse iteration) and the back-transform,
 // on the cluster, from d, e (de) and the Householder vectors (V).
+template <int MD>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vectors_cluster_kernel(EigArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
   extern __shared__ double dyn[];
-  double* lu = dyn;  // per warp: u0, u1, u2, x, multipliers, 1/u0 (kMaxD doubles each), swap flags
-  __shared__ double d[kMaxD], e[kMaxD], e2[kMaxD], lamv[kMaxD];
+  double* lu = dyn;  // per warp: u0, u1, u2, x, multipliers, 1/u0 (MD doubles each), swap flags
+  __shared__ double d[MD], e[MD], e2[MD], lamv[MD];
   __shared__ int s_prev[kWarps][16];
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < D; i += kT) {
     d[i] = a.de[i];
-    e[i] = i < D - 1 ? a.de[kMaxD + i] : 0.0;
+    e[i] = i < D - 1 ? a.de[kDeStride + i] : 0.0;
   }
   __syncthreads();
   if (a.stop == 1) return;
@@ -453,12 +456,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
       while (end < kk && fabs(lamv[end - 1] - lamv[end]) <= clus) ++end;
       const int slot = c % (kCl * kWarps);
       if (slot / kWarps == rank && slot % kWarps == warp) {
-        double* u0 = lu + warp * kLuStride;
+        double* u0 = lu + warp * lu_stride<MD>();
         int nprev = 0;
         for (int w = start; w < end; ++w) {
-          inverse_iteration(d, e, D, lamv[w], tnorm, pivmin, a.X + static_cast<int64_t>(w) * D, u0 + 3 * kMaxD, u0,
-                            u0 + kMaxD, u0 + 2 * kMaxD, u0 + 4 * kMaxD, u0 + 5 * kMaxD,
-                            reinterpret_cast<unsigned char*>(u0 + 6 * kMaxD), a.X, s_prev[warp], nprev, w, lane);
+          inverse_iteration(d, e, D, lamv[w], tnorm, pivmin, a.X + static_cast<int64_t>(w) * D, u0 + 3 * MD, u0,
+                            u0 + MD, u0 + 2 * MD, u0 + 4 * MD, u0 + 5 * MD,
+                            reinterpret_cast<unsigned char*>(u0 + 6 * MD), a.X, s_prev[warp], nprev, w, lane);
           if (lane == 0 && nprev < 16) s_prev[warp][nprev] = w;
           __syncwarp();
           if (nprev < 16) ++nprev;
@@ -479,7 +482,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
     // c = v_{j-1}.v_j reduced together, then y -= 2 a v_j and y -= 2 (b - 2 a c) v_{j-1}
     // (= v_{j-1}.(H_j y)); the rows of the next two pairs are prefetched into registers, so the
     // global-memory latency of V is not on the chain.
-    constexpr int kYT = kMaxD / 32;
+    constexpr int kYT = MD / 32;
     double yr[kYT];
     double p0[kYT], p1[kYT], q0[kYT], q1[kYT], r0[kYT], r1[kYT];
     auto ldrow = [&](int j, double(&r)[kYT]) {
@@ -579,23 +582,43 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_vecto
 
 cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, double* out64, float* out32,
                               double* lam, int* n_dirs, cudaStream_t st) {
-  if (D > kMaxD) return cudaErrorInvalidValue;
+  if (D > 2 * kMaxD) return cudaErrorInvalidValue;
   const int stop = opt(OPT_EIG_STOP) > 0 ? static_cast<int>(opt(OPT_EIG_STOP)) : 0;
   EigArgs a{C, D, k, V, X, out64, out32, lam, n_dirs, stop, V + static_cast<int64_t>(D) * D};
   cudaError_t e;
+  if (D > kMaxD) {
+    // 256 < D <= 512 (no BASELINE config): the same kernels instantiated for 512, the
+    // tridiagonalisation on a 16-CTA cluster (32 rows x 512 fp64 = 128 KB per CTA)
+    const size_t smem = sizeof(double) * static_cast<size_t>(512 / 16) * 512;
+    if ((e = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                  1)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem))) != cudaSuccess)
+      return e;
+    count_launch();
+    eigen_reduce_cluster_kernel<16, 512><<<16, kT, smem, st>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const size_t smem3 = sizeof(double) * static_cast<size_t>(kWarps) * lu_stride<512>();
+    if ((e = cudaFuncSetAttribute(eigen_vectors_cluster_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem3))) != cudaSuccess)
+      return e;
+    count_launch();
+    eigen_vectors_cluster_kernel<512><<<kCl, kT, smem3, st>>>(a);
+    return cudaGetLastError();
+  }
   // tridiagonalisation on a 16-CTA cluster (non-portable size; 2 rows per warp) for D > 160 where
   // the device allows it (D = 256: 0.87 -> 0.84 ms), else on 8 CTAs (faster below: the per-step
   // barrier dominates); option eig_cl = 8 forces the portable size (A/B)
   bool wide = D > 160 && opt(OPT_EIG_CL) != 8;
   if (wide) {
     const size_t smem16 = sizeof(double) * static_cast<size_t>(kMaxD / 16) * kMaxD;
-    wide = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+    wide = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16, kMaxD>, cudaFuncAttributeNonPortableClusterSizeAllowed,
                                 1) == cudaSuccess &&
-           cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+           cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16, kMaxD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem16)) == cudaSuccess;
     if (wide) {
       count_launch();
-      eigen_reduce_cluster_kernel<16><<<16, kT, smem16, st>>>(a);
+      eigen_reduce_cluster_kernel<16, kMaxD><<<16, kT, smem16, st>>>(a);
       wide = cudaPeekAtLastError() == cudaSuccess;
       if (!wide) (void)cudaGetLastError();  // clear a launch refusal; fall back to 8 CTAs
     } else {
@@ -604,18 +627,18 @@ cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, dou
   }
   if (!wide) {
     const size_t smem = sizeof(double) * static_cast<size_t>(kMaxD / kCl) * kMaxD;
-    if ((e = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<kCl>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<kCl, kMaxD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem))) != cudaSuccess)
       return e;
     count_launch();
-    eigen_reduce_cluster_kernel<kCl><<<kCl, kT, smem, st>>>(a);
+    eigen_reduce_cluster_kernel<kCl, kMaxD><<<kCl, kT, smem, st>>>(a);
   }
-  const size_t smem3 = sizeof(double) * static_cast<size_t>(kWarps) * kLuStride;
-  if ((e = cudaFuncSetAttribute(eigen_vectors_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem3 = sizeof(double) * static_cast<size_t>(kWarps) * lu_stride<kMaxD>();
+  if ((e = cudaFuncSetAttribute(eigen_vectors_cluster_kernel<kMaxD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem3))) != cudaSuccess)
     return e;
   count_launch();
-  eigen_vectors_cluster_kernel<<<kCl, kT, smem3, st>>>(a);
+  eigen_vectors_cluster_kernel<kMaxD><<<kCl, kT, smem3, st>>>(a);
   return cudaGetLastError();
 }
 

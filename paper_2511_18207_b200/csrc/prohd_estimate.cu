@@ -83,7 +83,7 @@ static size_t carve_est(Carver& c, EstWs& w, int64_t nA, int64_t nB, int D, int 
   w.mom.SB = c.take<double>(D);
   w.mom.mu = c.take<double>(D);
   w.mom.dnorm = c.take<double>(1);
-  w.V = c.take<double>(static_cast<int64_t>(D) * D + 2 * 256);  // Householder vectors + d, e of T
+  w.V = c.take<double>(static_cast<int64_t>(D) * D + 2 * 512);  // Householder vectors + d, e of T
   w.Xe = c.take<double>(static_cast<int64_t>(k > 0 ? k : 1) * D);
   w.U64 = c.take<double>(static_cast<int64_t>(L) * D);
   w.mom.u0 = w.U64;  // row 0 of U is the centroid axis
@@ -134,8 +134,8 @@ int prohd_run(prohd_ctx* ctx, const float* A, int64_t nA, const float* B, int64_
   if ((rc = check_sets(ctx, A, nA, B, nB, D))) return rc;
   if (k < 0 || k > D) return fail(ctx, PROHD_E_INVALID, "k must satisfy 0 <= k <= D (k=%d, D=%d)", k, D);
   if (m < 1) return fail(ctx, PROHD_E_INVALID, "m must be >= 1 (m=%lld)", static_cast<long long>(m));
-  if (dirs_in == nullptr && k > 0 && D > 256)
-    return fail(ctx, PROHD_E_NOTIMPL, "the device eigen-solver supports D <= 256 (D=%d)", D);
+  if (dirs_in == nullptr && k > 0 && D > 512)
+    return fail(ctx, PROHD_E_NOTIMPL, "the device eigen-solver supports D <= 512 (D=%d)", D);
   if (m > 0x7FFFFFFFLL) return fail(ctx, PROHD_E_INVALID, "m too large");
   const int L = k + 1;
   call_begin(ctx);

@@ -57,7 +57,7 @@ static size_t carve_shard(Carver& c, ShardWs& w, int64_t nA, int64_t nB, int64_t
   w.mom.SB = c.take<double>(D);
   w.mom.mu = c.take<double>(D);
   w.mom.dnorm = c.take<double>(1);
-  w.V = c.take<double>(static_cast<int64_t>(D) * D + 2 * 256);  // Householder vectors + d, e of T
+  w.V = c.take<double>(static_cast<int64_t>(D) * D + 2 * 512);  // Householder vectors + d, e of T
   w.Xe = c.take<double>(static_cast<int64_t>(k > 0 ? k : 1) * D);
   w.U64 = c.take<double>(static_cast<int64_t>(L) * D);
   w.mom.u0 = w.U64;
@@ -277,7 +277,7 @@ int prohd_directions(prohd_ctx* ctx, const double* moments, int64_t nA, int64_t 
     return fail(ctx, PROHD_E_INVALID, "null pointer");
   if (nA < 1 || nB < 1 || D < 1) return fail(ctx, PROHD_E_INVALID, "bad sizes");
   if (k < 0 || k > D) return fail(ctx, PROHD_E_INVALID, "k must satisfy 0 <= k <= D");
-  if (k > 0 && D > 256) return fail(ctx, PROHD_E_NOTIMPL, "the device eigen-solver supports D <= 256");
+  if (k > 0 && D > 512) return fail(ctx, PROHD_E_NOTIMPL, "the device eigen-solver supports D <= 512");
   call_begin(ctx);
   ShardWs w;
   if ((rc = shard_begin(ctx, w, 0, 0, 1, D, k, 1, false))) return rc;

@@ -1,5 +1,5 @@
 """GPU eigen-solver (K2) against the fp64 oracle's Jacobi (oracle/eigen.py) on prescribed
-spectra (D across the 8/16-CTA switch at 160), through the sharding phase call prohd_directions: moments [S_A | S_B | G] with
+spectra (D across the 8/16-CTA switch at 160 and the D <= 512 variant above 256), through the sharding phase call prohd_directions: moments [S_A | S_B | G] with
 S = 0 and G = N C give C itself, so rows 1..k of the returned directions are the top-k
 eigenvectors of C (Alg. 2 line 2; sign rule SPEC.md:245).
 
@@ -59,7 +59,7 @@ def _check(C, dirs, nd, k, lam_sorted, angle_gap=1e-6):
             assert v[i] > 0
 
 
-@pytest.mark.parametrize("D", [2, 3, 17, 64, 127, 128, 129, 130, 160, 161, 200, 231, 232, 256])
+@pytest.mark.parametrize("D", [2, 3, 17, 64, 127, 128, 129, 130, 160, 161, 200, 231, 232, 256, 257, 300, 512])
 def test_separated_spectrum(ctx, D):
     rng = np.random.default_rng(D)
     lam = np.sort(rng.uniform(0.1, 10.0, D))[::-1]

@@ -434,3 +434,20 @@ def test_graph_replay_matches_eager(ctx):
         e3 = ctx.prohd_estimate(At3, Bt3, c.k, c.m(12000), return_indices=True)
     g3 = ctx.prohd_estimate(At3, Bt3, c.k, c.m(12000), return_indices=True)
     assert g3["value"] == e3["value"] and np.array_equal(g3["IA"], e3["IA"])
+
+
+@pytest.mark.parametrize("D", [264, 320])
+def test_wide_d_end_to_end(ctx, D):
+    """ProHD with k > 0 above D = 256 (Alg. 2 needs only k <= D): the eigen-solver's
+    D <= 512 variant, the fp64 DMMA Gram and the SIMT projection; selected sets bit-exact with
+    the oracle, the estimate within 1e-4."""
+    rng = np.random.default_rng(D)
+    n = 6000
+    scales = np.geomspace(3.0, 0.1, D)
+    A = (rng.standard_normal((n, D)) * scales).astype(np.float32)
+    B = (rng.standard_normal((n + 7, D)) * scales + 0.05).astype(np.float32)
+    k, m = 8, 30
+    g = ctx.prohd_estimate(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), k, m, return_indices=True)
+    r = OP.estimate(A, B, k, m)
+    assert np.array_equal(g["IA"], r["IA"]) and np.array_equal(g["IB"], r["IB"])
+    assert abs(g["value"] - r["value"]) <= 1e-4 * r["value"]
