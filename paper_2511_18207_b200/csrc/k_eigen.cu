@@ -15,10 +15,11 @@
 //
 // Layout: ONE thread-block cluster of 8 (16 for D > 160) CTAs. The matrix is kept on chip:
 // row r lives in CTA r % kCl (cyclic, so every CTA keeps work as the trailing block shrinks),
-// <= 32 rows x 256 fp64 = 64 KB of shared memory per CTA. Each Householder step exchanges
-// p = 2 A v, the pre-update next column and the v.p partials by direct stores into every
-// CTA's shared memory (DSMEM) and needs ONE cluster barrier; every CTA forms v and the
-// updated next column itself. Latency-bound: ~(D-2) cluster barriers.
+// <= 32 rows x 256 fp64 = 64 KB of shared memory per CTA (the D <= 512 variant: 16 CTAs x 32
+// rows x 512 = 128 KB). Each Householder step exchanges p = 2 A v and the pre-update next column
+// by direct stores into every CTA's shared memory (DSMEM) and needs ONE cluster barrier; every
+// warp keeps the current column in registers and forms v and the updated next column itself.
+// Latency-bound: ~(D-2) cluster barriers.
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
 
