@@ -22,6 +22,7 @@
 // Latency-bound: ~(D-2) cluster barriers.
 #include "internal.cuh"
 #include "prohd_kernels.cuh"
+#include "sm100.cuh"
 
 #include <cooperative_groups.h>
 
@@ -79,6 +80,39 @@ __device__ __forceinline__ double rcp_sturm(double q) {
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
   return fma(r, fma(-q, r, 1.0), r);
 }
+// Remote shared-memory stores that complete on the DESTINATION CTA's mbarrier (st.async, the
+// async proxy): the receiver waits on its own barrier for the bytes, no release fence, no cluster
+// barrier. Both addresses are shared::cluster addresses (mapa).
+__device__ __forceinline__ void st_async_f64x2(uint32_t dst, double a0, double a1, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+               "d"(a0), "d"(a1), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_b64(uint32_t dst, unsigned long long v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(dst), "l"(v),
+               "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// acquire (cluster scope) wait on a local mbarrier fed by remote st.async; ~1 s watchdog
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  const long long t0 = clock64();
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(sm100::smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!ok && clock64() - t0 > 2000000000ll) __trap();
+  } while (!ok);
+}
+
 // number of eigenvalues of T (d, e2 = e^2) strictly less than x (Sturm count); |q| >= pivmin
 // (> DBL_MIN) at every division, so the reciprocal is taken on normal numbers
 __device__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
@@ -226,6 +260,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
   extern __shared__ double dyn[];
   double* M = dyn;  // [kRows][D] own rows (row r -> M[(r/kCl)*D])
   __shared__ double2 pc2[2][MD];  // scattered (p_r, pre-update M[r][j+1]): [j & 1]
+  __shared__ __align__(8) uint64_t pbar[2];          // complete_tx barriers of pc2[0], pc2[1]
+  __shared__ unsigned long long tok[kWarps];          // per-step tokens of every warp of every CTA
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nloc = (D - rank + kCl - 1) / kCl;  // rows r = rank + kCl*i, i < nloc
@@ -245,8 +281,15 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
     const int c = lane + 32 * t;
     x[t] = c < D ? a.C[static_cast<int64_t>(c) * D] : 0.0;
   }
+  if (tid == 0) {
+    sm100::mbar_init(&pbar[0], 1);
+    sm100::mbar_init(&pbar[1], 1);
+    sm100::fence_mbar_init();
+  }
   __syncthreads();
   cl.sync();
+  const uint32_t pbar_u32 = sm100::smem_u32(&pbar[0]), pc_u32 = sm100::smem_u32(&pc2[0][0]);
+  const uint32_t tok_u32 = sm100::smem_u32(&tok[warp]);
   double* dg = a.de;
   double* eg = a.de + kDeStride;
   constexpr int kRW = kRows / kWarps;  // own rows per warp
@@ -299,18 +342,25 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int q = 0; q < kRW; ++q) ps[q] += __shfl_xor_sync(0xffffffffu, ps[q], o);
+    // the exchange: one 16-byte st.async per row and target CTA, completing on the target's
+    // barrier of this buffer, plus one 8-byte token per warp and target (so a step's barrier
+    // completes only when EVERY warp of every CTA has finished the previous step, which makes the
+    // double buffer safe without a cluster barrier). Expected per CTA and step: 16 (D - j - 1)
+    // data bytes + 8 kCl kWarps token bytes.
+    const int b = j & 1;
+    if (tid == 0)
+      sm100::mbar_arrive_expect_tx(&pbar[b], static_cast<uint32_t>(16 * (D - j - 1) + 8 * kCl * kWarps));
+    const uint32_t rbar = mapa_u32(pbar_u32 + 8u * static_cast<uint32_t>(b), static_cast<uint32_t>(lane));
 #pragma unroll
     for (int q = 0; q < kRW; ++q) {
       const int i = warp + kWarps * q;
       const int r = rank + kCl * i;
-      // one 16-byte DSMEM store per row and target CTA
       if (i < nloc && r > j && lane < kCl)
-        *cl.map_shared_rank(&pc[r], lane) = make_double2(2.0 * ps[q], M[i * D + j + 1]);
+        st_async_f64x2(mapa_u32(pc_u32 + 16u * static_cast<uint32_t>(b * MD + r), static_cast<uint32_t>(lane)),
+                       2.0 * ps[q], M[i * D + j + 1], rbar);
     }
-    // split cluster barrier: the release covers the DSMEM stores above; this step's global
-    // outputs (d_j, e_j, Householder vector j) are stored between arrive and wait, so their
-    // latency is not on the barrier's path (the next step's release finds them long done)
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if (lane < kCl) st_async_b64(mapa_u32(tok_u32, static_cast<uint32_t>(lane)), 0ull, rbar);
+    // this step's global outputs (d_j, e_j, Householder vector j) while the exchange is in flight
     // d_j from the warp that owns (and last updated) row j: no cross-warp shared-memory hazard
     if (j % kCl == rank && warp == (j / kCl) % kWarps && lane == 0) dg[j] = M[(j / kCl) * D + j];
     if (rank == 0 && warp == 0) {
@@ -321,7 +371,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
         if (c > j && c < D) a.V[static_cast<int64_t>(j) * D + c] = v[t];
       }
     }
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    mbar_wait_acq_cluster(&pbar[b], static_cast<uint32_t>(j >> 1) & 1u);
     // C. K = v.p from the full p (same order in every warp and CTA), w = p - K v; M[r][c] -=
     // v_r w_c + w_r v_c on own rows; every warp forms the updated column j+1 (rows > j) in its
     // registers with the owner's expression, M[r][j+1] - (v_r w_{j+1} + w_r v_{j+1})
@@ -361,6 +411,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kT, 1) eigen_reduc
       }
     }
   }
+  cl.sync();  // every CTA's last exchange has landed before any CTA exits
   __syncthreads();  // the last step's row updates (other warps) before the 2x2 block
   // last 2x2 block
   if (D >= 2 && ((D - 2) % kCl) == rank && tid == 0) {
