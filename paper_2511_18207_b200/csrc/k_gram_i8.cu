@@ -80,7 +80,8 @@ struct I8Args {
   int ncs;
   unsigned* overflow;
   int ablate;            // dev timing only (option k1_ablate): 1 skip the slicing work, 2 skip the MMAs
-  int small;             // D <= 128: gram_i8s_kernel (one CTA per level set), nt0 + nt1 CTAs
+  int small;             // D <= 128: gram_i8s_kernel (one CTA per level set), nt0 + nt1 CTAs;
+                         // 2: D <= 64, gram_i8d_kernel (paired digit planes), nt0 CTAs
   int nt0, nt1;          //   CTAs of level set 0 ({0,1,2,3}) and of level set 1 ({4,5})
 };
 
@@ -672,6 +673,236 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// D <= 64 (gram_i8d_kernel): two digit planes share one 128-byte row (features 0-63 of plane t in
+// bytes 0-63, of plane t' in bytes 64-127): P0 = [2 d_0 | d_1], P1 = [d_2 | d_3]. One M = N = 128
+// MMA of two paired planes computes four useful 64 x 64 products (its quadrants), so three MMAs
+// per K-step cover every ordered digit pair: R0 = P0 x P0, R1 = P0 x P1 (standing for P1 x P0 too:
+// the final symmetrisation makes D_u^T D_t count as D_t^T D_u, so R1 is weighted x 2), R2 = P1 x P1
+// (including d_3 d_3: exact). Three 128-column regions of TMEM, ONE CTA type: every row is read and
+// sliced once. Each quadrant of a region gains one product (|.| <= 2^14) per point: drained every
+// kDrainChunksD chunks. The drain weights each (region, quadrant) by its level 2^(-8 L), the digit
+// doubling and the x2 of R1, into a per-CTA slab [quadrant][64 j][64 i] of fp64.
+constexpr int kDrainChunksD = 256;
+__device__ __forceinline__ void slice_chunk_pair(uint32_t xr, uint32_t pl, int ws, int lane, int valid,
+                                                 const float (&sc)[4], const float (&sh)[4]) {
+  if (lane >= 16) return;  // features 64-127 do not exist for D <= 64
+  constexpr int kPer = kPts / kSlicers;
+  float4 xs[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int p = ws + kSlicers * u;
+    xs[u] = lds128(xr + p * 128 + ((((lane & 7) ^ (p & 7)) & 7) << 4));
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int p = ws + kSlicers * u;
+    const bool ok = p < valid;
+    const float4 x4 = xs[u];
+    const float y0 = ok ? fmaf(x4.x, sc[0], -sh[0]) : 8421504.0f, y1 = ok ? fmaf(x4.y, sc[1], -sh[1]) : 8421504.0f;
+    const float y2 = ok ? fmaf(x4.z, sc[2], -sh[2]) : 8421504.0f, y3 = ok ? fmaf(x4.w, sc[3], -sh[3]) : 8421504.0f;
+    const uint32_t w0i = static_cast<uint32_t>(__float2int_rn(y0)), w1i = static_cast<uint32_t>(__float2int_rn(y1));
+    const uint32_t w2i = static_cast<uint32_t>(__float2int_rn(y2)), w3i = static_cast<uint32_t>(__float2int_rn(y3));
+    const uint32_t x01l = __byte_perm(w0i, w1i, 0x5140), x01h = __byte_perm(w0i, w1i, 0x7362);
+    const uint32_t x23l = __byte_perm(w2i, w3i, 0x5140), x23h = __byte_perm(w2i, w3i, 0x7362);
+    const uint32_t b0 = __byte_perm(x01l, x23l, 0x5410) ^ 0x80808080u;             // d_3
+    const uint32_t b1 = __byte_perm(x01l, x23l, 0x7632) ^ 0x80808080u;             // d_2
+    const uint32_t b2 = __byte_perm(x01h, x23h, 0x5410) ^ 0x80808080u;             // d_1
+    const uint32_t b3 = (__byte_perm(x01h, x23h, 0x7632) << 1) & 0xFEFEFEFEu;      // 2 d_0
+    // SWIZZLE_128B MN-major rows of 128 bytes: bytes 4 lane .. (chunk lane / 4) and 64 + 4 lane ..
+    // (chunk 4 + lane / 4), each XOR (p % 8)
+    const uint32_t rowb = static_cast<uint32_t>((p >> 3) * 1024 + (p & 7) * 128 + (lane & 3) * 4);
+    const uint32_t lo = rowb + ((((lane >> 2) ^ (p & 7)) & 7) << 4);
+    const uint32_t hi = rowb + ((((4 + (lane >> 2)) ^ (p & 7)) & 7) << 4);
+    sts32(pl + lo, b3);
+    sts32(pl + hi, b2);
+    sts32(pl + kPlane + lo, b1);
+    sts32(pl + kPlane + hi, b0);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gram_i8d_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, I8Args a) {
+  using namespace sm100;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* raw = smem;
+  uint8_t* sl = smem + kRawStages * kRawBytes;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(sl + kSlStages * kSlBytes);
+  uint64_t* raw_empty = raw_full + kRawStages;
+  uint64_t* sl_full = raw_empty + kRawStages;
+  uint64_t* sl_empty = sl_full + kSlStages;
+  uint64_t* tfull = sl_empty + kSlStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  constexpr uint32_t kRawD = kRawBytes / 2;  // two [32 features x 64 points] boxes
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Range R = group_range(a, static_cast<int>(blockIdx.x), a.nt0);
+  const int nchunks = R.na + R.nb;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRawStages; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], kSlicers);
+    }
+    for (int i = 0; i < kSlStages; ++i) {
+      mbar_init(&sl_full[i], kSlicers);
+      mbar_init(&sl_empty[i], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], kDrainWarps);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tA);
+    tma_prefetch(&tB);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        mbar_wait(&raw_empty[st], ph ^ 1u);
+        mbar_arrive_expect_tx(&raw_full[st], kRawD);
+        const bool inA = c < R.na;
+        const int64_t row = inA ? R.a0 + static_cast<int64_t>(c) * kPts : R.b0 + static_cast<int64_t>(c - R.na) * kPts;
+        for (int bx = 0; bx < 2; ++bx)
+          tma_load_2d(raw + st * kRawBytes + bx * (kRawBytes / 4), inA ? &tA : &tB, bx * 32, static_cast<int>(row),
+                      &raw_full[st]);
+        if (++st == kRawStages) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(128, 128);
+      int st = 0;
+      uint32_t ph = 0, tph = 0;
+      int since = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        if (since == 0 && c > 0) {
+          mbar_wait(&tempty[0], tph ^ 1u);
+          tc_fence_after();
+        }
+        mbar_wait(&sl_full[st], ph);
+        tc_fence_after();
+        const uint32_t base = smem_u32(sl + st * kSlBytes);
+        for (int kk = 0; kk < (a.ablate >= 2 ? 0 : 2); ++kk) {
+          const uint32_t acc = (since == 0 && kk == 0) ? 0u : 1u;
+          const uint64_t p0 = smem_desc_mn_sw128(base + kk * 4096), p1 = smem_desc_mn_sw128(base + kPlane + kk * 4096);
+          mma_i8_1sm(tmem_base + 0, p0, p0, idesc, acc);
+          mma_i8_1sm(tmem_base + 128, p0, p1, idesc, acc);
+          mma_i8_1sm(tmem_base + 256, p1, p1, idesc, acc);
+        }
+        mma_commit(&sl_empty[st]);
+        if (++st == kSlStages) {
+          st = 0;
+          ph ^= 1u;
+        }
+        if (++since == kDrainChunksD || c == nchunks - 1) {
+          mma_commit(&tfull[0]);
+          since = 0;
+          tph ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int ws = warp - 2;
+    const int fg0 = 4 * lane;
+    float sc[4], sh[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool live = fg0 + i < a.D;
+      sc[i] = live ? __ldg(a.scale + fg0 + i) : 0.0f;
+      sh[i] = live ? __ldg(a.shiftf + fg0 + i) : -8421504.0f;
+    }
+    const uint32_t raw_u32 = smem_u32(raw), sl_u32 = smem_u32(sl);
+    const int q = warp & 3, half = ws >> 2;
+    const int row = q * 32 + lane;            // TMEM lane: A-operand byte row = (row / 64 plane, feature row % 64)
+    const int ar = row >> 6, fi = row & 63;
+    const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+    const int quad = 2 * ar + half;
+    // weights of region R at this quadrant (see the kernel comment): level 2^(-8 L), / 2 per doubled
+    // d_0 factor, x 2 for R1
+    const double w00[3] = {0.25, 0x1p-16, 0x1p-32}, w01[3] = {0x1p-9, 0x1p-24, 0x1p-40};
+    const double w10[3] = {0x1p-9, 0x1p-23, 0x1p-40}, w11[3] = {0x1p-16, 0x1p-31, 0x1p-48};
+    double wt[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) wt[r] = quad == 0 ? w00[r] : (quad == 1 ? w01[r] : (quad == 2 ? w10[r] : w11[r]));
+    double* out = a.slab + static_cast<int64_t>(blockIdx.x) * kSmallSlab + quad * 4096 + fi;
+    int rst = 0, sst = 0, since = 0, ndr = 0;
+    uint32_t rph = 0, sph = 0, tph = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const bool inA = c < R.na;
+      const int64_t row0 = inA ? R.a0 + static_cast<int64_t>(c) * kPts : R.b0 + static_cast<int64_t>(c - R.na) * kPts;
+      const int64_t rend = inA ? R.a1 : R.b1;
+      const int valid = static_cast<int>(min(static_cast<int64_t>(kPts), rend - row0));
+      mbar_wait(&raw_full[rst], rph);
+      mbar_wait(&sl_empty[sst], sph ^ 1u);
+      const uint32_t xr = raw_u32 + rst * kRawBytes + (lane >> 3) * (kRawBytes / 4);
+      const uint32_t pl = sl_u32 + sst * kSlBytes;
+      if (!(a.ablate & 1)) slice_chunk_pair(xr, pl, ws, lane, valid, sc, sh);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&raw_empty[rst]);
+        mbar_arrive(&sl_full[sst]);
+      }
+      if (++rst == kRawStages) {
+        rst = 0;
+        rph ^= 1u;
+      }
+      if (++sst == kSlStages) {
+        sst = 0;
+        sph ^= 1u;
+      }
+      if (++since == kDrainChunksD || c == nchunks - 1) {
+        since = 0;
+        mbar_wait_sleep(&tfull[0], tph);
+        tph ^= 1u;
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < 64; cc += 32) {
+          double acc[32];
+#pragma unroll 1
+          for (int r = 0; r < 3; ++r) {
+            int v[32];
+            tmem_ld32i(tmem_base + lane_addr + static_cast<uint32_t>(r * 128 + half * 64 + cc), v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              acc[i] = r == 0 ? static_cast<double>(v[i]) * wt[0] : fma(static_cast<double>(v[i]), wt[r], acc[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) out[(cc + i) * 64] = ndr == 0 ? acc[i] : out[(cc + i) * 64] + acc[i];
+        }
+        ++ndr;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[0]);
+      }
+    }
+    if (nchunks == 0)
+      for (int j2 = 0; j2 < 64; ++j2) out[j2 * 64] = 0.0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
 // exact per-feature max |x - s_j| over all rows of A and B (one HBM-bound read) and fp64 column
 // sums of A and of B: thread = a 16-byte column piece (D % 4 == 0), rows strided over the grid;
 // block max -> atomicMax on the non-negative float bits (non-finite values force +inf); block
@@ -905,33 +1136,33 @@ __global__ void __launch_bounds__(kSRedThreads) gram_i8s_reduce_kernel(I8Args a,
   __shared__ double part[2][kSRedThreads];
   const int nct = a.nt0 + a.nt1;
   if (grp < ngrp) {
-    const double* col = a.slab + static_cast<int64_t>(i) * 128 + j;  // Z_c[i][j]: slab [column i][row j]
-    const double* row = a.slab + static_cast<int64_t>(j) * 128 + i;  // Z_c[j][i]
-    double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
-    int c = grp;
-    for (; c + ngrp < nct; c += 2 * ngrp) {
-      p0 += __ldg(col + static_cast<int64_t>(c) * kSmallSlab);
-      q0 += __ldg(row + static_cast<int64_t>(c) * kSmallSlab);
-      p1 += __ldg(col + static_cast<int64_t>(c + ngrp) * kSmallSlab);
-      q1 += __ldg(row + static_cast<int64_t>(c + ngrp) * kSmallSlab);
-    }
-    if (c < nct) {
-      p0 += __ldg(col + static_cast<int64_t>(c) * kSmallSlab);
-      q0 += __ldg(row + static_cast<int64_t>(c) * kSmallSlab);
+    // coalesced: the slabs' column i (contiguous over j); the transpose is summed by
+    // gram_i8_sym_kernel afterwards (a strided second read here cost as much as the Gram at cfg2)
+    double p0 = 0.0, p1 = 0.0;
+    if (a.small == 2) {  // gram_i8d_kernel slabs [quadrant][64 column][64 row]: the quadrants add up
+      const double* col = a.slab + static_cast<int64_t>(i) * 64 + j;
+      for (int c = grp; c < nct; c += ngrp) {
+        const int64_t o = static_cast<int64_t>(c) * kSmallSlab;
+        p0 += (__ldg(col + o) + __ldg(col + o + 4096)) + (__ldg(col + o + 8192) + __ldg(col + o + 12288));
+      }
+    } else {  // gram_i8s_kernel slabs [column 128][row 128]
+      const double* col = a.slab + static_cast<int64_t>(i) * 128 + j;
+      int c = grp;
+      for (; c + ngrp < nct; c += 2 * ngrp) {
+        p0 += __ldg(col + static_cast<int64_t>(c) * kSmallSlab);
+        p1 += __ldg(col + static_cast<int64_t>(c + ngrp) * kSmallSlab);
+      }
+      if (c < nct) p0 += __ldg(col + static_cast<int64_t>(c) * kSmallSlab);
     }
     part[0][t] = p0 + p1;
-    part[1][t] = q0 + q1;
   }
   __syncthreads();
   if (t < D) {
-    double p = 0.0, q = 0.0;
-    for (int g2 = 0; g2 < ngrp; ++g2) {
-      p += part[0][g2 * D + t];
-      q += part[1][g2 * D + t];
-    }
-    // slabs carry 2^-48 sum_L 2^(8 (6 - L)) G_L; (p + q) / 2 is the symmetric part
+    double p = 0.0;
+    for (int g2 = 0; g2 < ngrp; ++g2) p += part[0][g2 * D + t];
+    // slabs carry 2^-48 sum_L 2^(8 (6 - L)) G_L (gram_i8_sym_kernel then takes the symmetric part)
     G[static_cast<int64_t>(i) * D + t] =
-        ldexp(0.5 * (p + q), 48) / (static_cast<double>(a.scale[i]) * static_cast<double>(a.scale[t]));
+        ldexp(p, 48) / (static_cast<double>(a.scale[i]) * static_cast<double>(a.scale[t]));
   }
   __syncthreads();
   double sa = 0.0, sb = 0.0;
@@ -974,7 +1205,16 @@ bool plan_gram_i8(int64_t nA, int64_t nB, int D, int num_sms, GramI8Plan& p) {
     if (T > sms) T = sms;
     if (opt(OPT_K1_I8_CTAS) > 0 && T > opt(OPT_K1_I8_CTAS)) T = opt(OPT_K1_I8_CTAS);
     if (T < 2) T = 2;
-    p.small = true;
+    if (D <= 64) {  // paired digit planes: one CTA type (gram_i8d_kernel)
+      p.small = 2;
+      p.nt0 = static_cast<int>(T);
+      p.nt1 = 0;
+      p.ngroups = 0;
+      p.nctas = p.nt0;
+      p.slab_doubles = static_cast<int64_t>(p.nctas) * kSmallSlab;
+      return true;
+    }
+    p.small = 1;
     p.nt0 = static_cast<int>((T * kSet0Share + kSetShares / 2) / kSetShares);
     if (p.nt0 < 1) p.nt0 = 1;
     p.nt1 = static_cast<int>(T) - p.nt0;
@@ -990,7 +1230,7 @@ bool plan_gram_i8(int64_t nA, int64_t nB, int D, int num_sms, GramI8Plan& p) {
   if (per < 4 * kPts) groups = static_cast<int>((nA + nB) / (4 * kPts));  // small problems: fewer groups
   if (opt(OPT_K1_I8_CTAS) > 0 && groups * 6 > opt(OPT_K1_I8_CTAS)) groups = static_cast<int>(opt(OPT_K1_I8_CTAS) / 6);
   if (groups < 1) return false;
-  p.small = false;
+  p.small = 0;
   p.ngroups = groups;
   p.nctas = groups * 6;
   p.slab_doubles = static_cast<int64_t>(p.nctas) * kFeat * 256;
@@ -1039,8 +1279,8 @@ cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, cons
   i8_scale_kernel<<<1, 256, 0, st>>>(D, s, colmax_in != nullptr ? reinterpret_cast<const unsigned*>(colmax_in) : colmax,
                                      scale, shiftf, overflow);
   I8Args a{nA, nB, D, p.ngroups, scale, shiftf, slab, cpart, kColmaxBlocks, overflow,
-           opt(OPT_K1_ABLATE) > 0 ? static_cast<int>(opt(OPT_K1_ABLATE)) : 0, p.small ? 1 : 0, p.nt0, p.nt1};
-  auto kern = p.small ? gram_i8s_kernel : gram_i8_kernel;
+           opt(OPT_K1_ABLATE) > 0 ? static_cast<int>(opt(OPT_K1_ABLATE)) : 0, p.small, p.nt0, p.nt1};
+  auto kern = p.small == 2 ? gram_i8d_kernel : (p.small == 1 ? gram_i8s_kernel : gram_i8_kernel);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
   if (e != cudaSuccess) return e;
   count_launch();
@@ -1049,6 +1289,9 @@ cudaError_t launch_gram_i8(const GramI8Plan& p, const float* A, int64_t nA, cons
   if (p.small) {
     count_launch();
     gram_i8s_reduce_kernel<<<D, kSRedThreads, 0, st>>>(a, G, SA, SB, s);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    count_launch();
+    gram_i8_sym_kernel<<<D, 256, 0, st>>>(D, G);
   } else {
     count_launch();
     gram_i8_reduce_kernel<<<D, 256, 0, st>>>(a, G, SA, SB, s);

@@ -39,7 +39,7 @@ cudaError_t launch_gram(const GramPlan& p, const float* A, int64_t nA, const flo
 // reruns the fp64 DMMA Gram).
 struct GramI8Plan {
   int D = 0, ngroups = 0, nctas = 0;
-  bool small = false;  // D <= 128: gram_i8s_kernel, nt0 + nt1 single CTAs (level sets 0 and 1)
+  int small = 0;  // 1: D <= 128 gram_i8s_kernel, nt0 + nt1 single CTAs (level sets); 2: D <= 64 gram_i8d_kernel
   int nt0 = 0, nt1 = 0;
   int64_t slab_doubles = 0, csum_count = 0;
 };

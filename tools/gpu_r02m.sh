@@ -1,7 +1,13 @@
 #!/bin/bash
-python tools/prof_cov.py 5 4 > gpurun_out/r02m_time.log 2>&1
-PROHD_OPT_K1_ABLATE=1 python tools/prof_cov.py 5 4 >> gpurun_out/r02m_time.log 2>&1
-PROHD_OPT_K1_ABLATE=2 python tools/prof_cov.py 5 4 >> gpurun_out/r02m_time.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02m_l0.csv python tools/prof_cov.py 5 2 > /dev/null 2>&1
-PROHD_OPT_K1_ABLATE=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02m_l1.csv python tools/prof_cov.py 5 2 > /dev/null 2>&1
-PROHD_OPT_K1_ABLATE=2 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02m_l2.csv python tools/prof_cov.py 5 2 > /dev/null 2>&1
+# D <= 64 paired-plane int8 Gram (gram_i8d_kernel): tests and timings
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_moments.py tests/test_gpu_shard.py -x -q > gpurun_out/m_mom.log 2>&1
+echo "exit $?" >> gpurun_out/m_mom.log
+for cfg in 1 2; do
+  PROHD_OPT_K1_PATH=0 timeout 300 python tools/time_prohd.py $cfg | sed "s/^/dmma /"
+  timeout 300 python tools/time_prohd.py $cfg | sed "s/^/i8   /"
+done > gpurun_out/m_t.txt 2>&1
+timeout 300 python tools/time_small.py 1 2 > gpurun_out/m_small.txt 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/m_launches_cfg2.csv python tools/prof_prohd.py 2 > /dev/null 2>&1
+timeout 1800 python -m pytest tests/test_gpu_prohd.py tests/test_gpu_next.py tests/test_gpu_fullsize.py -x -q -k "not exact_full_size_sampled and not undirected_full" > gpurun_out/m_prohd.log 2>&1
+echo "exit $?" >> gpurun_out/m_prohd.log
