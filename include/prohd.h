@@ -94,7 +94,7 @@ int prohd_launch_count(int64_t* out);
  *   "shift"         0 never / 1 always shift the Gram by the sample mean
  *   "k3_simt"       1: SIMT projection kernel instead of tcgen05
  *   "eig_stop"      1|2|3: stop the eigen-solver after that stage (timing prefixes only)
- *   "eig_cl"        8: portable 8-CTA tridiagonalisation cluster
+ *   "eig_cl"        8: tridiagonalisation on the portable 8-CTA cluster (default 16 CTAs)
  *   "k1_ablate"     1|2: int8 Gram timing ablations (skip slicing / MMAs; WRONG results, dev only)
  *   "k4_sampled"    0: radix K4 over all projections; 1: sampled-threshold K4 wherever it applies
  *                   (default: sampled for n >= 262144, same selected indices either way);

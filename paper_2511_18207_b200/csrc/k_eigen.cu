@@ -658,10 +658,10 @@ cudaError_t launch_eigen_topk(double* C, int D, int k, double* V, double* X, dou
     eigen_vectors_cluster_kernel<512><<<kCl, kT, smem3, st>>>(a);
     return cudaGetLastError();
   }
-  // tridiagonalisation on a 16-CTA cluster (non-portable size; 2 rows per warp) for D > 160 where
-  // the device allows it (D = 256: 0.87 -> 0.84 ms), else on 8 CTAs (faster below: the per-step
-  // barrier dominates); option eig_cl = 8 forces the portable size (A/B)
-  bool wide = D > 160 && opt(OPT_EIG_CL) != 8;
+  // tridiagonalisation on a 16-CTA cluster (non-portable size) where the device allows it, else on
+  // 8 CTAs; with the st.async exchange 16 CTAs win at every D (D = 256: 0.455 vs 0.513 ms, D = 128:
+  // 0.208 vs 0.221, D = 64: 0.102 vs 0.104); option eig_cl = 8 forces the portable size (A/B)
+  bool wide = opt(OPT_EIG_CL) != 8;
   if (wide) {
     const size_t smem16 = sizeof(double) * static_cast<size_t>(kMaxD / 16) * kMaxD;
     wide = cudaFuncSetAttribute(eigen_reduce_cluster_kernel<16, kMaxD>, cudaFuncAttributeNonPortableClusterSizeAllowed,

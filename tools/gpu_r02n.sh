@@ -1,4 +1,3 @@
 #!/bin/bash
-for ab in 0 1 2 3; do PROHD_OPT_K1_ABLATE=$ab ncu --metrics gpu__time_duration.sum,lts__t_sector_hit_rate.pct,dram__bytes_read.sum --clock-control none --csv --log-file gpurun_out/r02n_l$ab.csv python tools/prof_cov.py 5 2 > /dev/null 2>&1; done
-python tools/prof_cov.py 5 4 > gpurun_out/r02n_time.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_moments.py -x -q -s -k "covariance" 2>&1 | tail -4 > gpurun_out/r02n_cov.log
+mkdir -p gpurun_out
+for cl in -1 8 16; do PROHD_OPT_EIG_CL=$cl PROHD_OPT_EIG_STOP=1 timeout 300 python tools/time_eigen.py | sed "s/^/cl=$cl /"; done > gpurun_out/n_cl.txt 2>&1
