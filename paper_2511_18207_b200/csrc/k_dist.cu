@@ -550,14 +550,38 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
             atomicMin(&colbuf[tb][cc * 32 + lane], __float_as_uint(v[0]));
           }
         };
-#pragma unroll 1
-        for (int cc = 0; cc < kBN / 32; cc += 2) {
-          float v0[32], v1[32];
-          tmem_ld32(taddr + cc * 32, v0);
-          tmem_ld32(taddr + (cc + 1) * 32, v1);
+        if constexpr (!kBidir) {
+          // software-pipelined drain: the next 64 columns load from TMEM while this 64 reduce
+          // (two register sets; the accumulators go back to the issuer one load latency sooner)
+          float v0[32], v1[32], w0[32], w1[32];
+          tmem_ld32(taddr, v0);
+          tmem_ld32(taddr + 32, v1);
           tmem_wait_ld();
-          chunk(v0, cc);
-          chunk(v1, cc + 1);
+#pragma unroll
+          for (int cc = 0; cc < kBN / 32; cc += 4) {
+            tmem_ld32(taddr + (cc + 2) * 32, w0);
+            tmem_ld32(taddr + (cc + 3) * 32, w1);
+            chunk(v0, cc);
+            chunk(v1, cc + 1);
+            tmem_wait_ld();
+            if (cc + 4 < kBN / 32) {
+              tmem_ld32(taddr + (cc + 4) * 32, v0);
+              tmem_ld32(taddr + (cc + 5) * 32, v1);
+            }
+            chunk(w0, cc + 2);
+            chunk(w1, cc + 3);
+            if (cc + 4 < kBN / 32) tmem_wait_ld();
+          }
+        } else {
+#pragma unroll 1
+          for (int cc = 0; cc < kBN / 32; cc += 2) {
+            float v0[32], v1[32];
+            tmem_ld32(taddr + cc * 32, v0);
+            tmem_ld32(taddr + (cc + 1) * 32, v1);
+            tmem_wait_ld();
+            chunk(v0, cc);
+            chunk(v1, cc + 1);
+          }
         }
         tc_fence_before();
         __syncwarp();
