@@ -115,9 +115,12 @@ struct DistArgs {
   float* rowmin;            // out: min_j d2(i, j), clamped >= 0
   int num_sms;
   float* colmin = nullptr;  // optional out (fused bidirectional pass): min_i d2(i, j), clamped >= 0
+  const CUtensorMap* maps_bhalf = nullptr;  // [B_H, B_L] with 128-row boxes (CTA-pair kernel), or null
 };
 // K6: fused split-precision tcgen05 distance + row-min kernel.
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st);
+// whether launch_dist_rowmin runs the CTA-pair kernel for this sweep (it then needs maps_bhalf)
+bool k6_uses_pair(int D, bool f16, bool bidir);
 
 // K7a: packed max key over rows: (bits(d2) << 32) | (0xFFFFFFFF - (row + row_offset)).
 cudaError_t launch_rowmax_key(const float* rowmin, int64_t n, int64_t row_offset, unsigned long long* key,

@@ -623,6 +623,230 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
   }
 }
 
+// ============================================================================
+// CTA-pair kernel (directed, fp16 split): a 2-CTA cluster computes a 256-row block of A against
+// 256-column tiles of B with M=256, N=256 `tcgen05.mma.cta_group::2` (three per 16 features).
+// Each CTA stages its own 128 rows of A and its 128-row half of the B tile (32 KB per stage with
+// hi + lo, 6 stages), so per SM the operand bytes per pair equal the two-A kernel's while each
+// CTA's accumulator is only 256 TMEM columns: two of them, double-buffered, and the drain of tile
+// t runs under the MMAs of tile t+1 (the two-A kernel's 512-column pair is drained with the
+// tensor pipe idle). Per SM the tensor core reads 8 KB of shared memory per 128-clock MMA
+// (A 4 KB + B half 4 KB; two-A: 12 KB).
+// Barriers: full[] in the leader counts both CTAs' TMA bytes (2-SM TMA, one plain arrive from the
+// peer); empty[] and tfull[] in both CTAs take the leader's multicast commit; tempty[] in the
+// leader counts the 16 epilogue warps of the pair. Epilogue: 8 warps per CTA, warp w drains TMEM
+// lane quarter w % 4 over column half (w - 2) / 4; the two halves of a row meet in shared memory.
+// ============================================================================
+constexpr int kStagesP = 6;
+constexpr uint32_t kHalfP = 128 * kRowBytes;        // 8 KB: 128 rows x 64 B
+constexpr uint32_t kStagePBytes = 4 * kHalfP;       // A_H, A_L, B_H half, B_L half
+constexpr size_t kSmemP = static_cast<size_t>(kStagesP) * kStagePBytes + 1024 + 256;
+constexpr int kThreadsP = 320;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
+    dist_rowmin_pair_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
+                            const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
+                            const float* __restrict__ na, const float* __restrict__ nb, const float* __restrict__ sa,
+                            const float* __restrict__ sb, const PrepStats* sta, const PrepStats* stb,
+                            float* __restrict__ rowmin) {
+  using namespace sm100;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStagesP * kStagePBytes);
+  uint64_t* empty = full + kStagesP;
+  uint64_t* tfull = empty + kStagesP;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ __align__(16) float nbuf[2][kBN];  // column norms per accumulator buffer
+  __shared__ __align__(16) float ubuf[2][kBN];  // per-row scale mode: 1 / s_j
+  __shared__ float rhalf[128];                  // row minima of column half 1, merged by half 0
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = static_cast<int>(cluster_id_x());
+  const int ncl = static_cast<int>(nclusters_x());
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStagesP; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 16);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tAh);
+    tma_prefetch(&tAl);
+    tma_prefetch(&tBh);
+    tma_prefetch(&tBl);
+  }
+  if (warp == 1) tmem_alloc_2sm<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int units = s.nrb * s.nsplit;  // nrb counts 256-row blocks here
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int pb = u / s.nsplit, sp = u % s.nsplit;
+        const int t0 = sp * s.tps;
+        const int t1 = min(s.nt, t0 + s.tps);
+        const int arow = pb * 256 + static_cast<int>(rank) * 128;
+        for (int t = t0; t < t1; ++t) {
+          const int brow = t * kBN + static_cast<int>(rank) * 128;
+          for (int c = 0; c < s.nk; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            // only the leader arrives (expecting both CTAs' bytes); the peer's TMA completes its
+            // bytes on the leader's barrier without an arrive (the tx-count may go transiently
+            // negative within the phase: the peer loads a slot only after the MMAs consumed the
+            // previous phase of it, so its bytes always land in the phase they belong to)
+            const uint32_t fl = mapa(smem_u32(&full[stage]), 0);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStagePBytes);
+            uint8_t* st = smem + stage * kStagePBytes;
+            tma_load_2d_2sm(st, &tAh, c * 16, arow, fl);
+            tma_load_2d_2sm(st + kHalfP, &tAl, c * 16, arow, fl);
+            tma_load_2d_2sm(st + 2 * kHalfP, &tBh, c * 16, brow, fl);
+            tma_load_2d_2sm(st + 3 * kHalfP, &tBl, c * 16, brow, fl);
+            if (++stage == kStagesP) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader) {
+      // ------------------------------------------------------------ MMA issuer (leader, warp-wide)
+      constexpr uint32_t id = idesc_f16(256, kBN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int sp = u % s.nsplit;
+        const int t0 = sp * s.tps;
+        const int t1 = min(s.nt, t0 + s.tps);
+        for (int t = t0; t < t1; ++t) {
+          mbar_wait(&tempty[acc], aphase ^ 1u);
+          tc_fence_after();
+          const uint32_t d = tmem_base + static_cast<uint32_t>(acc * kBN);
+          for (int c = 0; c < s.nk; ++c) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t ah = smem_u32(smem + stage * kStagePBytes);
+            const uint32_t al = ah + kHalfP, bh = ah + 2 * kHalfP, bl = ah + 3 * kHalfP;
+            const int ks = (c == s.nk - 1) ? s.ks_last : 2;
+            for (int kk = 0; kk < ks; ++kk) {
+              const uint32_t off = static_cast<uint32_t>(kk * 32);
+              const uint64_t dah = smem_desc_k_sw64(ah + off), dbh = smem_desc_k_sw64(bh + off);
+              mma_f16_2sm_w(d, dah, dbh, id, (c | kk) != 0 ? 1u : 0u);
+              mma_f16_2sm_w(d, dah, smem_desc_k_sw64(bl + off), id, 1u);
+              mma_f16_2sm_w(d, smem_desc_k_sw64(al + off), dbh, id, 1u);
+            }
+            mma_commit_2sm_mc_w(&empty[stage], 0x3);
+            if (++stage == kStagesP) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          mma_commit_2sm_mc_w(&tfull[acc], 0x3);
+          acc ^= 1;
+          if (acc == 0) aphase ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------------------------------- epilogue (both CTAs)
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;  // column half
+    const int row_local = q * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+    const int e = (warp - 2) * 32 + lane;  // 0..255: one column norm each
+    const bool perrow = prep_mode_perrow(sta, stb, s.D);
+    const uint32_t te[2] = {mapa(smem_u32(&tempty[0]), 0), mapa(smem_u32(&tempty[1]), 0)};
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int u = cid; u < units; u += ncl) {
+      const int pb = u / s.nsplit, sp = u % s.nsplit;
+      const int t0 = sp * s.tps;
+      const int t1 = min(s.nt, t0 + s.tps);
+      float rm = __int_as_float(0x7f800000);
+      const int64_t myrow = static_cast<int64_t>(pb) * 256 + static_cast<int64_t>(rank) * 128 + row_local;
+      const EpiScale es = epi_scale(true, sta, stb, sa, sb, myrow, s.nA, s.D);
+      for (int t = t0; t < t1; ++t) {
+        {
+          const int64_t col = static_cast<int64_t>(t) * kBN + e;
+          const float n1 = __ldg(nb + col);
+          const float u1 = perrow ? 1.0f / __ldg(sb + col) : 1.0f;
+          mbar_wait(&tfull[acc], aphase);
+          nbuf[acc][e] = n1;
+          ubuf[acc][e] = u1;
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+        }
+        tc_fence_after();
+        const float4* nbp = reinterpret_cast<const float4*>(nbuf[acc]) + h * 32;
+        const float4* ubp = reinterpret_cast<const float4*>(ubuf[acc]) + h * 32;
+        const uint32_t taddr = tmem_base + lane_addr + static_cast<uint32_t>(acc * kBN + h * 128);
+        auto chunk = [&](float (&v)[32], int cc) {
+          const float m = perrow ? epi_chunk<true>(v, es.k, nbp + cc * 8, ubp + cc * 8)
+                                 : epi_chunk<false>(v, es.k, nbp + cc * 8, ubp + cc * 8);
+          rm = fminf(rm, m);
+        };
+        {
+          float v0[32], v1[32], w0[32], w1[32];
+          tmem_ld32(taddr, v0);
+          tmem_ld32(taddr + 32, v1);
+          tmem_wait_ld();
+          tmem_ld32(taddr + 64, w0);
+          tmem_ld32(taddr + 96, w1);
+          chunk(v0, 0);
+          chunk(v1, 1);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0)  // accumulator free: the rest is in registers (release.cta arrive on the leader's barrier)
+            asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(te[acc]) : "memory");
+          chunk(w0, 2);
+          chunk(w1, 3);
+        }
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1u;
+      }
+      // the two column halves of each row meet in shared memory (the per-tile bar.sync above
+      // orders this unit's rhalf writes after the previous unit's reads)
+      if (h == 1) rhalf[row_local] = rm;
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      if (h == 0 && myrow < s.nA) {
+        const float d2 = fmaxf(fminf(rm, rhalf[row_local]) + __ldg(na + myrow), 0.0f);
+        if (s.atomic_out)
+          atomicMin(reinterpret_cast<int*>(rowmin + myrow), __float_as_int(d2));
+        else
+          rowmin[myrow] = d2;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm<kTmemCols>(tmem_base);
+  }
+}
+
 template <typename K>
 cudaError_t launch_k(K kern, int grid, int threads, size_t smem, cudaStream_t st, const DistArgs& a, const Sched& s) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -642,15 +866,18 @@ cudaError_t launch_k(K kern, int grid, int threads, size_t smem, cudaStream_t st
 // forces the single-block / two-A kernel; k6_bidir_2a = 1 runs the bidirectional sweep two-A.
 static int dist_variant(int D) {
   const long long v = opt(OPT_K6_VARIANT);
-  if (v == 1 || v == 3) return static_cast<int>(v);
-  return D >= 128 ? 3 : 1;
+  if (v == 1 || v == 2 || v == 3) return static_cast<int>(v);
+  return D >= 128 ? 2 : 1;  // 2: the CTA pair where it applies (fp16 directed), else the two-A kernel
 }
+
+bool k6_uses_pair(int D, bool f16, bool bidir) { return f16 && !bidir && dist_variant(D) == 2; }
 
 bool k6_split3() { return opt(OPT_K6_SPLIT3) == 1; }
 
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
-  const bool twoa = dist_variant(a.D) == 3 && (a.colmin == nullptr || opt(OPT_K6_BIDIR_2A) == 1);
-  const int rows_per_unit = twoa ? 256 : kBM;
+  const bool pair = k6_uses_pair(a.D, a.f16, a.colmin != nullptr) && a.maps_bhalf != nullptr && a.num_sms >= 2;
+  const bool twoa = !pair && dist_variant(a.D) >= 2 && (a.colmin == nullptr || opt(OPT_K6_BIDIR_2A) == 1);
+  const int rows_per_unit = (twoa || pair) ? 256 : kBM;
   Sched s{};
   s.nA = a.nA;
   s.nB = a.nB;
@@ -661,7 +888,7 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   const int fpk = fps / 2;          // features per 32-byte K-step
   s.nk = (a.D + fps - 1) / fps;
   s.ks_last = (a.D - (s.nk - 1) * fps + fpk - 1) / fpk;
-  const int slots = a.num_sms;  // concurrent units
+  const int slots = pair ? a.num_sms / 2 : a.num_sms;  // concurrent units
   // Column splits: units (row block, column range) are dealt round-robin to the persistent
   // CTAs, so the sweep takes ceil(units / slots) rounds of (tps + ~0.5) tile times (the half
   // tile: a unit's pipeline fill / drain and row-minimum merge). Small A (subset HD: 100-250
@@ -699,6 +926,16 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   const int units = s.nrb * s.nsplit;
   const int grid = units < slots ? units : slots;
   const bool bidir = a.colmin != nullptr;
+  if (pair) {
+    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemP));
+    if (e != cudaSuccess) return e;
+    count_launch();
+    dist_rowmin_pair_kernel<<<2 * grid, kThreadsP, kSmemP, st>>>(a.maps[0], a.maps[1], a.maps_bhalf[0],
+                                                                 a.maps_bhalf[1], s, a.na, a.nb, a.sa, a.sb, a.sta,
+                                                                 a.stb, a.rowmin);
+    return cudaGetLastError();
+  }
   if (twoa) {
     if (bidir)
       return a.f16 ? launch_k(dist_rowmin_2a_kernel<true, true>, grid, kThreadsA2, kSmemA2, st, a, s)

@@ -335,3 +335,42 @@ def test_graph_replay_exact(ctx):
         for _ in range(3):
             assert ctx.directed_hd(At, Bt) == d0
             assert ctx.hausdorff(At, Bt) == h0
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 128), (5, 300, 130), (257, 513, 256), (700, 2000, 128),
+                                   (513, 1100, 256), (129, 40000, 256), (20000, 3001, 200)])
+def test_rowmin_cta_pair(ctx, shape):
+    """The CTA-pair K6 (option k6_variant = 2: M=256 cta_group::2 MMAs, double-buffered 256-column
+    accumulators, B split across the pair): per-row Q17 against the oracle on ragged shapes (partial
+    256-row blocks, a single row, column-split units merged by atomicMin, feature counts off the
+    32-feature stage), the HD witness, and the per-row scale mode."""
+    from paper_2511_18207_b200 import option
+    nA, nB, D = shape
+    rng = np.random.default_rng(nA * 3 + nB + D)
+    A = rng.standard_normal((nA, D)).astype(np.float32)
+    B = (rng.standard_normal((nB, D)) * 1.5 + 0.25).astype(np.float32)
+    rows = None if nA * nB <= 4_000_000 else np.unique(rng.integers(0, nA, 400))
+    with option("k6_variant", 2):
+        At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        rm = ctx.directed_hd_rowmin(At, Bt).cpu().numpy()
+        got = ctx.directed_hd(At, Bt)
+    _check_rowmins(A, B, rm, rows=rows)
+    if rows is None:
+        ref = oracle.hausdorff(A, B)["ab"]
+        _check_directed(A, B, got, ref)
+    with option("k6_variant", 3):
+        rm3 = ctx.directed_hd_rowmin(At, Bt).cpu().numpy()
+    # same arithmetic per pair (three fp16 MMAs, fp32 accumulation in the same K order)
+    assert np.array_equal(rm, rm3)
+
+
+def test_rowmin_cta_pair_per_row_scales(ctx):
+    from paper_2511_18207_b200 import option
+    rng = np.random.default_rng(77)
+    A = (rng.standard_normal((700, 256)) * 1e-6).astype(np.float32)
+    B = (rng.standard_normal((900, 256)) * 1e-6 + 2e-7).astype(np.float32)
+    A[3], A[4] = 1e4, -1e4
+    B[5], B[600] = -1e4 - 0.5, 1e4 + 0.5
+    with option("k6_variant", 2):
+        rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    _check_rowmins(A, B, rm)

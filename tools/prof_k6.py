@@ -1,6 +1,9 @@
 """ncu target: one full-machine K6 launch (37888 x 262144, D=256) via directed_hd."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _opts  # noqa: E402
+_opts.apply_env()
 import torch
 from paper_2511_18207_b200 import Context
 ctx = Context(0)

@@ -1,4 +1,4 @@
-"""Dev timing: K6 (directed, D = 256, the two-A kernel) throughput per SM clock.
+"""Dev timing: K6 (directed sweeps, default variant unless PROHD_OPT_K6_VARIANT) throughput per SM clock.
 
 Runs directed_hd back to back for ~4 s while a thread samples the SM clock with NVML, and prints
 Gpair/s, the median SM clock under load and pairs per SM per clock (148 SMs) — the clock-invariant
@@ -14,6 +14,11 @@ import pynvml  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2511_18207_b200 import Context  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _opts  # noqa: E402
+
+_opts.apply_env()
 
 pynvml.nvmlInit()
 h = pynvml.nvmlDeviceGetHandleByIndex(int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or 0))
