@@ -34,11 +34,14 @@
 //   warps 2-9   epilogue (8 warps): tcgen05.ld 32x32b.x32 (one TMEM lane = one row per thread),
 //               v = fma(k_i, acc, ||b||^2), running min in a register across all B tiles of the
 //               unit.
-// Two kernels: the single-block kernel (one 128-row block of A per CTA, M=128 N=256, the
+// Three kernels: the single-block kernel (one 128-row block of A per CTA, M=128 N=256, the
 // accumulator double-buffered so the epilogue of tile t overlaps the MMAs of t+1; 4 stages of
-// 48 KB) and the two-A kernel (two 128-row blocks against each B tile, both accumulators = all
-// 512 TMEM columns, 3 stages of 64 KB: 2/3 of the operand bytes per pair), used for directed
-// sweeps at D >= 128.
+// 48 KB; directed sweeps at D < 128 and the fused bidirectional sweep), the two-A kernel (two
+// 128-row blocks against each B tile, both accumulators = all 512 TMEM columns, 3 stages of
+// 64 KB: 2/3 of the operand bytes per pair; literal 3xTF32 and option k6_variant 3), and the
+// CTA-pair kernel (2-CTA cluster, M=256 N=256 cta_group::2, B split across the pair, 256-column
+// accumulators double-buffered; see its header below) — the default for fp16 directed sweeps
+// at D >= 128 and the bench's dominant kernel.
 // Work unit = (row block, contiguous range of B tiles). With one range the row minimum is
 // stored; with several (small n_A) it is combined with an integer atomicMin on the float bits
 // (valid since d2 >= 0).
@@ -643,12 +646,13 @@ constexpr uint32_t kStagePBytes = 4 * kHalfP;       // A_H, A_L, B_H half, B_L h
 constexpr size_t kSmemP = static_cast<size_t>(kStagesP) * kStagePBytes + 1024 + 256;
 constexpr int kThreadsP = 320;
 
+template <bool kBidir>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
     dist_rowmin_pair_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                             const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, Sched s,
                             const float* __restrict__ na, const float* __restrict__ nb, const float* __restrict__ sa,
                             const float* __restrict__ sb, const PrepStats* sta, const PrepStats* stb,
-                            float* __restrict__ rowmin) {
+                            float* __restrict__ rowmin, float* __restrict__ colmin) {
   using namespace sm100;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -660,6 +664,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
   __shared__ __align__(16) float nbuf[2][kBN];  // column norms per accumulator buffer
   __shared__ __align__(16) float ubuf[2][kBN];  // per-row scale mode: 1 / s_j
   __shared__ float rhalf[128];                  // row minima of column half 1, merged by half 0
+  __shared__ unsigned colbuf[2][kBN];           // kBidir: this CTA's column minima per accumulator (float bits)
+  __shared__ unsigned tilecnt[2];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -667,6 +673,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
   const bool leader = rank == 0;
   const int cid = static_cast<int>(cluster_id_x());
   const int ncl = static_cast<int>(nclusters_x());
+  if (kBidir) {
+    for (int i = threadIdx.x; i < 2 * kBN; i += blockDim.x) (&colbuf[0][0])[i] = 0x7F800000u;
+    if (threadIdx.x < 2) tilecnt[threadIdx.x] = 0u;
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStagesP; ++i) {
       mbar_init(&full[i], 1);
@@ -786,6 +796,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
       float rm = __int_as_float(0x7f800000);
       const int64_t myrow = static_cast<int64_t>(pb) * 256 + static_cast<int64_t>(rank) * 128 + row_local;
       const EpiScale es = epi_scale(true, sta, stb, sa, sb, myrow, s.nA, s.D);
+      // kBidir: this row's ||a||^2, or +inf for rows past nA (excluded from column minima)
+      const float narow = kBidir ? (myrow < s.nA ? __ldg(na + myrow) : __int_as_float(0x7f800000)) : 0.0f;
       for (int t = t0; t < t1; ++t) {
         {
           const int64_t col = static_cast<int64_t>(t) * kBN + e;
@@ -804,6 +816,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
           const float m = perrow ? epi_chunk<true>(v, es.k, nbp + cc * 8, ubp + cc * 8)
                                  : epi_chunk<false>(v, es.k, nbp + cc * 8, ubp + cc * 8);
           rm = fminf(rm, m);
+          if (kBidir) {  // column minima over this warp's 32 rows, merged across the CTA's warps in shared memory
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + narow, 0.0f);
+            warp_colmin32(v, lane);
+            atomicMin(&colbuf[acc][h * 128 + cc * 32 + lane], __float_as_uint(v[0]));
+          }
         };
         {
           float v0[32], v1[32], w0[32], w1[32];
@@ -821,6 +839,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
             asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(te[acc]) : "memory");
           chunk(w0, 2);
           chunk(w1, 3);
+        }
+        if (kBidir) {
+          // the last of this CTA's 8 epilogue warps flushes the tile's 256 column minima (the next
+          // use of colbuf[acc] is two tiles on, behind two bar.sync of all 8 warps)
+          __syncwarp();
+          __threadfence_block();
+          unsigned old = 0;
+          if (lane == 0) old = atomicAdd(&tilecnt[acc], 1u);
+          old = __shfl_sync(0xffffffffu, old, 0);
+          if (old == 7u) {
+            __threadfence_block();
+            for (int j = lane; j < kBN; j += 32) {
+              const unsigned val = atomicExch(&colbuf[acc][j], 0x7F800000u);
+              const int64_t col = static_cast<int64_t>(t) * kBN + j;
+              if (col < s.nB) atomicMin(reinterpret_cast<unsigned*>(colmin) + col, val);
+            }
+            if (lane == 0) tilecnt[acc] = 0u;
+            __threadfence_block();
+          }
+          __syncwarp();
         }
         acc ^= 1;
         if (acc == 0) aphase ^= 1u;
@@ -859,18 +897,21 @@ cudaError_t launch_k(K kern, int grid, int threads, size_t smem, cudaStream_t st
 
 }  // namespace
 
-// Variants (one B200). Directed sweeps use the two-A-block kernel for D >= 128 and the
-// single-block kernel below (faster at small D, where the epilogue is not hidden behind fewer
-// MMAs). The fused bidirectional sweep keeps the single-block kernel (its column-minimum
-// epilogue is heavier and is not overlapped in the two-A kernel). option k6_variant = 1 | 3
-// forces the single-block / two-A kernel; k6_bidir_2a = 1 runs the bidirectional sweep two-A.
+// Variants (one B200). Directed fp16 sweeps at D >= 128 use the CTA-pair kernel (the literal
+// 3xTF32 split at D >= 128: the two-A kernel) and the single-block kernel below (faster at
+// small D, where the epilogue is not hidden behind fewer MMAs). The fused bidirectional sweep
+// keeps the single-block kernel (its column-minimum epilogue is heavier and is not overlapped
+// in the two-A kernel). option k6_variant = 1 | 2 | 3 forces the single-block / pair / two-A
+// kernel; k6_bidir_2a = 1 runs the bidirectional sweep two-A.
 static int dist_variant(int D) {
   const long long v = opt(OPT_K6_VARIANT);
   if (v == 1 || v == 2 || v == 3) return static_cast<int>(v);
   return D >= 128 ? 2 : 1;  // 2: the CTA pair where it applies (fp16 directed), else the two-A kernel
 }
 
-bool k6_uses_pair(int D, bool f16, bool bidir) { return f16 && !bidir && dist_variant(D) == 2; }
+bool k6_uses_pair(int D, bool f16, bool bidir) {
+  return f16 && dist_variant(D) == 2 && (!bidir || opt(OPT_K6_BIDIR_2A) == 2);
+}
 
 bool k6_split3() { return opt(OPT_K6_SPLIT3) == 1; }
 
@@ -927,13 +968,12 @@ cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
   const int grid = units < slots ? units : slots;
   const bool bidir = a.colmin != nullptr;
   if (pair) {
-    cudaError_t e = cudaFuncSetAttribute(dist_rowmin_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemP));
+    auto kern = bidir ? dist_rowmin_pair_kernel<true> : dist_rowmin_pair_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemP));
     if (e != cudaSuccess) return e;
     count_launch();
-    dist_rowmin_pair_kernel<<<2 * grid, kThreadsP, kSmemP, st>>>(a.maps[0], a.maps[1], a.maps_bhalf[0],
-                                                                 a.maps_bhalf[1], s, a.na, a.nb, a.sa, a.sb, a.sta,
-                                                                 a.stb, a.rowmin);
+    kern<<<2 * grid, kThreadsP, kSmemP, st>>>(a.maps[0], a.maps[1], a.maps_bhalf[0], a.maps_bhalf[1], s, a.na, a.nb,
+                                              a.sa, a.sb, a.sta, a.stb, a.rowmin, a.colmin);
     return cudaGetLastError();
   }
   if (twoa) {

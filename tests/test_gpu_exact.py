@@ -374,3 +374,31 @@ def test_rowmin_cta_pair_per_row_scales(ctx):
     with option("k6_variant", 2):
         rm = ctx.directed_hd_rowmin(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
     _check_rowmins(A, B, rm)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 128), (5, 300, 130), (257, 513, 256), (777, 513, 256),
+                                   (2048, 4099, 128), (129, 40000, 256), (20000, 3001, 200)])
+def test_bidirectional_cta_pair(ctx, shape):
+    """The fused bidirectional sweep on the CTA-pair K6 (option k6_bidir_2a = 2): hausdorff() against
+    the oracle in both directions on ragged shapes (partial 256-row blocks, rows past nA excluded from
+    the column minima, column-split units), and row / column minima bit-identical to the single-block
+    sweep (same three fp16 MMAs per accumulator element in the same K order; min is order-free)."""
+    from paper_2511_18207_b200 import option
+    nA, nB, D = shape
+    rng = np.random.default_rng(nA + 5 * nB + 11 * D)
+    A = rng.standard_normal((nA, D)).astype(np.float32)
+    B = (rng.standard_normal((nB, D)) * 1.3 + 0.2).astype(np.float32)
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    with option("k6_bidir_2a", 2):
+        h, rm, cm = ctx.hausdorff_minima(At, Bt)
+    with option("k6_bidir_2a", 0):
+        h1, rm1, cm1 = ctx.hausdorff_minima(At, Bt)
+    assert torch.equal(rm, rm1) and torch.equal(cm, cm1)
+    assert h == h1
+    if nA * nB <= 4_000_000:
+        ref = oracle.hausdorff(A, B)
+        _check_directed(A, B, h["ab"], ref["ab"])
+        _check_directed(B, A, h["ba"], ref["ba"])
+    else:
+        _check_rowmins(A, B, rm.cpu().numpy(), rows=np.unique(rng.integers(0, nA, 300)))
+        _check_rowmins(B, A, cm.cpu().numpy(), rows=np.unique(rng.integers(0, nB, 300)))
