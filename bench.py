@@ -512,7 +512,11 @@ def run_ours(args, rank: int, world: int):
                               "launch / mean launch time from CUDA events on the launch stream; peak = "
                               f"{pk['source']} bf16 (= fp16 dense rate) SUSTAINED {pk['bf16_tflops_sustained']} (K6 is "
                               f"one multi-second launch inside the step); against the burst figure "
-                              f"{pk['bf16_tflops']}: peak_burst / frac_burst"),
+                              f"{pk['bf16_tflops']}: peak_burst / frac_burst. Both this kernel and the sustained "
+                              "peak's cuBLAS GEMM run under the board power cap (clocks: sw_power_cap), so frac "
+                              "compares flops per joule as much as pipe utilisation and can pass 1: the CTA-pair "
+                              "kernel keeps the tensor pipe ~98 % busy (profiles/r02zh_k6_pair.md) at half the "
+                              "shared-memory operand traffic of a single-CTA tile"),
                      "launch_ms": k6_ms},
         "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }
