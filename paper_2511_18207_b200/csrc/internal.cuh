@@ -20,7 +20,7 @@ inline void count_launch(int n = 1) { launch_counter().fetch_add(n, std::memory_
 enum OptId {
   OPT_K6_VARIANT,    // 1 single A block, 2 two-SM pair (directed), 3 two A blocks per CTA
   OPT_K6_SPLIT3,     // 1: literal 3xTF32 (three TF32 MMAs on fp32 hi/lo)
-  OPT_K6_BIDIR_2A,   // 1: fused bidirectional sweep on the two-A kernel, 2: on the CTA-pair kernel
+  OPT_K6_BIDIR_2A,   // fused bidirectional sweep on 0 the single-block, 1 the two-A, 2 the CTA-pair kernel (default)
   OPT_K6_SPLITS_2X,  // 1: the old fill-twice column-split rule
   OPT_K1_PATH,       // 0 fp64 DMMA Gram, 1 int8 tcgen05 Gram, 2 legacy 64x64-tile moments kernel
   OPT_K1_CTAS,       // legacy moments kernel: resident CTAs per SM (3 or 4)

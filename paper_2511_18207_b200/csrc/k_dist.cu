@@ -40,8 +40,8 @@
 // 128-row blocks against each B tile, both accumulators = all 512 TMEM columns, 3 stages of
 // 64 KB: 2/3 of the operand bytes per pair; literal 3xTF32 and option k6_variant 3), and the
 // CTA-pair kernel (2-CTA cluster, M=256 N=256 cta_group::2, B split across the pair, 256-column
-// accumulators double-buffered; see its header below) — the default for fp16 directed sweeps
-// at D >= 128 and the bench's dominant kernel.
+// accumulators double-buffered; see its header below) — the default for fp16 sweeps at
+// D >= 128 (directed: the bench's dominant kernel; fused bidirectional: kBidir).
 // Work unit = (row block, contiguous range of B tiles). With one range the row minimum is
 // stored; with several (small n_A) it is combined with an integer atomicMin on the float bits
 // (valid since d2 >= 0).
@@ -627,7 +627,8 @@ __global__ void __launch_bounds__(kThreadsA2, 1)
 }
 
 // ============================================================================
-// CTA-pair kernel (directed, fp16 split): a 2-CTA cluster computes a 256-row block of A against
+// CTA-pair kernel (fp16 split; directed, or with kBidir the fused bidirectional sweep whose
+// epilogue also reduces this CTA's 128 rows to column minima): a 2-CTA cluster computes a 256-row block of A against
 // 256-column tiles of B with M=256, N=256 `tcgen05.mma.cta_group::2` (three per 16 features).
 // Each CTA stages its own 128 rows of A and its 128-row half of the B tile (32 KB per stage with
 // hi + lo, 6 stages), so per SM the operand bytes per pair equal the two-A kernel's while each
@@ -897,12 +898,12 @@ cudaError_t launch_k(K kern, int grid, int threads, size_t smem, cudaStream_t st
 
 }  // namespace
 
-// Variants (one B200). Directed fp16 sweeps at D >= 128 use the CTA-pair kernel (the literal
-// 3xTF32 split at D >= 128: the two-A kernel) and the single-block kernel below (faster at
-// small D, where the epilogue is not hidden behind fewer MMAs). The fused bidirectional sweep
-// keeps the single-block kernel (its column-minimum epilogue is heavier and is not overlapped
-// in the two-A kernel). option k6_variant = 1 | 2 | 3 forces the single-block / pair / two-A
-// kernel; k6_bidir_2a = 1 runs the bidirectional sweep two-A.
+// Variants (one B200). fp16 sweeps at D >= 128, directed and fused bidirectional, use the
+// CTA-pair kernel (the literal 3xTF32 split at D >= 128: the two-A kernel directed, the
+// single-block kernel bidirectional) and the single-block kernel below (faster at small D,
+// where the epilogue is not hidden behind fewer MMAs). option k6_variant = 1 | 2 | 3 forces the
+// single-block / pair / two-A kernel; k6_bidir_2a = 0 | 1 | 2 runs the bidirectional sweep on
+// the single-block / two-A / pair kernel.
 static int dist_variant(int D) {
   const long long v = opt(OPT_K6_VARIANT);
   if (v == 1 || v == 2 || v == 3) return static_cast<int>(v);
@@ -910,7 +911,8 @@ static int dist_variant(int D) {
 }
 
 bool k6_uses_pair(int D, bool f16, bool bidir) {
-  return f16 && dist_variant(D) == 2 && (!bidir || opt(OPT_K6_BIDIR_2A) == 2);
+  const long long b = opt(OPT_K6_BIDIR_2A);  // bidirectional: unset or 2 -> pair, 0 single-block, 1 two-A
+  return f16 && dist_variant(D) == 2 && (!bidir || b == 2 || b < 0);
 }
 
 bool k6_split3() { return opt(OPT_K6_SPLIT3) == 1; }

@@ -11,5 +11,6 @@ g = torch.Generator(device="cuda").manual_seed(0)
 nA, nB, D = 37888, 262144, int(sys.argv[1]) if len(sys.argv) > 1 else 256
 A = torch.randn(nA, D, device="cuda", generator=g)
 B = torch.randn(nB, D, device="cuda", generator=g)
-r = ctx.directed_hd(A, B)
-print(nA, nB, D, r["dist"])
+bidir = len(sys.argv) > 2 and sys.argv[2] == "bidir"  # the fused bidirectional sweep (hausdorff)
+r = ctx.hausdorff(A, B) if bidir else ctx.directed_hd(A, B)
+print(nA, nB, D, r["value"] if bidir else r["dist"])
