@@ -334,7 +334,7 @@ inline int run_dist(prohd_ctx* ctx, const SetOps& R, const SetOps& C, int D, flo
       !make_tmap_2d(&maps[3], reinterpret_cast<const float*>(C.L), C.n, cols, kBN, err, sizeof err, 16))
     return fail(ctx, PROHD_E_CUDA, "%s", err);
   CUtensorMap bhalf[2];
-  const bool pair = k6_uses_pair(D, R.f16, colmin != nullptr);
+  const bool pair = k6_uses_pair(D, R.f16, colmin != nullptr, R.n, C.n);
   if (pair && (!make_tmap_2d(&bhalf[0], reinterpret_cast<const float*>(C.H), C.n, cols, kBM, err, sizeof err, 16) ||
                !make_tmap_2d(&bhalf[1], reinterpret_cast<const float*>(C.L), C.n, cols, kBM, err, sizeof err, 16)))
     return fail(ctx, PROHD_E_CUDA, "%s", err);

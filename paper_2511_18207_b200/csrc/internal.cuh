@@ -120,7 +120,7 @@ struct DistArgs {
 // K6: fused split-precision tcgen05 distance + row-min kernel.
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st);
 // whether launch_dist_rowmin runs the CTA-pair kernel for this sweep (it then needs maps_bhalf)
-bool k6_uses_pair(int D, bool f16, bool bidir);
+bool k6_uses_pair(int D, bool f16, bool bidir, int64_t nA, int64_t nB);
 
 // K7a: packed max key over rows: (bits(d2) << 32) | (0xFFFFFFFF - (row + row_offset)).
 cudaError_t launch_rowmax_key(const float* rowmin, int64_t n, int64_t row_offset, unsigned long long* key,

@@ -910,15 +910,25 @@ static int dist_variant(int D) {
   return D >= 128 ? 2 : 1;  // 2: the CTA pair where it applies (fp16 directed), else the two-A kernel
 }
 
-bool k6_uses_pair(int D, bool f16, bool bidir) {
-  const long long b = opt(OPT_K6_BIDIR_2A);  // bidirectional: unset or 2 -> pair, 0 single-block, 1 two-A
-  return f16 && dist_variant(D) == 2 && (!bidir || b == 2 || b < 0);
+// Fused bidirectional sweeps (option k6_bidir_2a unset): the pair kernel up to kBidirPairMaxWork
+// = nA nB D, the single-block kernel above. Measured on a B200: short sweeps
+// (subset HD, cfg3) run 4-17 % faster on the pair; a multi-second D = 256 sweep is power-capped
+// and the pair kernel, tensor pipe and butterfly epilogue both busy, settles at a lower clock
+// (cfg5 undirected 5.03 s single-block, 5.71 s pair).
+constexpr double kBidirPairMaxWork = 1.0e14;
+bool k6_uses_pair(int D, bool f16, bool bidir, int64_t nA, int64_t nB) {
+  if (!f16 || dist_variant(D) != 2) return false;
+  if (!bidir) return true;
+  const long long b = opt(OPT_K6_BIDIR_2A);  // 0 single-block, 1 two-A, 2 pair
+  if (b >= 0) return b == 2;
+  return static_cast<double>(nA) * static_cast<double>(nB) * D <= kBidirPairMaxWork;
 }
 
 bool k6_split3() { return opt(OPT_K6_SPLIT3) == 1; }
 
 cudaError_t launch_dist_rowmin(const DistArgs& a, cudaStream_t st) {
-  const bool pair = k6_uses_pair(a.D, a.f16, a.colmin != nullptr) && a.maps_bhalf != nullptr && a.num_sms >= 2;
+  const bool pair =
+      k6_uses_pair(a.D, a.f16, a.colmin != nullptr, a.nA, a.nB) && a.maps_bhalf != nullptr && a.num_sms >= 2;
   const bool twoa = !pair && dist_variant(a.D) >= 2 && (a.colmin == nullptr || opt(OPT_K6_BIDIR_2A) == 1);
   const int rows_per_unit = (twoa || pair) ? 256 : kBM;
   Sched s{};

@@ -24,11 +24,13 @@ pynvml.nvmlInit()
 h = pynvml.nvmlDeviceGetHandleByIndex(int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or 0))
 ctx = Context(0)
 nA, nB = 65536, 262144
+BIDIR = os.environ.get("K6_CLOCK_BIDIR") == "1"  # time hausdorff() (the fused bidirectional sweep) instead
+call = ctx.hausdorff if BIDIR else ctx.directed_hd
 for D in [int(x) for x in (sys.argv[1:] or ["256"])]:
     g = torch.Generator(device="cuda").manual_seed(0)
     A = torch.randn(nA, D, device="cuda", generator=g)
     B = torch.randn(nB, D, device="cuda", generator=g)
-    ctx.directed_hd(A, B)
+    call(A, B)
     torch.cuda.synchronize()
     clocks, stop = [], threading.Event()
 
@@ -44,7 +46,7 @@ for D in [int(x) for x in (sys.argv[1:] or ["256"])]:
     ev0.record()
     while time.time() - t0 < 4.0:
         for _ in range(4):
-            ctx.directed_hd(A, B)
+            call(A, B)
         reps += 4
         torch.cuda.synchronize()
     ev1.record()
@@ -54,5 +56,5 @@ for D in [int(x) for x in (sys.argv[1:] or ["256"])]:
     ms = ev0.elapsed_time(ev1) / reps
     gp = nA * nB / ms / 1e6
     mhz = statistics.median(clocks[len(clocks) // 4:])
-    print(f"D={D}: {ms:.3f} ms/call  {gp:.1f} Gpair/s  SM median {mhz} MHz  "
+    print(f"{'bidir ' if BIDIR else ''}D={D}: {ms:.3f} ms/call  {gp:.1f} Gpair/s  SM median {mhz} MHz  "
           f"{gp * 1e9 / (148 * mhz * 1e6):.3f} pairs/SM/clk", flush=True)
