@@ -87,7 +87,7 @@ int prohd_launch_count(int64_t* out);
  *   "k6_variant"    1 single 128-row A block per CTA, 2 two-SM pair (directed), 3 two A blocks
  *   "k6_split3"     1: literal 3xTF32 distance products (three TF32 MMAs on fp32 hi/lo)
  *   "k6_bidir_2a"   fused bidirectional sweep on: 0 the single-block kernel, 1 the two-A kernel,
- *                   2 the CTA-pair kernel (the default for D >= 128)
+ *                   2 the CTA-pair kernel (default for D >= 128: 2 up to nA nB D = 1e14, 0 above)
  *   "k6_splits_2x"  1: the earlier fill-twice column-split rule
  *   "k1_path"       0 fp64 DMMA Gram, 1 int8 tcgen05 Gram (the default for D <= 256, D % 4 == 0),
  *                   2 legacy tile moments kernel
