@@ -898,9 +898,9 @@ cudaError_t launch_k(K kern, int grid, int threads, size_t smem, cudaStream_t st
 
 }  // namespace
 
-// Variants (one B200). fp16 sweeps at D >= 128, directed and fused bidirectional, use the
-// CTA-pair kernel (the literal 3xTF32 split at D >= 128: the two-A kernel directed, the
-// single-block kernel bidirectional) and the single-block kernel below (faster at small D,
+// Variants (one B200). fp16 sweeps at D >= 128, directed and fused bidirectional (the latter up
+// to kBidirPairMaxWork, below), use the CTA-pair kernel (the literal 3xTF32 split at D >= 128:
+// the two-A kernel directed, the single-block kernel bidirectional) and the single-block kernel below (faster at small D,
 // where the epilogue is not hidden behind fewer MMAs). option k6_variant = 1 | 2 | 3 forces the
 // single-block / pair / two-A kernel; k6_bidir_2a = 0 | 1 | 2 runs the bidirectional sweep on
 // the single-block / two-A / pair kernel.
